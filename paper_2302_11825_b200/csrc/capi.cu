@@ -1,0 +1,1528 @@
+// capi.cu — the C ABI (include/bvc_b200.h) over the sm_100a BVC kernels.
+//
+// Orchestrates the reference's operator API on the device:
+//   generateBoundaryCache (cache.cpp:301-390), generateSourceCache (392-406),
+//   markEvaluationPoints (263-276), splatSolution / splatGradient (426-497),
+//   updateSolution (622-684) and the pointwise estimators (pointwise.cpp:225-288).
+// Host preprocessing (scene build, solve region, BVH) is host_scene.cpp.
+// There is no CPU fallback: every compute entry point fails with
+// BVC_ERR_NO_DEVICE when no CUDA device is present.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <cub/device/device_radix_sort.cuh>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/bvc_b200.h"
+#include "gather.h"
+#include "host_scene.h"
+#include "internal.h"
+
+using bvc_host::Error;
+using namespace bvc_impl;
+using bvc_dev::Node2;
+using bvc_dev::Prim2;
+
+namespace {
+
+thread_local std::string g_error;
+cudaStream_t g_stream = nullptr;
+std::atomic<long long> g_launches{0};
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Error(bvc_host::kCuda, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+void require_device() {
+    static int state = -1;  // -1 unknown, 0 none, 1 ok
+    if (state < 0) {
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        state = (e == cudaSuccess && n > 0) ? 1 : 0;
+        if (e != cudaSuccess) cudaGetLastError();
+    }
+    if (!state) throw Error(bvc_host::kNoDevice, "no CUDA device: the BVC path has no CPU fallback");
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0, cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { if (p) cudaFree(p); }
+    void resize(size_t count) {
+        if (count > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+            cap = count;
+        }
+        n = count;
+    }
+    void upload(const T* h, size_t count) {
+        resize(count);
+        if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, g_stream));
+    }
+    void download(T* h, size_t count) const {
+        if (count) CK(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, g_stream));
+    }
+    void zero() { if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), g_stream)); }
+};
+
+// grow-only scratch buffers keyed by slot
+struct Workspace {
+    std::vector<std::unique_ptr<DevBuf<char>>> slots;
+    template <class T>
+    T* get(int slot, size_t count) {
+        if (static_cast<int>(slots.size()) <= slot) slots.resize(slot + 1);
+        if (!slots[slot]) slots[slot] = std::make_unique<DevBuf<char>>();
+        slots[slot]->resize(count * sizeof(T));
+        return reinterpret_cast<T*>(slots[slot]->p);
+    }
+};
+Workspace& ws() {
+    static Workspace w;
+    return w;
+}
+enum Slot {
+    kWsSamplesTmp, kWsStartU, kWsIsD, kWsGradR, kWsOutside, kWsDIdx, kWsCount, kWsXD, kWsND, kWsRD, kWsGidD, kWsOutU,
+    kWsOutD, kWsCounter, kWsSteps, kWsTrunc, kWsFailed, kWsPack, kWsPart, kWsSkipB, kWsSkipS, kWsPts, kWsCtr,
+    kWsSortKeysIn, kWsSortKeysOut, kWsSortValsIn, kWsSortTemp, kWsMean, kWsSe, kWsTruncPt, kWsHost1, kWsRegion,
+    kWsMean2, kWsSe2, kWsGidU, kWsSrcTmp, kWsSrcFlag, kWsEvalIn, kWsEvalOut
+};
+
+int fail(const std::exception& e) {
+    g_error = e.what();
+    if (auto* be = dynamic_cast<const Error*>(&e)) return be->code;
+    if (dynamic_cast<const std::bad_alloc*>(&e)) return BVC_ERR_CUDA;
+    return BVC_ERR_SOLVER;
+}
+
+#define API(...)                          \
+    try {                                 \
+        __VA_ARGS__;                      \
+        return BVC_OK;                    \
+    } catch (const std::exception& e) {   \
+        return fail(e);                   \
+    }
+
+void need(bool ok, const char* msg, int code = BVC_ERR_INVALID_ARGUMENT) {
+    if (!ok) throw Error(code, msg);
+}
+
+bvc_dev::DevField to_dev(const bvc_field& f) {
+    bvc_dev::DevField d{};
+    d.kind = f.kind;
+    d.n = f.n;
+    for (int i = 0; i < bvc_dev::kFieldMaxParams; ++i) d.p[i] = static_cast<float>(f.p[i]);
+    return d;
+}
+
+void validate_kernel(const bvc_kernel_spec& k) {  // KernelSpec::validate (kernels.h:32-37)
+    if ((k.sigma == 0.0) != (k.kind == BVC_KERNEL_POISSON))
+        throw Error(BVC_ERR_INVALID_ARGUMENT, "kernel: sigma = 0 iff kind = Poisson");
+    if (k.sigma < 0.0) throw Error(BVC_ERR_INVALID_ARGUMENT, "kernel: sigma must be >= 0");
+    if (k.dim != 2 && k.dim != 3) throw Error(BVC_ERR_INVALID_ARGUMENT, "kernel: dimension must be 2 or 3");
+}
+
+inline void key_of(uint64_t seed, uint64_t salt, uint64_t round, uint32_t& k0, uint32_t& k1) {
+    uint64_t k = bvc_dev::mixKey(bvc_dev::mixKey(bvc_dev::mix64(seed), salt), round);
+    k0 = static_cast<uint32_t>(k);
+    k1 = static_cast<uint32_t>(k >> 32);
+}
+
+// salts of the reference (cache.cpp:15-22)
+constexpr uint64_t kBoundaryPosSalt = 0x1001, kBoundaryWalkSalt = 0x1002, kBoundaryRedrawSalt = 0x1003,
+                   kSourceSalt = 0x1004, kFallbackSalt = 0x1005, kFallbackGradSalt = 0x1006, kPointwiseSalt = 0x2001;
+
+double device_seconds(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms * 1e-3;
+}
+
+}  // namespace
+
+namespace bvc_impl {
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace bvc_impl
+
+// ---------------------------------------------------------------------------
+// handles
+// ---------------------------------------------------------------------------
+struct bvc_scene_s {
+    bvc_host::HostScene host;
+    bvc_host::HostBvh bvh;
+    bool uploaded = false;
+    DevBuf<Node2> nodes;
+    DevBuf<Prim2> prims;
+    DevBuf<float2> segNormal, silP;
+    DevBuf<float4> segAB, silN;
+    DevBuf<int> silAlways;
+    // boundary sampler over all segments (BoundarySampler sampling.cpp:8-18)
+    DevBuf<double> cdf;
+    DevBuf<int> cdfIds;
+    DevBuf<float> segArc, segLen;
+    double total = 0.0;
+
+    void upload() {
+        if (uploaded) return;
+        require_device();
+        if (host.dim != 2) throw Error(BVC_ERR_SOLVER, "device queries support 2D scenes (3D walks: §8f)");
+        bvh = bvc_host::buildBvh(host, 4);
+        size_t nn = bvh.children.size() / 2;
+        std::vector<Node2> hn(nn);
+        for (size_t i = 0; i < nn; ++i) {
+            const float* b = &bvh.boxes[8 * i];
+            hn[i].lbox = make_float4(b[0], b[1], b[2], b[3]);
+            hn[i].rbox = make_float4(b[4], b[5], b[6], b[7]);
+            hn[i].left = bvh.children[2 * i];
+            hn[i].right = bvh.children[2 * i + 1];
+            hn[i].mask = bvh.masks[i];
+            hn[i].pad = 0;
+        }
+        nodes.upload(hn.data(), nn);
+        std::vector<Prim2> hp(host.ns);
+        for (int j = 0; j < host.ns; ++j) {
+            int id = bvh.order[j];
+            const double *a = host.vert(host.idx[2 * id]), *b = host.vert(host.idx[2 * id + 1]);
+            hp[j].seg = make_float4(a[0], a[1], b[0], b[1]);
+            hp[j].id = id;
+            hp[j].label = host.label[id];
+            hp[j].sil0 = host.segSil[2 * id];
+            hp[j].sil1 = host.segSil[2 * id + 1];
+        }
+        prims.upload(hp.data(), hp.size());
+        std::vector<float2> hnrm(host.ns);
+        std::vector<float4> hab(host.ns);
+        std::vector<float> harc(host.ns), hlen(host.ns);
+        for (int i = 0; i < host.ns; ++i) {
+            hnrm[i] = make_float2(host.normal[2 * i], host.normal[2 * i + 1]);
+            const double *a = host.vert(host.idx[2 * i]), *b = host.vert(host.idx[2 * i + 1]);
+            hab[i] = make_float4(a[0], a[1], b[0], b[1]);
+            harc[i] = static_cast<float>(host.arc[i]);
+            hlen[i] = static_cast<float>(host.measure[i]);
+        }
+        segNormal.upload(hnrm.data(), hnrm.size());
+        segAB.upload(hab.data(), hab.size());
+        segArc.upload(harc.data(), harc.size());
+        segLen.upload(hlen.data(), hlen.size());
+        size_t nsil = host.silAlways.size();
+        std::vector<float2> hsp(std::max<size_t>(nsil, 1));
+        std::vector<float4> hsn(std::max<size_t>(nsil, 1));
+        std::vector<int> hsa(std::max<size_t>(nsil, 1), 0);
+        for (size_t k = 0; k < nsil; ++k) {
+            hsp[k] = make_float2(host.silP[2 * k], host.silP[2 * k + 1]);
+            hsn[k] = make_float4(host.silN1[2 * k], host.silN1[2 * k + 1], host.silN2[2 * k], host.silN2[2 * k + 1]);
+            hsa[k] = host.silAlways[k];
+        }
+        silP.upload(hsp.data(), hsp.size());
+        silN.upload(hsn.data(), hsn.size());
+        silAlways.upload(hsa.data(), hsa.size());
+        std::vector<double> hc(host.ns);
+        std::vector<int> hid(host.ns);
+        double run = 0.0;
+        for (int i = 0; i < host.ns; ++i) {
+            run += host.measure[i];
+            hc[i] = run;
+            hid[i] = i;
+        }
+        total = run;
+        cdf.upload(hc.data(), hc.size());
+        cdfIds.upload(hid.data(), hid.size());
+        uploaded = true;
+    }
+    bvc_dev::SceneView2 view() {
+        upload();
+        bvc_dev::SceneView2 v;
+        v.nodes = nodes.p;
+        v.prims = prims.p;
+        v.segNormal = segNormal.p;
+        v.segAB = segAB.p;
+        v.silP = silP.p;
+        v.silN = silN.p;
+        v.silAlways = silAlways.p;
+        v.ns = host.ns;
+        v.diagonal = static_cast<float>(host.diagonal);
+        return v;
+    }
+};
+
+struct bvc_region_s {
+    bvc_host::HostRegion host;
+    bvc_scene_s boundary;
+    DevBuf<int> kinds, source;
+    void upload() {
+        boundary.upload();
+        if (!kinds.n) {
+            kinds.upload(host.kinds.data(), host.kinds.size());
+            source.upload(host.source.data(), host.source.size());
+        }
+    }
+};
+
+struct bvc_boundary_cache_s {
+    int n = 0, dim = 2, voronoi = 0;
+    double length = 0.0;
+    DevBuf<CacheSample> samples;
+};
+
+struct bvc_source_cache_s {
+    int m = 0, dim = 2;
+    double area = 0.0;
+    DevBuf<SourceSampleDev> samples;
+};
+
+struct bvc_eval_points_s {
+    size_t n = 0;
+    int dim = 2;
+    std::vector<double> hx;
+    DevBuf<double> x;
+    DevBuf<uint8_t> fallback, unreliable;
+    DevBuf<double> bsum, ssum, bgsum, sgsum, walkSum, gwalkSum;
+    DevBuf<long long> nb, ms, nbg, msg, walkCount, walkTrunc, gwalkCount, skipped;
+    // spatially sorted non-fallback points first, fallback points last
+    bool orderValid = false;
+    int active = 0;
+    DevBuf<int> order;
+    DevBuf<float> xs;
+
+    PointsDev dev() {
+        return PointsDev{bsum.p, ssum.p, nb.p, ms.p, bgsum.p, sgsum.p, nbg.p, msg.p, skipped.p};
+    }
+};
+
+namespace {
+
+__global__ void morton_keys_kernel(const double* x, const uint8_t* fb, int n, int dim, double lo0, double lo1,
+                                   double lo2, double inv, unsigned* keys, int* vals) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    auto spread2 = [](unsigned v) {  // 15 bits -> every other bit
+        v &= 0x7fff;
+        v = (v | (v << 8)) & 0x00ff00ff;
+        v = (v | (v << 4)) & 0x0f0f0f0f;
+        v = (v | (v << 2)) & 0x33333333;
+        v = (v | (v << 1)) & 0x55555555;
+        return v;
+    };
+    auto spread3 = [](unsigned v) {  // 10 bits -> every third bit
+        v &= 0x3ff;
+        v = (v | (v << 16)) & 0x030000ff;
+        v = (v | (v << 8)) & 0x0300f00f;
+        v = (v | (v << 4)) & 0x030c30c3;
+        v = (v | (v << 2)) & 0x09249249;
+        return v;
+    };
+    unsigned key;
+    if (dim == 2) {
+        unsigned a = static_cast<unsigned>(fmin(fmax((x[2 * i] - lo0) * inv, 0.0), 1.0) * 32767.0);
+        unsigned b = static_cast<unsigned>(fmin(fmax((x[2 * i + 1] - lo1) * inv, 0.0), 1.0) * 32767.0);
+        key = spread2(a) | (spread2(b) << 1);
+    } else {
+        unsigned a = static_cast<unsigned>(fmin(fmax((x[3 * i] - lo0) * inv, 0.0), 1.0) * 1023.0);
+        unsigned b = static_cast<unsigned>(fmin(fmax((x[3 * i + 1] - lo1) * inv, 0.0), 1.0) * 1023.0);
+        unsigned c = static_cast<unsigned>(fmin(fmax((x[3 * i + 2] - lo2) * inv, 0.0), 1.0) * 1023.0);
+        key = spread3(a) | (spread3(b) << 1) | (spread3(c) << 2);
+    }
+    if (fb && fb[i]) key |= 0x80000000u;
+    keys[i] = key;
+    vals[i] = i;
+}
+
+__global__ void count_active_kernel(const uint8_t* fb, int n, int* count) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int v = (i < n && !fb[i]) ? 1 : 0;
+    v = __reduce_add_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(count, v);
+}
+
+void ensure_order(bvc_eval_points_s* P) {
+    if (P->orderValid) return;
+    int n = static_cast<int>(P->n);
+    P->order.resize(n);
+    if (n == 0) {
+        P->active = 0;
+        P->orderValid = true;
+        return;
+    }
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int i = 0; i < n; ++i)
+        for (int d = 0; d < P->dim; ++d) {
+            lo[d] = std::min(lo[d], P->hx[P->dim * i + d]);
+            hi[d] = std::max(hi[d], P->hx[P->dim * i + d]);
+        }
+    double ext = 0.0;
+    for (int d = 0; d < P->dim; ++d) ext = std::max(ext, hi[d] - lo[d]);
+    double inv = ext > 0 ? 1.0 / ext : 1.0;
+    unsigned* kin = ws().get<unsigned>(kWsSortKeysIn, n);
+    unsigned* kout = ws().get<unsigned>(kWsSortKeysOut, n);
+    int* vin = ws().get<int>(kWsSortValsIn, n);
+    morton_keys_kernel<<<(n + 255) / 256, 256, 0, g_stream>>>(P->x.p, P->fallback.p, n, P->dim, lo[0], lo[1],
+                                                              P->dim == 3 ? lo[2] : 0.0, inv, kin, vin);
+    count_launch();
+    size_t tmp = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, P->order.p, n, 0, 32, g_stream));
+    void* t = ws().get<char>(kWsSortTemp, tmp);
+    CK(cub::DeviceRadixSort::SortPairs(t, tmp, kin, kout, vin, P->order.p, n, 0, 32, g_stream));
+    count_launch();
+    int* cnt = ws().get<int>(kWsCount, 1);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(int), g_stream));
+    count_active_kernel<<<(n + 255) / 256, 256, 0, g_stream>>>(P->fallback.p, n, cnt);
+    count_launch();
+    CK(cudaMemcpyAsync(&P->active, cnt, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+    P->xs.resize(static_cast<size_t>(P->dim) * std::max(P->active, 1));
+    gather_points(P->x.p, P->order.p, P->active, P->dim, P->xs.p, g_stream);
+    P->orderValid = true;
+}
+
+WalkEnv make_env(bvc_scene_s* S, const bvc_problem& pb, const bvc_walk_config& wc, uint64_t seed, uint64_t salt,
+                 uint64_t round) {
+    validate_kernel(pb.kernel);
+    if (pb.kernel.dim != 2) throw Error(BVC_ERR_SOLVER, "walk estimators support dim == 2 only");
+    WalkEnv E{};
+    E.S = S->view();
+    E.P.screened = pb.kernel.kind == BVC_KERNEL_SCREENED;
+    E.P.sigma = static_cast<float>(pb.kernel.sigma);
+    E.P.sqrtSigma = static_cast<float>(std::sqrt(pb.kernel.sigma));
+    E.P.dim = 2;
+    E.P.f = to_dev(pb.f);
+    E.P.g = to_dev(pb.g);
+    E.P.h = to_dev(pb.h);
+    double diag = S->host.diagonal;
+    double eps = wc.epsilon > 0.0 ? wc.epsilon : 1e-3 * diag;         // pointwise.h:36-38
+    double rmin = wc.rMin > 0.0 ? wc.rMin : eps;                        // pointwise.h:39-44
+    if (rmin > eps) throw Error(BVC_ERR_INVALID_ARGUMENT, "walk config: r_min must lie in (0, epsilon]");
+    E.eps = static_cast<float>(eps);
+    E.rmin = static_cast<float>(rmin);
+    // the reference's tGuard is 1e-9 diag (pointwise.cpp:115); FP32 positions need a
+    // guard above their rounding, and the current segment is skipped explicitly
+    E.tguard = static_cast<float>(1e-9 * diag);  // pointwise.cpp:115; the standing segment is skipped
+    E.insideTol = S->host.closed() ? static_cast<float>(std::max(1e-9, 1e-7) * diag) : -1.0f;
+    E.scale = static_cast<float>(diag);
+    E.nudge = static_cast<float>(9.5367431640625e-7 * diag);  // 2^-20 diag, << eps
+    E.cx = static_cast<float>(0.5 * (S->host.lo[0] + S->host.hi[0]));
+    E.cy = static_cast<float>(0.5 * (S->host.lo[1] + S->host.hi[1]));
+    E.escape = static_cast<float>(diag);
+    E.maxSteps = std::max(1, wc.maxSteps);
+    E.hasNeumann = S->host.hasNeumann() ? 1 : 0;
+    E.hasSource = pb.f.kind != BVC_FIELD_NONE ? 1 : 0;
+    E.hasH = pb.h.kind != BVC_FIELD_NONE ? 1 : 0;
+    E.closed = S->host.closed() ? 1 : 0;
+    if (!(S->host.dirichletMeasure > 0.0))
+        throw Error(BVC_ERR_SOLVER, "walk cannot terminate: scene has no Dirichlet boundary");
+    key_of(seed, salt, round, E.k0, E.k1);
+    return E;
+}
+
+struct GenStats {
+    long long walks = 0, truncated = 0, steps = 0, resampled = 0;
+};
+
+// walks for the samples [0, n) of `samples` (already positioned); writes uHat/dHat
+// and returns per-sample failure flags in `failed` (device)
+void run_cache_walks(bvc_scene_s* S, bvc_region_s* R, const WalkEnv& E, const bvc_cache_config& cfg,
+                     CacheSample* samples, int n, long long gidBase, const long long* gid, uint8_t* failed,
+                     GenStats& st) {
+    float2* startU = ws().get<float2>(kWsStartU, n);
+    int* isD = ws().get<int>(kWsIsD, n);
+    float* gradR = ws().get<float>(kWsGradR, n);
+    launch_prepare_samples(E, samples, n, R->kinds.p, R->source.p, startU, isD, gradR, failed, g_stream);
+    int* dIdx = ws().get<int>(kWsDIdx, n);
+    int* cnt = ws().get<int>(kWsCount, 1);
+    launch_compact(isD, n, dIdx, cnt, g_stream);
+    int nD = 0;
+    CK(cudaMemcpyAsync(&nD, cnt, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+    float2* xD = ws().get<float2>(kWsXD, std::max(nD, 1));
+    float2* nrmD = ws().get<float2>(kWsND, std::max(nD, 1));
+    float* rD = ws().get<float>(kWsRD, std::max(nD, 1));
+    long long* gidD = ws().get<long long>(kWsGidD, std::max(nD, 1));
+    launch_gather_dpoints(samples, dIdx, nD, gradR, gidBase, gid, xD, nrmD, rD, gidD, g_stream);
+    int nU = std::max(1, cfg.nWalksNeumann), nDw = std::max(1, cfg.nWalksDirichlet);
+    WalkJob J{};
+    J.nU = nU;
+    J.nPtsU = n;
+    J.startU = startU;
+    J.gidU = gid;
+    J.gidBaseU = gidBase;
+    J.outU = ws().get<float>(kWsOutU, static_cast<size_t>(n) * nU);
+    J.nD = nDw;
+    J.nPtsD = nD;
+    J.xD = xD;
+    J.normalD = nrmD;
+    J.radiusD = rD;
+    J.gidD = gidD;
+    J.outD = ws().get<float>(kWsOutD, std::max<size_t>(static_cast<size_t>(nD) * nDw, 1));
+    auto* ctr = ws().get<unsigned long long>(kWsCounter, 3);
+    CK(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), g_stream));
+    J.counter = ctr;
+    J.steps = ctr + 1;
+    J.truncTotal = ctr + 2;
+    launch_walk_job(E, J, g_stream);
+    launch_finish_samples(samples, n, J.outU, nU, dIdx, nD, J.outD, nDw, failed, g_stream);
+    unsigned long long h[3];
+    CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+    st.walks += static_cast<long long>(n) * nU + static_cast<long long>(nD) * nDw;
+    st.steps += static_cast<long long>(h[1]);
+    st.truncated += static_cast<long long>(h[2]);
+}
+
+__global__ void redraw_copy_kernel(const CacheSample* src, const int* idx, int n, CacheSample* dst) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) dst[idx[j]] = src[j];
+}
+
+void generate_cache(bvc_scene_s* S, const bvc_problem& pb, bvc_region_s* R, const bvc_cache_config& cfg, uint64_t seed,
+                    uint64_t round, int begin, int end, bvc_boundary_cache_s* out, GenStats& st) {
+    require_device();
+    need(S && R, "null scene or region");
+    R->upload();
+    const int N = std::max(1, cfg.nBoundary);
+    need(begin >= 0 && begin <= end && end <= N, "shard range outside [0, nBoundary]");
+    if (cfg.clampMode != BVC_CLAMP_OFF || cfg.sourceBall)
+        throw Error(BVC_ERR_INVALID_ARGUMENT, "clamped / ball-kernel splats are not implemented (SURVEY §8f.3)");
+    const int n = end - begin;
+    out->n = n;
+    out->dim = 2;
+    out->voronoi = cfg.voronoi;
+    out->length = R->boundary.total;
+    out->samples.resize(std::max(n, 1));
+    if (n == 0) return;
+    bvc_scene_s& B = R->boundary;
+    uint32_t k0, k1;
+    key_of(seed, kBoundaryPosSalt, round, k0, k1);
+    launch_sample_boundary(B.cdf.p, B.cdfIds.p, B.host.ns, B.total, B.segAB.p, B.segNormal.p, B.segArc.p, B.segLen.p, N,
+                           begin, n, nullptr, cfg.stratified, k0, k1, out->samples.p, g_stream);
+    WalkEnv E = make_env(S, pb, cfg.walk, seed, kBoundaryWalkSalt, round);
+    uint8_t* failed = ws().get<uint8_t>(kWsFailed, n);
+    run_cache_walks(S, R, E, cfg, out->samples.p, n, begin, nullptr, failed, st);
+    // deterministic redraw of failed samples (cache.cpp:365-379): a fresh uniform
+    // position per (sample, attempt), walks keyed by the redraw salt
+    std::vector<uint8_t> hf(n);
+    CK(cudaMemcpyAsync(hf.data(), failed, n, cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+    std::vector<int> bad;
+    for (int i = 0; i < n; ++i) if (hf[i]) bad.push_back(i);
+    WalkEnv Er = make_env(S, pb, cfg.walk, seed, kBoundaryRedrawSalt, round);
+    for (int guard = 1; !bad.empty(); ++guard) {
+        if (guard > 64) throw Error(BVC_ERR_SOLVER, "boundary cache: sample kept failing after 64 redraws");
+        int nb = static_cast<int>(bad.size());
+        st.resampled += nb;
+        std::vector<long long> hc(nb);
+        for (int j = 0; j < nb; ++j) hc[j] = (static_cast<long long>(begin) + bad[j]) * 131 + guard;
+        long long* dctr = ws().get<long long>(kWsCtr, nb);
+        CK(cudaMemcpyAsync(dctr, hc.data(), nb * sizeof(long long), cudaMemcpyHostToDevice, g_stream));
+        CacheSample* tmp = ws().get<CacheSample>(kWsSamplesTmp, nb);
+        uint32_t r0, r1;
+        key_of(seed, kBoundaryRedrawSalt, round, r0, r1);
+        launch_sample_boundary(B.cdf.p, B.cdfIds.p, B.host.ns, B.total, B.segAB.p, B.segNormal.p, B.segArc.p,
+                               B.segLen.p, N, 0, nb, dctr, 0, r0, r1, tmp, g_stream);
+        uint8_t* f2 = ws().get<uint8_t>(kWsSrcFlag, nb);
+        run_cache_walks(S, R, Er, cfg, tmp, nb, 0, dctr, f2, st);
+        int* didx = ws().get<int>(kWsDIdx + 0, nb);  // reuse after walks are done
+        std::vector<int> hb(bad.begin(), bad.end());
+        CK(cudaMemcpyAsync(didx, hb.data(), nb * sizeof(int), cudaMemcpyHostToDevice, g_stream));
+        redraw_copy_kernel<<<(nb + 127) / 128, 128, 0, g_stream>>>(tmp, didx, nb, out->samples.p);
+        count_launch();
+        std::vector<uint8_t> hf2(nb);
+        CK(cudaMemcpyAsync(hf2.data(), f2, nb, cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+        std::vector<int> still;
+        for (int j = 0; j < nb; ++j) if (hf2[j]) still.push_back(bad[j]);
+        bad.swap(still);
+    }
+    if (cfg.voronoi) {  // assignVoronoiWeights cache.cpp:280-297, on the host (rare mode)
+        std::vector<CacheSample> hs(n);
+        out->samples.download(hs.data(), n);
+        CK(cudaStreamSynchronize(g_stream));
+        const auto& bh = B.host;
+        std::vector<std::vector<std::pair<double, int>>> per(bh.loopLength.size());
+        for (int i = 0; i < n; ++i) per[bh.loop[hs[i].segment]].push_back({hs[i].arc, i});
+        for (size_t li = 0; li < per.size(); ++li) {
+            auto& e = per[li];
+            if (e.empty()) continue;
+            std::sort(e.begin(), e.end());
+            size_t m = e.size();
+            double L = bh.loopLength[li];
+            for (size_t k = 0; k < m; ++k) {
+                double w;
+                if (m == 1) w = L;
+                else {
+                    double prev = k > 0 ? e[k].first - e[k - 1].first : e[0].first + L - e[m - 1].first;
+                    double next = k + 1 < m ? e[k + 1].first - e[k].first : e[0].first + L - e[m - 1].first;
+                    w = 0.5 * (prev + next);
+                }
+                hs[e[k].second].weight = static_cast<float>(w);
+            }
+        }
+        out->samples.upload(hs.data(), n);
+    }
+}
+
+// RegionSampler::sample (sampling.cpp:62-108): jittered strata over the bounding
+// box, rejection by the device inside test; the last pass keeps a random subset
+__global__ void region_propose_kernel(int g, double lo0, double lo1, double ex, double ey, int pass, int stratified,
+                                      uint32_t k0, uint32_t k1, float insideTol, bvc_dev::SceneView2 S, float* y,
+                                      int* ok, unsigned* prio) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= g * g) return;
+    bvc_dev::U4 r = bvc_dev::philox4x32_10(bvc_dev::U4{static_cast<uint32_t>(c), static_cast<uint32_t>(pass), 7u, 0u}, k0, k1);
+    double ux = (static_cast<double>(r.x >> 5) * 67108864.0 + (r.y >> 6)) * (1.0 / 9007199254740992.0);
+    double uy = (static_cast<double>(r.z >> 5) * 67108864.0 + (r.w >> 6)) * (1.0 / 9007199254740992.0);
+    double px, py;
+    if (stratified) {
+        int cx = c % g, cy = c / g;
+        px = lo0 + (cx + ux) / g * ex;
+        py = lo1 + (cy + uy) / g * ey;
+    } else {
+        px = lo0 + ux * ex;
+        py = lo1 + uy * ey;
+    }
+    y[2 * c] = static_cast<float>(px);
+    y[2 * c + 1] = static_cast<float>(py);
+    ok[c] = bvc_dev::inside(S, static_cast<float>(px), static_cast<float>(py), insideTol) ? 1 : 0;
+    bvc_dev::U4 q = bvc_dev::philox4x32_10(bvc_dev::U4{static_cast<uint32_t>(c), static_cast<uint32_t>(pass), 9u, 0u}, k0, k1);
+    prio[c] = q.x;
+}
+
+__global__ void source_emit_kernel(const float* y, const int* idx, int n, int base, float pdf, bvc_dev::DevField f,
+                                   SourceSampleDev* out) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int c = idx[j];
+    SourceSampleDev s{};
+    s.y[0] = y[2 * c];
+    s.y[1] = y[2 * c + 1];
+    s.pdf = pdf;
+    s.f = bvc_dev::field_eval(f, s.y[0], s.y[1]);
+    out[base + j] = s;
+}
+
+void generate_source(const bvc_problem& pb, bvc_region_s* R, const bvc_cache_config& cfg, uint64_t seed, uint64_t round,
+                     bvc_source_cache_s* out) {
+    require_device();
+    R->upload();
+    bvc_scene_s& B = R->boundary;
+    out->dim = 2;
+    out->area = bvc_host::loopArea(B.host);
+    if (!B.host.closed()) throw Error(BVC_ERR_PARSE, "region sampler requires closed loops");
+    if (out->area <= 0.0) throw Error(BVC_ERR_PARSE, "region sampler: non-positive area");
+    if (pb.f.kind == BVC_FIELD_NONE) {
+        out->m = 0;
+        return;
+    }
+    const int M = std::max(1, cfg.nSource);
+    out->m = M;
+    out->samples.resize(M);
+    int g = std::max(1, static_cast<int>(std::ceil(std::sqrt(static_cast<double>(M)))));
+    int cells = cfg.stratified ? g * g : M;
+    if (!cfg.stratified) g = static_cast<int>(std::ceil(std::sqrt(static_cast<double>(cells))));
+    float* y = ws().get<float>(kWsSrcTmp, 2 * static_cast<size_t>(g) * g);
+    int* ok = ws().get<int>(kWsIsD, static_cast<size_t>(g) * g);
+    unsigned* prio = ws().get<unsigned>(kWsSortKeysIn, static_cast<size_t>(g) * g);
+    int* idx = ws().get<int>(kWsDIdx, static_cast<size_t>(g) * g);
+    int* cnt = ws().get<int>(kWsCount, 1);
+    uint32_t k0, k1;
+    key_of(seed, kSourceSalt, round, k0, k1);
+    const auto& h = B.host;
+    double ex = h.hi[0] - h.lo[0], ey = h.hi[1] - h.lo[1];
+    float tol = static_cast<float>(1e-7 * h.diagonal);
+    bvc_dev::SceneView2 SV = B.view();
+    bvc_dev::DevField f = to_dev(pb.f);
+    long long proposals = 0;
+    int accepted = 0;
+    for (int pass = 0; accepted < M; ++pass) {
+        int nc = g * g;
+        region_propose_kernel<<<(nc + 127) / 128, 128, 0, g_stream>>>(g, h.lo[0], h.lo[1], ex, ey, pass,
+                                                                      cfg.stratified, k0, k1, tol, SV, y, ok, prio);
+        count_launch();
+        launch_compact(ok, nc, idx, cnt, g_stream);
+        int na = 0;
+        CK(cudaMemcpyAsync(&na, cnt, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+        proposals += nc;
+        if (proposals >= 1000000 && accepted + na < proposals / 10000)
+            throw Error(BVC_ERR_PARSE, "degenerate region: rejection acceptance rate below 1e-4");
+        int take = std::min(na, M - accepted);
+        if (take < na) {  // final pass: a random subset (a shuffled visiting order)
+            std::vector<int> hidx(na);
+            std::vector<unsigned> hp(static_cast<size_t>(nc));
+            CK(cudaMemcpyAsync(hidx.data(), idx, na * sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+            CK(cudaMemcpyAsync(hp.data(), prio, nc * sizeof(unsigned), cudaMemcpyDeviceToHost, g_stream));
+            CK(cudaStreamSynchronize(g_stream));
+            std::stable_sort(hidx.begin(), hidx.end(), [&](int a, int b) { return hp[a] < hp[b]; });
+            hidx.resize(take);
+            std::sort(hidx.begin(), hidx.end());
+            CK(cudaMemcpyAsync(idx, hidx.data(), take * sizeof(int), cudaMemcpyHostToDevice, g_stream));
+        }
+        source_emit_kernel<<<(take + 127) / 128, 128, 0, g_stream>>>(y, idx, take, accepted, static_cast<float>(1.0 / out->area), f,
+                                                                     out->samples.p);
+        count_launch();
+        accepted += take;
+    }
+}
+
+int gather_kind(const bvc_kernel_spec& k) {
+    bool scr = k.kind == BVC_KERNEL_SCREENED;
+    return k.dim == 2 ? (scr ? kScr2 : kLap2) : (scr ? kScr3 : kLap3);
+}
+
+void splat(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_points_s* P, const bvc_splat_config& cfg,
+           size_t begin, size_t end, bool val, bool grad) {
+    require_device();
+    need(P != nullptr, "null evaluation points");
+    validate_kernel(cfg.kernel);
+    if (cfg.useBallGreens) throw Error(BVC_ERR_INVALID_ARGUMENT, "ball-kernel splats are not implemented (SURVEY §8f.3)");
+    int dim = cfg.kernel.dim;
+    need(P->dim == dim, "evaluation points and kernel differ in dimension");
+    int N = b ? b->n : 0, M = s ? s->m : 0;
+    need(!b || b->dim == dim, "boundary cache dimension mismatch");
+    need(!s || s->dim == dim, "source cache dimension mismatch");
+    ensure_order(P);
+    size_t Ka = static_cast<size_t>(P->active);
+    end = std::min(end, Ka);
+    if (begin >= end) return;
+    int K = static_cast<int>(end - begin);
+    int kind = gather_kind(cfg.kernel);
+    float4* pack = ws().get<float4>(kWsPack, 2 * static_cast<size_t>(std::max(N + M, 1)));
+    if (N) pack_boundary(b->samples.p, N, kind, cfg.voronoi, pack, g_stream);
+    if (M) pack_source(s->samples.p, M, kind, pack + 2 * static_cast<size_t>(N), g_stream);
+    GatherPlan plan = plan_gather(kind, K, N, M, val, grad);
+    double* part = ws().get<double>(kWsPart, std::max<size_t>(static_cast<size_t>(plan.chunksB + plan.chunksS) * plan.comps * K, 1));
+    int* skipB = ws().get<int>(kWsSkipB, K);
+    int* skipS = ws().get<int>(kWsSkipS, K);
+    CK(cudaMemsetAsync(skipB, 0, K * sizeof(int), g_stream));
+    CK(cudaMemsetAsync(skipS, 0, K * sizeof(int), g_stream));
+    if (N + M > 0)
+        launch_gather(kind, plan, pack, N, M, P->xs.p + static_cast<size_t>(dim) * begin, K, dim,
+                      static_cast<float>(cfg.kernel.sigma), static_cast<float>(cfg.coincidenceTol), val, grad, part,
+                      skipB, skipS, g_stream);
+    else
+        CK(cudaMemsetAsync(part, 0, sizeof(double), g_stream));
+    if (N + M > 0)
+        launch_finalize(part, plan, K, P->order.p + begin, N, M, val, grad, dim, skipB, skipS, P->dev(), g_stream);
+    CK(cudaGetLastError());
+}
+
+// estimator job over host points (pointwise.h:62-76)
+void pointwise(bvc_scene_s* S, const bvc_problem& pb, const double* x, const double* normal, size_t n,
+               const bvc_walk_config& cfg, const uint64_t* streams, int mode, double* mean, double* se,
+               long long* count, long long* trunc) {
+    // mode 0: wos / wost solve, 1: gradient (2 comps), 2: normal derivative
+    require_device();
+    need(S && x, "null scene or points");
+    if (n == 0) return;
+    WalkEnv E = make_env(S, pb, cfg, cfg.seed, kPointwiseSalt, 0);
+    int nw = std::max(1, cfg.nWalks);
+    int ni = static_cast<int>(n);
+    std::vector<long long> gid(ni);
+    for (int i = 0; i < ni; ++i) {
+        uint64_t st = streams ? streams[i] : (ni == 1 ? cfg.stream : bvc_dev::mixKey(cfg.stream, i));
+        gid[i] = static_cast<long long>(bvc_dev::mix64(st) >> 1);
+    }
+    // requireInterior (pointwise.cpp:188-191)
+    double* xd = ws().get<double>(kWsEvalIn, 2 * n);
+    CK(cudaMemcpyAsync(xd, x, 2 * n * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+    if (S->host.closed()) {
+        uint8_t* ins = ws().get<uint8_t>(kWsOutside, n);
+        launch_inside(E.S, xd, ni, E.insideTol, ins, g_stream);
+        std::vector<uint8_t> h(n);
+        CK(cudaMemcpyAsync(h.data(), ins, n, cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+        for (size_t i = 0; i < n; ++i)
+            if (!h[i]) throw Error(BVC_ERR_SOLVER, "evaluation point lies outside the domain");
+    }
+    std::vector<float2> hx(n);
+    for (size_t i = 0; i < n; ++i) hx[i] = make_float2(static_cast<float>(x[2 * i]), static_cast<float>(x[2 * i + 1]));
+    float2* px = ws().get<float2>(kWsStartU, n);
+    CK(cudaMemcpyAsync(px, hx.data(), n * sizeof(float2), cudaMemcpyHostToDevice, g_stream));
+    long long* dg = ws().get<long long>(kWsGidU, n);
+    CK(cudaMemcpyAsync(dg, gid.data(), n * sizeof(long long), cudaMemcpyHostToDevice, g_stream));
+    int* tr = ws().get<int>(kWsTruncPt, n);
+    CK(cudaMemsetAsync(tr, 0, n * sizeof(int), g_stream));
+    auto* ctr = ws().get<unsigned long long>(kWsCounter, 3);
+    CK(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), g_stream));
+    WalkJob J{};
+    J.counter = ctr;
+    J.steps = ctr + 1;
+    J.truncTotal = ctr + 2;
+    int comps = 1;
+    if (mode == 0) {
+        J.nU = nw;
+        J.nPtsU = ni;
+        J.startU = px;
+        J.gidU = dg;
+        J.outU = ws().get<float>(kWsOutU, n * nw);
+        J.truncU = tr;
+    } else {
+        // gradientBallRadius: closest point on the whole boundary (pointwise.cpp:217-221)
+        double* cpp = ws().get<double>(kWsEvalOut, 2 * n);
+        double* cpd = ws().get<double>(kWsMean2, n);
+        int* cps = ws().get<int>(kWsSkipB, n);
+        double* cpt = ws().get<double>(kWsSe2, n);
+        launch_closest(E.S, xd, ni, 3u, cpp, cpd, cps, cpt, g_stream);
+        std::vector<double> hd(n);
+        CK(cudaMemcpyAsync(hd.data(), cpd, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+        std::vector<float> hr(n);
+        for (size_t i = 0; i < n; ++i) hr[i] = static_cast<float>(std::max(hd[i], static_cast<double>(E.rmin)));
+        float* rD = ws().get<float>(kWsRD, n);
+        CK(cudaMemcpyAsync(rD, hr.data(), n * sizeof(float), cudaMemcpyHostToDevice, g_stream));
+        J.nD = nw;
+        J.nPtsD = ni;
+        J.xD = px;
+        J.radiusD = rD;
+        J.gidD = dg;
+        J.truncD = tr;
+        if (mode == 2) {
+            std::vector<float2> hn(n);
+            for (size_t i = 0; i < n; ++i) hn[i] = make_float2(static_cast<float>(normal[2 * i]), static_cast<float>(normal[2 * i + 1]));
+            float2* dn = ws().get<float2>(kWsND, n);
+            CK(cudaMemcpyAsync(dn, hn.data(), n * sizeof(float2), cudaMemcpyHostToDevice, g_stream));
+            J.normalD = dn;
+        } else {
+            comps = 2;
+        }
+        J.outD = ws().get<float>(kWsOutD, n * nw * comps);
+    }
+    launch_walk_job(E, J, g_stream);
+    const float* vals = mode == 0 ? J.outU : J.outD;
+    double* dm = ws().get<double>(kWsMean, n * comps);
+    double* ds = ws().get<double>(kWsSe, n * comps);
+    for (int c = 0; c < comps; ++c) launch_reduce_estimates(vals, ni, nw, comps, c, dm + c * n, ds + c * n, g_stream);
+    std::vector<double> hm(n * comps), hs(n * comps);
+    std::vector<int> ht(n);
+    CK(cudaMemcpyAsync(hm.data(), dm, n * comps * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaMemcpyAsync(hs.data(), ds, n * comps * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaMemcpyAsync(ht.data(), tr, n * sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+    for (size_t i = 0; i < n; ++i) {
+        for (int c = 0; c < comps; ++c) {
+            mean[comps * i + c] = hm[c * n + i];
+            se[comps * i + c] = hs[c * n + i];
+        }
+        count[i] = nw;
+        trunc[i] = ht[i];
+    }
+    for (size_t i = 0; i < n * comps; ++i)
+        if (!std::isfinite(mean[i])) throw Error(BVC_ERR_SOLVER, "walk cannot terminate: scene has no Dirichlet boundary");
+}
+
+// fallback walks of updateSolution (cache.cpp:665-681), accumulated on the device
+__global__ void fallback_accumulate_kernel(const int* idx, int n, const double* mean, const double* g0,
+                                           const double* g1, int nw, int ngw, const int* trunc, double* walkSum,
+                                           long long* walkCount, long long* walkTrunc, double* gws, long long* gwc) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int p = idx[j];
+    walkSum[p] += mean[j] * nw;
+    walkCount[p] += nw;
+    walkTrunc[p] += trunc[j];
+    if (g0) {
+        gws[2 * p] += g0[j] * ngw;
+        gws[2 * p + 1] += g1[j] * ngw;
+        gwc[p] += ngw;
+    }
+}
+
+__global__ void gather_fallback_kernel(const int* idx, int n, const double* x, float2* out, long long* gid) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int p = idx[j];
+    out[j] = make_float2(static_cast<float>(x[2 * p]), static_cast<float>(x[2 * p + 1]));
+    gid[j] = p;
+}
+
+void fallback_walks(bvc_scene_s* S, const bvc_problem& pb, const bvc_cache_config& cfg, bvc_eval_points_s* P,
+                    uint64_t seed, uint64_t round, bool gradients) {
+    ensure_order(P);
+    int nf = static_cast<int>(P->n) - P->active;
+    if (nf <= 0) return;
+    const int* idx = P->order.p + P->active;
+    int nw = std::max(1, cfg.walk.nWalks);
+    float2* px = ws().get<float2>(kWsStartU, nf);
+    long long* gid = ws().get<long long>(kWsGidU, nf);
+    gather_fallback_kernel<<<(nf + 127) / 128, 128, 0, g_stream>>>(idx, nf, P->x.p, px, gid);
+    count_launch();
+    if (S->host.closed()) {  // requireInterior
+        WalkEnv E0 = make_env(S, pb, cfg.walk, seed, kFallbackSalt, round);
+        double* xd = ws().get<double>(kWsEvalIn, 2 * static_cast<size_t>(nf));
+        // positions of fallback points in double
+        std::vector<int> hidx(nf);
+        CK(cudaMemcpyAsync(hidx.data(), idx, nf * sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+        std::vector<double> hx(2 * static_cast<size_t>(nf));
+        for (int j = 0; j < nf; ++j) { hx[2 * j] = P->hx[2 * hidx[j]]; hx[2 * j + 1] = P->hx[2 * hidx[j] + 1]; }
+        CK(cudaMemcpyAsync(xd, hx.data(), hx.size() * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        uint8_t* ins = ws().get<uint8_t>(kWsOutside, nf);
+        launch_inside(E0.S, xd, nf, E0.insideTol, ins, g_stream);
+        std::vector<uint8_t> h(nf);
+        CK(cudaMemcpyAsync(h.data(), ins, nf, cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+        for (int j = 0; j < nf; ++j)
+            if (!h[j]) throw Error(BVC_ERR_SOLVER, "evaluation point lies outside the domain");
+    }
+    auto* ctr = ws().get<unsigned long long>(kWsCounter, 3);
+    int* tr = ws().get<int>(kWsTruncPt, nf);
+    CK(cudaMemsetAsync(tr, 0, nf * sizeof(int), g_stream));
+    CK(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), g_stream));
+    WalkEnv E = make_env(S, pb, cfg.walk, seed, kFallbackSalt, round);
+    WalkJob J{};
+    J.counter = ctr;
+    J.nU = nw;
+    J.nPtsU = nf;
+    J.startU = px;
+    J.gidU = gid;
+    J.outU = ws().get<float>(kWsOutU, static_cast<size_t>(nf) * nw);
+    J.truncU = tr;
+    launch_walk_job(E, J, g_stream);
+    double* dm = ws().get<double>(kWsMean, nf);
+    launch_reduce_estimates(J.outU, nf, nw, 1, 0, dm, nullptr, g_stream);
+    double *g0 = nullptr, *g1 = nullptr;
+    if (gradients) {
+        WalkEnv Eg = make_env(S, pb, cfg.walk, seed, kFallbackGradSalt, round);
+        double* xd = ws().get<double>(kWsEvalIn, 2 * static_cast<size_t>(nf));
+        std::vector<int> hidx(nf);
+        CK(cudaMemcpyAsync(hidx.data(), idx, nf * sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+        std::vector<double> hx(2 * static_cast<size_t>(nf));
+        for (int j = 0; j < nf; ++j) { hx[2 * j] = P->hx[2 * hidx[j]]; hx[2 * j + 1] = P->hx[2 * hidx[j] + 1]; }
+        CK(cudaMemcpyAsync(xd, hx.data(), hx.size() * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        double* cpp = ws().get<double>(kWsEvalOut, 2 * static_cast<size_t>(nf));
+        double* cpd = ws().get<double>(kWsMean2, nf);
+        int* cps = ws().get<int>(kWsSkipB, nf);
+        double* cpt = ws().get<double>(kWsSe2, nf);
+        launch_closest(Eg.S, xd, nf, 3u, cpp, cpd, cps, cpt, g_stream);
+        std::vector<double> hd(nf);
+        CK(cudaMemcpyAsync(hd.data(), cpd, nf * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+        std::vector<float> hr(nf);
+        for (int j = 0; j < nf; ++j) hr[j] = static_cast<float>(std::max(hd[j], static_cast<double>(Eg.rmin)));
+        float* rD = ws().get<float>(kWsRD, nf);
+        CK(cudaMemcpyAsync(rD, hr.data(), nf * sizeof(float), cudaMemcpyHostToDevice, g_stream));
+        CK(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), g_stream));
+        WalkJob G{};
+        G.counter = ctr;
+        G.nD = nw;
+        G.nPtsD = nf;
+        G.xD = px;
+        G.radiusD = rD;
+        G.gidD = gid;
+        G.outD = ws().get<float>(kWsOutD, static_cast<size_t>(nf) * nw * 2);
+        launch_walk_job(Eg, G, g_stream);
+        g0 = ws().get<double>(kWsSe, nf);
+        g1 = ws().get<double>(kWsMean2, nf);
+        launch_reduce_estimates(G.outD, nf, nw, 2, 0, g0, nullptr, g_stream);
+        launch_reduce_estimates(G.outD, nf, nw, 2, 1, g1, nullptr, g_stream);
+    }
+    fallback_accumulate_kernel<<<(nf + 127) / 128, 128, 0, g_stream>>>(idx, nf, dm, g0, g1, nw, nw, tr, P->walkSum.p,
+                                                                       P->walkCount.p, P->walkTrunc.p, P->gwalkSum.p,
+                                                                       P->gwalkCount.p);
+    count_launch();
+}
+
+bvc_splat_config make_splat_config(bvc_scene_s* S, const bvc_problem& pb, const bvc_cache_config& cfg) {
+    validate_kernel(pb.kernel);
+    bvc_splat_config s{};
+    s.kernel = pb.kernel;
+    s.kernel.scale = S->host.diagonal;
+    s.coincidenceTol = 1e-12 * S->host.diagonal;
+    s.voronoi = cfg.voronoi;
+    s.useBallGreens = cfg.sourceBall;
+    if (s.useBallGreens && s.kernel.kind != BVC_KERNEL_POISSON)
+        throw Error(BVC_ERR_SOLVER, "ball-kernel source mode requires the Poisson kernel");
+    return s;
+}
+
+void alloc_points(bvc_eval_points_s* P) {
+    size_t n = std::max<size_t>(P->n, 1);
+    int d = P->dim;
+    P->x.resize(d * n);
+    P->fallback.resize(n);
+    P->unreliable.resize(n);
+    P->bsum.resize(n); P->ssum.resize(n); P->bgsum.resize(d * n); P->sgsum.resize(d * n);
+    P->walkSum.resize(n); P->gwalkSum.resize(d * n);
+    P->nb.resize(n); P->ms.resize(n); P->nbg.resize(n); P->msg.resize(n);
+    P->walkCount.resize(n); P->walkTrunc.resize(n); P->gwalkCount.resize(n); P->skipped.resize(n);
+}
+
+void zero_points(bvc_eval_points_s* P) {
+    P->fallback.zero(); P->unreliable.zero();
+    P->bsum.zero(); P->ssum.zero(); P->bgsum.zero(); P->sgsum.zero(); P->walkSum.zero(); P->gwalkSum.zero();
+    P->nb.zero(); P->ms.zero(); P->nbg.zero(); P->msg.zero(); P->walkCount.zero(); P->walkTrunc.zero();
+    P->gwalkCount.zero(); P->skipped.zero();
+}
+
+__global__ void mark_kernel(const bvc_dev::SceneView2 scene, const bvc_dev::SceneView2 region, const double* x, int n,
+                            float offset, int whole, uint8_t* fb, uint8_t* gu) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float px = static_cast<float>(x[2 * i]), py = static_cast<float>(x[2 * i + 1]);
+    // fallbackBand cache.cpp:131-135: whole-domain points within l of the Dirichlet boundary
+    uint8_t f = 0;
+    if (whole) {
+        bvc_dev::Closest c = bvc_dev::closest_point(scene, px, py, 1u);
+        f = (c.seg >= 0 && c.d2 < offset * offset) ? 1 : 0;
+    }
+    bvc_dev::Closest r = bvc_dev::closest_point(region, px, py, 3u);
+    fb[i] = f;
+    gu[i] = (r.seg >= 0 && r.d2 < offset * offset) ? 1 : 0;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* bvc_last_error(void) { return g_error.c_str(); }
+int bvc_abi_version(void) { return BVC_ABI_VERSION; }
+long long bvc_kernel_launch_count(void) { return g_launches.load(); }
+
+int bvc_set_device(int device) { API(require_device(); CK(cudaSetDevice(device))) }
+int bvc_set_stream(void* s) { API(g_stream = static_cast<cudaStream_t>(s)) }
+int bvc_synchronize(void) { API(require_device(); CK(cudaStreamSynchronize(g_stream))) }
+
+int bvc_scene_create(const double* v, int nv, const int* segs, const int* labels, int ns, bvc_scene* out) {
+    API({
+        need(out && v && segs && labels, "null argument");
+        auto s = std::make_unique<bvc_scene_s>();
+        s->host = bvc_host::buildScene2(v, nv, segs, labels, ns);
+        *out = s.release();
+    })
+}
+int bvc_scene_create_mesh3(const double* v, int nv, const int* tris, const int* labels, int nt, bvc_scene* out) {
+    API({
+        need(out && v && tris && labels, "null argument");
+        auto s = std::make_unique<bvc_scene_s>();
+        s->host = bvc_host::buildMesh3(v, nv, tris, labels, nt);
+        *out = s.release();
+    })
+}
+int bvc_scene_destroy(bvc_scene s) { API(delete s) }
+int bvc_scene_info(bvc_scene s, int* dim, double* diag, double* lo, double* hi, double* dl, double* nl, int* closed,
+                   int* nloops) {
+    API({
+        need(s, "null scene");
+        const auto& h = s->host;
+        if (dim) *dim = h.dim;
+        if (diag) *diag = h.diagonal;
+        for (int k = 0; k < h.dim; ++k) {
+            if (lo) lo[k] = h.lo[k];
+            if (hi) hi[k] = h.hi[k];
+        }
+        if (dl) *dl = h.dirichletMeasure;
+        if (nl) *nl = h.neumannMeasure;
+        if (closed) *closed = h.closed() ? 1 : 0;
+        if (nloops) *nloops = static_cast<int>(h.loopLength.size());
+    })
+}
+
+int bvc_scene_closest_point(bvc_scene s, const double* x, size_t n, int filter, double* point, double* dist, int* seg,
+                            double* t) {
+    API({
+        require_device();
+        need(s && x, "null argument");
+        if (n == 0) return BVC_OK;
+        unsigned mask = filter == BVC_FILTER_DIRICHLET ? 1u : filter == BVC_FILTER_NEUMANN ? 2u : 3u;
+        double* xd = ws().get<double>(kWsEvalIn, 2 * n);
+        double* o = ws().get<double>(kWsEvalOut, 4 * n);
+        int* sg = ws().get<int>(kWsSkipB, n);
+        CK(cudaMemcpyAsync(xd, x, 2 * n * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        launch_closest(s->view(), xd, static_cast<int>(n), mask, o, o + 2 * n, sg, o + 3 * n, g_stream);
+        CK(cudaMemcpyAsync(point, o, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaMemcpyAsync(dist, o + 2 * n, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaMemcpyAsync(seg, sg, n * sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaMemcpyAsync(t, o + 3 * n, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+    })
+}
+int bvc_scene_silhouette_distance(bvc_scene s, const double* x, size_t n, double* dist) {
+    API({
+        require_device();
+        need(s && x, "null argument");
+        if (n == 0) return BVC_OK;
+        double* xd = ws().get<double>(kWsEvalIn, 2 * n);
+        double* o = ws().get<double>(kWsEvalOut, n);
+        CK(cudaMemcpyAsync(xd, x, 2 * n * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        launch_silhouette(s->view(), xd, static_cast<int>(n), o, g_stream);
+        CK(cudaMemcpyAsync(dist, o, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+    })
+}
+int bvc_scene_intersect_ray(bvc_scene s, const double* o, const double* d, size_t n, double tMax, int filter,
+                            double tMin, double* t, int* seg, double* point, double* sp) {
+    API({
+        require_device();
+        need(s && o && d, "null argument");
+        if (n == 0) return BVC_OK;
+        unsigned mask = filter == BVC_FILTER_DIRICHLET ? 1u : filter == BVC_FILTER_NEUMANN ? 2u : 3u;
+        double* in = ws().get<double>(kWsEvalIn, 4 * n);
+        double* out = ws().get<double>(kWsEvalOut, 4 * n);
+        int* sg = ws().get<int>(kWsSkipB, n);
+        CK(cudaMemcpyAsync(in, o, 2 * n * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        CK(cudaMemcpyAsync(in + 2 * n, d, 2 * n * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        launch_ray(s->view(), in, in + 2 * n, static_cast<int>(n), tMax, mask, tMin, out, sg, out + n, out + 3 * n, g_stream);
+        CK(cudaMemcpyAsync(t, out, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaMemcpyAsync(seg, sg, n * sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaMemcpyAsync(point, out + n, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaMemcpyAsync(sp, out + 3 * n, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+    })
+}
+int bvc_scene_inside(bvc_scene s, const double* x, size_t n, uint8_t* inside) {
+    API({
+        require_device();
+        need(s && x, "null argument");
+        if (n == 0) return BVC_OK;
+        double* xd = ws().get<double>(kWsEvalIn, 2 * n);
+        uint8_t* o = ws().get<uint8_t>(kWsOutside, n);
+        CK(cudaMemcpyAsync(xd, x, 2 * n * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        launch_inside(s->view(), xd, static_cast<int>(n), static_cast<float>(1e-7 * s->host.diagonal), o, g_stream);
+        CK(cudaMemcpyAsync(inside, o, n, cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+    })
+}
+
+int bvc_region_build(bvc_scene s, const bvc_region_request* req, double eps, bvc_region* out) {
+    API({
+        need(s && req && out, "null argument");
+        auto r = std::make_unique<bvc_region_s>();
+        r->host = bvc_host::buildSolveRegion(s->host, req->mode, req->offset, req->subdomain ? &req->subdomain->host : nullptr,
+                                             eps);
+        r->boundary.host = r->host.boundary;
+        *out = r.release();
+    })
+}
+int bvc_region_destroy(bvc_region r) { API(delete r) }
+int bvc_region_info(bvc_region r, int* nv, int* ns, double* offset, double* area, int* whole) {
+    API({
+        need(r, "null region");
+        if (nv) *nv = r->host.boundary.nv;
+        if (ns) *ns = r->host.boundary.ns;
+        if (offset) *offset = r->host.offset;
+        if (area) *area = r->host.area;
+        if (whole) *whole = r->host.wholeDomain ? 1 : 0;
+    })
+}
+int bvc_region_export(bvc_region r, double* v, int* segs, int* labels, int* kinds, int* src) {
+    API({
+        need(r, "null region");
+        const auto& b = r->host.boundary;
+        if (v) std::copy(b.v.begin(), b.v.end(), v);
+        if (segs) std::copy(b.idx.begin(), b.idx.end(), segs);
+        if (labels) std::copy(b.label.begin(), b.label.end(), labels);
+        if (kinds) std::copy(r->host.kinds.begin(), r->host.kinds.end(), kinds);
+        if (src) std::copy(r->host.source.begin(), r->host.source.end(), src);
+    })
+}
+bvc_scene bvc_region_boundary(bvc_region r) { return r ? &r->boundary : nullptr; }
+
+int bvc_points_create(const double* x, size_t n, int dim, bvc_eval_points* out) {
+    API({
+        require_device();
+        need(out && (x || n == 0), "null argument");
+        need(dim == 2 || dim == 3, "points must be 2D or 3D");
+        auto P = std::make_unique<bvc_eval_points_s>();
+        P->n = n;
+        P->dim = dim;
+        P->hx.assign(x, x + dim * n);
+        alloc_points(P.get());
+        P->x.upload(P->hx.data(), dim * n);
+        zero_points(P.get());
+        *out = P.release();
+    })
+}
+int bvc_points_destroy(bvc_eval_points p) { API(delete p) }
+int bvc_points_reset(bvc_eval_points p) {
+    API({
+        require_device();
+        need(p, "null points");
+        uint8_t* keepF = nullptr;
+        (void)keepF;
+        // keep the classification, zero the running sums
+        p->bsum.zero(); p->ssum.zero(); p->bgsum.zero(); p->sgsum.zero(); p->walkSum.zero(); p->gwalkSum.zero();
+        p->nb.zero(); p->ms.zero(); p->nbg.zero(); p->msg.zero(); p->walkCount.zero(); p->walkTrunc.zero();
+        p->gwalkCount.zero(); p->skipped.zero();
+    })
+}
+int bvc_points_download(bvc_eval_points p, bvc_point_state* h) {
+    API({
+        require_device();
+        need(p && h, "null argument");
+        size_t n = p->n;
+        int d = p->dim;
+        h->count = n;
+        h->dim = d;
+        if (h->x) std::copy(p->hx.begin(), p->hx.end(), h->x);
+        if (h->fallback) p->fallback.download(h->fallback, n);
+        if (h->gradientUnreliable) p->unreliable.download(h->gradientUnreliable, n);
+        if (h->boundarySum) p->bsum.download(h->boundarySum, n);
+        if (h->sourceSum) p->ssum.download(h->sourceSum, n);
+        if (h->nBoundary) p->nb.download(h->nBoundary, n);
+        if (h->mSource) p->ms.download(h->mSource, n);
+        if (h->boundaryGradSum) p->bgsum.download(h->boundaryGradSum, d * n);
+        if (h->sourceGradSum) p->sgsum.download(h->sourceGradSum, d * n);
+        if (h->nBoundaryGrad) p->nbg.download(h->nBoundaryGrad, n);
+        if (h->mSourceGrad) p->msg.download(h->mSourceGrad, n);
+        if (h->walkSum) p->walkSum.download(h->walkSum, n);
+        if (h->walkCount) p->walkCount.download(h->walkCount, n);
+        if (h->walkTruncated) p->walkTrunc.download(h->walkTruncated, n);
+        if (h->gradientWalkSum) p->gwalkSum.download(h->gradientWalkSum, d * n);
+        if (h->gradientWalkCount) p->gwalkCount.download(h->gradientWalkCount, n);
+        if (h->skipped) p->skipped.download(h->skipped, n);
+        CK(cudaStreamSynchronize(g_stream));
+    })
+}
+int bvc_points_upload(bvc_eval_points p, const bvc_point_state* h) {
+    API({
+        require_device();
+        need(p && h, "null argument");
+        size_t n = p->n;
+        int d = p->dim;
+        need(h->count == n, "point count mismatch");
+        if (h->fallback) { p->fallback.upload(h->fallback, n); p->orderValid = false; }
+        if (h->gradientUnreliable) p->unreliable.upload(h->gradientUnreliable, n);
+        if (h->boundarySum) p->bsum.upload(h->boundarySum, n);
+        if (h->sourceSum) p->ssum.upload(h->sourceSum, n);
+        if (h->nBoundary) p->nb.upload(h->nBoundary, n);
+        if (h->mSource) p->ms.upload(h->mSource, n);
+        if (h->boundaryGradSum) p->bgsum.upload(h->boundaryGradSum, d * n);
+        if (h->sourceGradSum) p->sgsum.upload(h->sourceGradSum, d * n);
+        if (h->nBoundaryGrad) p->nbg.upload(h->nBoundaryGrad, n);
+        if (h->mSourceGrad) p->msg.upload(h->mSourceGrad, n);
+        if (h->walkSum) p->walkSum.upload(h->walkSum, n);
+        if (h->walkCount) p->walkCount.upload(h->walkCount, n);
+        if (h->walkTruncated) p->walkTrunc.upload(h->walkTruncated, n);
+        if (h->gradientWalkSum) p->gwalkSum.upload(h->gradientWalkSum, d * n);
+        if (h->gradientWalkCount) p->gwalkCount.upload(h->gradientWalkCount, n);
+        if (h->skipped) p->skipped.upload(h->skipped, n);
+        CK(cudaStreamSynchronize(g_stream));
+    })
+}
+int bvc_mark_evaluation_points(bvc_scene s, bvc_region r, const bvc_cache_config* cfg, bvc_eval_points p) {
+    API({
+        require_device();
+        need(s && r && cfg && p, "null argument");
+        need(p->dim == 2, "markEvaluationPoints: 2D points");
+        if (cfg->sourceBall) throw Error(BVC_ERR_INVALID_ARGUMENT, "ball-kernel mode is not implemented (SURVEY §8f.3)");
+        r->upload();
+        int n = static_cast<int>(p->n);
+        if (n)
+            mark_kernel<<<(n + 127) / 128, 128, 0, g_stream>>>(s->view(), r->boundary.view(), p->x.p, n,
+                                                               static_cast<float>(r->host.offset), r->host.wholeDomain ? 1 : 0,
+                                                               p->fallback.p, p->unreliable.p);
+        count_launch();
+        p->orderValid = false;
+        CK(cudaGetLastError());
+    })
+}
+
+int bvc_generate_boundary_cache_shard(bvc_scene s, const bvc_problem* pb, bvc_region r, const bvc_cache_config* cfg,
+                                      uint64_t seed, uint64_t round, int begin, int end, bvc_round_stats* stats,
+                                      bvc_boundary_cache* out) {
+    API({
+        need(s && pb && r && cfg && out, "null argument");
+        auto c = std::make_unique<bvc_boundary_cache_s>();
+        GenStats st;
+        generate_cache(s, *pb, r, *cfg, seed, round, begin, end, c.get(), st);
+        if (stats) {
+            stats->resampled += st.resampled;
+            stats->cacheWalks += st.walks;
+            stats->cacheTruncated += st.truncated;
+            stats->cacheSteps += st.steps;
+        }
+        *out = c.release();
+    })
+}
+int bvc_generate_boundary_cache(bvc_scene s, const bvc_problem* pb, bvc_region r, const bvc_cache_config* cfg,
+                                uint64_t seed, uint64_t round, bvc_round_stats* stats, bvc_boundary_cache* out) {
+    return bvc_generate_boundary_cache_shard(s, pb, r, cfg, seed, round, 0, std::max(1, cfg ? cfg->nBoundary : 1), stats,
+                                             out);
+}
+int bvc_generate_source_cache(const bvc_problem* pb, bvc_region r, const bvc_cache_config* cfg, uint64_t seed,
+                              uint64_t round, bvc_source_cache* out) {
+    API({
+        need(pb && r && cfg && out, "null argument");
+        auto c = std::make_unique<bvc_source_cache_s>();
+        generate_source(*pb, r, *cfg, seed, round, c.get());
+        *out = c.release();
+    })
+}
+int bvc_boundary_cache_create(const bvc_boundary_sample* smp, int n, int dim, int voronoi, double length,
+                              bvc_boundary_cache* out) {
+    API({
+        require_device();
+        need(out && (smp || n == 0) && n >= 0, "null argument");
+        need(dim == 2 || dim == 3, "cache dimension must be 2 or 3");
+        auto c = std::make_unique<bvc_boundary_cache_s>();
+        c->n = n;
+        c->dim = dim;
+        c->voronoi = voronoi;
+        c->length = length;
+        std::vector<CacheSample> h(std::max(n, 1));
+        for (int i = 0; i < n; ++i) {
+            CacheSample& o = h[i];
+            for (int k = 0; k < 3; ++k) {
+                o.z[k] = static_cast<float>(smp[i].z[k]);
+                o.n[k] = static_cast<float>(smp[i].n[k]);
+            }
+            if (dim == 2) o.z[2] = o.n[2] = 0.f;
+            o.pdf = static_cast<float>(smp[i].pdf);
+            o.uHat = static_cast<float>(smp[i].uHat);
+            o.dHat = static_cast<float>(smp[i].dHat);
+            o.weight = static_cast<float>(smp[i].weight);
+            o.arc = static_cast<float>(smp[i].arc);
+            o.segment = smp[i].segment;
+        }
+        c->samples.upload(h.data(), std::max(n, 1));
+        *out = c.release();
+    })
+}
+int bvc_boundary_cache_size(bvc_boundary_cache c, int* n, int* dim) {
+    API({
+        need(c, "null cache");
+        if (n) *n = c->n;
+        if (dim) *dim = c->dim;
+    })
+}
+int bvc_boundary_cache_download(bvc_boundary_cache c, bvc_boundary_sample* smp) {
+    API({
+        require_device();
+        need(c && smp, "null argument");
+        std::vector<CacheSample> h(c->n);
+        c->samples.download(h.data(), c->n);
+        CK(cudaStreamSynchronize(g_stream));
+        for (int i = 0; i < c->n; ++i) {
+            bvc_boundary_sample& o = smp[i];
+            for (int k = 0; k < 3; ++k) {
+                o.z[k] = h[i].z[k];
+                o.n[k] = h[i].n[k];
+            }
+            o.pdf = h[i].pdf;
+            o.uHat = h[i].uHat;
+            o.dHat = h[i].dHat;
+            o.weight = h[i].weight;
+            o.segment = h[i].segment;
+            o.arc = h[i].arc;
+        }
+    })
+}
+int bvc_boundary_cache_packed(bvc_boundary_cache c, void** ptr, size_t* bytes) {
+    API({
+        need(c && ptr && bytes, "null argument");
+        *ptr = c->samples.p;
+        *bytes = static_cast<size_t>(c->n) * sizeof(CacheSample);
+    })
+}
+int bvc_boundary_cache_from_packed(const void* ptr, int n, int dim, int voronoi, double length, bvc_boundary_cache* out) {
+    API({
+        require_device();
+        need(out && (ptr || n == 0), "null argument");
+        auto c = std::make_unique<bvc_boundary_cache_s>();
+        c->n = n;
+        c->dim = dim;
+        c->voronoi = voronoi;
+        c->length = length;
+        c->samples.resize(std::max(n, 1));
+        if (n) CK(cudaMemcpyAsync(c->samples.p, ptr, n * sizeof(CacheSample), cudaMemcpyDeviceToDevice, g_stream));
+        *out = c.release();
+    })
+}
+int bvc_boundary_cache_destroy(bvc_boundary_cache c) { API(delete c) }
+int bvc_source_cache_create(const bvc_source_sample* smp, int m, int dim, double area, bvc_source_cache* out) {
+    API({
+        require_device();
+        need(out && (smp || m == 0) && m >= 0, "null argument");
+        auto c = std::make_unique<bvc_source_cache_s>();
+        c->m = m;
+        c->dim = dim;
+        c->area = area;
+        std::vector<SourceSampleDev> h(std::max(m, 1));
+        for (int i = 0; i < m; ++i) {
+            for (int k = 0; k < 3; ++k) h[i].y[k] = static_cast<float>(smp[i].y[k]);
+            if (dim == 2) h[i].y[2] = 0.f;
+            h[i].pdf = static_cast<float>(smp[i].pdf);
+            h[i].f = static_cast<float>(smp[i].f);
+        }
+        c->samples.upload(h.data(), std::max(m, 1));
+        *out = c.release();
+    })
+}
+int bvc_source_cache_size(bvc_source_cache c, int* m, int* dim) {
+    API({
+        need(c, "null cache");
+        if (m) *m = c->m;
+        if (dim) *dim = c->dim;
+    })
+}
+int bvc_source_cache_download(bvc_source_cache c, bvc_source_sample* smp) {
+    API({
+        require_device();
+        need(c && smp, "null argument");
+        std::vector<SourceSampleDev> h(std::max(c->m, 1));
+        c->samples.download(h.data(), c->m);
+        CK(cudaStreamSynchronize(g_stream));
+        for (int i = 0; i < c->m; ++i) {
+            for (int k = 0; k < 3; ++k) smp[i].y[k] = h[i].y[k];
+            smp[i].pdf = h[i].pdf;
+            smp[i].f = h[i].f;
+        }
+    })
+}
+int bvc_source_cache_destroy(bvc_source_cache c) { API(delete c) }
+
+int bvc_make_splat_config(bvc_scene s, const bvc_problem* pb, const bvc_cache_config* cfg, bvc_splat_config* out) {
+    API({
+        need(s && pb && cfg && out, "null argument");
+        *out = make_splat_config(s, *pb, *cfg);
+    })
+}
+int bvc_splat_solution(bvc_boundary_cache b, bvc_source_cache s, bvc_eval_points p, const bvc_splat_config* cfg) {
+    API(need(cfg, "null config"); splat(b, s, p, *cfg, 0, SIZE_MAX, true, false))
+}
+int bvc_splat_gradient(bvc_boundary_cache b, bvc_source_cache s, bvc_eval_points p, const bvc_splat_config* cfg) {
+    API(need(cfg, "null config"); splat(b, s, p, *cfg, 0, SIZE_MAX, false, true))
+}
+int bvc_splat_solution_gradient(bvc_boundary_cache b, bvc_source_cache s, bvc_eval_points p, const bvc_splat_config* cfg) {
+    API(need(cfg, "null config"); splat(b, s, p, *cfg, 0, SIZE_MAX, true, true))
+}
+int bvc_splat_range(bvc_boundary_cache b, bvc_source_cache s, bvc_eval_points p, const bvc_splat_config* cfg,
+                    size_t begin, size_t end, int value, int gradient) {
+    API(need(cfg, "null config"); splat(b, s, p, *cfg, begin, end, value != 0, gradient != 0))
+}
+
+int bvc_update_solution(bvc_scene s, const bvc_problem* pb, bvc_region r, const bvc_cache_config* cfg,
+                        bvc_eval_points p, uint64_t seed, uint64_t round, int gradients, bvc_round_stats* stats) {
+    API({
+        require_device();
+        need(s && pb && r && cfg && p, "null argument");
+        validate_kernel(pb->kernel);
+        if (cfg->sourceBall && gradients)
+            throw Error(BVC_ERR_SOLVER, "ball-kernel source mode does not support gradient splats");
+        bvc_splat_config scfg = make_splat_config(s, *pb, *cfg);
+        cudaEvent_t e0, e1, e2;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventCreate(&e2));
+        CK(cudaEventRecord(e0, g_stream));
+        bvc_boundary_cache_s bc;
+        bvc_source_cache_s sc;
+        GenStats st;
+        generate_cache(s, *pb, r, *cfg, seed, round, 0, std::max(1, cfg->nBoundary), &bc, st);
+        generate_source(*pb, r, *cfg, seed, round, &sc);
+        CK(cudaEventRecord(e1, g_stream));
+        splat(&bc, sc.m ? &sc : nullptr, p, scfg, 0, SIZE_MAX, true, gradients != 0);
+        fallback_walks(s, *pb, *cfg, p, seed, round, gradients != 0);
+        CK(cudaEventRecord(e2, g_stream));
+        CK(cudaEventSynchronize(e2));
+        if (stats) {
+            stats->resampled = st.resampled;
+            stats->cacheWalks = st.walks;
+            stats->cacheTruncated = st.truncated;
+            stats->cacheSteps = st.steps;
+            stats->generateSeconds = device_seconds(e0, e1);
+            stats->splatSeconds = device_seconds(e1, e2);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaEventDestroy(e2);
+    })
+}
+
+int bvc_wos_solve(bvc_scene s, const bvc_problem* pb, const double* x, size_t n, const bvc_walk_config* cfg,
+                  const uint64_t* streams, bvc_scalar_estimate* out) {
+    API({
+        need(s && pb && cfg && out, "null argument");
+        if (s->host.hasNeumann()) throw Error(BVC_ERR_SOLVER, "wosSolve requires an all-Dirichlet scene");
+        std::vector<double> m(n), se(n);
+        std::vector<long long> c(n), t(n);
+        pointwise(s, *pb, x, nullptr, n, *cfg, streams, 0, m.data(), se.data(), c.data(), t.data());
+        for (size_t i = 0; i < n; ++i) out[i] = bvc_scalar_estimate{m[i], se[i], c[i], t[i]};
+    })
+}
+int bvc_wost_solve(bvc_scene s, const bvc_problem* pb, const double* x, size_t n, const bvc_walk_config* cfg,
+                   const uint64_t* streams, bvc_scalar_estimate* out) {
+    API({
+        need(s && pb && cfg && out, "null argument");
+        std::vector<double> m(n), se(n);
+        std::vector<long long> c(n), t(n);
+        pointwise(s, *pb, x, nullptr, n, *cfg, streams, 0, m.data(), se.data(), c.data(), t.data());
+        for (size_t i = 0; i < n; ++i) out[i] = bvc_scalar_estimate{m[i], se[i], c[i], t[i]};
+    })
+}
+int bvc_wost_gradient(bvc_scene s, const bvc_problem* pb, const double* x, size_t n, const bvc_walk_config* cfg,
+                      const uint64_t* streams, bvc_vector_estimate* out) {
+    API({
+        need(s && pb && cfg && out, "null argument");
+        std::vector<double> m(2 * n), se(2 * n);
+        std::vector<long long> c(n), t(n);
+        pointwise(s, *pb, x, nullptr, n, *cfg, streams, 1, m.data(), se.data(), c.data(), t.data());
+        for (size_t i = 0; i < n; ++i) {
+            out[i].mean[0] = m[2 * i];
+            out[i].mean[1] = m[2 * i + 1];
+            out[i].se[0] = se[2 * i];
+            out[i].se[1] = se[2 * i + 1];
+            out[i].count = c[i];
+            out[i].truncated = t[i];
+        }
+    })
+}
+int bvc_wost_normal_derivative(bvc_scene s, const bvc_problem* pb, const double* x, const double* normal, size_t n,
+                               const bvc_walk_config* cfg, const uint64_t* streams, bvc_scalar_estimate* out) {
+    API({
+        need(s && pb && cfg && out && normal, "null argument");
+        std::vector<double> m(n), se(n);
+        std::vector<long long> c(n), t(n);
+        pointwise(s, *pb, x, normal, n, *cfg, streams, 2, m.data(), se.data(), c.data(), t.data());
+        for (size_t i = 0; i < n; ++i) out[i] = bvc_scalar_estimate{m[i], se[i], c[i], t[i]};
+    })
+}
+
+int bvc_eval_kernels(const bvc_kernel_spec* spec, const double* x, const double* y, const double* n, size_t count,
+                     double* out) {
+    API({
+        require_device();
+        need(spec && x && y && n && out, "null argument");
+        validate_kernel(*spec);
+        if (count == 0) return BVC_OK;
+        int d = spec->dim;
+        double* in = ws().get<double>(kWsEvalIn, 3 * d * count);
+        double* o = ws().get<double>(kWsEvalOut, (2 + 2 * d) * count);
+        CK(cudaMemcpyAsync(in, x, d * count * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        CK(cudaMemcpyAsync(in + d * count, y, d * count * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        CK(cudaMemcpyAsync(in + 2 * d * count, n, d * count * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        eval_kernels(gather_kind(*spec), in, in + d * count, in + 2 * d * count, static_cast<int>(count), d,
+                     static_cast<float>(spec->sigma), o, g_stream);
+        CK(cudaMemcpyAsync(out, o, (2 + 2 * d) * count * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+    })
+}
+int bvc_eval_bessel(int which, const double* t, size_t count, double* out) {
+    API({
+        require_device();
+        need(t && out && which >= 0 && which <= 3, "bad argument");
+        if (count == 0) return BVC_OK;
+        double* in = ws().get<double>(kWsEvalIn, count);
+        double* o = ws().get<double>(kWsEvalOut, count);
+        CK(cudaMemcpyAsync(in, t, count * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        eval_bessel(which, in, static_cast<int>(count), o, g_stream);
+        CK(cudaMemcpyAsync(out, o, count * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+    })
+}
+
+}  // extern "C"

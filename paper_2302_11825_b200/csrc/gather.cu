@@ -1,0 +1,582 @@
+// gather.cu — the dense interior evaluation (boundary-integral splats) on sm_100a.
+//
+// Reference: splatSolution cache.cpp:426-461 and splatGradient cache.cpp:463-497
+// over the kernels of kernels.h:78-129 (reference sign convention).
+//
+// N-body style FP32 gather. Per-sample constants are folded once (pack_*):
+//   2D Laplace boundary: A = w u/2pi, B = w d ln2/4pi, Bg = w d/2pi  (w = 1/pdf or
+//   Voronoi weight*N), so a pair costs dx,dy,r2,nd, rcp, lg2 and a few FMAs.
+// Each CTA owns PT query points (Q per thread, register-blocked) and streams a
+// chunk of the cache through shared memory in tiles of TS samples; tiles arrive
+// by 1D TMA bulk copies (cp.async.bulk + mbarrier, double-buffered) and are read
+// as warp-wide broadcasts. Tile partials are FP32; tiles and chunks accumulate in
+// FP64 in a fixed order, so sums are deterministic and independent of the grid
+// and of how points are sharded across GPUs. Near-coincident pairs
+// (r < 1e-12 diag, cache.cpp:436-440) are rare: the hot loop only tracks min r^2
+// and a slow path redoes a tile for a point that hit one.
+#include <cuda_runtime.h>
+
+#include "gather.h"
+
+namespace bvc_impl {
+
+using namespace bvc_dev;
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kQ = 4;
+constexpr int kPT = kThreads * kQ;  // points per CTA tile
+constexpr int kTS = 256;            // samples per shared-memory tile
+
+// --- TMA bulk copy + mbarrier helpers ----------------------------------------
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
+// --- per-pair kernels ---------------------------------------------------------
+// 2D: payload a = (zx, zy, nx, ny), b = per-kind constants
+struct Acc {
+    float v, gx, gy, gz;
+};
+
+// Bessel pieces for screened 2D: K0(t) and Q = t K1(t)
+__device__ __forceinline__ void k0_q(float t, float& K0, float& Q) {
+    if (t <= 2.0f) {
+        float h = 0.5f * t, y = h * h;
+        float lnh = f_lg2(h) * kLn2;
+        float w = t * t * (1.0f / 14.0625f);
+        float i0 = 1.0f + w * (3.5156229f + w * (3.0899424f + w * (1.2067492f + w * (0.2659732f + w * (0.0360768f + w * 0.0045813f)))));
+        float i1 = t * (0.5f + w * (0.87890594f + w * (0.51498869f + w * (0.15084934f + w * (0.02658733f + w * (0.00301532f + w * 0.00032411f))))));
+        float p0 = -0.57721566f + y * (0.42278420f + y * (0.23069756f + y * (0.03488590f + y * (0.00262698f + y * (0.00010750f + y * 0.0000074f)))));
+        float p1 = 1.0f + y * (0.15443144f + y * (-0.67278579f + y * (-0.18156897f + y * (-0.01919402f + y * (-0.00110404f - y * 0.00004686f)))));
+        K0 = fmaf(-lnh, i0, p0);
+        Q = fmaf(t * lnh, i1, p1);
+    } else {
+        float rt = f_rsq(t);
+        float e = f_ex2(-1.44269504088896340736f * t);
+        float y = 2.0f * rt * rt;
+        float p0 = 1.25331414f + y * (-0.07832358f + y * (0.02189568f + y * (-0.01062446f + y * (0.00587872f + y * (-0.00251540f + y * 0.00053208f)))));
+        float p1 = 1.25331414f + y * (0.23498619f + y * (-0.03655620f + y * (0.01504268f + y * (-0.00780353f + y * (0.00325614f - y * 0.00068245f)))));
+        float er = e * rt;
+        K0 = p0 * er;
+        Q = p1 * er * t;
+    }
+}
+
+template <int KIND, bool SRC, bool VAL, bool GRAD>
+__device__ __forceinline__ void pair(const float4 a, const float4 b, float px, float py, float pz, float sigma,
+                                     float s, Acc& acc, float& mn) {
+    if constexpr (KIND == kLap2 || KIND == kScr2) {
+        float dx = a.x - px, dy = a.y - py;
+        float r2 = fmaf(dx, dx, dy * dy);
+        mn = fminf(mn, r2);
+        if constexpr (KIND == kLap2) {
+            float ir2 = f_rcp(r2);
+            if constexpr (!SRC) {
+                float nd = fmaf(a.z, dx, a.w * dy);
+                float p = nd * ir2;
+                if constexpr (VAL) acc.v = fmaf(b.x, p, fmaf(-b.y, f_lg2(r2), acc.v));
+                if constexpr (GRAD) {
+                    float q = fmaf(b.w, p, b.z) * ir2;  // (2A p + Bg) / r^2
+                    float c = b.x * ir2;                // A / r^2
+                    acc.gx = fmaf(q, dx, fmaf(-c, a.z, acc.gx));
+                    acc.gy = fmaf(q, dy, fmaf(-c, a.w, acc.gy));
+                }
+            } else {
+                if constexpr (VAL) acc.v = fmaf(b.x, f_lg2(r2), acc.v);
+                if constexpr (GRAD) {
+                    float c = b.y * ir2;
+                    acc.gx = fmaf(-c, dx, acc.gx);
+                    acc.gy = fmaf(-c, dy, acc.gy);
+                }
+            }
+        } else {
+            float ir = f_rsq(r2);
+            float ir2 = ir * ir;
+            float t = s * (r2 * ir);
+            float K0, Q;
+            k0_q(t, K0, Q);
+            if constexpr (!SRC) {
+                float nd = fmaf(a.z, dx, a.w * dy);
+                float p = nd * ir2;
+                if constexpr (VAL) acc.v = fmaf(b.x * Q, p, fmaf(b.y, K0, acc.v));
+                if constexpr (GRAD) {
+                    float aq = b.x * Q;
+                    // d (A (2 Q p ir2 + sigma K0 p) + Bk Q ir2) - n (A Q ir2)
+                    float q = fmaf(aq + aq, p * ir2, fmaf(b.x * sigma, K0 * p, b.y * Q * ir2));
+                    float c = aq * ir2;
+                    acc.gx = fmaf(q, dx, fmaf(-c, a.z, acc.gx));
+                    acc.gy = fmaf(q, dy, fmaf(-c, a.w, acc.gy));
+                }
+            } else {
+                if constexpr (VAL) acc.v = fmaf(-b.x, K0, acc.v);
+                if constexpr (GRAD) {
+                    float c = b.x * Q * ir2;
+                    acc.gx = fmaf(-c, dx, acc.gx);
+                    acc.gy = fmaf(-c, dy, acc.gy);
+                }
+            }
+        }
+    } else {
+        // 3D: boundary payload a = (zx, zy, zz, nx), b = (ny, nz, A, B); source a = (y, C)
+        float dx = a.x - px, dy = a.y - py, dz = a.z - pz;
+        float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        mn = fminf(mn, r2);
+        float ir = f_rsq(r2);
+        float ir2 = ir * ir, ir3 = ir2 * ir;
+        float e = 1.0f, Q = 1.0f;
+        if constexpr (KIND == kScr3) {
+            float t = s * (r2 * ir);
+            e = f_ex2(-1.44269504088896340736f * t);
+            Q = e * (t + 1.0f);
+        }
+        if constexpr (!SRC) {
+            float nd = fmaf(a.w, dx, fmaf(b.x, dy, b.y * dz));
+            float pn = nd * ir3;
+            if constexpr (VAL) {
+                if constexpr (KIND == kScr3) acc.v = fmaf(b.z * Q, pn, fmaf(b.w * e, ir, acc.v));
+                else acc.v = fmaf(b.z, pn, fmaf(b.w, ir, acc.v));
+            }
+            if constexpr (GRAD) {
+                float aq = b.z * Q;
+                float q = fmaf(3.0f * aq, pn * ir2, b.w * Q * ir3);
+                if constexpr (KIND == kScr3) q = fmaf(b.z * sigma * e, pn, q);
+                float c = aq * ir3;
+                acc.gx = fmaf(q, dx, fmaf(-c, a.w, acc.gx));
+                acc.gy = fmaf(q, dy, fmaf(-c, b.x, acc.gy));
+                acc.gz = fmaf(q, dz, fmaf(-c, b.y, acc.gz));
+            }
+        } else {
+            if constexpr (VAL) acc.v = fmaf(-a.w * e, ir, acc.v);
+            if constexpr (GRAD) {
+                float c = a.w * Q * ir3;
+                acc.gx = fmaf(-c, dx, acc.gx);
+                acc.gy = fmaf(-c, dy, acc.gy);
+                acc.gz = fmaf(-c, dz, acc.gz);
+            }
+        }
+    }
+}
+
+struct Params {
+    const float4* pack;      // 2 float4 per sample; boundary samples [0, N), source [N, N+M)
+    int N, M;
+    const float* px;         // dim * K (active points, sorted order)
+    int K, dim;
+    int chunk;               // samples per chunk (multiple of kTS)
+    int chunksB, chunksS;    // chunks over boundary / source samples
+    int tiles;               // point tiles
+    float sigma, s, tol2;
+    double* part;            // [(chunksB + chunksS)][comps][K]
+    int comps;               // 1 (value) + dim (gradient) as enabled
+    int* skipB;              // [K]
+    int* skipS;
+};
+
+// slow path: recompute one point's tile partial, skipping near-coincident samples
+template <int KIND, bool SRC, bool VAL, bool GRAD>
+__device__ void tile_slow(const float4* sm, int cnt, float px, float py, float pz, const Params& P, Acc& acc,
+                          int& skips) {
+    acc = Acc{0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < cnt; ++j) {
+        float4 a = sm[2 * j], b = sm[2 * j + 1];
+        float dx = a.x - px, dy = a.y - py, dz = (KIND == kLap3 || KIND == kScr3) ? a.z - pz : 0.0f;
+        if (dx * dx + dy * dy + dz * dz < P.tol2) { ++skips; continue; }
+        float mn = 0.f;
+        pair<KIND, SRC, VAL, GRAD>(a, b, px, py, pz, P.sigma, P.s, acc, mn);
+    }
+}
+
+template <int KIND, bool VAL, bool GRAD>
+__global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
+    __shared__ __align__(128) float4 sm[2][2 * kTS];
+    __shared__ __align__(8) uint64_t bar[2];
+    const int tid = threadIdx.x;
+    const int units = P.tiles * (P.chunksB + P.chunksS);
+    constexpr bool D3 = (KIND == kLap3 || KIND == kScr3);
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    unsigned phase[2] = {0u, 0u};
+    for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
+        const int chunkId = unit % (P.chunksB + P.chunksS);
+        const int tile = unit / (P.chunksB + P.chunksS);
+        const bool src = chunkId >= P.chunksB;
+        const int c0 = src ? P.N + (chunkId - P.chunksB) * P.chunk : chunkId * P.chunk;
+        const int cEnd = src ? min(c0 + P.chunk, P.N + P.M) : min(c0 + P.chunk, P.N);
+        const int nT = (cEnd - c0 + kTS - 1) / kTS;
+        // points
+        float px[kQ], py[kQ], pz[kQ];
+        int pidx[kQ];
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            int i = tile * kPT + q * kThreads + tid;
+            pidx[q] = i;
+            bool ok = i < P.K;
+            px[q] = ok ? P.px[P.dim * i] : 1e30f;
+            py[q] = ok ? P.px[P.dim * i + 1] : 1e30f;
+            pz[q] = (ok && D3) ? P.px[P.dim * i + 2] : 0.0f;
+        }
+        double dv[kQ], dg0[kQ], dg1[kQ], dg2[kQ];
+        int skips[kQ];
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) { dv[q] = dg0[q] = dg1[q] = dg2[q] = 0.0; skips[q] = 0; }
+        // prologue: first two tiles in flight
+        if (tid == 0) {
+#pragma unroll
+            for (int st = 0; st < 2; ++st)
+                if (st < nT) {
+                    int s0 = c0 + st * kTS, cnt = min(kTS, cEnd - s0);
+                    mbar_expect_tx(&bar[st], cnt * 32u);
+                    bulk_g2s(sm[st], P.pack + 2 * static_cast<size_t>(s0), cnt * 32u, &bar[st]);
+                }
+        }
+        for (int it = 0; it < nT; ++it) {
+            const int st = it & 1;
+            const int s0 = c0 + it * kTS, cnt = min(kTS, cEnd - s0);
+            mbar_wait(&bar[st], phase[st]);
+            phase[st] ^= 1u;
+            Acc acc[kQ];
+            float mn[kQ];
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) { acc[q] = Acc{0.f, 0.f, 0.f, 0.f}; mn[q] = 3.0e38f; }
+            const float4* S = sm[st];
+            if (!src) {
+#pragma unroll 2
+                for (int j = 0; j < cnt; ++j) {
+                    const float4 a = S[2 * j], b = S[2 * j + 1];
+#pragma unroll
+                    for (int q = 0; q < kQ; ++q) pair<KIND, false, VAL, GRAD>(a, b, px[q], py[q], pz[q], P.sigma, P.s, acc[q], mn[q]);
+                }
+            } else {
+#pragma unroll 2
+                for (int j = 0; j < cnt; ++j) {
+                    const float4 a = S[2 * j], b = S[2 * j + 1];
+#pragma unroll
+                    for (int q = 0; q < kQ; ++q) pair<KIND, true, VAL, GRAD>(a, b, px[q], py[q], pz[q], P.sigma, P.s, acc[q], mn[q]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) {
+                if (mn[q] < P.tol2 && pidx[q] < P.K) {
+                    if (!src) tile_slow<KIND, false, VAL, GRAD>(S, cnt, px[q], py[q], pz[q], P, acc[q], skips[q]);
+                    else tile_slow<KIND, true, VAL, GRAD>(S, cnt, px[q], py[q], pz[q], P, acc[q], skips[q]);
+                }
+                dv[q] += acc[q].v;
+                dg0[q] += acc[q].gx;
+                dg1[q] += acc[q].gy;
+                dg2[q] += acc[q].gz;
+            }
+            __syncthreads();  // everyone is done reading buffer st
+            if (tid == 0 && it + 2 < nT) {
+                int s2 = c0 + (it + 2) * kTS, cnt2 = min(kTS, cEnd - s2);
+                mbar_expect_tx(&bar[st], cnt2 * 32u);
+                bulk_g2s(sm[st], P.pack + 2 * static_cast<size_t>(s2), cnt2 * 32u, &bar[st]);
+            }
+        }
+        // chunk partials: fixed slot per (chunk, component, point)
+        double* out = P.part + static_cast<size_t>(chunkId) * P.comps * P.K;
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            int i = pidx[q];
+            if (i >= P.K) continue;
+            int c = 0;
+            if (VAL) out[static_cast<size_t>(c++) * P.K + i] = dv[q];
+            if (GRAD) {
+                out[static_cast<size_t>(c++) * P.K + i] = dg0[q];
+                out[static_cast<size_t>(c++) * P.K + i] = dg1[q];
+                if (D3) out[static_cast<size_t>(c++) * P.K + i] = dg2[q];
+            }
+            if (skips[q]) atomicAdd(src ? P.skipS + i : P.skipB + i, skips[q]);
+        }
+    }
+}
+
+// fold per-sample constants (the "pack-cache epilogue")
+__device__ __forceinline__ void pack_boundary_one(const CacheSample& s, int n, int kind, int voronoi, float4* out,
+                                                  int i) {
+    double w = voronoi ? static_cast<double>(s.weight) * n : 1.0 / static_cast<double>(s.pdf);
+    double u = s.uHat, d = s.dHat;
+    const double inv2pi = 0.15915494309189533577, inv4pi = 0.07957747154594766788, ln2 = 0.69314718055994530942;
+    float4 a, b;
+    if (kind == kLap2) {
+        a = make_float4(s.z[0], s.z[1], s.n[0], s.n[1]);
+        double A = w * u * inv2pi;
+        b = make_float4(static_cast<float>(A), static_cast<float>(w * d * ln2 * 0.5 * inv2pi),
+                        static_cast<float>(w * d * inv2pi), static_cast<float>(2.0 * A));
+    } else if (kind == kScr2) {
+        a = make_float4(s.z[0], s.z[1], s.n[0], s.n[1]);
+        b = make_float4(static_cast<float>(w * u * inv2pi), static_cast<float>(w * d * inv2pi), 0.f, 0.f);
+    } else {
+        a = make_float4(s.z[0], s.z[1], s.z[2], s.n[0]);
+        b = make_float4(s.n[1], s.n[2], static_cast<float>(w * u * inv4pi), static_cast<float>(w * d * inv4pi));
+    }
+    out[2 * i] = a;
+    out[2 * i + 1] = b;
+}
+__global__ void pack_boundary_kernel(const CacheSample* cs, int n, int kind, int voronoi, float4* out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    pack_boundary_one(cs[i], n, kind, voronoi, out, i);
+}
+
+__device__ __forceinline__ void pack_source_one(const SourceSampleDev& s, int kind, float4* out, int i) {
+    double c = static_cast<double>(s.f) / static_cast<double>(s.pdf);
+    const double inv2pi = 0.15915494309189533577, inv4pi = 0.07957747154594766788, ln2 = 0.69314718055994530942;
+    float4 a, b = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (kind == kLap2) {
+        a = make_float4(s.y[0], s.y[1], 0.f, 0.f);
+        b = make_float4(static_cast<float>(c * ln2 * 0.5 * inv2pi), static_cast<float>(c * inv2pi), 0.f, 0.f);
+    } else if (kind == kScr2) {
+        a = make_float4(s.y[0], s.y[1], 0.f, 0.f);
+        b = make_float4(static_cast<float>(c * inv2pi), 0.f, 0.f, 0.f);
+    } else {
+        a = make_float4(s.y[0], s.y[1], s.y[2], static_cast<float>(c * inv4pi));
+    }
+    out[2 * i] = a;
+    out[2 * i + 1] = b;
+}
+__global__ void pack_source_kernel(const SourceSampleDev* ss, int m, int kind, float4* out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    pack_source_one(ss[i], kind, out, i);
+}
+
+// G, dG/dx, dG/dn_y, d2G/dx dn_y through the hot loop's own pair() code with
+// unit payloads (u = 1, d = 0, w = 1 for the double layer; f/pdf = 1 for G)
+template <int KIND>
+__global__ void eval_kernels_kernel(const double* x, const double* y, const double* n, int count, int dim,
+                                    float sigma, double* out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    float px = x[dim * i], py = x[dim * i + 1], pz = dim == 3 ? x[dim * i + 2] : 0.f;
+    CacheSample cs{};
+    SourceSampleDev ss{};
+    for (int k = 0; k < dim; ++k) {
+        cs.z[k] = y[dim * i + k];
+        cs.n[k] = n[dim * i + k];
+        ss.y[k] = y[dim * i + k];
+    }
+    cs.pdf = 1.f; cs.uHat = 1.f; cs.dHat = 0.f;
+    ss.pdf = 1.f; ss.f = 1.f;
+    float4 pb[2], ps[2];
+    pack_boundary_one(cs, 1, KIND, 0, pb, 0);
+    pack_source_one(ss, KIND, ps, 0);
+    Acc ab{0.f, 0.f, 0.f, 0.f}, as{0.f, 0.f, 0.f, 0.f};
+    float mn = 0.f, s = sqrtf(sigma);
+    pair<KIND, false, true, true>(pb[0], pb[1], px, py, pz, sigma, s, ab, mn);
+    pair<KIND, true, true, true>(ps[0], ps[1], px, py, pz, sigma, s, as, mn);
+    double* o = out + (2 + 2 * dim) * i;
+    o[0] = as.v;
+    o[1] = as.gx; o[2] = as.gy; if (dim == 3) o[3] = as.gz;
+    o[1 + dim] = ab.v;
+    o[2 + dim] = ab.gx; o[3 + dim] = ab.gy; if (dim == 3) o[4 + dim] = ab.gz;
+}
+
+__global__ void eval_bessel_kernel(int which, const double* t, int count, double* out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    float v = static_cast<float>(t[i]);
+    out[i] = which == 0 ? bessel_k0(v) : which == 1 ? bessel_k1(v) : which == 2 ? bessel_i0(v) : bessel_i1(v);
+}
+
+// partials -> running sums of the evaluation points (cache.cpp:455-459, 491-495)
+__global__ void finalize_kernel(const double* part, int chunksB, int chunksS, int comps, int K, const int* order,
+                                int N, int M, int val, int grad, int dim, const int* skipB, const int* skipS,
+                                PointsDev pts) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= K) return;
+    int p = order[i];
+    size_t stride = static_cast<size_t>(comps) * K;
+    double b[4] = {0, 0, 0, 0}, s[4] = {0, 0, 0, 0};
+    for (int c = 0; c < chunksB; ++c)
+        for (int k = 0; k < comps; ++k) b[k] += part[c * stride + static_cast<size_t>(k) * K + i];
+    for (int c = chunksB; c < chunksB + chunksS; ++c)
+        for (int k = 0; k < comps; ++k) s[k] += part[c * stride + static_cast<size_t>(k) * K + i];
+    int sb = skipB[i], sS = skipS[i];
+    int k = 0;
+    if (val) {
+        pts.bsum[p] += b[k];
+        pts.ssum[p] += s[k];
+        pts.nb[p] += N - sb;
+        pts.ms[p] += M - sS;
+        pts.skipped[p] += sb + sS;
+        ++k;
+    }
+    if (grad) {
+        for (int d = 0; d < dim; ++d) {
+            pts.bgsum[static_cast<size_t>(dim) * p + d] += b[k + d];
+            pts.sgsum[static_cast<size_t>(dim) * p + d] += s[k + d];
+        }
+        pts.nbg[p] += N - sb;
+        pts.msg[p] += M - sS;
+        pts.skipped[p] += sb + sS;
+    }
+}
+
+__global__ void gather_points_kernel(const double* x, const int* order, int K, int dim, float* out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= K) return;
+    int p = order[i];
+    for (int d = 0; d < dim; ++d) out[static_cast<size_t>(dim) * i + d] = static_cast<float>(x[static_cast<size_t>(dim) * p + d]);
+}
+
+template <int KIND>
+void launch_kind(const Params& P, bool val, bool grad, int grid, cudaStream_t st) {
+    if (val && grad) gather_kernel<KIND, true, true><<<grid, kThreads, 0, st>>>(P);
+    else if (val) gather_kernel<KIND, true, false><<<grid, kThreads, 0, st>>>(P);
+    else gather_kernel<KIND, false, true><<<grid, kThreads, 0, st>>>(P);
+}
+
+template <int KIND>
+int occupancy(bool val, bool grad) {
+    int occ = 0;
+    if (val && grad) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel<KIND, true, true>, kThreads, 0);
+    else if (val) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel<KIND, true, false>, kThreads, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel<KIND, false, true>, kThreads, 0);
+    return occ > 0 ? occ : 1;
+}
+
+inline int blocks(long long n, int t) { return static_cast<int>((n + t - 1) / t); }
+
+}  // namespace
+
+void pack_boundary(const CacheSample* cs, int n, int kind, int voronoi, float4* out, cudaStream_t st) {
+    if (n <= 0) return;
+    pack_boundary_kernel<<<blocks(n, 256), 256, 0, st>>>(cs, n, kind, voronoi, out);
+    count_launch();
+}
+
+void pack_source(const SourceSampleDev* ss, int m, int kind, float4* out, cudaStream_t st) {
+    if (m <= 0) return;
+    pack_source_kernel<<<blocks(m, 256), 256, 0, st>>>(ss, m, kind, out);
+    count_launch();
+}
+
+void eval_kernels(int kind, const double* x, const double* y, const double* n, int count, int dim, float sigma,
+                  double* out, cudaStream_t st) {
+    if (count <= 0) return;
+    int g = blocks(count, 128);
+    switch (kind) {
+        case kLap2: eval_kernels_kernel<kLap2><<<g, 128, 0, st>>>(x, y, n, count, dim, sigma, out); break;
+        case kScr2: eval_kernels_kernel<kScr2><<<g, 128, 0, st>>>(x, y, n, count, dim, sigma, out); break;
+        case kLap3: eval_kernels_kernel<kLap3><<<g, 128, 0, st>>>(x, y, n, count, dim, sigma, out); break;
+        default: eval_kernels_kernel<kScr3><<<g, 128, 0, st>>>(x, y, n, count, dim, sigma, out); break;
+    }
+    count_launch();
+}
+
+void eval_bessel(int which, const double* t, int count, double* out, cudaStream_t st) {
+    if (count <= 0) return;
+    eval_bessel_kernel<<<blocks(count, 128), 128, 0, st>>>(which, t, count, out);
+    count_launch();
+}
+
+void gather_points(const double* x, const int* order, int K, int dim, float* out, cudaStream_t st) {
+    if (K <= 0) return;
+    gather_points_kernel<<<blocks(K, 256), 256, 0, st>>>(x, order, K, dim, out);
+    count_launch();
+}
+
+GatherPlan plan_gather(int kind, int K, int N, int M, bool val, bool grad) {
+    GatherPlan g;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int occ = kind == kLap2 ? occupancy<kLap2>(val, grad)
+              : kind == kScr2 ? occupancy<kScr2>(val, grad)
+              : kind == kLap3 ? occupancy<kLap3>(val, grad)
+                              : occupancy<kScr3>(val, grad);
+    g.tiles = (K + kPT - 1) / kPT;
+    long long slots = static_cast<long long>(sms) * occ;
+    // pick the chunk size (a multiple of kTS) whose unit count fills whole waves best,
+    // preferring fewer, larger chunks on ties
+    double bestEff = -1.0;
+    int total = N + M;
+    int maxTiles = (total + kTS - 1) / kTS;
+    for (int ct = 1; ct <= maxTiles; ++ct) {
+        int chunk = ct * kTS;
+        int cb = (N + chunk - 1) / chunk, cs = (M + chunk - 1) / chunk;
+        long long units = static_cast<long long>(g.tiles) * (cb + cs);
+        long long waves = (units + slots - 1) / slots;
+        double eff = static_cast<double>(units) / static_cast<double>(waves * slots);
+        // small per-unit overhead penalty for tiny chunks
+        eff *= static_cast<double>(chunk) / (chunk + 2.0 * kTS);
+        if (eff > bestEff + 1e-9) { bestEff = eff; g.chunk = chunk; g.chunksB = cb; g.chunksS = cs; }
+        if (units < slots && ct > 1 && cb + cs <= 1) break;
+    }
+    long long units = static_cast<long long>(g.tiles) * (g.chunksB + g.chunksS);
+    g.grid = static_cast<int>(units < slots ? units : slots);
+    g.grid = g.grid > 0 ? g.grid : 1;
+    g.comps = (val ? 1 : 0) + (grad ? (kind >= kLap3 ? 3 : 2) : 0);
+    return g;
+}
+
+void launch_gather(int kind, const GatherPlan& g, const float4* pack, int N, int M, const float* px, int K, int dim,
+                   float sigma, float tol, bool val, bool grad, double* part, int* skipB, int* skipS,
+                   cudaStream_t st) {
+    if (K <= 0 || (N + M) <= 0) return;
+    Params P;
+    P.pack = pack;
+    P.N = N;
+    P.M = M;
+    P.px = px;
+    P.K = K;
+    P.dim = dim;
+    P.chunk = g.chunk;
+    P.chunksB = g.chunksB;
+    P.chunksS = g.chunksS;
+    P.tiles = g.tiles;
+    P.sigma = sigma;
+    P.s = sqrtf(sigma);
+    P.tol2 = tol * tol;
+    P.part = part;
+    P.comps = g.comps;
+    P.skipB = skipB;
+    P.skipS = skipS;
+    switch (kind) {
+        case kLap2: launch_kind<kLap2>(P, val, grad, g.grid, st); break;
+        case kScr2: launch_kind<kScr2>(P, val, grad, g.grid, st); break;
+        case kLap3: launch_kind<kLap3>(P, val, grad, g.grid, st); break;
+        default: launch_kind<kScr3>(P, val, grad, g.grid, st); break;
+    }
+    count_launch();
+}
+
+void launch_finalize(const double* part, const GatherPlan& g, int K, const int* order, int N, int M, bool val,
+                     bool grad, int dim, const int* skipB, const int* skipS, const PointsDev& pts, cudaStream_t st) {
+    if (K <= 0) return;
+    finalize_kernel<<<blocks(K, 256), 256, 0, st>>>(part, g.chunksB, g.chunksS, g.comps, K, order, N, M, val ? 1 : 0,
+                                                    grad ? 1 : 0, dim, skipB, skipS, pts);
+    count_launch();
+}
+
+}  // namespace bvc_impl

@@ -1,0 +1,120 @@
+// internal.h — types shared by the CUDA translation units of libbvc_b200.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "device_math.cuh"
+#include "host_scene.h"
+#include "scene_dev.cuh"
+
+namespace bvc_impl {
+
+using bvc_dev::DevField;
+using bvc_dev::SceneView2;
+
+// PdeProblem with device field descriptors (pointwise.h:19-26)
+struct DevProblem {
+    int screened;   // KernelKind::ScreenedPoisson
+    float sigma, sqrtSigma;
+    int dim;
+    DevField f, g, h;
+};
+
+// WalkContext (pointwise.cpp:11-35) in device form
+struct WalkEnv {
+    SceneView2 S;
+    DevProblem P;
+    float eps, rmin, tguard, insideTol, scale, nudge;
+    float cx, cy, escape;  // scene box centre and escape half-width
+    int maxSteps;
+    int hasNeumann, hasSource, hasH, closed;
+    uint32_t k0, k1;  // Philox key of the job (seed, salt, round)
+};
+
+// A batch of estimator tasks. U tasks: nU plain walks from each U start point.
+// D tasks: nD first-ball gradient samples (pointwise.cpp:195-215) at each D point.
+// Outputs land in fixed slots, so results do not depend on scheduling.
+struct WalkJob {
+    int nU;
+    int nPtsU;
+    const float2* startU;
+    const long long* gidU;  // global id per U point (RNG keying; NULL => local index)
+    float* outU;            // [pt * nU + k]
+    int* truncU;            // per point, may be NULL
+    int nD;
+    int nPtsD;
+    const float2* xD;       // gradient ball center
+    const float2* normalD;  // NULL => vector output (wostGradient)
+    const float* radiusD;   // first-ball radius
+    const long long* gidD;
+    float* outD;            // [pt * nD + k] or [2 * (pt * nD + k) + c]
+    int* truncD;
+    long long gidBaseU;     // global id of U point 0 when gidU is NULL
+    unsigned long long* truncTotal;  // total truncated walks (may be NULL)
+    unsigned long long* steps;  // total closest-Dirichlet queries (may be NULL)
+    unsigned long long* counter; // work-queue head, zeroed by the launcher
+};
+
+void launch_walk_job(const WalkEnv& env, const WalkJob& job, cudaStream_t st);
+
+// per-point mean / standard error (runWalks pointwise.cpp:167-186), fixed order
+void launch_reduce_estimates(const float* vals, int nPts, int per, int comps, int comp, double* mean,
+                             double* se, cudaStream_t st);
+
+// device boundary sampler (BoundarySampler::sample sampling.cpp:37-44)
+struct CacheSample {
+    float z[3];
+    float n[3];
+    float pdf, uHat, dHat, weight, arc;
+    int segment;
+};
+static_assert(sizeof(CacheSample) == 48, "packed cache sample is 48 bytes");
+
+struct SourceSampleDev {
+    float y[3];
+    float pdf, f;
+    float pad[3];
+};
+static_assert(sizeof(SourceSampleDev) == 32, "packed source sample is 32 bytes");
+
+// k-th sample of `count` draws u = stratified ? (k + U)/count : U from Philox
+// (key, counter = ctr[j] or begin + j), then the CDF lookup of fromUnit (sampling.cpp:20-35)
+void launch_sample_boundary(const double* cdf, const int* ids, int m, double total, const float4* segAB,
+                            const float2* segNormal, const float* segArc, const float* segLen, int count,
+                            int begin, int n, const long long* ctr, int stratified, uint32_t k0, uint32_t k1,
+                            CacheSample* out, cudaStream_t st);
+
+// per-sample preparation for cache generation (cache.cpp:318-352): walk start
+// (z, or z - eps/2 n on known-Neumann pieces), D flag, first-ball radius
+// (gradientBallRadius pointwise.cpp:217-221), interior check (requireInterior
+// pointwise.cpp:188-191) and the exact Neumann data h(z) for Neumann samples
+void launch_prepare_samples(const WalkEnv& env, CacheSample* samples, int n, const int* regionKinds,
+                            const int* regionSource, float2* startU, int* isD, float* gradR, uint8_t* outside,
+                            cudaStream_t st);
+
+// gathers the D points of a cache job from their samples
+void launch_gather_dpoints(const CacheSample* samples, const int* dIdx, int nD, const float* gradR,
+                           long long gidBase, const long long* gid, float2* xD, float2* nD_, float* rD,
+                           long long* gidD, cudaStream_t st);
+
+// writes uHat / dHat means into the cache samples and flags non-finite results
+void launch_finish_samples(CacheSample* samples, int n, const float* outU, int nU, const int* dIdx, int nDpts,
+                           const float* outD, int nD, uint8_t* failed, cudaStream_t st);
+
+// single-CTA stream compaction of nonzero flags; writes the count to *outCount
+void launch_compact(const int* flags, int n, int* outIdx, int* outCount, cudaStream_t st);
+
+// scene queries for the ABI (batched)
+void launch_closest(const SceneView2& S, const double* x, int n, unsigned mask, double* point, double* dist,
+                    int* seg, double* t, cudaStream_t st);
+void launch_silhouette(const SceneView2& S, const double* x, int n, double* dist, cudaStream_t st);
+void launch_ray(const SceneView2& S, const double* o, const double* d, int n, double tMax, unsigned mask,
+                double tMin, double* t, int* seg, double* point, double* s, cudaStream_t st);
+void launch_inside(const SceneView2& S, const double* x, int n, float tol, uint8_t* out, cudaStream_t st);
+
+// kernel-launch accounting (bench gpu_launches)
+void count_launch(int n = 1);
+
+}  // namespace bvc_impl

@@ -1,0 +1,294 @@
+// scene_dev.cuh — device scene layout and BVH traversals (2D segments).
+//
+// Replaces the reference's recursive AoS double-precision BVH queries
+// (bvh.h:107-146, bvh.cpp:53-83, scene.cpp:133-254) with stack-based FP32
+// traversals over a flattened binary BVH whose nodes hold both child boxes
+// (one 48-byte node fetch orders and prunes both children).
+#pragma once
+#include <cstdint>
+
+#include "device_math.cuh"
+
+namespace bvc_dev {
+
+constexpr float kFInf = __builtin_huge_valf();
+
+struct alignas(16) Node2 {
+    float4 lbox;  // lo.x, lo.y, hi.x, hi.y
+    float4 rbox;
+    int left, right;  // >= 0 internal node; < 0 leaf: ~((start << 3) | (count - 1))
+    unsigned mask;    // left label mask | right label mask << 2
+    int pad;
+};
+
+struct alignas(16) Prim2 {
+    float4 seg;      // a.x, a.y, b.x, b.y
+    int id;          // caller-side segment index
+    int label;       // 0 Dirichlet, 1 Neumann
+    int sil0, sil1;  // silhouette candidate slots (-1 none)
+};
+
+struct SceneView2 {
+    const Node2* nodes;
+    const Prim2* prims;        // leaf order
+    const float2* segNormal;   // by segment id: unit outward normal
+    const float4* segAB;       // by segment id: a.x, a.y, b.x, b.y
+    const float2* silP;        // silhouette vertex
+    const float4* silN;        // n1, n2
+    const int* silAlways;
+    int ns;
+    float diagonal;
+};
+
+__device__ __forceinline__ float box_dist2(const float4& b, float x, float y) {
+    float dx = fmaxf(fmaxf(b.x - x, 0.0f), x - b.z);
+    float dy = fmaxf(fmaxf(b.y - y, 0.0f), y - b.w);
+    return dx * dx + dy * dy;
+}
+
+// closest point on a segment (bvh.h:153-159); returns squared distance
+__device__ __forceinline__ float seg_closest(const float4& s, float x, float y, float& px, float& py, float& t) {
+    float ux = s.z - s.x, uy = s.w - s.y;
+    float l2 = ux * ux + uy * uy;
+    float tt = l2 > 0.0f ? ((x - s.x) * ux + (y - s.y) * uy) / l2 : 0.0f;
+    tt = fminf(fmaxf(tt, 0.0f), 1.0f);
+    px = fmaf(tt, ux, s.x);
+    py = fmaf(tt, uy, s.y);
+    t = tt;
+    float dx = px - x, dy = py - y;
+    return dx * dx + dy * dy;
+}
+
+constexpr int kStack = 48;
+
+// Generic best-first traversal. visit(prim) handles one primitive of a visited
+// leaf; threshold() returns the current squared pruning radius.
+template <class Visit, class Thr>
+__device__ __forceinline__ void traverse_near(const SceneView2& S, float x, float y, unsigned qmask, Visit&& visit,
+                                              Thr&& threshold) {
+    int stackRef[kStack];
+    float stackD[kStack];
+    int sp = 0;
+    int ref = 0;
+    for (;;) {
+        if (ref >= 0) {
+            const Node2 nd = S.nodes[ref];
+            float thr = threshold();
+            float dl = (nd.mask & qmask) ? box_dist2(nd.lbox, x, y) : kFInf;
+            float dr = ((nd.mask >> 2) & qmask) ? box_dist2(nd.rbox, x, y) : kFInf;
+            bool vl = dl <= thr, vr = dr <= thr;
+            if (vl && vr) {
+                int nearRef = dl <= dr ? nd.left : nd.right;
+                int farRef = dl <= dr ? nd.right : nd.left;
+                stackRef[sp] = farRef;
+                stackD[sp] = fmaxf(dl, dr);
+                ++sp;
+                ref = nearRef;
+                continue;
+            }
+            if (vl) { ref = nd.left; continue; }
+            if (vr) { ref = nd.right; continue; }
+        } else {
+            int code = ~ref;
+            int start = code >> 3, count = (code & 7) + 1;
+            for (int i = start; i < start + count; ++i) {
+                const Prim2 p = S.prims[i];
+                if ((1u << p.label) & qmask) visit(p);
+            }
+        }
+        // pop, skipping entries pruned since they were pushed
+        for (;;) {
+            if (sp == 0) return;
+            --sp;
+            if (stackD[sp] <= threshold()) break;
+        }
+        ref = stackRef[sp];
+    }
+}
+
+struct Closest {
+    float d2;
+    float px, py, t;
+    int seg;
+};
+
+// Scene::closestPoint (scene.cpp:133-144; bvh.cpp:53-69)
+__device__ __forceinline__ Closest closest_point(const SceneView2& S, float x, float y, unsigned qmask,
+                                                 float maxD2 = kFInf) {
+    Closest c{maxD2, 0.0f, 0.0f, 0.0f, -1};
+    traverse_near(
+        S, x, y, qmask,
+        [&](const Prim2& p) {
+            float px, py, t;
+            float d2 = seg_closest(p.seg, x, y, px, py, t);
+            if (d2 < c.d2) { c.d2 = d2; c.px = px; c.py = py; c.t = t; c.seg = p.id; }
+        },
+        [&]() { return c.d2; });
+    return c;
+}
+
+// silhouetteTest (scene.cpp:166-172)
+__device__ __forceinline__ bool silhouette_ok(const SceneView2& S, int k, float x, float y, float& d2) {
+    float2 p = S.silP[k];
+    float dx = p.x - x, dy = p.y - y;
+    d2 = dx * dx + dy * dy;
+    if (S.silAlways[k]) return true;
+    float4 n = S.silN[k];
+    float d1 = n.x * dx + n.y * dy, d2n = n.z * dx + n.w * dy;
+    return d1 * d2n <= 0.0f;
+}
+
+// Scene::silhouetteDistance (scene.cpp:174-185); returns squared distance
+__device__ __forceinline__ float silhouette_dist2(const SceneView2& S, float x, float y) {
+    float best = kFInf;
+    traverse_near(
+        S, x, y, 2u,
+        [&](const Prim2& p) {
+            float d2;
+            if (p.sil0 >= 0 && silhouette_ok(S, p.sil0, x, y, d2) && d2 < best) best = d2;
+            if (p.sil1 >= 0 && silhouette_ok(S, p.sil1, x, y, d2) && d2 < best) best = d2;
+        },
+        [&]() { return best; });
+    return best;
+}
+
+// One WoSt step's geometry in a single traversal: the closest Dirichlet point and
+// the closest visible Neumann silhouette vertex (pointwise.cpp:216-222). Pruning
+// uses max(min(bestD, bestS), eps): everything the reference's two separate
+// queries would decide on (termination within eps; R = min(dD, dS)) is exact.
+struct StarQuery {
+    Closest D;
+    float s2;
+};
+__device__ __forceinline__ StarQuery star_query(const SceneView2& S, float x, float y, float eps2) {
+    StarQuery q;
+    q.D = Closest{kFInf, 0.0f, 0.0f, 0.0f, -1};
+    q.s2 = kFInf;
+    traverse_near(
+        S, x, y, 3u,
+        [&](const Prim2& p) {
+            if (p.label == 0) {
+                float px, py, t;
+                float d2 = seg_closest(p.seg, x, y, px, py, t);
+                if (d2 < q.D.d2) { q.D.d2 = d2; q.D.px = px; q.D.py = py; q.D.t = t; q.D.seg = p.id; }
+            } else {
+                float d2;
+                if (p.sil0 >= 0 && silhouette_ok(S, p.sil0, x, y, d2) && d2 < q.s2) q.s2 = d2;
+                if (p.sil1 >= 0 && silhouette_ok(S, p.sil1, x, y, d2) && d2 < q.s2) q.s2 = d2;
+            }
+        },
+        [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); });
+    return q;
+}
+
+// slab test against o + t d, t in [0, tMax] (bvh.h:32-43)
+__device__ __forceinline__ bool ray_box(const float4& b, float ox, float oy, float idx, float idy, float tMax) {
+    float t0 = 0.0f, t1 = tMax;
+    float tn = (b.x - ox) * idx, tf = (b.z - ox) * idx;
+    if (tn > tf) { float s = tn; tn = tf; tf = s; }
+    t0 = fmaxf(t0, tn);
+    t1 = fminf(t1, tf);
+    if (t0 > t1) return false;
+    tn = (b.y - oy) * idy;
+    tf = (b.w - oy) * idy;
+    if (tn > tf) { float s = tn; tn = tf; tf = s; }
+    t0 = fmaxf(t0, tn);
+    t1 = fminf(t1, tf);
+    return t0 <= t1;
+}
+
+// side of v relative to the ray o + t d; explicit roundings (no FMA contraction)
+// so a vertex shared by two segments is classified identically for both
+__device__ __forceinline__ float ray_side(float dx, float dy, float ox, float oy, float vx, float vy) {
+    return __fsub_rn(__fmul_rn(dx, __fsub_rn(vy, oy)), __fmul_rn(dy, __fsub_rn(vx, ox)));
+}
+
+struct RayHit {
+    float t, s, px, py;
+    int seg;
+};
+
+// Scene::intersectRay (scene.cpp:196-208; raySegment bvh.cpp:71-83): first hit
+// with t in (tMin, tMax] among the filtered segments, skipping `skipSeg` (the
+// segment the walk currently stands on: a ray leaving a straight segment cannot
+// hit it again, and skipping it keeps FP32 re-hits out).
+__device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, float oy, float dx, float dy,
+                                                float tMax, unsigned qmask, float tMin, int skipSeg) {
+    RayHit h{kFInf, 0.0f, 0.0f, 0.0f, -1};
+    float idx = 1.0f / dx, idy = 1.0f / dy;
+    float limit = tMax;
+    int stack[kStack];
+    int sp = 0, ref = 0;
+    for (;;) {
+        if (ref >= 0) {
+            const Node2 nd = S.nodes[ref];
+            bool vl = (nd.mask & qmask) && ray_box(nd.lbox, ox, oy, idx, idy, limit);
+            bool vr = ((nd.mask >> 2) & qmask) && ray_box(nd.rbox, ox, oy, idx, idy, limit);
+            if (vl && vr) { stack[sp++] = nd.right; ref = nd.left; continue; }
+            if (vl) { ref = nd.left; continue; }
+            if (vr) { ref = nd.right; continue; }
+        } else {
+            int code = ~ref;
+            int start = code >> 3, count = (code & 7) + 1;
+            for (int i = start; i < start + count; ++i) {
+                const Prim2 p = S.prims[i];
+                if (!((1u << p.label) & qmask) || p.id == skipSeg) continue;
+                // watertight crossing test: each endpoint is classified by its side
+                // of the ray; a vertex shared by two segments gets the same sign in
+                // both, so a ray can never slip between them (raySegment bvh.cpp:71-83
+                // decides via s in [0,1], which FP32 cancellation breaks near vertices)
+                float sa = ray_side(dx, dy, ox, oy, p.seg.x, p.seg.y);
+                float sb = ray_side(dx, dy, ox, oy, p.seg.z, p.seg.w);
+                if ((sa > 0.0f && sb > 0.0f) || (sa < 0.0f && sb < 0.0f)) continue;
+                float den = sa - sb;  // = cross(d, e) with e = b - a, up to sign convention
+                if (den == 0.0f) continue;  // parallel / collinear: miss
+                float s = sa / den;
+                float ex = p.seg.z - p.seg.x, ey = p.seg.w - p.seg.y;
+                float px = fmaf(s, ex, p.seg.x), py = fmaf(s, ey, p.seg.y);
+                float t = (px - ox) * dx + (py - oy) * dy;  // unit direction: distance along the ray
+                if (t <= 0.0f || t > limit) continue;
+                if (t > tMin && t < h.t) {
+                    h.t = t; h.s = s; h.seg = p.id;
+                    h.px = px; h.py = py;
+                    limit = t;
+                }
+            }
+        }
+        if (sp == 0) return h;
+        ref = stack[--sp];
+    }
+}
+
+// Scene::inside (scene.cpp:240-254): boundary-inclusive within tol, then crossing
+// parity along +x with the straddle form; only leaves whose box spans x.y and
+// reaches past x.x are visited.
+__device__ __forceinline__ bool inside(const SceneView2& S, float x, float y, float tol) {
+    Closest c = closest_point(S, x, y, 3u, tol * tol);
+    if (c.seg >= 0) return true;
+    bool in = false;
+    int stack[kStack];
+    int sp = 0, ref = 0;
+    for (;;) {
+        if (ref >= 0) {
+            const Node2 nd = S.nodes[ref];
+            bool vl = (nd.mask & 3u) && nd.lbox.y <= y && nd.lbox.w >= y && nd.lbox.z > x;
+            bool vr = ((nd.mask >> 2) & 3u) && nd.rbox.y <= y && nd.rbox.w >= y && nd.rbox.z > x;
+            if (vl && vr) { stack[sp++] = nd.right; ref = nd.left; continue; }
+            if (vl) { ref = nd.left; continue; }
+            if (vr) { ref = nd.right; continue; }
+        } else {
+            int code = ~ref;
+            int start = code >> 3, count = (code & 7) + 1;
+            for (int i = start; i < start + count; ++i) {
+                const float4 s = S.prims[i].seg;
+                if ((s.y > y) == (s.w > y)) continue;
+                float xc = s.x + (y - s.y) / (s.w - s.y) * (s.z - s.x);
+                if (x < xc) in = !in;
+            }
+        }
+        if (sp == 0) return in;
+        ref = stack[--sp];
+    }
+}
+
+}  // namespace bvc_dev
