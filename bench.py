@@ -1,0 +1,417 @@
+"""BVC hot-path benchmark (BASELINE.json metric) on BASELINE config 2 by default.
+
+A step is one progressive BVC round, updateSolution (cache.cpp:622-684), on
+C2 — the 2D mixed Dirichlet/Neumann square: 16384 boundary samples x (512 u-walks
++ 512 du/dn walks on the estimated pieces), WoSt walks with eps = 1e-3, then the
+u and grad-u gather at the 512 x 512 grid's non-fallback nodes plus pointwise
+walks at the fallback-band nodes. Inputs are seeded synthetic data of that shape
+(no dataset exists for this path).
+
+value  = interactions/s = (non-fallback points x cache samples) per round / round time,
+         whole job (all ranks). Walk steps/s (closest-Dirichlet queries) are reported
+         next to it.
+e2e    = the same metric through the public API with host buffers: each step
+         uploads the query points (H2D), runs the round and reads u back (D2H).
+--impl reference: the reference's own CPU implementation (oracle/_ref, compiled from
+         /root/reference) on a bounded sample of the same round, extrapolated.
+
+Multi-GPU (torchrun): cache samples and query points are sharded by rank; the
+packed cache shards are all-gathered with NCCL; each rank gathers its points.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        d["source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    return dict(PEAKS_FALLBACK)
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device=0):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.QUERY}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 4 + i and "Active" in s[4 + i]
+                          and "Not" not in s[4 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def build_problem(cfg_id, B, configs, abi):
+    c = configs.CONFIGS[cfg_id]()
+    scene = B.Scene(c.vertices, c.segments, c.labels)
+    if c.region_mode == abi.REGION_SUBDOMAIN:
+        sub = B.Scene(c.sub_vertices, c.sub_segments, np.zeros(len(c.sub_segments), np.int32))
+        region = B.SolveRegion(scene, abi.REGION_SUBDOMAIN, c.region_offset, sub, epsilon=c.epsilon)
+        keep = region.boundary.inside(c.points)
+    else:
+        region = B.SolveRegion(scene, offset=c.region_offset, epsilon=c.epsilon)
+        keep = scene.inside(c.points)
+    c.points = c.points[keep]
+    return c, scene, region
+
+
+def run_gpu(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2302_11825_b200 as B
+    from paper_2302_11825_b200 import abi, configs
+
+    B.lib().bvc_set_device(local)
+    c, scene, region = build_problem(args.config, B, configs, abi)
+    cfg = c.cache
+    N, M = cfg.nBoundary, (cfg.nSource if c.problem.f.kind else 0)
+    K_all = len(c.points)
+    # points of this rank: a contiguous slice (the spatial sort keeps shards compact)
+    lo_p, hi_p = rank * K_all // world, (rank + 1) * K_all // world
+    my_points = c.points[lo_p:hi_p]
+    pts = B.EvaluationPoints(my_points)
+    B.mark_evaluation_points(scene, region, cfg, pts)
+    st0 = pts.download()
+    k_active = int((~st0["fallback"]).sum())
+    k_fallback = len(my_points) - k_active
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
+
+    def round_multi(p, rnd):
+        """shard walks by global sample index, NCCL all-gather of the packed cache
+        shards (48 B/sample), then each rank gathers its own query points"""
+        from paper_2302_11825_b200 import distributed
+
+        stats = {}
+        cache = distributed.generate_and_allgather(B, dist, torch, scene, c.problem, region, cfg, c.seed, rnd,
+                                                   rank, world, stats)
+        scache = B.generate_source_cache(c.problem, region, cfg, c.seed, rnd) if M else None
+        spec = B.make_splat_config(scene, c.problem, cfg)
+        B.splat_range(cache, scache, p, spec, 0, 1 << 62, True, bool(c.gradients))
+        return stats
+
+    def round_single(p, rnd):
+        return B.update_solution(scene, c.problem, region, cfg, p, c.seed, rnd, gradients=bool(c.gradients))
+
+    step = round_single if world == 1 else round_multi
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for w in range(args.warmup):
+        step(pts, 1000 + w)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = B.launch_count()
+    times, steps_total, walks_total = [], 0, 0
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            st = step(pts, k)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+            steps_total += st.get("cacheSteps", 0)
+            walks_total += st.get("cacheWalks", 0)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+    launches = B.launch_count() - launches0
+    t_step = float(np.mean(times))
+    if dist is not None:
+        t = torch.tensor([t_step], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step = float(t.item())
+        tot = torch.tensor([k_active, steps_total, walks_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tot)
+        k_active_all, steps_total, walks_total = (float(v) for v in tot.tolist())
+    else:
+        k_active_all = k_active
+    pairs = k_active_all * (N + M)
+    value = pairs / t_step
+    out = {"metric": "BVC eval interactions/s and walk steps/s per GPU; % of FP32/SFU roofline",
+           "value": value, "unit": "interactions/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak" if False else "strong",
+           "vs_baseline": None, "dtype": "fp32 (fp64 accumulation)", "data": "synthetic (seeded, configs.py)",
+           "gpu_launches": int(launches / max(args.steps, 1))}
+    out["walk_steps_per_s"] = steps_total / (t_step * args.steps)
+    out["walks_per_s"] = walks_total / (t_step * args.steps)
+    out["config"] = {"workload": c.name, "config_index": args.config, "boundary_samples": N, "source_samples": M,
+                     "walks_u": cfg.nWalksNeumann, "walks_dudn": cfg.nWalksDirichlet, "epsilon": c.epsilon,
+                     "region_offset": cfg.offset, "query_points": int(K_all), "nonfallback_points": int(k_active_all),
+                     "fallback_points": int(K_all - k_active_all), "gradients": bool(c.gradients),
+                     "parallelism": f"dp{world} (samples and points sharded)",
+                     "l2": "flushed between timed steps (256 MB write)"}
+    out["clocks"] = clk.summary()
+    if rank == 0:
+        out.update(phase_breakdown(B, c, scene, region, pts, args))
+        out["e2e"] = e2e_measure(B, c, scene, region, my_points, args, world)
+        if world == 1 and not args.no_cpu:
+            out["cpu_baseline"] = cpu_baseline(c, args.cpu_sample_s)
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def phase_breakdown(B, c, scene, region, pts, args):
+    """Per-kernel timings with CUDA events (outside the timed steps) and the roofline."""
+    import torch
+
+    cfg = c.cache
+    N, M = cfg.nBoundary, (cfg.nSource if c.problem.f.kind else 0)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev[0].record()
+    stats = {}
+    cache = B.generate_boundary_cache(scene, c.problem, region, cfg, c.seed, 77, stats=stats)
+    ev[1].record()
+    scache = B.generate_source_cache(c.problem, region, cfg, c.seed, 77) if M else None
+    spec = B.make_splat_config(scene, c.problem, cfg)
+    B.splat_range(cache, scache, pts, spec, 0, 1 << 62, True, bool(c.gradients))  # warm the sort/order
+    torch.cuda.synchronize()
+    reps = 5
+    ev[2].record()
+    for _ in range(reps):
+        B.splat_range(cache, scache, pts, spec, 0, 1 << 62, True, bool(c.gradients))
+    ev[3].record()
+    torch.cuda.synchronize()
+    t_gen = ev[0].elapsed_time(ev[1]) / 1e3
+    t_gather = ev[2].elapsed_time(ev[3]) / 1e3 / reps
+    st = pts.download()
+    k_active = int((~st["fallback"]).sum())
+    pairs = k_active * (N + M)
+    peaks = load_peaks()
+    # walk traffic: algorithmic bytes per step from a counting launch
+    prof = B.walk_traffic_profile(scene, c.problem, region, cfg, c.seed, 77)
+    steps = max(prof["steps"], 1.0)
+    bytes_per_step = (prof["node_fetches"] * 48 + prof["prim_fetches"] * 32) / steps + 32.0
+    walk_bytes = bytes_per_step * stats["cacheSteps"]
+    achieved = walk_bytes / t_gen / 1e9
+    # gather bound: 148 SMs * f_SM / max(F/128, S/16) pairs/s (SURVEY §8d, V2 = 18 F, 2 S)
+    props = torch.cuda.get_device_properties(0)
+    sms = props.multi_processor_count
+    f_sm = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    per_pair = {"lap2_u": (9, 2), "lap2_ugrad": (18, 2), "scr2_ugrad": (50, 3), "lap3_u": (14, 1), "scr3_u": (20, 2)}
+    key = ("scr2_ugrad" if c.problem.kernel.kind else "lap2_ugrad") if c.gradients else "lap2_u"
+    F, S = per_pair[key]
+    bound = sms * f_sm / max(F / 128.0, S / 16.0)
+    gather_rate = pairs / t_gather
+    dominant = "walk" if t_gen >= t_gather else "gather"
+    return {
+        "phases_s": {"cache_generation": t_gen, "gather": t_gather},
+        "roofline": {"bound": "hbm", "kernel": "bvc walk_kernel (cache generation)", "achieved": achieved,
+                     "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s",
+                     "frac": achieved / float(peaks.get("hbm_gbs", 6650.0)), "traffic": None,
+                     "algorithmic_bytes_per_step": bytes_per_step,
+                     "node_fetches_per_step": prof["node_fetches"] / steps,
+                     "prim_fetches_per_step": prof["prim_fetches"] / steps, "peak_source": peaks["source"],
+                     "dominant": dominant},
+        "gather_roofline": {"bound": "fp32+sfu", "kernel": f"bvc gather_kernel ({key})", "achieved": gather_rate,
+                            "peak": bound, "unit": "pairs/s", "frac": gather_rate / bound,
+                            "peak_formula": f"{sms} SMs x {f_sm / 1e6:.0f} MHz / max({F}/128, {S}/16)",
+                            "pairs_per_launch": pairs},
+    }
+
+
+def e2e_measure(B, c, scene, region, points, args, world):
+    """Public API with host buffers: H2D points, one round, D2H of u (and grad u)."""
+    import torch
+
+    times = []
+    reps = max(2, min(args.steps, 5))
+    for k in range(reps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pts = B.EvaluationPoints(points)               # H2D from host memory
+        B.mark_evaluation_points(scene, region, c.cache, pts)
+        B.update_solution(scene, c.problem, region, c.cache, pts, c.seed, 500 + k, gradients=bool(c.gradients))
+        st = pts.download()                            # D2H of the running sums
+        u = pts.solution(st)
+        torch.cuda.synchronize()
+        if k:
+            times.append(time.perf_counter() - t0)
+        assert np.all(np.isfinite(u))
+    N, M = c.cache.nBoundary, (c.cache.nSource if c.problem.f.kind else 0)
+    k_active = int((~st["fallback"]).sum())
+    t = float(np.mean(times))
+    d2h = len(points) * (8 * 2 + 8 * 2 + 8 * 4 + 8 * 4 + 8 * 3 + 8 * 2 + 2)  # the downloaded state arrays
+    return {"value": k_active * world * (N + M) / t, "unit": "interactions/s", "ms_per_step": t * 1e3,
+            "h2d_bytes_per_step": int(points.size * 8), "d2h_bytes_per_step": int(d2h),
+            "note": "wall clock per call incl. point upload, classification, round and state download"}
+
+
+def reference_round_estimate(c, sample_s=20.0, threads=0):
+    """Time the reference's own updateSolution pieces (oracle/_ref) on a bounded sample of
+    the round and extrapolate: generateBoundaryCache on n_sub samples (cost ~ #walks) and
+    splatSolution+splatGradient on k_sub points against the full cache (cost ~ K (N+M))."""
+    from oracle import oracle as O
+    from paper_2302_11825_b200 import abi
+
+    O.ref_lib()
+    rs = O.RefScene(c.vertices, c.segments, c.labels)
+    if c.region_mode == abi.REGION_SUBDOMAIN:
+        sub = O.RefScene(c.sub_vertices, c.sub_segments, np.zeros(len(c.sub_segments), np.int32))
+        rr = O.RefRegion(rs, abi.REGION_SUBDOMAIN, c.region_offset, sub, eps=c.epsilon)
+    else:
+        rr = O.RefRegion(rs, abi.REGION_WHOLE_DOMAIN, c.region_offset, eps=c.epsilon)
+    cfg = c.cache
+    N, M = cfg.nBoundary, (cfg.nSource if c.problem.f.kind else 0)
+    cfg.threads = threads
+    cores = O.ref_lib().ref_thread_count(threads)
+    # walks: grow the sample until ~40% of the budget is spent
+    n_sub, t_gen = 8, 0.0
+    while True:
+        sub_cfg = abi.CacheConfig.from_buffer_copy(cfg)
+        sub_cfg.nBoundary = n_sub
+        t0 = time.perf_counter()
+        small = O.ref_generate_boundary_cache(rs, c.problem, rr, sub_cfg, c.seed, 0)
+        t_gen = time.perf_counter() - t0
+        if t_gen > 0.4 * sample_s or n_sub >= N:
+            break
+        n_sub = min(N, int(n_sub * max(2.0, 0.4 * sample_s / max(t_gen, 1e-3) * 0.8)))
+    gen_full = t_gen * N / n_sub
+    # gather: the reference splats on a point subset against a full-size cache
+    rng = np.random.default_rng(0)
+    reps = int(np.ceil(N / n_sub))
+    cache = {k: np.tile(v, (reps, 1) if np.ndim(v) == 2 else reps)[:N] for k, v in small.items()
+             if k in ("z", "n", "pdf", "uHat", "dHat", "weight")}
+    scache = None
+    if M:
+        scache = O.ref_generate_source_cache(c.problem, rr, cfg, c.seed, 0)
+    fb, _ = O.ref_mark_points(rs, rr, cfg, c.points)
+    act = c.points[~fb]
+    k_sub = 64
+    while True:
+        xs = act[rng.choice(len(act), size=min(k_sub, len(act)), replace=False)]
+        spec = abi.KernelSpec(c.problem.kernel.kind, c.problem.kernel.sigma, 2, rs.diagonal)
+        st = O.ref_splat(spec, 1e-12 * rs.diagonal, cache, scache, xs, value=True, gradient=bool(c.gradients),
+                         threads=threads)
+        t_spl = st["seconds"]
+        if t_spl > 0.4 * sample_s or k_sub >= len(act):
+            break
+        k_sub = min(len(act), int(k_sub * max(2.0, 0.4 * sample_s / max(t_spl, 1e-3) * 0.8)))
+    splat_full = t_spl * len(act) / len(xs)
+    t_round = gen_full + splat_full
+    pairs = len(act) * (N + M)
+    return {"value": pairs / t_round, "unit": "interactions/s", "cores": int(cores), "kind": "reference",
+            "sample": (f"generateBoundaryCache on {n_sub}/{N} samples ({t_gen:.1f} s) + splatSolution"
+                       f"{'+splatGradient' if c.gradients else ''} on {len(xs)}/{len(act)} points vs the full "
+                       f"{N}+{M}-sample cache ({t_spl:.1f} s); extrapolated linearly (cost ~ walks, ~ K(N+M))"),
+            "round_seconds_extrapolated": t_round}
+
+
+def cpu_baseline(c, sample_s):
+    try:
+        return reference_round_estimate(c, sample_s)
+    except Exception as e:  # oracle/_ref missing on this host
+        return {"value": None, "unit": "interactions/s", "cores": os.cpu_count(), "kind": "reference",
+                "sample": f"unavailable: {e}"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2302_11825_b200 import abi, configs  # noqa: F401 (structs only; no GPU use)
+
+    c = configs.CONFIGS[args.config]()
+    vals = []
+    t0 = time.perf_counter()
+    for k in range(args.warmup + args.steps):
+        est = reference_round_estimate(c, args.cpu_sample_s / max(args.steps + args.warmup, 1) * 2, threads=0)
+        if k >= args.warmup:
+            vals.append(est)
+    value = float(np.mean([v["value"] for v in vals]))
+    out = {"metric": "BVC eval interactions/s and walk steps/s per GPU; % of FP32/SFU roofline", "value": value,
+           "unit": "interactions/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": float(np.mean([v["round_seconds_extrapolated"] for v in vals])) * 1e3,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded, configs.py)", "impl": "reference",
+           "config": {"workload": c.name, "config_index": args.config},
+           "cpu_baseline": {"value": value, "unit": "interactions/s", "cores": vals[-1]["cores"],
+                            "kind": "reference", "sample": vals[-1]["sample"]},
+           "e2e": {"value": value, "unit": "interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "wall_s": time.perf_counter() - t0}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3])
+    ap.add_argument("--cpu-sample-s", type=float, default=20.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -307,6 +307,12 @@ int bvc_wost_normal_derivative(bvc_scene scene, const bvc_problem* problem, cons
                                const double* normal, size_t n, const bvc_walk_config* cfg,
                                const uint64_t* streams, bvc_scalar_estimate* out);
 
+/* ---- diagnostics ---------------------------------------------------------- */
+/* one generateBoundaryCache with per-thread traversal counters (roofline bytes):
+   out = [closest-Dirichlet steps, BVH node fetches (48 B), primitive fetches (32 B), walks] */
+int bvc_walk_traffic_profile(bvc_scene scene, const bvc_problem* problem, bvc_region region,
+                             const bvc_cache_config* cfg, uint64_t seed, uint64_t round, double* out);
+
 /* ---- free-space kernels (kernels.h:78-129) and Bessel functions (kernels.h:46-49),
         evaluated in the device's FP32 arithmetic for parity tests -------------- */
 /* out per point: [G, dG/dx (dim), dG/dn_y, d2G/dx dn_y (dim)] = 2 + 2*dim floats */

@@ -625,8 +625,11 @@ int or_region_sample(const or_scene* s, int count, int stratified, uint64_t seed
         while (accepted < count) {
             proposals++;
             if (proposals >= 1000000 && accepted < proposals / 10000) return BVC_ERR_PARSE;
-            double q[2] = {s->lo[0] + rng_uniform(&rng) * ex, 0};
+            /* Vector2(u*ex, u*ey): g++ evaluates the constructor arguments right to
+               left, so the reference draws y first (sampling.cpp:86) */
+            double q[2];
             q[1] = s->lo[1] + rng_uniform(&rng) * ey;
+            q[0] = s->lo[0] + rng_uniform(&rng) * ex;
             if (scene_inside(s, q)) { p[2 * accepted] = q[0]; p[2 * accepted + 1] = q[1]; pdf[accepted] = pd; accepted++; }
         }
         return 0;
@@ -646,8 +649,8 @@ int or_region_sample(const or_scene* s, int count, int stratified, uint64_t seed
             if (proposals >= 1000000 && accepted < proposals / 10000) { free(order); return BVC_ERR_PARSE; }
             int cx = order[c] % g, cy = order[c] / g;
             double q[2];
+            q[1] = s->lo[1] + (cy + rng_uniform(&rng)) / g * ey; /* y first, as above */
             q[0] = s->lo[0] + (cx + rng_uniform(&rng)) / g * ex;
-            q[1] = s->lo[1] + (cy + rng_uniform(&rng)) / g * ey;
             if (scene_inside(s, q)) { p[2 * accepted] = q[0]; p[2 * accepted + 1] = q[1]; pdf[accepted] = pd; accepted++; }
         }
     }

@@ -31,7 +31,7 @@ SYMBOLS = (
     "bvc_source_cache_create bvc_source_cache_size bvc_source_cache_download bvc_source_cache_destroy "
     "bvc_make_splat_config bvc_splat_solution bvc_splat_gradient bvc_splat_solution_gradient bvc_splat_range "
     "bvc_update_solution bvc_wos_solve bvc_wost_solve bvc_wost_gradient bvc_wost_normal_derivative "
-    "bvc_eval_kernels bvc_eval_bessel"
+    "bvc_walk_traffic_profile bvc_eval_kernels bvc_eval_bessel"
 ).split()
 
 
@@ -556,6 +556,14 @@ def wost_gradient(scene, pb, x, cfg, streams=None):
 def wost_normal_derivative(scene, pb, x, normal, cfg, streams=None):
     """wostNormalDerivative (pointwise.h:75-76), batched."""
     return _estimates(lib().bvc_wost_normal_derivative, scene, pb, x, cfg, streams, normal=normal)
+
+
+def walk_traffic_profile(scene: Scene, pb, region: SolveRegion, cfg, seed, round_) -> dict:
+    """Counts BVH node / primitive fetches of one cache generation (diagnostic launch)."""
+    out = (C.c_double * 4)()
+    _check(lib().bvc_walk_traffic_profile(scene.h, C.byref(pb), region.h, C.byref(cfg), C.c_uint64(seed),
+                                          C.c_uint64(round_), out))
+    return dict(steps=out[0], node_fetches=out[1], prim_fetches=out[2], walks=out[3])
 
 
 def eval_kernels(spec, x, y, n):

@@ -33,6 +33,9 @@ namespace {
 
 thread_local std::string g_error;
 cudaStream_t g_stream = nullptr;
+// diagnostic traversal counting (bvc_walk_traffic_profile); off in production
+bool g_profile = false;
+unsigned long long g_profileTotals[2] = {0, 0};
 std::atomic<long long> g_launches{0};
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -253,6 +256,7 @@ struct bvc_scene_s {
         v.silAlways = silAlways.p;
         v.ns = host.ns;
         v.diagonal = static_cast<float>(host.diagonal);
+        v.counts = nullptr;
         return v;
     }
 };
@@ -469,7 +473,23 @@ void run_cache_walks(bvc_scene_s* S, bvc_region_s* R, const WalkEnv& E, const bv
     J.counter = ctr;
     J.steps = ctr + 1;
     J.truncTotal = ctr + 2;
-    launch_walk_job(E, J, g_stream);
+    if (g_profile) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        size_t slots = static_cast<size_t>(sms) * 32 * 256 * 2;
+        auto* cnt = ws().get<unsigned long long>(kWsEvalOut, slots);
+        CK(cudaMemsetAsync(cnt, 0, slots * sizeof(unsigned long long), g_stream));
+        WalkEnv Ec = E;
+        Ec.S.counts = cnt;
+        launch_walk_job(Ec, J, g_stream);
+        std::vector<unsigned long long> h(slots);
+        CK(cudaMemcpyAsync(h.data(), cnt, slots * sizeof(unsigned long long), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+        for (size_t i = 0; i < slots; ++i) g_profileTotals[i & 1] += h[i];
+    } else {
+        launch_walk_job(E, J, g_stream);
+    }
     launch_finish_samples(samples, n, J.outU, nU, dIdx, nD, J.outD, nDw, failed, g_stream);
     unsigned long long h[3];
     CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, g_stream));
@@ -1489,6 +1509,28 @@ int bvc_wost_normal_derivative(bvc_scene s, const bvc_problem* pb, const double*
         std::vector<long long> c(n), t(n);
         pointwise(s, *pb, x, normal, n, *cfg, streams, 2, m.data(), se.data(), c.data(), t.data());
         for (size_t i = 0; i < n; ++i) out[i] = bvc_scalar_estimate{m[i], se[i], c[i], t[i]};
+    })
+}
+
+int bvc_walk_traffic_profile(bvc_scene s, const bvc_problem* pb, bvc_region r, const bvc_cache_config* cfg,
+                             uint64_t seed, uint64_t round, double* out) {
+    API({
+        need(s && pb && r && cfg && out, "null argument");
+        bvc_boundary_cache_s c;
+        GenStats st;
+        g_profile = true;
+        g_profileTotals[0] = g_profileTotals[1] = 0;
+        try {
+            generate_cache(s, *pb, r, *cfg, seed, round, 0, std::max(1, cfg->nBoundary), &c, st);
+        } catch (...) {
+            g_profile = false;
+            throw;
+        }
+        g_profile = false;
+        out[0] = static_cast<double>(st.steps);
+        out[1] = static_cast<double>(g_profileTotals[0]);
+        out[2] = static_cast<double>(g_profileTotals[1]);
+        out[3] = static_cast<double>(st.walks);
     })
 }
 

@@ -38,7 +38,14 @@ struct SceneView2 {
     const int* silAlways;
     int ns;
     float diagonal;
+    // diagnostic traversal counters (NULL in production launches): per thread,
+    // [2 t] node fetches (48 B each), [2 t + 1] primitive fetches (32 B each)
+    unsigned long long* counts;
 };
+
+__device__ __forceinline__ void count_fetch(const SceneView2& S, int which) {
+    if (S.counts) S.counts[2 * (blockIdx.x * blockDim.x + threadIdx.x) + which] += 1;
+}
 
 __device__ __forceinline__ float box_dist2(const float4& b, float x, float y) {
     float dx = fmaxf(fmaxf(b.x - x, 0.0f), x - b.z);
@@ -73,6 +80,7 @@ __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, floa
     for (;;) {
         if (ref >= 0) {
             const Node2 nd = S.nodes[ref];
+            count_fetch(S, 0);
             float thr = threshold();
             float dl = (nd.mask & qmask) ? box_dist2(nd.lbox, x, y) : kFInf;
             float dr = ((nd.mask >> 2) & qmask) ? box_dist2(nd.rbox, x, y) : kFInf;
@@ -93,6 +101,7 @@ __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, floa
             int start = code >> 3, count = (code & 7) + 1;
             for (int i = start; i < start + count; ++i) {
                 const Prim2 p = S.prims[i];
+                count_fetch(S, 1);
                 if ((1u << p.label) & qmask) visit(p);
             }
         }
@@ -222,6 +231,7 @@ __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, f
     for (;;) {
         if (ref >= 0) {
             const Node2 nd = S.nodes[ref];
+            count_fetch(S, 0);
             bool vl = (nd.mask & qmask) && ray_box(nd.lbox, ox, oy, idx, idy, limit);
             bool vr = ((nd.mask >> 2) & qmask) && ray_box(nd.rbox, ox, oy, idx, idy, limit);
             if (vl && vr) { stack[sp++] = nd.right; ref = nd.left; continue; }
@@ -232,6 +242,7 @@ __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, f
             int start = code >> 3, count = (code & 7) + 1;
             for (int i = start; i < start + count; ++i) {
                 const Prim2 p = S.prims[i];
+                count_fetch(S, 1);
                 if (!((1u << p.label) & qmask) || p.id == skipSeg) continue;
                 // watertight crossing test: each endpoint is classified by its side
                 // of the ray; a vertex shared by two segments gets the same sign in
@@ -271,6 +282,7 @@ __device__ __forceinline__ bool inside(const SceneView2& S, float x, float y, fl
     for (;;) {
         if (ref >= 0) {
             const Node2 nd = S.nodes[ref];
+            count_fetch(S, 0);
             bool vl = (nd.mask & 3u) && nd.lbox.y <= y && nd.lbox.w >= y && nd.lbox.z > x;
             bool vr = ((nd.mask >> 2) & 3u) && nd.rbox.y <= y && nd.rbox.w >= y && nd.rbox.z > x;
             if (vl && vr) { stack[sp++] = nd.right; ref = nd.left; continue; }
@@ -281,6 +293,7 @@ __device__ __forceinline__ bool inside(const SceneView2& S, float x, float y, fl
             int start = code >> 3, count = (code & 7) + 1;
             for (int i = start; i < start + count; ++i) {
                 const float4 s = S.prims[i].seg;
+                count_fetch(S, 1);
                 if ((s.y > y) == (s.w > y)) continue;
                 float xc = s.x + (y - s.y) / (s.w - s.y) * (s.z - s.x);
                 if (x < xc) in = !in;

@@ -1,0 +1,62 @@
+"""Multi-GPU sharding of the BVC round.
+
+* cache: rank r builds samples [r N / W, (r + 1) N / W); the walks' RNG is keyed by
+  the GLOBAL sample index, so the union of shards equals the single-GPU cache
+  bitwise (tests/test_gpu_cache.py::test_shard_union_equals_full_cache);
+* exchange: one all-gather of the packed 48-byte samples (NCCL over NVLink on the
+  GPU box; gloo in the CPU tests);
+* gather: query points are split into contiguous ranges; no reduction is needed
+  because every point is owned by exactly one rank.
+
+torch.distributed is plumbing here: the collective moves raw bytes of the
+library's device buffers, wrapped without copies through __cuda_array_interface__.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+SAMPLE_BYTES = 48  # struct CacheSample (csrc/internal.h)
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced [begin, end) of n units for `rank` of `world`."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return rank * n // world, (rank + 1) * n // world
+
+
+def shard_sizes(n: int, world: int) -> list[int]:
+    return [shard_range(n, r, world)[1] - shard_range(n, r, world)[0] for r in range(world)]
+
+
+class _DeviceBytes:
+    """Zero-copy view of a device buffer for torch.as_tensor."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes // 4,), "typestr": "<i4", "data": (ptr, False),
+                                         "version": 3}
+
+
+def allgather_bytes(dist, torch, local, sizes_bytes):
+    """All-gather variable-size int32 shards (padded to the largest) and concatenate."""
+    words = max(sizes_bytes) // 4
+    buf = torch.zeros(words, dtype=torch.int32, device=local.device)
+    buf[: local.numel()] = local
+    parts = [torch.empty_like(buf) for _ in sizes_bytes]
+    dist.all_gather(parts, buf)
+    return torch.cat([p[: s // 4] for p, s in zip(parts, sizes_bytes)])
+
+
+def generate_and_allgather(B, dist, torch, scene, problem, region, cfg, seed, rnd, rank, world, stats=None):
+    N = max(1, cfg.nBoundary)
+    s0, s1 = shard_range(N, rank, world)
+    shard = B.generate_boundary_cache(scene, problem, region, cfg, seed, rnd, begin=s0, end=s1, stats=stats)
+    ptr, nbytes = shard.packed()
+    local = torch.as_tensor(_DeviceBytes(ptr, nbytes), device="cuda") if nbytes else \
+        torch.empty(0, dtype=torch.int32, device="cuda")
+    full = allgather_bytes(dist, torch, local, [s * SAMPLE_BYTES for s in shard_sizes(N, world)])
+    torch.cuda.synchronize()
+    h = C.c_void_p()
+    B.api._check(B.lib().bvc_boundary_cache_from_packed(C.c_void_p(full.data_ptr()), N, 2, cfg.voronoi,
+                                                        C.c_double(0.0), C.byref(h)))
+    return B.BoundaryCache(h)
