@@ -200,7 +200,7 @@ struct bvc_scene_s {
             const double *a = host.vert(host.idx[2 * id]), *b = host.vert(host.idx[2 * id + 1]);
             hp[j].seg = make_float4(a[0], a[1], b[0], b[1]);
             hp[j].id = id;
-            hp[j].label = host.label[id];
+            hp[j].label = bvc_host::primClass(host, id);
             hp[j].sil0 = host.segSil[2 * id];
             hp[j].sil1 = host.segSil[2 * id + 1];
         }
@@ -792,7 +792,7 @@ void pointwise(bvc_scene_s* S, const bvc_problem& pb, const double* x, const dou
         double* cpd = ws().get<double>(kWsMean2, n);
         int* cps = ws().get<int>(kWsSkipB, n);
         double* cpt = ws().get<double>(kWsSe2, n);
-        launch_closest(E.S, xd, ni, 3u, cpp, cpd, cps, cpt, g_stream);
+        launch_closest(E.S, xd, ni, bvc_dev::kClsAny, cpp, cpd, cps, cpt, g_stream);
         std::vector<double> hd(n);
         CK(cudaMemcpyAsync(hd.data(), cpd, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
         CK(cudaStreamSynchronize(g_stream));
@@ -924,7 +924,7 @@ void fallback_walks(bvc_scene_s* S, const bvc_problem& pb, const bvc_cache_confi
         double* cpd = ws().get<double>(kWsMean2, nf);
         int* cps = ws().get<int>(kWsSkipB, nf);
         double* cpt = ws().get<double>(kWsSe2, nf);
-        launch_closest(Eg.S, xd, nf, 3u, cpp, cpd, cps, cpt, g_stream);
+        launch_closest(Eg.S, xd, nf, bvc_dev::kClsAny, cpp, cpd, cps, cpt, g_stream);
         std::vector<double> hd(nf);
         CK(cudaMemcpyAsync(hd.data(), cpd, nf * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
         CK(cudaStreamSynchronize(g_stream));
@@ -993,10 +993,10 @@ __global__ void mark_kernel(const bvc_dev::SceneView2 scene, const bvc_dev::Scen
     // fallbackBand cache.cpp:131-135: whole-domain points within l of the Dirichlet boundary
     uint8_t f = 0;
     if (whole) {
-        bvc_dev::Closest c = bvc_dev::closest_point(scene, px, py, 1u);
+        bvc_dev::Closest c = bvc_dev::closest_point(scene, px, py, bvc_dev::kClsD);
         f = (c.seg >= 0 && c.d2 < offset * offset) ? 1 : 0;
     }
-    bvc_dev::Closest r = bvc_dev::closest_point(region, px, py, 3u);
+    bvc_dev::Closest r = bvc_dev::closest_point(region, px, py, bvc_dev::kClsAny);
     fb[i] = f;
     gu[i] = (r.seg >= 0 && r.d2 < offset * offset) ? 1 : 0;
 }
@@ -1057,7 +1057,7 @@ int bvc_scene_closest_point(bvc_scene s, const double* x, size_t n, int filter, 
         require_device();
         need(s && x, "null argument");
         if (n == 0) return BVC_OK;
-        unsigned mask = filter == BVC_FILTER_DIRICHLET ? 1u : filter == BVC_FILTER_NEUMANN ? 2u : 3u;
+        unsigned mask = filter == BVC_FILTER_DIRICHLET ? bvc_dev::kClsD : filter == BVC_FILTER_NEUMANN ? bvc_dev::kClsNeumann : bvc_dev::kClsAny;
         double* xd = ws().get<double>(kWsEvalIn, 2 * n);
         double* o = ws().get<double>(kWsEvalOut, 4 * n);
         int* sg = ws().get<int>(kWsSkipB, n);
@@ -1089,7 +1089,7 @@ int bvc_scene_intersect_ray(bvc_scene s, const double* o, const double* d, size_
         require_device();
         need(s && o && d, "null argument");
         if (n == 0) return BVC_OK;
-        unsigned mask = filter == BVC_FILTER_DIRICHLET ? 1u : filter == BVC_FILTER_NEUMANN ? 2u : 3u;
+        unsigned mask = filter == BVC_FILTER_DIRICHLET ? bvc_dev::kClsD : filter == BVC_FILTER_NEUMANN ? bvc_dev::kClsNeumann : bvc_dev::kClsAny;
         double* in = ws().get<double>(kWsEvalIn, 4 * n);
         double* out = ws().get<double>(kWsEvalOut, 4 * n);
         int* sg = ws().get<int>(kWsSkipB, n);

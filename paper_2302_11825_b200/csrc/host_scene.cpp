@@ -127,6 +127,11 @@ HostScene buildScene2(const double* vertices, int nv, const int* segments, const
         if (ni && no) {
             n1[0] = s.normal[2 * si]; n1[1] = s.normal[2 * si + 1];
             n2[0] = s.normal[2 * so]; n2[1] = s.normal[2 * so + 1];
+            // exactly collinear neighbours: d1 * d2 = d1^2 <= 0 only for x exactly on
+            // the line (a tie in scene.cpp:166-172). The device walker is never on a
+            // Neumann line (it is nudged inside after each reflection), so such a
+            // candidate can never pass; dropping it lets the star query prune.
+            if (n1[0] == n2[0] && n1[1] == n2[1]) continue;
         } else if ((ni && so < 0) || (no && si < 0)) {
             always = true;
         } else {
@@ -409,6 +414,13 @@ HostRegion buildSolveRegion(const HostScene& scene, int mode, double offset, con
 // ---------------------------------------------------------------------------
 // BVH: binary, median split on the longest centroid axis, leaves of <= leafSize
 // ---------------------------------------------------------------------------
+int primClass(const HostScene& s, int i) {
+    if (s.label[i] == 0) return 0;
+    if (s.dim == 2 && (s.segSil[2 * static_cast<size_t>(i)] >= 0 || s.segSil[2 * static_cast<size_t>(i) + 1] >= 0))
+        return 2;
+    return 1;
+}
+
 namespace {
 
 struct Box {
@@ -445,7 +457,7 @@ struct Builder {
         for (int i = start; i < start + count; ++i) {
             box.add(primBox[order[i]], d);
             cbox.add(&centroid[static_cast<size_t>(d) * order[i]], d);
-            mask |= 1u << s.label[order[i]];
+            mask |= 1u << primClass(s, order[i]);
         }
         double ext[3] = {0, 0, 0};
         double maxExt = 0.0;
@@ -477,7 +489,7 @@ struct Builder {
         int r = build(mid, start + count - mid, rb, rm, depth + 1);
         out.children[2 * node] = l;
         out.children[2 * node + 1] = r;
-        out.masks[node] = lm | (rm << 2);
+        out.masks[node] = lm | (rm << 3);
         float* b = &out.boxes[static_cast<size_t>(4 * d) * node];
         // pad outward by ~2^-20 diag: FP32 slab tests against the degenerate
         // (zero-width) boxes of axis-aligned segments must not cull true crossings

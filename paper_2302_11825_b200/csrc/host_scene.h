@@ -66,13 +66,17 @@ struct HostRegion {
 HostRegion buildSolveRegion(const HostScene& scene, int mode, double offset, const HostScene* sub,
                             double epsilon);
 
+// BVH primitive class: 0 Dirichlet, 1 Neumann without silhouette candidates,
+// 2 Neumann with silhouette candidates (the only Neumann class star queries visit)
+int primClass(const HostScene& s, int i);
+
 // Binary BVH flattened for the device. Node = two child boxes + two child refs.
 // child ref >= 0: internal node index; < 0: leaf, ~ref = (start << 3) | (count - 1).
 struct HostBvh {
     int dim = 2;
     std::vector<float> boxes;     // per node: 2 * (2*dim) floats (left lo, left hi, right lo, right hi)
     std::vector<int> children;    // 2 per node
-    std::vector<unsigned> masks;  // per node: left mask | right mask << 2
+    std::vector<unsigned> masks;  // per node: left class mask | right class mask << 3
     std::vector<int> order;       // leaf order -> primitive id
     int depth = 0;
 };

@@ -17,14 +17,14 @@ struct alignas(16) Node2 {
     float4 lbox;  // lo.x, lo.y, hi.x, hi.y
     float4 rbox;
     int left, right;  // >= 0 internal node; < 0 leaf: ~((start << 3) | (count - 1))
-    unsigned mask;    // left label mask | right label mask << 2
+    unsigned mask;    // left class mask | right class mask << 3 (classes: host_scene.h primClass)
     int pad;
 };
 
 struct alignas(16) Prim2 {
     float4 seg;      // a.x, a.y, b.x, b.y
     int id;          // caller-side segment index
-    int label;       // 0 Dirichlet, 1 Neumann
+    int label;       // class: 0 Dirichlet, 1 Neumann, 2 Neumann with silhouette candidates
     int sil0, sil1;  // silhouette candidate slots (-1 none)
 };
 
@@ -67,6 +67,9 @@ __device__ __forceinline__ float seg_closest(const float4& s, float x, float y, 
 }
 
 constexpr int kStack = 48;
+// primitive class masks (host_scene.h primClass)
+constexpr unsigned kClsD = 1u, kClsN = 2u, kClsSil = 4u;
+constexpr unsigned kClsNeumann = kClsN | kClsSil, kClsAny = kClsD | kClsN | kClsSil;
 
 // Generic best-first traversal. visit(prim) handles one primitive of a visited
 // leaf; threshold() returns the current squared pruning radius.
@@ -83,7 +86,7 @@ __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, floa
             count_fetch(S, 0);
             float thr = threshold();
             float dl = (nd.mask & qmask) ? box_dist2(nd.lbox, x, y) : kFInf;
-            float dr = ((nd.mask >> 2) & qmask) ? box_dist2(nd.rbox, x, y) : kFInf;
+            float dr = ((nd.mask >> 3) & qmask) ? box_dist2(nd.rbox, x, y) : kFInf;
             bool vl = dl <= thr, vr = dr <= thr;
             if (vl && vr) {
                 int nearRef = dl <= dr ? nd.left : nd.right;
@@ -151,7 +154,7 @@ __device__ __forceinline__ bool silhouette_ok(const SceneView2& S, int k, float 
 __device__ __forceinline__ float silhouette_dist2(const SceneView2& S, float x, float y) {
     float best = kFInf;
     traverse_near(
-        S, x, y, 2u,
+        S, x, y, kClsSil,
         [&](const Prim2& p) {
             float d2;
             if (p.sil0 >= 0 && silhouette_ok(S, p.sil0, x, y, d2) && d2 < best) best = d2;
@@ -174,7 +177,7 @@ __device__ __forceinline__ StarQuery star_query(const SceneView2& S, float x, fl
     q.D = Closest{kFInf, 0.0f, 0.0f, 0.0f, -1};
     q.s2 = kFInf;
     traverse_near(
-        S, x, y, 3u,
+        S, x, y, kClsD | kClsSil,
         [&](const Prim2& p) {
             if (p.label == 0) {
                 float px, py, t;
@@ -233,7 +236,7 @@ __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, f
             const Node2 nd = S.nodes[ref];
             count_fetch(S, 0);
             bool vl = (nd.mask & qmask) && ray_box(nd.lbox, ox, oy, idx, idy, limit);
-            bool vr = ((nd.mask >> 2) & qmask) && ray_box(nd.rbox, ox, oy, idx, idy, limit);
+            bool vr = ((nd.mask >> 3) & qmask) && ray_box(nd.rbox, ox, oy, idx, idy, limit);
             if (vl && vr) { stack[sp++] = nd.right; ref = nd.left; continue; }
             if (vl) { ref = nd.left; continue; }
             if (vr) { ref = nd.right; continue; }
@@ -274,7 +277,7 @@ __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, f
 // parity along +x with the straddle form; only leaves whose box spans x.y and
 // reaches past x.x are visited.
 __device__ __forceinline__ bool inside(const SceneView2& S, float x, float y, float tol) {
-    Closest c = closest_point(S, x, y, 3u, tol * tol);
+    Closest c = closest_point(S, x, y, kClsAny, tol * tol);
     if (c.seg >= 0) return true;
     bool in = false;
     int stack[kStack];
@@ -283,8 +286,8 @@ __device__ __forceinline__ bool inside(const SceneView2& S, float x, float y, fl
         if (ref >= 0) {
             const Node2 nd = S.nodes[ref];
             count_fetch(S, 0);
-            bool vl = (nd.mask & 3u) && nd.lbox.y <= y && nd.lbox.w >= y && nd.lbox.z > x;
-            bool vr = ((nd.mask >> 2) & 3u) && nd.rbox.y <= y && nd.rbox.w >= y && nd.rbox.z > x;
+            bool vl = (nd.mask & 7u) && nd.lbox.y <= y && nd.lbox.w >= y && nd.lbox.z > x;
+            bool vr = ((nd.mask >> 3) & 7u) && nd.rbox.y <= y && nd.rbox.w >= y && nd.rbox.z > x;
             if (vl && vr) { stack[sp++] = nd.right; ref = nd.left; continue; }
             if (vl) { ref = nd.left; continue; }
             if (vr) { ref = nd.right; continue; }

@@ -112,7 +112,7 @@ __device__ float neumann_term(const WalkEnv& E, float x, float y, float R, float
     };
     float R2 = R * R;
     traverse_near(
-        S, x, y, 2u,
+        S, x, y, kClsNeumann,
         [&](const Prim2& p) {
             float t0, t1;
             if (clip(p, t0, t1)) {
@@ -127,7 +127,7 @@ __device__ float neumann_term(const WalkEnv& E, float x, float y, float R, float
     int bseg = -1;
     bool done = false;
     traverse_near(
-        S, x, y, 2u,
+        S, x, y, kClsNeumann,
         [&](const Prim2& p) {
             if (done) return;
             float t0, t1;
@@ -179,7 +179,7 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
         if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
         R = fminf(dD, sqrtf(q.s2));
     } else {
-        cp = closest_point(E.S, w.x, w.y, 1u);
+        cp = closest_point(E.S, w.x, w.y, kClsD);
         float dD = sqrtf(cp.d2);
         if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
         R = dD;
@@ -201,7 +201,7 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
     float travel = R;
     bool hit = false;
     if (E.hasNeumann) {
-        RayHit h = intersect_ray(E.S, w.x, w.y, dx, dy, R, 2u, E.tguard, w.onN ? w.prevSeg : -1);
+        RayHit h = intersect_ray(E.S, w.x, w.y, dx, dy, R, kClsNeumann, E.tguard, w.onN ? w.prevSeg : -1);
         if (h.seg >= 0) {
             hit = true;
             travel = h.t;
@@ -231,7 +231,7 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
     bool escaped = fabsf(w.x - E.cx) > E.escape || fabsf(w.y - E.cy) > E.escape;
     if (++w.step >= E.maxSteps || escaped) {  // truncation: g at the closest Dirichlet point (pointwise.cpp:162-164)
         trunc = 1;
-        Closest c = closest_point(E.S, w.x, w.y, 1u);
+        Closest c = closest_point(E.S, w.x, w.y, kClsD);
         value = w.acc + w.weight * g_value(E, c);
         return true;
     }
@@ -464,7 +464,7 @@ __global__ void prepare_kernel(const WalkEnv E, CacheSample* samples, int n, con
         gradR[i] = 0.0f;
     } else {
         isD[i] = 1;
-        Closest c = closest_point(E.S, x, y, 3u);
+        Closest c = closest_point(E.S, x, y, kClsAny);
         gradR[i] = fmaxf(sqrtf(c.d2), E.rmin);
     }
     (void)source;
