@@ -287,19 +287,21 @@ def e2e_measure(B, c, scene, region, points, args, world):
         pts = B.EvaluationPoints(points)               # H2D from host memory
         B.mark_evaluation_points(scene, region, c.cache, pts)
         B.update_solution(scene, c.problem, region, c.cache, pts, c.seed, 500 + k, gradients=bool(c.gradients))
-        st = pts.download()                            # D2H of the running sums
-        u = pts.solution(st)
+        if c.gradients:
+            u, g = pts.read_solution(gradient=True)    # D2H of u and grad u
+        else:
+            u = pts.read_solution(gradient=False)
         torch.cuda.synchronize()
         if k:
             times.append(time.perf_counter() - t0)
         assert np.all(np.isfinite(u))
     N, M = c.cache.nBoundary, (c.cache.nSource if c.problem.f.kind else 0)
-    k_active = int((~st["fallback"]).sum())
+    k_active = int((~pts.download()["fallback"]).sum())
     t = float(np.mean(times))
-    d2h = len(points) * (8 * 2 + 8 * 2 + 8 * 4 + 8 * 4 + 8 * 3 + 8 * 2 + 2)  # the downloaded state arrays
+    d2h = len(points) * 8 * (1 + (2 if c.gradients else 0))
     return {"value": k_active * world * (N + M) / t, "unit": "interactions/s", "ms_per_step": t * 1e3,
             "h2d_bytes_per_step": int(points.size * 8), "d2h_bytes_per_step": int(d2h),
-            "note": "wall clock per call incl. point upload, classification, round and state download"}
+            "note": "wall clock per call: point upload (H2D), classification, one round, u/grad-u readout (D2H)"}
 
 
 def reference_round_estimate(c, sample_s=20.0, threads=0):

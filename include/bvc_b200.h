@@ -237,6 +237,9 @@ int bvc_points_create(const double* x, size_t n, int dim, bvc_eval_points* out);
 int bvc_points_destroy(bvc_eval_points pts);
 int bvc_points_download(bvc_eval_points pts, bvc_point_state* host); /* fills non-NULL arrays */
 int bvc_points_upload(bvc_eval_points pts, const bvc_point_state* host); /* non-NULL arrays */
+/* EvaluationPoint::solution() / gradient() (cache.h:91-105) evaluated on the device;
+   u: count doubles, grad: dim*count doubles (either may be NULL) */
+int bvc_points_solution(bvc_eval_points pts, double* u, double* grad);
 int bvc_points_reset(bvc_eval_points pts);  /* zero all running sums */
 /* markEvaluationPoints (cache.h:154; cache.cpp:263-276) */
 int bvc_mark_evaluation_points(bvc_scene scene, bvc_region region, const bvc_cache_config* cfg,

@@ -25,7 +25,7 @@ SYMBOLS = (
     "bvc_scene_create bvc_scene_create_mesh3 bvc_scene_destroy bvc_scene_info bvc_scene_closest_point "
     "bvc_scene_silhouette_distance bvc_scene_intersect_ray bvc_scene_inside bvc_region_build bvc_region_destroy "
     "bvc_region_info bvc_region_export bvc_region_boundary bvc_points_create bvc_points_destroy bvc_points_download "
-    "bvc_points_upload bvc_points_reset bvc_mark_evaluation_points bvc_generate_boundary_cache "
+    "bvc_points_upload bvc_points_solution bvc_points_reset bvc_mark_evaluation_points bvc_generate_boundary_cache "
     "bvc_generate_boundary_cache_shard bvc_generate_source_cache bvc_boundary_cache_create bvc_boundary_cache_size "
     "bvc_boundary_cache_download bvc_boundary_cache_packed bvc_boundary_cache_from_packed bvc_boundary_cache_destroy "
     "bvc_source_cache_create bvc_source_cache_size bvc_source_cache_download bvc_source_cache_destroy "
@@ -333,6 +333,14 @@ class EvaluationPoints:
 
     def reset(self):
         _check(lib().bvc_points_reset(self.h))
+
+    def read_solution(self, gradient=True):
+        """u (and grad u) computed on the device (EvaluationPoint::solution/gradient, cache.h:91-105);
+        only these arrays cross to the host."""
+        u = np.zeros(self.n)
+        g = np.zeros((self.n, self.dim)) if gradient else None
+        _check(lib().bvc_points_solution(self.h, _ptr(u), _ptr(g) if g is not None else None))
+        return (u, g) if gradient else u
 
     def solution(self, st=None):
         """EvaluationPoint::solution() (cache.h:91-96)."""

@@ -54,6 +54,19 @@ void require_device() {
     if (!state) throw Error(bvc_host::kNoDevice, "no CUDA device: the BVC path has no CPU fallback");
 }
 
+void ensure_pool() {
+    static int device = -1;
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d == device) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    device = d;
+}
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -61,12 +74,15 @@ struct DevBuf {
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    ~DevBuf() { if (p) cudaFree(p); }
+    ~DevBuf() { if (p) cudaFreeAsync(p, g_stream); }
+    // stream-ordered allocations from a pool that retains freed memory, so that
+    // per-call handles (evaluation points, caches) do not pay cudaMalloc/cudaFree
     void resize(size_t count) {
         if (count > cap) {
-            if (p) cudaFree(p);
+            ensure_pool();
+            if (p) CK(cudaFreeAsync(p, g_stream));
             p = nullptr;
-            CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+            CK(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), g_stream));
             cap = count;
         }
         n = count;
@@ -100,7 +116,7 @@ enum Slot {
     kWsSamplesTmp, kWsStartU, kWsIsD, kWsGradR, kWsOutside, kWsDIdx, kWsCount, kWsXD, kWsND, kWsRD, kWsGidD, kWsOutU,
     kWsOutD, kWsCounter, kWsSteps, kWsTrunc, kWsFailed, kWsPack, kWsPart, kWsSkipB, kWsSkipS, kWsPts, kWsCtr,
     kWsSortKeysIn, kWsSortKeysOut, kWsSortValsIn, kWsSortTemp, kWsMean, kWsSe, kWsTruncPt, kWsHost1, kWsRegion,
-    kWsMean2, kWsSe2, kWsGidU, kWsSrcTmp, kWsSrcFlag, kWsEvalIn, kWsEvalOut
+    kWsMean2, kWsSe2, kWsGidU, kWsSrcTmp, kWsSrcFlag, kWsEvalIn, kWsEvalOut, kWsTileBox, kWsUnitCtr
 };
 
 int fail(const std::exception& e) {
@@ -728,7 +744,8 @@ void splat(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_points_s* P,
     if (N + M > 0)
         launch_gather(kind, plan, pack, N, M, P->xs.p + static_cast<size_t>(dim) * begin, K, dim,
                       static_cast<float>(cfg.kernel.sigma), static_cast<float>(cfg.coincidenceTol), val, grad, part,
-                      skipB, skipS, g_stream);
+                      skipB, skipS, ws().get<float4>(kWsTileBox, 2 * static_cast<size_t>((N + 255) / 256 + (M + 255) / 256 + 1)),
+                      ws().get<unsigned>(kWsUnitCtr, 1), g_stream);
     else
         CK(cudaMemsetAsync(part, 0, sizeof(double), g_stream));
     if (N + M > 0)
@@ -985,6 +1002,30 @@ void zero_points(bvc_eval_points_s* P) {
     P->gwalkCount.zero(); P->skipped.zero();
 }
 
+// EvaluationPoint::solution() / gradient() (cache.h:91-105)
+__global__ void solution_kernel(int n, int d, const uint8_t* fb, const double* bsum, const double* ssum,
+                                const long long* nb, const long long* ms, const double* bgsum, const double* sgsum,
+                                const long long* nbg, const long long* msg, const double* walkSum,
+                                const long long* walkCount, const double* gws, const long long* gwc, double* u,
+                                double* g) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (fb[i]) {
+        u[i] = walkCount[i] > 0 ? walkSum[i] / walkCount[i] : 0.0;
+        for (int k = 0; k < d; ++k) g[static_cast<size_t>(d) * i + k] = gwc[i] > 0 ? gws[static_cast<size_t>(d) * i + k] / gwc[i] : 0.0;
+        return;
+    }
+    double v = nb[i] > 0 ? bsum[i] / nb[i] : 0.0;
+    if (ms[i] > 0) v += ssum[i] / ms[i];
+    u[i] = v;
+    for (int k = 0; k < d; ++k) {
+        size_t j = static_cast<size_t>(d) * i + k;
+        double w = nbg[i] > 0 ? bgsum[j] / nbg[i] : 0.0;
+        if (msg[i] > 0) w += sgsum[j] / msg[i];
+        g[j] = w;
+    }
+}
+
 __global__ void mark_kernel(const bvc_dev::SceneView2 scene, const bvc_dev::SceneView2 region, const double* x, int n,
                             float offset, int whole, uint8_t* fb, uint8_t* gu) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1207,6 +1248,24 @@ int bvc_points_download(bvc_eval_points p, bvc_point_state* h) {
         CK(cudaStreamSynchronize(g_stream));
     })
 }
+int bvc_points_solution(bvc_eval_points p, double* u, double* grad) {
+    API({
+        require_device();
+        need(p && (u || grad), "null argument");
+        size_t n = p->n;
+        if (n == 0) return BVC_OK;
+        int d = p->dim;
+        double* o = ws().get<double>(kWsEvalOut, (1 + d) * n);
+        solution_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, g_stream>>>(
+            static_cast<int>(n), d, p->fallback.p, p->bsum.p, p->ssum.p, p->nb.p, p->ms.p, p->bgsum.p, p->sgsum.p,
+            p->nbg.p, p->msg.p, p->walkSum.p, p->walkCount.p, p->gwalkSum.p, p->gwalkCount.p, o, o + n);
+        count_launch();
+        if (u) CK(cudaMemcpyAsync(u, o, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        if (grad) CK(cudaMemcpyAsync(grad, o + n, d * n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+    })
+}
+
 int bvc_points_upload(bvc_eval_points p, const bvc_point_state* h) {
     API({
         require_device();

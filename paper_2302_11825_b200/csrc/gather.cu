@@ -88,13 +88,13 @@ __device__ __forceinline__ void k0_q(float t, float& K0, float& Q) {
     }
 }
 
-template <int KIND, bool SRC, bool VAL, bool GRAD>
+template <int KIND, bool SRC, bool VAL, bool GRAD, bool TRACK = false>
 __device__ __forceinline__ void pair(const float4 a, const float4 b, float px, float py, float pz, float sigma,
                                      float s, Acc& acc, float& mn) {
     if constexpr (KIND == kLap2 || KIND == kScr2) {
         float dx = a.x - px, dy = a.y - py;
         float r2 = fmaf(dx, dx, dy * dy);
-        mn = fminf(mn, r2);
+        if constexpr (TRACK) mn = fminf(mn, r2);
         if constexpr (KIND == kLap2) {
             float ir2 = f_rcp(r2);
             if constexpr (!SRC) {
@@ -146,7 +146,7 @@ __device__ __forceinline__ void pair(const float4 a, const float4 b, float px, f
         // 3D: boundary payload a = (zx, zy, zz, nx), b = (ny, nz, A, B); source a = (y, C)
         float dx = a.x - px, dy = a.y - py, dz = a.z - pz;
         float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        mn = fminf(mn, r2);
+        if constexpr (TRACK) mn = fminf(mn, r2);
         float ir = f_rsq(r2);
         float ir2 = ir * ir, ir3 = ir2 * ir;
         float e = 1.0f, Q = 1.0f;
@@ -191,11 +191,14 @@ struct Params {
     int chunk;               // samples per chunk (multiple of kTS)
     int chunksB, chunksS;    // chunks over boundary / source samples
     int tiles;               // point tiles
-    float sigma, s, tol2;
+    float sigma, s, tol, tol2;
     double* part;            // [(chunksB + chunksS)][comps][K]
     int comps;               // 1 (value) + dim (gradient) as enabled
     int* skipB;              // [K]
     int* skipS;
+    const float4* tileBox;   // per shared-memory tile: lo (x, y, z), hi (x, y, z) of its samples
+    int tilesB;              // boundary tiles (source tiles follow)
+    unsigned* unitCounter;   // dynamic work-unit queue (zeroed per launch)
 };
 
 // slow path: recompute one point's tile partial, skipping near-coincident samples
@@ -206,9 +209,21 @@ __device__ void tile_slow(const float4* sm, int cnt, float px, float py, float p
     for (int j = 0; j < cnt; ++j) {
         float4 a = sm[2 * j], b = sm[2 * j + 1];
         float dx = a.x - px, dy = a.y - py, dz = (KIND == kLap3 || KIND == kScr3) ? a.z - pz : 0.0f;
-        if (dx * dx + dy * dy + dz * dz < P.tol2) { ++skips; continue; }
+        if (dx * dx + dy * dy + dz * dz < P.tol2) { ++skips; continue; }  // cache.cpp:436-440
         float mn = 0.f;
         pair<KIND, SRC, VAL, GRAD>(a, b, px, py, pz, P.sigma, P.s, acc, mn);
+    }
+}
+
+template <int KIND, bool SRC, bool VAL, bool GRAD, bool TRACK>
+__device__ __forceinline__ void tile_loop(const float4* S, int cnt, const float* px, const float* py, const float* pz,
+                                          const Params& P, Acc* acc, float* mn) {
+#pragma unroll 2
+    for (int j = 0; j < cnt; ++j) {
+        const float4 a = S[2 * j], b = S[2 * j + 1];
+#pragma unroll
+        for (int q = 0; q < kQ; ++q)
+            pair<KIND, SRC, VAL, GRAD, TRACK>(a, b, px[q], py[q], pz[q], P.sigma, P.s, acc[q], mn[q]);
     }
 }
 
@@ -216,6 +231,7 @@ template <int KIND, bool VAL, bool GRAD>
 __global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
     __shared__ __align__(128) float4 sm[2][2 * kTS];
     __shared__ __align__(8) uint64_t bar[2];
+    __shared__ int sUnit;
     const int tid = threadIdx.x;
     const int units = P.tiles * (P.chunksB + P.chunksS);
     constexpr bool D3 = (KIND == kLap3 || KIND == kScr3);
@@ -226,7 +242,9 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
     }
     __syncthreads();
     unsigned phase[2] = {0u, 0u};
-    for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
+    // units are equal-cost (point tile x sample chunk); CTAs take them from a queue
+    // so the last partial wave is filled by whichever CTAs finish first
+    for (int unit = blockIdx.x; unit < units;) {
         const int chunkId = unit % (P.chunksB + P.chunksS);
         const int tile = unit / (P.chunksB + P.chunksS);
         const bool src = chunkId >= P.chunksB;
@@ -262,6 +280,17 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
         for (int it = 0; it < nT; ++it) {
             const int st = it & 1;
             const int s0 = c0 + it * kTS, cnt = min(kTS, cEnd - s0);
+            // near-coincidence (r < tol) is only possible for points inside the tile's
+            // sample box grown by tol; those (point, tile) pairs take the exact slow path
+            const int tb = src ? P.tilesB + (s0 - P.N) / kTS : s0 / kTS;
+            const float4 blo = P.tileBox[2 * tb], bhi = P.tileBox[2 * tb + 1];
+            bool near = false;
+#pragma unroll
+            for (int q = 0; q < kQ; ++q)
+                near |= pidx[q] < P.K && px[q] >= blo.x - P.tol && px[q] <= bhi.x + P.tol && py[q] >= blo.y - P.tol &&
+                        py[q] <= bhi.y + P.tol && (!D3 || (pz[q] >= blo.z - P.tol && pz[q] <= bhi.z + P.tol));
+            // warp-uniform: warps with a point inside the tile box track min r^2 per pair
+            const bool track = __any_sync(0xffffffffu, near);
             mbar_wait(&bar[st], phase[st]);
             phase[st] ^= 1u;
             Acc acc[kQ];
@@ -270,19 +299,11 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
             for (int q = 0; q < kQ; ++q) { acc[q] = Acc{0.f, 0.f, 0.f, 0.f}; mn[q] = 3.0e38f; }
             const float4* S = sm[st];
             if (!src) {
-#pragma unroll 2
-                for (int j = 0; j < cnt; ++j) {
-                    const float4 a = S[2 * j], b = S[2 * j + 1];
-#pragma unroll
-                    for (int q = 0; q < kQ; ++q) pair<KIND, false, VAL, GRAD>(a, b, px[q], py[q], pz[q], P.sigma, P.s, acc[q], mn[q]);
-                }
+                if (track) tile_loop<KIND, false, VAL, GRAD, true>(S, cnt, px, py, pz, P, acc, mn);
+                else tile_loop<KIND, false, VAL, GRAD, false>(S, cnt, px, py, pz, P, acc, mn);
             } else {
-#pragma unroll 2
-                for (int j = 0; j < cnt; ++j) {
-                    const float4 a = S[2 * j], b = S[2 * j + 1];
-#pragma unroll
-                    for (int q = 0; q < kQ; ++q) pair<KIND, true, VAL, GRAD>(a, b, px[q], py[q], pz[q], P.sigma, P.s, acc[q], mn[q]);
-                }
+                if (track) tile_loop<KIND, true, VAL, GRAD, true>(S, cnt, px, py, pz, P, acc, mn);
+                else tile_loop<KIND, true, VAL, GRAD, false>(S, cnt, px, py, pz, P, acc, mn);
             }
 #pragma unroll
             for (int q = 0; q < kQ; ++q) {
@@ -317,6 +338,34 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
             }
             if (skips[q]) atomicAdd(src ? P.skipS + i : P.skipB + i, skips[q]);
         }
+        if (tid == 0) sUnit = static_cast<int>(gridDim.x + atomicAdd(P.unitCounter, 1u));
+        __syncthreads();
+        unit = sUnit;
+        __syncthreads();
+    }
+}
+
+// bounding box of each 256-sample tile (one warp per tile)
+__global__ void tile_box_kernel(const float4* pack, int N, int M, int kind, float4* box) {
+    int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    int tilesB = (N + kTS - 1) / kTS, tilesS = (M + kTS - 1) / kTS;
+    if (warp >= tilesB + tilesS) return;
+    int s0 = warp < tilesB ? warp * kTS : N + (warp - tilesB) * kTS;
+    int s1 = warp < tilesB ? min(s0 + kTS, N) : min(s0 + kTS, N + M);
+    float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
+    for (int j = s0 + lane; j < s1; j += 32) {
+        float4 a = pack[2 * j];
+        float c[3] = {a.x, a.y, (kind == kLap3 || kind == kScr3) ? a.z : 0.f};
+        for (int k = 0; k < 3; ++k) { lo[k] = fminf(lo[k], c[k]); hi[k] = fmaxf(hi[k], c[k]); }
+    }
+    for (int o = 16; o > 0; o >>= 1)
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = fminf(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+            hi[k] = fmaxf(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+        }
+    if (lane == 0) {
+        box[2 * warp] = make_float4(lo[0], lo[1], lo[2], 0.f);
+        box[2 * warp + 1] = make_float4(hi[0], hi[1], hi[2], 0.f);
     }
 }
 
@@ -542,7 +591,7 @@ GatherPlan plan_gather(int kind, int K, int N, int M, bool val, bool grad) {
 
 void launch_gather(int kind, const GatherPlan& g, const float4* pack, int N, int M, const float* px, int K, int dim,
                    float sigma, float tol, bool val, bool grad, double* part, int* skipB, int* skipS,
-                   cudaStream_t st) {
+                   float4* tileBox, unsigned* unitCounter, cudaStream_t st) {
     if (K <= 0 || (N + M) <= 0) return;
     Params P;
     P.pack = pack;
@@ -557,7 +606,17 @@ void launch_gather(int kind, const GatherPlan& g, const float4* pack, int N, int
     P.tiles = g.tiles;
     P.sigma = sigma;
     P.s = sqrtf(sigma);
+    P.tol = tol;
     P.tol2 = tol * tol;
+    P.tilesB = (N + kTS - 1) / kTS;
+    P.tileBox = tileBox;
+    P.unitCounter = unitCounter;
+    {
+        int tiles = P.tilesB + (M + kTS - 1) / kTS;
+        tile_box_kernel<<<blocks(static_cast<long long>(tiles) * 32, 256), 256, 0, st>>>(pack, N, M, kind, tileBox);
+        count_launch();
+        cudaMemsetAsync(unitCounter, 0, sizeof(unsigned), st);
+    }
     P.part = part;
     P.comps = g.comps;
     P.skipB = skipB;

@@ -32,7 +32,7 @@ void eval_bessel(int which, const double* t, int count, double* out, cudaStream_
 void gather_points(const double* x, const int* order, int K, int dim, float* out, cudaStream_t st);
 void launch_gather(int kind, const GatherPlan& g, const float4* pack, int N, int M, const float* px, int K, int dim,
                    float sigma, float tol, bool val, bool grad, double* part, int* skipB, int* skipS,
-                   cudaStream_t st);
+                   float4* tileBox, unsigned* unitCounter, cudaStream_t st);
 void launch_finalize(const double* part, const GatherPlan& g, int K, const int* order, int N, int M, bool val,
                      bool grad, int dim, const int* skipB, const int* skipS, const PointsDev& pts, cudaStream_t st);
 
