@@ -216,6 +216,24 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
+def ncu_traffic(kernel="walk"):
+    """DRAM bytes (read + write) per launch from the latest committed ncu --set full
+    summary (profiles/<round>_<kernel>_ncu.txt), or None."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_{kernel}_ncu.txt")))
+    if not files:
+        return None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total = 0.0
+    for line in open(files[-1]):
+        for key in ("dram__bytes_read.sum =", "dram__bytes_write.sum ="):
+            if line.startswith(key):
+                parts = line.split("=")[1].split()
+                total += float(parts[0]) * scale.get(parts[1] if len(parts) > 1 else "byte", 1.0)
+    return {"bytes": total, "source": os.path.relpath(files[-1], ROOT)}
+
+
 def phase_breakdown(B, c, scene, region, pts, args):
     """Per-kernel timings with CUDA events (outside the timed steps) and the roofline."""
     import torch
@@ -263,7 +281,10 @@ def phase_breakdown(B, c, scene, region, pts, args):
         "phases_s": {"cache_generation": t_gen, "gather": t_gather},
         "roofline": {"bound": "hbm", "kernel": "bvc walk_kernel (cache generation)", "achieved": achieved,
                      "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s",
-                     "frac": achieved / float(peaks.get("hbm_gbs", 6650.0)), "traffic": None,
+                     "frac": achieved / float(peaks.get("hbm_gbs", 6650.0)),
+                     "traffic": (ncu_traffic("walk") or {}).get("bytes"),
+                     "traffic_source": (ncu_traffic("walk") or {}).get("source"),
+                     "algorithmic_bytes_per_launch": walk_bytes,
                      "algorithmic_bytes_per_step": bytes_per_step,
                      "node_fetches_per_step": prof["node_fetches"] / steps,
                      "prim_fetches_per_step": prof["prim_fetches"] / steps, "peak_source": peaks["source"],

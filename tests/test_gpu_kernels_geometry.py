@@ -52,8 +52,11 @@ def test_kernel_formulas_fp32_vs_reference(golden, name):
     for c in range(ref.shape[1]):
         err = np.abs(got[:, c] - ref[:, c]) / scales[c]
         assert err.max() < 2e-5, (name, c, err.max())
-    # and against the reference's outputs on the unrounded inputs, to input rounding
-    assert np.max(np.abs(got - g[name + "_out"]) / (np.abs(g[name + "_out"]) + 1e-3)) < 1e-3
+    # and against the reference's own outputs on the unrounded inputs (the FP32
+    # rounding of x and y perturbs a quantity by ~ulp(x)/r of its magnitude)
+    gold = g[name + "_out"]
+    for c in range(gold.shape[1]):
+        assert np.max(np.abs(got[:, c] - gold[:, c]) / scales[c]) < 1e-3, (name, c)
 
 
 @pytest.mark.parametrize("k", [0, 1, 2])
