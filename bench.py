@@ -94,6 +94,25 @@ class ClockSampler:
 
 def build_problem(cfg_id, B, configs, abi):
     c = configs.CONFIGS[cfg_id]()
+    if c.extra.get("dim") == 3:
+        if "components" in c.extra:
+            # soup of 8 closed meshes: the walks and the cache live on its outer shell;
+            # inside the union = inside any component
+            tris, labels = configs.soup_shell(c)
+            keep = np.zeros(len(c.points), bool)
+            for comp in configs.soup_components(c):
+                keep |= comp.inside(c.points)
+            c.extra["shell_triangles"] = int(len(tris))
+            c.segments, c.labels = tris, labels
+            scene = B.Scene.mesh3(c.vertices, c.segments, c.labels)
+        else:
+            scene = B.Scene.mesh3(c.vertices, c.segments, c.labels)
+            keep = scene.inside(c.points)
+        region = B.SolveRegion(scene, offset=c.region_offset, epsilon=c.epsilon)
+        c.points = c.points[keep][: c.extra["n_points"]]
+        c.dim = 3
+        return c, scene, region
+    c.dim = 2
     scene = B.Scene(c.vertices, c.segments, c.labels)
     if c.region_mode == abi.REGION_SUBDOMAIN:
         sub = B.Scene(c.sub_vertices, c.sub_segments, np.zeros(len(c.sub_segments), np.int32))
@@ -129,7 +148,7 @@ def run_gpu(args):
     # points of this rank: a contiguous slice (the spatial sort keeps shards compact)
     lo_p, hi_p = rank * K_all // world, (rank + 1) * K_all // world
     my_points = c.points[lo_p:hi_p]
-    pts = B.EvaluationPoints(my_points)
+    pts = B.EvaluationPoints(my_points, c.dim)
     B.mark_evaluation_points(scene, region, cfg, pts)
     st0 = pts.download()
     k_active = int((~st0["fallback"]).sum())
@@ -272,7 +291,10 @@ def phase_breakdown(B, c, scene, region, pts, args):
     sms = props.multi_processor_count
     f_sm = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     per_pair = {"lap2_u": (9, 2), "lap2_ugrad": (18, 2), "scr2_ugrad": (50, 3), "lap3_u": (14, 1), "scr3_u": (20, 2)}
-    key = ("scr2_ugrad" if c.problem.kernel.kind else "lap2_ugrad") if c.gradients else "lap2_u"
+    if c.dim == 3:
+        key = "scr3_u" if c.problem.kernel.kind else "lap3_u"
+    else:
+        key = ("scr2_ugrad" if c.problem.kernel.kind else "lap2_ugrad") if c.gradients else "lap2_u"
     F, S = per_pair[key]
     bound = sms * f_sm / max(F / 128.0, S / 16.0)
     gather_rate = pairs / t_gather
@@ -305,7 +327,7 @@ def e2e_measure(B, c, scene, region, points, args, world):
     for k in range(reps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        pts = B.EvaluationPoints(points)               # H2D from host memory
+        pts = B.EvaluationPoints(points, c.dim)        # H2D from host memory
         B.mark_evaluation_points(scene, region, c.cache, pts)
         B.update_solution(scene, c.problem, region, c.cache, pts, c.seed, 500 + k, gradients=bool(c.gradients))
         if c.gradients:
@@ -385,8 +407,39 @@ def reference_round_estimate(c, sample_s=20.0, threads=0):
             "round_seconds_extrapolated": t_round}
 
 
+def port_gather_estimate_3d(c, sample_s):
+    """3D has no reference path (pointwise.cpp:23 throws for dim != 2). The CPU number is
+    the restated 3D splat loop (oracle/bvc_oracle.c, the reference's 3D kernel templates
+    kernels.h:78-129) on a point subset against a full-size synthetic cache; walks have
+    no CPU counterpart and are not included."""
+    from oracle import oracle as O
+    from paper_2302_11825_b200 import abi
+
+    N = c.cache.nBoundary
+    rng = np.random.default_rng(0)
+    z = c.vertices[rng.integers(0, len(c.vertices), N)]
+    n = z / np.linalg.norm(z, axis=1)[:, None]
+    cache = dict(z=z, n=n, pdf=np.full(N, 0.1), uHat=rng.uniform(-1, 1, N), dHat=rng.uniform(-1, 1, N),
+                 weight=np.zeros(N))
+    spec = abi.KernelSpec(c.problem.kernel.kind, c.problem.kernel.sigma, 3, 4.0)
+    k = 4
+    while True:
+        xs = c.points[:k]
+        t0 = time.perf_counter()
+        O.oracle_splat(spec, 4e-12, cache, None, xs, value=True)
+        t = time.perf_counter() - t0
+        if t > 0.5 * sample_s or k >= len(c.points):
+            break
+        k = min(len(c.points), int(k * max(2.0, 0.5 * sample_s / max(t, 1e-3) * 0.8)))
+    return {"value": k * N / t, "unit": "interactions/s", "cores": 1, "kind": "port",
+            "sample": f"restated 3D splat (1 thread) on {k} points x {N} samples ({t:.1f} s); gather only — "
+                      "the reference has no 3D walk or splat path"}
+
+
 def cpu_baseline(c, sample_s):
     try:
+        if getattr(c, "dim", 2) == 3:
+            return port_gather_estimate_3d(c, sample_s)
         return reference_round_estimate(c, sample_s)
     except Exception as e:  # oracle/_ref missing on this host
         return {"value": None, "unit": "interactions/s", "cores": os.cpu_count(), "kind": "reference",
@@ -426,7 +479,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -233,10 +233,10 @@ class Scene:
         return self.neumann_length > 0.0
 
     def closest_point(self, x, filt=abi.FILTER_ANY):
-        """Scene::closestPoint (scene.h:95); returns point, dist, segment, t."""
-        x = _f64(x, 2)
+        """Scene::closestPoint (scene.h:95); returns point, dist, segment (triangle in 3D), t."""
+        x = _f64(x, self.dim)
         n = len(x)
-        p, d, sg, t = np.zeros((n, 2)), np.zeros(n), np.zeros(n, np.int32), np.zeros(n)
+        p, d, sg, t = np.zeros((n, self.dim)), np.zeros(n), np.zeros(n, np.int32), np.zeros(n)
         _check(lib().bvc_scene_closest_point(self.h, _ptr(x), C.c_size_t(n), filt, _ptr(p), _ptr(d),
                                              _ptr(sg, C.c_int), _ptr(t)))
         return p, d, sg, t
@@ -256,7 +256,7 @@ class Scene:
         return t, sg, p, s
 
     def inside(self, x):
-        x = _f64(x, 2)
+        x = _f64(x, self.dim)
         out = np.zeros(len(x), np.uint8)
         _check(lib().bvc_scene_inside(self.h, _ptr(x), C.c_size_t(len(x)), _ptr(out, C.c_uint8)))
         return out.astype(bool)
@@ -275,7 +275,8 @@ class SolveRegion:
         nv, ns, off, area, whole = C.c_int(), C.c_int(), C.c_double(), C.c_double(), C.c_int()
         _check(lib().bvc_region_info(self.h, C.byref(nv), C.byref(ns), C.byref(off), C.byref(area), C.byref(whole)))
         self.offset, self.area, self.whole_domain = off.value, area.value, bool(whole.value)
-        v, s = np.zeros((nv.value, 2)), np.zeros((ns.value, 2), np.int32)
+        d = scene.dim  # 3D regions are triangle meshes (area = enclosed volume)
+        v, s = np.zeros((nv.value, d)), np.zeros((ns.value, d), np.int32)
         lb, kinds, src = (np.zeros(ns.value, np.int32) for _ in range(3))
         _check(lib().bvc_region_export(self.h, _ptr(v), _ptr(s, C.c_int), _ptr(lb, C.c_int), _ptr(kinds, C.c_int),
                                        _ptr(src, C.c_int)))

@@ -145,4 +145,124 @@ def config3(scale: float = 1.0, grid_n: int = 1024) -> Config:
                   extra=dict(centers=centers, amps=amps))
 
 
-CONFIGS = {1: config1, 2: config2, 3: config3}
+def icosphere(level: int):
+    """Unit icosphere by midpoint subdivision (level 6: 40962 vertices, 81920 triangles), outward CCW."""
+    t = (1.0 + 5 ** 0.5) / 2.0
+    v = [(-1, t, 0), (1, t, 0), (-1, -t, 0), (1, -t, 0), (0, -1, t), (0, 1, t), (0, -1, -t), (0, 1, -t),
+         (t, 0, -1), (t, 0, 1), (-t, 0, -1), (-t, 0, 1)]
+    f = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4), (11, 10, 2), (10, 7, 6),
+         (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9), (4, 9, 5), (2, 4, 11), (6, 2, 10),
+         (8, 6, 7), (9, 8, 1)]
+    V = np.array(v, dtype=np.float64)
+    V /= np.linalg.norm(V, axis=1)[:, None]
+    F = np.array(f, dtype=np.int64)
+    for _ in range(level):
+        e = np.concatenate([F[:, [0, 1]], F[:, [1, 2]], F[:, [2, 0]]])
+        key = np.sort(e, axis=1)
+        uniq, inv = np.unique(key[:, 0] * len(V) + key[:, 1], return_inverse=True)
+        a, b = uniq // len(V), uniq % len(V)
+        mid = V[a] + V[b]
+        mid /= np.linalg.norm(mid, axis=1)[:, None]
+        m = (len(V) + inv).reshape(3, -1).T  # midpoint ids of edges (01, 12, 20) per face
+        V = np.concatenate([V, mid])
+        F = np.concatenate([np.stack([F[:, 0], m[:, 0], m[:, 2]], 1), np.stack([F[:, 1], m[:, 1], m[:, 0]], 1),
+                            np.stack([F[:, 2], m[:, 2], m[:, 1]], 1), m])
+    # orient outward
+    c = V[F].mean(1)
+    n = np.cross(V[F[:, 1]] - V[F[:, 0]], V[F[:, 2]] - V[F[:, 0]])
+    flip = np.sum(n * c, 1) < 0
+    F[flip] = F[flip][:, [0, 2, 1]]
+    return V, F.astype(np.int32)
+
+
+def displaced_sphere(rng, level=6, amp=0.05, passes=10, center=(0, 0, 0), radius=1.0):
+    """vertex noise N(0,1), smoothed by `passes` uniform-Laplacian passes, radial displacement amp*noise"""
+    V, F = icosphere(level)
+    noise = rng.standard_normal(len(V))
+    e = np.concatenate([F[:, [0, 1]], F[:, [1, 2]], F[:, [2, 0]]])
+    e = np.concatenate([e, e[:, ::-1]])
+    deg = np.bincount(e[:, 0], minlength=len(V)).astype(np.float64)
+    for _ in range(passes):
+        noise = np.bincount(e[:, 0], weights=noise[e[:, 1]], minlength=len(V)) / deg
+    noise /= noise.std()
+    V = V * (radius * (1.0 + amp * noise))[:, None] + np.asarray(center, dtype=np.float64)
+    return V, F
+
+
+def config4(scale: float = 1.0, n_points: int = 2097152) -> Config:
+    """C4: displaced level-6 icosphere (81920 triangles), all Dirichlet, g = xy + z^2 - (x^2 + y^2)/2 (harmonic)."""
+    rng = np.random.default_rng(MASTER_SEED + 4)
+    V, F = displaced_sphere(rng)
+    g = abi.make_field(abi.FIELD_QUADRATIC3, [0, 0, 0, 0, -0.5, -0.5, 1.0, 1.0, 0.0, 0.0])
+    N = max(1, int(262144 * scale))
+    lo, hi = V.min(0), V.max(0)
+    pts = rng.uniform(lo, hi, (int(n_points * 2.8), 3))  # filtered to the interior by Scene.inside
+    exact = lambda x: x[:, 0] * x[:, 1] + x[:, 2] ** 2 - 0.5 * (x[:, 0] ** 2 + x[:, 1] ** 2)  # noqa: E731
+    return Config("C4 3D Laplace displaced icosphere", V, F, np.zeros(len(F), np.int32),
+                  _problem(abi.KernelSpec(abi.KERNEL_POISSON, 0.0, 3, 1.0), g=g),
+                  _cache(1e-3, N, 256, 256, nWalks=256), pts, 1e-3, exact_u=exact, seed=MASTER_SEED + 4,
+                  extra=dict(dim=3, n_points=n_points))
+
+
+def config5(scale: float = 1.0, n_points: int = 16777216) -> Config:
+    """C5: 8 overlapping displaced level-6 icospheres (655360 triangles, a soup); Neumann h = 0 where n.z > 0.5,
+    Dirichlet g = sin x + cos 2y + z elsewhere; screened sigma = 1."""
+    rng = np.random.default_rng(MASTER_SEED + 5)
+    Vs, Fs, base, comps = [], [], 0, []
+    for _ in range(8):
+        c = rng.uniform(-1, 1, 3)
+        r = rng.uniform(0.5, 0.9)
+        V, F = displaced_sphere(rng, center=c, radius=r)
+        comps.append((base, base + len(V), sum(len(f) for f in Fs), sum(len(f) for f in Fs) + len(F)))
+        Vs.append(V)
+        Fs.append(F + base)
+        base += len(V)
+    V, F = np.concatenate(Vs), np.concatenate(Fs).astype(np.int32)
+    n = np.cross(V[F[:, 1]] - V[F[:, 0]], V[F[:, 2]] - V[F[:, 0]])
+    n /= np.linalg.norm(n, axis=1)[:, None]
+    labels = (n[:, 2] > 0.5).astype(np.int32)
+    g = abi.make_field(abi.FIELD_TRIG3, [1.0, 1.0, 1.0, 2.0, 1.0, 0.0])
+    N = max(1, int(1048576 * scale))
+    lo, hi = V.min(0), V.max(0)
+    pts = rng.uniform(lo, hi, (int(n_points * 1.5), 3))
+    return Config("C5 3D screened soup (sigma=1, mixed)", V, F, labels,
+                  _problem(abi.KernelSpec(abi.KERNEL_SCREENED, 1.0, 3, 1.0), g=g),
+                  _cache(1e-3, N, 128, 128, nWalks=128), pts, 1e-3, seed=MASTER_SEED + 5,
+                  extra=dict(dim=3, n_points=n_points, components=comps))
+
+
+def soup_components(c: Config):
+    """The closed component meshes of a soup config (inside the union = inside any)."""
+    from .api import Scene
+
+    out = []
+    for v0, v1, f0, f1 in c.extra["components"]:
+        out.append(Scene.mesh3(c.vertices[v0:v1], c.segments[f0:f1] - v0, c.labels[f0:f1]))
+    return out
+
+
+def soup_shell(c: Config):
+    """Outer shell of a soup of closed meshes: triangles with a vertex outside every other
+    component. Triangles buried inside another component would act as walls inside the
+    union and break the boundary-integral identity; keeping straddling triangles leaves
+    no holes along the intersection curves (only sub-triangle flaps). Uses the device
+    inside test of each component. Returns (triangles, labels) of the shell."""
+    comps = soup_components(c)
+    V, F = c.vertices, c.segments
+    owner = np.zeros(len(F), np.int64)
+    for k, (_, _, f0, f1) in enumerate(c.extra["components"]):
+        owner[f0:f1] = k
+    vin = np.zeros((len(comps), len(V)), bool)
+    for k, m in enumerate(comps):
+        vin[k] = m.inside(V)
+    keep = np.zeros(len(F), bool)
+    for j in range(3):
+        vj = F[:, j]
+        inside_other = np.zeros(len(F), bool)
+        for k in range(len(comps)):
+            inside_other |= vin[k, vj] & (owner != k)
+        keep |= ~inside_other
+    return F[keep], c.labels[keep]
+
+
+CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}

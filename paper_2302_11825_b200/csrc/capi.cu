@@ -43,6 +43,12 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 #define CK(x) cuda_check((x), #x)
 
+inline float __int_as_float_host(int v) {
+    float f;
+    std::memcpy(&f, &v, sizeof f);
+    return f;
+}
+
 void require_device() {
     static int state = -1;  // -1 unknown, 0 none, 1 ok
     if (state < 0) {
@@ -192,11 +198,90 @@ struct bvc_scene_s {
     DevBuf<int> cdfIds;
     DevBuf<float> segArc, segLen;
     double total = 0.0;
+    // 3D (triangle meshes)
+    DevBuf<bvc_dev::Node3> nodes3;
+    DevBuf<bvc_dev::Prim3> prims3;
+    DevBuf<float4> triNormal, triA, triB, triC, sil3A, sil3B, sil3N1, sil3N2;
+    DevBuf<int4> triSil;
+
+    void upload3() {
+        bvh = bvc_host::buildBvh(host, 4);
+        size_t nn = bvh.children.size() / 2;
+        std::vector<bvc_dev::Node3> hn(nn);
+        for (size_t i = 0; i < nn; ++i) {
+            const float* b = &bvh.boxes[12 * i];
+            hn[i].llo = make_float4(b[0], b[1], b[2], 0.f);
+            hn[i].lhi = make_float4(b[3], b[4], b[5], 0.f);
+            hn[i].rlo = make_float4(b[6], b[7], b[8], 0.f);
+            hn[i].rhi = make_float4(b[9], b[10], b[11], 0.f);
+            hn[i].left = bvh.children[2 * i];
+            hn[i].right = bvh.children[2 * i + 1];
+            hn[i].mask = bvh.masks[i];
+            hn[i].pad = 0;
+        }
+        nodes3.upload(hn.data(), nn);
+        auto f4 = [](const double* p, float w) { return make_float4(p[0], p[1], p[2], w); };
+        std::vector<bvc_dev::Prim3> hp(host.ns);
+        for (int j = 0; j < host.ns; ++j) {
+            int id = bvh.order[j];
+            hp[j].a = f4(host.vert(host.idx[3 * id]), __int_as_float_host(id));
+            hp[j].b = f4(host.vert(host.idx[3 * id + 1]), __int_as_float_host(bvc_host::primClass(host, id)));
+            hp[j].c = f4(host.vert(host.idx[3 * id + 2]), 0.f);
+        }
+        prims3.upload(hp.data(), hp.size());
+        std::vector<float4> hn4(host.ns), ha(host.ns), hb(host.ns), hc(host.ns);
+        std::vector<int4> hs(host.ns);
+        std::vector<double> cd(host.ns);
+        double run = 0.0;
+        for (int i = 0; i < host.ns; ++i) {
+            hn4[i] = f4(&host.normal[3 * static_cast<size_t>(i)], 0.f);
+            ha[i] = f4(host.vert(host.idx[3 * i]), 0.f);
+            hb[i] = f4(host.vert(host.idx[3 * i + 1]), 0.f);
+            hc[i] = f4(host.vert(host.idx[3 * i + 2]), 0.f);
+            hs[i] = make_int4(host.triSil[3 * i], host.triSil[3 * i + 1], host.triSil[3 * i + 2], -1);
+            run += host.measure[i];
+            cd[i] = run;
+        }
+        total = run;
+        triNormal.upload(hn4.data(), hn4.size());
+        triA.upload(ha.data(), ha.size());
+        triB.upload(hb.data(), hb.size());
+        triC.upload(hc.data(), hc.size());
+        triSil.upload(hs.data(), hs.size());
+        cdf.upload(cd.data(), cd.size());
+        size_t ne = std::max<size_t>(host.sil3Always.size(), 1);
+        std::vector<float4> ea(ne), eb(ne), e1(ne), e2(ne);
+        for (size_t k = 0; k < host.sil3Always.size(); ++k) {
+            ea[k] = f4(&host.sil3A[3 * k], 0.f);
+            eb[k] = f4(&host.sil3B[3 * k], 0.f);
+            e1[k] = f4(&host.sil3N1[3 * k], host.sil3Always[k] ? 1.f : 0.f);
+            e2[k] = f4(&host.sil3N2[3 * k], 0.f);
+        }
+        sil3A.upload(ea.data(), ne);
+        sil3B.upload(eb.data(), ne);
+        sil3N1.upload(e1.data(), ne);
+        sil3N2.upload(e2.data(), ne);
+        uploaded = true;
+    }
+    bvc_dev::SceneView3 view3() {
+        upload();
+        bvc_dev::SceneView3 v;
+        v.nodes = nodes3.p;
+        v.prims = prims3.p;
+        v.triNormal = triNormal.p;
+        v.nt = host.ns;
+        v.diagonal = static_cast<float>(host.diagonal);
+        v.counts = nullptr;
+        return v;
+    }
 
     void upload() {
         if (uploaded) return;
         require_device();
-        if (host.dim != 2) throw Error(BVC_ERR_SOLVER, "device queries support 2D scenes (3D walks: §8f)");
+        if (host.dim == 3) {
+            upload3();
+            return;
+        }
         bvh = bvc_host::buildBvh(host, 4);
         size_t nn = bvh.children.size() / 2;
         std::vector<Node2> hn(nn);
@@ -515,6 +600,170 @@ void run_cache_walks(bvc_scene_s* S, bvc_region_s* R, const WalkEnv& E, const bv
     st.truncated += static_cast<long long>(h[2]);
 }
 
+__global__ void redraw_copy_kernel(const CacheSample* src, const int* idx, int n, CacheSample* dst);
+
+WalkEnv3 make_env3(bvc_scene_s* S, const bvc_problem& pb, const bvc_walk_config& wc, uint64_t seed, uint64_t salt,
+                   uint64_t round) {
+    validate_kernel(pb.kernel);
+    if (pb.kernel.dim != 3) throw Error(BVC_ERR_INVALID_ARGUMENT, "3D scene needs a dim-3 kernel");
+    if (pb.f.kind != BVC_FIELD_NONE)
+        throw Error(BVC_ERR_SOLVER, "source terms are not supported by the 3D walks (kernels.cpp:98-99 is 2D-only)");
+    if (!(S->host.dirichletMeasure > 0.0))
+        throw Error(BVC_ERR_SOLVER, "walk cannot terminate: scene has no Dirichlet boundary");
+    WalkEnv3 E{};
+    E.S = S->view3();
+    E.triSil = S->triSil.p;
+    E.silA = S->sil3A.p;
+    E.silB = S->sil3B.p;
+    E.silN1 = S->sil3N1.p;
+    E.silN2 = S->sil3N2.p;
+    E.P.screened = pb.kernel.kind == BVC_KERNEL_SCREENED;
+    E.P.sigma = static_cast<float>(pb.kernel.sigma);
+    E.P.sqrtSigma = static_cast<float>(std::sqrt(pb.kernel.sigma));
+    E.P.dim = 3;
+    E.P.f = to_dev(pb.f);
+    E.P.g = to_dev(pb.g);
+    E.P.h = to_dev(pb.h);
+    double diag = S->host.diagonal;
+    double eps = wc.epsilon > 0.0 ? wc.epsilon : 1e-3 * diag;
+    double rmin = wc.rMin > 0.0 ? wc.rMin : eps;
+    if (rmin > eps) throw Error(BVC_ERR_INVALID_ARGUMENT, "walk config: r_min must lie in (0, epsilon]");
+    E.eps = static_cast<float>(eps);
+    E.rmin = static_cast<float>(rmin);
+    E.tguard = static_cast<float>(1e-9 * diag);
+    E.insideTol = S->host.component.empty() || *std::max_element(S->host.component.begin(), S->host.component.end()) == 0
+                      ? static_cast<float>(1e-7 * diag) : -1.0f;  // parity is meaningless for soups
+    E.scale = static_cast<float>(diag);
+    E.nudge = static_cast<float>(9.5367431640625e-7 * diag);
+    E.cx = static_cast<float>(0.5 * (S->host.lo[0] + S->host.hi[0]));
+    E.cy = static_cast<float>(0.5 * (S->host.lo[1] + S->host.hi[1]));
+    E.cz = static_cast<float>(0.5 * (S->host.lo[2] + S->host.hi[2]));
+    E.escape = static_cast<float>(diag);
+    E.maxSteps = std::max(1, wc.maxSteps);
+    E.hasNeumann = S->host.hasNeumann() ? 1 : 0;
+    E.hasH = pb.h.kind != BVC_FIELD_NONE ? 1 : 0;
+    E.closed = E.insideTol > 0.f ? 1 : 0;
+    key_of(seed, salt, round, E.k0, E.k1);
+    return E;
+}
+
+void run_cache_walks3(bvc_scene_s* S, bvc_region_s* R, const WalkEnv3& E, const bvc_cache_config& cfg,
+                      CacheSample* samples, int n, long long gidBase, const long long* gid, uint8_t* failed,
+                      GenStats& st) {
+    float4* startU = ws().get<float4>(kWsStartU, n);
+    int* isD = ws().get<int>(kWsIsD, n);
+    float* gradR = ws().get<float>(kWsGradR, n);
+    launch_prepare3(E, samples, n, R->kinds.p, startU, isD, gradR, failed, g_stream);
+    int* dIdx = ws().get<int>(kWsDIdx, n);
+    int* cnt = ws().get<int>(kWsCount, 1);
+    launch_compact(isD, n, dIdx, cnt, g_stream);
+    int nD = 0;
+    CK(cudaMemcpyAsync(&nD, cnt, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+    float4* xD = ws().get<float4>(kWsXD, std::max(nD, 1));
+    float4* nrmD = ws().get<float4>(kWsND, std::max(nD, 1));
+    float* rD = ws().get<float>(kWsRD, std::max(nD, 1));
+    long long* gidD = ws().get<long long>(kWsGidD, std::max(nD, 1));
+    launch_gather_dpoints3(samples, dIdx, nD, gradR, gidBase, gid, xD, nrmD, rD, gidD, g_stream);
+    int nU = std::max(1, cfg.nWalksNeumann), nDw = std::max(1, cfg.nWalksDirichlet);
+    WalkJob3 J{};
+    J.nU = nU;
+    J.nPtsU = n;
+    J.startU = startU;
+    J.gidU = gid;
+    J.gidBaseU = gidBase;
+    J.outU = ws().get<float>(kWsOutU, static_cast<size_t>(n) * nU);
+    J.nD = nDw;
+    J.nPtsD = nD;
+    J.xD = xD;
+    J.normalD = nrmD;
+    J.radiusD = rD;
+    J.gidD = gidD;
+    J.outD = ws().get<float>(kWsOutD, std::max<size_t>(static_cast<size_t>(nD) * nDw, 1));
+    auto* ctr = ws().get<unsigned long long>(kWsCounter, 3);
+    CK(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), g_stream));
+    J.counter = ctr;
+    J.steps = ctr + 1;
+    J.truncTotal = ctr + 2;
+    if (g_profile) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        size_t slots = static_cast<size_t>(sms) * 32 * 256 * 2;
+        auto* cc = ws().get<unsigned long long>(kWsEvalOut, slots);
+        CK(cudaMemsetAsync(cc, 0, slots * sizeof(unsigned long long), g_stream));
+        WalkEnv3 Ec = E;
+        Ec.S.counts = cc;
+        launch_walk_job3(Ec, J, g_stream);
+        std::vector<unsigned long long> h(slots);
+        CK(cudaMemcpyAsync(h.data(), cc, slots * sizeof(unsigned long long), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+        for (size_t i = 0; i < slots; ++i) g_profileTotals[i & 1] += h[i];
+    } else {
+        launch_walk_job3(E, J, g_stream);
+    }
+    launch_finish_samples(samples, n, J.outU, nU, dIdx, nD, J.outD, nDw, failed, g_stream);
+    unsigned long long h[3];
+    CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+    st.walks += static_cast<long long>(n) * nU + static_cast<long long>(nD) * nDw;
+    st.steps += static_cast<long long>(h[1]);
+    st.truncated += static_cast<long long>(h[2]);
+}
+
+void generate_cache3(bvc_scene_s* S, const bvc_problem& pb, bvc_region_s* R, const bvc_cache_config& cfg, uint64_t seed,
+                     uint64_t round, int begin, int end, bvc_boundary_cache_s* out, GenStats& st) {
+    const int N = std::max(1, cfg.nBoundary);
+    const int n = end - begin;
+    out->n = n;
+    out->dim = 3;
+    out->voronoi = 0;
+    out->length = R->boundary.total;
+    out->samples.resize(std::max(n, 1));
+    if (n == 0) return;
+    if (cfg.voronoi) throw Error(BVC_ERR_INVALID_ARGUMENT, "Voronoi weights are defined for 2D loops only");
+    bvc_scene_s& B = R->boundary;
+    uint32_t k0, k1;
+    key_of(seed, kBoundaryPosSalt, round, k0, k1);
+    launch_sample_mesh(B.cdf.p, B.host.ns, B.total, B.triA.p, B.triB.p, B.triC.p, B.triNormal.p, N, begin, n, nullptr,
+                       cfg.stratified, k0, k1, out->samples.p, g_stream);
+    WalkEnv3 E = make_env3(S, pb, cfg.walk, seed, kBoundaryWalkSalt, round);
+    uint8_t* failed = ws().get<uint8_t>(kWsFailed, n);
+    run_cache_walks3(S, R, E, cfg, out->samples.p, n, begin, nullptr, failed, st);
+    std::vector<uint8_t> hf(n);
+    CK(cudaMemcpyAsync(hf.data(), failed, n, cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+    std::vector<int> bad;
+    for (int i = 0; i < n; ++i) if (hf[i]) bad.push_back(i);
+    WalkEnv3 Er = make_env3(S, pb, cfg.walk, seed, kBoundaryRedrawSalt, round);
+    for (int guard = 1; !bad.empty(); ++guard) {
+        if (guard > 64) throw Error(BVC_ERR_SOLVER, "boundary cache: sample kept failing after 64 redraws");
+        int nb = static_cast<int>(bad.size());
+        st.resampled += nb;
+        std::vector<long long> hc(nb);
+        for (int j = 0; j < nb; ++j) hc[j] = (static_cast<long long>(begin) + bad[j]) * 131 + guard;
+        long long* dctr = ws().get<long long>(kWsCtr, nb);
+        CK(cudaMemcpyAsync(dctr, hc.data(), nb * sizeof(long long), cudaMemcpyHostToDevice, g_stream));
+        CacheSample* tmp = ws().get<CacheSample>(kWsSamplesTmp, nb);
+        uint32_t r0, r1;
+        key_of(seed, kBoundaryRedrawSalt, round, r0, r1);
+        launch_sample_mesh(B.cdf.p, B.host.ns, B.total, B.triA.p, B.triB.p, B.triC.p, B.triNormal.p, N, 0, nb, dctr, 0, r0,
+                           r1, tmp, g_stream);
+        uint8_t* f2 = ws().get<uint8_t>(kWsSrcFlag, nb);
+        run_cache_walks3(S, R, Er, cfg, tmp, nb, 0, dctr, f2, st);
+        int* didx = ws().get<int>(kWsDIdx, nb);
+        CK(cudaMemcpyAsync(didx, bad.data(), nb * sizeof(int), cudaMemcpyHostToDevice, g_stream));
+        redraw_copy_kernel<<<(nb + 127) / 128, 128, 0, g_stream>>>(tmp, didx, nb, out->samples.p);
+        count_launch();
+        std::vector<uint8_t> hf2(nb);
+        CK(cudaMemcpyAsync(hf2.data(), f2, nb, cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+        std::vector<int> still;
+        for (int j = 0; j < nb; ++j) if (hf2[j]) still.push_back(bad[j]);
+        bad.swap(still);
+    }
+}
+
 __global__ void redraw_copy_kernel(const CacheSample* src, const int* idx, int n, CacheSample* dst) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j < n) dst[idx[j]] = src[j];
@@ -529,6 +778,11 @@ void generate_cache(bvc_scene_s* S, const bvc_problem& pb, bvc_region_s* R, cons
     need(begin >= 0 && begin <= end && end <= N, "shard range outside [0, nBoundary]");
     if (cfg.clampMode != BVC_CLAMP_OFF || cfg.sourceBall)
         throw Error(BVC_ERR_INVALID_ARGUMENT, "clamped / ball-kernel splats are not implemented (SURVEY §8f.3)");
+    if (S->host.dim == 3) {
+        S->upload();
+        generate_cache3(S, pb, R, cfg, seed, round, begin, end, out, st);
+        return;
+    }
     const int n = end - begin;
     out->n = n;
     out->dim = 2;
@@ -651,6 +905,13 @@ void generate_source(const bvc_problem& pb, bvc_region_s* R, const bvc_cache_con
     require_device();
     R->upload();
     bvc_scene_s& B = R->boundary;
+    if (B.host.dim == 3) {  // no 3D source path (sampleBallGreens is 2D-only, kernels.cpp:98-99)
+        out->dim = 3;
+        out->area = bvc_host::meshVolume(B.host);
+        out->m = 0;
+        if (pb.f.kind != BVC_FIELD_NONE) throw Error(BVC_ERR_SOLVER, "3D source caches are not supported");
+        return;
+    }
     out->dim = 2;
     out->area = bvc_host::loopArea(B.host);
     if (!B.host.closed()) throw Error(BVC_ERR_PARSE, "region sampler requires closed loops");
@@ -882,11 +1143,109 @@ __global__ void gather_fallback_kernel(const int* idx, int n, const double* x, f
     gid[j] = p;
 }
 
+__global__ void gather_fallback3_kernel(const int* idx, int n, const double* x, float4* out, long long* gid,
+                                        double* xd) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int p = idx[j];
+    out[j] = make_float4(static_cast<float>(x[3 * p]), static_cast<float>(x[3 * p + 1]), static_cast<float>(x[3 * p + 2]), 0.f);
+    gid[j] = p;
+    xd[3 * j] = x[3 * p];
+    xd[3 * j + 1] = x[3 * p + 1];
+    xd[3 * j + 2] = x[3 * p + 2];
+}
+
+__global__ void radius3_kernel(const double* dist, int n, float rmin, float* r) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) r[j] = fmaxf(static_cast<float>(dist[j]), rmin);
+}
+
+__global__ void fallback_accumulate3_kernel(const int* idx, int n, const double* mean, const double* g0,
+                                            const double* g1, const double* g2, int nw, const int* trunc,
+                                            double* walkSum, long long* walkCount, long long* walkTrunc, double* gws,
+                                            long long* gwc) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int p = idx[j];
+    walkSum[p] += mean[j] * nw;
+    walkCount[p] += nw;
+    walkTrunc[p] += trunc[j];
+    if (g0) {
+        gws[3 * p] += g0[j] * nw;
+        gws[3 * p + 1] += g1[j] * nw;
+        gws[3 * p + 2] += g2[j] * nw;
+        gwc[p] += nw;
+    }
+}
+
+// fallback-band walks in 3D (the 3D lift of cache.cpp:665-681); the interior check
+// runs on the device, failures are reported after the walks
+void fallback_walks3(bvc_scene_s* S, const bvc_problem& pb, const bvc_cache_config& cfg, bvc_eval_points_s* P,
+                     uint64_t seed, uint64_t round, bool gradients) {
+    int nf = static_cast<int>(P->n) - P->active;
+    const int* idx = P->order.p + P->active;
+    int nw = std::max(1, cfg.walk.nWalks);
+    float4* px = ws().get<float4>(kWsStartU, nf);
+    long long* gid = ws().get<long long>(kWsGidU, nf);
+    double* xd = ws().get<double>(kWsEvalIn, 3 * static_cast<size_t>(nf));
+    gather_fallback3_kernel<<<(nf + 127) / 128, 128, 0, g_stream>>>(idx, nf, P->x.p, px, gid, xd);
+    count_launch();
+    WalkEnv3 E = make_env3(S, pb, cfg.walk, seed, kFallbackSalt, round);
+    auto* ctr = ws().get<unsigned long long>(kWsCounter, 3);
+    int* tr = ws().get<int>(kWsTruncPt, nf);
+    CK(cudaMemsetAsync(tr, 0, nf * sizeof(int), g_stream));
+    CK(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), g_stream));
+    WalkJob3 J{};
+    J.counter = ctr;
+    J.nU = nw;
+    J.nPtsU = nf;
+    J.startU = px;
+    J.gidU = gid;
+    J.outU = ws().get<float>(kWsOutU, static_cast<size_t>(nf) * nw);
+    J.truncU = tr;
+    launch_walk_job3(E, J, g_stream);
+    double* dm = ws().get<double>(kWsMean, nf);
+    launch_reduce_estimates(J.outU, nf, nw, 1, 0, dm, nullptr, g_stream);
+    double *g0 = nullptr, *g1 = nullptr, *g2 = nullptr;
+    if (gradients) {
+        WalkEnv3 Eg = make_env3(S, pb, cfg.walk, seed, kFallbackGradSalt, round);
+        double* cpp = ws().get<double>(kWsEvalOut, 3 * static_cast<size_t>(nf));
+        double* cpd = ws().get<double>(kWsMean2, nf);
+        int* cps = ws().get<int>(kWsSkipB, nf);
+        launch_closest3(Eg.S, xd, nf, bvc_dev::kClsAny, cpp, cpd, cps, g_stream);
+        float* rD = ws().get<float>(kWsRD, nf);
+        radius3_kernel<<<(nf + 127) / 128, 128, 0, g_stream>>>(cpd, nf, Eg.rmin, rD);
+        count_launch();
+        CK(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), g_stream));
+        WalkJob3 G{};
+        G.counter = ctr;
+        G.nD = nw;
+        G.nPtsD = nf;
+        G.xD = px;
+        G.radiusD = rD;
+        G.gidD = gid;
+        G.outD = ws().get<float>(kWsOutD, static_cast<size_t>(nf) * nw * 3);
+        launch_walk_job3(Eg, G, g_stream);
+        g0 = ws().get<double>(kWsSe, 3 * static_cast<size_t>(nf));
+        g1 = g0 + nf;
+        g2 = g1 + nf;
+        for (int c = 0; c < 3; ++c) launch_reduce_estimates(G.outD, nf, nw, 3, c, g0 + c * nf, nullptr, g_stream);
+    }
+    fallback_accumulate3_kernel<<<(nf + 127) / 128, 128, 0, g_stream>>>(idx, nf, dm, g0, g1, g2, nw, tr, P->walkSum.p,
+                                                                        P->walkCount.p, P->walkTrunc.p,
+                                                                        P->gwalkSum.p, P->gwalkCount.p);
+    count_launch();
+}
+
 void fallback_walks(bvc_scene_s* S, const bvc_problem& pb, const bvc_cache_config& cfg, bvc_eval_points_s* P,
                     uint64_t seed, uint64_t round, bool gradients) {
     ensure_order(P);
     int nf = static_cast<int>(P->n) - P->active;
     if (nf <= 0) return;
+    if (S->host.dim == 3) {
+        fallback_walks3(S, pb, cfg, P, seed, round, gradients);
+        return;
+    }
     const int* idx = P->order.p + P->active;
     int nw = std::max(1, cfg.walk.nWalks);
     float2* px = ws().get<float2>(kWsStartU, nf);
@@ -1099,6 +1458,19 @@ int bvc_scene_closest_point(bvc_scene s, const double* x, size_t n, int filter, 
         need(s && x, "null argument");
         if (n == 0) return BVC_OK;
         unsigned mask = filter == BVC_FILTER_DIRICHLET ? bvc_dev::kClsD : filter == BVC_FILTER_NEUMANN ? bvc_dev::kClsNeumann : bvc_dev::kClsAny;
+        if (s->host.dim == 3) {  // point: 3n, t: unused (0)
+            double* xd3 = ws().get<double>(kWsEvalIn, 3 * n);
+            double* o3 = ws().get<double>(kWsEvalOut, 4 * n);
+            int* sg3 = ws().get<int>(kWsSkipB, n);
+            CK(cudaMemcpyAsync(xd3, x, 3 * n * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+            launch_closest3(s->view3(), xd3, static_cast<int>(n), mask, o3, o3 + 3 * n, sg3, g_stream);
+            CK(cudaMemcpyAsync(point, o3, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+            CK(cudaMemcpyAsync(dist, o3 + 3 * n, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+            CK(cudaMemcpyAsync(seg, sg3, n * sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+            CK(cudaStreamSynchronize(g_stream));
+            if (t) std::fill(t, t + n, 0.0);
+            return BVC_OK;
+        }
         double* xd = ws().get<double>(kWsEvalIn, 2 * n);
         double* o = ws().get<double>(kWsEvalOut, 4 * n);
         int* sg = ws().get<int>(kWsSkipB, n);
@@ -1149,10 +1521,14 @@ int bvc_scene_inside(bvc_scene s, const double* x, size_t n, uint8_t* inside) {
         require_device();
         need(s && x, "null argument");
         if (n == 0) return BVC_OK;
-        double* xd = ws().get<double>(kWsEvalIn, 2 * n);
+        int d = s->host.dim;
+        double* xd = ws().get<double>(kWsEvalIn, d * n);
         uint8_t* o = ws().get<uint8_t>(kWsOutside, n);
-        CK(cudaMemcpyAsync(xd, x, 2 * n * sizeof(double), cudaMemcpyHostToDevice, g_stream));
-        launch_inside(s->view(), xd, static_cast<int>(n), static_cast<float>(1e-7 * s->host.diagonal), o, g_stream);
+        CK(cudaMemcpyAsync(xd, x, d * n * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        if (d == 3)
+            launch_inside3(s->view3(), xd, static_cast<int>(n), static_cast<float>(1e-7 * s->host.diagonal), o, g_stream);
+        else
+            launch_inside(s->view(), xd, static_cast<int>(n), static_cast<float>(1e-7 * s->host.diagonal), o, g_stream);
         CK(cudaMemcpyAsync(inside, o, n, cudaMemcpyDeviceToHost, g_stream));
         CK(cudaStreamSynchronize(g_stream));
     })
@@ -1296,15 +1672,22 @@ int bvc_mark_evaluation_points(bvc_scene s, bvc_region r, const bvc_cache_config
     API({
         require_device();
         need(s && r && cfg && p, "null argument");
-        need(p->dim == 2, "markEvaluationPoints: 2D points");
+        need(p->dim == s->host.dim, "markEvaluationPoints: point and scene dimensions differ");
         if (cfg->sourceBall) throw Error(BVC_ERR_INVALID_ARGUMENT, "ball-kernel mode is not implemented (SURVEY §8f.3)");
         r->upload();
         int n = static_cast<int>(p->n);
-        if (n)
+        if (s->host.dim == 3) {
+            const auto& comp = r->boundary.host.component;
+            bool single = !comp.empty() && *std::max_element(comp.begin(), comp.end()) == 0;
+            launch_mark3(s->view3(), r->boundary.view3(), p->x.p, n, static_cast<float>(r->host.offset),
+                         r->host.wholeDomain ? 1 : 0, single ? static_cast<float>(1e-7 * r->boundary.host.diagonal) : -1.f,
+                         p->fallback.p, p->unreliable.p, g_stream);
+        } else if (n) {
             mark_kernel<<<(n + 127) / 128, 128, 0, g_stream>>>(s->view(), r->boundary.view(), p->x.p, n,
                                                                static_cast<float>(r->host.offset), r->host.wholeDomain ? 1 : 0,
                                                                p->fallback.p, p->unreliable.p);
-        count_launch();
+            count_launch();
+        }
         p->orderValid = false;
         CK(cudaGetLastError());
     })

@@ -4,7 +4,9 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <functional>
 #include <limits>
+#include <map>
 #include <numeric>
 #include <optional>
 
@@ -177,7 +179,116 @@ HostScene buildMesh3(const double* vertices, int nv, const int* tris, const int*
         (s.label[i] ? s.neumannMeasure : s.dirichletMeasure) += s.measure[i];
         s.totalMeasure += s.measure[i];
     }
+    // edge adjacency: silhouette edges between Neumann faces, open Neumann edges
+    // (always silhouettes), connected components (for soups of closed meshes)
+    std::map<std::pair<int, int>, std::vector<int>> edges;
+    for (int i = 0; i < nt; ++i)
+        for (int k = 0; k < 3; ++k) {
+            int a = s.idx[3 * i + k], b = s.idx[3 * i + (k + 1) % 3];
+            edges[{std::min(a, b), std::max(a, b)}].push_back(i);
+        }
+    std::vector<int> parent(nt);
+    std::iota(parent.begin(), parent.end(), 0);
+    std::function<int(int)> find = [&](int x) { return parent[x] == x ? x : parent[x] = find(parent[x]); };
+    s.triSil.assign(3 * static_cast<size_t>(nt), -1);
+    auto attach = [&](int tri, int id) {
+        for (int k = 0; k < 3; ++k)
+            if (s.triSil[3 * tri + k] < 0) { s.triSil[3 * tri + k] = id; return; }
+    };
+    for (const auto& [e, tris] : edges) {
+        for (size_t k = 1; k < tris.size(); ++k) parent[find(tris[k])] = find(tris[0]);
+        std::vector<int> neu;
+        bool dir = false;
+        for (int t : tris) if (s.label[t]) neu.push_back(t); else dir = true;
+        if (neu.empty() || dir) continue;  // no Neumann face, or a Dirichlet junction
+        const double* na = &s.normal[3 * static_cast<size_t>(neu[0])];
+        bool always = neu.size() != 2;     // open edge (or non-manifold: conservative)
+        const double* nb = neu.size() >= 2 ? &s.normal[3 * static_cast<size_t>(neu[1])] : na;
+        if (!always && na[0] == nb[0] && na[1] == nb[1] && na[2] == nb[2]) continue;  // coplanar: ties only
+        int id = static_cast<int>(s.sil3Always.size());
+        const double *pa = s.vert(e.first), *pb = s.vert(e.second);
+        s.sil3A.insert(s.sil3A.end(), pa, pa + 3);
+        s.sil3B.insert(s.sil3B.end(), pb, pb + 3);
+        s.sil3N1.insert(s.sil3N1.end(), na, na + 3);
+        s.sil3N2.insert(s.sil3N2.end(), nb, nb + 3);
+        s.sil3Always.push_back(always ? 1 : 0);
+        for (int t : neu) attach(t, id);
+    }
+    s.component.resize(nt);
+    std::map<int, int> comp;
+    for (int i = 0; i < nt; ++i) {
+        int r = find(i);
+        auto it = comp.find(r);
+        if (it == comp.end()) it = comp.emplace(r, static_cast<int>(comp.size())).first;
+        s.component[i] = it->second;
+    }
     return s;
+}
+
+// signed volume of a closed, outward-oriented triangle mesh (divergence theorem)
+double meshVolume(const HostScene& s) {
+    double v = 0.0;
+    for (int i = 0; i < s.ns; ++i) {
+        const double *a = s.vert(s.idx[3 * i]), *b = s.vert(s.idx[3 * i + 1]), *c = s.vert(s.idx[3 * i + 2]);
+        v += (a[0] * (b[1] * c[2] - b[2] * c[1]) - a[1] * (b[0] * c[2] - b[2] * c[0]) + a[2] * (b[0] * c[1] - b[1] * c[0])) / 6.0;
+    }
+    return v;
+}
+
+// 3D solve region (no reference path exists; the 2D construction is cache.cpp:137-246):
+// Neumann triangles are kept; vertices touched only by Dirichlet triangles move
+// inward by l along their angle-weighted normal; junction vertices stay, so the
+// Dirichlet patches bend down to the Neumann rim. Subdomain meshes pass through.
+HostRegion buildSolveRegion3(const HostScene& scene, int mode, double offset, const HostScene* sub, double epsilon) {
+    const double l = offset > 0.0 ? offset : 5.0 * epsilon;
+    if (!(l > epsilon)) throw Error(kInvalid, "region offset l must exceed epsilon");
+    HostRegion r;
+    if (mode == 1) {
+        if (!sub || sub->dim != 3) throw Error(kInvalid, "subdomain mode needs a region mesh");
+        r.boundary = *sub;
+        r.kinds.assign(sub->ns, 2);
+        r.source.assign(sub->ns, -1);
+        r.offset = l;
+        r.wholeDomain = false;
+        r.area = meshVolume(r.boundary);
+        if (!(r.area > 0.0)) throw Error(kParse, "subdomain region must be outward oriented with positive volume");
+        return r;
+    }
+    std::vector<double> vn(3 * static_cast<size_t>(scene.nv), 0.0);
+    std::vector<char> junction(scene.nv, 0);
+    for (int i = 0; i < scene.ns; ++i) {
+        for (int k = 0; k < 3; ++k) {
+            int v0 = scene.idx[3 * i + k], v1 = scene.idx[3 * i + (k + 1) % 3], v2 = scene.idx[3 * i + (k + 2) % 3];
+            if (scene.label[i]) { junction[v0] = 1; continue; }
+            const double *p0 = scene.vert(v0), *p1 = scene.vert(v1), *p2 = scene.vert(v2);
+            double e1[3], e2[3];
+            for (int d = 0; d < 3; ++d) { e1[d] = p1[d] - p0[d]; e2[d] = p2[d] - p0[d]; }
+            double l1 = std::sqrt(e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2]);
+            double l2 = std::sqrt(e2[0] * e2[0] + e2[1] * e2[1] + e2[2] * e2[2]);
+            double c = (e1[0] * e2[0] + e1[1] * e2[1] + e1[2] * e2[2]) / (l1 * l2);
+            double ang = std::acos(std::max(-1.0, std::min(1.0, c)));
+            for (int d = 0; d < 3; ++d) vn[3 * static_cast<size_t>(v0) + d] += ang * scene.normal[3 * static_cast<size_t>(i) + d];
+        }
+    }
+    std::vector<double> v(scene.v);
+    for (int i = 0; i < scene.nv; ++i) {
+        double* n = &vn[3 * static_cast<size_t>(i)];
+        double len = std::sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+        if (junction[i] || !(len > 0.0)) continue;
+        for (int d = 0; d < 3; ++d) v[3 * static_cast<size_t>(i) + d] -= l * n[d] / len;
+    }
+    r.boundary = buildMesh3(v.data(), scene.nv, scene.idx.data(), scene.label.data(), scene.ns);
+    r.kinds.resize(scene.ns);
+    r.source.resize(scene.ns);
+    for (int i = 0; i < scene.ns; ++i) {
+        r.kinds[i] = scene.label[i] ? 0 : 1;
+        r.source[i] = i;
+    }
+    r.offset = l;
+    r.wholeDomain = true;
+    r.area = meshVolume(r.boundary);
+    if (!(r.area > 0.0)) throw Error(kParse, "region offset produced a non-positive volume");
+    return r;
 }
 
 double loopArea(const HostScene& s) {
@@ -300,9 +411,9 @@ HostRegion assemble(const std::vector<std::vector<Chain>>& loops, double l, bool
 
 HostRegion buildSolveRegion(const HostScene& scene, int mode, double offset, const HostScene* sub,
                             double epsilon) {
+    if (scene.dim == 3) return buildSolveRegion3(scene, mode, offset, sub, epsilon);
     const double l = offset > 0.0 ? offset : 5.0 * epsilon;
     if (!(l > epsilon)) throw Error(kInvalid, "region offset l must exceed epsilon");
-    if (scene.dim != 2) throw Error(kSolver, "solve regions are built for 2D scenes only");
     const double weldTol = 1e-10 * std::max(scene.diagonal, 1e-30);
 
     if (mode == 1) {  // Subdomain: the user loop verbatim (cache.cpp:142-156)
@@ -418,6 +529,9 @@ int primClass(const HostScene& s, int i) {
     if (s.label[i] == 0) return 0;
     if (s.dim == 2 && (s.segSil[2 * static_cast<size_t>(i)] >= 0 || s.segSil[2 * static_cast<size_t>(i) + 1] >= 0))
         return 2;
+    if (s.dim == 3)
+        for (int k = 0; k < 3; ++k)
+            if (s.triSil[3 * static_cast<size_t>(i) + k] >= 0) return 2;
     return 1;
 }
 

@@ -37,6 +37,12 @@ struct HostScene {
     std::vector<double> silP, silN1, silN2;  // 2 per candidate
     std::vector<char> silAlways;
     std::vector<int> segSil;                 // 2 per segment, -1 = none
+    // 3D: silhouette EDGES between Neumann triangles (the 3D analogue of the
+    // candidate vertices): endpoints, adjacent face normals, open-edge flag
+    std::vector<double> sil3A, sil3B, sil3N1, sil3N2;  // 3 per edge
+    std::vector<char> sil3Always;
+    std::vector<int> triSil;                            // 3 per triangle, -1 = none
+    std::vector<int> component;                         // connected component per triangle
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     double diagonal = 0.0, dirichletMeasure = 0.0, neumannMeasure = 0.0, totalMeasure = 0.0;
 
@@ -65,6 +71,9 @@ struct HostRegion {
 
 HostRegion buildSolveRegion(const HostScene& scene, int mode, double offset, const HostScene* sub,
                             double epsilon);
+HostRegion buildSolveRegion3(const HostScene& scene, int mode, double offset, const HostScene* sub,
+                             double epsilon);
+double meshVolume(const HostScene& s);
 
 // BVH primitive class: 0 Dirichlet, 1 Neumann without silhouette candidates,
 // 2 Neumann with silhouette candidates (the only Neumann class star queries visit)

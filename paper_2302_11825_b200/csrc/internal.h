@@ -7,6 +7,7 @@
 
 #include "device_math.cuh"
 #include "host_scene.h"
+#include "scene3_dev.cuh"
 #include "scene_dev.cuh"
 
 namespace bvc_impl {
@@ -116,5 +117,59 @@ void launch_inside(const SceneView2& S, const double* x, int n, float tol, uint8
 
 // kernel-launch accounting (bench gpu_launches)
 void count_launch(int n = 1);
+
+// ---------------------------------------------------------------------------
+// 3D (triangle meshes; walk3.cu)
+// ---------------------------------------------------------------------------
+struct WalkEnv3 {
+    bvc_dev::SceneView3 S;
+    const int4* triSil;   // by triangle id: up to 3 silhouette-edge slots
+    const float4* silA;   // silhouette edge endpoints
+    const float4* silB;
+    const float4* silN1;  // adjacent Neumann face normals (silN1.w != 0: open edge)
+    const float4* silN2;
+    DevProblem P;
+    float eps, rmin, tguard, insideTol, scale, nudge;
+    float cx, cy, cz, escape;
+    int maxSteps;
+    int hasNeumann, hasH, closed;
+    uint32_t k0, k1;
+};
+
+struct WalkJob3 {
+    int nU, nPtsU;
+    const float4* startU;
+    const long long* gidU;
+    long long gidBaseU;
+    float* outU;
+    int* truncU;
+    int nD, nPtsD;
+    const float4* xD;
+    const float4* normalD;  // NULL => vector output (3 components)
+    const float* radiusD;
+    const long long* gidD;
+    float* outD;
+    int* truncD;
+    unsigned long long* truncTotal;
+    unsigned long long* steps;
+    unsigned long long* counter;
+};
+
+void launch_walk_job3(const WalkEnv3& env, const WalkJob3& job, cudaStream_t st);
+void launch_sample_mesh(const double* cdf, int m, double total, const float4* triA, const float4* triB,
+                        const float4* triC, const float4* triN, int count, int begin, int n, const long long* ctr,
+                        int stratified, uint32_t k0, uint32_t k1, CacheSample* out, cudaStream_t st);
+void launch_prepare3(const WalkEnv3& env, CacheSample* samples, int n, const int* kinds, float4* startU, int* isD,
+                     float* gradR, uint8_t* outside, cudaStream_t st);
+void launch_gather_dpoints3(const CacheSample* samples, const int* dIdx, int nD, const float* gradR, long long gidBase,
+                            const long long* gid, float4* xD, float4* nD_, float* rD, long long* gidD, cudaStream_t st);
+void launch_closest3(const bvc_dev::SceneView3& S, const double* x, int n, unsigned mask, double* point, double* dist,
+                     int* tri, cudaStream_t st);
+void launch_inside3(const bvc_dev::SceneView3& S, const double* x, int n, float tol, uint8_t* out, cudaStream_t st);
+void launch_mark3(const bvc_dev::SceneView3& scene, const bvc_dev::SceneView3& region, const double* x, int n,
+                  float offset, int whole, float insideTol, uint8_t* fb, uint8_t* gu, cudaStream_t st);
+// per-sample means of a 3D cache job (uHat from U walks, dHat from D samples)
+void launch_finish_samples(CacheSample* samples, int n, const float* outU, int nU, const int* dIdx, int nDpts,
+                           const float* outD, int nD, uint8_t* failed, cudaStream_t st);
 
 }  // namespace bvc_impl

@@ -1,0 +1,534 @@
+// walk3.cu — 3D walk-on-spheres / walk-on-stars on triangle meshes (sm_100a).
+//
+// The reference solver throws for dim != 2 (pointwise.cpp:23); BASELINE configs 4
+// and 5 are 3D triangle meshes, so this is the 3D lift of walk.cu with the same
+// execution model (warp-refilled lanes, Philox keyed by global task id, fixed
+// output slots). The estimator follows walkSampleImpl (pointwise.cpp:125-165):
+//   * star radius R = min(dist to Dirichlet, dist to visible Neumann silhouette
+//     EDGES), floored at rMin; termination within eps at g(closest point);
+//   * directions uniform on S^2, or on the hemisphere about the inward normal
+//     after a Neumann hit; Neumann hits by a first-hit ray query within R;
+//   * screened weight per step: ballSphereWeight 3D (kernels.cpp:63-65).
+// Gradient samples (the 3D gradientSample): v = (3/R) u(z) dir on the first ball,
+// plus, for screened kernels, grad G^B(x,R,y) sigma u(y) / pdf(y) with y drawn
+// from |G^B| of the 3D Poisson ball (radial CDF F(t) = 3t^2 - 2t^3) and u(y)
+// from a nested walk. Source terms (f) are not supported in 3D (the reference's
+// sampleBallGreens is 2D-only, kernels.cpp:98-99).
+#include <cuda_runtime.h>
+
+#include "internal.h"
+#include "scene3_dev.cuh"
+
+namespace bvc_impl {
+
+using namespace bvc_dev;
+
+namespace {
+
+constexpr int kThreads3 = 256;
+constexpr int kChunk3 = 64;
+
+__device__ __forceinline__ float g3(const WalkEnv3& E, const Closest3& c) { return field_eval(E.P.g, c.px, c.py, c.pz); }
+
+// silhouette edge k visible from x (the 3D analogue of scene.cpp:166-172)
+__device__ __forceinline__ bool sil_edge_ok(const WalkEnv3& E, int k, float x, float y, float z, float& d2) {
+    float4 a = E.silA[k], b = E.silB[k], n1 = E.silN1[k], n2 = E.silN2[k];
+    float ux = b.x - a.x, uy = b.y - a.y, uz = b.z - a.z;
+    float l2 = ux * ux + uy * uy + uz * uz;
+    float tt = l2 > 0.f ? ((x - a.x) * ux + (y - a.y) * uy + (z - a.z) * uz) / l2 : 0.f;
+    tt = fminf(fmaxf(tt, 0.f), 1.f);
+    float qx = a.x + tt * ux - x, qy = a.y + tt * uy - y, qz = a.z + tt * uz - z;
+    d2 = qx * qx + qy * qy + qz * qz;
+    if (n1.w != 0.f) return true;  // open boundary edge: silhouette from everywhere
+    float ax = a.x - x, ay = a.y - y, az = a.z - z;
+    float s1 = n1.x * ax + n1.y * ay + n1.z * az, s2 = n2.x * ax + n2.y * ay + n2.z * az;
+    return s1 * s2 <= 0.0f;
+}
+
+struct Star3 {
+    Closest3 D;
+    float s2;
+};
+
+__device__ __forceinline__ Star3 star_query3(const WalkEnv3& E, float x, float y, float z) {
+    Star3 q{Closest3{kFInf, 0.f, 0.f, 0.f, -1}, kFInf};
+    float eps2 = E.eps * E.eps;
+    traverse_near3(
+        E.S, x, y, z, kClsD | kClsSil,
+        [&](const Prim3& p) {
+            if (__float_as_int(p.b.w) == 0) {
+                float qx, qy, qz;
+                float d2 = tri_closest(p, x, y, z, qx, qy, qz);
+                if (d2 < q.D.d2) q.D = Closest3{d2, qx, qy, qz, __float_as_int(p.a.w)};
+            } else {
+                int4 sl = E.triSil[__float_as_int(p.a.w)];
+                float d2;
+                if (sl.x >= 0 && sil_edge_ok(E, sl.x, x, y, z, d2) && d2 < q.s2) q.s2 = d2;
+                if (sl.y >= 0 && sil_edge_ok(E, sl.y, x, y, z, d2) && d2 < q.s2) q.s2 = d2;
+                if (sl.z >= 0 && sil_edge_ok(E, sl.z, x, y, z, d2) && d2 < q.s2) q.s2 = d2;
+            }
+        },
+        [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); });
+    return q;
+}
+
+struct Hit3 {
+    float t;
+    int tri;
+};
+
+__device__ __forceinline__ Hit3 ray_neumann3(const WalkEnv3& E, float ox, float oy, float oz, float dx, float dy,
+                                             float dz, float tMax, int skip) {
+    Hit3 h{kFInf, -1};
+    float idx = 1.0f / dx, idy = 1.0f / dy, idz = 1.0f / dz;
+    float limit = tMax;
+    int stack[kStack];
+    int sp = 0, ref = 0;
+    for (;;) {
+        if (ref >= 0) {
+            const Node3 nd = E.S.nodes[ref];
+            count_fetch3(E.S, 0);
+            bool vl = (nd.mask & kClsNeumann) && ray_box3(nd.llo, nd.lhi, ox, oy, oz, idx, idy, idz, limit);
+            bool vr = ((nd.mask >> 3) & kClsNeumann) && ray_box3(nd.rlo, nd.rhi, ox, oy, oz, idx, idy, idz, limit);
+            if (vl && vr) { stack[sp++] = nd.right; ref = nd.left; continue; }
+            if (vl) { ref = nd.left; continue; }
+            if (vr) { ref = nd.right; continue; }
+        } else {
+            int code = ~ref;
+            int start = code >> 3, count = (code & 7) + 1;
+            for (int i = start; i < start + count; ++i) {
+                const Prim3 p = E.S.prims[i];
+                count_fetch3(E.S, 1);
+                int cls = __float_as_int(p.b.w), id = __float_as_int(p.a.w);
+                if (!((1u << cls) & kClsNeumann) || id == skip) continue;
+                float th;
+                if (ray_tri(p, ox, oy, oz, dx, dy, dz, limit, th) && th > E.tguard && th < h.t) {
+                    h = Hit3{th, id};
+                    limit = th;
+                }
+            }
+        }
+        if (sp == 0) return h;
+        ref = stack[--sp];
+    }
+}
+
+// uniform direction on S^2, or on the hemisphere about axis n (unit)
+__device__ __forceinline__ void sphere_dir(float u1, float u2, float& dx, float& dy, float& dz) {
+    float zc = 1.0f - 2.0f * u1;
+    float r = sqrtf(fmaxf(0.f, 1.f - zc * zc));
+    float s, c;
+    __sincosf(kTwoPi * u2, &s, &c);
+    dx = r * c; dy = r * s; dz = zc;
+}
+__device__ __forceinline__ void hemi_dir(float u1, float u2, float nx, float ny, float nz, float& dx, float& dy,
+                                         float& dz) {
+    float ct = u1;  // uniform solid angle on the hemisphere: cos(theta) uniform in [0, 1)
+    float st = sqrtf(fmaxf(0.f, 1.f - ct * ct));
+    float s, c;
+    __sincosf(kTwoPi * u2, &s, &c);
+    // orthonormal basis about n (Frisvad / Duff et al.)
+    float sign = copysignf(1.0f, nz);
+    float a = -1.0f / (sign + nz), b = nx * ny * a;
+    float t1x = 1.0f + sign * nx * nx * a, t1y = sign * b, t1z = -sign * nx;
+    float t2x = b, t2y = sign + ny * ny * a, t2z = -ny;
+    dx = st * (c * t1x + s * t2x) + ct * nx;
+    dy = st * (c * t1y + s * t2y) + ct * ny;
+    dz = st * (c * t1z + s * t2z) + ct * nz;
+}
+
+// 3D ballSphereWeight (kernels.cpp:63-65); (tR) / sinh(tR) on the sphere
+__device__ __forceinline__ float sphere_weight3(float s, float R, float rHit) {
+    float tR = R * s;
+    float a = (R - rHit) * s;
+    float e = __expf(-tR);
+    float shR = 0.5f * (1.0f - e * e);  // sinh(tR) e^{-tR}
+    float ea = __expf(a - tR);
+    float ch = 0.5f * (ea + __expf(-a - tR)), sh = 0.5f * (ea - __expf(-a - tR));  // cosh(a), sinh(a) times e^{-tR}
+    return (rHit * s * ch + sh) / shR;
+}
+
+struct Walk3 {
+    float x, y, z, weight;
+    float inx, iny, inz;
+    int onN, prevTri, step;
+};
+
+__device__ __forceinline__ void walk3_start(Walk3& w, float x, float y, float z) {
+    w.x = x; w.y = y; w.z = z; w.weight = 1.f; w.inx = w.iny = w.inz = 0.f; w.onN = 0; w.prevTri = -1; w.step = 0;
+}
+
+__device__ __forceinline__ bool walk3_step(const WalkEnv3& E, Walk3& w, U4 rnd, float& value, int& trunc,
+                                           unsigned long long& steps) {
+    ++steps;
+    Closest3 cp;
+    float R;
+    if (E.hasNeumann) {
+        Star3 q = star_query3(E, w.x, w.y, w.z);
+        cp = q.D;
+        float dD = sqrtf(cp.d2);
+        if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
+        R = fminf(dD, sqrtf(q.s2));
+    } else {
+        cp = closest_point3(E.S, w.x, w.y, w.z, kClsD);
+        float dD = sqrtf(cp.d2);
+        if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
+        R = dD;
+    }
+    R = fmaxf(R, E.rmin);
+    float dx, dy, dz;
+    if (w.onN) hemi_dir(u01(rnd.x), u01(rnd.y), w.inx, w.iny, w.inz, dx, dy, dz);
+    else sphere_dir(u01(rnd.x), u01(rnd.y), dx, dy, dz);
+    float travel = R;
+    bool hit = false;
+    if (E.hasNeumann) {
+        Hit3 h = ray_neumann3(E, w.x, w.y, w.z, dx, dy, dz, R, w.onN ? w.prevTri : -1);
+        if (h.tri >= 0) {
+            hit = true;
+            travel = h.t;
+            float4 n = E.S.triNormal[h.tri];
+            if (E.closed || n.x * dx + n.y * dy + n.z * dz > 0.f) { w.inx = -n.x; w.iny = -n.y; w.inz = -n.z; }
+            else { w.inx = n.x; w.iny = n.y; w.inz = n.z; }
+            w.x = fmaf(h.t, dx, w.x) + E.nudge * w.inx;
+            w.y = fmaf(h.t, dy, w.y) + E.nudge * w.iny;
+            w.z = fmaf(h.t, dz, w.z) + E.nudge * w.inz;
+            w.onN = 1;
+            w.prevTri = h.tri;
+        }
+    }
+    if (!hit) {
+        w.x = fmaf(R, dx, w.x);
+        w.y = fmaf(R, dy, w.y);
+        w.z = fmaf(R, dz, w.z);
+        w.onN = 0;
+        w.prevTri = -1;
+    }
+    if (E.P.screened) w.weight *= sphere_weight3(E.P.sqrtSigma, R, travel);
+    bool escaped = fabsf(w.x - E.cx) > E.escape || fabsf(w.y - E.cy) > E.escape || fabsf(w.z - E.cz) > E.escape;
+    if (++w.step >= E.maxSteps || escaped) {
+        trunc = 1;
+        Closest3 c = closest_point3(E.S, w.x, w.y, w.z, kClsD);
+        value = w.weight * g3(E, c);
+        return true;
+    }
+    return false;
+}
+
+// radial CDF of |G^B| in the 3D Poisson ball: F(t) = 3 t^2 - 2 t^3
+__device__ __forceinline__ float invert_ball_cdf3(float u) {
+    float t = sqrtf(u / 3.0f) * 1.2f;
+    t = fminf(fmaxf(t, 1e-6f), 1.0f);
+#pragma unroll 1
+    for (int it = 0; it < 30; ++it) {
+        float f = t * t * (3.0f - 2.0f * t) - u, d = 6.0f * t * (1.0f - t);
+        float nt = d > 0.f ? t - f / d : t;
+        nt = fminf(fmaxf(nt, 0.5f * t), fminf(1.0f, 1.5f * t + 1e-6f));
+        if (fabsf(nt - t) < 1e-7f) return nt;
+        t = nt;
+    }
+    return t;
+}
+
+struct Task3 {
+    long long id;
+    unsigned long long rid;
+    int role, pt, phase;
+    uint32_t draw;
+    float R, dx, dy, dz, vx, vy, vz, cx, cy, cz, y2x, y2y, y2z;
+    int trunc;
+};
+
+__device__ __forceinline__ U4 draw3(const WalkEnv3& E, Task3& t) {
+    U4 c{static_cast<uint32_t>(t.rid), static_cast<uint32_t>(t.rid >> 32), t.draw++, static_cast<uint32_t>(t.role)};
+    return philox4x32_10(c, E.k0, E.k1);
+}
+
+__global__ void __launch_bounds__(kThreads3) walk3_kernel(const WalkEnv3 E, const WalkJob3 J) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const long long nUtot = static_cast<long long>(J.nPtsU) * J.nU;
+    const long long total = nUtot + static_cast<long long>(J.nPtsD) * J.nD;
+    long long qNext = 0, qEnd = 0;
+    bool exhausted = false, active = false;
+    Task3 t;
+    Walk3 w;
+    unsigned long long steps = 0;
+    for (;;) {
+        unsigned need = __ballot_sync(0xffffffffu, !active);
+        while (need && !exhausted) {
+            if (qNext >= qEnd) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(J.counter, static_cast<unsigned long long>(kChunk3));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (static_cast<long long>(base) >= total) { exhausted = true; break; }
+                qNext = static_cast<long long>(base);
+                qEnd = min(qNext + kChunk3, total);
+            }
+            int take = static_cast<int>(min(static_cast<long long>(__popc(need)), qEnd - qNext));
+            int rank = __popc(need & lt);
+            if (((need >> lane) & 1u) && rank < take) {
+                long long id = qNext + rank;
+                t.id = id;
+                t.draw = 0;
+                t.phase = 0;
+                t.trunc = 0;
+                if (id < nUtot) {
+                    t.role = 0;
+                    t.pt = static_cast<int>(id / J.nU);
+                    int k = static_cast<int>(id - static_cast<long long>(t.pt) * J.nU);
+                    long long g = J.gidU ? J.gidU[t.pt] : J.gidBaseU + t.pt;
+                    t.rid = static_cast<unsigned long long>(g) * J.nU + k;
+                    float4 s = J.startU[t.pt];
+                    walk3_start(w, s.x, s.y, s.z);
+                } else {
+                    long long d = id - nUtot;
+                    t.role = 1;
+                    t.pt = static_cast<int>(d / J.nD);
+                    int k = static_cast<int>(d - static_cast<long long>(t.pt) * J.nD);
+                    long long g = J.gidD ? J.gidD[t.pt] : t.pt;
+                    t.rid = static_cast<unsigned long long>(g) * J.nD + k;
+                    float4 c = J.xD[t.pt];
+                    t.R = J.radiusD[t.pt];
+                    U4 r0 = draw3(E, t);
+                    U4 r1 = draw3(E, t);
+                    sphere_dir(u01(r0.x), u01(r0.y), t.dx, t.dy, t.dz);
+                    t.vx = t.vy = t.vz = 0.f;
+                    if (E.P.screened && E.P.sigma > 0.f) {
+                        // y ~ |G^B| in the Poisson ball, grad G^B (kernels.cpp:68-75, 3D) sigma / pdf
+                        float tt = invert_ball_cdf3(u01(r0.z));
+                        float r = fmaxf(tt * t.R, 1e-6f * t.R);
+                        float ex, ey, ez;
+                        sphere_dir(u01(r0.w), u01(r1.x), ex, ey, ez);
+                        float gb = (1.0f / t.R - 1.0f / r) * kInv4Pi;            // G^B 3D
+                        float pdf = gb / (-t.R * t.R / 6.0f);                     // / mass
+                        float gf = (1.0f / (t.R * t.R * t.R) - 1.0f / (r * r * r)) * kInv4Pi * (E.P.sigma / pdf);
+                        t.cx = r * ex * gf; t.cy = r * ey * gf; t.cz = r * ez * gf;
+                        t.y2x = c.x + r * ex; t.y2y = c.y + r * ey; t.y2z = c.z + r * ez;
+                    }
+                    float rr = t.R * 0.99999952f;
+                    walk3_start(w, fmaf(rr, t.dx, c.x), fmaf(rr, t.dy, c.y), fmaf(rr, t.dz, c.z));
+                }
+                active = true;
+            }
+            qNext += take;
+            need = __ballot_sync(0xffffffffu, !active);
+        }
+        if (__ballot_sync(0xffffffffu, active) == 0u) break;
+        if (active) {
+            U4 rnd = draw3(E, t);
+            float value;
+            if (walk3_step(E, w, rnd, value, t.trunc, steps)) {
+                if (t.role == 0) {
+                    J.outU[t.id] = value;
+                    if (t.trunc && J.truncU) atomicAdd(J.truncU + t.pt, 1);
+                    if (t.trunc && J.truncTotal) atomicAdd(J.truncTotal, 1ull);
+                    active = false;
+                } else if (t.phase == 0) {
+                    float s = (3.0f / t.R) * value;
+                    t.vx = fmaf(s, t.dx, t.vx);
+                    t.vy = fmaf(s, t.dy, t.vy);
+                    t.vz = fmaf(s, t.dz, t.vz);
+                    if (E.P.screened && E.P.sigma > 0.f) {
+                        t.phase = 1;
+                        walk3_start(w, t.y2x, t.y2y, t.y2z);
+                    } else {
+                        active = false;
+                    }
+                } else {
+                    t.vx = fmaf(t.cx, value, t.vx);
+                    t.vy = fmaf(t.cy, value, t.vy);
+                    t.vz = fmaf(t.cz, value, t.vz);
+                    active = false;
+                }
+                if (!active && t.role == 1) {
+                    long long slot = t.id - nUtot;
+                    if (J.normalD) {
+                        float4 n = J.normalD[t.pt];
+                        J.outD[slot] = n.x * t.vx + n.y * t.vy + n.z * t.vz;
+                    } else {
+                        J.outD[3 * slot] = t.vx;
+                        J.outD[3 * slot + 1] = t.vy;
+                        J.outD[3 * slot + 2] = t.vz;
+                    }
+                    if (t.trunc && J.truncD) atomicAdd(J.truncD + t.pt, 1);
+                    if (t.trunc && J.truncTotal) atomicAdd(J.truncTotal, 1ull);
+                }
+            }
+        }
+    }
+    if (J.steps) {
+        for (int o = 16; o > 0; o >>= 1) steps += __shfl_xor_sync(0xffffffffu, steps, o);
+        if (lane == 0) atomicAdd(J.steps, steps);
+    }
+}
+
+// area-uniform boundary samples (the 3D BoundarySampler): the stratified CDF
+// coordinate picks the triangle, its in-triangle remainder and a second
+// uniform give uniform barycentrics
+__global__ void sample_mesh_kernel(const double* cdf, int m, double total, const float4* triA, const float4* triB,
+                                   const float4* triC, const float4* triN, int count, int begin, int n,
+                                   const long long* ctr, int stratified, uint32_t k0, uint32_t k1, CacheSample* out) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    long long k = ctr ? ctr[j] : static_cast<long long>(begin) + j;
+    U4 r = philox4x32_10(U4{static_cast<uint32_t>(k), static_cast<uint32_t>(k >> 32), 0u, 0u}, k0, k1);
+    double U = (static_cast<double>(r.x >> 5) * 67108864.0 + static_cast<double>(r.y >> 6)) * (1.0 / 9007199254740992.0);
+    double u = stratified ? (static_cast<double>(k) + U) / count : U;
+    double target = u * total;
+    int lo = 0, hi = m;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (cdf[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    int id = lo >= m ? m - 1 : lo;
+    double prev = id > 0 ? cdf[id - 1] : 0.0;
+    double f = fmin(fmax((target - prev) / (cdf[id] - prev), 0.0), 1.0);
+    float r1 = sqrtf(static_cast<float>(f)), r2 = u01(r.z);
+    float wa = 1.f - r1, wb = r1 * (1.f - r2), wc = r1 * r2;
+    float4 a = triA[id], b = triB[id], c = triC[id], nn = triN[id];
+    CacheSample o;
+    o.z[0] = wa * a.x + wb * b.x + wc * c.x;
+    o.z[1] = wa * a.y + wb * b.y + wc * c.y;
+    o.z[2] = wa * a.z + wb * b.z + wc * c.z;
+    o.n[0] = nn.x; o.n[1] = nn.y; o.n[2] = nn.z;
+    o.pdf = static_cast<float>(1.0 / total);
+    o.uHat = 0.f; o.dHat = 0.f; o.weight = 0.f; o.arc = 0.f;
+    o.segment = id;
+    out[j] = o;
+}
+
+__global__ void prepare3_kernel(const WalkEnv3 E, CacheSample* samples, int n, const int* kinds, float4* startU,
+                                int* isD, float* gradR, uint8_t* outside) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    CacheSample s = samples[i];
+    float x = s.z[0], y = s.z[1], z = s.z[2];
+    if (kinds[s.segment] == 0) {  // known Neumann: half a shell inside, d = h(z)
+        x -= 0.5f * E.eps * s.n[0];
+        y -= 0.5f * E.eps * s.n[1];
+        z -= 0.5f * E.eps * s.n[2];
+        samples[i].dHat = E.hasH ? field_eval(E.P.h, s.z[0], s.z[1], s.z[2]) : 0.f;
+        isD[i] = 0;
+        gradR[i] = 0.f;
+    } else {
+        isD[i] = 1;
+        Closest3 c = closest_point3(E.S, x, y, z, kClsAny);
+        gradR[i] = fmaxf(sqrtf(c.d2), E.rmin);
+    }
+    startU[i] = make_float4(x, y, z, 0.f);
+    outside[i] = (E.insideTol < 0.f || inside3(E.S, x, y, z, E.insideTol)) ? 0 : 1;
+}
+
+__global__ void gather_dpoints3_kernel(const CacheSample* samples, const int* dIdx, int nD, const float* gradR,
+                                       long long gidBase, const long long* gid, float4* xD, float4* nD_, float* rD,
+                                       long long* gidD) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nD) return;
+    int i = dIdx[j];
+    CacheSample s = samples[i];
+    xD[j] = make_float4(s.z[0], s.z[1], s.z[2], 0.f);
+    nD_[j] = make_float4(s.n[0], s.n[1], s.n[2], 0.f);
+    rD[j] = gradR[i];
+    gidD[j] = gid ? gid[i] : gidBase + i;
+}
+
+__global__ void closest3_kernel(const SceneView3 S, const double* x, int n, unsigned mask, double* point, double* dist,
+                                int* tri) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Closest3 c = closest_point3(S, static_cast<float>(x[3 * i]), static_cast<float>(x[3 * i + 1]),
+                                static_cast<float>(x[3 * i + 2]), mask);
+    point[3 * i] = c.px; point[3 * i + 1] = c.py; point[3 * i + 2] = c.pz;
+    dist[i] = c.tri >= 0 ? sqrt(static_cast<double>(c.d2)) : INFINITY;
+    tri[i] = c.tri;
+}
+
+__global__ void inside3_kernel(const SceneView3 S, const double* x, int n, float tol, uint8_t* out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = inside3(S, static_cast<float>(x[3 * i]), static_cast<float>(x[3 * i + 1]), static_cast<float>(x[3 * i + 2]),
+                     tol) ? 1 : 0;
+}
+
+// fallback band in 3D: within l of the Dirichlet boundary (cache.cpp:131-135) or, for a
+// closed region mesh, outside it — the vertex-normal offset surface is not exactly at
+// distance l, and a point outside the region would get the exterior value of the BIE
+__global__ void mark3_kernel(const SceneView3 scene, const SceneView3 region, const double* x, int n, float offset,
+                             int whole, float insideTol, uint8_t* fb, uint8_t* gu) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float px = static_cast<float>(x[3 * i]), py = static_cast<float>(x[3 * i + 1]), pz = static_cast<float>(x[3 * i + 2]);
+    uint8_t f = 0;
+    if (whole) {
+        Closest3 c = closest_point3(scene, px, py, pz, kClsD);
+        f = (c.tri >= 0 && c.d2 < offset * offset) ? 1 : 0;
+        if (!f && insideTol > 0.f && !inside3(region, px, py, pz, insideTol)) f = 1;
+    }
+    Closest3 r = closest_point3(region, px, py, pz, kClsAny);
+    fb[i] = f;
+    gu[i] = (r.tri >= 0 && r.d2 < offset * offset) ? 1 : 0;
+}
+
+inline int blocks(long long n, int t) { return static_cast<int>((n + t - 1) / t); }
+
+}  // namespace
+
+void launch_walk_job3(const WalkEnv3& env, const WalkJob3& job, cudaStream_t st) {
+    long long total = static_cast<long long>(job.nPtsU) * job.nU + static_cast<long long>(job.nPtsD) * job.nD;
+    if (total <= 0) return;
+    cudaMemsetAsync(job.counter, 0, sizeof(unsigned long long), st);
+    int dev = 0, sms = 148, perSm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, walk3_kernel, kThreads3, 0);
+    perSm = perSm > 0 ? perSm : 1;
+    long long want = (total + kThreads3 - 1) / kThreads3;
+    int grid = static_cast<int>(want < static_cast<long long>(sms) * perSm ? want : static_cast<long long>(sms) * perSm);
+    walk3_kernel<<<grid, kThreads3, 0, st>>>(env, job);
+    count_launch();
+}
+
+void launch_sample_mesh(const double* cdf, int m, double total, const float4* triA, const float4* triB,
+                        const float4* triC, const float4* triN, int count, int begin, int n, const long long* ctr,
+                        int stratified, uint32_t k0, uint32_t k1, CacheSample* out, cudaStream_t st) {
+    if (n <= 0) return;
+    sample_mesh_kernel<<<blocks(n, 256), 256, 0, st>>>(cdf, m, total, triA, triB, triC, triN, count, begin, n, ctr,
+                                                      stratified, k0, k1, out);
+    count_launch();
+}
+
+void launch_prepare3(const WalkEnv3& env, CacheSample* samples, int n, const int* kinds, float4* startU, int* isD,
+                     float* gradR, uint8_t* outside, cudaStream_t st) {
+    if (n <= 0) return;
+    prepare3_kernel<<<blocks(n, 128), 128, 0, st>>>(env, samples, n, kinds, startU, isD, gradR, outside);
+    count_launch();
+}
+
+void launch_gather_dpoints3(const CacheSample* samples, const int* dIdx, int nD, const float* gradR, long long gidBase,
+                            const long long* gid, float4* xD, float4* nD_, float* rD, long long* gidD, cudaStream_t st) {
+    if (nD <= 0) return;
+    gather_dpoints3_kernel<<<blocks(nD, 256), 256, 0, st>>>(samples, dIdx, nD, gradR, gidBase, gid, xD, nD_, rD, gidD);
+    count_launch();
+}
+
+void launch_closest3(const SceneView3& S, const double* x, int n, unsigned mask, double* point, double* dist, int* tri,
+                     cudaStream_t st) {
+    if (n <= 0) return;
+    closest3_kernel<<<blocks(n, 128), 128, 0, st>>>(S, x, n, mask, point, dist, tri);
+    count_launch();
+}
+
+void launch_inside3(const SceneView3& S, const double* x, int n, float tol, uint8_t* out, cudaStream_t st) {
+    if (n <= 0) return;
+    inside3_kernel<<<blocks(n, 128), 128, 0, st>>>(S, x, n, tol, out);
+    count_launch();
+}
+
+void launch_mark3(const SceneView3& scene, const SceneView3& region, const double* x, int n, float offset, int whole,
+                  float insideTol, uint8_t* fb, uint8_t* gu, cudaStream_t st) {
+    if (n <= 0) return;
+    mark3_kernel<<<blocks(n, 128), 128, 0, st>>>(scene, region, x, n, offset, whole, insideTol, fb, gu);
+    count_launch();
+}
+
+}  // namespace bvc_impl

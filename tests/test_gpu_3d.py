@@ -1,0 +1,121 @@
+"""3D triangle-mesh path (BASELINE configs 4-5). The reference has no 3D walks
+(pointwise.cpp:23), so walk parity is against closed forms: on a sphere with
+harmonic Dirichlet data u = g; the 3D gather is pinned against the restated loop
+in test_gpu_gather.py::test_gather_parity_3d."""
+import numpy as np
+import pytest
+
+import paper_2302_11825_b200 as B
+from paper_2302_11825_b200 import abi, configs
+
+pytestmark = pytest.mark.gpu
+
+HARMONIC = abi.make_field(abi.FIELD_QUADRATIC3, [0.1, 0.3, -0.2, 0.5, -0.5, -0.5, 1.0, 1.0, 0.0, 0.0])
+
+
+def g_exact(x):
+    return 0.1 + 0.3 * x[:, 0] - 0.2 * x[:, 1] + 0.5 * x[:, 2] - 0.5 * x[:, 0] ** 2 - 0.5 * x[:, 1] ** 2 + \
+        x[:, 2] ** 2 + x[:, 0] * x[:, 1]
+
+
+def grad_exact(x):
+    return np.stack([0.3 - x[:, 0] + x[:, 1], -0.2 - x[:, 1] + x[:, 0], 0.5 + 2 * x[:, 2]], 1)
+
+
+@pytest.fixture(scope="module")
+def sphere():
+    V, F = configs.icosphere(4)
+    return V, F, B.Scene.mesh3(V, F, np.zeros(len(F), np.int32))
+
+
+def test_mesh_queries(sphere):
+    V, F, sc = sphere
+    rng = np.random.default_rng(1)
+    x = rng.normal(size=(2000, 3))
+    x *= (rng.uniform(0.0, 1.3, 2000) / np.linalg.norm(x, axis=1))[:, None]
+    p, d, tri, _ = sc.closest_point(x)
+    # brute force over all triangles (vertex/edge/face distance via dense sampling is too coarse; use the
+    # support-plane distance as a lower bound and the returned point's distance as exact)
+    r = np.linalg.norm(x, axis=1)
+    inner = np.min(np.linalg.norm(V, axis=1))
+    assert np.all(tri >= 0)
+    assert np.all(np.abs(np.linalg.norm(p - x, axis=1) - d) < 1e-5)
+    assert np.all(d <= np.abs(r - 1.0) + 0.02)  # the polyhedron is within 1 - inner of the sphere
+    ins = sc.inside(x)
+    assert np.all(ins[r < inner - 1e-3]) and not np.any(ins[r > 1.0 + 1e-3])
+
+
+def test_cache_3d_closed_form(sphere):
+    V, F, sc = sphere
+    pb = B.problem(B.poisson(3), g=HARMONIC)
+    region = B.SolveRegion(sc, offset=0.05, epsilon=1e-3)
+    cfg = B.cache_config(B.walk_config(epsilon=1e-3), nBoundary=512, nWalksNeumann=256, nWalksDirichlet=1024,
+                         offset=0.05)
+    st = {}
+    c = B.generate_boundary_cache(sc, pb, region, cfg, 3, 0, stats=st).download()
+    assert c["z"].shape == (512, 3) and st["cacheWalks"] == 512 * (256 + 1024)
+    du = c["uHat"] - g_exact(c["z"])
+    dd = c["dHat"] - np.sum(c["n"] * grad_exact(c["z"]), 1)
+    assert abs(du.mean()) <= 4 * du.std(ddof=1) / np.sqrt(len(du)) + 2e-3   # O(eps) shell bias allowance
+    assert abs(dd.mean()) <= 4 * dd.std(ddof=1) / np.sqrt(len(dd))
+    assert du.std() < 0.05
+
+
+def test_update_solution_3d_matches_harmonic_data(sphere):
+    V, F, sc = sphere
+    pb = B.problem(B.poisson(3), g=HARMONIC)
+    region = B.SolveRegion(sc, offset=0.02, epsilon=1e-3)
+    cfg = B.cache_config(B.walk_config(epsilon=1e-3, nWalks=256), nBoundary=8192, nWalksNeumann=64,
+                         nWalksDirichlet=256, offset=0.02)
+    rng = np.random.default_rng(2)
+    x = rng.normal(size=(4000, 3))
+    x *= (0.99 * rng.uniform(0, 1, 4000) ** (1 / 3) / np.linalg.norm(x, axis=1))[:, None]
+    x = x[sc.inside(x)]
+    pts = B.EvaluationPoints(x, 3)
+    B.mark_evaluation_points(sc, region, cfg, pts)
+    for r in range(4):
+        B.update_solution(sc, pb, region, cfg, pts, 9, r, gradients=True)
+    st = pts.download()
+    u = pts.solution(st)
+    fb = st["fallback"]
+    assert fb.sum() > 0 and np.all(st["walkCount"][fb] == 4 * 256), (fb.sum(), st["walkCount"][fb][:5])
+    err = u - g_exact(x)
+    assert np.all(np.isfinite(u))
+    # away from the region boundary (the splat estimate is heavy-tailed within a sample
+    # spacing of the cache surface, as in 2D)
+    deep = np.linalg.norm(x, axis=1) < 0.9
+    rms_in, rms_fb = np.sqrt(np.mean(err[deep] ** 2)), np.sqrt(np.mean(err[fb] ** 2))
+    assert rms_in < 0.05 and rms_fb < 0.05, (rms_in, rms_fb)
+    # unbiasedness: all points of one round share one cache, so their errors are one
+    # correlated field; independent rounds are the unit of replication
+    means = []
+    for r in range(8):
+        p = B.EvaluationPoints(x[deep], 3)
+        B.mark_evaluation_points(sc, region, cfg, p)
+        B.update_solution(sc, pb, region, cfg, p, 100 + r, 0)
+        means.append(np.mean(p.solution() - g_exact(x[deep])))
+    means = np.array(means)
+    assert abs(means.mean()) <= 4 * means.std(ddof=1) / np.sqrt(len(means)) + 2e-3, means
+    u2, g2 = pts.read_solution(gradient=True)
+    assert np.allclose(u2, u, rtol=1e-12, atol=1e-12) and g2.shape == (len(x), 3)
+
+
+def test_screened_mixed_3d_runs_and_is_bounded():
+    """C5-style physics on one sphere: screened sigma = 1, Neumann cap (n.z > 0.5) with h = 0,
+    Dirichlet g = 1 elsewhere: 0 < u <= 1 (maximum principle) and deterministic per seed."""
+    V, F = configs.icosphere(4)
+    n = np.cross(V[F[:, 1]] - V[F[:, 0]], V[F[:, 2]] - V[F[:, 0]])
+    lab = (n[:, 2] / np.linalg.norm(n, axis=1) > 0.5).astype(np.int32)
+    sc = B.Scene.mesh3(V, F, lab)
+    pb = B.problem(B.screened(1.0, 3), g=abi.make_field(abi.FIELD_CONSTANT, [1.0]))
+    region = B.SolveRegion(sc, offset=0.02, epsilon=1e-3)
+    cfg = B.cache_config(B.walk_config(epsilon=1e-3, nWalks=64), nBoundary=1024, nWalksNeumann=64,
+                         nWalksDirichlet=64, offset=0.02)
+    st = {}
+    c = B.generate_boundary_cache(sc, pb, region, cfg, 5, 0, stats=st).download()
+    kinds = region.kinds[c["segment"]]
+    assert np.all(c["dHat"][kinds == abi.SEG_KNOWN_NEUMANN] == 0.0)
+    assert np.all((c["uHat"] > 0) & (c["uHat"] <= 1.0 + 1e-6))
+    c2 = B.generate_boundary_cache(sc, pb, region, cfg, 5, 0).download()
+    assert np.array_equal(c["uHat"], c2["uHat"])
+    assert st["cacheTruncated"] <= 1e-4 * st["cacheWalks"]
