@@ -307,6 +307,10 @@ def phase_breakdown(B, c, scene, region, pts, args):
                      "traffic": (ncu_traffic("walk") or {}).get("bytes"),
                      "traffic_source": (ncu_traffic("walk") or {}).get("source"),
                      "algorithmic_bytes_per_launch": walk_bytes,
+                     "note": ("algorithmic bytes = BVH node (48 B) + primitive (32 B) fetches + 32 B walk state per "
+                              "step (SURVEY §8d); the scene is L1/L2-resident (ncu: DRAM traffic per launch is the "
+                              "`traffic` field), so the fraction of the HBM copy peak can exceed 1 — the kernel is "
+                              "issue/latency-bound, see profiles/"),
                      "algorithmic_bytes_per_step": bytes_per_step,
                      "node_fetches_per_step": prof["node_fetches"] / steps,
                      "prim_fetches_per_step": prof["prim_fetches"] / steps, "peak_source": peaks["source"],
