@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define BVC_ABI_VERSION 1
+#define BVC_ABI_VERSION 2
 
 /* ---- status codes (exception classes of the reference) ------------------- */
 typedef enum {
@@ -109,8 +109,8 @@ typedef struct {
     int nWalksDirichlet; /* du/dn walk budget, default 160 */
     double offset;       /* l; 0 => 5 epsilon */
     double clamp;        /* c; 0 => 10 / diagonal */
-    int clampMode;       /* bvc_clamp_mode; only OFF is implemented on the GPU (§8f.3) */
-    int sourceBall;      /* ball-kernel source mode; not implemented (§8f.3) */
+    int clampMode;       /* bvc_clamp_mode */
+    int sourceBall;      /* ball-kernel source mode (Poisson, 2D) */
     int correctionWalks; /* default 4 */
     int voronoi;         /* Voronoi weights instead of 1/(N pdf) */
     int stratified;      /* default 1 */
@@ -145,7 +145,7 @@ typedef struct {
     bvc_kernel_spec kernel; /* scale = scene diagonal */
     double coincidenceTol;  /* 1e-12 x diagonal */
     int voronoi;
-    int useBallGreens;      /* not implemented on the GPU (§8f.3) */
+    int useBallGreens;      /* G -> G^B(x, ballRadius) in the d-hat and source terms */
 } bvc_splat_config;
 
 /* CachedBoundarySample (cache.h:43-52), host AoS exchange format (2D or 3D) */
@@ -180,6 +180,7 @@ typedef struct {
     double* gradientWalkSum;   /* dim*count */
     long long* gradientWalkCount;
     long long* skipped;
+    double* ballRadius;        /* ball-kernel mode radius (cache.h:77) */
 } bvc_point_state;
 
 typedef struct bvc_region_s* bvc_region;
@@ -291,6 +292,35 @@ int bvc_splat_solution_gradient(bvc_boundary_cache bcache, bvc_source_cache scac
 int bvc_splat_range(bvc_boundary_cache bcache, bvc_source_cache scache, bvc_eval_points pts,
                     const bvc_splat_config* cfg, size_t begin, size_t end, int value,
                     int gradient);
+
+/* BoundaryEvaluator (cache.h:175-176): the u(z) estimate the clamp correction
+   multiplies each saturated crossing by. A std::function cannot cross the C ABI or
+   run on the device, so it is one of: NONE (the empty callback), FIELD (exact data
+   u(z) = field(z), e.g. the tests' constant evaluators), or WALKS (the default
+   evaluator of updateSolution, makeDefaultEvaluator cache.cpp:600-620:
+   cfg->correctionWalks WoSt walks in `scene` from each crossing, KnownNeumann
+   crossings shifted eps/2 inside). */
+typedef enum { BVC_EVALUATOR_NONE = 0, BVC_EVALUATOR_FIELD = 1, BVC_EVALUATOR_WALKS = 2 } bvc_evaluator_kind;
+typedef struct {
+    int kind;                     /* bvc_evaluator_kind */
+    bvc_field field;              /* FIELD */
+    bvc_scene scene;              /* WALKS */
+    const bvc_problem* problem;   /* WALKS */
+    const bvc_cache_config* cfg;  /* WALKS: walk settings and correctionWalks */
+} bvc_boundary_evaluator;
+
+/* correctedBoundarySplat (cache.h:178-184; cache.cpp:499-553): boundary splat with
+   dG/dn clamped to [-c, c]; CLAMP_CORRECT adds one ray-sampled correction per point
+   (RNG keyed by (seed, stream, point index)). eval may be NULL for CLAMP_ONLY. */
+int bvc_corrected_boundary_splat(bvc_boundary_cache bcache, bvc_eval_points pts, bvc_region region,
+                                 const bvc_splat_config* cfg, double clampBound, int clampMode,
+                                 const bvc_boundary_evaluator* eval, uint64_t seed, uint64_t stream);
+/* correctedSourceSplat (cache.h:186-191; cache.cpp:555-597): source splat through the
+   clamped ball kernel G^B plus one ball-sampled correction per point when clampBound
+   is finite and f is not NULL / NONE. 2D Poisson only; points need ball radii. */
+int bvc_corrected_source_splat(bvc_source_cache scache, bvc_eval_points pts, bvc_region region,
+                               const bvc_splat_config* cfg, double clampBound, const bvc_field* f,
+                               uint64_t seed, uint64_t stream);
 
 /* ---- one progressive round (updateSolution cache.h:195-198; cache.cpp:622-684) */
 int bvc_update_solution(bvc_scene scene, const bvc_problem* problem, bvc_region region,

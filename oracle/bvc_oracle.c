@@ -1023,3 +1023,57 @@ int or_splat(const bvc_kernel_spec* spec, double coincidence_tol, int voronoi, i
     }
     return 0;
 }
+
+/* The clamped and ball-kernel splat loops, value only, 2D (mode bits as the GPU's
+   gather.cu SplatMode):
+     1  dG/dn clamped to [-c, c]  correctedBoundarySplat cache.cpp:512-524 (kernels.h:52)
+     2  G -> G^B(x, R_x)           greensValue cache.cpp:410-416 (ballGreens kernels.cpp:31-43)
+     4  source G^B clamped         correctedSourceSplat cache.cpp:573-582
+   The sampled correction terms (cache.cpp:526-550, 584-592) are random and are
+   checked statistically against closed forms instead. */
+int or_clamped_splat(const bvc_kernel_spec* spec, double tol, int voronoi, int N, const double* bz,
+                     const double* bn, const double* bpdf, const double* bu, const double* bd,
+                     const double* bw, int M, const double* sy, const double* spdf, const double* sf,
+                     size_t K, const double* px, const uint8_t* fallback, int mode, double clamp,
+                     const double* ballR, double* bsum, double* ssum, long long* nb, long long* ms,
+                     long long* skipped) {
+    if (spec->dim != 2) return 1;
+    bvc_kernel_spec ball = {BVC_KERNEL_POISSON, 0.0, 2, spec->scale};
+    for (size_t k = 0; k < K; k++) {
+        if (fallback && fallback[k]) continue;
+        const double* x = px + 2 * k;
+        double R = ballR ? ballR[k] : 0.0;
+        if ((mode & 6) && !(R > 0.0)) return 2; /* requireBallRadius cache.cpp:418-423 */
+        double b = 0.0, s = 0.0;
+        long long bn_ = 0, mn = 0, skip = 0;
+        for (int i = 0; i < N; i++) {
+            double r = vdist(x, bz + 2 * i, 2);
+            if (r < tol) { skip++; continue; }
+            double P, G;
+            int e = or_poisson_kernel(spec, x, bz + 2 * i, bn + 2 * i, &P);
+            if (e) return e;
+            if (mode & 1) P = fmax(-clamp, fmin(clamp, P));
+            if (mode & 2) G = or_ball_greens(&ball, R, fmin(r, R));
+            else if ((e = or_greens(spec, x, bz + 2 * i, &G))) return e;
+            double val = P * bu[i] - G * bd[i];
+            b += voronoi ? val * bw[i] * N : val / bpdf[i];
+            bn_++;
+        }
+        for (int j = 0; j < M; j++) {
+            double r = vdist(x, sy + 2 * j, 2);
+            if (r < tol) { skip++; continue; }
+            double G;
+            if (mode & 2) {
+                G = or_ball_greens(&ball, R, fmin(r, R));
+                if (mode & 4) G = fmax(-clamp, fmin(clamp, G));
+            } else {
+                int e = or_greens(spec, x, sy + 2 * j, &G);
+                if (e) return e;
+            }
+            s += G * sf[j] / spdf[j];
+            mn++;
+        }
+        bsum[k] += b; nb[k] += bn_; ssum[k] += s; ms[k] += mn; skipped[k] += skip;
+    }
+    return 0;
+}

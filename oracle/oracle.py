@@ -98,6 +98,9 @@ def oracle_lib():
         L.or_splat.argtypes = [C.POINTER(abi.KernelSpec), C.c_double, C.c_int, C.c_int, _dp, _dp, _dp,
                                _dp, _dp, _dp, C.c_int, _dp, _dp, _dp, C.c_size_t, _dp, C.c_void_p,
                                C.c_int, C.c_int, _dp, _dp, _i64p, _i64p, _dp, _dp, _i64p, _i64p, _i64p]
+        L.or_clamped_splat.argtypes = [C.POINTER(abi.KernelSpec), C.c_double, C.c_int, C.c_int, _dp, _dp, _dp,
+                                       _dp, _dp, _dp, C.c_int, _dp, _dp, _dp, C.c_size_t, _dp, C.c_void_p,
+                                       C.c_int, C.c_double, C.c_void_p, _dp, _dp, _i64p, _i64p, _i64p]
         _oracle = L
     return _oracle
 
@@ -157,6 +160,10 @@ def ref_lib():
                                 _dp, _dp, C.c_void_p, C.c_int, _dp, _dp, _dp, C.c_size_t, _dp,
                                 C.c_void_p, C.c_int, C.c_int, C.c_int, _dp, _dp, _i64p, _i64p, _dp,
                                 _dp, _i64p, _i64p, _i64p, C.POINTER(C.c_double)]
+        L.ref_clamped_splat.argtypes = [C.POINTER(abi.KernelSpec), C.c_double, C.c_int, C.c_int, _dp, _dp, _dp,
+                                        _dp, _dp, C.c_void_p, C.c_int, _dp, _dp, _dp, C.c_size_t, _dp, C.c_int,
+                                        C.c_double, C.c_void_p, _dp, _dp, _i64p, _i64p, _i64p]
+        L.ref_ball_radius.argtypes = [C.c_void_p, C.c_void_p, _dp, C.c_size_t, _dp]
         L.ref_mark_points.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(abi.CacheConfig), _dp,
                                       C.c_size_t, _u8p, _u8p]
         L.ref_update_solution.argtypes = [C.c_void_p, C.POINTER(abi.Problem), C.c_void_p,
@@ -482,6 +489,52 @@ def ref_splat(spec, tol, bcache, scache, x, fallback=None, value=True, gradient=
                                    st["skipped"], C.byref(sec)))
     st["seconds"] = sec.value
     return st
+
+
+def _clamped_args(bcache, scache, x, ball_radius):
+    x = _f64(x).reshape(-1, 2)
+    K = len(x)
+    st = _splat_arrays(K, 2)
+    R = None if ball_radius is None else _f64(ball_radius).reshape(K)
+    return x, K, st, R
+
+
+def oracle_clamped_splat(spec, tol, bcache, scache, x, mode, clamp, ball_radius=None, voronoi=False,
+                         fallback=None):
+    """The clamped / ball-kernel splat loops restated (cache.cpp:410-416, 512-524, 573-582);
+    mode bits 1 clamp dG/dn, 2 ball kernel G^B, 4 clamp the source G^B."""
+    x, K, st, R = _clamped_args(bcache, scache, x, ball_radius)
+    N, bz, bn, bp, bu, bd, bw, M, sy, sp, sf = _cache_args(bcache, scache, 2)
+    fb = None if fallback is None else np.ascontiguousarray(fallback, dtype=np.uint8)
+    e = oracle_lib().or_clamped_splat(C.byref(spec), C.c_double(tol), int(voronoi), N, bz, bn, bp, bu, bd, bw, M,
+                                      sy, sp, sf, C.c_size_t(K), x.ravel(),
+                                      None if fb is None else fb.ctypes.data, int(mode), C.c_double(clamp),
+                                      None if R is None else R.ctypes.data, st["boundarySum"], st["sourceSum"],
+                                      st["nBoundary"], st["mSource"], st["skipped"])
+    if e:
+        raise RuntimeError(f"oracle clamped splat error {e}")
+    return st
+
+
+def ref_clamped_splat(spec, tol, bcache, scache, x, mode, clamp, ball_radius=None, voronoi=False):
+    """The reference's correctedBoundarySplat (ClampOnly) / correctedSourceSplat without
+    their sampled terms, or splatSolution, on an identical host cache."""
+    x, K, st, R = _clamped_args(bcache, scache, x, ball_radius)
+    N, bz, bn, bp, bu, bd, bw, M, sy, sp, sf = _cache_args(bcache, scache, 2)
+    _check_ref(ref_lib().ref_clamped_splat(C.byref(spec), C.c_double(tol), int(voronoi), N, bz, bn, bp, bu, bd,
+                                           bw.ctypes.data, M, sy, sp, sf, C.c_size_t(K), x.ravel(), int(mode),
+                                           C.c_double(clamp), None if R is None else R.ctypes.data,
+                                           st["boundarySum"], st["sourceSum"], st["nBoundary"], st["mSource"],
+                                           st["skipped"]))
+    return st
+
+
+def ref_ball_radius(scene: "RefScene", region: "RefRegion", x):
+    """markEvaluationPoints with sourceBall: ballRadius per point (cache.cpp:268-274)."""
+    x = _f64(x).reshape(-1, 2)
+    R = np.zeros(len(x))
+    _check_ref(ref_lib().ref_ball_radius(scene.h, region.h, x.ravel(), C.c_size_t(len(x)), R))
+    return R
 
 
 def solution(st):

@@ -397,6 +397,62 @@ int ref_splat(const bvc_kernel_spec* spec, double tol, int voronoi, int N, const
     });
 }
 
+// correctedBoundarySplat (ClampOnly) / correctedSourceSplat without the sampled
+// terms (empty evaluator / f), or splatSolution, per the mode bits of or_clamped_splat
+int ref_clamped_splat(const bvc_kernel_spec* spec, double tol, int voronoi, int N, const double* bz,
+                      const double* bn, const double* bpdf, const double* bu, const double* bd,
+                      const double* bw, int M, const double* sy, const double* spdf, const double* sf,
+                      size_t K, const double* px, int mode, double clamp, const double* ballR, double* bsum,
+                      double* ssum, long long* nb, long long* ms, long long* skipped) {
+    GUARD({
+        BoundaryCache bc;
+        bc.voronoi = voronoi != 0;
+        bc.samples.resize(N);
+        for (int i = 0; i < N; ++i) {
+            auto& s = bc.samples[i];
+            s.z = Vector2(bz[2 * i], bz[2 * i + 1]); s.n = Vector2(bn[2 * i], bn[2 * i + 1]);
+            s.pdf = bpdf[i]; s.uHat = bu[i]; s.dHat = bd[i]; s.weight = bw ? bw[i] : 0.0;
+        }
+        SourceCache sc;
+        sc.samples.resize(M);
+        for (int j = 0; j < M; ++j) sc.samples[j] = {Vector2(sy[2 * j], sy[2 * j + 1]), spdf[j], sf[j]};
+        std::vector<EvaluationPoint> pts(K);
+        for (size_t k = 0; k < K; ++k) {
+            pts[k].x = Vector2(px[2 * k], px[2 * k + 1]);
+            if (ballR) pts[k].ballRadius = ballR[k];
+        }
+        SplatConfig cfg;
+        cfg.kernel = toSpec(*spec);
+        cfg.coincidenceTol = tol;
+        cfg.voronoi = voronoi != 0;
+        cfg.useBallGreens = (mode & 2) != 0;
+        cfg.threads = 1;
+        SolveRegion none;  // unused without the sampled corrections
+        BoundaryCache noB;
+        SourceCache noS;
+        if (mode & 1) correctedBoundarySplat(bc, pts, none, cfg, clamp, ClampMode::ClampOnly, {}, 0, 0);
+        else splatSolution(bc, noS, pts, cfg);
+        if (mode & 4) correctedSourceSplat(sc, pts, none, cfg, clamp, {}, 0, 0);
+        else splatSolution(noB, sc, pts, cfg);
+        for (size_t k = 0; k < K; ++k) {
+            bsum[k] = pts[k].boundarySum; ssum[k] = pts[k].sourceSum; nb[k] = pts[k].nBoundary;
+            ms[k] = pts[k].mSource; skipped[k] = pts[k].skipped;
+        }
+    });
+}
+
+// markEvaluationPoints with sourceBall: EvaluationPoint::ballRadius (cache.cpp:268-274)
+int ref_ball_radius(void* sp, void* rp, const double* x, size_t n, double* radius) {
+    GUARD({
+        std::vector<EvaluationPoint> pts(n);
+        for (size_t k = 0; k < n; ++k) pts[k].x = Vector2(x[2 * k], x[2 * k + 1]);
+        CacheConfig c;
+        c.sourceBall = true;
+        markEvaluationPoints(*static_cast<Scene*>(sp), *static_cast<SolveRegion*>(rp), c, pts);
+        for (size_t k = 0; k < n; ++k) radius[k] = pts[k].ballRadius;
+    });
+}
+
 // markEvaluationPoints: fallback / gradientUnreliable flags
 int ref_mark_points(void* sp, void* rp, const bvc_cache_config* cfg, const double* x, size_t n,
                     uint8_t* fallback, uint8_t* unreliable) {

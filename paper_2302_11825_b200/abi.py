@@ -111,7 +111,17 @@ class PointState(C.Structure):
                 ("nBoundaryGrad", _P(C.c_longlong)), ("mSourceGrad", _P(C.c_longlong)),
                 ("walkSum", _P(C.c_double)), ("walkCount", _P(C.c_longlong)),
                 ("walkTruncated", _P(C.c_longlong)), ("gradientWalkSum", _P(C.c_double)),
-                ("gradientWalkCount", _P(C.c_longlong)), ("skipped", _P(C.c_longlong))]
+                ("gradientWalkCount", _P(C.c_longlong)), ("skipped", _P(C.c_longlong)),
+                ("ballRadius", _P(C.c_double))]
+
+
+# BoundaryEvaluator (cache.h:175-176) kinds
+EVALUATOR_NONE, EVALUATOR_FIELD, EVALUATOR_WALKS = 0, 1, 2
+
+
+class BoundaryEvaluator(C.Structure):
+    _fields_ = [("kind", C.c_int), ("field", Field), ("scene", C.c_void_p), ("problem", _P(Problem)),
+                ("cfg", _P(CacheConfig))]
 
 
 def make_field(kind: int = FIELD_NONE, params=(), n: int = 0) -> Field:

@@ -31,7 +31,8 @@ SYMBOLS = (
     "bvc_source_cache_create bvc_source_cache_size bvc_source_cache_download bvc_source_cache_destroy "
     "bvc_make_splat_config bvc_splat_solution bvc_splat_gradient bvc_splat_solution_gradient bvc_splat_range "
     "bvc_update_solution bvc_wos_solve bvc_wost_solve bvc_wost_gradient bvc_wost_normal_derivative "
-    "bvc_walk_traffic_profile bvc_eval_kernels bvc_eval_bessel"
+    "bvc_walk_traffic_profile bvc_eval_kernels bvc_eval_bessel bvc_corrected_boundary_splat "
+    "bvc_corrected_source_splat"
 ).split()
 
 
@@ -314,7 +315,7 @@ class EvaluationPoints:
                   nBoundaryGrad=np.zeros(n, np.int64), mSourceGrad=np.zeros(n, np.int64), walkSum=np.zeros(n),
                   walkCount=np.zeros(n, np.int64), walkTruncated=np.zeros(n, np.int64),
                   gradientWalkSum=np.zeros((n, d)), gradientWalkCount=np.zeros(n, np.int64),
-                  skipped=np.zeros(n, np.int64))
+                  skipped=np.zeros(n, np.int64), ballRadius=np.zeros(n))
         ps = abi.PointState()
         ps.count, ps.dim = n, d
         for name, arr in st.items():
@@ -330,6 +331,14 @@ class EvaluationPoints:
         ps = abi.PointState()
         ps.count, ps.dim = self.n, self.dim
         ps.fallback = _ptr(f, C.c_uint8)
+        _check(lib().bvc_points_upload(self.h, C.byref(ps)))
+
+    def set_ball_radius(self, radius):
+        """EvaluationPoint::ballRadius (cache.h:77), as markEvaluationPoints would set it."""
+        r = np.ascontiguousarray(radius, dtype=np.float64)
+        ps = abi.PointState()
+        ps.count, ps.dim = self.n, self.dim
+        ps.ballRadius = _ptr(r)
         _check(lib().bvc_points_upload(self.h, C.byref(ps)))
 
     def reset(self):
@@ -510,6 +519,43 @@ def splat_solution_gradient(bcache, scache, pts: EvaluationPoints, cfg):
 def splat_range(bcache, scache, pts: EvaluationPoints, cfg, begin, end, value=True, gradient=False):
     _check(lib().bvc_splat_range(bcache.h if bcache else None, scache.h if scache else None, pts.h, C.byref(cfg),
                                  C.c_size_t(begin), C.c_size_t(end), int(value), int(gradient)))
+
+
+def field_evaluator(f) -> abi.BoundaryEvaluator:
+    """A BoundaryEvaluator returning exact data u(z) = f(z) (e.g. the constant 1 of
+    test_cache.cpp:785)."""
+    ev = abi.BoundaryEvaluator()
+    ev.kind = abi.EVALUATOR_FIELD
+    ev.field = f
+    return ev
+
+
+def walk_evaluator(scene: Scene, pb, cfg) -> abi.BoundaryEvaluator:
+    """makeDefaultEvaluator (cache.cpp:600-620): cfg.correctionWalks WoSt walks per crossing."""
+    ev = abi.BoundaryEvaluator()
+    ev.kind = abi.EVALUATOR_WALKS
+    ev.scene = scene.h
+    ev._keep = (pb, cfg)  # the struct holds raw pointers to these
+    ev.problem = C.pointer(pb)
+    ev.cfg = C.pointer(cfg)
+    return ev
+
+
+def corrected_boundary_splat(bcache, pts: EvaluationPoints, region: SolveRegion, cfg, clamp_bound, mode,
+                             evaluator=None, seed=0, stream=0):
+    """correctedBoundarySplat (cache.h:178-184; cache.cpp:499-553)."""
+    _check(lib().bvc_corrected_boundary_splat(bcache.h if bcache else None, pts.h, region.h, C.byref(cfg),
+                                              C.c_double(clamp_bound), int(mode),
+                                              C.byref(evaluator) if evaluator is not None else None,
+                                              C.c_uint64(seed), C.c_uint64(stream)))
+
+
+def corrected_source_splat(scache, pts: EvaluationPoints, region: SolveRegion, cfg, clamp_bound, f=None, seed=0,
+                           stream=0):
+    """correctedSourceSplat (cache.h:186-191; cache.cpp:555-597); f is a field descriptor or None."""
+    _check(lib().bvc_corrected_source_splat(scache.h if scache else None, pts.h, region.h, C.byref(cfg),
+                                            C.c_double(clamp_bound), C.byref(f) if f is not None else None,
+                                            C.c_uint64(seed), C.c_uint64(stream)))
 
 
 def mark_evaluation_points(scene: Scene, region: SolveRegion, cfg, pts: EvaluationPoints):

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstring>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <memory>
 #include <string>
 #include <vector>
@@ -122,7 +123,9 @@ enum Slot {
     kWsSamplesTmp, kWsStartU, kWsIsD, kWsGradR, kWsOutside, kWsDIdx, kWsCount, kWsXD, kWsND, kWsRD, kWsGidD, kWsOutU,
     kWsOutD, kWsCounter, kWsSteps, kWsTrunc, kWsFailed, kWsPack, kWsPart, kWsSkipB, kWsSkipS, kWsPts, kWsCtr,
     kWsSortKeysIn, kWsSortKeysOut, kWsSortValsIn, kWsSortTemp, kWsMean, kWsSe, kWsTruncPt, kWsHost1, kWsRegion,
-    kWsMean2, kWsSe2, kWsGidU, kWsSrcTmp, kWsSrcFlag, kWsEvalIn, kWsEvalOut, kWsTileBox, kWsUnitCtr
+    kWsMean2, kWsSe2, kWsGidU, kWsSrcTmp, kWsSrcFlag, kWsEvalIn, kWsEvalOut, kWsTileBox, kWsUnitCtr,
+    kWsCorrCounts, kWsCorrOffsets, kWsCorrStarts, kWsCorrGid, kWsCorrW, kWsCorrOut, kWsCorrMean, kWsCorrScan,
+    kWsCorrFlag, kWsBallRs, kWsHull
 };
 
 int fail(const std::exception& e) {
@@ -167,7 +170,8 @@ inline void key_of(uint64_t seed, uint64_t salt, uint64_t round, uint32_t& k0, u
 
 // salts of the reference (cache.cpp:15-22)
 constexpr uint64_t kBoundaryPosSalt = 0x1001, kBoundaryWalkSalt = 0x1002, kBoundaryRedrawSalt = 0x1003,
-                   kSourceSalt = 0x1004, kFallbackSalt = 0x1005, kFallbackGradSalt = 0x1006, kPointwiseSalt = 0x2001;
+                   kSourceSalt = 0x1004, kFallbackSalt = 0x1005, kFallbackGradSalt = 0x1006, kPointwiseSalt = 0x2001,
+                   kBoundaryCorrSalt = 0x1007, kSourceCorrSalt = 0x1008;
 
 double device_seconds(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0.f;
@@ -400,6 +404,9 @@ struct bvc_eval_points_s {
     int active = 0;
     DevBuf<int> order;
     DevBuf<float> xs;
+    // ball-kernel mode (cache.h:77): radius per point, valid once marked / uploaded
+    DevBuf<double> ballR;
+    bool ballValid = false;
 
     PointsDev dev() {
         return PointsDev{bsum.p, ssum.p, nb.p, ms.p, bgsum.p, sgsum.p, nbg.p, msg.p, skipped.p};
@@ -776,8 +783,6 @@ void generate_cache(bvc_scene_s* S, const bvc_problem& pb, bvc_region_s* R, cons
     R->upload();
     const int N = std::max(1, cfg.nBoundary);
     need(begin >= 0 && begin <= end && end <= N, "shard range outside [0, nBoundary]");
-    if (cfg.clampMode != BVC_CLAMP_OFF || cfg.sourceBall)
-        throw Error(BVC_ERR_INVALID_ARGUMENT, "clamped / ball-kernel splats are not implemented (SURVEY §8f.3)");
     if (S->host.dim == 3) {
         S->upload();
         generate_cache3(S, pb, R, cfg, seed, round, begin, end, out, st);
@@ -976,18 +981,12 @@ int gather_kind(const bvc_kernel_spec& k) {
     return k.dim == 2 ? (scr ? kScr2 : kLap2) : (scr ? kScr3 : kLap3);
 }
 
-void splat(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_points_s* P, const bvc_splat_config& cfg,
-           size_t begin, size_t end, bool val, bool grad) {
-    require_device();
-    need(P != nullptr, "null evaluation points");
-    validate_kernel(cfg.kernel);
-    if (cfg.useBallGreens) throw Error(BVC_ERR_INVALID_ARGUMENT, "ball-kernel splats are not implemented (SURVEY §8f.3)");
+// one gather launch over [begin, end) of the active points; mode = SplatMode bits
+// (gather.cu) for the clamped / ball-kernel variants (value only)
+void splat_launch(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_points_s* P, const bvc_splat_config& cfg,
+                  size_t begin, size_t end, bool val, bool grad, int mode, double clamp) {
     int dim = cfg.kernel.dim;
-    need(P->dim == dim, "evaluation points and kernel differ in dimension");
     int N = b ? b->n : 0, M = s ? s->m : 0;
-    need(!b || b->dim == dim, "boundary cache dimension mismatch");
-    need(!s || s->dim == dim, "source cache dimension mismatch");
-    ensure_order(P);
     size_t Ka = static_cast<size_t>(P->active);
     end = std::min(end, Ka);
     if (begin >= end) return;
@@ -1002,16 +1001,194 @@ void splat(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_points_s* P,
     int* skipS = ws().get<int>(kWsSkipS, K);
     CK(cudaMemsetAsync(skipB, 0, K * sizeof(int), g_stream));
     CK(cudaMemsetAsync(skipS, 0, K * sizeof(int), g_stream));
+    float* ballRs = nullptr;
+    if (mode & kModeBall) {
+        ballRs = ws().get<float>(kWsBallRs, K);
+        launch_gather_f32(P->ballR.p, P->order.p + begin, K, ballRs, g_stream);
+    }
     if (N + M > 0)
         launch_gather(kind, plan, pack, N, M, P->xs.p + static_cast<size_t>(dim) * begin, K, dim,
                       static_cast<float>(cfg.kernel.sigma), static_cast<float>(cfg.coincidenceTol), val, grad, part,
                       skipB, skipS, ws().get<float4>(kWsTileBox, 2 * static_cast<size_t>((N + 255) / 256 + (M + 255) / 256 + 1)),
-                      ws().get<unsigned>(kWsUnitCtr, 1), g_stream);
+                      ws().get<unsigned>(kWsUnitCtr, 1), g_stream, mode, static_cast<float>(clamp), ballRs);
     else
         CK(cudaMemsetAsync(part, 0, sizeof(double), g_stream));
     if (N + M > 0)
         launch_finalize(part, plan, K, P->order.p + begin, N, M, val, grad, dim, skipB, skipS, P->dev(), g_stream);
     CK(cudaGetLastError());
+}
+
+// requireBallRadius (cache.cpp:418-423)
+void require_ball(bvc_eval_points_s* P) {
+    if (!P->ballValid)
+        throw Error(BVC_ERR_SOLVER, "ball-kernel mode: evaluation point has no ball radius "
+                                    "(markEvaluationPoints not applied)");
+}
+
+// splatSolution / splatGradient (cache.cpp:426-497), optionally with the boundary
+// dG/dn clamped (mode bits) as in correctedBoundarySplat's first loop
+void splat(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_points_s* P, const bvc_splat_config& cfg,
+           size_t begin, size_t end, bool val, bool grad, int mode = 0, double clamp = 0.0) {
+    require_device();
+    need(P != nullptr, "null evaluation points");
+    validate_kernel(cfg.kernel);
+    int dim = cfg.kernel.dim;
+    need(P->dim == dim, "evaluation points and kernel differ in dimension");
+    need(!b || b->dim == dim, "boundary cache dimension mismatch");
+    need(!s || s->dim == dim, "source cache dimension mismatch");
+    if (cfg.useBallGreens && val) {
+        if (cfg.kernel.kind != BVC_KERNEL_POISSON || dim != 2)
+            throw Error(BVC_ERR_SOLVER, "ball-kernel source mode requires the 2D Poisson kernel");
+        mode |= kModeBall;
+    }
+    if (mode && dim != 2) throw Error(BVC_ERR_INVALID_ARGUMENT, "clamped / ball-kernel splats are 2D (cache.cpp:499-597)");
+    ensure_order(P);
+    if (mode & kModeBall) require_ball(P);
+    if (val && grad && mode) {  // the gradient splat never clamps (cache.cpp:463-497)
+        splat_launch(b, s, P, cfg, begin, end, true, false, mode, clamp);
+        splat_launch(b, s, P, cfg, begin, end, false, true, 0, 0.0);
+    } else {
+        splat_launch(b, s, P, cfg, begin, end, val, grad, val ? mode : 0, clamp);
+    }
+}
+
+// correctedBoundarySplat (cache.cpp:499-553)
+void corrected_boundary(bvc_boundary_cache_s* b, bvc_eval_points_s* P, bvc_region_s* R, const bvc_splat_config& cfg,
+                        double clamp, int mode, const bvc_boundary_evaluator* ev, uint64_t seed, uint64_t stream) {
+    require_device();
+    need(P && R, "null argument");
+    if (mode == BVC_CLAMP_OFF) throw Error(BVC_ERR_INVALID_ARGUMENT, "corrected splat called with clamping off");
+    need(mode == BVC_CLAMP_ONLY || mode == BVC_CLAMP_CORRECT, "unknown clamp mode");
+    if (!(clamp > 0.0)) throw Error(BVC_ERR_INVALID_ARGUMENT, "clamp bound must be positive");
+    bool haveEval = ev && ev->kind != BVC_EVALUATOR_NONE;
+    if (mode == BVC_CLAMP_CORRECT && !haveEval)
+        throw Error(BVC_ERR_INVALID_ARGUMENT, "clamp correction needs a boundary evaluator");
+    need(cfg.kernel.dim == 2, "clamped splats are 2D (cache.cpp:499)");
+    splat(b, nullptr, P, cfg, 0, SIZE_MAX, true, false, kModeClampP, clamp);
+    if (mode != BVC_CLAMP_CORRECT) return;
+    int K = P->active;
+    if (K == 0) return;
+    R->upload();
+    int N = b ? b->n : 0;
+    CorrRayEnv E{};
+    E.region = R->boundary.view();
+    E.kinds = R->kinds.p;
+    E.screened = cfg.kernel.kind == BVC_KERNEL_SCREENED ? 1 : 0;
+    E.sqrtSigma = std::sqrt(cfg.kernel.sigma);
+    E.clamp = clamp;
+    E.tol2 = cfg.coincidenceTol * cfg.coincidenceTol;
+    E.nRound = static_cast<double>(N);
+    E.insideTol = static_cast<float>(1e-7 * R->boundary.host.diagonal);
+    key_of(seed, stream, 0, E.k0, E.k1);
+    int* noHit = ws().get<int>(kWsCorrFlag, 1);
+    CK(cudaMemsetAsync(noHit, 0, sizeof(int), g_stream));
+    auto check_hits = [&]() {
+        int h = 0;
+        CK(cudaMemcpyAsync(&h, noHit, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+        if (h) throw Error(BVC_ERR_SOLVER, "clamp correction: no boundary ray hits from an interior point");
+    };
+    if (ev->kind == BVC_EVALUATOR_FIELD) {
+        E.useField = 1;
+        E.field = to_dev(ev->field);
+        launch_corr_rays(E, P->x.p, P->order.p, K, nullptr, P->bsum.p, noHit, g_stream);
+        check_hits();
+        return;
+    }
+    need(ev->kind == BVC_EVALUATOR_WALKS && ev->scene && ev->problem && ev->cfg,
+         "walk evaluator needs scene, problem and cache config");
+    need(ev->scene->host.dim == 2, "walk evaluator scene must be 2D");
+    // makeDefaultEvaluator (cache.cpp:600-620): correctionWalks WoSt walks per crossing
+    WalkEnv W = make_env(ev->scene, *ev->problem, ev->cfg->walk, seed, stream, 1);
+    E.eps = W.eps;
+    int* counts = ws().get<int>(kWsCorrCounts, K);
+    int* offsets = ws().get<int>(kWsCorrOffsets, K);
+    launch_corr_rays(E, P->x.p, P->order.p, K, counts, nullptr, noHit, g_stream);
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts, offsets, K, g_stream));
+    CK(cub::DeviceScan::ExclusiveSum(ws().get<char>(kWsCorrScan, tmp), tmp, counts, offsets, K, g_stream));
+    count_launch();
+    int last[2] = {0, 0};
+    CK(cudaMemcpyAsync(&last[0], offsets + K - 1, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaMemcpyAsync(&last[1], counts + K - 1, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+    check_hits();
+    int H = last[0] + last[1];
+    if (H == 0) return;
+    float2* starts = ws().get<float2>(kWsCorrStarts, H);
+    long long* gid = ws().get<long long>(kWsCorrGid, H);
+    double* w = ws().get<double>(kWsCorrW, H);
+    launch_corr_emit(E, P->x.p, P->order.p, K, offsets, starts, gid, w, g_stream);
+    int nw = std::max(1, ev->cfg->correctionWalks);
+    auto* ctr = ws().get<unsigned long long>(kWsCounter, 3);
+    CK(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), g_stream));
+    WalkJob J{};
+    J.counter = ctr;
+    J.nU = nw;
+    J.nPtsU = H;
+    J.startU = starts;
+    J.gidU = gid;
+    J.outU = ws().get<float>(kWsCorrOut, static_cast<size_t>(H) * nw);
+    launch_walk_job(W, J, g_stream);
+    double* mean = ws().get<double>(kWsCorrMean, H);
+    launch_reduce_estimates(J.outU, H, nw, 1, 0, mean, nullptr, g_stream);
+    launch_corr_apply(offsets, counts, P->order.p, K, w, mean, E.nRound, P->bsum.p, g_stream);
+    CK(cudaGetLastError());
+}
+
+// correctedSourceSplat (cache.cpp:555-597)
+void corrected_source(bvc_source_cache_s* s, bvc_eval_points_s* P, bvc_region_s* R, const bvc_splat_config& cfg,
+                      double clamp, const bvc_field* f, uint64_t seed, uint64_t stream) {
+    require_device();
+    need(P && R, "null argument");
+    if (cfg.kernel.kind != BVC_KERNEL_POISSON || cfg.kernel.dim != 2)
+        throw Error(BVC_ERR_SOLVER, "ball-kernel source mode requires the 2D Poisson kernel");
+    if (!(clamp > 0.0)) throw Error(BVC_ERR_INVALID_ARGUMENT, "clamp bound must be positive");
+    need(P->dim == 2, "evaluation points must be 2D");
+    ensure_order(P);
+    require_ball(P);
+    bvc_splat_config c = cfg;
+    c.useBallGreens = 1;
+    splat(nullptr, s, P, c, 0, SIZE_MAX, true, false, kModeClampS, clamp);
+    int K = P->active;
+    if (!(std::isfinite(clamp) && f && f->kind != BVC_FIELD_NONE) || K == 0) return;
+    R->upload();
+    uint32_t k0, k1;
+    key_of(seed, stream, 0, k0, k1);
+    launch_ball_corr(R->boundary.view(), static_cast<float>(1e-7 * R->boundary.host.diagonal), P->x.p, P->order.p,
+                     P->ballR.p, K, to_dev(*f), clamp, static_cast<double>(s ? s->m : 0), k0, k1, P->ssum.p, g_stream);
+    CK(cudaGetLastError());
+}
+
+// Andrew's monotone chain; the farthest vertex from any point is a hull vertex
+std::vector<double> convex_hull2(const std::vector<double>& v) {
+    size_t n = v.size() / 2;
+    std::vector<std::pair<double, double>> p(n);
+    for (size_t i = 0; i < n; ++i) p[i] = {v[2 * i], v[2 * i + 1]};
+    std::sort(p.begin(), p.end());
+    p.erase(std::unique(p.begin(), p.end()), p.end());
+    if (p.size() < 3) {
+        std::vector<double> out;
+        for (auto& q : p) { out.push_back(q.first); out.push_back(q.second); }
+        return out;
+    }
+    auto cross = [](const std::pair<double, double>& o, const std::pair<double, double>& a,
+                    const std::pair<double, double>& b) {
+        return (a.first - o.first) * (b.second - o.second) - (a.second - o.second) * (b.first - o.first);
+    };
+    std::vector<std::pair<double, double>> h(2 * p.size());
+    size_t k = 0;
+    for (size_t i = 0; i < p.size(); ++i) {
+        while (k >= 2 && cross(h[k - 2], h[k - 1], p[i]) <= 0) --k;
+        h[k++] = p[i];
+    }
+    for (size_t i = p.size() - 1, t = k + 1; i-- > 0;) {
+        while (k >= t && cross(h[k - 2], h[k - 1], p[i]) <= 0) --k;
+        h[k++] = p[i];
+    }
+    h.resize(k - 1);
+    std::vector<double> out;
+    for (auto& q : h) { out.push_back(q.first); out.push_back(q.second); }
+    return out;
 }
 
 // estimator job over host points (pointwise.h:62-76)
@@ -1352,6 +1529,7 @@ void alloc_points(bvc_eval_points_s* P) {
     P->walkSum.resize(n); P->gwalkSum.resize(d * n);
     P->nb.resize(n); P->ms.resize(n); P->nbg.resize(n); P->msg.resize(n);
     P->walkCount.resize(n); P->walkTrunc.resize(n); P->gwalkCount.resize(n); P->skipped.resize(n);
+    P->ballR.resize(n);
 }
 
 void zero_points(bvc_eval_points_s* P) {
@@ -1359,6 +1537,8 @@ void zero_points(bvc_eval_points_s* P) {
     P->bsum.zero(); P->ssum.zero(); P->bgsum.zero(); P->sgsum.zero(); P->walkSum.zero(); P->gwalkSum.zero();
     P->nb.zero(); P->ms.zero(); P->nbg.zero(); P->msg.zero(); P->walkCount.zero(); P->walkTrunc.zero();
     P->gwalkCount.zero(); P->skipped.zero();
+    P->ballR.zero();
+    P->ballValid = false;
 }
 
 // EvaluationPoint::solution() / gradient() (cache.h:91-105)
@@ -1621,6 +1801,7 @@ int bvc_points_download(bvc_eval_points p, bvc_point_state* h) {
         if (h->gradientWalkSum) p->gwalkSum.download(h->gradientWalkSum, d * n);
         if (h->gradientWalkCount) p->gwalkCount.download(h->gradientWalkCount, n);
         if (h->skipped) p->skipped.download(h->skipped, n);
+        if (h->ballRadius) p->ballR.download(h->ballRadius, n);
         CK(cudaStreamSynchronize(g_stream));
     })
 }
@@ -1665,6 +1846,16 @@ int bvc_points_upload(bvc_eval_points p, const bvc_point_state* h) {
         if (h->gradientWalkSum) p->gwalkSum.upload(h->gradientWalkSum, d * n);
         if (h->gradientWalkCount) p->gwalkCount.upload(h->gradientWalkCount, n);
         if (h->skipped) p->skipped.upload(h->skipped, n);
+        if (h->ballRadius) {
+            p->ballR.upload(h->ballRadius, n);
+            // requireBallRadius (cache.cpp:418-423) for every non-fallback point
+            std::vector<uint8_t> fb(n);
+            p->fallback.download(fb.data(), n);
+            CK(cudaStreamSynchronize(g_stream));
+            p->ballValid = true;
+            for (size_t i = 0; i < n; ++i)
+                if (!fb[i] && !(h->ballRadius[i] > 0.0)) p->ballValid = false;
+        }
         CK(cudaStreamSynchronize(g_stream));
     })
 }
@@ -1673,8 +1864,17 @@ int bvc_mark_evaluation_points(bvc_scene s, bvc_region r, const bvc_cache_config
         require_device();
         need(s && r && cfg && p, "null argument");
         need(p->dim == s->host.dim, "markEvaluationPoints: point and scene dimensions differ");
-        if (cfg->sourceBall) throw Error(BVC_ERR_INVALID_ARGUMENT, "ball-kernel mode is not implemented (SURVEY §8f.3)");
         r->upload();
+        if (cfg->sourceBall) {  // cache.cpp:268-274
+            need(s->host.dim == 2, "ball-kernel mode is 2D only", BVC_ERR_SOLVER);
+            std::vector<double> hull = convex_hull2(r->host.boundary.v);
+            double* dh = ws().get<double>(kWsHull, std::max<size_t>(hull.size(), 2));
+            CK(cudaMemcpyAsync(dh, hull.data(), hull.size() * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+            launch_ball_radius(p->x.p, static_cast<int>(p->n), 2, dh, static_cast<int>(hull.size() / 2), p->ballR.p,
+                               g_stream);
+            CK(cudaStreamSynchronize(g_stream));  // hull is a pageable host buffer
+            p->ballValid = !hull.empty();
+        }
         int n = static_cast<int>(p->n);
         if (s->host.dim == 3) {
             const auto& comp = r->boundary.host.component;
@@ -1867,6 +2067,16 @@ int bvc_splat_range(bvc_boundary_cache b, bvc_source_cache s, bvc_eval_points p,
     API(need(cfg, "null config"); splat(b, s, p, *cfg, begin, end, value != 0, gradient != 0))
 }
 
+int bvc_corrected_boundary_splat(bvc_boundary_cache b, bvc_eval_points p, bvc_region r, const bvc_splat_config* cfg,
+                                 double clampBound, int clampMode, const bvc_boundary_evaluator* eval, uint64_t seed,
+                                 uint64_t stream) {
+    API(need(cfg, "null config"); corrected_boundary(b, p, r, *cfg, clampBound, clampMode, eval, seed, stream))
+}
+int bvc_corrected_source_splat(bvc_source_cache s, bvc_eval_points p, bvc_region r, const bvc_splat_config* cfg,
+                               double clampBound, const bvc_field* f, uint64_t seed, uint64_t stream) {
+    API(need(cfg, "null config"); corrected_source(s, p, r, *cfg, clampBound, f, seed, stream))
+}
+
 int bvc_update_solution(bvc_scene s, const bvc_problem* pb, bvc_region r, const bvc_cache_config* cfg,
                         bvc_eval_points p, uint64_t seed, uint64_t round, int gradients, bvc_round_stats* stats) {
     API({
@@ -1876,6 +2086,7 @@ int bvc_update_solution(bvc_scene s, const bvc_problem* pb, bvc_region r, const 
         if (cfg->sourceBall && gradients)
             throw Error(BVC_ERR_SOLVER, "ball-kernel source mode does not support gradient splats");
         bvc_splat_config scfg = make_splat_config(s, *pb, *cfg);
+        need(cfg->clampMode >= BVC_CLAMP_OFF && cfg->clampMode <= BVC_CLAMP_CORRECT, "unknown clamp mode");
         cudaEvent_t e0, e1, e2;
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
@@ -1887,7 +2098,30 @@ int bvc_update_solution(bvc_scene s, const bvc_problem* pb, bvc_region r, const 
         generate_cache(s, *pb, r, *cfg, seed, round, 0, std::max(1, cfg->nBoundary), &bc, st);
         generate_source(*pb, r, *cfg, seed, round, &sc);
         CK(cudaEventRecord(e1, g_stream));
-        splat(&bc, sc.m ? &sc : nullptr, p, scfg, 0, SIZE_MAX, true, gradients != 0);
+        bool hasSource = pb->f.kind != BVC_FIELD_NONE;
+        bvc_source_cache_s* sp = sc.m ? &sc : nullptr;
+        // the mode dispatch of updateSolution (cache.cpp:639-662)
+        if (cfg->clampMode == BVC_CLAMP_OFF) {
+            // ball mode: splatSolution with G^B plus the unclamped (infinite-bound,
+            // correction-free) ball source splat, i.e. one ball-kernel splat
+            splat(&bc, sp, p, scfg, 0, SIZE_MAX, true, gradients != 0);
+        } else {
+            double c = cfg->clamp > 0.0 ? cfg->clamp : 10.0 / s->host.diagonal;  // resolvedClamp cache.h:129-131
+            bvc_boundary_evaluator ev{};
+            ev.kind = BVC_EVALUATOR_WALKS;
+            ev.scene = s;
+            ev.problem = pb;
+            ev.cfg = cfg;
+            corrected_boundary(&bc, p, r, scfg, c, cfg->clampMode, &ev, seed, bvc_dev::mixKey(kBoundaryCorrSalt, round));
+            if (hasSource) {
+                if (cfg->sourceBall) {
+                    corrected_source(sp, p, r, scfg, c, &pb->f, seed, bvc_dev::mixKey(kSourceCorrSalt, round));
+                } else {
+                    splat(nullptr, sp, p, scfg, 0, SIZE_MAX, true, false);
+                }
+            }
+            if (gradients) splat(&bc, sp, p, scfg, 0, SIZE_MAX, false, true);
+        }
         fallback_walks(s, *pb, *cfg, p, seed, round, gradients != 0);
         CK(cudaEventRecord(e2, g_stream));
         CK(cudaEventSynchronize(e2));

@@ -88,9 +88,21 @@ __device__ __forceinline__ void k0_q(float t, float& K0, float& Q) {
     }
 }
 
-template <int KIND, bool SRC, bool VAL, bool GRAD, bool TRACK = false>
+// splat variants of correctedBoundarySplat / correctedSourceSplat (cache.cpp:499-597):
+//   kClampP: dG/dn clamped to [-c, c] in the boundary term (clampKernel kernels.h:52)
+//   kBall:   G -> G^B(x, R_x) (ballGreens kernels.cpp:31-43) in the d-hat and source terms
+//   kClampS: source G^B clamped to [-c, c]
+enum SplatMode { kClampP = 1, kBall = 2, kClampS = 4 };
+struct ModeCtx {
+    float c2pi;   // 2 pi c (the clamp in the units of nd / r^2)
+    float R2;     // R_x^2 (ball radius of the evaluation point)
+    float lgR2;   // log2 R_x^2
+    float sclamp; // c 4 pi / ln 2 (the source clamp in log2 units)
+};
+
+template <int KIND, bool SRC, bool VAL, bool GRAD, bool TRACK = false, int MODE = 0>
 __device__ __forceinline__ void pair(const float4 a, const float4 b, float px, float py, float pz, float sigma,
-                                     float s, Acc& acc, float& mn) {
+                                     float s, Acc& acc, float& mn, const ModeCtx* mc = nullptr) {
     if constexpr (KIND == kLap2 || KIND == kScr2) {
         float dx = a.x - px, dy = a.y - py;
         float r2 = fmaf(dx, dx, dy * dy);
@@ -100,7 +112,15 @@ __device__ __forceinline__ void pair(const float4 a, const float4 b, float px, f
             if constexpr (!SRC) {
                 float nd = fmaf(a.z, dx, a.w * dy);
                 float p = nd * ir2;
-                if constexpr (VAL) acc.v = fmaf(b.x, p, fmaf(-b.y, f_lg2(r2), acc.v));
+                if constexpr (VAL) {
+                    if constexpr (MODE == 0) {
+                        acc.v = fmaf(b.x, p, fmaf(-b.y, f_lg2(r2), acc.v));
+                    } else {
+                        float pc = (MODE & kClampP) ? fminf(fmaxf(p, -mc->c2pi), mc->c2pi) : p;
+                        float l = (MODE & kBall) ? f_lg2(fminf(r2, mc->R2)) - mc->lgR2 : f_lg2(r2);
+                        acc.v = fmaf(b.x, pc, fmaf(-b.y, l, acc.v));
+                    }
+                }
                 if constexpr (GRAD) {
                     float q = fmaf(b.w, p, b.z) * ir2;  // (2A p + Bg) / r^2
                     float c = b.x * ir2;                // A / r^2
@@ -108,7 +128,15 @@ __device__ __forceinline__ void pair(const float4 a, const float4 b, float px, f
                     acc.gy = fmaf(q, dy, fmaf(-c, a.w, acc.gy));
                 }
             } else {
-                if constexpr (VAL) acc.v = fmaf(b.x, f_lg2(r2), acc.v);
+                if constexpr (VAL) {
+                    if constexpr (MODE == 0) {
+                        acc.v = fmaf(b.x, f_lg2(r2), acc.v);
+                    } else {
+                        float l = (MODE & kBall) ? f_lg2(fminf(r2, mc->R2)) - mc->lgR2 : f_lg2(r2);
+                        if constexpr ((MODE & kClampS) != 0) l = fmaxf(l, -mc->sclamp);
+                        acc.v = fmaf(b.x, l, acc.v);
+                    }
+                }
                 if constexpr (GRAD) {
                     float c = b.y * ir2;
                     acc.gx = fmaf(-c, dx, acc.gx);
@@ -124,7 +152,11 @@ __device__ __forceinline__ void pair(const float4 a, const float4 b, float px, f
             if constexpr (!SRC) {
                 float nd = fmaf(a.z, dx, a.w * dy);
                 float p = nd * ir2;
-                if constexpr (VAL) acc.v = fmaf(b.x * Q, p, fmaf(b.y, K0, acc.v));
+                if constexpr (VAL) {
+                    float qp = Q * p;
+                    if constexpr ((MODE & kClampP) != 0) qp = fminf(fmaxf(qp, -mc->c2pi), mc->c2pi);
+                    acc.v = fmaf(b.x, qp, fmaf(b.y, K0, acc.v));
+                }
                 if constexpr (GRAD) {
                     float aq = b.x * Q;
                     // d (A (2 Q p ir2 + sigma K0 p) + Bk Q ir2) - n (A Q ir2)
@@ -199,35 +231,48 @@ struct Params {
     const float4* tileBox;   // per shared-memory tile: lo (x, y, z), hi (x, y, z) of its samples
     int tilesB;              // boundary tiles (source tiles follow)
     unsigned* unitCounter;   // dynamic work-unit queue (zeroed per launch)
+    // corrected-splat variants (MODE != 0)
+    float clamp;             // c
+    const float* ballR;      // per active point (sorted order): ball radius R_x
 };
 
+__device__ __forceinline__ ModeCtx mode_ctx(const Params& P, int i) {
+    ModeCtx m;
+    m.c2pi = kTwoPi * P.clamp;
+    m.sclamp = P.clamp * 4.0f * kPi / kLn2;
+    float R = (P.ballR && i < P.K) ? P.ballR[i] : 1.0f;
+    m.R2 = R * R;
+    m.lgR2 = f_lg2(m.R2);
+    return m;
+}
+
 // slow path: recompute one point's tile partial, skipping near-coincident samples
-template <int KIND, bool SRC, bool VAL, bool GRAD>
+template <int KIND, bool SRC, bool VAL, bool GRAD, int MODE>
 __device__ void tile_slow(const float4* sm, int cnt, float px, float py, float pz, const Params& P, Acc& acc,
-                          int& skips) {
+                          int& skips, const ModeCtx* mc) {
     acc = Acc{0.f, 0.f, 0.f, 0.f};
     for (int j = 0; j < cnt; ++j) {
         float4 a = sm[2 * j], b = sm[2 * j + 1];
         float dx = a.x - px, dy = a.y - py, dz = (KIND == kLap3 || KIND == kScr3) ? a.z - pz : 0.0f;
         if (dx * dx + dy * dy + dz * dz < P.tol2) { ++skips; continue; }  // cache.cpp:436-440
         float mn = 0.f;
-        pair<KIND, SRC, VAL, GRAD>(a, b, px, py, pz, P.sigma, P.s, acc, mn);
+        pair<KIND, SRC, VAL, GRAD, false, MODE>(a, b, px, py, pz, P.sigma, P.s, acc, mn, mc);
     }
 }
 
-template <int KIND, bool SRC, bool VAL, bool GRAD, bool TRACK>
+template <int KIND, bool SRC, bool VAL, bool GRAD, bool TRACK, int MODE>
 __device__ __forceinline__ void tile_loop(const float4* S, int cnt, const float* px, const float* py, const float* pz,
-                                          const Params& P, Acc* acc, float* mn) {
+                                          const Params& P, Acc* acc, float* mn, const ModeCtx* mc) {
 #pragma unroll 2
     for (int j = 0; j < cnt; ++j) {
         const float4 a = S[2 * j], b = S[2 * j + 1];
 #pragma unroll
         for (int q = 0; q < kQ; ++q)
-            pair<KIND, SRC, VAL, GRAD, TRACK>(a, b, px[q], py[q], pz[q], P.sigma, P.s, acc[q], mn[q]);
+            pair<KIND, SRC, VAL, GRAD, TRACK, MODE>(a, b, px[q], py[q], pz[q], P.sigma, P.s, acc[q], mn[q], mc + q);
     }
 }
 
-template <int KIND, bool VAL, bool GRAD>
+template <int KIND, bool VAL, bool GRAD, int MODE = 0>
 __global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
     __shared__ __align__(128) float4 sm[2][2 * kTS];
     __shared__ __align__(8) uint64_t bar[2];
@@ -267,6 +312,11 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
         int skips[kQ];
 #pragma unroll
         for (int q = 0; q < kQ; ++q) { dv[q] = dg0[q] = dg1[q] = dg2[q] = 0.0; skips[q] = 0; }
+        ModeCtx mc[kQ];
+        if constexpr (MODE != 0) {
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) mc[q] = mode_ctx(P, pidx[q]);
+        }
         // prologue: first two tiles in flight
         if (tid == 0) {
 #pragma unroll
@@ -299,17 +349,17 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
             for (int q = 0; q < kQ; ++q) { acc[q] = Acc{0.f, 0.f, 0.f, 0.f}; mn[q] = 3.0e38f; }
             const float4* S = sm[st];
             if (!src) {
-                if (track) tile_loop<KIND, false, VAL, GRAD, true>(S, cnt, px, py, pz, P, acc, mn);
-                else tile_loop<KIND, false, VAL, GRAD, false>(S, cnt, px, py, pz, P, acc, mn);
+                if (track) tile_loop<KIND, false, VAL, GRAD, true, MODE>(S, cnt, px, py, pz, P, acc, mn, mc);
+                else tile_loop<KIND, false, VAL, GRAD, false, MODE>(S, cnt, px, py, pz, P, acc, mn, mc);
             } else {
-                if (track) tile_loop<KIND, true, VAL, GRAD, true>(S, cnt, px, py, pz, P, acc, mn);
-                else tile_loop<KIND, true, VAL, GRAD, false>(S, cnt, px, py, pz, P, acc, mn);
+                if (track) tile_loop<KIND, true, VAL, GRAD, true, MODE>(S, cnt, px, py, pz, P, acc, mn, mc);
+                else tile_loop<KIND, true, VAL, GRAD, false, MODE>(S, cnt, px, py, pz, P, acc, mn, mc);
             }
 #pragma unroll
             for (int q = 0; q < kQ; ++q) {
                 if (mn[q] < P.tol2 && pidx[q] < P.K) {
-                    if (!src) tile_slow<KIND, false, VAL, GRAD>(S, cnt, px[q], py[q], pz[q], P, acc[q], skips[q]);
-                    else tile_slow<KIND, true, VAL, GRAD>(S, cnt, px[q], py[q], pz[q], P, acc[q], skips[q]);
+                    if (!src) tile_slow<KIND, false, VAL, GRAD, MODE>(S, cnt, px[q], py[q], pz[q], P, acc[q], skips[q], mc + q);
+                    else tile_slow<KIND, true, VAL, GRAD, MODE>(S, cnt, px[q], py[q], pz[q], P, acc[q], skips[q], mc + q);
                 }
                 dv[q] += acc[q].v;
                 dg0[q] += acc[q].gx;
@@ -591,7 +641,8 @@ GatherPlan plan_gather(int kind, int K, int N, int M, bool val, bool grad) {
 
 void launch_gather(int kind, const GatherPlan& g, const float4* pack, int N, int M, const float* px, int K, int dim,
                    float sigma, float tol, bool val, bool grad, double* part, int* skipB, int* skipS,
-                   float4* tileBox, unsigned* unitCounter, cudaStream_t st) {
+                   float4* tileBox, unsigned* unitCounter, cudaStream_t st, int mode, float clamp,
+                   const float* ballR) {
     if (K <= 0 || (N + M) <= 0) return;
     Params P;
     P.pack = pack;
@@ -621,6 +672,23 @@ void launch_gather(int kind, const GatherPlan& g, const float4* pack, int N, int
     P.comps = g.comps;
     P.skipB = skipB;
     P.skipS = skipS;
+    P.clamp = clamp;
+    P.ballR = ballR;
+    if (mode != 0) {  // corrected-splat variants: value only (cache.cpp:499-597)
+        if (kind == kLap2) {
+            switch (mode) {
+                case kClampP: gather_kernel<kLap2, true, false, kClampP><<<g.grid, kThreads, 0, st>>>(P); break;
+                case kBall: gather_kernel<kLap2, true, false, kBall><<<g.grid, kThreads, 0, st>>>(P); break;
+                case kClampP | kBall: gather_kernel<kLap2, true, false, kClampP | kBall><<<g.grid, kThreads, 0, st>>>(P); break;
+                case kBall | kClampS: gather_kernel<kLap2, true, false, kBall | kClampS><<<g.grid, kThreads, 0, st>>>(P); break;
+                default: gather_kernel<kLap2, true, false, kClampP | kBall | kClampS><<<g.grid, kThreads, 0, st>>>(P); break;
+            }
+        } else {
+            gather_kernel<kScr2, true, false, kClampP><<<g.grid, kThreads, 0, st>>>(P);
+        }
+        count_launch();
+        return;
+    }
     switch (kind) {
         case kLap2: launch_kind<kLap2>(P, val, grad, g.grid, st); break;
         case kScr2: launch_kind<kScr2>(P, val, grad, g.grid, st); break;

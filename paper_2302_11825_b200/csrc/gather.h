@@ -32,7 +32,36 @@ void eval_bessel(int which, const double* t, int count, double* out, cudaStream_
 void gather_points(const double* x, const int* order, int K, int dim, float* out, cudaStream_t st);
 void launch_gather(int kind, const GatherPlan& g, const float4* pack, int N, int M, const float* px, int K, int dim,
                    float sigma, float tol, bool val, bool grad, double* part, int* skipB, int* skipS,
-                   float4* tileBox, unsigned* unitCounter, cudaStream_t st);
+                   float4* tileBox, unsigned* unitCounter, cudaStream_t st, int mode = 0, float clamp = 0.f,
+                   const float* ballR = nullptr);
+// splat modes (gather.cu SplatMode): 1 clamp dG/dn, 2 ball Green's function, 4 clamp source G^B
+constexpr int kModeClampP = 1, kModeBall = 2, kModeClampS = 4;
+
+// ray-sampled clamp correction (cache.cpp:526-550) and the ball-source correction
+// (cache.cpp:584-592); see correct.cu
+struct CorrRayEnv {
+    bvc_dev::SceneView2 region;  // region boundary
+    const int* kinds;            // region segment kinds (0 = KnownNeumann)
+    int screened;
+    double sqrtSigma;
+    double clamp, tol2, nRound;
+    float eps;                   // walk epsilon (Neumann crossings start eps/2 inside)
+    float insideTol;
+    uint32_t k0, k1;             // ray-direction key (seed, stream)
+    int useField;                // 1: u(z) = field(z); 0: counts for the walk evaluator
+    bvc_dev::DevField field;
+};
+void launch_corr_rays(const CorrRayEnv& E, const double* x, const int* order, int K, int* counts, double* bsum,
+                      int* noHit, cudaStream_t st);
+void launch_corr_emit(const CorrRayEnv& E, const double* x, const int* order, int K, const int* offsets,
+                      float2* starts, long long* gid, double* w, cudaStream_t st);
+void launch_corr_apply(const int* offsets, const int* counts, const int* order, int K, const double* w,
+                       const double* mean, double nRound, double* bsum, cudaStream_t st);
+void launch_ball_corr(const bvc_dev::SceneView2& region, float insideTol, const double* x, const int* order,
+                      const double* ballR, int K, const bvc_dev::DevField& f, double clamp, double mRound, uint32_t k0,
+                      uint32_t k1, double* ssum, cudaStream_t st);
+void launch_ball_radius(const double* x, int n, int dim, const double* hull, int nh, double* R, cudaStream_t st);
+void launch_gather_f32(const double* v, const int* order, int K, float* out, cudaStream_t st);
 void launch_finalize(const double* part, const GatherPlan& g, int K, const int* order, int N, int M, bool val,
                      bool grad, int dim, const int* skipB, const int* skipS, const PointsDev& pts, cudaStream_t st);
 

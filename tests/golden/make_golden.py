@@ -223,6 +223,36 @@ def main():
     cfg.walk.epsilon = 1e-3
     c = O.ref_generate_boundary_cache(sc, lin, rg, cfg, 11, 0)
     np.savez(os.path.join(OUT, "cache.npz"), **{k: np.asarray(v_) for k, v_ in c.items() if k != "seconds"})
+    # --- clamped / ball-kernel splats (cache.cpp:410-416, 499-597) ------------------
+    # the deterministic loops of correctedBoundarySplat (ClampOnly) and
+    # correctedSourceSplat (no f: no sampled term), and markEvaluationPoints' ball radius
+    cl = {}
+    g3 = np.random.default_rng(23)
+    v, s, lab = O.circle_geometry(segments=256)
+    sc = O.RefScene(v, s, lab)
+    loop = O.RefScene(v, s, lab)
+    rg = O.RefRegion(sc, abi.REGION_SUBDOMAIN, 0.0, subdomain=loop, eps=1e-3)
+    z, n, pdf, seg, arc = sc.boundary_sample(512, False, int(g3.integers(1 << 30)))
+    cache = dict(z=z, n=n, pdf=pdf, uHat=z[:, 0] + 0.5, dHat=n[:, 0] - 0.25, weight=np.zeros(len(z)))
+    yy, ypdf = sc.region_sample(256, False, int(g3.integers(1 << 30)))
+    scache = dict(y=yy, pdf=ypdf, f=1.0 + yy[:, 0] ** 2)
+    rr = np.concatenate([[0.0, 0.3, 0.9, 0.95, 0.99], g3.uniform(0, 0.995, 27)])
+    ph = g3.uniform(0, 2 * np.pi, len(rr))
+    xs = np.stack([rr * np.cos(ph), rr * np.sin(ph)], 1)
+    R = O.ref_ball_radius(sc, rg, xs)
+    k2 = spec(0, 0.0, 2, sc.diagonal)
+    for key, val in cache.items():
+        cl[f"b_{key}"] = val
+    for key, val in scache.items():
+        cl[f"s_{key}"] = val
+    cl["x"], cl["ballRadius"], cl["region_v"] = xs, R, rg.vertices
+    cases = [(1, 1.0), (1, 0.05), (2, 0.0), (3, 1.0), (6, 0.2), (7, 0.2)]
+    cl["cases"] = np.array(cases)
+    for i, (mode, c) in enumerate(cases):
+        st = O.ref_clamped_splat(k2, 1e-12 * sc.diagonal, cache, scache, xs, mode, c, R)
+        for key in ("boundarySum", "sourceSum", "nBoundary", "mSource", "skipped"):
+            cl[f"{i}_{key}"] = st[key]
+    np.savez(os.path.join(OUT, "clamp.npz"), **cl)
     print("golden fixtures written to", OUT)
 
 

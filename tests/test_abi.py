@@ -24,7 +24,8 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
     assert sorted(B.api.SYMBOLS) == names
-    assert lib.bvc_abi_version() == 1
+    version = int(re.search(r"#define BVC_ABI_VERSION (\d+)", open(os.path.join(ROOT, "include", "bvc_b200.h")).read())[1])
+    assert lib.bvc_abi_version() == version
 
 
 def test_library_is_built_for_sm100a():

@@ -205,3 +205,36 @@ def test_generate_boundary_cache_restatement_matches_reference(golden):
     np.testing.assert_allclose(u, g["uHat"], rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(d, g["dHat"], rtol=1e-9, atol=1e-9)
     assert stats[1] == g["stats"][1]
+
+
+def _clamp_fixture(g):
+    cache = {key: g[f"b_{key}"] for key in ("z", "n", "pdf", "uHat", "dHat", "weight")}
+    scache = {key: g[f"s_{key}"] for key in ("y", "pdf", "f")}
+    return cache, scache
+
+
+def test_clamped_splat_restatement_matches_reference(golden):
+    """correctedBoundarySplat (ClampOnly) / ball-kernel greensValue / correctedSourceSplat
+    loops (cache.cpp:410-416, 512-524, 573-582) vs the reference on identical caches."""
+    g = golden("clamp")
+    cache, scache = _clamp_fixture(g)
+    diag = 2.0 * np.sqrt(2.0)  # bounding-box diagonal of the unit 256-gon
+    spec = H.kspec(0, 0, 2, diag)
+    for i, (mode, c) in enumerate(g["cases"]):
+        st = O.oracle_clamped_splat(spec, 1e-12 * diag, cache, scache, g["x"], int(mode), float(c), g["ballRadius"])
+        for key in ("boundarySum", "sourceSum"):
+            np.testing.assert_allclose(st[key], g[f"{i}_{key}"], rtol=1e-12, atol=1e-14)
+        for key in ("nBoundary", "mSource", "skipped"):
+            assert np.array_equal(st[key], g[f"{i}_{key}"])
+    # an infinite bound is the plain splat (test_cache.cpp:748-764)
+    inf = O.oracle_clamped_splat(spec, 1e-12 * diag, cache, None, g["x"], 1, np.inf)
+    plain = O.oracle_splat(spec, 1e-12 * diag, cache, None, g["x"])
+    assert np.array_equal(inf["boundarySum"], plain["boundarySum"])
+
+
+def test_ball_radius_is_farthest_region_vertex(golden):
+    """markEvaluationPoints' ballRadius (cache.cpp:268-274)."""
+    g = golden("clamp")
+    x, v = g["x"], g["region_v"]
+    R = np.max(np.linalg.norm(v[None, :, :] - x[:, None, :], axis=2), axis=1)
+    np.testing.assert_allclose(R, g["ballRadius"], rtol=1e-15)
