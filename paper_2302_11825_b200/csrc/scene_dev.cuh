@@ -43,8 +43,12 @@ struct SceneView2 {
     unsigned long long* counts;
 };
 
+// compiled in only for the instrumented launch (bvc_walk_traffic_profile)
+template <bool COUNT>
 __device__ __forceinline__ void count_fetch(const SceneView2& S, int which) {
-    if (S.counts) S.counts[2 * (blockIdx.x * blockDim.x + threadIdx.x) + which] += 1;
+    if constexpr (COUNT) {
+        if (S.counts) S.counts[2 * (blockIdx.x * blockDim.x + threadIdx.x) + which] += 1;
+    }
 }
 
 __device__ __forceinline__ float box_dist2(const float4& b, float x, float y) {
@@ -57,7 +61,9 @@ __device__ __forceinline__ float box_dist2(const float4& b, float x, float y) {
 __device__ __forceinline__ float seg_closest(const float4& s, float x, float y, float& px, float& py, float& t) {
     float ux = s.z - s.x, uy = s.w - s.y;
     float l2 = ux * ux + uy * uy;
-    float tt = l2 > 0.0f ? ((x - s.x) * ux + (y - s.y) * uy) / l2 : 0.0f;
+    // fast division: t only places the closest point, and the distance is
+    // stationary in t there, so a 2-ulp quotient moves d^2 at second order
+    float tt = l2 > 0.0f ? __fdividef((x - s.x) * ux + (y - s.y) * uy, l2) : 0.0f;
     tt = fminf(fmaxf(tt, 0.0f), 1.0f);
     px = fmaf(tt, ux, s.x);
     py = fmaf(tt, uy, s.y);
@@ -73,7 +79,7 @@ constexpr unsigned kClsNeumann = kClsN | kClsSil, kClsAny = kClsD | kClsN | kCls
 
 // Generic best-first traversal. visit(prim) handles one primitive of a visited
 // leaf; threshold() returns the current squared pruning radius.
-template <class Visit, class Thr>
+template <bool COUNT = false, class Visit, class Thr>
 __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, float y, unsigned qmask, Visit&& visit,
                                               Thr&& threshold) {
     int stackRef[kStack];
@@ -83,7 +89,7 @@ __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, floa
     for (;;) {
         if (ref >= 0) {
             const Node2 nd = S.nodes[ref];
-            count_fetch(S, 0);
+            count_fetch<COUNT>(S, 0);
             float thr = threshold();
             float dl = (nd.mask & qmask) ? box_dist2(nd.lbox, x, y) : kFInf;
             float dr = ((nd.mask >> 3) & qmask) ? box_dist2(nd.rbox, x, y) : kFInf;
@@ -104,7 +110,7 @@ __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, floa
             int start = code >> 3, count = (code & 7) + 1;
             for (int i = start; i < start + count; ++i) {
                 const Prim2 p = S.prims[i];
-                count_fetch(S, 1);
+                count_fetch<COUNT>(S, 1);
                 if ((1u << p.label) & qmask) visit(p);
             }
         }
@@ -124,11 +130,26 @@ struct Closest {
     int seg;
 };
 
-// Scene::closestPoint (scene.cpp:133-144; bvh.cpp:53-69)
+// closest point of one segment (by id) as a traversal warm start
+__device__ __forceinline__ Closest closest_on(const SceneView2& S, int seg, float x, float y) {
+    Closest c;
+    c.d2 = seg_closest(S.segAB[seg], x, y, c.px, c.py, c.t);
+    c.seg = seg;
+    return c;
+}
+
+// Scene::closestPoint (scene.cpp:133-144; bvh.cpp:53-69). hint >= 0: a segment of
+// the queried classes whose distance seeds the pruning radius (the walker's
+// previous closest segment), so far subtrees are never pushed.
+template <bool COUNT = false>
 __device__ __forceinline__ Closest closest_point(const SceneView2& S, float x, float y, unsigned qmask,
-                                                 float maxD2 = kFInf) {
+                                                 float maxD2 = kFInf, int hint = -1) {
     Closest c{maxD2, 0.0f, 0.0f, 0.0f, -1};
-    traverse_near(
+    if (hint >= 0) {
+        Closest h = closest_on(S, hint, x, y);
+        if (h.d2 < c.d2) c = h;
+    }
+    traverse_near<COUNT>(
         S, x, y, qmask,
         [&](const Prim2& p) {
             float px, py, t;
@@ -151,9 +172,10 @@ __device__ __forceinline__ bool silhouette_ok(const SceneView2& S, int k, float 
 }
 
 // Scene::silhouetteDistance (scene.cpp:174-185); returns squared distance
+template <bool COUNT = false>
 __device__ __forceinline__ float silhouette_dist2(const SceneView2& S, float x, float y) {
     float best = kFInf;
-    traverse_near(
+    traverse_near<COUNT>(
         S, x, y, kClsSil,
         [&](const Prim2& p) {
             float d2;
@@ -172,11 +194,12 @@ struct StarQuery {
     Closest D;
     float s2;
 };
-__device__ __forceinline__ StarQuery star_query(const SceneView2& S, float x, float y, float eps2) {
+template <bool COUNT = false>
+__device__ __forceinline__ StarQuery star_query(const SceneView2& S, float x, float y, float eps2, int hint = -1) {
     StarQuery q;
-    q.D = Closest{kFInf, 0.0f, 0.0f, 0.0f, -1};
+    q.D = hint >= 0 ? closest_on(S, hint, x, y) : Closest{kFInf, 0.0f, 0.0f, 0.0f, -1};
     q.s2 = kFInf;
-    traverse_near(
+    traverse_near<COUNT>(
         S, x, y, kClsD | kClsSil,
         [&](const Prim2& p) {
             if (p.label == 0) {
@@ -224,6 +247,7 @@ struct RayHit {
 // with t in (tMin, tMax] among the filtered segments, skipping `skipSeg` (the
 // segment the walk currently stands on: a ray leaving a straight segment cannot
 // hit it again, and skipping it keeps FP32 re-hits out).
+template <bool COUNT = false>
 __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, float oy, float dx, float dy,
                                                 float tMax, unsigned qmask, float tMin, int skipSeg) {
     RayHit h{kFInf, 0.0f, 0.0f, 0.0f, -1};
@@ -234,7 +258,7 @@ __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, f
     for (;;) {
         if (ref >= 0) {
             const Node2 nd = S.nodes[ref];
-            count_fetch(S, 0);
+            count_fetch<COUNT>(S, 0);
             bool vl = (nd.mask & qmask) && ray_box(nd.lbox, ox, oy, idx, idy, limit);
             bool vr = ((nd.mask >> 3) & qmask) && ray_box(nd.rbox, ox, oy, idx, idy, limit);
             if (vl && vr) { stack[sp++] = nd.right; ref = nd.left; continue; }
@@ -245,7 +269,7 @@ __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, f
             int start = code >> 3, count = (code & 7) + 1;
             for (int i = start; i < start + count; ++i) {
                 const Prim2 p = S.prims[i];
-                count_fetch(S, 1);
+                count_fetch<COUNT>(S, 1);
                 if (!((1u << p.label) & qmask) || p.id == skipSeg) continue;
                 // watertight crossing test: each endpoint is classified by its side
                 // of the ray; a vertex shared by two segments gets the same sign in
@@ -276,8 +300,9 @@ __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, f
 // Scene::inside (scene.cpp:240-254): boundary-inclusive within tol, then crossing
 // parity along +x with the straddle form; only leaves whose box spans x.y and
 // reaches past x.x are visited.
+template <bool COUNT = false>
 __device__ __forceinline__ bool inside(const SceneView2& S, float x, float y, float tol) {
-    Closest c = closest_point(S, x, y, kClsAny, tol * tol);
+    Closest c = closest_point<COUNT>(S, x, y, kClsAny, tol * tol);
     if (c.seg >= 0) return true;
     bool in = false;
     int stack[kStack];
@@ -285,7 +310,7 @@ __device__ __forceinline__ bool inside(const SceneView2& S, float x, float y, fl
     for (;;) {
         if (ref >= 0) {
             const Node2 nd = S.nodes[ref];
-            count_fetch(S, 0);
+            count_fetch<COUNT>(S, 0);
             bool vl = (nd.mask & 7u) && nd.lbox.y <= y && nd.lbox.w >= y && nd.lbox.z > x;
             bool vr = ((nd.mask >> 3) & 7u) && nd.rbox.y <= y && nd.rbox.w >= y && nd.rbox.z > x;
             if (vl && vr) { stack[sp++] = nd.right; ref = nd.left; continue; }
@@ -296,7 +321,7 @@ __device__ __forceinline__ bool inside(const SceneView2& S, float x, float y, fl
             int start = code >> 3, count = (code & 7) + 1;
             for (int i = start; i < start + count; ++i) {
                 const float4 s = S.prims[i].seg;
-                count_fetch(S, 1);
+                count_fetch<COUNT>(S, 1);
                 if ((s.y > y) == (s.w > y)) continue;
                 float xc = s.x + (y - s.y) / (s.w - s.y) * (s.z - s.x);
                 if (x < xc) in = !in;

@@ -155,39 +155,44 @@ __device__ float neumann_term(const WalkEnv& E, float x, float y, float R, float
 struct Walk {
     float x, y, acc, weight, inx, iny;
     int onN, prevSeg, step;
+    int lastD;  // previous step's closest Dirichlet segment: the next query's warm start
 };
 
 __device__ __forceinline__ void walk_start(Walk& w, float x, float y) {
     w.x = x; w.y = y; w.acc = 0.0f; w.weight = 1.0f; w.inx = 0.0f; w.iny = 0.0f;
-    w.onN = 0; w.prevSeg = -1; w.step = 0;
+    w.onN = 0; w.prevSeg = -1; w.step = 0; w.lastD = -1;
 }
 
 // One iteration of walkSampleImpl's loop (pointwise.cpp:130-161). Returns true
-// when the walk terminated; then *value holds its estimate.
+// when the walk terminated; then *value holds its estimate. The scene traits
+// (Neumann boundary, screening, source) and the traffic counters are
+// compile-time, so each configuration runs only its own code.
+template <bool NEU, bool SCR, bool SRC, bool COUNT>
 __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, float& value, int& trunc,
                                           unsigned long long& steps) {
     Closest cp;
     float R;
     ++steps;
     // (scenes without Dirichlet segments are rejected on the host, pointwise.cpp:217-218)
-    if (E.hasNeumann) {
+    if constexpr (NEU) {
         // a Dirichlet segment farther than the closest visible silhouette may be
         // pruned (q.D.seg < 0, d2 = inf): R is then the silhouette distance
-        StarQuery q = star_query(E.S, w.x, w.y, E.eps * E.eps);
+        StarQuery q = star_query<COUNT>(E.S, w.x, w.y, E.eps * E.eps, w.lastD);
         cp = q.D;
         float dD = sqrtf(cp.d2);
         if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
         R = fminf(dD, sqrtf(q.s2));
     } else {
-        cp = closest_point(E.S, w.x, w.y, kClsD);
+        cp = closest_point<COUNT>(E.S, w.x, w.y, kClsD, kFInf, w.lastD);
         float dD = sqrtf(cp.d2);
         if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
         R = dD;
     }
+    w.lastD = cp.seg;
     R = fmaxf(R, E.rmin);
     float factor = w.onN ? 2.0f : 1.0f;
-    if (E.hasSource) w.acc += w.weight * factor * source_term(E, w.x, w.y, R, u01(rnd.y), u01(rnd.z));
-    if (E.hasNeumann && E.hasH) w.acc += w.weight * factor * neumann_term(E, w.x, w.y, R, u01(rnd.w));
+    if constexpr (SRC) w.acc += w.weight * factor * source_term(E, w.x, w.y, R, u01(rnd.y), u01(rnd.z));
+    if (NEU && E.hasH) w.acc += w.weight * factor * neumann_term(E, w.x, w.y, R, u01(rnd.w));
     // direction: full circle, or the half circle around the inward normal on Neumann
     float dx, dy;
     if (w.onN) {
@@ -200,8 +205,8 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
     }
     float travel = R;
     bool hit = false;
-    if (E.hasNeumann) {
-        RayHit h = intersect_ray(E.S, w.x, w.y, dx, dy, R, kClsNeumann, E.tguard, w.onN ? w.prevSeg : -1);
+    if constexpr (NEU) {
+        RayHit h = intersect_ray<COUNT>(E.S, w.x, w.y, dx, dy, R, kClsNeumann, E.tguard, w.onN ? w.prevSeg : -1);
         if (h.seg >= 0) {
             hit = true;
             travel = h.t;
@@ -225,7 +230,7 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
         w.onN = 0;
         w.prevSeg = -1;
     }
-    if (E.P.screened) w.weight *= ball_sphere_weight(E.P.sqrtSigma, R, travel);
+    if constexpr (SCR) w.weight *= ball_sphere_weight(E.P.sqrtSigma, R, travel);
     // safety net: a walker that left the scene's neighbourhood (impossible in exact
     // arithmetic) ends like a truncated walk instead of wandering to maxSteps
     bool escaped = fabsf(w.x - E.cx) > E.escape || fabsf(w.y - E.cy) > E.escape;
@@ -256,6 +261,7 @@ __device__ __forceinline__ U4 draw4(const WalkEnv& E, Task& t) {
     return philox4x32_10(c, E.k0, E.k1);
 }
 
+template <bool NEU, bool SCR, bool SRC, bool COUNT>
 __global__ void __launch_bounds__(kWalkThreads) walk_kernel(const WalkEnv E, const WalkJob J) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -288,7 +294,8 @@ __global__ void __launch_bounds__(kWalkThreads) walk_kernel(const WalkEnv E, con
                 t.trunc = 0;
                 if (id < nUtot) {
                     t.role = 0;
-                    t.pt = static_cast<int>(id / J.nU);
+                    t.pt = id < 0x7fffffffLL ? static_cast<int>(static_cast<unsigned>(id) / static_cast<unsigned>(J.nU))
+                                             : static_cast<int>(id / J.nU);
                     t.k = static_cast<int>(id - static_cast<long long>(t.pt) * J.nU);
                     long long g = J.gidU ? J.gidU[t.pt] : J.gidBaseU + t.pt;
                     t.rid = static_cast<unsigned long long>(g) * J.nU + t.k;
@@ -297,7 +304,8 @@ __global__ void __launch_bounds__(kWalkThreads) walk_kernel(const WalkEnv E, con
                 } else {
                     long long d = id - nUtot;
                     t.role = 1;
-                    t.pt = static_cast<int>(d / J.nD);
+                    t.pt = d < 0x7fffffffLL ? static_cast<int>(static_cast<unsigned>(d) / static_cast<unsigned>(J.nD))
+                                            : static_cast<int>(d / J.nD);
                     t.k = static_cast<int>(d - static_cast<long long>(t.pt) * J.nD);
                     long long g = J.gidD ? J.gidD[t.pt] : t.pt;
                     t.rid = static_cast<unsigned long long>(g) * J.nD + t.k;
@@ -309,7 +317,7 @@ __global__ void __launch_bounds__(kWalkThreads) walk_kernel(const WalkEnv E, con
                     __sincosf(kTwoPi * u01(r0.x), &t.diry, &t.dirx);
                     t.vx = 0.0f;
                     t.vy = 0.0f;
-                    if (E.hasSource) {
+                    if constexpr (SRC) {
                         BallSample b = sample_ball(c.x, c.y, t.R, u01(r0.y), u01(r0.z));
                         float fy = field_eval(E.P.f, b.x, b.y);
                         if (fy != 0.0f) {
@@ -319,7 +327,7 @@ __global__ void __launch_bounds__(kWalkThreads) walk_kernel(const WalkEnv E, con
                             t.vy += ddy * gf;
                         }
                     }
-                    if (E.P.screened && E.P.sigma > 0.0f) {
+                    if (SCR && E.P.sigma > 0.0f) {
                         BallSample b = sample_ball(c.x, c.y, t.R, u01(r0.w), u01(r1.x));
                         float ddx = b.x - c.x, ddy = b.y - c.y;
                         float gf = (1.0f / (t.R * t.R) - 1.0f / (ddx * ddx + ddy * ddy)) * kInv2Pi *
@@ -342,7 +350,7 @@ __global__ void __launch_bounds__(kWalkThreads) walk_kernel(const WalkEnv E, con
         if (active) {
             U4 rnd = draw4(E, t);
             float value;
-            if (walk_step(E, w, rnd, value, t.trunc, steps)) {
+            if (walk_step<NEU, SCR, SRC, COUNT>(E, w, rnd, value, t.trunc, steps)) {
                 if (t.role == 0) {
                     J.outU[t.id] = value;
                     if (t.trunc && J.truncU) atomicAdd(J.truncU + t.pt, 1);
@@ -352,7 +360,7 @@ __global__ void __launch_bounds__(kWalkThreads) walk_kernel(const WalkEnv E, con
                     float s = (2.0f / t.R) * value;
                     t.vx = fmaf(s, t.dirx, t.vx);
                     t.vy = fmaf(s, t.diry, t.vy);
-                    if (E.P.screened && E.P.sigma > 0.0f) {
+                    if (SCR && E.P.sigma > 0.0f) {
                         t.phase = 1;
                         walk_start(w, t.y2x, t.y2y);
                     } else {
@@ -568,19 +576,34 @@ inline int blocks(long long n, int t) { return static_cast<int>((n + t - 1) / t)
 
 }  // namespace
 
-void launch_walk_job(const WalkEnv& env, const WalkJob& job, cudaStream_t st) {
-    long long total = static_cast<long long>(job.nPtsU) * job.nU + static_cast<long long>(job.nPtsD) * job.nD;
-    if (total <= 0) return;
-    cudaMemsetAsync(job.counter, 0, sizeof(unsigned long long), st);
+template <bool NEU, bool SCR, bool SRC, bool COUNT>
+void launch_walk_t(const WalkEnv& env, const WalkJob& job, long long total, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int perSm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, walk_kernel, kWalkThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, walk_kernel<NEU, SCR, SRC, COUNT>, kWalkThreads, 0);
     perSm = perSm > 0 ? perSm : 1;
     long long want = (total + kWalkThreads - 1) / kWalkThreads;
     int grid = static_cast<int>(want < static_cast<long long>(sms) * perSm ? want : static_cast<long long>(sms) * perSm);
-    walk_kernel<<<grid, kWalkThreads, 0, st>>>(env, job);
+    walk_kernel<NEU, SCR, SRC, COUNT><<<grid, kWalkThreads, 0, st>>>(env, job);
+}
+
+void launch_walk_job(const WalkEnv& env, const WalkJob& job, cudaStream_t st) {
+    long long total = static_cast<long long>(job.nPtsU) * job.nU + static_cast<long long>(job.nPtsD) * job.nD;
+    if (total <= 0) return;
+    cudaMemsetAsync(job.counter, 0, sizeof(unsigned long long), st);
+    const int code = (env.hasNeumann ? 1 : 0) | (env.P.screened ? 2 : 0) | (env.hasSource ? 4 : 0) |
+                     (env.S.counts ? 8 : 0);
+    switch (code) {
+#define BVC_WALK_CASE(c) \
+    case c: launch_walk_t<(c & 1) != 0, (c & 2) != 0, (c & 4) != 0, (c & 8) != 0>(env, job, total, st); break;
+        BVC_WALK_CASE(0) BVC_WALK_CASE(1) BVC_WALK_CASE(2) BVC_WALK_CASE(3)
+        BVC_WALK_CASE(4) BVC_WALK_CASE(5) BVC_WALK_CASE(6) BVC_WALK_CASE(7)
+        BVC_WALK_CASE(8) BVC_WALK_CASE(9) BVC_WALK_CASE(10) BVC_WALK_CASE(11)
+        BVC_WALK_CASE(12) BVC_WALK_CASE(13) BVC_WALK_CASE(14) BVC_WALK_CASE(15)
+#undef BVC_WALK_CASE
+    }
     count_launch();
 }
 
