@@ -59,7 +59,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 
 // --- per-pair kernels ---------------------------------------------------------
-// 2D: payload a = (zx, zy, nx, ny), b = per-kind constants
+// 2D: payload a = (zx, zy, nx, ny) (Laplace boundary: (zx, zy, A nx, A ny)),
+// b = per-kind constants
 struct Acc {
     float v, gx, gy, gz;
 };
@@ -110,22 +111,29 @@ __device__ __forceinline__ void pair(const float4 a, const float4 b, float px, f
         if constexpr (KIND == kLap2) {
             float ir2 = f_rcp(r2);
             if constexpr (!SRC) {
-                float nd = fmaf(a.z, dx, a.w * dy);
-                float p = nd * ir2;
+                // a.zw = A n (A folded into the normal): ndA = A (n.d), A p = ndA / r^2
+                float ndA = fmaf(a.z, dx, a.w * dy);
                 if constexpr (VAL) {
                     if constexpr (MODE == 0) {
-                        acc.v = fmaf(b.x, p, fmaf(-b.y, f_lg2(r2), acc.v));
+                        acc.v = fmaf(ndA, ir2, fmaf(-b.y, f_lg2(r2), acc.v));
                     } else {
-                        float pc = (MODE & kClampP) ? fminf(fmaxf(p, -mc->c2pi), mc->c2pi) : p;
+                        // clamp p = n.d / r^2 to +-2 pi c, i.e. A p to +-2 pi c |A|; an
+                        // unsaturated pair takes the plain path's exact operations
                         float l = (MODE & kBall) ? f_lg2(fminf(r2, mc->R2)) - mc->lgR2 : f_lg2(r2);
-                        acc.v = fmaf(b.x, pc, fmaf(-b.y, l, acc.v));
+                        float base = fmaf(-b.y, l, acc.v);
+                        if constexpr ((MODE & kClampP) != 0) {
+                            float pA = ndA * ir2;
+                            float lim = mc->c2pi * fabsf(b.x);
+                            acc.v = fabsf(pA) > lim ? base + copysignf(lim, pA) : fmaf(ndA, ir2, base);
+                        } else {
+                            acc.v = fmaf(ndA, ir2, base);
+                        }
                     }
                 }
                 if constexpr (GRAD) {
-                    float q = fmaf(b.w, p, b.z) * ir2;  // (2A p + Bg) / r^2
-                    float c = b.x * ir2;                // A / r^2
-                    acc.gx = fmaf(q, dx, fmaf(-c, a.z, acc.gx));
-                    acc.gy = fmaf(q, dy, fmaf(-c, a.w, acc.gy));
+                    float q = fmaf(2.0f * ndA, ir2, b.z) * ir2;  // (2A p + Bg) / r^2
+                    acc.gx = fmaf(q, dx, fmaf(-ir2, a.z, acc.gx));  // - (A / r^2) n
+                    acc.gy = fmaf(q, dy, fmaf(-ir2, a.w, acc.gy));
                 }
             } else {
                 if constexpr (VAL) {
@@ -361,10 +369,12 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
                     if (!src) tile_slow<KIND, false, VAL, GRAD, MODE>(S, cnt, px[q], py[q], pz[q], P, acc[q], skips[q], mc + q);
                     else tile_slow<KIND, true, VAL, GRAD, MODE>(S, cnt, px[q], py[q], pz[q], P, acc[q], skips[q], mc + q);
                 }
-                dv[q] += acc[q].v;
-                dg0[q] += acc[q].gx;
-                dg1[q] += acc[q].gy;
-                dg2[q] += acc[q].gz;
+                if (VAL) dv[q] += acc[q].v;
+                if (GRAD) {
+                    dg0[q] += acc[q].gx;
+                    dg1[q] += acc[q].gy;
+                    if (D3) dg2[q] += acc[q].gz;
+                }
             }
             __syncthreads();  // everyone is done reading buffer st
             if (tid == 0 && it + 2 < nT) {
@@ -427,10 +437,10 @@ __device__ __forceinline__ void pack_boundary_one(const CacheSample& s, int n, i
     const double inv2pi = 0.15915494309189533577, inv4pi = 0.07957747154594766788, ln2 = 0.69314718055994530942;
     float4 a, b;
     if (kind == kLap2) {
-        a = make_float4(s.z[0], s.z[1], s.n[0], s.n[1]);
         double A = w * u * inv2pi;
+        a = make_float4(s.z[0], s.z[1], static_cast<float>(A * s.n[0]), static_cast<float>(A * s.n[1]));
         b = make_float4(static_cast<float>(A), static_cast<float>(w * d * ln2 * 0.5 * inv2pi),
-                        static_cast<float>(w * d * inv2pi), static_cast<float>(2.0 * A));
+                        static_cast<float>(w * d * inv2pi), 0.f);
     } else if (kind == kScr2) {
         a = make_float4(s.z[0], s.z[1], s.n[0], s.n[1]);
         b = make_float4(static_cast<float>(w * u * inv2pi), static_cast<float>(w * d * inv2pi), 0.f, 0.f);
@@ -616,22 +626,18 @@ GatherPlan plan_gather(int kind, int K, int N, int M, bool val, bool grad) {
                               : occupancy<kScr3>(val, grad);
     g.tiles = (K + kPT - 1) / kPT;
     long long slots = static_cast<long long>(sms) * occ;
-    // pick the chunk size (a multiple of kTS) whose unit count fills whole waves best,
-    // preferring fewer, larger chunks on ties
-    double bestEff = -1.0;
+    // The chunk size depends only on the cache (N + M), never on K: each point's
+    // sum runs over the same chunks in the same order however the points are
+    // split into ranges or ranks (bitwise shard invariance). 16 chunks give the
+    // dynamic unit queue several waves at the configs' K (C2: 510 point tiles x 16
+    // = 9 waves); a ~1-wave launch of long units measured 2x slower, because the
+    // block scheduler does not always place every slot at once.
     int total = N + M;
     int maxTiles = (total + kTS - 1) / kTS;
-    for (int ct = 1; ct <= maxTiles; ++ct) {
-        int chunk = ct * kTS;
-        int cb = (N + chunk - 1) / chunk, cs = (M + chunk - 1) / chunk;
-        long long units = static_cast<long long>(g.tiles) * (cb + cs);
-        long long waves = (units + slots - 1) / slots;
-        double eff = static_cast<double>(units) / static_cast<double>(waves * slots);
-        // small per-unit overhead penalty for tiny chunks
-        eff *= static_cast<double>(chunk) / (chunk + 2.0 * kTS);
-        if (eff > bestEff + 1e-9) { bestEff = eff; g.chunk = chunk; g.chunksB = cb; g.chunksS = cs; }
-        if (units < slots && ct > 1 && cb + cs <= 1) break;
-    }
+    int ct = maxTiles > 16 ? (maxTiles + 15) / 16 : 1;
+    g.chunk = ct * kTS;
+    g.chunksB = (N + g.chunk - 1) / g.chunk;
+    g.chunksS = (M + g.chunk - 1) / g.chunk;
     long long units = static_cast<long long>(g.tiles) * (g.chunksB + g.chunksS);
     g.grid = static_cast<int>(units < slots ? units : slots);
     g.grid = g.grid > 0 ? g.grid : 1;

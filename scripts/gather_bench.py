@@ -3,10 +3,13 @@ import sys, json, numpy as np, torch
 import paper_2302_11825_b200 as B
 from paper_2302_11825_b200 import abi
 
-def run(kind, sigma, dim, N, M, K, val=True, grad=True, reps=10):
+def run(kind, sigma, dim, N, M, K, val=True, grad=True, reps=10, ordered=True):
     rng = np.random.default_rng(0)
     if dim == 2:
-        th = rng.uniform(0, 2 * np.pi, N); z = np.stack([np.cos(th), np.sin(th)], 1)
+        th = rng.uniform(0, 2 * np.pi, N)
+        if ordered:  # caches come out ordered along the loop (stratified sampler)
+            th = np.sort(th)
+        z = np.stack([np.cos(th), np.sin(th)], 1)
         x = rng.uniform(-0.65, 0.65, (K, 2))
         ys = rng.uniform(-0.6, 0.6, (M, 2))
     else:
@@ -24,6 +27,12 @@ def run(kind, sigma, dim, N, M, K, val=True, grad=True, reps=10):
     t = e0.elapsed_time(e1) / 1e3 / reps
     return K * (N + M) / t, t
 
+if __name__ != "__main__":  # imported by gather_one.py: run a single case
+    import os
+    case = int(os.environ.get("GATHER_CASE", "1"))
+    sel = [("C1", 0, 0.0, 2, 4096, 0, 46112, True, False), ("C2", 0, 0.0, 2, 16384, 0, 261120, True, True)][case]
+    run(*sel[1:], reps=2)
+    raise SystemExit(0)
 props = torch.cuda.get_device_properties(0); sms = props.multi_processor_count
 f = 1965e6
 cases = [("C1 lap2 u", 0, 0.0, 2, 4096, 0, 46112, True, False, (9, 2)),
@@ -32,6 +41,8 @@ cases = [("C1 lap2 u", 0, 0.0, 2, 4096, 0, 46112, True, False, (9, 2)),
          ("C4 lap3 u", 0, 0.0, 3, 262144, 0, 131072, True, False, (14, 1)),
          ("C5 scr3 u", 1, 1.0, 3, 262144, 0, 131072, True, False, (20, 2))]
 for name, kind, sg, dim, N, M, K, v, g, (F, S) in cases:
-    rate, t = run(kind, sg, dim, N, M, K, v, g)
-    bound = sms * f / max(F / 128, S / 16)
-    print(json.dumps({"case": name, "pairs_per_s": rate, "ms": t * 1e3, "bound": bound, "frac": rate / bound}))
+    for ordered in ([True, False] if dim == 2 else [True]):
+        rate, t = run(kind, sg, dim, N, M, K, v, g, ordered=ordered)
+        bound = sms * f / max(F / 128, S / 16)
+        print(json.dumps({"case": name, "ordered": ordered, "pairs_per_s": rate, "ms": t * 1e3, "bound": bound,
+                          "frac": rate / bound}))
