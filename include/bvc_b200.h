@@ -327,6 +327,35 @@ int bvc_update_solution(bvc_scene scene, const bvc_problem* problem, bvc_region 
                         const bvc_cache_config* cfg, bvc_eval_points pts, uint64_t seed,
                         uint64_t round, int gradients, bvc_round_stats* stats);
 
+/* ---- streamlines (runStreamlines tools/src/runner.cpp:285-373) -------------- */
+typedef enum { BVC_STREAM_OK = 0, BVC_STREAM_OUTSIDE = 1, BVC_STREAM_ZERO_GRADIENT = 2 } bvc_stream_reason;
+/* Heun tracing along the unit gradient of `rounds` retained cache rounds (seed,
+   round 0..rounds-1), all seeds advancing together (two batched gradient gathers
+   per step). points: nSeeds * (steps + 1) * 2 doubles, seed s's polyline at
+   [s * (steps + 1) * 2 ...], counts[s] points (0 = the seed itself is outside);
+   reasons[s] = bvc_stream_reason (why the trace stopped; OK = ran all steps). */
+int bvc_trace_streamlines(bvc_scene scene, const bvc_problem* problem, bvc_region region,
+                          const bvc_cache_config* cfg, uint64_t seed, int rounds, const double* seeds,
+                          int nSeeds, double step, int steps, double* points, int* counts,
+                          int* reasons);
+
+/* ---- data formats -------------------------------------------- */
+/* GridField CSV `x,y,value,valid`, %.17g, row-major y-rows (grid.h:35-37, grid.cpp:22-80);
+   valid may be NULL (all valid). load: call with values = valid = NULL to read the shape. */
+int bvc_grid_save_csv(const char* path, double originX, double originY, double spacing, int nx,
+                      int ny, const double* values, const uint8_t* valid);
+int bvc_grid_load_csv(const char* path, double* originX, double* originY, double* spacing,
+                      int* nx, int* ny, double* values, uint8_t* valid, size_t capacity);
+/* rmse over jointly valid nodes (grid.cpp:82-96) */
+int bvc_grid_rmse(const double* a, const uint8_t* validA, const double* b, const uint8_t* validB,
+                  size_t n, double* out);
+/* binary PGM (P5) plus the `.txt` legend (tools/src/image.cpp:12-51) */
+int bvc_grid_save_pgm(const char* path, int nx, int ny, const double* values, const uint8_t* valid,
+                      int autoRange, double lo, double hi);
+/* streamline CSV `seed,step,x,y,reason` (runner.cpp:333-369) */
+int bvc_streamlines_write_csv(const char* path, const double* seeds, int nSeeds, int steps,
+                              const double* points, const int* counts, const int* reasons);
+
 /* ---- pointwise estimators (pointwise.h:62-76), batched over n points -------- */
 /* point i uses cfg->stream for i == 0 when n == 1, else streams[i] (NULL => mixKey(stream,i)) */
 int bvc_wos_solve(bvc_scene scene, const bvc_problem* problem, const double* x, size_t n,

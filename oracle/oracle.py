@@ -164,6 +164,9 @@ def ref_lib():
                                         _dp, _dp, C.c_void_p, C.c_int, _dp, _dp, _dp, C.c_size_t, _dp, C.c_int,
                                         C.c_double, C.c_void_p, _dp, _dp, _i64p, _i64p, _i64p]
         L.ref_ball_radius.argtypes = [C.c_void_p, C.c_void_p, _dp, C.c_size_t, _dp]
+        L.ref_grid_save_csv.argtypes = [C.c_char_p, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, _dp,
+                                        C.c_void_p]
+        L.ref_grid_load_rmse.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_double)]
         L.ref_mark_points.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(abi.CacheConfig), _dp,
                                       C.c_size_t, _u8p, _u8p]
         L.ref_update_solution.argtypes = [C.c_void_p, C.POINTER(abi.Problem), C.c_void_p,
@@ -535,6 +538,72 @@ def ref_ball_radius(scene: "RefScene", region: "RefRegion", x):
     R = np.zeros(len(x))
     _check_ref(ref_lib().ref_ball_radius(scene.h, region.h, x.ravel(), C.c_size_t(len(x)), R))
     return R
+
+
+def ref_grid_save_csv(path, origin, spacing, values, valid=None):
+    """The reference's saveGridCsv (grid.cpp:22-34)."""
+    v = _f64(values)
+    ny, nx = v.shape
+    ok = None if valid is None else np.ascontiguousarray(valid, dtype=np.uint8)
+    _check_ref(ref_lib().ref_grid_save_csv(str(path).encode(), origin[0], origin[1], spacing, nx, ny, v.ravel(),
+                                           None if ok is None else ok.ctypes.data))
+
+
+def ref_grid_load_rmse(path_a, path_b):
+    """rmse(loadGridCsv(a), loadGridCsv(b)) of the reference (grid.cpp:36-96)."""
+    out = C.c_double()
+    _check_ref(ref_lib().ref_grid_load_rmse(str(path_a).encode(), str(path_b).encode(), C.byref(out)))
+    return out.value
+
+
+def ref_streamlines(scene, region, cfg, spec, tol, caches, seeds, h, steps):
+    """runStreamlines' tracing loop (tools/src/runner.cpp:310-369) restated in Python over
+    the reference's own Scene::inside, markEvaluationPoints and splatGradient, on given
+    (boundary, source) cache pairs. Returns (polylines, reasons) like api.trace_streamlines."""
+    def direction(p):
+        if not scene.inside(np.array([p]))[0]:
+            return None, "outside"
+        if not region.whole_domain and not region.boundary.inside(np.array([p]))[0]:
+            return None, "outside"
+        fb, _ = ref_mark_points(scene, region, cfg, [p])
+        if fb[0]:
+            return None, "outside"
+        st = None
+        for bc, sc in caches:
+            st = ref_splat(spec, tol, bc, sc, [p], value=False, gradient=True, threads=1, state=st)
+        g = gradient(st)[0]
+        n = float(np.linalg.norm(g))
+        if n < 1e-12:
+            return None, "zero-gradient"
+        return g / n, ""
+
+    lines, reasons = [], []
+    for x0 in np.asarray(seeds, float):
+        x = x0.copy()
+        _, reason = direction(x)
+        if reason == "outside":
+            lines.append(np.zeros((0, 2)))
+            reasons.append("outside")
+            continue
+        pts = [x.copy()]
+        stop = reason
+        k = 1
+        while k <= steps and not stop:
+            k1, stop = direction(x)
+            if stop:
+                break
+            k2, probe = direction(x + h * k1)
+            nxt = x + 0.5 * h * (k1 + k2) if not probe else x + h * k1
+            _, landed = direction(nxt)
+            if landed == "outside":
+                stop = "outside"
+                break
+            x = nxt
+            pts.append(x.copy())
+            k += 1
+        lines.append(np.array(pts))
+        reasons.append(stop or "ok")
+    return lines, reasons
 
 
 def solution(st):

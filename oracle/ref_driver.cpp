@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "bvc/cache.h"
+#include "bvc/grid.h"
 #include "bvc/kernels.h"
 #include "bvc/parallel.h"
 #include "bvc/pointwise.h"
@@ -451,6 +452,22 @@ int ref_ball_radius(void* sp, void* rp, const double* x, size_t n, double* radiu
         markEvaluationPoints(*static_cast<Scene*>(sp), *static_cast<SolveRegion*>(rp), c, pts);
         for (size_t k = 0; k < n; ++k) radius[k] = pts[k].ballRadius;
     });
+}
+
+// GridField CSV writer and rmse (grid.cpp:22-34, 82-96)
+int ref_grid_save_csv(const char* path, double ox, double oy, double h, int nx, int ny, const double* values,
+                      const uint8_t* valid) {
+    GUARD({
+        GridField g = GridField::make(Vector2(ox, oy), h, nx, ny);
+        for (size_t i = 0; i < g.values.size(); ++i) {
+            g.values[i] = values[i];
+            g.valid[i] = valid ? valid[i] != 0 : 1;
+        }
+        saveGridCsv(g, path);
+    });
+}
+int ref_grid_load_rmse(const char* pathA, const char* pathB, double* out) {
+    GUARD({ *out = rmse(loadGridCsv(pathA), loadGridCsv(pathB)); });
 }
 
 // markEvaluationPoints: fallback / gradientUnreliable flags

@@ -32,7 +32,8 @@ SYMBOLS = (
     "bvc_make_splat_config bvc_splat_solution bvc_splat_gradient bvc_splat_solution_gradient bvc_splat_range "
     "bvc_update_solution bvc_wos_solve bvc_wost_solve bvc_wost_gradient bvc_wost_normal_derivative "
     "bvc_walk_traffic_profile bvc_eval_kernels bvc_eval_bessel bvc_corrected_boundary_splat "
-    "bvc_corrected_source_splat"
+    "bvc_corrected_source_splat bvc_trace_streamlines bvc_grid_save_csv bvc_grid_load_csv bvc_grid_rmse "
+    "bvc_grid_save_pgm bvc_streamlines_write_csv"
 ).split()
 
 
@@ -636,3 +637,79 @@ def eval_bessel(which, t):
     out = np.zeros(len(t))
     _check(lib().bvc_eval_bessel(int(which), _ptr(t), C.c_size_t(len(t)), _ptr(out)))
     return out
+
+
+# ----------------------------------------------------------------------------
+# streamlines and data formats
+# ----------------------------------------------------------------------------
+
+STREAM_REASONS = ("ok", "outside", "zero-gradient")
+
+
+def trace_streamlines(scene: Scene, pb, region: SolveRegion, cfg, seed, rounds, seeds, step, steps) -> dict:
+    """runStreamlines (tools/src/runner.cpp:285-373) on the device: Heun steps along the
+    unit gradient of `rounds` retained cache rounds. Returns the polylines (one (m, 2)
+    array per seed, empty for a seed outside the region) and the stop reasons."""
+    seeds = _f64(seeds, 2)
+    n = len(seeds)
+    pts = np.zeros((n, steps + 1, 2))
+    counts = np.zeros(n, np.int32)
+    reasons = np.zeros(n, np.int32)
+    _check(lib().bvc_trace_streamlines(scene.h, C.byref(pb), region.h, C.byref(cfg), C.c_uint64(seed), int(rounds),
+                                       _ptr(seeds), n, C.c_double(step), int(steps), _ptr(pts),
+                                       _ptr(counts, C.c_int), _ptr(reasons, C.c_int)))
+    return dict(seeds=seeds, points=pts, counts=counts, reason_codes=reasons, steps=steps,
+                polylines=[pts[i, :counts[i]].copy() for i in range(n)],
+                reasons=[STREAM_REASONS[r] for r in reasons])
+
+
+def write_streamlines_csv(path, traced: dict):
+    """The streamline CSV of runStreamlines (`seed,step,x,y,reason`, %.17g)."""
+    _check(lib().bvc_streamlines_write_csv(str(path).encode(), _ptr(traced["seeds"]), len(traced["seeds"]),
+                                           int(traced["steps"]), _ptr(traced["points"]),
+                                           _ptr(traced["counts"], C.c_int), _ptr(traced["reason_codes"], C.c_int)))
+
+
+def save_grid_csv(path, origin, spacing, values, valid=None):
+    """saveGridCsv (grid.h:35-37): values shaped (ny, nx), row-major y-rows."""
+    v = _f64(values)
+    ny, nx = v.shape
+    ok = None if valid is None else np.ascontiguousarray(valid, dtype=np.uint8)
+    _check(lib().bvc_grid_save_csv(str(path).encode(), C.c_double(origin[0]), C.c_double(origin[1]),
+                                   C.c_double(spacing), nx, ny, _ptr(v),
+                                   None if ok is None else _ptr(ok, C.c_uint8)))
+
+
+def load_grid_csv(path):
+    """loadGridCsv (grid.cpp:36-80): returns (origin, spacing, values (ny, nx), valid (ny, nx))."""
+    ox, oy, h, nx, ny = C.c_double(), C.c_double(), C.c_double(), C.c_int(), C.c_int()
+    b = str(path).encode()
+    _check(lib().bvc_grid_load_csv(b, C.byref(ox), C.byref(oy), C.byref(h), C.byref(nx), C.byref(ny), None, None,
+                                   C.c_size_t(0)))
+    v = np.zeros((ny.value, nx.value))
+    ok = np.zeros((ny.value, nx.value), np.uint8)
+    _check(lib().bvc_grid_load_csv(b, None, None, None, C.byref(nx), C.byref(ny), _ptr(v), _ptr(ok, C.c_uint8),
+                                   C.c_size_t(v.size)))
+    return (ox.value, oy.value), h.value, v, ok.astype(bool)
+
+
+def grid_rmse(a, b, valid_a=None, valid_b=None) -> float:
+    """rmse over jointly valid nodes (grid.cpp:82-96)."""
+    a, b = _f64(a).ravel(), _f64(b).ravel()
+    if a.shape != b.shape:
+        raise ParseError(abi.BVC_ERR_PARSE, "rmse: grid layouts do not match")
+    va = None if valid_a is None else np.ascontiguousarray(valid_a, dtype=np.uint8).ravel()
+    vb = None if valid_b is None else np.ascontiguousarray(valid_b, dtype=np.uint8).ravel()
+    out = C.c_double()
+    _check(lib().bvc_grid_rmse(_ptr(a), None if va is None else _ptr(va, C.c_uint8), _ptr(b),
+                               None if vb is None else _ptr(vb, C.c_uint8), C.c_size_t(a.size), C.byref(out)))
+    return out.value
+
+
+def save_grid_pgm(path, values, valid=None, auto_range=True, lo=0.0, hi=1.0):
+    """saveGridImage (tools/src/image.cpp:12-51): binary PGM plus a `.txt` legend."""
+    v = _f64(values)
+    ny, nx = v.shape
+    ok = None if valid is None else np.ascontiguousarray(valid, dtype=np.uint8)
+    _check(lib().bvc_grid_save_pgm(str(path).encode(), nx, ny, _ptr(v), None if ok is None else _ptr(ok, C.c_uint8),
+                                   int(auto_range), C.c_double(lo), C.c_double(hi)))
