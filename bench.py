@@ -54,8 +54,13 @@ class ClockSampler:
 
     def __init__(self, device=0):
         self.device = device
-        self.samples = []
+        self.samples = []  # (time, fields)
         self.proc = None
+        self.t_start = self.t_end = None
+
+    def mark(self, which):
+        """bracket the timed region; samples are taken from the whole run, kept inside it"""
+        setattr(self, "t_" + which, time.time())
 
     def __enter__(self):
         try:
@@ -70,9 +75,12 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.samples.append([x.strip() for x in line.split(",")])
+            self.samples.append((time.time(), [x.strip() for x in line.split(",")]))
 
     def __exit__(self, *a):
+        t0 = time.time()
+        while self.proc and time.time() - t0 < 3.0 and not any(t >= (self.t_end or 0) for t, _ in self.samples):
+            time.sleep(0.05)  # a short region: wait for the first sample after it
         if self.proc:
             self.proc.terminate()
             try:
@@ -81,15 +89,21 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.samples:
+        inside = [f for t, f in self.samples if self.t_start is not None and self.t_start <= t <= (self.t_end or t)]
+        where = "inside the timed region"
+        if not inside and self.samples and self.t_end is not None:  # region shorter than the 100 ms period
+            inside = [min(self.samples, key=lambda tf: abs(tf[0] - self.t_end))[1]]
+            where = "nearest sample to the end of the timed region (region < 100 ms)"
+        if not inside:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        samples = inside
+        sm = [float(s[0]) for s in samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 4 + i and "Active" in s[4 + i]
+        reasons = sorted({names[i] for s in samples for i in range(4) if len(s) > 4 + i and "Active" in s[4 + i]
                           and "Not" not in s[4 + i]})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(samples), "sampled": where}
 
 
 def build_problem(cfg_id, B, configs, abi):
@@ -177,6 +191,7 @@ def run_gpu(args):
         if dist is not None:
             dist.barrier()
 
+    clk = ClockSampler(local).__enter__()  # running before the timed region; samples kept inside it
     for w in range(args.warmup):
         step(pts, 1000 + w)
     torch.cuda.synchronize()
@@ -184,20 +199,22 @@ def run_gpu(args):
     torch.cuda.synchronize()
     launches0 = B.launch_count()
     times, steps_total, walks_total = [], 0, 0
-    with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            flush.fill_(float(k))
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            st = step(pts, k)
-            e1.record()
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1) / 1e3)
-            steps_total += st.get("cacheSteps", 0)
-            walks_total += st.get("cacheWalks", 0)
+    clk.mark("start")
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = step(pts, k)
+        e1.record()
         torch.cuda.synchronize()
-        barrier()
-        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+        steps_total += st.get("cacheSteps", 0)
+        walks_total += st.get("cacheWalks", 0)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clk.mark("end")
+    clk.__exit__(None, None, None)
     launches = B.launch_count() - launches0
     t_step = float(np.mean(times))
     if dist is not None:
@@ -283,7 +300,8 @@ def phase_breakdown(B, c, scene, region, pts, args):
     # walk traffic: algorithmic bytes per step from a counting launch
     prof = B.walk_traffic_profile(scene, c.problem, region, cfg, c.seed, 77)
     steps = max(prof["steps"], 1.0)
-    bytes_per_step = (prof["node_fetches"] * 48 + prof["prim_fetches"] * 32) / steps + 32.0
+    node_b, prim_b = (80, 48) if c.dim == 3 else (48, 32)  # Node3 / Prim3 vs Node2 / Prim2
+    bytes_per_step = (prof["node_fetches"] * node_b + prof["prim_fetches"] * prim_b) / steps + 32.0
     walk_bytes = bytes_per_step * stats["cacheSteps"]
     achieved = walk_bytes / t_gen / 1e9
     # gather bound: 148 SMs * f_SM / max(F/128, S/16) pairs/s (SURVEY §8d, V2 = 18 F, 2 S)
@@ -299,7 +317,31 @@ def phase_breakdown(B, c, scene, region, pts, args):
     bound = sms * f_sm / max(F / 128.0, S / 16.0)
     gather_rate = pairs / t_gather
     dominant = "walk" if t_gen >= t_gather else "gather"
+    # measured pipe rates and L2 bandwidth (bvc_pipe_probe) next to the canonical bound
+    pipes = B.pipe_probe()
+    mufu = min(pipes["mufu_lg2"], pipes["mufu_rcp"]) if c.dim == 2 else pipes["mufu_rsq"]
+    bound_meas = min(pipes["ffma"] / F, mufu / S)
+    extra = {}
+    if args.config == 1:  # BASELINE C1 also asks for fp64: the FP64 gather on the same cache
+        spec64 = B.make_splat_config(scene, c.problem, cfg)
+        spec64.fp64 = 1
+        B.splat_range(cache, scache, pts, spec64, 0, 1 << 62, True, bool(c.gradients))
+        torch.cuda.synchronize()
+        ev[2].record()
+        for _ in range(reps):
+            B.splat_range(cache, scache, pts, spec64, 0, 1 << 62, True, bool(c.gradients))
+        ev[3].record()
+        torch.cuda.synchronize()
+        t64 = ev[2].elapsed_time(ev[3]) / 1e3 / reps
+        extra["gather_fp64"] = {"ms": t64 * 1e3, "pairs_per_s": pairs / t64, "dfma_per_s": pipes["dfma"],
+                                "note": "every pair in FP64 (rcp/rsqrt: FP32 seed + 2 Newton steps, libdevice log); "
+                                        "parity with the reference's double loop <= 1e-12 (tests)"}
     return {
+        **extra,
+        "pipe_peaks": {k: v for k, v in pipes.items()},
+        "walk_stats": {"steps_per_walk": stats["cacheSteps"] / max(stats["cacheWalks"], 1),
+                       "truncated_fraction": stats["cacheTruncated"] / max(stats["cacheWalks"], 1),
+                       "walks": stats["cacheWalks"]},
         "phases_s": {"cache_generation": t_gen, "gather": t_gather},
         "roofline": {"bound": "hbm", "kernel": "bvc walk_kernel (cache generation)", "achieved": achieved,
                      "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s",
@@ -314,10 +356,13 @@ def phase_breakdown(B, c, scene, region, pts, args):
                      "algorithmic_bytes_per_step": bytes_per_step,
                      "node_fetches_per_step": prof["node_fetches"] / steps,
                      "prim_fetches_per_step": prof["prim_fetches"] / steps, "peak_source": peaks["source"],
+                     "l2_read_peak_gbs": pipes["l2_read_bytes"] / 1e9,
+                     "frac_of_l2_read_peak": achieved / (pipes["l2_read_bytes"] / 1e9),
                      "dominant": dominant},
         "gather_roofline": {"bound": "fp32+sfu", "kernel": f"bvc gather_kernel ({key})", "achieved": gather_rate,
                             "peak": bound, "unit": "pairs/s", "frac": gather_rate / bound,
                             "peak_formula": f"{sms} SMs x {f_sm / 1e6:.0f} MHz / max({F}/128, {S}/16)",
+                            "peak_measured_pipes": bound_meas, "frac_measured_pipes": gather_rate / bound_meas,
                             "pairs_per_launch": pairs},
     }
 

@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define BVC_ABI_VERSION 2
+#define BVC_ABI_VERSION 3
 
 /* ---- status codes (exception classes of the reference) ------------------- */
 typedef enum {
@@ -146,6 +146,7 @@ typedef struct {
     double coincidenceTol;  /* 1e-12 x diagonal */
     int voronoi;
     int useBallGreens;      /* G -> G^B(x, ballRadius) in the d-hat and source terms */
+    int fp64;               /* GPU extra: evaluate every pair in FP64 (Poisson kernels; BASELINE C1 fp64) */
 } bvc_splat_config;
 
 /* CachedBoundarySample (cache.h:43-52), host AoS exchange format (2D or 3D) */
@@ -196,6 +197,10 @@ int bvc_set_stream(void* cuda_stream);       /* stream for all subsequent launch
 int bvc_synchronize(void);
 /* launches of this library's kernels since process start (bench gpu_launches) */
 long long bvc_kernel_launch_count(void);
+/* pipe / cache microbenchmarks behind the rooflines: which = 0 FFMA,
+   1 MUFU.LG2, 2 MUFU.RCP, 3 DFMA, 4 MUFU.RSQ, 5 MUFU.EX2 (instructions/s, per GPU),
+   6 L2-resident read bandwidth (bytes/s) */
+int bvc_pipe_probe(int which, double* opsPerSecond);
 
 /* ---- scene (Scene::build scene.h:84, scene.cpp:11-125) --------------------- */
 /* 2D: vertices = 2*nv doubles, segments = 2*ns vertex ids, labels = ns bvc_label */

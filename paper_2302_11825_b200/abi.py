@@ -86,7 +86,7 @@ class VectorEstimate(C.Structure):
 
 class SplatConfig(C.Structure):
     _fields_ = [("kernel", KernelSpec), ("coincidenceTol", C.c_double), ("voronoi", C.c_int),
-                ("useBallGreens", C.c_int)]
+                ("useBallGreens", C.c_int), ("fp64", C.c_int)]
 
 
 class BoundarySample(C.Structure):

@@ -33,7 +33,7 @@ SYMBOLS = (
     "bvc_update_solution bvc_wos_solve bvc_wost_solve bvc_wost_gradient bvc_wost_normal_derivative "
     "bvc_walk_traffic_profile bvc_eval_kernels bvc_eval_bessel bvc_corrected_boundary_splat "
     "bvc_corrected_source_splat bvc_trace_streamlines bvc_grid_save_csv bvc_grid_load_csv bvc_grid_rmse "
-    "bvc_grid_save_pgm bvc_streamlines_write_csv"
+    "bvc_grid_save_pgm bvc_streamlines_write_csv bvc_pipe_probe"
 ).split()
 
 
@@ -495,9 +495,9 @@ def make_splat_config(scene: Scene, pb, cfg) -> abi.SplatConfig:
     return out
 
 
-def splat_config(kernel, diagonal, voronoi=False) -> abi.SplatConfig:
+def splat_config(kernel, diagonal, voronoi=False, fp64=False) -> abi.SplatConfig:
     k = abi.KernelSpec(kernel.kind, kernel.sigma, kernel.dim, diagonal)
-    return abi.SplatConfig(k, 1e-12 * diagonal, int(voronoi), 0)
+    return abi.SplatConfig(k, 1e-12 * diagonal, int(voronoi), 0, int(fp64))
 
 
 def splat_solution(bcache, scache, pts: EvaluationPoints, cfg):
@@ -713,3 +713,16 @@ def save_grid_pgm(path, values, valid=None, auto_range=True, lo=0.0, hi=1.0):
     ok = None if valid is None else np.ascontiguousarray(valid, dtype=np.uint8)
     _check(lib().bvc_grid_save_pgm(str(path).encode(), nx, ny, _ptr(v), None if ok is None else _ptr(ok, C.c_uint8),
                                    int(auto_range), C.c_double(lo), C.c_double(hi)))
+
+
+PROBES = ("ffma", "mufu_lg2", "mufu_rcp", "dfma", "mufu_rsq", "mufu_ex2", "l2_read_bytes")
+
+
+def pipe_probe() -> dict:
+    """Measured FP32/MUFU/FP64 issue rates (instructions/s) and L2 read bandwidth (B/s)."""
+    out = {}
+    for i, name in enumerate(PROBES):
+        v = C.c_double()
+        _check(lib().bvc_pipe_probe(i, C.byref(v)))
+        out[name] = v.value
+    return out

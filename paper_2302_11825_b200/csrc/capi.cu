@@ -125,7 +125,7 @@ enum Slot {
     kWsSortKeysIn, kWsSortKeysOut, kWsSortValsIn, kWsSortTemp, kWsMean, kWsSe, kWsTruncPt, kWsHost1, kWsRegion,
     kWsMean2, kWsSe2, kWsGidU, kWsSrcTmp, kWsSrcFlag, kWsEvalIn, kWsEvalOut, kWsTileBox, kWsUnitCtr,
     kWsCorrCounts, kWsCorrOffsets, kWsCorrStarts, kWsCorrGid, kWsCorrW, kWsCorrOut, kWsCorrMean, kWsCorrScan,
-    kWsCorrFlag, kWsBallRs, kWsHull
+    kWsCorrFlag, kWsBallRs, kWsHull, kWsXs64
 };
 
 int fail(const std::exception& e) {
@@ -993,6 +993,26 @@ void splat_launch(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_point
     if (begin >= end) return;
     int K = static_cast<int>(end - begin);
     int kind = gather_kind(cfg.kernel);
+    if (cfg.fp64) {  // FP64 variant (gather64.cu)
+        double4* pack64 = ws().get<double4>(kWsPack, 2 * static_cast<size_t>(std::max(N + M, 1)));
+        if (N) pack64_boundary(b->samples.p, N, kind, cfg.voronoi, pack64, g_stream);
+        if (M) pack64_source(s->samples.p, M, kind, pack64 + 2 * static_cast<size_t>(N), g_stream);
+        GatherPlan plan = plan_gather64(kind, K, N, M, val, grad);
+        double* part = ws().get<double>(kWsPart, std::max<size_t>(static_cast<size_t>(plan.chunksB + plan.chunksS) * plan.comps * K, 1));
+        int* skipB = ws().get<int>(kWsSkipB, K);
+        int* skipS = ws().get<int>(kWsSkipS, K);
+        CK(cudaMemsetAsync(skipB, 0, K * sizeof(int), g_stream));
+        CK(cudaMemsetAsync(skipS, 0, K * sizeof(int), g_stream));
+        double* px64 = ws().get<double>(kWsXs64, static_cast<size_t>(dim) * K);
+        gather_points64(P->x.p, P->order.p + begin, K, dim, px64, g_stream);
+        if (N + M > 0) {
+            launch_gather64(kind, plan, pack64, N, M, px64, K, dim, cfg.coincidenceTol, val, grad, part, skipB, skipS,
+                            ws().get<unsigned>(kWsUnitCtr, 1), g_stream);
+            launch_finalize(part, plan, K, P->order.p + begin, N, M, val, grad, dim, skipB, skipS, P->dev(), g_stream);
+        }
+        CK(cudaGetLastError());
+        return;
+    }
     float4* pack = ws().get<float4>(kWsPack, 2 * static_cast<size_t>(std::max(N + M, 1)));
     if (N) pack_boundary(b->samples.p, N, kind, cfg.voronoi, pack, g_stream);
     if (M) pack_source(s->samples.p, M, kind, pack + 2 * static_cast<size_t>(N), g_stream);
@@ -1043,6 +1063,8 @@ void splat(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_points_s* P,
         mode |= kModeBall;
     }
     if (mode && dim != 2) throw Error(BVC_ERR_INVALID_ARGUMENT, "clamped / ball-kernel splats are 2D (cache.cpp:499-597)");
+    if (cfg.fp64 && (cfg.kernel.kind != BVC_KERNEL_POISSON || mode))
+        throw Error(BVC_ERR_INVALID_ARGUMENT, "fp64 splats: plain Poisson kernels only");
     ensure_order(P);
     if (mode & kModeBall) require_ball(P);
     if (val && grad && mode) {  // the gradient splat never clamps (cache.cpp:463-497)

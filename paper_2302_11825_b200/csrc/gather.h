@@ -62,6 +62,14 @@ void launch_ball_corr(const bvc_dev::SceneView2& region, float insideTol, const 
                       uint32_t k1, double* ssum, cudaStream_t st);
 void launch_ball_radius(const double* x, int n, int dim, const double* hull, int nh, double* R, cudaStream_t st);
 void launch_gather_f32(const double* v, const int* order, int K, float* out, cudaStream_t st);
+// FP64 variant (gather64.cu): Poisson kernels, exact per-pair coincidence test
+void pack64_boundary(const CacheSample* cs, int n, int kind, int voronoi, double4* out, cudaStream_t st);
+void pack64_source(const SourceSampleDev* ss, int m, int kind, double4* out, cudaStream_t st);
+void gather_points64(const double* x, const int* order, int K, int dim, double* out, cudaStream_t st);
+GatherPlan plan_gather64(int kind, int K, int N, int M, bool val, bool grad);
+void launch_gather64(int kind, const GatherPlan& g, const double4* pack, int N, int M, const double* px, int K,
+                     int dim, double tol, bool val, bool grad, double* part, int* skipB, int* skipS,
+                     unsigned* unitCounter, cudaStream_t st);
 void launch_finalize(const double* part, const GatherPlan& g, int K, const int* order, int N, int M, bool val,
                      bool grad, int dim, const int* skipB, const int* skipS, const PointsDev& pts, cudaStream_t st);
 

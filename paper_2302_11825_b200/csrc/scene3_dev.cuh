@@ -34,8 +34,11 @@ struct SceneView3 {
     unsigned long long* counts;  // diagnostic traversal counters (as SceneView2)
 };
 
+template <bool COUNT = false>
 __device__ __forceinline__ void count_fetch3(const SceneView3& S, int which) {
-    if (S.counts) S.counts[2 * (blockIdx.x * blockDim.x + threadIdx.x) + which] += 1;
+    if constexpr (COUNT) {
+        if (S.counts) S.counts[2 * (blockIdx.x * blockDim.x + threadIdx.x) + which] += 1;
+    }
 }
 
 __device__ __forceinline__ float box3_dist2(const float4& lo, const float4& hi, float x, float y, float z) {
@@ -62,7 +65,7 @@ __device__ __forceinline__ float tri_closest(const Prim3& t, float px, float py,
         else {
             float vc = d1 * d4 - d3 * d2;
             if (vc <= 0.0f && d1 >= 0.0f && d3 <= 0.0f) {
-                v = d1 / (d1 - d3);
+                v = __fdividef(d1, d1 - d3);
                 qx = ax + v * abx; qy = ay + v * aby; qz = az + v * abz;
             } else {
                 float cpx = px - t.c.x, cpy = py - t.c.y, cpz = pz - t.c.z;
@@ -71,15 +74,15 @@ __device__ __forceinline__ float tri_closest(const Prim3& t, float px, float py,
                 else {
                     float vb = d5 * d2 - d1 * d6;
                     if (vb <= 0.0f && d2 >= 0.0f && d6 <= 0.0f) {
-                        w = d2 / (d2 - d6);
+                        w = __fdividef(d2, d2 - d6);
                         qx = ax + w * acx; qy = ay + w * acy; qz = az + w * acz;
                     } else {
                         float va = d3 * d6 - d5 * d4;
                         if (va <= 0.0f && (d4 - d3) >= 0.0f && (d5 - d6) >= 0.0f) {
-                            w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+                            w = __fdividef(d4 - d3, (d4 - d3) + (d5 - d6));
                             qx = t.b.x + w * (t.c.x - t.b.x); qy = t.b.y + w * (t.c.y - t.b.y); qz = t.b.z + w * (t.c.z - t.b.z);
                         } else {
-                            float denom = 1.0f / (va + vb + vc);
+                            float denom = __frcp_rn(va + vb + vc);
                             v = vb * denom;
                             w = vc * denom;
                             qx = ax + abx * v + acx * w; qy = ay + aby * v + acy * w; qz = az + abz * v + acz * w;
@@ -93,7 +96,7 @@ __device__ __forceinline__ float tri_closest(const Prim3& t, float px, float py,
     return dx * dx + dy * dy + dz * dz;
 }
 
-template <class Visit, class Thr>
+template <bool COUNT = false, class Visit, class Thr>
 __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, float y, float z, unsigned qmask,
                                                Visit&& visit, Thr&& threshold) {
     int stackRef[kStack];
@@ -102,7 +105,7 @@ __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, flo
     for (;;) {
         if (ref >= 0) {
             const Node3 nd = S.nodes[ref];
-            count_fetch3(S, 0);
+            count_fetch3<COUNT>(S, 0);
             float thr = threshold();
             float dl = (nd.mask & qmask) ? box3_dist2(nd.llo, nd.lhi, x, y, z) : kFInf;
             float dr = ((nd.mask >> 3) & qmask) ? box3_dist2(nd.rlo, nd.rhi, x, y, z) : kFInf;
@@ -122,8 +125,8 @@ __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, flo
             int start = code >> 3, count = (code & 7) + 1;
             for (int i = start; i < start + count; ++i) {
                 const Prim3 p = S.prims[i];
-                count_fetch3(S, 1);
-                if ((1u << __float_as_int(p.b.w)) & qmask) visit(p);
+                count_fetch3<COUNT>(S, 1);
+                if ((1u << __float_as_int(p.b.w)) & qmask) visit(p, i);
             }
         }
         for (;;) {
@@ -138,17 +141,35 @@ __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, flo
 struct Closest3 {
     float d2, px, py, pz;
     int tri;
+    int prim;  // leaf-order index of the triangle (a warm-start hint for the next query)
 };
 
+// closest point on the primitive at leaf-order index `prim` (a traversal warm start)
+__device__ __forceinline__ Closest3 closest_on3(const SceneView3& S, int prim, float x, float y, float z) {
+    const Prim3 p = S.prims[prim];
+    Closest3 c;
+    c.d2 = tri_closest(p, x, y, z, c.px, c.py, c.pz);
+    c.tri = __float_as_int(p.a.w);
+    c.prim = prim;
+    return c;
+}
+
+// hint >= 0: leaf-order index of a primitive of the queried classes whose distance
+// seeds the pruning radius (the walker's previous closest triangle)
+template <bool COUNT = false>
 __device__ __forceinline__ Closest3 closest_point3(const SceneView3& S, float x, float y, float z, unsigned qmask,
-                                                   float maxD2 = kFInf) {
-    Closest3 c{maxD2, 0.f, 0.f, 0.f, -1};
-    traverse_near3(
+                                                   float maxD2 = kFInf, int hint = -1) {
+    Closest3 c{maxD2, 0.f, 0.f, 0.f, -1, -1};
+    if (hint >= 0) {
+        Closest3 h = closest_on3(S, hint, x, y, z);
+        if (h.d2 < c.d2) c = h;
+    }
+    traverse_near3<COUNT>(
         S, x, y, z, qmask,
-        [&](const Prim3& p) {
+        [&](const Prim3& p, int i) {
             float qx, qy, qz;
             float d2 = tri_closest(p, x, y, z, qx, qy, qz);
-            if (d2 < c.d2) c = Closest3{d2, qx, qy, qz, __float_as_int(p.a.w)};
+            if (d2 < c.d2) c = Closest3{d2, qx, qy, qz, __float_as_int(p.a.w), i};
         },
         [&]() { return c.d2; });
     return c;

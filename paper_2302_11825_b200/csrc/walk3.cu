@@ -50,16 +50,17 @@ struct Star3 {
     float s2;
 };
 
-__device__ __forceinline__ Star3 star_query3(const WalkEnv3& E, float x, float y, float z) {
-    Star3 q{Closest3{kFInf, 0.f, 0.f, 0.f, -1}, kFInf};
+template <bool COUNT>
+__device__ __forceinline__ Star3 star_query3(const WalkEnv3& E, float x, float y, float z, int hint) {
+    Star3 q{hint >= 0 ? closest_on3(E.S, hint, x, y, z) : Closest3{kFInf, 0.f, 0.f, 0.f, -1, -1}, kFInf};
     float eps2 = E.eps * E.eps;
-    traverse_near3(
+    traverse_near3<COUNT>(
         E.S, x, y, z, kClsD | kClsSil,
-        [&](const Prim3& p) {
+        [&](const Prim3& p, int i) {
             if (__float_as_int(p.b.w) == 0) {
                 float qx, qy, qz;
                 float d2 = tri_closest(p, x, y, z, qx, qy, qz);
-                if (d2 < q.D.d2) q.D = Closest3{d2, qx, qy, qz, __float_as_int(p.a.w)};
+                if (d2 < q.D.d2) q.D = Closest3{d2, qx, qy, qz, __float_as_int(p.a.w), i};
             } else {
                 int4 sl = E.triSil[__float_as_int(p.a.w)];
                 float d2;
@@ -77,6 +78,7 @@ struct Hit3 {
     int tri;
 };
 
+template <bool COUNT>
 __device__ __forceinline__ Hit3 ray_neumann3(const WalkEnv3& E, float ox, float oy, float oz, float dx, float dy,
                                              float dz, float tMax, int skip) {
     Hit3 h{kFInf, -1};
@@ -87,7 +89,7 @@ __device__ __forceinline__ Hit3 ray_neumann3(const WalkEnv3& E, float ox, float 
     for (;;) {
         if (ref >= 0) {
             const Node3 nd = E.S.nodes[ref];
-            count_fetch3(E.S, 0);
+            count_fetch3<COUNT>(E.S, 0);
             bool vl = (nd.mask & kClsNeumann) && ray_box3(nd.llo, nd.lhi, ox, oy, oz, idx, idy, idz, limit);
             bool vr = ((nd.mask >> 3) & kClsNeumann) && ray_box3(nd.rlo, nd.rhi, ox, oy, oz, idx, idy, idz, limit);
             if (vl && vr) { stack[sp++] = nd.right; ref = nd.left; continue; }
@@ -98,7 +100,7 @@ __device__ __forceinline__ Hit3 ray_neumann3(const WalkEnv3& E, float ox, float 
             int start = code >> 3, count = (code & 7) + 1;
             for (int i = start; i < start + count; ++i) {
                 const Prim3 p = E.S.prims[i];
-                count_fetch3(E.S, 1);
+                count_fetch3<COUNT>(E.S, 1);
                 int cls = __float_as_int(p.b.w), id = __float_as_int(p.a.w);
                 if (!((1u << cls) & kClsNeumann) || id == skip) continue;
                 float th;
@@ -152,37 +154,41 @@ struct Walk3 {
     float x, y, z, weight;
     float inx, iny, inz;
     int onN, prevTri, step;
+    int lastD;  // leaf-order index of the previous closest Dirichlet triangle (warm start)
 };
 
 __device__ __forceinline__ void walk3_start(Walk3& w, float x, float y, float z) {
     w.x = x; w.y = y; w.z = z; w.weight = 1.f; w.inx = w.iny = w.inz = 0.f; w.onN = 0; w.prevTri = -1; w.step = 0;
+    w.lastD = -1;
 }
 
+template <bool NEU, bool SCR, bool COUNT>
 __device__ __forceinline__ bool walk3_step(const WalkEnv3& E, Walk3& w, U4 rnd, float& value, int& trunc,
                                            unsigned long long& steps) {
     ++steps;
     Closest3 cp;
     float R;
-    if (E.hasNeumann) {
-        Star3 q = star_query3(E, w.x, w.y, w.z);
+    if constexpr (NEU) {
+        Star3 q = star_query3<COUNT>(E, w.x, w.y, w.z, w.lastD);
         cp = q.D;
         float dD = sqrtf(cp.d2);
         if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
         R = fminf(dD, sqrtf(q.s2));
     } else {
-        cp = closest_point3(E.S, w.x, w.y, w.z, kClsD);
+        cp = closest_point3<COUNT>(E.S, w.x, w.y, w.z, kClsD, kFInf, w.lastD);
         float dD = sqrtf(cp.d2);
         if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
         R = dD;
     }
+    w.lastD = cp.prim;
     R = fmaxf(R, E.rmin);
     float dx, dy, dz;
     if (w.onN) hemi_dir(u01(rnd.x), u01(rnd.y), w.inx, w.iny, w.inz, dx, dy, dz);
     else sphere_dir(u01(rnd.x), u01(rnd.y), dx, dy, dz);
     float travel = R;
     bool hit = false;
-    if (E.hasNeumann) {
-        Hit3 h = ray_neumann3(E, w.x, w.y, w.z, dx, dy, dz, R, w.onN ? w.prevTri : -1);
+    if constexpr (NEU) {
+        Hit3 h = ray_neumann3<COUNT>(E, w.x, w.y, w.z, dx, dy, dz, R, w.onN ? w.prevTri : -1);
         if (h.tri >= 0) {
             hit = true;
             travel = h.t;
@@ -203,7 +209,7 @@ __device__ __forceinline__ bool walk3_step(const WalkEnv3& E, Walk3& w, U4 rnd, 
         w.onN = 0;
         w.prevTri = -1;
     }
-    if (E.P.screened) w.weight *= sphere_weight3(E.P.sqrtSigma, R, travel);
+    if constexpr (SCR) w.weight *= sphere_weight3(E.P.sqrtSigma, R, travel);
     bool escaped = fabsf(w.x - E.cx) > E.escape || fabsf(w.y - E.cy) > E.escape || fabsf(w.z - E.cz) > E.escape;
     if (++w.step >= E.maxSteps || escaped) {
         trunc = 1;
@@ -243,6 +249,7 @@ __device__ __forceinline__ U4 draw3(const WalkEnv3& E, Task3& t) {
     return philox4x32_10(c, E.k0, E.k1);
 }
 
+template <bool NEU, bool SCR, bool COUNT>
 __global__ void __launch_bounds__(kThreads3) walk3_kernel(const WalkEnv3 E, const WalkJob3 J) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -274,7 +281,8 @@ __global__ void __launch_bounds__(kThreads3) walk3_kernel(const WalkEnv3 E, cons
                 t.trunc = 0;
                 if (id < nUtot) {
                     t.role = 0;
-                    t.pt = static_cast<int>(id / J.nU);
+                    t.pt = id < 0x7fffffffLL ? static_cast<int>(static_cast<unsigned>(id) / static_cast<unsigned>(J.nU))
+                                             : static_cast<int>(id / J.nU);
                     int k = static_cast<int>(id - static_cast<long long>(t.pt) * J.nU);
                     long long g = J.gidU ? J.gidU[t.pt] : J.gidBaseU + t.pt;
                     t.rid = static_cast<unsigned long long>(g) * J.nU + k;
@@ -283,7 +291,8 @@ __global__ void __launch_bounds__(kThreads3) walk3_kernel(const WalkEnv3 E, cons
                 } else {
                     long long d = id - nUtot;
                     t.role = 1;
-                    t.pt = static_cast<int>(d / J.nD);
+                    t.pt = d < 0x7fffffffLL ? static_cast<int>(static_cast<unsigned>(d) / static_cast<unsigned>(J.nD))
+                                            : static_cast<int>(d / J.nD);
                     int k = static_cast<int>(d - static_cast<long long>(t.pt) * J.nD);
                     long long g = J.gidD ? J.gidD[t.pt] : t.pt;
                     t.rid = static_cast<unsigned long long>(g) * J.nD + k;
@@ -293,7 +302,7 @@ __global__ void __launch_bounds__(kThreads3) walk3_kernel(const WalkEnv3 E, cons
                     U4 r1 = draw3(E, t);
                     sphere_dir(u01(r0.x), u01(r0.y), t.dx, t.dy, t.dz);
                     t.vx = t.vy = t.vz = 0.f;
-                    if (E.P.screened && E.P.sigma > 0.f) {
+                    if (SCR && E.P.sigma > 0.f) {
                         // y ~ |G^B| in the Poisson ball, grad G^B (kernels.cpp:68-75, 3D) sigma / pdf
                         float tt = invert_ball_cdf3(u01(r0.z));
                         float r = fmaxf(tt * t.R, 1e-6f * t.R);
@@ -317,7 +326,7 @@ __global__ void __launch_bounds__(kThreads3) walk3_kernel(const WalkEnv3 E, cons
         if (active) {
             U4 rnd = draw3(E, t);
             float value;
-            if (walk3_step(E, w, rnd, value, t.trunc, steps)) {
+            if (walk3_step<NEU, SCR, COUNT>(E, w, rnd, value, t.trunc, steps)) {
                 if (t.role == 0) {
                     J.outU[t.id] = value;
                     if (t.trunc && J.truncU) atomicAdd(J.truncU + t.pt, 1);
@@ -328,7 +337,7 @@ __global__ void __launch_bounds__(kThreads3) walk3_kernel(const WalkEnv3 E, cons
                     t.vx = fmaf(s, t.dx, t.vx);
                     t.vy = fmaf(s, t.dy, t.vy);
                     t.vz = fmaf(s, t.dz, t.vz);
-                    if (E.P.screened && E.P.sigma > 0.f) {
+                    if (SCR && E.P.sigma > 0.f) {
                         t.phase = 1;
                         walk3_start(w, t.y2x, t.y2y, t.y2z);
                     } else {
@@ -473,18 +482,33 @@ inline int blocks(long long n, int t) { return static_cast<int>((n + t - 1) / t)
 
 }  // namespace
 
+template <bool NEU, bool SCR, bool COUNT>
+void launch_walk3_t(const WalkEnv3& env, const WalkJob3& job, long long total, cudaStream_t st) {
+    int dev = 0, sms = 148, perSm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, walk3_kernel<NEU, SCR, COUNT>, kThreads3, 0);
+    perSm = perSm > 0 ? perSm : 1;
+    long long want = (total + kThreads3 - 1) / kThreads3;
+    int grid = static_cast<int>(want < static_cast<long long>(sms) * perSm ? want : static_cast<long long>(sms) * perSm);
+    walk3_kernel<NEU, SCR, COUNT><<<grid, kThreads3, 0, st>>>(env, job);
+}
+
 void launch_walk_job3(const WalkEnv3& env, const WalkJob3& job, cudaStream_t st) {
     long long total = static_cast<long long>(job.nPtsU) * job.nU + static_cast<long long>(job.nPtsD) * job.nD;
     if (total <= 0) return;
     cudaMemsetAsync(job.counter, 0, sizeof(unsigned long long), st);
-    int dev = 0, sms = 148, perSm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, walk3_kernel, kThreads3, 0);
-    perSm = perSm > 0 ? perSm : 1;
-    long long want = (total + kThreads3 - 1) / kThreads3;
-    int grid = static_cast<int>(want < static_cast<long long>(sms) * perSm ? want : static_cast<long long>(sms) * perSm);
-    walk3_kernel<<<grid, kThreads3, 0, st>>>(env, job);
+    const int code = (env.hasNeumann ? 1 : 0) | (env.P.screened ? 2 : 0) | (env.S.counts ? 4 : 0);
+    switch (code) {
+        case 0: launch_walk3_t<false, false, false>(env, job, total, st); break;
+        case 1: launch_walk3_t<true, false, false>(env, job, total, st); break;
+        case 2: launch_walk3_t<false, true, false>(env, job, total, st); break;
+        case 3: launch_walk3_t<true, true, false>(env, job, total, st); break;
+        case 4: launch_walk3_t<false, false, true>(env, job, total, st); break;
+        case 5: launch_walk3_t<true, false, true>(env, job, total, st); break;
+        case 6: launch_walk3_t<false, true, true>(env, job, total, st); break;
+        default: launch_walk3_t<true, true, true>(env, job, total, st); break;
+    }
     count_launch();
 }
 

@@ -225,3 +225,65 @@ def test_voronoi_weights_gather():
     st, _ = _gpu_splat(spec, cache, None, x, gradient=False, voronoi=True)
     ref = O.oracle_splat(spec, 1e-12 * spec.scale, cache, None, x, voronoi=True)
     assert H.rel_err(st["boundarySum"], ref["boundarySum"]) <= TOL
+
+
+@pytest.mark.parametrize("name", ["square_ux", "disk_poisson"])
+def test_fp64_gather_matches_reference_to_rounding(golden, name):
+    """The FP64 variant (BASELINE C1 "u (fp32 and fp64)"): on the FP32-stored cache the
+    reference's own double loop and the GPU's FP64 loop agree to ~1e-13."""
+    g = golden("splat")
+    k, sg, dim, scale = g[name + "_spec"]
+    spec = H.kspec(int(k), sg, int(dim), scale)
+    cache = _fp32({key: g[f"{name}_b_{key}"] for key in ("z", "n", "pdf", "uHat", "dHat", "weight")})
+    scache = None
+    if f"{name}_s_y" in g.files:
+        scache = _fp32({key: g[f"{name}_s_{key}"] for key in ("y", "pdf", "f")})
+    x = np.asarray(g[name + "_x"], np.float64)
+    bc = B.BoundaryCache.from_arrays(cache["z"], cache["n"], cache["pdf"], cache["uHat"], cache["dHat"])
+    sc = B.SourceCache.from_arrays(scache["y"], scache["pdf"], scache["f"]) if scache is not None else None
+    pts = B.EvaluationPoints(x)
+    cfg = abi.SplatConfig(spec, 1e-12 * scale, 0, 0, 1)
+    B.splat_solution_gradient(bc, sc, pts, cfg)
+    st = pts.download()
+    ref = O.oracle_splat(spec, 1e-12 * scale, cache, scache, x, value=True, gradient=True)
+    for key in ("boundarySum", "sourceSum"):
+        assert H.rel_err(st[key], ref[key]) <= 1e-12, (key, H.rel_err(st[key], ref[key]))
+    for key in ("boundaryGradSum", "sourceGradSum"):
+        for c in range(2):
+            assert H.rel_err(st[key][:, c], ref[key][:, c]) <= 1e-12, (key, c)
+    assert np.array_equal(st["nBoundary"], ref["nBoundary"]) and np.array_equal(st["skipped"], ref["skipped"])
+    # the exact per-pair coincidence test: a point on a sample skips exactly that sample
+    on = B.EvaluationPoints(cache["z"][:3])
+    B.splat_solution(bc, sc, on, cfg)
+    so = on.download()
+    ro = O.oracle_splat(spec, 1e-12 * scale, cache, scache, cache["z"][:3])
+    assert np.array_equal(so["skipped"], ro["skipped"]) and np.all(so["skipped"] >= 1)
+    assert H.rel_err(so["boundarySum"], ro["boundarySum"]) <= 1e-12
+
+
+def test_fp64_gather_3d_and_c1_config():
+    rng = np.random.default_rng(5)
+    z = rng.normal(size=(3000, 3))
+    z /= np.linalg.norm(z, axis=1)[:, None]
+    cache = dict(z=z, n=z, pdf=np.full(3000, 1 / (4 * np.pi)), uHat=rng.uniform(-1, 1, 3000),
+                 dHat=rng.uniform(-1, 1, 3000), weight=np.zeros(3000))
+    cache = _fp32(cache)
+    x = rng.uniform(-0.5, 0.5, (700, 3))
+    spec = H.kspec(0, 0, 3, 2.0)
+    bc = B.BoundaryCache.from_arrays(cache["z"], cache["n"], cache["pdf"], cache["uHat"], cache["dHat"])
+    pts = B.EvaluationPoints(x, 3)
+    B.splat_solution_gradient(bc, None, pts, abi.SplatConfig(spec, 2e-12, 0, 0, 1))
+    st = pts.download()
+    ref = O.oracle_splat(spec, 2e-12, cache, None, x, value=True, gradient=True)
+    assert H.rel_err(st["boundarySum"], ref["boundarySum"]) <= 1e-12
+    for c in range(3):
+        assert H.rel_err(st["boundaryGradSum"][:, c], ref["boundaryGradSum"][:, c]) <= 1e-12
+    # C1's cache through both precisions: the FP32 gather sits within its 1e-4 bar of FP64
+    c, scene, region, cache1, _, x1 = _config_cache(configs.config1, 4000)
+    spec1 = H.kspec(0, 0, 2, scene.diagonal)
+    a, b = B.EvaluationPoints(x1), B.EvaluationPoints(x1)
+    B.splat_solution(cache1, None, a, abi.SplatConfig(spec1, 1e-12 * scene.diagonal, 0, 0, 0))
+    B.splat_solution(cache1, None, b, abi.SplatConfig(spec1, 1e-12 * scene.diagonal, 0, 0, 1))
+    assert H.rel_err(a.solution(), b.solution()) <= TOL
+    with pytest.raises(B.InvalidArgument):
+        B.splat_solution(cache1, None, a, abi.SplatConfig(H.kspec(1, 1.0, 2, 2.0), 1e-12, 0, 0, 1))
