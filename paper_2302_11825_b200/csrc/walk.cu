@@ -262,7 +262,7 @@ __device__ __forceinline__ U4 draw4(const WalkEnv& E, Task& t) {
 }
 
 template <bool NEU, bool SCR, bool SRC, bool COUNT>
-__global__ void __launch_bounds__(kWalkThreads) walk_kernel(const WalkEnv E, const WalkJob J) {
+__global__ void __launch_bounds__(kWalkThreads, NEU ? 4 : 6) walk_kernel(const WalkEnv E, const WalkJob J) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const long long nUtot = static_cast<long long>(J.nPtsU) * J.nU;

@@ -250,7 +250,7 @@ __device__ __forceinline__ U4 draw3(const WalkEnv3& E, Task3& t) {
 }
 
 template <bool NEU, bool SCR, bool COUNT>
-__global__ void __launch_bounds__(kThreads3) walk3_kernel(const WalkEnv3 E, const WalkJob3 J) {
+__global__ void __launch_bounds__(kThreads3, 6) walk3_kernel(const WalkEnv3 E, const WalkJob3 J) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const long long nUtot = static_cast<long long>(J.nPtsU) * J.nU;
