@@ -69,9 +69,15 @@ def test_bvh_queries_vs_reference(golden, k):
         p, dist, seg, _ = sc.closest_point(q, filt)
         ref = g[f"s{k}_cp{filt}_dist"]
         np.testing.assert_allclose(dist, ref, atol=tol, rtol=0)
-        same = seg == g[f"s{k}_cp{filt}_seg"]
-        # different segment ids only at (near-)ties, e.g. a shared closest vertex
-        assert np.mean(same) > 0.97
+        rseg = g[f"s{k}_cp{filt}_seg"]
+        # different segment ids only at (near-)ties, e.g. a shared closest vertex: the
+        # reference's segment is then equally close (ties break by traversal order)
+        v, sg = g[f"s{k}_v"], g[f"s{k}_s"]
+        diff = np.nonzero(seg != rseg)[0]
+        for i in diff:
+            a, b = v[sg[rseg[i], 0]], v[sg[rseg[i], 1]]
+            t = np.clip(np.dot(q[i] - a, b - a) / np.dot(b - a, b - a), 0.0, 1.0)
+            assert abs(np.linalg.norm(a + t * (b - a) - q[i]) - dist[i]) <= tol, (filt, i)
     sil = sc.silhouette_distance(q)
     ref = g[f"s{k}_sil"]
     fin = np.isfinite(ref)
