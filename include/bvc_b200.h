@@ -199,7 +199,8 @@ int bvc_synchronize(void);
 long long bvc_kernel_launch_count(void);
 /* pipe / cache microbenchmarks behind the rooflines: which = 0 FFMA,
    1 MUFU.LG2, 2 MUFU.RCP, 3 DFMA, 4 MUFU.RSQ, 5 MUFU.EX2 (instructions/s, per GPU),
-   6 L2-resident read bandwidth (bytes/s) */
+   6 L2-resident read bandwidth (bytes/s), 7 FFMA / 8 FMUL / 9 FADD with register
+   operands only (no immediate or constant-bank operand), 10 packed FFMA2 (FP32 FMAs/s) */
 int bvc_pipe_probe(int which, double* opsPerSecond);
 
 /* ---- scene (Scene::build scene.h:84, scene.cpp:11-125) --------------------- */

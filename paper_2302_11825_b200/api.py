@@ -715,7 +715,8 @@ def save_grid_pgm(path, values, valid=None, auto_range=True, lo=0.0, hi=1.0):
                                    int(auto_range), C.c_double(lo), C.c_double(hi)))
 
 
-PROBES = ("ffma", "mufu_lg2", "mufu_rcp", "dfma", "mufu_rsq", "mufu_ex2", "l2_read_bytes")
+PROBES = ("ffma", "mufu_lg2", "mufu_rcp", "dfma", "mufu_rsq", "mufu_ex2", "l2_read_bytes", "ffma_reg", "fmul_reg",
+          "fadd_reg", "ffma2_fp32_ops")
 
 
 def pipe_probe() -> dict:

@@ -73,54 +73,61 @@ struct ModeCtx {
     float sclamp; // c 4 pi / ln 2 (the source clamp in log2 units)
 };
 
+// Accumulator sign conventions, chosen so that no pair needs a negation (the tile
+// end restores the signs): 2D Laplace values are accumulated negated (-u), 3D
+// Laplace boundary gradients negated; everything else as is.
+template <int KIND, bool SRC>
+struct Conv {
+    static constexpr bool negV = KIND == kLap2;
+    static constexpr bool negG = KIND == kLap3 && !SRC;
+};
+
+// Scalar pair. Plain products and sums use the non-contracting __fmul_rn /
+// __fadd_rn, so this is bit-identical, lane by lane, to the packed pair2 below
+// (FMUL2 / FADD2 / FFMA2 round each lane exactly like FMUL / FADD / FFMA):
+// points take the packed or the scalar path (slow tiles, clamp modes) and get
+// the same bits either way.
 template <int KIND, bool SRC, bool VAL, bool GRAD, bool TRACK = false, int MODE = 0>
 __device__ __forceinline__ void pair(const float4 a, const float4 b, float px, float py, float pz, float sigma,
                                      float s, Acc& acc, float& mn, const ModeCtx* mc = nullptr) {
     if constexpr (KIND == kLap2 || KIND == kScr2) {
-        float dx = a.x - px, dy = a.y - py;
-        float r2 = fmaf(dx, dx, dy * dy);
+        float dx = __fsub_rn(a.x, px), dy = __fsub_rn(a.y, py);
+        float r2 = fmaf(dx, dx, __fmul_rn(dy, dy));
         if constexpr (TRACK) mn = fminf(mn, r2);
         if constexpr (KIND == kLap2) {
-            float ir2 = f_rcp(r2);
+            float nir2 = f_rcp(-r2);  // -1 / r^2
             if constexpr (!SRC) {
-                // a.zw = A n (A folded into the normal): ndA = A (n.d), A p = ndA / r^2
-                float ndA = fmaf(a.z, dx, a.w * dy);
+                // a.zw = A n, b = (A, B ln2/4pi-scaled, -Bg, 0): t = -A p, -u += B lg2 r^2 + t
+                float ndA = fmaf(a.z, dx, __fmul_rn(a.w, dy));
+                float t = __fmul_rn(ndA, nir2);
                 if constexpr (VAL) {
-                    if constexpr (MODE == 0) {
-                        acc.v = fmaf(ndA, ir2, fmaf(-b.y, f_lg2(r2), acc.v));
-                    } else {
+                    float l = (MODE & kBall) ? f_lg2(fminf(r2, mc->R2)) - mc->lgR2 : f_lg2(r2);
+                    float base = fmaf(b.y, l, acc.v);
+                    if constexpr ((MODE & kClampP) != 0) {
                         // clamp p = n.d / r^2 to +-2 pi c, i.e. A p to +-2 pi c |A|; an
-                        // unsaturated pair takes the plain path's exact operations
-                        float l = (MODE & kBall) ? f_lg2(fminf(r2, mc->R2)) - mc->lgR2 : f_lg2(r2);
-                        float base = fmaf(-b.y, l, acc.v);
-                        if constexpr ((MODE & kClampP) != 0) {
-                            float pA = ndA * ir2;
-                            float lim = mc->c2pi * fabsf(b.x);
-                            acc.v = fabsf(pA) > lim ? base + copysignf(lim, pA) : fmaf(ndA, ir2, base);
-                        } else {
-                            acc.v = fmaf(ndA, ir2, base);
-                        }
+                        // unsaturated pair gets exactly the plain path's bits
+                        float lim = mc->c2pi * fabsf(b.x);
+                        acc.v = fabsf(t) > lim ? __fadd_rn(base, copysignf(lim, t)) : fmaf(ndA, nir2, base);
+                    } else {
+                        acc.v = fmaf(ndA, nir2, base);
                     }
                 }
                 if constexpr (GRAD) {
-                    float q = fmaf(2.0f * ndA, ir2, b.z) * ir2;  // (2A p + Bg) / r^2
-                    acc.gx = fmaf(q, dx, fmaf(-ir2, a.z, acc.gx));  // - (A / r^2) n
-                    acc.gy = fmaf(q, dy, fmaf(-ir2, a.w, acc.gy));
+                    float q = __fmul_rn(fmaf(t, 2.0f, b.z), nir2);     // (2 A p + Bg) / r^2
+                    acc.gx = fmaf(q, dx, fmaf(nir2, a.z, acc.gx));     // - (A / r^2) n
+                    acc.gy = fmaf(q, dy, fmaf(nir2, a.w, acc.gy));
                 }
             } else {
+                // b = (-c ln2/4pi, c/2pi, 0, 0)
                 if constexpr (VAL) {
-                    if constexpr (MODE == 0) {
-                        acc.v = fmaf(b.x, f_lg2(r2), acc.v);
-                    } else {
-                        float l = (MODE & kBall) ? f_lg2(fminf(r2, mc->R2)) - mc->lgR2 : f_lg2(r2);
-                        if constexpr ((MODE & kClampS) != 0) l = fmaxf(l, -mc->sclamp);
-                        acc.v = fmaf(b.x, l, acc.v);
-                    }
+                    float l = (MODE & kBall) ? f_lg2(fminf(r2, mc->R2)) - mc->lgR2 : f_lg2(r2);
+                    if constexpr ((MODE & kClampS) != 0) l = fmaxf(l, -mc->sclamp);
+                    acc.v = fmaf(b.x, l, acc.v);
                 }
                 if constexpr (GRAD) {
-                    float c = b.y * ir2;
-                    acc.gx = fmaf(-c, dx, acc.gx);
-                    acc.gy = fmaf(-c, dy, acc.gy);
+                    float c = __fmul_rn(b.y, nir2);
+                    acc.gx = fmaf(c, dx, acc.gx);
+                    acc.gy = fmaf(c, dy, acc.gy);
                 }
             }
         } else {
@@ -155,41 +162,174 @@ __device__ __forceinline__ void pair(const float4 a, const float4 b, float px, f
             }
         }
     } else {
-        // 3D: boundary payload a = (zx, zy, zz, nx), b = (ny, nz, A, B); source a = (y, C)
-        float dx = a.x - px, dy = a.y - py, dz = a.z - pz;
-        float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        // 3D boundary payload a = (zx, zy, zz, A nx), b = (A ny, A nz, -B, B); source a = (y, -C)
+        float dx = __fsub_rn(a.x, px), dy = __fsub_rn(a.y, py), dz = __fsub_rn(a.z, pz);
+        float r2 = fmaf(dx, dx, fmaf(dy, dy, __fmul_rn(dz, dz)));
         if constexpr (TRACK) mn = fminf(mn, r2);
         float ir = f_rsq(r2);
-        float ir2 = ir * ir, ir3 = ir2 * ir;
-        float e = 1.0f, Q = 1.0f;
-        if constexpr (KIND == kScr3) {
-            float t = s * (r2 * ir);
-            e = f_ex2(-1.44269504088896340736f * t);
-            Q = e * (t + 1.0f);
-        }
-        if constexpr (!SRC) {
-            float nd = fmaf(a.w, dx, fmaf(b.x, dy, b.y * dz));
-            float pn = nd * ir3;
-            if constexpr (VAL) {
-                if constexpr (KIND == kScr3) acc.v = fmaf(b.z * Q, pn, fmaf(b.w * e, ir, acc.v));
-                else acc.v = fmaf(b.z, pn, fmaf(b.w, ir, acc.v));
+        float ir2 = __fmul_rn(ir, ir), ir3 = __fmul_rn(ir2, ir);
+        if constexpr (KIND == kLap3) {
+            if constexpr (!SRC) {
+                float ndA = fmaf(a.w, dx, fmaf(b.x, dy, __fmul_rn(b.y, dz)));
+                if constexpr (VAL) acc.v = fmaf(ndA, ir3, fmaf(b.w, ir, acc.v));
+                if constexpr (GRAD) {  // accumulated negated: (A/r^3) n - q d
+                    float nq = __fmul_rn(fmaf(__fmul_rn(ndA, -3.0f), ir2, b.z), ir3);
+                    acc.gx = fmaf(nq, dx, fmaf(ir3, a.w, acc.gx));
+                    acc.gy = fmaf(nq, dy, fmaf(ir3, b.x, acc.gy));
+                    acc.gz = fmaf(nq, dz, fmaf(ir3, b.y, acc.gz));
+                }
+            } else {
+                if constexpr (VAL) acc.v = fmaf(a.w, ir, acc.v);
+                if constexpr (GRAD) {
+                    float c = __fmul_rn(a.w, ir3);
+                    acc.gx = fmaf(c, dx, acc.gx);
+                    acc.gy = fmaf(c, dy, acc.gy);
+                    acc.gz = fmaf(c, dz, acc.gz);
+                }
             }
+        } else {  // screened 3D: e = exp(-s r), Q = e (s r + 1)
+            float r = __fmul_rn(r2, ir);
+            float t = __fmul_rn(s, r);
+            float e = f_ex2(__fmul_rn(r, -1.44269504088896340736f * s));
+            float Q = fmaf(e, t, e);
+            if constexpr (!SRC) {
+                float ndA = fmaf(a.w, dx, fmaf(b.x, dy, __fmul_rn(b.y, dz)));
+                float pA = __fmul_rn(ndA, ir3);  // A p
+                if constexpr (VAL) acc.v = fmaf(pA, Q, fmaf(__fmul_rn(b.w, ir), e, acc.v));
+                if constexpr (GRAD) {
+                    float q = fmaf(3.0f * Q * pA, ir2, b.w * Q * ir3);
+                    q = fmaf(sigma * e, pA, q);
+                    float c = Q * ir3;
+                    acc.gx = fmaf(q, dx, fmaf(-c, a.w, acc.gx));
+                    acc.gy = fmaf(q, dy, fmaf(-c, b.x, acc.gy));
+                    acc.gz = fmaf(q, dz, fmaf(-c, b.y, acc.gz));
+                }
+            } else {
+                if constexpr (VAL) acc.v = fmaf(__fmul_rn(a.w, ir), e, acc.v);
+                if constexpr (GRAD) {
+                    float c = a.w * Q * ir3;
+                    acc.gx = fmaf(c, dx, acc.gx);
+                    acc.gy = fmaf(c, dy, acc.gy);
+                    acc.gz = fmaf(c, dz, acc.gz);
+                }
+            }
+        }
+    }
+}
+
+// --- packed FP32 (sm_100a FFMA2 / FMUL2 / FADD2): two query points per op --------
+// The gather is issue-bound, not FP32-pipe-bound: a packed op does two lanes' work
+// in one issue slot (measured: FFMA2 sustains the full 128 FP32 FMA/clk/SM), which
+// leaves slots for the MUFU, LDS and loop instructions. Scalar sample operands
+// broadcast for free (ptxas folds them into a .F32 operand).
+struct F2 {
+    unsigned long long v;
+};
+__device__ __forceinline__ F2 pk(float lo, float hi) {
+    F2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ F2 bc(float x) { return pk(x, x); }
+__device__ __forceinline__ void upk(F2 a, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v)); }
+__device__ __forceinline__ F2 add2(F2 a, F2 b) { F2 r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
+__device__ __forceinline__ F2 sub2(F2 a, F2 b) { F2 r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
+__device__ __forceinline__ F2 mul2(F2 a, F2 b) { F2 r; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+    F2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+    return r;
+}
+template <class Fn>
+__device__ __forceinline__ F2 each(F2 a, Fn&& f) {
+    float lo, hi;
+    upk(a, lo, hi);
+    return pk(f(lo), f(hi));
+}
+struct Acc2 {
+    F2 v, gx, gy, gz;
+};
+
+// which (KIND, VAL, GRAD, MODE) run packed: 2D and 3D Laplace, 3D screened values
+template <int KIND, bool VAL, bool GRAD, int MODE>
+struct Packed {
+    static constexpr bool value = MODE == 0 && (KIND == kLap2 || KIND == kLap3 || (KIND == kScr3 && !GRAD));
+};
+
+// pair() on two query points at once; same operations, same rounding per lane
+template <int KIND, bool SRC, bool VAL, bool GRAD, bool TRACK>
+__device__ __forceinline__ void pair2(const float4 a, const float4 b, F2 px, F2 py, F2 pz, float s, Acc2& acc,
+                                      float* mn) {
+    if constexpr (KIND == kLap2) {
+        F2 dx = sub2(bc(a.x), px), dy = sub2(bc(a.y), py);
+        F2 r2 = fma2(dx, dx, mul2(dy, dy));
+        if constexpr (TRACK) {
+            float lo, hi;
+            upk(r2, lo, hi);
+            mn[0] = fminf(mn[0], lo);
+            mn[1] = fminf(mn[1], hi);
+        }
+        F2 nir2 = each(r2, [](float x) { return f_rcp(-x); });
+        if constexpr (!SRC) {
+            F2 ndA = fma2(bc(a.z), dx, mul2(bc(a.w), dy));
+            F2 t = mul2(ndA, nir2);
+            // (ptxas contracts a mul2 feeding an add2 into FFMA2 even for .rn, so the
+            // fused form is written out, here and in the scalar pair())
+            if constexpr (VAL) acc.v = fma2(ndA, nir2, fma2(bc(b.y), each(r2, [](float x) { return f_lg2(x); }), acc.v));
             if constexpr (GRAD) {
-                float aq = b.z * Q;
-                float q = fmaf(3.0f * aq, pn * ir2, b.w * Q * ir3);
-                if constexpr (KIND == kScr3) q = fmaf(b.z * sigma * e, pn, q);
-                float c = aq * ir3;
-                acc.gx = fmaf(q, dx, fmaf(-c, a.w, acc.gx));
-                acc.gy = fmaf(q, dy, fmaf(-c, b.x, acc.gy));
-                acc.gz = fmaf(q, dz, fmaf(-c, b.y, acc.gz));
+                F2 q = mul2(fma2(t, bc(2.0f), bc(b.z)), nir2);
+                acc.gx = fma2(q, dx, fma2(nir2, bc(a.z), acc.gx));
+                acc.gy = fma2(q, dy, fma2(nir2, bc(a.w), acc.gy));
             }
         } else {
-            if constexpr (VAL) acc.v = fmaf(-a.w * e, ir, acc.v);
+            if constexpr (VAL) acc.v = fma2(bc(b.x), each(r2, [](float x) { return f_lg2(x); }), acc.v);
             if constexpr (GRAD) {
-                float c = a.w * Q * ir3;
-                acc.gx = fmaf(-c, dx, acc.gx);
-                acc.gy = fmaf(-c, dy, acc.gy);
-                acc.gz = fmaf(-c, dz, acc.gz);
+                F2 c = mul2(bc(b.y), nir2);
+                acc.gx = fma2(c, dx, acc.gx);
+                acc.gy = fma2(c, dy, acc.gy);
+            }
+        }
+    } else {
+        F2 dx = sub2(bc(a.x), px), dy = sub2(bc(a.y), py), dz = sub2(bc(a.z), pz);
+        F2 r2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+        if constexpr (TRACK) {
+            float lo, hi;
+            upk(r2, lo, hi);
+            mn[0] = fminf(mn[0], lo);
+            mn[1] = fminf(mn[1], hi);
+        }
+        F2 ir = each(r2, [](float x) { return f_rsq(x); });
+        F2 ir2 = mul2(ir, ir), ir3 = mul2(ir2, ir);
+        if constexpr (KIND == kLap3) {
+            if constexpr (!SRC) {
+                F2 ndA = fma2(bc(a.w), dx, fma2(bc(b.x), dy, mul2(bc(b.y), dz)));
+                if constexpr (VAL) acc.v = fma2(ndA, ir3, fma2(bc(b.w), ir, acc.v));
+                if constexpr (GRAD) {
+                    F2 nq = mul2(fma2(mul2(ndA, bc(-3.0f)), ir2, bc(b.z)), ir3);
+                    acc.gx = fma2(nq, dx, fma2(ir3, bc(a.w), acc.gx));
+                    acc.gy = fma2(nq, dy, fma2(ir3, bc(b.x), acc.gy));
+                    acc.gz = fma2(nq, dz, fma2(ir3, bc(b.y), acc.gz));
+                }
+            } else {
+                if constexpr (VAL) acc.v = fma2(bc(a.w), ir, acc.v);
+                if constexpr (GRAD) {
+                    F2 c = mul2(bc(a.w), ir3);
+                    acc.gx = fma2(c, dx, acc.gx);
+                    acc.gy = fma2(c, dy, acc.gy);
+                    acc.gz = fma2(c, dz, acc.gz);
+                }
+            }
+        } else {  // kScr3, values only
+            F2 r = mul2(r2, ir);
+            F2 t = mul2(bc(s), r);
+            F2 e = each(mul2(r, bc(-1.44269504088896340736f * s)), [](float x) { return f_ex2(x); });
+            F2 Q = fma2(e, t, e);
+            if constexpr (!SRC) {
+                F2 ndA = fma2(bc(a.w), dx, fma2(bc(b.x), dy, mul2(bc(b.y), dz)));
+                F2 pA = mul2(ndA, ir3);
+                acc.v = fma2(pA, Q, fma2(mul2(bc(b.w), ir), e, acc.v));
+            } else {
+                acc.v = fma2(mul2(bc(a.w), ir), e, acc.v);
             }
         }
     }
@@ -243,12 +383,38 @@ __device__ void tile_slow(const float4* sm, int cnt, float px, float py, float p
 template <int KIND, bool SRC, bool VAL, bool GRAD, bool TRACK, int MODE>
 __device__ __forceinline__ void tile_loop(const float4* S, int cnt, const float* px, const float* py, const float* pz,
                                           const Params& P, Acc* acc, float* mn, const ModeCtx* mc) {
-#pragma unroll 2
-    for (int j = 0; j < cnt; ++j) {
-        const float4 a = S[2 * j], b = S[2 * j + 1];
+    if constexpr (Packed<KIND, VAL, GRAD, MODE>::value) {
+        F2 px2[kQ / 2], py2[kQ / 2], pz2[kQ / 2];
+        Acc2 a2[kQ / 2];
 #pragma unroll
-        for (int q = 0; q < kQ; ++q)
-            pair<KIND, SRC, VAL, GRAD, TRACK, MODE>(a, b, px[q], py[q], pz[q], P.sigma, P.s, acc[q], mn[q], mc + q);
+        for (int h = 0; h < kQ / 2; ++h) {
+            px2[h] = pk(px[2 * h], px[2 * h + 1]);
+            py2[h] = pk(py[2 * h], py[2 * h + 1]);
+            pz2[h] = pk(pz[2 * h], pz[2 * h + 1]);
+            a2[h].v = a2[h].gx = a2[h].gy = a2[h].gz = pk(0.f, 0.f);
+        }
+#pragma unroll 2
+        for (int j = 0; j < cnt; ++j) {
+            const float4 a = S[2 * j], b = S[2 * j + 1];
+#pragma unroll
+            for (int h = 0; h < kQ / 2; ++h)
+                pair2<KIND, SRC, VAL, GRAD, TRACK>(a, b, px2[h], py2[h], pz2[h], P.s, a2[h], mn + 2 * h);
+        }
+#pragma unroll
+        for (int h = 0; h < kQ / 2; ++h) {
+            upk(a2[h].v, acc[2 * h].v, acc[2 * h + 1].v);
+            upk(a2[h].gx, acc[2 * h].gx, acc[2 * h + 1].gx);
+            upk(a2[h].gy, acc[2 * h].gy, acc[2 * h + 1].gy);
+            upk(a2[h].gz, acc[2 * h].gz, acc[2 * h + 1].gz);
+        }
+    } else {
+#pragma unroll 2
+        for (int j = 0; j < cnt; ++j) {
+            const float4 a = S[2 * j], b = S[2 * j + 1];
+#pragma unroll
+            for (int q = 0; q < kQ; ++q)
+                pair<KIND, SRC, VAL, GRAD, TRACK, MODE>(a, b, px[q], py[q], pz[q], P.sigma, P.s, acc[q], mn[q], mc + q);
+        }
     }
 }
 
@@ -341,11 +507,14 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
                     if (!src) tile_slow<KIND, false, VAL, GRAD, MODE>(S, cnt, px[q], py[q], pz[q], P, acc[q], skips[q], mc + q);
                     else tile_slow<KIND, true, VAL, GRAD, MODE>(S, cnt, px[q], py[q], pz[q], P, acc[q], skips[q], mc + q);
                 }
-                if (VAL) dv[q] += acc[q].v;
+                // undo the accumulator sign conventions (Conv)
+                const bool nv = src ? Conv<KIND, true>::negV : Conv<KIND, false>::negV;
+                const bool ng = src ? Conv<KIND, true>::negG : Conv<KIND, false>::negG;
+                if (VAL) dv[q] += nv ? -static_cast<double>(acc[q].v) : static_cast<double>(acc[q].v);
                 if (GRAD) {
-                    dg0[q] += acc[q].gx;
-                    dg1[q] += acc[q].gy;
-                    if (D3) dg2[q] += acc[q].gz;
+                    dg0[q] += ng ? -static_cast<double>(acc[q].gx) : static_cast<double>(acc[q].gx);
+                    dg1[q] += ng ? -static_cast<double>(acc[q].gy) : static_cast<double>(acc[q].gy);
+                    if (D3) dg2[q] += ng ? -static_cast<double>(acc[q].gz) : static_cast<double>(acc[q].gz);
                 }
             }
             __syncthreads();  // everyone is done reading buffer st
@@ -412,13 +581,15 @@ __device__ __forceinline__ void pack_boundary_one(const CacheSample& s, int n, i
         double A = w * u * inv2pi;
         a = make_float4(s.z[0], s.z[1], static_cast<float>(A * s.n[0]), static_cast<float>(A * s.n[1]));
         b = make_float4(static_cast<float>(A), static_cast<float>(w * d * ln2 * 0.5 * inv2pi),
-                        static_cast<float>(w * d * inv2pi), 0.f);
+                        static_cast<float>(-w * d * inv2pi), 0.f);
     } else if (kind == kScr2) {
         a = make_float4(s.z[0], s.z[1], s.n[0], s.n[1]);
         b = make_float4(static_cast<float>(w * u * inv2pi), static_cast<float>(w * d * inv2pi), 0.f, 0.f);
-    } else {
-        a = make_float4(s.z[0], s.z[1], s.z[2], s.n[0]);
-        b = make_float4(s.n[1], s.n[2], static_cast<float>(w * u * inv4pi), static_cast<float>(w * d * inv4pi));
+    } else {  // 3D: A folded into the normal, b = (A ny, A nz, -B, B)
+        double A = w * u * inv4pi, Bv = w * d * inv4pi;
+        a = make_float4(s.z[0], s.z[1], s.z[2], static_cast<float>(A * s.n[0]));
+        b = make_float4(static_cast<float>(A * s.n[1]), static_cast<float>(A * s.n[2]), static_cast<float>(-Bv),
+                        static_cast<float>(Bv));
     }
     out[2 * i] = a;
     out[2 * i + 1] = b;
@@ -435,12 +606,12 @@ __device__ __forceinline__ void pack_source_one(const SourceSampleDev& s, int ki
     float4 a, b = make_float4(0.f, 0.f, 0.f, 0.f);
     if (kind == kLap2) {
         a = make_float4(s.y[0], s.y[1], 0.f, 0.f);
-        b = make_float4(static_cast<float>(c * ln2 * 0.5 * inv2pi), static_cast<float>(c * inv2pi), 0.f, 0.f);
+        b = make_float4(static_cast<float>(-c * ln2 * 0.5 * inv2pi), static_cast<float>(c * inv2pi), 0.f, 0.f);
     } else if (kind == kScr2) {
         a = make_float4(s.y[0], s.y[1], 0.f, 0.f);
         b = make_float4(static_cast<float>(c * inv2pi), 0.f, 0.f, 0.f);
     } else {
-        a = make_float4(s.y[0], s.y[1], s.y[2], static_cast<float>(c * inv4pi));
+        a = make_float4(s.y[0], s.y[1], s.y[2], static_cast<float>(-c * inv4pi));
     }
     out[2 * i] = a;
     out[2 * i + 1] = b;
@@ -475,6 +646,10 @@ __global__ void eval_kernels_kernel(const double* x, const double* y, const doub
     float mn = 0.f, s = sqrtf(sigma);
     pair<KIND, false, true, true>(pb[0], pb[1], px, py, pz, sigma, s, ab, mn);
     pair<KIND, true, true, true>(ps[0], ps[1], px, py, pz, sigma, s, as, mn);
+    if (Conv<KIND, false>::negV) ab.v = -ab.v;
+    if (Conv<KIND, true>::negV) as.v = -as.v;
+    if (Conv<KIND, false>::negG) { ab.gx = -ab.gx; ab.gy = -ab.gy; ab.gz = -ab.gz; }
+    if (Conv<KIND, true>::negG) { as.gx = -as.gx; as.gy = -as.gy; as.gz = -as.gz; }
     double* o = out + (2 + 2 * dim) * i;
     o[0] = as.v;
     o[1] = as.gx; o[2] = as.gy; if (dim == 3) o[3] = as.gz;

@@ -39,6 +39,51 @@ __global__ void __launch_bounds__(256) pipe_kernel(float* out, float seed) {
     if (s == 1.2345f) out[threadIdx.x] = s;  // keep the chains alive
 }
 
+// register-operand forms (no immediates / constant-bank operands): OP 0 FFMA, 1 FMUL, 2 FADD
+template <int OP>
+__global__ void __launch_bounds__(256) pipe_reg_kernel(float* out, float seed) {
+    float v[8];
+    const float m = 0.999f + 1e-9f * threadIdx.x, c = 1e-4f * (1.0f + 1e-9f * threadIdx.x);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = seed + 0.001f * (threadIdx.x + k);
+#pragma unroll 16
+    for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if constexpr (OP == 0) v[k] = fmaf(v[k], m, c);
+            else if constexpr (OP == 1) v[k] = v[k] * m;
+            else v[k] = v[k] + c;
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[k];
+    if (s == 1.2345f) out[threadIdx.x] = s;
+}
+
+// packed FP32 (FFMA2, sm_100a): each instruction does two FMAs
+__global__ void __launch_bounds__(256) ffma2_kernel(float* out, float seed) {
+    unsigned long long v[8];
+    const float m = 0.999f + 1e-9f * threadIdx.x, c = 1e-4f;
+    unsigned long long M, Cc;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(M) : "f"(m), "f"(m));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(Cc) : "f"(c), "f"(c));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        float a = seed + 0.001f * (threadIdx.x + k), b = a + 0.5f;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(v[k]) : "f"(a), "f"(b));
+    }
+#pragma unroll 16
+    for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(v[k]) : "l"(M), "l"(Cc));
+    }
+    unsigned long long s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s ^= v[k];
+    if (s == 12345ull) out[threadIdx.x] = 1.f;
+}
+
 __global__ void __launch_bounds__(256) dfma_kernel(double* out, double seed) {
     double v[8];
 #pragma unroll
@@ -96,6 +141,10 @@ extern "C" int bvc_pipe_probe(int which, double* opsPerSecond) {
             case 3: dfma_kernel<<<grid, threads>>>(static_cast<double*>(scratch), 1.0); ops = 0.25; break;
             case 4: pipe_kernel<4><<<grid, threads>>>(static_cast<float*>(scratch), 1.5f); ops = 1.0; break;
             case 5: pipe_kernel<5><<<grid, threads>>>(static_cast<float*>(scratch), 0.5f); ops = 1.0; break;
+            case 7: pipe_reg_kernel<0><<<grid, threads>>>(static_cast<float*>(scratch), 1.0f); ops = 1.0; break;
+            case 8: pipe_reg_kernel<1><<<grid, threads>>>(static_cast<float*>(scratch), 1.0f); ops = 1.0; break;
+            case 9: pipe_reg_kernel<2><<<grid, threads>>>(static_cast<float*>(scratch), 1.0f); ops = 1.0; break;
+            case 10: ffma2_kernel<<<grid, threads>>>(static_cast<float*>(scratch), 1.0f); ops = 2.0; break;
             case 6: {
                 size_t n = (32u << 20) / sizeof(float4);
                 l2_kernel<<<grid, threads>>>(static_cast<const float4*>(scratch), n, 8,
