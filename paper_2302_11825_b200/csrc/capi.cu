@@ -13,6 +13,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -189,6 +190,17 @@ int api_fail(const std::exception& e) { return fail(e); }
 // ---------------------------------------------------------------------------
 // handles
 // ---------------------------------------------------------------------------
+// BVH leaf size (<= 8: the leaf code keeps count - 1 in 3 bits). Measured walk
+// time by leaf size 1/2/3/4/8: 3D C4 642/613/620/643/743 ms, C5 leaf 2 -9% vs 4;
+// 2D C2 7.84/7.34/7.34/7.55/8.21 ms, C3 185/186/189/195/218 ms, but the 1024-segment
+// C1 1.65 (leaf 2) vs 1.46 ms (leaf 4). BVC_LEAF2 / BVC_LEAF3 override (tuning).
+int leaf_size(int dim, int ns) {
+    const char* e = std::getenv(dim == 2 ? "BVC_LEAF2" : "BVC_LEAF3");
+    int def = (dim == 3 || ns > 1024) ? 2 : 4;
+    int v = e ? std::atoi(e) : def;
+    return v >= 1 && v <= 8 ? v : def;
+}
+
 struct bvc_scene_s {
     bvc_host::HostScene host;
     bvc_host::HostBvh bvh;
@@ -210,7 +222,7 @@ struct bvc_scene_s {
     DevBuf<int4> triSil;
 
     void upload3() {
-        bvh = bvc_host::buildBvh(host, 4);
+        bvh = bvc_host::buildBvh(host, leaf_size(3, host.ns));
         size_t nn = bvh.children.size() / 2;
         std::vector<bvc_dev::Node3> hn(nn);
         for (size_t i = 0; i < nn; ++i) {
@@ -287,7 +299,7 @@ struct bvc_scene_s {
             upload3();
             return;
         }
-        bvh = bvc_host::buildBvh(host, 4);
+        bvh = bvc_host::buildBvh(host, leaf_size(2, host.ns));
         size_t nn = bvh.children.size() / 2;
         std::vector<Node2> hn(nn);
         for (size_t i = 0; i < nn; ++i) {
