@@ -147,7 +147,7 @@ def run_gpu(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or os.environ.get("BVC_BENCH_SHARDED") == "1":
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -180,12 +180,15 @@ def run_gpu(args):
         scache = B.generate_source_cache(c.problem, region, cfg, c.seed, rnd) if M else None
         spec = B.make_splat_config(scene, c.problem, cfg)
         B.splat_range(cache, scache, p, spec, 0, 1 << 62, True, bool(c.gradients))
+        B.fallback_walks(scene, c.problem, cfg, p, c.seed, rnd, bool(c.gradients))  # this rank's band points
         return stats
 
     def round_single(p, rnd):
         return B.update_solution(scene, c.problem, region, cfg, p, c.seed, rnd, gradients=bool(c.gradients))
 
-    step = round_single if world == 1 else round_multi
+    # BVC_BENCH_SHARDED=1 runs the sharded path (NCCL all-gather) even at N=1, to
+    # exercise the multi-GPU plumbing on a single device
+    step = round_multi if (world > 1 or os.environ.get("BVC_BENCH_SHARDED") == "1") else round_single
 
     def barrier():
         if dist is not None:

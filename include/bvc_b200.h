@@ -274,6 +274,9 @@ int bvc_boundary_cache_download(bvc_boundary_cache c, bvc_boundary_sample* sampl
 int bvc_boundary_cache_packed(bvc_boundary_cache c, void** device_ptr, size_t* bytes);
 int bvc_boundary_cache_from_packed(const void* device_ptr, int n, int dim, int voronoi,
                                    double boundaryLength, bvc_boundary_cache* out);
+/* assignVoronoiWeights (cache.cpp:280-297) over a whole round's cache: a sharded
+   generation skips it, the all-gathered cache gets it once (multi-GPU + voronoi) */
+int bvc_boundary_cache_assign_voronoi(bvc_boundary_cache cache, bvc_region region);
 int bvc_boundary_cache_destroy(bvc_boundary_cache c);
 int bvc_source_cache_create(const bvc_source_sample* samples, int m, int dim, double area,
                             bvc_source_cache* out);
@@ -332,6 +335,11 @@ int bvc_corrected_source_splat(bvc_source_cache scache, bvc_eval_points pts, bvc
 int bvc_update_solution(bvc_scene scene, const bvc_problem* problem, bvc_region region,
                         const bvc_cache_config* cfg, bvc_eval_points pts, uint64_t seed,
                         uint64_t round, int gradients, bvc_round_stats* stats);
+
+/* the fallback-band walks of updateSolution (cache.cpp:665-681) alone, for the
+   sharded multi-GPU round (generate shard, all-gather, splat_range, then this) */
+int bvc_fallback_walks(bvc_scene scene, const bvc_problem* problem, const bvc_cache_config* cfg,
+                       bvc_eval_points pts, uint64_t seed, uint64_t round, int gradients);
 
 /* ---- streamlines (runStreamlines tools/src/runner.cpp:285-373) -------------- */
 typedef enum { BVC_STREAM_OK = 0, BVC_STREAM_OUTSIDE = 1, BVC_STREAM_ZERO_GRADIENT = 2 } bvc_stream_reason;

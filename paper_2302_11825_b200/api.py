@@ -33,7 +33,8 @@ SYMBOLS = (
     "bvc_update_solution bvc_wos_solve bvc_wost_solve bvc_wost_gradient bvc_wost_normal_derivative "
     "bvc_walk_traffic_profile bvc_eval_kernels bvc_eval_bessel bvc_corrected_boundary_splat "
     "bvc_corrected_source_splat bvc_trace_streamlines bvc_grid_save_csv bvc_grid_load_csv bvc_grid_rmse "
-    "bvc_grid_save_pgm bvc_streamlines_write_csv bvc_pipe_probe"
+    "bvc_grid_save_pgm bvc_streamlines_write_csv bvc_pipe_probe bvc_boundary_cache_assign_voronoi "
+    "bvc_fallback_walks"
 ).split()
 
 
@@ -417,6 +418,10 @@ class BoundaryCache:
         return dict(z=raw[:, 0:d].copy(), n=raw[:, 3:3 + d].copy(), pdf=raw[:, 6].copy(), uHat=raw[:, 7].copy(),
                     dHat=raw[:, 8].copy(), weight=raw[:, 9].copy(), segment=seg, arc=raw[:, 11].copy())
 
+    def assign_voronoi(self, region: "SolveRegion"):
+        """assignVoronoiWeights (cache.cpp:280-297) over this (whole-round) cache."""
+        _check(lib().bvc_boundary_cache_assign_voronoi(self.h, region.h))
+
     def packed(self):
         p, b = C.c_void_p(), C.c_size_t()
         _check(lib().bvc_boundary_cache_packed(self.h, C.byref(p), C.byref(b)))
@@ -571,6 +576,12 @@ def update_solution(scene: Scene, pb, region: SolveRegion, cfg, pts: EvaluationP
     _check(lib().bvc_update_solution(scene.h, C.byref(pb), region.h, C.byref(cfg), pts.h, C.c_uint64(seed),
                                      C.c_uint64(round_), int(gradients), C.byref(st)))
     return _stats_dict(st)
+
+
+def fallback_walks(scene: Scene, pb, cfg, pts: EvaluationPoints, seed, round_, gradients=False):
+    """updateSolution's fallback-band loop (cache.cpp:665-681) on its own (sharded rounds)."""
+    _check(lib().bvc_fallback_walks(scene.h, C.byref(pb), C.byref(cfg), pts.h, C.c_uint64(seed), C.c_uint64(round_),
+                                    int(gradients)))
 
 
 def _estimates(fn, scene, pb, x, cfg, streams, normal=None, vector=False):

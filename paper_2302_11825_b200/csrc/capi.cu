@@ -789,6 +789,39 @@ __global__ void redraw_copy_kernel(const CacheSample* src, const int* idx, int n
     if (j < n) dst[idx[j]] = src[j];
 }
 
+// assignVoronoiWeights (cache.cpp:280-297), on the host (rare mode): per region
+// loop, each sample's weight is half the arc distance to its two neighbours
+void assign_voronoi(bvc_region_s* R, bvc_boundary_cache_s* c) {
+    need(c->dim == 2, "Voronoi weights are defined for 2D loops only");
+    int n = c->n;
+    if (n == 0) return;
+    std::vector<CacheSample> hs(n);
+    c->samples.download(hs.data(), n);
+    CK(cudaStreamSynchronize(g_stream));
+    const auto& bh = R->boundary.host;
+    std::vector<std::vector<std::pair<double, int>>> per(bh.loopLength.size());
+    for (int i = 0; i < n; ++i) per[bh.loop[hs[i].segment]].push_back({hs[i].arc, i});
+    for (size_t li = 0; li < per.size(); ++li) {
+        auto& e = per[li];
+        if (e.empty()) continue;
+        std::sort(e.begin(), e.end());
+        size_t m = e.size();
+        double L = bh.loopLength[li];
+        for (size_t k = 0; k < m; ++k) {
+            double w;
+            if (m == 1) w = L;
+            else {
+                double prev = k > 0 ? e[k].first - e[k - 1].first : e[0].first + L - e[m - 1].first;
+                double next = k + 1 < m ? e[k + 1].first - e[k].first : e[0].first + L - e[m - 1].first;
+                w = 0.5 * (prev + next);
+            }
+            hs[e[k].second].weight = static_cast<float>(w);
+        }
+    }
+    c->samples.upload(hs.data(), n);
+    c->voronoi = 1;
+}
+
 void generate_cache(bvc_scene_s* S, const bvc_problem& pb, bvc_region_s* R, const bvc_cache_config& cfg, uint64_t seed,
                     uint64_t round, int begin, int end, bvc_boundary_cache_s* out, GenStats& st) {
     require_device();
@@ -804,7 +837,7 @@ void generate_cache(bvc_scene_s* S, const bvc_problem& pb, bvc_region_s* R, cons
     const int n = end - begin;
     out->n = n;
     out->dim = 2;
-    out->voronoi = cfg.voronoi;
+    out->voronoi = 0;  // set by assign_voronoi once the whole round is present
     out->length = R->boundary.total;
     out->samples.resize(std::max(n, 1));
     if (n == 0) return;
@@ -851,32 +884,9 @@ void generate_cache(bvc_scene_s* S, const bvc_problem& pb, bvc_region_s* R, cons
         for (int j = 0; j < nb; ++j) if (hf2[j]) still.push_back(bad[j]);
         bad.swap(still);
     }
-    if (cfg.voronoi) {  // assignVoronoiWeights cache.cpp:280-297, on the host (rare mode)
-        std::vector<CacheSample> hs(n);
-        out->samples.download(hs.data(), n);
-        CK(cudaStreamSynchronize(g_stream));
-        const auto& bh = B.host;
-        std::vector<std::vector<std::pair<double, int>>> per(bh.loopLength.size());
-        for (int i = 0; i < n; ++i) per[bh.loop[hs[i].segment]].push_back({hs[i].arc, i});
-        for (size_t li = 0; li < per.size(); ++li) {
-            auto& e = per[li];
-            if (e.empty()) continue;
-            std::sort(e.begin(), e.end());
-            size_t m = e.size();
-            double L = bh.loopLength[li];
-            for (size_t k = 0; k < m; ++k) {
-                double w;
-                if (m == 1) w = L;
-                else {
-                    double prev = k > 0 ? e[k].first - e[k - 1].first : e[0].first + L - e[m - 1].first;
-                    double next = k + 1 < m ? e[k + 1].first - e[k].first : e[0].first + L - e[m - 1].first;
-                    w = 0.5 * (prev + next);
-                }
-                hs[e[k].second].weight = static_cast<float>(w);
-            }
-        }
-        out->samples.upload(hs.data(), n);
-    }
+    // assignVoronoiWeights needs every sample of the round: a shard leaves it to the
+    // caller (distributed.py assigns after the all-gather)
+    if (cfg.voronoi && begin == 0 && end == N) assign_voronoi(R, out);
 }
 
 // RegionSampler::sample (sampling.cpp:62-108): jittered strata over the bounding
@@ -2200,6 +2210,9 @@ int bvc_boundary_cache_from_packed(const void* ptr, int n, int dim, int voronoi,
         *out = c.release();
     })
 }
+int bvc_boundary_cache_assign_voronoi(bvc_boundary_cache c, bvc_region r) {
+    API(need(c && r, "null argument"); r->upload(); assign_voronoi(r, c))
+}
 int bvc_boundary_cache_destroy(bvc_boundary_cache c) { API(delete c) }
 int bvc_source_cache_create(const bvc_source_sample* smp, int m, int dim, double area, bvc_source_cache* out) {
     API({
@@ -2332,6 +2345,18 @@ int bvc_update_solution(bvc_scene s, const bvc_problem* pb, bvc_region r, const 
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         cudaEventDestroy(e2);
+    })
+}
+
+// the fallback-band loop of updateSolution (cache.cpp:665-681) alone: the sharded
+// multi-GPU round runs it for the rank's own points after the exchange and gather
+int bvc_fallback_walks(bvc_scene s, const bvc_problem* pb, const bvc_cache_config* cfg, bvc_eval_points p,
+                       uint64_t seed, uint64_t round, int gradients) {
+    API({
+        require_device();
+        need(s && pb && cfg && p, "null argument");
+        fallback_walks(s, *pb, *cfg, p, seed, round, gradients != 0);
+        CK(cudaGetLastError());
     })
 }
 

@@ -57,6 +57,9 @@ def generate_and_allgather(B, dist, torch, scene, problem, region, cfg, seed, rn
     full = allgather_bytes(dist, torch, local, [s * SAMPLE_BYTES for s in shard_sizes(N, world)])
     torch.cuda.synchronize()
     h = C.c_void_p()
-    B.api._check(B.lib().bvc_boundary_cache_from_packed(C.c_void_p(full.data_ptr()), N, 2, cfg.voronoi,
+    B.api._check(B.lib().bvc_boundary_cache_from_packed(C.c_void_p(full.data_ptr()), N, shard.dim, 0,
                                                         C.c_double(0.0), C.byref(h)))
-    return B.BoundaryCache(h)
+    cache = B.BoundaryCache(h)
+    if cfg.voronoi:  # the weights need the whole round's samples
+        cache.assign_voronoi(region)
+    return cache

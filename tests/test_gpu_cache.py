@@ -100,6 +100,39 @@ def test_shard_union_equals_full_cache():
     assert not np.array_equal(other["uHat"], full["uHat"])
 
 
+def test_allgathered_shards_with_voronoi_weights_match_the_full_cache():
+    """The multi-GPU exchange (distributed.generate_and_allgather) on one device: packed
+    shards concatenated in order, then assignVoronoiWeights over the whole round."""
+    import torch
+
+    from paper_2302_11825_b200 import distributed
+
+    geom, pb, sc, region = _setup(H.disk_linear)
+    cfg = B.cache_config(B.walk_config(epsilon=1e-3), nBoundary=300, nWalksNeumann=8, nWalksDirichlet=16,
+                         offset=0.05, voronoi=1)
+    full = B.generate_boundary_cache(sc, pb, region, cfg, 8, 1).download()
+    assert abs(full["weight"].sum() - np.sum(np.linalg.norm(
+        region.vertices[region.segments[:, 1]] - region.vertices[region.segments[:, 0]], axis=1))) < 1e-4
+    parts = []
+    for r in range(3):
+        lo, hi = distributed.shard_range(300, r, 3)
+        shard = B.generate_boundary_cache(sc, pb, region, cfg, 8, 1, begin=lo, end=hi)
+        ptr, nbytes = shard.packed()
+        parts.append(torch.as_tensor(distributed._DeviceBytes(ptr, nbytes), device="cuda").clone())
+        del shard
+    joined = torch.cat(parts)
+    torch.cuda.synchronize()
+    import ctypes as C
+    h = C.c_void_p()
+    B.api._check(B.lib().bvc_boundary_cache_from_packed(C.c_void_p(joined.data_ptr()), 300, 2, 0, C.c_double(0.0),
+                                                        C.byref(h)))
+    cache = B.BoundaryCache(h)
+    cache.assign_voronoi(region)
+    got = cache.download()
+    for key in ("z", "n", "uHat", "dHat", "pdf", "weight", "arc"):
+        assert np.array_equal(got[key], full[key]), key
+
+
 def test_source_cache_fields():
     """test_cache.cpp:363-379."""
     geom, pb, sc, region = _setup(H.disk_poisson)
