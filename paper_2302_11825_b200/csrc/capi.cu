@@ -220,32 +220,60 @@ struct bvc_scene_s {
     DevBuf<bvc_dev::Prim3> prims3;
     DevBuf<float4> triNormal, triA, triB, triC, sil3A, sil3B, sil3N1, sil3N2;
     DevBuf<int4> triSil;
+    // GPU BVH build inputs (lbvh.cu)
+    DevBuf<int> cls;
+    DevBuf<int2> segSilD;
+    int bvhHeight = 0;
+
+    // BVC_BVH=gpu builds the BVH on the device (linear BVH, lbvh.cu); the default is
+    // the host binned-SAH build, whose trees measured faster to walk
+    bool build_on_gpu() const {
+        const char* e = std::getenv("BVC_BVH");
+        return e && std::string(e) == "gpu" && host.ns > 64;  // tiny scenes: one host pass
+    }
+    void gpu_build(int dim, const float4* a, const float4* b, const float4* c, const int2* sil) {
+        int n = host.ns, leaf = leaf_size(dim, n);
+        double pad = 9.5367431640625e-7 * std::max(host.diagonal, 1e-30);
+        size_t nn = static_cast<size_t>(std::max(n - 1, 1));
+        if (dim == 2) { nodes.resize(nn); prims.resize(std::max(n, 1)); }
+        else { nodes3.resize(nn); prims3.resize(std::max(n, 1)); }
+        int h = n > leaf ? build_lbvh(dim, a, b, c, cls.p, sil, n, leaf, host.lo, host.hi, pad, dim == 2 ? 1 : 0,
+                                      dim == 2 ? static_cast<void*>(nodes.p) : static_cast<void*>(nodes3.p),
+                                      dim == 2 ? static_cast<void*>(prims.p) : static_cast<void*>(prims3.p), g_stream)
+                         : -1;
+        CK(cudaGetLastError());
+        if (h < 0 || h >= 47)  // deeper than the device traversal stack (degenerate Morton keys)
+            throw Error(BVC_ERR_SOLVER, "GPU BVH build: tree deeper than the traversal stack; use the host build");
+        bvhHeight = h;
+    }
 
     void upload3() {
-        bvh = bvc_host::buildBvh(host, leaf_size(3, host.ns));
-        size_t nn = bvh.children.size() / 2;
-        std::vector<bvc_dev::Node3> hn(nn);
-        for (size_t i = 0; i < nn; ++i) {
-            const float* b = &bvh.boxes[12 * i];
-            hn[i].llo = make_float4(b[0], b[1], b[2], 0.f);
-            hn[i].lhi = make_float4(b[3], b[4], b[5], 0.f);
-            hn[i].rlo = make_float4(b[6], b[7], b[8], 0.f);
-            hn[i].rhi = make_float4(b[9], b[10], b[11], 0.f);
-            hn[i].left = bvh.children[2 * i];
-            hn[i].right = bvh.children[2 * i + 1];
-            hn[i].mask = bvh.masks[i];
-            hn[i].pad = 0;
-        }
-        nodes3.upload(hn.data(), nn);
         auto f4 = [](const double* p, float w) { return make_float4(p[0], p[1], p[2], w); };
-        std::vector<bvc_dev::Prim3> hp(host.ns);
-        for (int j = 0; j < host.ns; ++j) {
-            int id = bvh.order[j];
-            hp[j].a = f4(host.vert(host.idx[3 * id]), __int_as_float_host(id));
-            hp[j].b = f4(host.vert(host.idx[3 * id + 1]), __int_as_float_host(bvc_host::primClass(host, id)));
-            hp[j].c = f4(host.vert(host.idx[3 * id + 2]), 0.f);
+        if (!build_on_gpu()) {
+            bvh = bvc_host::buildBvh(host, leaf_size(3, host.ns));
+            size_t nn = bvh.children.size() / 2;
+            std::vector<bvc_dev::Node3> hn(nn);
+            for (size_t i = 0; i < nn; ++i) {
+                const float* b = &bvh.boxes[12 * i];
+                hn[i].llo = make_float4(b[0], b[1], b[2], 0.f);
+                hn[i].lhi = make_float4(b[3], b[4], b[5], 0.f);
+                hn[i].rlo = make_float4(b[6], b[7], b[8], 0.f);
+                hn[i].rhi = make_float4(b[9], b[10], b[11], 0.f);
+                hn[i].left = bvh.children[2 * i];
+                hn[i].right = bvh.children[2 * i + 1];
+                hn[i].mask = bvh.masks[i];
+                hn[i].pad = 0;
+            }
+            nodes3.upload(hn.data(), nn);
+            std::vector<bvc_dev::Prim3> hp(host.ns);
+            for (int j = 0; j < host.ns; ++j) {
+                int id = bvh.order[j];
+                hp[j].a = f4(host.vert(host.idx[3 * id]), __int_as_float_host(id));
+                hp[j].b = f4(host.vert(host.idx[3 * id + 1]), __int_as_float_host(bvc_host::primClass(host, id)));
+                hp[j].c = f4(host.vert(host.idx[3 * id + 2]), 0.f);
+            }
+            prims3.upload(hp.data(), hp.size());
         }
-        prims3.upload(hp.data(), hp.size());
         std::vector<float4> hn4(host.ns), ha(host.ns), hb(host.ns), hc(host.ns);
         std::vector<int4> hs(host.ns);
         std::vector<double> cd(host.ns);
@@ -278,6 +306,12 @@ struct bvc_scene_s {
         sil3B.upload(eb.data(), ne);
         sil3N1.upload(e1.data(), ne);
         sil3N2.upload(e2.data(), ne);
+        if (build_on_gpu()) {
+            std::vector<int> hcls(host.ns);
+            for (int i = 0; i < host.ns; ++i) hcls[i] = bvc_host::primClass(host, i);
+            cls.upload(hcls.data(), hcls.size());
+            gpu_build(3, triA.p, triB.p, triC.p, nullptr);
+        }
         uploaded = true;
     }
     bvc_dev::SceneView3 view3() {
@@ -299,30 +333,32 @@ struct bvc_scene_s {
             upload3();
             return;
         }
-        bvh = bvc_host::buildBvh(host, leaf_size(2, host.ns));
-        size_t nn = bvh.children.size() / 2;
-        std::vector<Node2> hn(nn);
-        for (size_t i = 0; i < nn; ++i) {
-            const float* b = &bvh.boxes[8 * i];
-            hn[i].lbox = make_float4(b[0], b[1], b[2], b[3]);
-            hn[i].rbox = make_float4(b[4], b[5], b[6], b[7]);
-            hn[i].left = bvh.children[2 * i];
-            hn[i].right = bvh.children[2 * i + 1];
-            hn[i].mask = bvh.masks[i];
-            hn[i].pad = 0;
+        if (!build_on_gpu()) {
+            bvh = bvc_host::buildBvh(host, leaf_size(2, host.ns));
+            size_t nn = bvh.children.size() / 2;
+            std::vector<Node2> hn(nn);
+            for (size_t i = 0; i < nn; ++i) {
+                const float* b = &bvh.boxes[8 * i];
+                hn[i].lbox = make_float4(b[0], b[1], b[2], b[3]);
+                hn[i].rbox = make_float4(b[4], b[5], b[6], b[7]);
+                hn[i].left = bvh.children[2 * i];
+                hn[i].right = bvh.children[2 * i + 1];
+                hn[i].mask = bvh.masks[i];
+                hn[i].pad = 0;
+            }
+            nodes.upload(hn.data(), nn);
+            std::vector<Prim2> hp(host.ns);
+            for (int j = 0; j < host.ns; ++j) {
+                int id = bvh.order[j];
+                const double *a = host.vert(host.idx[2 * id]), *b = host.vert(host.idx[2 * id + 1]);
+                hp[j].seg = make_float4(a[0], a[1], b[0], b[1]);
+                hp[j].id = id;
+                hp[j].label = bvc_host::primClass(host, id);
+                hp[j].sil0 = host.segSil[2 * id];
+                hp[j].sil1 = host.segSil[2 * id + 1];
+            }
+            prims.upload(hp.data(), hp.size());
         }
-        nodes.upload(hn.data(), nn);
-        std::vector<Prim2> hp(host.ns);
-        for (int j = 0; j < host.ns; ++j) {
-            int id = bvh.order[j];
-            const double *a = host.vert(host.idx[2 * id]), *b = host.vert(host.idx[2 * id + 1]);
-            hp[j].seg = make_float4(a[0], a[1], b[0], b[1]);
-            hp[j].id = id;
-            hp[j].label = bvc_host::primClass(host, id);
-            hp[j].sil0 = host.segSil[2 * id];
-            hp[j].sil1 = host.segSil[2 * id + 1];
-        }
-        prims.upload(hp.data(), hp.size());
         std::vector<float2> hnrm(host.ns);
         std::vector<float4> hab(host.ns);
         std::vector<float> harc(host.ns), hlen(host.ns);
@@ -349,6 +385,17 @@ struct bvc_scene_s {
         silP.upload(hsp.data(), hsp.size());
         silN.upload(hsn.data(), hsn.size());
         silAlways.upload(hsa.data(), hsa.size());
+        if (build_on_gpu()) {
+            std::vector<int> hcls(host.ns);
+            std::vector<int2> hsl(host.ns);
+            for (int i = 0; i < host.ns; ++i) {
+                hcls[i] = bvc_host::primClass(host, i);
+                hsl[i] = make_int2(host.segSil[2 * i], host.segSil[2 * i + 1]);
+            }
+            cls.upload(hcls.data(), hcls.size());
+            segSilD.upload(hsl.data(), hsl.size());
+            gpu_build(2, segAB.p, nullptr, nullptr, segSilD.p);
+        }
         std::vector<double> hc(host.ns);
         std::vector<int> hid(host.ns);
         double run = 0.0;

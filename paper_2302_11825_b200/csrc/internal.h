@@ -117,6 +117,11 @@ void launch_inside(const SceneView2& S, const double* x, int n, float tol, uint8
 
 // kernel-launch accounting (bench gpu_launches)
 void count_launch(int n = 1);
+// GPU linear BVH build (lbvh.cu): nodes in Node2/Node3 format, primitives in leaf
+// order; returns the tree height, or -1 if n <= leafSize
+int build_lbvh(int dim, const float4* a, const float4* b, const float4* c, const int* cls, const int2* sil, int n,
+               int leafSize, const double* lo, const double* hi, double pad, int classFirst, void* nodesOut,
+               void* primsOut, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // 3D (triangle meshes; walk3.cu)

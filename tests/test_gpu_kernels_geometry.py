@@ -94,3 +94,46 @@ def test_bvh_queries_vs_reference(golden, k):
     _, dany, _, _ = sc.closest_point(q, abi.FILTER_ANY)
     clear = dany > 1e-5
     assert np.array_equal(ins[clear], g[f"s{k}_inside"][clear])
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_gpu_built_bvh_queries_vs_reference(golden, k, monkeypatch):
+    """The device-built linear BVH (lbvh.cu, BVC_BVH=gpu) answers the same queries."""
+    monkeypatch.setenv("BVC_BVH", "gpu")
+    g = golden("geometry")
+    v, s, lab = g[f"s{k}_v"], g[f"s{k}_s"], g[f"s{k}_lab"]
+    reps = max(1, 80 // len(s))  # above the 64-primitive threshold of the device build
+    sc = B.Scene(np.concatenate([v + 10.0 * r for r in range(reps)]),
+                 np.concatenate([s + len(v) * r for r in range(reps)]), np.tile(lab, reps))
+    q, d = g[f"s{k}_q"], g[f"s{k}_d"]
+    tol = 2e-6 * B.Scene(v, s, lab).diagonal
+    for filt in (abi.FILTER_ANY, abi.FILTER_DIRICHLET, abi.FILTER_NEUMANN):
+        _, dist, _, _ = sc.closest_point(q, filt)
+        np.testing.assert_allclose(dist, g[f"s{k}_cp{filt}_dist"], atol=tol, rtol=0)
+    sil = sc.silhouette_distance(q)
+    ref = g[f"s{k}_sil"]
+    fin = np.isfinite(ref)
+    np.testing.assert_allclose(sil[fin], ref[fin], atol=tol)
+    ins = sc.inside(q)
+    _, dany, _, _ = sc.closest_point(q, abi.FILTER_ANY)
+    clear = dany > 1e-5
+    assert np.array_equal(ins[clear], g[f"s{k}_inside"][clear])
+
+
+def test_gpu_built_bvh_gives_the_same_cache(monkeypatch):
+    """Walks are tree-independent (exact nearest queries): host SAH and device LBVH trees
+    give the same boundary cache up to closest-point ties."""
+    from paper_2302_11825_b200 import configs
+
+    c = configs.config2(scale=1 / 16)
+    caches = []
+    for mode in ("host", "gpu"):
+        if mode == "gpu":
+            monkeypatch.setenv("BVC_BVH", "gpu")
+        sc = B.Scene(c.vertices, c.segments, c.labels)
+        region = B.SolveRegion(sc, offset=c.region_offset, epsilon=c.epsilon)
+        caches.append(B.generate_boundary_cache(sc, c.problem, region, c.cache, 3, 0).download())
+    a, b = caches
+    assert np.array_equal(a["z"], b["z"])
+    same = np.mean(a["uHat"] == b["uHat"])
+    assert same > 0.99, same
