@@ -346,11 +346,14 @@ class EvaluationPoints:
     def reset(self):
         _check(lib().bvc_points_reset(self.h))
 
-    def read_solution(self, gradient=True):
+    def read_solution(self, gradient=True, out=None):
         """u (and grad u) computed on the device (EvaluationPoint::solution/gradient, cache.h:91-105);
-        only these arrays cross to the host."""
-        u = np.zeros(self.n)
-        g = np.zeros((self.n, self.dim)) if gradient else None
+        only these arrays cross to the host. `out` = (u, grad) host arrays to fill (e.g. pinned)."""
+        if out is not None:
+            u, g = out
+        else:
+            u = np.zeros(self.n)
+            g = np.zeros((self.n, self.dim)) if gradient else None
         _check(lib().bvc_points_solution(self.h, _ptr(u), _ptr(g) if g is not None else None))
         return (u, g) if gradient else u
 

@@ -126,7 +126,7 @@ enum Slot {
     kWsSortKeysIn, kWsSortKeysOut, kWsSortValsIn, kWsSortTemp, kWsMean, kWsSe, kWsTruncPt, kWsHost1, kWsRegion,
     kWsMean2, kWsSe2, kWsGidU, kWsSrcTmp, kWsSrcFlag, kWsEvalIn, kWsEvalOut, kWsTileBox, kWsUnitCtr,
     kWsCorrCounts, kWsCorrOffsets, kWsCorrStarts, kWsCorrGid, kWsCorrW, kWsCorrOut, kWsCorrMean, kWsCorrScan,
-    kWsCorrFlag, kWsBallRs, kWsHull, kWsXs64
+    kWsCorrFlag, kWsBallRs, kWsHull, kWsXs64, kWsBounds, kWsFlag2
 };
 
 int fail(const std::exception& e) {
@@ -454,7 +454,6 @@ struct bvc_source_cache_s {
 struct bvc_eval_points_s {
     size_t n = 0;
     int dim = 2;
-    std::vector<double> hx;
     DevBuf<double> x;
     DevBuf<uint8_t> fallback, unreliable;
     DevBuf<double> bsum, ssum, bgsum, sgsum, walkSum, gwalkSum;
@@ -475,10 +474,43 @@ struct bvc_eval_points_s {
 
 namespace {
 
-__global__ void morton_keys_kernel(const double* x, const uint8_t* fb, int n, int dim, double lo0, double lo1,
-                                   double lo2, double inv, unsigned* keys, int* vals) {
+// order-preserving map of a double to an unsigned 64-bit key (for atomicMin/Max)
+__device__ __forceinline__ unsigned long long dkey(double v) {
+    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double dval(unsigned long long k) {
+    return __longlong_as_double(static_cast<long long>((k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k));
+}
+// bounding box of the points: keys[0..2] = min, [3..5] = max (initialised by the host)
+__global__ void bounds_kernel(const double* x, int n, int dim, unsigned long long* keys) {
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        for (int d = 0; d < dim; ++d) {
+            double v = x[static_cast<size_t>(dim) * i + d];
+            lo[d] = fmin(lo[d], v);
+            hi[d] = fmax(hi[d], v);
+        }
+    for (int d = 0; d < dim; ++d)
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+            hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+        }
+    if ((threadIdx.x & 31) == 0)
+        for (int d = 0; d < dim; ++d) {
+            atomicMin(keys + d, dkey(lo[d]));
+            atomicMax(keys + 3 + d, dkey(hi[d]));
+        }
+}
+
+__global__ void morton_keys_kernel(const double* x, const uint8_t* fb, int n, int dim,
+                                   const unsigned long long* bounds, unsigned* keys, int* vals) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    double lo0 = dval(bounds[0]), lo1 = dval(bounds[1]), lo2 = dim == 3 ? dval(bounds[2]) : 0.0;
+    double ext = 0.0;
+    for (int d = 0; d < dim; ++d) ext = fmax(ext, dval(bounds[3 + d]) - dval(bounds[d]));
+    double inv = ext > 0 ? 1.0 / ext : 1.0;
     auto spread2 = [](unsigned v) {  // 15 bits -> every other bit
         v &= 0x7fff;
         v = (v | (v << 8)) & 0x00ff00ff;
@@ -527,21 +559,16 @@ void ensure_order(bvc_eval_points_s* P) {
         P->orderValid = true;
         return;
     }
-    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-    for (int i = 0; i < n; ++i)
-        for (int d = 0; d < P->dim; ++d) {
-            lo[d] = std::min(lo[d], P->hx[P->dim * i + d]);
-            hi[d] = std::max(hi[d], P->hx[P->dim * i + d]);
-        }
-    double ext = 0.0;
-    for (int d = 0; d < P->dim; ++d) ext = std::max(ext, hi[d] - lo[d]);
-    double inv = ext > 0 ? 1.0 / ext : 1.0;
+    // bounding box on the device (no host copy of the points is kept)
+    unsigned long long* bk = ws().get<unsigned long long>(kWsBounds, 6);
+    const unsigned long long init[6] = {~0ULL, ~0ULL, ~0ULL, 0ULL, 0ULL, 0ULL};
+    CK(cudaMemcpyAsync(bk, init, sizeof(init), cudaMemcpyHostToDevice, g_stream));
+    bounds_kernel<<<std::min((n + 255) / 256, 1184), 256, 0, g_stream>>>(P->x.p, n, P->dim, bk);
     unsigned* kin = ws().get<unsigned>(kWsSortKeysIn, n);
     unsigned* kout = ws().get<unsigned>(kWsSortKeysOut, n);
     int* vin = ws().get<int>(kWsSortValsIn, n);
-    morton_keys_kernel<<<(n + 255) / 256, 256, 0, g_stream>>>(P->x.p, P->fallback.p, n, P->dim, lo[0], lo[1],
-                                                              P->dim == 3 ? lo[2] : 0.0, inv, kin, vin);
-    count_launch();
+    morton_keys_kernel<<<(n + 255) / 256, 256, 0, g_stream>>>(P->x.p, P->fallback.p, n, P->dim, bk, kin, vin);
+    count_launch(2);
     size_t tmp = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, P->order.p, n, 0, 32, g_stream));
     void* t = ws().get<char>(kWsSortTemp, tmp);
@@ -1404,6 +1431,11 @@ __global__ void fallback_accumulate_kernel(const int* idx, int n, const double* 
     }
 }
 
+__global__ void first_ball_radius_kernel(const double* dist, int n, float rmin, float* r) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) r[i] = static_cast<float>(fmax(dist[i], static_cast<double>(rmin)));
+}
+
 __global__ void gather_fallback_kernel(const int* idx, int n, const double* x, float2* out, long long* gid) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
@@ -1524,13 +1556,7 @@ void fallback_walks(bvc_scene_s* S, const bvc_problem& pb, const bvc_cache_confi
     if (S->host.closed()) {  // requireInterior
         WalkEnv E0 = make_env(S, pb, cfg.walk, seed, kFallbackSalt, round);
         double* xd = ws().get<double>(kWsEvalIn, 2 * static_cast<size_t>(nf));
-        // positions of fallback points in double
-        std::vector<int> hidx(nf);
-        CK(cudaMemcpyAsync(hidx.data(), idx, nf * sizeof(int), cudaMemcpyDeviceToHost, g_stream));
-        CK(cudaStreamSynchronize(g_stream));
-        std::vector<double> hx(2 * static_cast<size_t>(nf));
-        for (int j = 0; j < nf; ++j) { hx[2 * j] = P->hx[2 * hidx[j]]; hx[2 * j + 1] = P->hx[2 * hidx[j] + 1]; }
-        CK(cudaMemcpyAsync(xd, hx.data(), hx.size() * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        gather_points64(P->x.p, idx, nf, 2, xd, g_stream);  // positions of the fallback points
         uint8_t* ins = ws().get<uint8_t>(kWsOutside, nf);
         launch_inside(E0.S, xd, nf, E0.insideTol, ins, g_stream);
         std::vector<uint8_t> h(nf);
@@ -1559,24 +1585,15 @@ void fallback_walks(bvc_scene_s* S, const bvc_problem& pb, const bvc_cache_confi
     if (gradients) {
         WalkEnv Eg = make_env(S, pb, cfg.walk, seed, kFallbackGradSalt, round);
         double* xd = ws().get<double>(kWsEvalIn, 2 * static_cast<size_t>(nf));
-        std::vector<int> hidx(nf);
-        CK(cudaMemcpyAsync(hidx.data(), idx, nf * sizeof(int), cudaMemcpyDeviceToHost, g_stream));
-        CK(cudaStreamSynchronize(g_stream));
-        std::vector<double> hx(2 * static_cast<size_t>(nf));
-        for (int j = 0; j < nf; ++j) { hx[2 * j] = P->hx[2 * hidx[j]]; hx[2 * j + 1] = P->hx[2 * hidx[j] + 1]; }
-        CK(cudaMemcpyAsync(xd, hx.data(), hx.size() * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        gather_points64(P->x.p, idx, nf, 2, xd, g_stream);
         double* cpp = ws().get<double>(kWsEvalOut, 2 * static_cast<size_t>(nf));
         double* cpd = ws().get<double>(kWsMean2, nf);
         int* cps = ws().get<int>(kWsSkipB, nf);
         double* cpt = ws().get<double>(kWsSe2, nf);
         launch_closest(Eg.S, xd, nf, bvc_dev::kClsAny, cpp, cpd, cps, cpt, g_stream);
-        std::vector<double> hd(nf);
-        CK(cudaMemcpyAsync(hd.data(), cpd, nf * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
-        CK(cudaStreamSynchronize(g_stream));
-        std::vector<float> hr(nf);
-        for (int j = 0; j < nf; ++j) hr[j] = static_cast<float>(std::max(hd[j], static_cast<double>(Eg.rmin)));
         float* rD = ws().get<float>(kWsRD, nf);
-        CK(cudaMemcpyAsync(rD, hr.data(), nf * sizeof(float), cudaMemcpyHostToDevice, g_stream));
+        first_ball_radius_kernel<<<(nf + 127) / 128, 128, 0, g_stream>>>(cpd, nf, Eg.rmin, rD);  // pointwise.cpp:217-221
+        count_launch();
         CK(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), g_stream));
         WalkJob G{};
         G.counter = ctr;
@@ -1710,9 +1727,8 @@ std::unique_ptr<bvc_eval_points_s> make_points(const double* x, size_t n, int di
     auto P = std::make_unique<bvc_eval_points_s>();
     P->n = n;
     P->dim = dim;
-    P->hx.assign(x, x + dim * n);
     alloc_points(P.get());
-    P->x.upload(P->hx.data(), dim * n);
+    P->x.upload(x, dim * n);
     zero_points(P.get());
     return P;
 }
@@ -2032,10 +2048,10 @@ int bvc_points_create(const double* x, size_t n, int dim, bvc_eval_points* out) 
         auto P = std::make_unique<bvc_eval_points_s>();
         P->n = n;
         P->dim = dim;
-        P->hx.assign(x, x + dim * n);
         alloc_points(P.get());
-        P->x.upload(P->hx.data(), dim * n);
+        P->x.upload(x, dim * n);
         zero_points(P.get());
+        CK(cudaStreamSynchronize(g_stream));  // x is read before the call returns (pinned x copies async)
         *out = P.release();
     })
 }
@@ -2060,7 +2076,7 @@ int bvc_points_download(bvc_eval_points p, bvc_point_state* h) {
         int d = p->dim;
         h->count = n;
         h->dim = d;
-        if (h->x) std::copy(p->hx.begin(), p->hx.end(), h->x);
+        if (h->x) p->x.download(h->x, static_cast<size_t>(d) * n);
         if (h->fallback) p->fallback.download(h->fallback, n);
         if (h->gradientUnreliable) p->unreliable.download(h->gradientUnreliable, n);
         if (h->boundarySum) p->bsum.download(h->boundarySum, n);
