@@ -2060,8 +2060,6 @@ int bvc_points_reset(bvc_eval_points p) {
     API({
         require_device();
         need(p, "null points");
-        uint8_t* keepF = nullptr;
-        (void)keepF;
         // keep the classification, zero the running sums
         p->bsum.zero(); p->ssum.zero(); p->bgsum.zero(); p->sgsum.zero(); p->walkSum.zero(); p->gwalkSum.zero();
         p->nb.zero(); p->ms.zero(); p->nbg.zero(); p->msg.zero(); p->walkCount.zero(); p->walkTrunc.zero();

@@ -124,7 +124,6 @@ __device__ float neumann_term(const WalkEnv& E, float x, float y, float R, float
     if (total <= 0.0f) return 0.0f;
     float target = u * total, run = 0.0f;
     float bx = x, by = y;
-    int bseg = -1;
     bool done = false;
     traverse_near(
         S, x, y, kClsNeumann,
@@ -138,7 +137,6 @@ __device__ float neumann_term(const WalkEnv& E, float x, float y, float R, float
             float t = t0 + (t1 - t0) * local;
             bx = p.seg.x + t * ux;
             by = p.seg.y + t * uy;
-            bseg = p.id;
             if (target <= run + len) done = true;
             run += len;
         },
@@ -146,7 +144,6 @@ __device__ float neumann_term(const WalkEnv& E, float x, float y, float R, float
     float dx = bx - x, dy = by - y;
     float r = fminf(fmaxf(sqrtf(dx * dx + dy * dy), 1e-12f * E.scale), R);
     float hv = field_eval(E.P.h, bx, by);
-    (void)bseg;
     float gb = E.P.screened ? ball_greens_screened(E.P.sqrtSigma, R, r) : ball_greens_poisson(R, r);
     return -gb * hv * total;
 }
