@@ -99,8 +99,7 @@ __device__ __forceinline__ float tri_closest(const Prim3& t, float px, float py,
 template <bool COUNT = false, class Visit, class Thr>
 __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, float y, float z, unsigned qmask,
                                                Visit&& visit, Thr&& threshold) {
-    int stackRef[kStack];
-    float stackD[kStack];
+    unsigned long long stack[kStack];  // (distance bits << 32 | ref): one local load per pop
     int sp = 0, ref = 0;
     for (;;) {
         if (ref >= 0) {
@@ -112,9 +111,8 @@ __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, flo
             bool vl = dl <= thr, vr = dr <= thr;
             if (vl && vr) {
                 bool lfirst = dl <= dr;
-                stackRef[sp] = lfirst ? nd.right : nd.left;
-                stackD[sp] = fmaxf(dl, dr);
-                ++sp;
+                stack[sp++] = (static_cast<unsigned long long>(__float_as_uint(fmaxf(dl, dr))) << 32) |
+                              static_cast<unsigned>(lfirst ? nd.right : nd.left);
                 ref = lfirst ? nd.left : nd.right;
                 continue;
             }
@@ -131,10 +129,12 @@ __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, flo
         }
         for (;;) {
             if (sp == 0) return;
-            --sp;
-            if (stackD[sp] <= threshold()) break;
+            unsigned long long e = stack[--sp];
+            if (__uint_as_float(static_cast<unsigned>(e >> 32)) <= threshold()) {
+                ref = static_cast<int>(static_cast<unsigned>(e));
+                break;
+            }
         }
-        ref = stackRef[sp];
     }
 }
 

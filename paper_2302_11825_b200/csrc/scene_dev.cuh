@@ -82,8 +82,8 @@ constexpr unsigned kClsNeumann = kClsN | kClsSil, kClsAny = kClsD | kClsN | kCls
 template <bool COUNT = false, class Visit, class Thr>
 __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, float y, unsigned qmask, Visit&& visit,
                                               Thr&& threshold) {
-    int stackRef[kStack];
-    float stackD[kStack];
+    // (distance bits << 32 | ref) per entry: one local load per pop
+    unsigned long long stack[kStack];
     int sp = 0;
     int ref = 0;
     for (;;) {
@@ -97,9 +97,8 @@ __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, floa
             if (vl && vr) {
                 int nearRef = dl <= dr ? nd.left : nd.right;
                 int farRef = dl <= dr ? nd.right : nd.left;
-                stackRef[sp] = farRef;
-                stackD[sp] = fmaxf(dl, dr);
-                ++sp;
+                stack[sp++] = (static_cast<unsigned long long>(__float_as_uint(fmaxf(dl, dr))) << 32) |
+                              static_cast<unsigned>(farRef);
                 ref = nearRef;
                 continue;
             }
@@ -117,10 +116,12 @@ __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, floa
         // pop, skipping entries pruned since they were pushed
         for (;;) {
             if (sp == 0) return;
-            --sp;
-            if (stackD[sp] <= threshold()) break;
+            unsigned long long e = stack[--sp];
+            if (__uint_as_float(static_cast<unsigned>(e >> 32)) <= threshold()) {
+                ref = static_cast<int>(static_cast<unsigned>(e));
+                break;
+            }
         }
-        ref = stackRef[sp];
     }
 }
 
