@@ -252,7 +252,7 @@ template <bool COUNT = false>
 __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, float oy, float dx, float dy,
                                                 float tMax, unsigned qmask, float tMin, int skipSeg) {
     RayHit h{kFInf, 0.0f, 0.0f, 0.0f, -1};
-    float idx = 1.0f / dx, idy = 1.0f / dy;
+    float idx = f_rcp(dx), idy = f_rcp(dy);  // slab tests on padded boxes: an approximate reciprocal suffices
     float limit = tMax;
     int stack[kStack];
     int sp = 0, ref = 0;

@@ -82,7 +82,7 @@ template <bool COUNT>
 __device__ __forceinline__ Hit3 ray_neumann3(const WalkEnv3& E, float ox, float oy, float oz, float dx, float dy,
                                              float dz, float tMax, int skip) {
     Hit3 h{kFInf, -1};
-    float idx = 1.0f / dx, idy = 1.0f / dy, idz = 1.0f / dz;
+    float idx = f_rcp(dx), idy = f_rcp(dy), idz = f_rcp(dz);  // slab tests on padded boxes
     float limit = tMax;
     int stack[kStack];
     int sp = 0, ref = 0;
