@@ -19,7 +19,7 @@ LIB = os.path.join(OUT, "libbvc_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
-SOURCES = ["capi.cu", "walk.cu", "walk3.cu", "gather.cu", "gather64.cu", "correct.cu", "probe.cu", "lbvh.cu", "host_scene.cpp", "io.cpp"]
+SOURCES = ["capi.cu", "walk.cu", "walk3.cu", "gather.cu", "gather64.cu", "correct.cu", "probe.cu", "lbvh.cu", "sahbvh.cu", "host_scene.cpp", "io.cpp"]
 HEADERS = ["device_math.cuh", "scene_dev.cuh", "scene3_dev.cuh", "internal.h", "gather.h", "host_scene.h"]
 
 

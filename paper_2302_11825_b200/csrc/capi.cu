@@ -225,25 +225,40 @@ struct bvc_scene_s {
     DevBuf<int2> segSilD;
     int bvhHeight = 0;
 
-    // BVC_BVH=gpu builds the BVH on the device (linear BVH, lbvh.cu); the default is
-    // the host binned-SAH build, whose trees measured faster to walk
-    bool build_on_gpu() const {
+    // BVH builder: "sah" = binned SAH on the device (sahbvh.cu; the default for 3D and
+    // 2D scenes of >= 4096 segments), "lbvh" = linear BVH on the device (lbvh.cu),
+    // "host" = the host builder (host_scene.cpp; the default for small 2D scenes,
+    // median splits). BVC_BVH overrides the choice.
+    std::string builder() const {
         const char* e = std::getenv("BVC_BVH");
-        return e && std::string(e) == "gpu" && host.ns > 64;  // tiny scenes: one host pass
+        std::string v = e ? e : "";
+        if (v == "gpu") v = "lbvh";
+        if (v != "sah" && v != "lbvh" && v != "host") v = (host.dim == 3 || host.ns >= 4096) ? "sah" : "host";
+        return host.ns > 64 ? v : "host";  // tiny scenes: one host pass
     }
+    bool build_on_gpu() const { return builder() != "host"; }
     void gpu_build(int dim, const float4* a, const float4* b, const float4* c, const int2* sil) {
         int n = host.ns, leaf = leaf_size(dim, n);
         double pad = 9.5367431640625e-7 * std::max(host.diagonal, 1e-30);
         size_t nn = static_cast<size_t>(std::max(n - 1, 1));
         if (dim == 2) { nodes.resize(nn); prims.resize(std::max(n, 1)); }
         else { nodes3.resize(nn); prims3.resize(std::max(n, 1)); }
-        int h = n > leaf ? build_lbvh(dim, a, b, c, cls.p, sil, n, leaf, host.lo, host.hi, pad, dim == 2 ? 1 : 0,
-                                      dim == 2 ? static_cast<void*>(nodes.p) : static_cast<void*>(nodes3.p),
-                                      dim == 2 ? static_cast<void*>(prims.p) : static_cast<void*>(prims3.p), g_stream)
-                         : -1;
+        void* nodesOut = dim == 2 ? static_cast<void*>(nodes.p) : static_cast<void*>(nodes3.p);
+        void* primsOut = dim == 2 ? static_cast<void*>(prims.p) : static_cast<void*>(prims3.p);
+        int h;
+        if (builder() == "lbvh") {
+            h = build_lbvh(dim, a, b, c, cls.p, sil, n, leaf, host.lo, host.hi, pad, dim == 2 ? 1 : 0, nodesOut,
+                           primsOut, g_stream);
+        } else {
+            DevBuf<int> ids;
+            ids.resize(n);
+            h = build_sah_gpu(dim, a, b, c, cls.p, n, leaf, pad, dim == 2 ? 1 : 0, nodesOut, ids.p, g_stream);
+            launch_leaf_prims(dim, a, b, c, cls.p, sil, ids.p, n, primsOut, g_stream);
+            CK(cudaStreamSynchronize(g_stream));
+        }
         CK(cudaGetLastError());
-        if (h < 0 || h >= 47)  // deeper than the device traversal stack (degenerate Morton keys)
-            throw Error(BVC_ERR_SOLVER, "GPU BVH build: tree deeper than the traversal stack; use the host build");
+        if (h < 0 || h >= 47)  // deeper than the device traversal stack
+            throw Error(BVC_ERR_SOLVER, "GPU BVH build: tree deeper than the traversal stack; use BVC_BVH=host");
         bvhHeight = h;
     }
 

@@ -122,6 +122,12 @@ void count_launch(int n = 1);
 int build_lbvh(int dim, const float4* a, const float4* b, const float4* c, const int* cls, const int2* sil, int n,
                int leafSize, const double* lo, const double* hi, double pad, int classFirst, void* nodesOut,
                void* primsOut, cudaStream_t st);
+// GPU binned-SAH build (sahbvh.cu): nodes plus the leaf order of the ids; returns the
+// number of levels, or -1 if n <= leafSize
+int build_sah_gpu(int dim, const float4* a, const float4* b, const float4* c, const int* cls, int n, int leafSize,
+                  double pad, int classFirst, void* nodesOut, int* idsOut, cudaStream_t st);
+void launch_leaf_prims(int dim, const float4* a, const float4* b, const float4* c, const int* cls, const int2* sil,
+                       const int* ids, int n, void* primsOut, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // 3D (triangle meshes; walk3.cu)

@@ -309,4 +309,13 @@ int build_lbvh(int dim, const float4* a, const float4* b, const float4* c, const
     return height;
 }
 
+// primitives in leaf order from a permutation of ids (shared with sahbvh.cu)
+void launch_leaf_prims(int dim, const float4* a, const float4* b, const float4* c, const int* cls, const int2* sil,
+                       const int* ids, int n, void* primsOut, cudaStream_t st) {
+    PrimIn in{a, b, c, cls, sil, dim};
+    if (dim == 2) prims2_kernel<<<blocks(n, 256), 256, 0, st>>>(in, ids, n, static_cast<Prim2*>(primsOut));
+    else prims3_kernel<<<blocks(n, 256), 256, 0, st>>>(in, ids, n, static_cast<Prim3*>(primsOut));
+    count_launch();
+}
+
 }  // namespace bvc_impl

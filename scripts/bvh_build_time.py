@@ -1,4 +1,4 @@
-"""Scene BVH build time, host SAH vs GPU LBVH (BVC_BVH=gpu), per config."""
+"""Scene BVH build time per builder (BVC_BVH = host | sah | lbvh), per config."""
 import os
 import sys
 import time
@@ -11,11 +11,8 @@ from paper_2302_11825_b200 import configs  # noqa: E402
 
 for cid in (2, 3, 4, 5):
     c = getattr(configs, f"config{cid}")()
-    for mode in ("host", "gpu"):
-        if mode == "gpu":
-            os.environ["BVC_BVH"] = "gpu"
-        else:
-            os.environ.pop("BVC_BVH", None)
+    for mode in ("host", "sah", "lbvh"):
+        os.environ["BVC_BVH"] = mode
         dim = c.extra.get("dim", 2) if c.extra else 2
         if dim == 2:
             sc = B.Scene(c.vertices, c.segments, c.labels)

@@ -96,10 +96,11 @@ def test_bvh_queries_vs_reference(golden, k):
     assert np.array_equal(ins[clear], g[f"s{k}_inside"][clear])
 
 
+@pytest.mark.parametrize("builder", ["lbvh", "sah"])
 @pytest.mark.parametrize("k", [0, 1, 2])
-def test_gpu_built_bvh_queries_vs_reference(golden, k, monkeypatch):
-    """The device-built linear BVH (lbvh.cu, BVC_BVH=gpu) answers the same queries."""
-    monkeypatch.setenv("BVC_BVH", "gpu")
+def test_gpu_built_bvh_queries_vs_reference(golden, k, builder, monkeypatch):
+    """The device-built trees (lbvh.cu linear BVH, sahbvh.cu binned SAH) answer the same queries."""
+    monkeypatch.setenv("BVC_BVH", builder)
     g = golden("geometry")
     v, s, lab = g[f"s{k}_v"], g[f"s{k}_s"], g[f"s{k}_lab"]
     reps = max(1, 80 // len(s))  # above the 64-primitive threshold of the device build
@@ -120,16 +121,16 @@ def test_gpu_built_bvh_queries_vs_reference(golden, k, monkeypatch):
     assert np.array_equal(ins[clear], g[f"s{k}_inside"][clear])
 
 
-def test_gpu_built_bvh_gives_the_same_cache(monkeypatch):
-    """Walks are tree-independent (exact nearest queries): host SAH and device LBVH trees
+@pytest.mark.parametrize("builder", ["lbvh", "sah"])
+def test_gpu_built_bvh_gives_the_same_cache(builder, monkeypatch):
+    """Walks are tree-independent (exact nearest queries): host and device-built trees
     give the same boundary cache up to closest-point ties."""
     from paper_2302_11825_b200 import configs
 
     c = configs.config2(scale=1 / 16)
     caches = []
-    for mode in ("host", "gpu"):
-        if mode == "gpu":
-            monkeypatch.setenv("BVC_BVH", "gpu")
+    for mode in ("host", builder):
+        monkeypatch.setenv("BVC_BVH", mode)
         sc = B.Scene(c.vertices, c.segments, c.labels)
         region = B.SolveRegion(sc, offset=c.region_offset, epsilon=c.epsilon)
         caches.append(B.generate_boundary_cache(sc, c.problem, region, c.cache, 3, 0).download())
