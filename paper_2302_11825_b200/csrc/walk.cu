@@ -45,16 +45,18 @@ __device__ __forceinline__ float ball_sphere_weight(float s, float R, float rHit
 __device__ __forceinline__ float invert_ball_cdf(float u) {
     if (u <= 0.0f) return 1e-8f;
     if (u >= 1.0f) return 1.0f;
-    float lo = 0.0f, hi = 1.0f, t = sqrtf(u);
+    // start near the root: F ~ 1 - 2 (1 - t)^2 at t -> 1 (double root of F - 1),
+    // sqrt(u) elsewhere; safeguarded Newton with the SFU log
+    float lo = 0.0f, hi = 1.0f, t = u > 0.9f ? 1.0f - sqrtf(0.5f * (1.0f - u)) : sqrtf(u);
 #pragma unroll 1
     for (int it = 0; it < 16; ++it) {
-        float lt = logf(t);
+        float lt = f_ln(t);
         float fv = t * t * (1.0f - 2.0f * lt) - u;
         if (fv > 0.0f) hi = t; else lo = t;
         float der = -4.0f * t * lt;
-        float nxt = der != 0.0f ? t - fv / der : 0.5f * (lo + hi);
+        float nxt = der != 0.0f ? t - __fdividef(fv, der) : 0.5f * (lo + hi);
         if (!(nxt > lo && nxt < hi)) nxt = 0.5f * (lo + hi);
-        if (fabsf(nxt - t) < 1e-7f) return nxt;
+        if (fabsf(nxt - t) < 2e-7f) return nxt;
         t = nxt;
     }
     return t;
