@@ -1695,14 +1695,16 @@ __global__ void mark_kernel(const bvc_dev::SceneView2 scene, const bvc_dev::Scen
     if (i >= n) return;
     float px = static_cast<float>(x[2 * i]), py = static_cast<float>(x[2 * i + 1]);
     // fallbackBand cache.cpp:131-135: whole-domain points within l of the Dirichlet boundary
+    // both tests only ask "closer than l": queries bounded by l prune everything farther
+    const float l2 = offset * offset;
     uint8_t f = 0;
     if (whole) {
-        bvc_dev::Closest c = bvc_dev::closest_point(scene, px, py, bvc_dev::kClsD);
-        f = (c.seg >= 0 && c.d2 < offset * offset) ? 1 : 0;
+        bvc_dev::Closest c = bvc_dev::closest_point(scene, px, py, bvc_dev::kClsD, l2);
+        f = c.seg >= 0 ? 1 : 0;
     }
-    bvc_dev::Closest r = bvc_dev::closest_point(region, px, py, bvc_dev::kClsAny);
+    bvc_dev::Closest r = bvc_dev::closest_point(region, px, py, bvc_dev::kClsAny, l2);
     fb[i] = f;
-    gu[i] = (r.seg >= 0 && r.d2 < offset * offset) ? 1 : 0;
+    gu[i] = r.seg >= 0 ? 1 : 0;
 }
 
 

@@ -467,15 +467,16 @@ __global__ void mark3_kernel(const SceneView3 scene, const SceneView3 region, co
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float px = static_cast<float>(x[3 * i]), py = static_cast<float>(x[3 * i + 1]), pz = static_cast<float>(x[3 * i + 2]);
+    const float l2 = offset * offset;  // bounded queries: only "closer than l" matters
     uint8_t f = 0;
     if (whole) {
-        Closest3 c = closest_point3(scene, px, py, pz, kClsD);
-        f = (c.tri >= 0 && c.d2 < offset * offset) ? 1 : 0;
+        Closest3 c = closest_point3(scene, px, py, pz, kClsD, l2);
+        f = c.tri >= 0 ? 1 : 0;
         if (!f && insideTol > 0.f && !inside3(region, px, py, pz, insideTol)) f = 1;
     }
-    Closest3 r = closest_point3(region, px, py, pz, kClsAny);
+    Closest3 r = closest_point3(region, px, py, pz, kClsAny, l2);
     fb[i] = f;
-    gu[i] = (r.tri >= 0 && r.d2 < offset * offset) ? 1 : 0;
+    gu[i] = r.tri >= 0 ? 1 : 0;
 }
 
 inline int blocks(long long n, int t) { return static_cast<int>((n + t - 1) / t); }
