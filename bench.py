@@ -321,7 +321,11 @@ def phase_breakdown(B, c, scene, region, pts, args):
     gather_rate = pairs / t_gather
     dominant = "walk" if t_gen >= t_gather else "gather"
     # measured pipe rates and L2 bandwidth (bvc_pipe_probe) next to the canonical bound
-    pipes = B.pipe_probe()
+    if args.no_probe:  # profiling runs: reuse the committed measurement
+        pipes = json.load(open(os.path.join(ROOT, "profiles", "r1_pipe_peaks.json")))["rates"]
+        pipes = {k: v["per_s"] for k, v in pipes.items()}
+    else:
+        pipes = B.pipe_probe()
     mufu = min(pipes["mufu_lg2"], pipes["mufu_rcp"]) if c.dim == 2 else pipes["mufu_rsq"]
     bound_meas = min(pipes["ffma"] / F, mufu / S)
     extra = {}
@@ -539,6 +543,7 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-probe", action="store_true", help="skip the pipe microbenchmarks (profiling runs)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -126,7 +126,7 @@ enum Slot {
     kWsSortKeysIn, kWsSortKeysOut, kWsSortValsIn, kWsSortTemp, kWsMean, kWsSe, kWsTruncPt, kWsHost1, kWsRegion,
     kWsMean2, kWsSe2, kWsGidU, kWsSrcTmp, kWsSrcFlag, kWsEvalIn, kWsEvalOut, kWsTileBox, kWsUnitCtr,
     kWsCorrCounts, kWsCorrOffsets, kWsCorrStarts, kWsCorrGid, kWsCorrW, kWsCorrOut, kWsCorrMean, kWsCorrScan,
-    kWsCorrFlag, kWsBallRs, kWsHull, kWsXs64, kWsBounds, kWsFlag2
+    kWsCorrFlag, kWsBallRs, kWsHull, kWsXs64, kWsBounds, kWsFlag2, kWsHintU, kWsHintD
 };
 
 int fail(const std::exception& e) {
@@ -220,8 +220,9 @@ struct bvc_scene_s {
     DevBuf<bvc_dev::Prim3> prims3;
     DevBuf<float4> triNormal, triA, triB, triC, sil3A, sil3B, sil3N1, sil3N2;
     DevBuf<int4> triSil;
-    // GPU BVH build inputs (lbvh.cu)
-    DevBuf<int> cls;
+    // per primitive id: class (host_scene.h primClass; also the GPU build input) and,
+    // in 3D, its leaf index (walk warm starts name leaf slots)
+    DevBuf<int> cls, leafOf;
     DevBuf<int2> segSilD;
     int bvhHeight = 0;
 
@@ -321,12 +322,12 @@ struct bvc_scene_s {
         sil3B.upload(eb.data(), ne);
         sil3N1.upload(e1.data(), ne);
         sil3N2.upload(e2.data(), ne);
-        if (build_on_gpu()) {
-            std::vector<int> hcls(host.ns);
-            for (int i = 0; i < host.ns; ++i) hcls[i] = bvc_host::primClass(host, i);
-            cls.upload(hcls.data(), hcls.size());
-            gpu_build(3, triA.p, triB.p, triC.p, nullptr);
-        }
+        std::vector<int> hcls(host.ns);
+        for (int i = 0; i < host.ns; ++i) hcls[i] = bvc_host::primClass(host, i);
+        cls.upload(hcls.data(), hcls.size());
+        if (build_on_gpu()) gpu_build(3, triA.p, triB.p, triC.p, nullptr);
+        leafOf.resize(std::max(host.ns, 1));  // triangle id -> leaf index (walk warm starts)
+        launch_leaf_index(3, prims3.p, host.ns, leafOf.p, g_stream);
         uploaded = true;
     }
     bvc_dev::SceneView3 view3() {
@@ -400,14 +401,12 @@ struct bvc_scene_s {
         silP.upload(hsp.data(), hsp.size());
         silN.upload(hsn.data(), hsn.size());
         silAlways.upload(hsa.data(), hsa.size());
+        std::vector<int> hcls(host.ns);
+        for (int i = 0; i < host.ns; ++i) hcls[i] = bvc_host::primClass(host, i);
+        cls.upload(hcls.data(), hcls.size());
         if (build_on_gpu()) {
-            std::vector<int> hcls(host.ns);
             std::vector<int2> hsl(host.ns);
-            for (int i = 0; i < host.ns; ++i) {
-                hcls[i] = bvc_host::primClass(host, i);
-                hsl[i] = make_int2(host.segSil[2 * i], host.segSil[2 * i + 1]);
-            }
-            cls.upload(hcls.data(), hcls.size());
+            for (int i = 0; i < host.ns; ++i) hsl[i] = make_int2(host.segSil[2 * i], host.segSil[2 * i + 1]);
             segSilD.upload(hsl.data(), hsl.size());
             gpu_build(2, segAB.p, nullptr, nullptr, segSilD.p);
         }
@@ -664,7 +663,12 @@ void run_cache_walks(bvc_scene_s* S, bvc_region_s* R, const WalkEnv& E, const bv
     long long* gidD = ws().get<long long>(kWsGidD, std::max(nD, 1));
     launch_gather_dpoints(samples, dIdx, nD, gradR, gidBase, gid, xD, nrmD, rD, gidD, g_stream);
     int nU = std::max(1, cfg.nWalksNeumann), nDw = std::max(1, cfg.nWalksDirichlet);
+    int* hintU = ws().get<int>(kWsHintU, std::max(n, 1));
+    int* hintD = ws().get<int>(kWsHintD, std::max(nD, 1));
+    launch_start_hints(samples, n, R->source.p, S->cls.p, nullptr, dIdx, nD, hintU, hintD, g_stream);
     WalkJob J{};
+    J.hintU = hintU;
+    J.hintD = hintD;
     J.nU = nU;
     J.nPtsU = n;
     J.startU = startU;
@@ -775,7 +779,12 @@ void run_cache_walks3(bvc_scene_s* S, bvc_region_s* R, const WalkEnv3& E, const 
     long long* gidD = ws().get<long long>(kWsGidD, std::max(nD, 1));
     launch_gather_dpoints3(samples, dIdx, nD, gradR, gidBase, gid, xD, nrmD, rD, gidD, g_stream);
     int nU = std::max(1, cfg.nWalksNeumann), nDw = std::max(1, cfg.nWalksDirichlet);
+    int* hintU = ws().get<int>(kWsHintU, std::max(n, 1));
+    int* hintD = ws().get<int>(kWsHintD, std::max(nD, 1));
+    launch_start_hints(samples, n, R->source.p, S->cls.p, S->leafOf.p, dIdx, nD, hintU, hintD, g_stream);
     WalkJob3 J{};
+    J.hintU = hintU;
+    J.hintD = hintD;
     J.nU = nU;
     J.nPtsU = n;
     J.startU = startU;

@@ -56,6 +56,9 @@ struct WalkJob {
     unsigned long long* truncTotal;  // total truncated walks (may be NULL)
     unsigned long long* steps;  // total closest-Dirichlet queries (may be NULL)
     unsigned long long* counter; // work-queue head, zeroed by the launcher
+    // first-step warm starts (may be NULL): a Dirichlet segment id per U / D point
+    const int* hintU;
+    const int* hintD;
 };
 
 void launch_walk_job(const WalkEnv& env, const WalkJob& job, cudaStream_t st);
@@ -126,6 +129,11 @@ int build_lbvh(int dim, const float4* a, const float4* b, const float4* c, const
 // number of levels, or -1 if n <= leafSize
 int build_sah_gpu(int dim, const float4* a, const float4* b, const float4* c, const int* cls, int n, int leafSize,
                   double pad, int classFirst, void* nodesOut, int* idsOut, cudaStream_t st);
+// first-step warm starts for cache walks: the scene primitive a sample's region
+// segment came from, if Dirichlet (its distance seeds the first closest-point query)
+void launch_start_hints(const CacheSample* samples, int n, const int* source, const int* cls, const int* leafOf,
+                        const int* dIdx, int nD, int* hintU, int* hintD, cudaStream_t st);
+void launch_leaf_index(int dim, const void* prims, int n, int* leafOf, cudaStream_t st);
 void launch_leaf_prims(int dim, const float4* a, const float4* b, const float4* c, const int* cls, const int2* sil,
                        const int* ids, int n, void* primsOut, cudaStream_t st);
 
@@ -164,6 +172,9 @@ struct WalkJob3 {
     unsigned long long* truncTotal;
     unsigned long long* steps;
     unsigned long long* counter;
+    // first-step warm starts (may be NULL): leaf index of a Dirichlet triangle per U / D point
+    const int* hintU;
+    const int* hintD;
 };
 
 void launch_walk_job3(const WalkEnv3& env, const WalkJob3& job, cudaStream_t st);

@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(kWalkThreads, NEU ? 4 : 6) walk_kernel(const W
                     t.rid = static_cast<unsigned long long>(g) * J.nU + t.k;
                     float2 s = J.startU[t.pt];
                     walk_start(w, s.x, s.y);
+                    if (J.hintU) w.lastD = J.hintU[t.pt];
                 } else {
                     long long d = id - nUtot;
                     t.role = 1;
@@ -339,6 +340,7 @@ __global__ void __launch_bounds__(kWalkThreads, NEU ? 4 : 6) walk_kernel(const W
                     // the first ball touches the boundary: start a hair inside it
                     float rr = t.R * 0.99999952f;
                     walk_start(w, fmaf(rr, t.dirx, c.x), fmaf(rr, t.diry, c.y));
+                    if (J.hintD) w.lastD = J.hintD[t.pt];
                 }
                 active = true;
             }
@@ -362,6 +364,7 @@ __global__ void __launch_bounds__(kWalkThreads, NEU ? 4 : 6) walk_kernel(const W
                     if (SCR && E.P.sigma > 0.0f) {
                         t.phase = 1;
                         walk_start(w, t.y2x, t.y2y);
+                        if (J.hintD) w.lastD = J.hintD[t.pt];
                     } else {
                         active = false;
                     }
@@ -573,6 +576,27 @@ __global__ void inside_kernel(const SceneView2 S, const double* x, int n, float 
 
 inline int blocks(long long n, int t) { return static_cast<int>((n + t - 1) / t); }
 
+__global__ void start_hints_kernel(const CacheSample* samples, int n, const int* source, const int* cls,
+                                   const int* leafOf, const int* dIdx, int nD, int* hintU, int* hintD) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    auto hint = [&](int k) {
+        int seg = samples[k].segment;
+        int src = source ? (seg >= 0 ? source[seg] : -1) : seg;
+        if (src < 0 || cls[src] != 0) return -1;  // only a Dirichlet primitive may seed the D distance
+        return leafOf ? leafOf[src] : src;
+    };
+    if (i < n) hintU[i] = hint(i);
+    if (i < nD) hintD[i] = hint(dIdx[i]);
+}
+
+__global__ void leaf_index_kernel(int dim, const void* prims, int n, int* leafOf) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int id = dim == 2 ? static_cast<const Prim2*>(prims)[j].id
+                      : __float_as_int(static_cast<const bvc_dev::Prim3*>(prims)[j].a.w);
+    leafOf[id] = j;
+}
+
 }  // namespace
 
 template <bool NEU, bool SCR, bool SRC, bool COUNT>
@@ -586,6 +610,19 @@ void launch_walk_t(const WalkEnv& env, const WalkJob& job, long long total, cuda
     long long want = (total + kWalkThreads - 1) / kWalkThreads;
     int grid = static_cast<int>(want < static_cast<long long>(sms) * perSm ? want : static_cast<long long>(sms) * perSm);
     walk_kernel<NEU, SCR, SRC, COUNT><<<grid, kWalkThreads, 0, st>>>(env, job);
+}
+
+void launch_start_hints(const CacheSample* samples, int n, const int* source, const int* cls, const int* leafOf,
+                        const int* dIdx, int nD, int* hintU, int* hintD, cudaStream_t st) {
+    int m = n > nD ? n : nD;
+    if (m <= 0) return;
+    start_hints_kernel<<<blocks(m, 256), 256, 0, st>>>(samples, n, source, cls, leafOf, dIdx, nD, hintU, hintD);
+    count_launch();
+}
+void launch_leaf_index(int dim, const void* prims, int n, int* leafOf, cudaStream_t st) {
+    if (n <= 0) return;
+    leaf_index_kernel<<<blocks(n, 256), 256, 0, st>>>(dim, prims, n, leafOf);
+    count_launch();
 }
 
 void launch_walk_job(const WalkEnv& env, const WalkJob& job, cudaStream_t st) {

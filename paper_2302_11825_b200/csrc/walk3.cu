@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(kThreads3, 6) walk3_kernel(const WalkEnv3 E, c
                     t.rid = static_cast<unsigned long long>(g) * J.nU + k;
                     float4 s = J.startU[t.pt];
                     walk3_start(w, s.x, s.y, s.z);
+                    if (J.hintU) w.lastD = J.hintU[t.pt];
                 } else {
                     long long d = id - nUtot;
                     t.role = 1;
@@ -316,6 +317,7 @@ __global__ void __launch_bounds__(kThreads3, 6) walk3_kernel(const WalkEnv3 E, c
                     }
                     float rr = t.R * 0.99999952f;
                     walk3_start(w, fmaf(rr, t.dx, c.x), fmaf(rr, t.dy, c.y), fmaf(rr, t.dz, c.z));
+                    if (J.hintD) w.lastD = J.hintD[t.pt];
                 }
                 active = true;
             }
@@ -340,6 +342,7 @@ __global__ void __launch_bounds__(kThreads3, 6) walk3_kernel(const WalkEnv3 E, c
                     if (SCR && E.P.sigma > 0.f) {
                         t.phase = 1;
                         walk3_start(w, t.y2x, t.y2y, t.y2z);
+                        if (J.hintD) w.lastD = J.hintD[t.pt];
                     } else {
                         active = false;
                     }

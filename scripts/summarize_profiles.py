@@ -53,8 +53,8 @@ def summarize(tag):
             lines.append(f"  {k.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')}"
                          f" = {v:.3f}")
         open(os.path.join(ROOT, "profiles", f"{tag}_{name}_ncu.txt"), "w").write("\n".join(lines) + "\n")
-    lpath = os.path.join(ROOT, "gpurun_out", "launches.csv")
-    if os.path.exists(lpath):
+    for lpath in sorted(glob.glob(os.path.join(ROOT, "gpurun_out", "launches*.csv"))):
+        suffix = os.path.basename(lpath)[len("launches"):-len(".csv")]
         text = open(lpath).read()
         start = text.find('"ID"')
         rows = list(csv.reader(io.StringIO(text[start:]))) if start >= 0 else []
@@ -74,10 +74,11 @@ def summarize(tag):
                 per[name] = (c + 1, t + v)
         total = sum(t for _, t in per.values()) or 1.0
         lines = [f"# ncu launch list (gpu__time_duration.sum, cold-cache & serialised: compare SHARES) ({tag})",
-                 f"# command: python bench.py --steps 2 --warmup 1 --no-cpu", "kernel, launches, total_ns, share"]
+                 "# command: scripts/profile.sh (python bench.py --config C --steps 2 --warmup 3 --no-cpu)",
+                 "kernel, launches, total_ns, share"]
         for n, (c, t) in sorted(per.items(), key=lambda kv: -kv[1][1]):
             lines.append(f"{n}, {c}, {t:.0f}, {t / total:.3f}")
-        open(os.path.join(ROOT, "profiles", f"{tag}_launches.txt"), "w").write("\n".join(lines) + "\n")
+        open(os.path.join(ROOT, "profiles", f"{tag}_launches{suffix}.txt"), "w").write("\n".join(lines) + "\n")
 
 
 if __name__ == "__main__":
