@@ -96,13 +96,26 @@ __device__ __forceinline__ float tri_closest(const Prim3& t, float px, float py,
     return dx * dx + dy * dy + dz * dz;
 }
 
+// "while-while" structure (Aila & Laine, HPG 2009): each lane descends inner nodes
+// in one loop and handles leaves in the next, so the warp switches between the two
+// code paths once per leaf instead of once per node visit
 template <bool COUNT = false, class Visit, class Thr>
 __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, float y, float z, unsigned qmask,
                                                Visit&& visit, Thr&& threshold) {
     unsigned long long stack[kStack];  // (distance bits << 32 | ref): one local load per pop
     int sp = 0, ref = 0;
+    auto pop = [&]() -> bool {  // next entry still within the pruning radius; false when empty
+        for (;;) {
+            if (sp == 0) return false;
+            unsigned long long e = stack[--sp];
+            if (__uint_as_float(static_cast<unsigned>(e >> 32)) <= threshold()) {
+                ref = static_cast<int>(static_cast<unsigned>(e));
+                return true;
+            }
+        }
+    };
     for (;;) {
-        if (ref >= 0) {
+        while (ref >= 0) {
             const Node3 nd = S.nodes[ref];
             count_fetch3<COUNT>(S, 0);
             float thr = threshold();
@@ -114,27 +127,22 @@ __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, flo
                 stack[sp++] = (static_cast<unsigned long long>(__float_as_uint(fmaxf(dl, dr))) << 32) |
                               static_cast<unsigned>(lfirst ? nd.right : nd.left);
                 ref = lfirst ? nd.left : nd.right;
-                continue;
-            }
-            if (vl) { ref = nd.left; continue; }
-            if (vr) { ref = nd.right; continue; }
-        } else {
-            int code = ~ref;
-            int start = code >> 3, count = (code & 7) + 1;
-            for (int i = start; i < start + count; ++i) {
-                const Prim3 p = S.prims[i];
-                count_fetch3<COUNT>(S, 1);
-                if ((1u << __float_as_int(p.b.w)) & qmask) visit(p, i);
+            } else if (vl) {
+                ref = nd.left;
+            } else if (vr) {
+                ref = nd.right;
+            } else if (!pop()) {
+                return;
             }
         }
-        for (;;) {
-            if (sp == 0) return;
-            unsigned long long e = stack[--sp];
-            if (__uint_as_float(static_cast<unsigned>(e >> 32)) <= threshold()) {
-                ref = static_cast<int>(static_cast<unsigned>(e));
-                break;
-            }
+        int code = ~ref;
+        int start = code >> 3, count = (code & 7) + 1;
+        for (int i = start; i < start + count; ++i) {
+            const Prim3 p = S.prims[i];
+            count_fetch3<COUNT>(S, 1);
+            if ((1u << __float_as_int(p.b.w)) & qmask) visit(p, i);
         }
+        if (!pop()) return;
     }
 }
 

@@ -78,7 +78,8 @@ constexpr unsigned kClsD = 1u, kClsN = 2u, kClsSil = 4u;
 constexpr unsigned kClsNeumann = kClsN | kClsSil, kClsAny = kClsD | kClsN | kClsSil;
 
 // Generic best-first traversal. visit(prim) handles one primitive of a visited
-// leaf; threshold() returns the current squared pruning radius.
+// leaf; threshold() returns the current squared pruning radius. "While-while"
+// structure (Aila & Laine, HPG 2009): inner nodes in one loop, leaves in the next.
 template <bool COUNT = false, class Visit, class Thr>
 __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, float y, unsigned qmask, Visit&& visit,
                                               Thr&& threshold) {
@@ -86,8 +87,18 @@ __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, floa
     unsigned long long stack[kStack];
     int sp = 0;
     int ref = 0;
+    auto pop = [&]() -> bool {  // next entry still within the pruning radius; false when empty
+        for (;;) {
+            if (sp == 0) return false;
+            unsigned long long e = stack[--sp];
+            if (__uint_as_float(static_cast<unsigned>(e >> 32)) <= threshold()) {
+                ref = static_cast<int>(static_cast<unsigned>(e));
+                return true;
+            }
+        }
+    };
     for (;;) {
-        if (ref >= 0) {
+        while (ref >= 0) {
             const Node2 nd = S.nodes[ref];
             count_fetch<COUNT>(S, 0);
             float thr = threshold();
@@ -100,28 +111,22 @@ __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, floa
                 stack[sp++] = (static_cast<unsigned long long>(__float_as_uint(fmaxf(dl, dr))) << 32) |
                               static_cast<unsigned>(farRef);
                 ref = nearRef;
-                continue;
-            }
-            if (vl) { ref = nd.left; continue; }
-            if (vr) { ref = nd.right; continue; }
-        } else {
-            int code = ~ref;
-            int start = code >> 3, count = (code & 7) + 1;
-            for (int i = start; i < start + count; ++i) {
-                const Prim2 p = S.prims[i];
-                count_fetch<COUNT>(S, 1);
-                if ((1u << p.label) & qmask) visit(p);
+            } else if (vl) {
+                ref = nd.left;
+            } else if (vr) {
+                ref = nd.right;
+            } else if (!pop()) {
+                return;
             }
         }
-        // pop, skipping entries pruned since they were pushed
-        for (;;) {
-            if (sp == 0) return;
-            unsigned long long e = stack[--sp];
-            if (__uint_as_float(static_cast<unsigned>(e >> 32)) <= threshold()) {
-                ref = static_cast<int>(static_cast<unsigned>(e));
-                break;
-            }
+        int code = ~ref;
+        int start = code >> 3, count = (code & 7) + 1;
+        for (int i = start; i < start + count; ++i) {
+            const Prim2 p = S.prims[i];
+            count_fetch<COUNT>(S, 1);
+            if ((1u << p.label) & qmask) visit(p);
         }
+        if (!pop()) return;
     }
 }
 
