@@ -238,6 +238,21 @@ __device__ __forceinline__ bool ray_box(const float4& b, float ox, float oy, flo
     return t0 <= t1;
 }
 
+// the same slab test, returning the entry distance (kFInf on a miss)
+__device__ __forceinline__ float ray_box_t(const float4& b, float ox, float oy, float idx, float idy, float tMax) {
+    float t0 = 0.0f, t1 = tMax;
+    float tn = (b.x - ox) * idx, tf = (b.z - ox) * idx;
+    if (tn > tf) { float s = tn; tn = tf; tf = s; }
+    t0 = fmaxf(t0, tn);
+    t1 = fminf(t1, tf);
+    tn = (b.y - oy) * idy;
+    tf = (b.w - oy) * idy;
+    if (tn > tf) { float s = tn; tn = tf; tf = s; }
+    t0 = fmaxf(t0, tn);
+    t1 = fminf(t1, tf);
+    return t0 <= t1 ? t0 : kFInf;
+}
+
 // side of v relative to the ray o + t d; explicit roundings (no FMA contraction)
 // so a vertex shared by two segments is classified identically for both
 __device__ __forceinline__ float ray_side(float dx, float dy, float ox, float oy, float vx, float vy) {
@@ -259,47 +274,67 @@ __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, f
     RayHit h{kFInf, 0.0f, 0.0f, 0.0f, -1};
     float idx = f_rcp(dx), idy = f_rcp(dy);  // slab tests on padded boxes: an approximate reciprocal suffices
     float limit = tMax;
-    int stack[kStack];
+    // nearer child first (entry distance), the other pushed with its entry distance and
+    // dropped at pop time once a hit closer than it is known; while-while structure
+    unsigned long long stack[kStack];
     int sp = 0, ref = 0;
-    for (;;) {
-        if (ref >= 0) {
-            const Node2 nd = S.nodes[ref];
-            count_fetch<COUNT>(S, 0);
-            bool vl = (nd.mask & qmask) && ray_box(nd.lbox, ox, oy, idx, idy, limit);
-            bool vr = ((nd.mask >> 3) & qmask) && ray_box(nd.rbox, ox, oy, idx, idy, limit);
-            if (vl && vr) { stack[sp++] = nd.right; ref = nd.left; continue; }
-            if (vl) { ref = nd.left; continue; }
-            if (vr) { ref = nd.right; continue; }
-        } else {
-            int code = ~ref;
-            int start = code >> 3, count = (code & 7) + 1;
-            for (int i = start; i < start + count; ++i) {
-                const Prim2 p = S.prims[i];
-                count_fetch<COUNT>(S, 1);
-                if (!((1u << p.label) & qmask) || p.id == skipSeg) continue;
-                // watertight crossing test: each endpoint is classified by its side
-                // of the ray; a vertex shared by two segments gets the same sign in
-                // both, so a ray can never slip between them (raySegment bvh.cpp:71-83
-                // decides via s in [0,1], which FP32 cancellation breaks near vertices)
-                float sa = ray_side(dx, dy, ox, oy, p.seg.x, p.seg.y);
-                float sb = ray_side(dx, dy, ox, oy, p.seg.z, p.seg.w);
-                if ((sa > 0.0f && sb > 0.0f) || (sa < 0.0f && sb < 0.0f)) continue;
-                float den = sa - sb;  // = cross(d, e) with e = b - a, up to sign convention
-                if (den == 0.0f) continue;  // parallel / collinear: miss
-                float s = sa / den;
-                float ex = p.seg.z - p.seg.x, ey = p.seg.w - p.seg.y;
-                float px = fmaf(s, ex, p.seg.x), py = fmaf(s, ey, p.seg.y);
-                float t = (px - ox) * dx + (py - oy) * dy;  // unit direction: distance along the ray
-                if (t <= 0.0f || t > limit) continue;
-                if (t > tMin && t < h.t) {
-                    h.t = t; h.s = s; h.seg = p.id;
-                    h.px = px; h.py = py;
-                    limit = t;
-                }
+    auto pop = [&]() -> bool {
+        for (;;) {
+            if (sp == 0) return false;
+            unsigned long long e = stack[--sp];
+            if (__uint_as_float(static_cast<unsigned>(e >> 32)) <= limit) {
+                ref = static_cast<int>(static_cast<unsigned>(e));
+                return true;
             }
         }
-        if (sp == 0) return h;
-        ref = stack[--sp];
+    };
+    for (;;) {
+        while (ref >= 0) {
+            const Node2 nd = S.nodes[ref];
+            count_fetch<COUNT>(S, 0);
+            float tl = (nd.mask & qmask) ? ray_box_t(nd.lbox, ox, oy, idx, idy, limit) : kFInf;
+            float tr = ((nd.mask >> 3) & qmask) ? ray_box_t(nd.rbox, ox, oy, idx, idy, limit) : kFInf;
+            bool vl = tl != kFInf, vr = tr != kFInf;
+            if (vl && vr) {
+                bool lf = tl <= tr;
+                stack[sp++] = (static_cast<unsigned long long>(__float_as_uint(lf ? tr : tl)) << 32) |
+                              static_cast<unsigned>(lf ? nd.right : nd.left);
+                ref = lf ? nd.left : nd.right;
+            } else if (vl) {
+                ref = nd.left;
+            } else if (vr) {
+                ref = nd.right;
+            } else if (!pop()) {
+                return h;
+            }
+        }
+        int code = ~ref;
+        int start = code >> 3, count = (code & 7) + 1;
+        for (int i = start; i < start + count; ++i) {
+            const Prim2 p = S.prims[i];
+            count_fetch<COUNT>(S, 1);
+            if (!((1u << p.label) & qmask) || p.id == skipSeg) continue;
+            // watertight crossing test: each endpoint is classified by its side
+            // of the ray; a vertex shared by two segments gets the same sign in
+            // both, so a ray can never slip between them (raySegment bvh.cpp:71-83
+            // decides via s in [0,1], which FP32 cancellation breaks near vertices)
+            float sa = ray_side(dx, dy, ox, oy, p.seg.x, p.seg.y);
+            float sb = ray_side(dx, dy, ox, oy, p.seg.z, p.seg.w);
+            if ((sa > 0.0f && sb > 0.0f) || (sa < 0.0f && sb < 0.0f)) continue;
+            float den = sa - sb;  // = cross(d, e) with e = b - a, up to sign convention
+            if (den == 0.0f) continue;  // parallel / collinear: miss
+            float s = sa / den;
+            float ex = p.seg.z - p.seg.x, ey = p.seg.w - p.seg.y;
+            float px = fmaf(s, ex, p.seg.x), py = fmaf(s, ey, p.seg.y);
+            float t = (px - ox) * dx + (py - oy) * dy;  // unit direction: distance along the ray
+            if (t <= 0.0f || t > limit) continue;
+            if (t > tMin && t < h.t) {
+                h.t = t; h.s = s; h.seg = p.id;
+                h.px = px; h.py = py;
+                limit = t;
+            }
+        }
+        if (!pop()) return h;
     }
 }
 
