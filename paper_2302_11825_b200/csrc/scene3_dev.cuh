@@ -218,6 +218,19 @@ __device__ __forceinline__ bool ray_box3(const float4& lo, const float4& hi, flo
     return t0 <= t1;
 }
 
+// the same slab test, returning the entry distance (kFInf on a miss)
+__device__ __forceinline__ float ray_box3_t(const float4& lo, const float4& hi, float ox, float oy, float oz,
+                                            float idx, float idy, float idz, float tMax) {
+    float t0 = 0.0f, t1 = tMax;
+    float tn = (lo.x - ox) * idx, tf = (hi.x - ox) * idx;
+    t0 = fmaxf(t0, fminf(tn, tf)); t1 = fminf(t1, fmaxf(tn, tf));
+    tn = (lo.y - oy) * idy; tf = (hi.y - oy) * idy;
+    t0 = fmaxf(t0, fminf(tn, tf)); t1 = fminf(t1, fmaxf(tn, tf));
+    tn = (lo.z - oz) * idz; tf = (hi.z - oz) * idz;
+    t0 = fmaxf(t0, fminf(tn, tf)); t1 = fminf(t1, fmaxf(tn, tf));
+    return t0 <= t1 ? t0 : kFInf;
+}
+
 // inside: boundary-inclusive within tol, then ray-crossing parity along a fixed
 // irrational direction (avoids axis-aligned edge degeneracies of meshes)
 __device__ __forceinline__ bool inside3(const SceneView3& S, float x, float y, float z, float tol) {

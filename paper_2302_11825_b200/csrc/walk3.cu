@@ -84,34 +84,55 @@ __device__ __forceinline__ Hit3 ray_neumann3(const WalkEnv3& E, float ox, float 
     Hit3 h{kFInf, -1};
     float idx = f_rcp(dx), idy = f_rcp(dy), idz = f_rcp(dz);  // slab tests on padded boxes
     float limit = tMax;
-    int stack[kStack];
+    // nearer child first, the other pushed with its entry distance (dropped at pop once
+    // a closer hit is known); while-while structure
+    unsigned long long stack[kStack];
     int sp = 0, ref = 0;
-    for (;;) {
-        if (ref >= 0) {
-            const Node3 nd = E.S.nodes[ref];
-            count_fetch3<COUNT>(E.S, 0);
-            bool vl = (nd.mask & kClsNeumann) && ray_box3(nd.llo, nd.lhi, ox, oy, oz, idx, idy, idz, limit);
-            bool vr = ((nd.mask >> 3) & kClsNeumann) && ray_box3(nd.rlo, nd.rhi, ox, oy, oz, idx, idy, idz, limit);
-            if (vl && vr) { stack[sp++] = nd.right; ref = nd.left; continue; }
-            if (vl) { ref = nd.left; continue; }
-            if (vr) { ref = nd.right; continue; }
-        } else {
-            int code = ~ref;
-            int start = code >> 3, count = (code & 7) + 1;
-            for (int i = start; i < start + count; ++i) {
-                const Prim3 p = E.S.prims[i];
-                count_fetch3<COUNT>(E.S, 1);
-                int cls = __float_as_int(p.b.w), id = __float_as_int(p.a.w);
-                if (!((1u << cls) & kClsNeumann) || id == skip) continue;
-                float th;
-                if (ray_tri(p, ox, oy, oz, dx, dy, dz, limit, th) && th > E.tguard && th < h.t) {
-                    h = Hit3{th, id};
-                    limit = th;
-                }
+    auto pop = [&]() -> bool {
+        for (;;) {
+            if (sp == 0) return false;
+            unsigned long long e = stack[--sp];
+            if (__uint_as_float(static_cast<unsigned>(e >> 32)) <= limit) {
+                ref = static_cast<int>(static_cast<unsigned>(e));
+                return true;
             }
         }
-        if (sp == 0) return h;
-        ref = stack[--sp];
+    };
+    for (;;) {
+        while (ref >= 0) {
+            const Node3 nd = E.S.nodes[ref];
+            count_fetch3<COUNT>(E.S, 0);
+            float tl = (nd.mask & kClsNeumann) ? ray_box3_t(nd.llo, nd.lhi, ox, oy, oz, idx, idy, idz, limit) : kFInf;
+            float tr = ((nd.mask >> 3) & kClsNeumann) ? ray_box3_t(nd.rlo, nd.rhi, ox, oy, oz, idx, idy, idz, limit)
+                                                      : kFInf;
+            bool vl = tl != kFInf, vr = tr != kFInf;
+            if (vl && vr) {
+                bool lf = tl <= tr;
+                stack[sp++] = (static_cast<unsigned long long>(__float_as_uint(lf ? tr : tl)) << 32) |
+                              static_cast<unsigned>(lf ? nd.right : nd.left);
+                ref = lf ? nd.left : nd.right;
+            } else if (vl) {
+                ref = nd.left;
+            } else if (vr) {
+                ref = nd.right;
+            } else if (!pop()) {
+                return h;
+            }
+        }
+        int code = ~ref;
+        int start = code >> 3, count = (code & 7) + 1;
+        for (int i = start; i < start + count; ++i) {
+            const Prim3 p = E.S.prims[i];
+            count_fetch3<COUNT>(E.S, 1);
+            int cls = __float_as_int(p.b.w), id = __float_as_int(p.a.w);
+            if (!((1u << cls) & kClsNeumann) || id == skip) continue;
+            float th;
+            if (ray_tri(p, ox, oy, oz, dx, dy, dz, limit, th) && th > E.tguard && th < h.t) {
+                h = Hit3{th, id};
+                limit = th;
+            }
+        }
+        if (!pop()) return h;
     }
 }
 
