@@ -171,7 +171,8 @@ __device__ __forceinline__ void pair(const float4 a, const float4 b, float px, f
         if constexpr (KIND == kLap3) {
             if constexpr (!SRC) {
                 float ndA = fmaf(a.w, dx, fmaf(b.x, dy, __fmul_rn(b.y, dz)));
-                if constexpr (VAL) acc.v = fmaf(ndA, ir3, fmaf(b.w, ir, acc.v));
+                // A (n.d) / r^3 + B / r = (A (n.d) / r^2 + B) / r: no 1/r^3 for values
+                if constexpr (VAL) acc.v = fmaf(ir, fmaf(ndA, ir2, b.w), acc.v);
                 if constexpr (GRAD) {  // accumulated negated: (A/r^3) n - q d
                     float nq = __fmul_rn(fmaf(__fmul_rn(ndA, -3.0f), ir2, b.z), ir3);
                     acc.gx = fmaf(nq, dx, fmaf(ir3, a.w, acc.gx));
@@ -195,7 +196,9 @@ __device__ __forceinline__ void pair(const float4 a, const float4 b, float px, f
             if constexpr (!SRC) {
                 float ndA = fmaf(a.w, dx, fmaf(b.x, dy, __fmul_rn(b.y, dz)));
                 float pA = __fmul_rn(ndA, ir3);  // A p
-                if constexpr (VAL) acc.v = fmaf(pA, Q, fmaf(__fmul_rn(b.w, ir), e, acc.v));
+                // A p Q + B e / r = (e / r) (A (n.d) / r^2 (1 + s r) + B): two fewer ops per pair
+                if constexpr (VAL)
+                    acc.v = fmaf(__fmul_rn(e, ir), fmaf(__fmul_rn(ndA, ir2), fmaf(s, r, 1.0f), b.w), acc.v);
                 if constexpr (GRAD) {
                     float q = fmaf(3.0f * Q * pA, ir2, b.w * Q * ir3);
                     q = fmaf(sigma * e, pA, q);
@@ -303,7 +306,7 @@ __device__ __forceinline__ void pair2(const float4 a, const float4 b, F2 px, F2 
         if constexpr (KIND == kLap3) {
             if constexpr (!SRC) {
                 F2 ndA = fma2(bc(a.w), dx, fma2(bc(b.x), dy, mul2(bc(b.y), dz)));
-                if constexpr (VAL) acc.v = fma2(ndA, ir3, fma2(bc(b.w), ir, acc.v));
+                if constexpr (VAL) acc.v = fma2(ir, fma2(ndA, ir2, bc(b.w)), acc.v);
                 if constexpr (GRAD) {
                     F2 nq = mul2(fma2(mul2(ndA, bc(-3.0f)), ir2, bc(b.z)), ir3);
                     acc.gx = fma2(nq, dx, fma2(ir3, bc(a.w), acc.gx));
@@ -321,13 +324,10 @@ __device__ __forceinline__ void pair2(const float4 a, const float4 b, F2 px, F2 
             }
         } else {  // kScr3, values only
             F2 r = mul2(r2, ir);
-            F2 t = mul2(bc(s), r);
             F2 e = each(mul2(r, bc(-1.44269504088896340736f * s)), [](float x) { return f_ex2(x); });
-            F2 Q = fma2(e, t, e);
             if constexpr (!SRC) {
                 F2 ndA = fma2(bc(a.w), dx, fma2(bc(b.x), dy, mul2(bc(b.y), dz)));
-                F2 pA = mul2(ndA, ir3);
-                acc.v = fma2(pA, Q, fma2(mul2(bc(b.w), ir), e, acc.v));
+                acc.v = fma2(mul2(e, ir), fma2(mul2(ndA, ir2), fma2(bc(s), r, bc(1.0f)), bc(b.w)), acc.v);
             } else {
                 acc.v = fma2(mul2(bc(a.w), ir), e, acc.v);
             }
