@@ -23,6 +23,17 @@ struct DevProblem {
     DevField f, g, h;
 };
 
+// Far-field distance bounds: the exact distance to the whole boundary (any class) at
+// the vertices of a uniform grid. At x, d(v) - |x - v| (minus a rounding margin) is a
+// lower bound of d(x); when it exceeds tau the step uses it as the ball radius and
+// skips the BVH queries (any ball inside the domain keeps walk-on-spheres unbiased;
+// near the boundary, where walks terminate, the exact queries run as before).
+struct FarField {
+    const float* d;  // NULL: disabled
+    float lox, loy, loz, h, invH, tau, margin;
+    int nx, ny, nz;
+};
+
 // WalkContext (pointwise.cpp:11-35) in device form
 struct WalkEnv {
     SceneView2 S;
@@ -32,6 +43,7 @@ struct WalkEnv {
     int maxSteps;
     int hasNeumann, hasSource, hasH, closed;
     uint32_t k0, k1;  // Philox key of the job (seed, salt, round)
+    FarField ff;
 };
 
 // A batch of estimator tasks. U tasks: nU plain walks from each U start point.
@@ -62,6 +74,9 @@ struct WalkJob {
 };
 
 void launch_walk_job(const WalkEnv& env, const WalkJob& job, cudaStream_t st);
+// fills the far-field grid (distance to any boundary primitive at every vertex)
+void launch_farfield2(const SceneView2& S, const FarField& F, float* d, cudaStream_t st);
+void launch_farfield3(const bvc_dev::SceneView3& S, const FarField& F, float* d, cudaStream_t st);
 
 // per-point mean / standard error (runWalks pointwise.cpp:167-186), fixed order
 void launch_reduce_estimates(const float* vals, int nPts, int per, int comps, int comp, double* mean,
@@ -153,6 +168,7 @@ struct WalkEnv3 {
     int maxSteps;
     int hasNeumann, hasH, closed;
     uint32_t k0, k1;
+    FarField ff;
 };
 
 struct WalkJob3 {

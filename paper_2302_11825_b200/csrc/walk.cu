@@ -150,6 +150,15 @@ __device__ float neumann_term(const WalkEnv& E, float x, float y, float R, float
     return -gb * hv * total;
 }
 
+// far-field lower bound of the distance to the boundary at (x, y), or -1 (FarField)
+__device__ __forceinline__ float farfield_bound(const FarField& F, float x, float y) {
+    float gx = (x - F.lox) * F.invH, gy = (y - F.loy) * F.invH;
+    int ix = __float2int_rn(gx), iy = __float2int_rn(gy);
+    if (ix < 0 || iy < 0 || ix >= F.nx || iy >= F.ny) return -1.0f;
+    float dx = x - fmaf(static_cast<float>(ix), F.h, F.lox), dy = y - fmaf(static_cast<float>(iy), F.h, F.loy);
+    return __ldg(F.d + static_cast<size_t>(iy) * F.nx + ix) - sqrtf(fmaf(dx, dx, dy * dy)) - F.margin;
+}
+
 // per-lane walk state
 struct Walk {
     float x, y, acc, weight, inx, iny;
@@ -172,26 +181,34 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
     Closest cp;
     float R;
     ++steps;
-    // (scenes without Dirichlet segments are rejected on the host, pointwise.cpp:217-218)
-    if constexpr (NEU) {
-        // a Dirichlet segment farther than the closest visible silhouette may be
-        // pruned (q.D.seg < 0, d2 = inf): R is then the silhouette distance
-        StarQuery q = star_query<COUNT>(E.S, w.x, w.y, E.eps * E.eps, w.lastD);
-        cp = q.D;
-        float dD = sqrtf(cp.d2);
-        if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
-        R = fminf(dD, sqrtf(q.s2));
+    // far field: a ball from the distance grid, no BVH query (FarField); such a ball
+    // holds no boundary point, so no Neumann crossing and no Neumann-data term either
+    const float lb = E.ff.d ? farfield_bound(E.ff, w.x, w.y) : -1.0f;
+    const bool far = lb >= E.ff.tau;
+    if (far) {
+        R = lb;
     } else {
-        cp = closest_point<COUNT>(E.S, w.x, w.y, kClsD, kFInf, w.lastD);
-        float dD = sqrtf(cp.d2);
-        if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
-        R = dD;
+        // (scenes without Dirichlet segments are rejected on the host, pointwise.cpp:217-218)
+        if constexpr (NEU) {
+            // a Dirichlet segment farther than the closest visible silhouette may be
+            // pruned (q.D.seg < 0, d2 = inf): R is then the silhouette distance
+            StarQuery q = star_query<COUNT>(E.S, w.x, w.y, E.eps * E.eps, w.lastD);
+            cp = q.D;
+            float dD = sqrtf(cp.d2);
+            if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
+            R = fminf(dD, sqrtf(q.s2));
+        } else {
+            cp = closest_point<COUNT>(E.S, w.x, w.y, kClsD, kFInf, w.lastD);
+            float dD = sqrtf(cp.d2);
+            if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
+            R = dD;
+        }
+        w.lastD = cp.seg;
     }
-    w.lastD = cp.seg;
     R = fmaxf(R, E.rmin);
     float factor = w.onN ? 2.0f : 1.0f;
     if constexpr (SRC) w.acc += w.weight * factor * source_term(E, w.x, w.y, R, u01(rnd.y), u01(rnd.z));
-    if (NEU && E.hasH) w.acc += w.weight * factor * neumann_term(E, w.x, w.y, R, u01(rnd.w));
+    if (NEU && E.hasH && !far) w.acc += w.weight * factor * neumann_term(E, w.x, w.y, R, u01(rnd.w));
     // direction: full circle, or the half circle around the inward normal on Neumann
     float dx, dy;
     if (w.onN) {
@@ -204,7 +221,7 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
     }
     float travel = R;
     bool hit = false;
-    if constexpr (NEU) {
+    if (NEU && !far) {
         RayHit h = intersect_ray<COUNT>(E.S, w.x, w.y, dx, dy, R, kClsNeumann, E.tguard, w.onN ? w.prevSeg : -1);
         if (h.seg >= 0) {
             hit = true;
@@ -576,6 +593,14 @@ __global__ void inside_kernel(const SceneView2 S, const double* x, int n, float 
 
 inline int blocks(long long n, int t) { return static_cast<int>((n + t - 1) / t); }
 
+__global__ void farfield2_kernel(const SceneView2 S, const FarField F, float* d) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= F.nx * F.ny) return;
+    int ix = i % F.nx, iy = i / F.nx;
+    float x = fmaf(static_cast<float>(ix), F.h, F.lox), y = fmaf(static_cast<float>(iy), F.h, F.loy);
+    d[i] = sqrtf(closest_point(S, x, y, kClsAny).d2);
+}
+
 __global__ void start_hints_kernel(const CacheSample* samples, int n, const int* source, const int* cls,
                                    const int* leafOf, const int* dIdx, int nD, int* hintU, int* hintD) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -610,6 +635,11 @@ void launch_walk_t(const WalkEnv& env, const WalkJob& job, long long total, cuda
     long long want = (total + kWalkThreads - 1) / kWalkThreads;
     int grid = static_cast<int>(want < static_cast<long long>(sms) * perSm ? want : static_cast<long long>(sms) * perSm);
     walk_kernel<NEU, SCR, SRC, COUNT><<<grid, kWalkThreads, 0, st>>>(env, job);
+}
+
+void launch_farfield2(const SceneView2& S, const FarField& F, float* d, cudaStream_t st) {
+    farfield2_kernel<<<blocks(static_cast<long long>(F.nx) * F.ny, 128), 128, 0, st>>>(S, F, d);
+    count_launch();
 }
 
 void launch_start_hints(const CacheSample* samples, int n, const int* source, const int* cls, const int* leafOf,

@@ -183,32 +183,50 @@ __device__ __forceinline__ void walk3_start(Walk3& w, float x, float y, float z)
     w.lastD = -1;
 }
 
+// far-field lower bound of the distance to the boundary at x, or -1 (FarField)
+__device__ __forceinline__ float farfield_bound3(const FarField& F, float x, float y, float z) {
+    int ix = __float2int_rn((x - F.lox) * F.invH), iy = __float2int_rn((y - F.loy) * F.invH),
+        iz = __float2int_rn((z - F.loz) * F.invH);
+    if (ix < 0 || iy < 0 || iz < 0 || ix >= F.nx || iy >= F.ny || iz >= F.nz) return -1.0f;
+    float dx = x - fmaf(static_cast<float>(ix), F.h, F.lox), dy = y - fmaf(static_cast<float>(iy), F.h, F.loy),
+          dz = z - fmaf(static_cast<float>(iz), F.h, F.loz);
+    return __ldg(F.d + (static_cast<size_t>(iz) * F.ny + iy) * F.nx + ix) - sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))) -
+           F.margin;
+}
+
 template <bool NEU, bool SCR, bool COUNT>
 __device__ __forceinline__ bool walk3_step(const WalkEnv3& E, Walk3& w, U4 rnd, float& value, int& trunc,
                                            unsigned long long& steps) {
     ++steps;
     Closest3 cp;
     float R;
-    if constexpr (NEU) {
-        Star3 q = star_query3<COUNT>(E, w.x, w.y, w.z, w.lastD);
-        cp = q.D;
-        float dD = sqrtf(cp.d2);
-        if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
-        R = fminf(dD, sqrtf(q.s2));
+    // far field: a ball from the distance grid, no BVH queries (FarField)
+    const float lb = E.ff.d ? farfield_bound3(E.ff, w.x, w.y, w.z) : -1.0f;
+    const bool far = lb >= E.ff.tau;
+    if (far) {
+        R = lb;
     } else {
-        cp = closest_point3<COUNT>(E.S, w.x, w.y, w.z, kClsD, kFInf, w.lastD);
-        float dD = sqrtf(cp.d2);
-        if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
-        R = dD;
+        if constexpr (NEU) {
+            Star3 q = star_query3<COUNT>(E, w.x, w.y, w.z, w.lastD);
+            cp = q.D;
+            float dD = sqrtf(cp.d2);
+            if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
+            R = fminf(dD, sqrtf(q.s2));
+        } else {
+            cp = closest_point3<COUNT>(E.S, w.x, w.y, w.z, kClsD, kFInf, w.lastD);
+            float dD = sqrtf(cp.d2);
+            if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
+            R = dD;
+        }
+        w.lastD = cp.prim;
     }
-    w.lastD = cp.prim;
     R = fmaxf(R, E.rmin);
     float dx, dy, dz;
     if (w.onN) hemi_dir(u01(rnd.x), u01(rnd.y), w.inx, w.iny, w.inz, dx, dy, dz);
     else sphere_dir(u01(rnd.x), u01(rnd.y), dx, dy, dz);
     float travel = R;
     bool hit = false;
-    if constexpr (NEU) {
+    if (NEU && !far) {
         Hit3 h = ray_neumann3<COUNT>(E, w.x, w.y, w.z, dx, dy, dz, R, w.onN ? w.prevTri : -1);
         if (h.tri >= 0) {
             hit = true;
@@ -507,6 +525,15 @@ inline int blocks(long long n, int t) { return static_cast<int>((n + t - 1) / t)
 
 }  // namespace
 
+__global__ void farfield3_kernel(const SceneView3 S, const FarField F, float* d) {
+    long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= static_cast<long long>(F.nx) * F.ny * F.nz) return;
+    int ix = static_cast<int>(i % F.nx), iy = static_cast<int>((i / F.nx) % F.ny), iz = static_cast<int>(i / (static_cast<long long>(F.nx) * F.ny));
+    float x = fmaf(static_cast<float>(ix), F.h, F.lox), y = fmaf(static_cast<float>(iy), F.h, F.loy),
+          z = fmaf(static_cast<float>(iz), F.h, F.loz);
+    d[i] = sqrtf(closest_point3(S, x, y, z, kClsAny).d2);
+}
+
 template <bool NEU, bool SCR, bool COUNT>
 void launch_walk3_t(const WalkEnv3& env, const WalkJob3& job, long long total, cudaStream_t st) {
     int dev = 0, sms = 148, perSm = 0;
@@ -517,6 +544,12 @@ void launch_walk3_t(const WalkEnv3& env, const WalkJob3& job, long long total, c
     long long want = (total + kThreads3 - 1) / kThreads3;
     int grid = static_cast<int>(want < static_cast<long long>(sms) * perSm ? want : static_cast<long long>(sms) * perSm);
     walk3_kernel<NEU, SCR, COUNT><<<grid, kThreads3, 0, st>>>(env, job);
+}
+
+void launch_farfield3(const SceneView3& S, const FarField& F, float* d, cudaStream_t st) {
+    long long n = static_cast<long long>(F.nx) * F.ny * F.nz;
+    farfield3_kernel<<<blocks(n, 128), 128, 0, st>>>(S, F, d);
+    count_launch();
 }
 
 void launch_walk_job3(const WalkEnv3& env, const WalkJob3& job, cudaStream_t st) {

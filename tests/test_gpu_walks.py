@@ -141,3 +141,16 @@ def test_wos_equals_wost_on_dirichlet_scene():
     a = B.wos_solve(sc, pb, [[0.4, -0.2]], _wc(50000, seed=9))
     b = B.wost_solve(sc, pb, [[0.4, -0.2]], _wc(50000, seed=10))
     assert abs(H.zscore(a["mean"][0], a["se"][0], b["mean"][0], b["se"][0])) < Z
+
+
+def test_farfield_option_stays_within_the_eps_shell_bias(monkeypatch):
+    """BVC_FARFIELD=1 (opt-in): far-field balls from a distance grid keep walk-on-spheres
+    unbiased up to the usual O(eps) shell bias (closed forms within 2e-3 at eps = 1e-3 diag)."""
+    monkeypatch.setenv("BVC_FARFIELD", "1")
+    for maker, x, exact in ((H.disk_linear, [0.3, 0.4], 0.3), (H.disk_poisson, [0.0, 0.0], -0.25),
+                            (H.disk_poisson, [0.5, -0.2], 0.25 * (0.29 - 1.0))):
+        geom, pb = maker()
+        sc = _scene(geom)
+        e = B.wos_solve(sc, pb, [x], _wc(200000, seed=9))
+        m, se = e["mean"][0], e["se"][0]
+        assert abs(m - exact) <= Z * se + 2e-3, (x, m, se, exact)
