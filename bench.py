@@ -462,6 +462,7 @@ def reference_round_estimate(c, sample_s=20.0, threads=0):
     t_round = gen_full + splat_full
     pairs = len(act) * (N + M)
     return {"value": pairs / t_round, "unit": "interactions/s", "cores": int(cores), "kind": "reference",
+            "cpu": cpu_model(), "host_threads": os.cpu_count(),
             "sample": (f"generateBoundaryCache on {n_sub}/{N} samples ({t_gen:.1f} s) + splatSolution"
                        f"{'+splatGradient' if c.gradients else ''} on {len(xs)}/{len(act)} points vs the full "
                        f"{N}+{M}-sample cache ({t_spl:.1f} s); extrapolated linearly (cost ~ walks, ~ K(N+M))"),
@@ -492,9 +493,21 @@ def port_gather_estimate_3d(c, sample_s):
         if t > 0.5 * sample_s or k >= len(c.points):
             break
         k = min(len(c.points), int(k * max(2.0, 0.5 * sample_s / max(t, 1e-3) * 0.8)))
-    return {"value": k * N / t, "unit": "interactions/s", "cores": 1, "kind": "port",
+    return {"value": k * N / t, "unit": "interactions/s", "cores": 1, "kind": "port", "cpu": cpu_model(),
             "sample": f"restated 3D splat (1 thread) on {k} points x {N} samples ({t:.1f} s); gather only — "
                       "the reference has no 3D walk or splat path"}
+
+
+def cpu_model():
+    """`model name` of the host CPU (SURVEY 8d asks for the core count and model per run)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def cpu_baseline(c, sample_s):
@@ -528,7 +541,7 @@ def run_reference(args):
            "data": "synthetic (seeded, configs.py)", "impl": "reference",
            "config": {"workload": c.name, "config_index": args.config},
            "cpu_baseline": {"value": value, "unit": "interactions/s", "cores": vals[-1]["cores"],
-                            "kind": "reference", "sample": vals[-1]["sample"]},
+                            "cpu": vals[-1]["cpu"], "kind": "reference", "sample": vals[-1]["sample"]},
            "e2e": {"value": value, "unit": "interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "wall_s": time.perf_counter() - t0}
     print(json.dumps(out), flush=True)

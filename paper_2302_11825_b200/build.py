@@ -19,8 +19,8 @@ LIB = os.path.join(OUT, "libbvc_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
-SOURCES = ["capi.cu", "walk.cu", "walk3.cu", "gather.cu", "gather64.cu", "correct.cu", "probe.cu", "lbvh.cu", "sahbvh.cu", "host_scene.cpp", "io.cpp"]
-HEADERS = ["device_math.cuh", "scene_dev.cuh", "scene3_dev.cuh", "internal.h", "gather.h", "host_scene.h"]
+SOURCES = ["capi.cu", "capi_cache.cu", "capi_points.cu", "capi_splat.cu", "capi_walks.cu", "capi_stream.cu", "walk.cu", "walk3.cu", "gather.cu", "gather64.cu", "correct.cu", "probe.cu", "lbvh.cu", "sahbvh.cu", "host_scene.cpp", "io.cpp"]
+HEADERS = ["capi_common.cuh", "tma.cuh", "device_math.cuh", "scene_dev.cuh", "scene3_dev.cuh", "internal.h", "gather.h", "host_scene.h"]
 
 
 def _stale(obj: str, src: str) -> bool:

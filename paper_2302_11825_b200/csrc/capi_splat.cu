@@ -1,0 +1,324 @@
+// capi_splat.cu — the dense interior evaluation: splatSolution / splatGradient
+// (cache.cpp:426-497), correctedBoundarySplat / correctedSourceSplat (499-597) and
+// updateSolution's round with its clamp-mode dispatch (622-684).
+#include <cub/device/device_scan.cuh>
+
+#include "capi_common.cuh"
+
+namespace bvc_capi {
+
+int gather_kind(const bvc_kernel_spec& k) {
+    bool scr = k.kind == BVC_KERNEL_SCREENED;
+    return k.dim == 2 ? (scr ? kScr2 : kLap2) : (scr ? kScr3 : kLap3);
+}
+
+// one gather launch over [begin, end) of the active points; mode = SplatMode bits
+// (gather.cu) for the clamped / ball-kernel variants (value only)
+void splat_launch(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_points_s* P, const bvc_splat_config& cfg,
+                  size_t begin, size_t end, bool val, bool grad, int mode, double clamp) {
+    int dim = cfg.kernel.dim;
+    int N = b ? b->n : 0, M = s ? s->m : 0;
+    size_t Ka = static_cast<size_t>(P->active);
+    end = std::min(end, Ka);
+    if (begin >= end) return;
+    int K = static_cast<int>(end - begin);
+    int kind = gather_kind(cfg.kernel);
+    if (cfg.fp64) {  // FP64 variant (gather64.cu)
+        double4* pack64 = ws().get<double4>(kWsPack, 2 * static_cast<size_t>(std::max(N + M, 1)));
+        if (N) pack64_boundary(b->samples.p, N, kind, cfg.voronoi, pack64, g_stream);
+        if (M) pack64_source(s->samples.p, M, kind, pack64 + 2 * static_cast<size_t>(N), g_stream);
+        GatherPlan plan = plan_gather64(kind, K, N, M, val, grad);
+        double* part = ws().get<double>(kWsPart, std::max<size_t>(static_cast<size_t>(plan.chunksB + plan.chunksS) * plan.comps * K, 1));
+        int* skipB = ws().get<int>(kWsSkipB, K);
+        int* skipS = ws().get<int>(kWsSkipS, K);
+        CK(cudaMemsetAsync(skipB, 0, K * sizeof(int), g_stream));
+        CK(cudaMemsetAsync(skipS, 0, K * sizeof(int), g_stream));
+        double* px64 = ws().get<double>(kWsXs64, static_cast<size_t>(dim) * K);
+        gather_points64(P->x.p, P->order.p + begin, K, dim, px64, g_stream);
+        if (N + M > 0) {
+            launch_gather64(kind, plan, pack64, N, M, px64, K, dim, cfg.coincidenceTol, val, grad, part, skipB, skipS,
+                            ws().get<unsigned>(kWsUnitCtr, 1), g_stream);
+            launch_finalize(part, plan, K, P->order.p + begin, N, M, val, grad, dim, skipB, skipS, P->dev(), g_stream);
+        }
+        CK(cudaGetLastError());
+        return;
+    }
+    float4* pack = ws().get<float4>(kWsPack, 2 * static_cast<size_t>(std::max(N + M, 1)));
+    if (N) pack_boundary(b->samples.p, N, kind, cfg.voronoi, pack, g_stream);
+    if (M) pack_source(s->samples.p, M, kind, pack + 2 * static_cast<size_t>(N), g_stream);
+    GatherPlan plan = plan_gather(kind, K, N, M, val, grad);
+    double* part = ws().get<double>(kWsPart, std::max<size_t>(static_cast<size_t>(plan.chunksB + plan.chunksS) * plan.comps * K, 1));
+    int* skipB = ws().get<int>(kWsSkipB, K);
+    int* skipS = ws().get<int>(kWsSkipS, K);
+    CK(cudaMemsetAsync(skipB, 0, K * sizeof(int), g_stream));
+    CK(cudaMemsetAsync(skipS, 0, K * sizeof(int), g_stream));
+    float* ballRs = nullptr;
+    if (mode & kModeBall) {
+        ballRs = ws().get<float>(kWsBallRs, K);
+        launch_gather_f32(P->ballR.p, P->order.p + begin, K, ballRs, g_stream);
+    }
+    if (N + M > 0)
+        launch_gather(kind, plan, pack, N, M, P->xs.p + static_cast<size_t>(dim) * begin, K, dim,
+                      static_cast<float>(cfg.kernel.sigma), static_cast<float>(cfg.coincidenceTol), val, grad, part,
+                      skipB, skipS, ws().get<float4>(kWsTileBox, 2 * static_cast<size_t>((N + 255) / 256 + (M + 255) / 256 + 1)),
+                      ws().get<unsigned>(kWsUnitCtr, 1), g_stream, mode, static_cast<float>(clamp), ballRs);
+    else
+        CK(cudaMemsetAsync(part, 0, sizeof(double), g_stream));
+    if (N + M > 0)
+        launch_finalize(part, plan, K, P->order.p + begin, N, M, val, grad, dim, skipB, skipS, P->dev(), g_stream);
+    CK(cudaGetLastError());
+}
+
+// requireBallRadius (cache.cpp:418-423)
+void require_ball(bvc_eval_points_s* P) {
+    if (!P->ballValid)
+        throw Error(BVC_ERR_SOLVER, "ball-kernel mode: evaluation point has no ball radius "
+                                    "(markEvaluationPoints not applied)");
+}
+
+// splatSolution / splatGradient (cache.cpp:426-497), optionally with the boundary
+// dG/dn clamped (mode bits) as in correctedBoundarySplat's first loop
+void splat(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_points_s* P, const bvc_splat_config& cfg,
+           size_t begin, size_t end, bool val, bool grad, int mode, double clamp) {
+    require_device();
+    need(P != nullptr, "null evaluation points");
+    validate_kernel(cfg.kernel);
+    int dim = cfg.kernel.dim;
+    need(P->dim == dim, "evaluation points and kernel differ in dimension");
+    need(!b || b->dim == dim, "boundary cache dimension mismatch");
+    need(!s || s->dim == dim, "source cache dimension mismatch");
+    if (cfg.useBallGreens && val) {
+        if (cfg.kernel.kind != BVC_KERNEL_POISSON || dim != 2)
+            throw Error(BVC_ERR_SOLVER, "ball-kernel source mode requires the 2D Poisson kernel");
+        mode |= kModeBall;
+    }
+    if (mode && dim != 2) throw Error(BVC_ERR_INVALID_ARGUMENT, "clamped / ball-kernel splats are 2D (cache.cpp:499-597)");
+    if (cfg.fp64 && (cfg.kernel.kind != BVC_KERNEL_POISSON || mode))
+        throw Error(BVC_ERR_INVALID_ARGUMENT, "fp64 splats: plain Poisson kernels only");
+    ensure_order(P);
+    if (mode & kModeBall) require_ball(P);
+    if (val && grad && mode) {  // the gradient splat never clamps (cache.cpp:463-497)
+        splat_launch(b, s, P, cfg, begin, end, true, false, mode, clamp);
+        splat_launch(b, s, P, cfg, begin, end, false, true, 0, 0.0);
+    } else {
+        splat_launch(b, s, P, cfg, begin, end, val, grad, val ? mode : 0, clamp);
+    }
+}
+
+// correctedBoundarySplat (cache.cpp:499-553)
+void corrected_boundary(bvc_boundary_cache_s* b, bvc_eval_points_s* P, bvc_region_s* R, const bvc_splat_config& cfg,
+                        double clamp, int mode, const bvc_boundary_evaluator* ev, uint64_t seed, uint64_t stream) {
+    require_device();
+    need(P && R, "null argument");
+    if (mode == BVC_CLAMP_OFF) throw Error(BVC_ERR_INVALID_ARGUMENT, "corrected splat called with clamping off");
+    need(mode == BVC_CLAMP_ONLY || mode == BVC_CLAMP_CORRECT, "unknown clamp mode");
+    if (!(clamp > 0.0)) throw Error(BVC_ERR_INVALID_ARGUMENT, "clamp bound must be positive");
+    bool haveEval = ev && ev->kind != BVC_EVALUATOR_NONE;
+    if (mode == BVC_CLAMP_CORRECT && !haveEval)
+        throw Error(BVC_ERR_INVALID_ARGUMENT, "clamp correction needs a boundary evaluator");
+    need(cfg.kernel.dim == 2, "clamped splats are 2D (cache.cpp:499)");
+    splat(b, nullptr, P, cfg, 0, SIZE_MAX, true, false, kModeClampP, clamp);
+    if (mode != BVC_CLAMP_CORRECT) return;
+    int K = P->active;
+    if (K == 0) return;
+    R->upload();
+    int N = b ? b->n : 0;
+    CorrRayEnv E{};
+    E.region = R->boundary.view();
+    E.kinds = R->kinds.p;
+    E.screened = cfg.kernel.kind == BVC_KERNEL_SCREENED ? 1 : 0;
+    E.sqrtSigma = std::sqrt(cfg.kernel.sigma);
+    E.clamp = clamp;
+    E.tol2 = cfg.coincidenceTol * cfg.coincidenceTol;
+    E.nRound = static_cast<double>(N);
+    E.insideTol = static_cast<float>(1e-7 * R->boundary.host.diagonal);
+    key_of(seed, stream, 0, E.k0, E.k1);
+    int* noHit = ws().get<int>(kWsCorrFlag, 1);
+    CK(cudaMemsetAsync(noHit, 0, sizeof(int), g_stream));
+    auto check_hits = [&]() {
+        int h = 0;
+        CK(cudaMemcpyAsync(&h, noHit, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+        if (h) throw Error(BVC_ERR_SOLVER, "clamp correction: no boundary ray hits from an interior point");
+    };
+    if (ev->kind == BVC_EVALUATOR_FIELD) {
+        E.useField = 1;
+        E.field = to_dev(ev->field);
+        launch_corr_rays(E, P->x.p, P->order.p, K, nullptr, P->bsum.p, noHit, g_stream);
+        check_hits();
+        return;
+    }
+    need(ev->kind == BVC_EVALUATOR_WALKS && ev->scene && ev->problem && ev->cfg,
+         "walk evaluator needs scene, problem and cache config");
+    need(ev->scene->host.dim == 2, "walk evaluator scene must be 2D");
+    // makeDefaultEvaluator (cache.cpp:600-620): correctionWalks WoSt walks per crossing
+    WalkEnv W = make_env(ev->scene, *ev->problem, ev->cfg->walk, seed, stream, 1);
+    E.eps = W.eps;
+    int* counts = ws().get<int>(kWsCorrCounts, K);
+    int* offsets = ws().get<int>(kWsCorrOffsets, K);
+    launch_corr_rays(E, P->x.p, P->order.p, K, counts, nullptr, noHit, g_stream);
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts, offsets, K, g_stream));
+    CK(cub::DeviceScan::ExclusiveSum(ws().get<char>(kWsCorrScan, tmp), tmp, counts, offsets, K, g_stream));
+    count_launch();
+    int last[2] = {0, 0};
+    CK(cudaMemcpyAsync(&last[0], offsets + K - 1, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaMemcpyAsync(&last[1], counts + K - 1, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+    check_hits();
+    int H = last[0] + last[1];
+    if (H == 0) return;
+    float2* starts = ws().get<float2>(kWsCorrStarts, H);
+    long long* gid = ws().get<long long>(kWsCorrGid, H);
+    double* w = ws().get<double>(kWsCorrW, H);
+    launch_corr_emit(E, P->x.p, P->order.p, K, offsets, starts, gid, w, g_stream);
+    int nw = std::max(1, ev->cfg->correctionWalks);
+    auto* ctr = ws().get<unsigned long long>(kWsCounter, 3);
+    CK(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), g_stream));
+    WalkJob J{};
+    J.counter = ctr;
+    J.nU = nw;
+    J.nPtsU = H;
+    J.startU = starts;
+    J.gidU = gid;
+    J.outU = ws().get<float>(kWsCorrOut, static_cast<size_t>(H) * nw);
+    launch_walk_job(W, J, g_stream);
+    double* mean = ws().get<double>(kWsCorrMean, H);
+    launch_reduce_estimates(J.outU, H, nw, 1, 0, mean, nullptr, g_stream);
+    launch_corr_apply(offsets, counts, P->order.p, K, w, mean, E.nRound, P->bsum.p, g_stream);
+    CK(cudaGetLastError());
+}
+
+// correctedSourceSplat (cache.cpp:555-597)
+void corrected_source(bvc_source_cache_s* s, bvc_eval_points_s* P, bvc_region_s* R, const bvc_splat_config& cfg,
+                      double clamp, const bvc_field* f, uint64_t seed, uint64_t stream) {
+    require_device();
+    need(P && R, "null argument");
+    if (cfg.kernel.kind != BVC_KERNEL_POISSON || cfg.kernel.dim != 2)
+        throw Error(BVC_ERR_SOLVER, "ball-kernel source mode requires the 2D Poisson kernel");
+    if (!(clamp > 0.0)) throw Error(BVC_ERR_INVALID_ARGUMENT, "clamp bound must be positive");
+    need(P->dim == 2, "evaluation points must be 2D");
+    ensure_order(P);
+    require_ball(P);
+    bvc_splat_config c = cfg;
+    c.useBallGreens = 1;
+    splat(nullptr, s, P, c, 0, SIZE_MAX, true, false, kModeClampS, clamp);
+    int K = P->active;
+    if (!(std::isfinite(clamp) && f && f->kind != BVC_FIELD_NONE) || K == 0) return;
+    R->upload();
+    uint32_t k0, k1;
+    key_of(seed, stream, 0, k0, k1);
+    launch_ball_corr(R->boundary.view(), static_cast<float>(1e-7 * R->boundary.host.diagonal), P->x.p, P->order.p,
+                     P->ballR.p, K, to_dev(*f), clamp, static_cast<double>(s ? s->m : 0), k0, k1, P->ssum.p, g_stream);
+    CK(cudaGetLastError());
+}
+
+bvc_splat_config make_splat_config(bvc_scene_s* S, const bvc_problem& pb, const bvc_cache_config& cfg) {
+    validate_kernel(pb.kernel);
+    bvc_splat_config s{};
+    s.kernel = pb.kernel;
+    s.kernel.scale = S->host.diagonal;
+    s.coincidenceTol = 1e-12 * S->host.diagonal;
+    s.voronoi = cfg.voronoi;
+    s.useBallGreens = cfg.sourceBall;
+    if (s.useBallGreens && s.kernel.kind != BVC_KERNEL_POISSON)
+        throw Error(BVC_ERR_SOLVER, "ball-kernel source mode requires the Poisson kernel");
+    return s;
+}
+
+}  // namespace bvc_capi
+
+extern "C" {
+
+int bvc_make_splat_config(bvc_scene s, const bvc_problem* pb, const bvc_cache_config* cfg, bvc_splat_config* out) {
+    API({
+        need(s && pb && cfg && out, "null argument");
+        *out = make_splat_config(s, *pb, *cfg);
+    })
+}
+int bvc_splat_solution(bvc_boundary_cache b, bvc_source_cache s, bvc_eval_points p, const bvc_splat_config* cfg) {
+    API(need(cfg, "null config"); splat(b, s, p, *cfg, 0, SIZE_MAX, true, false))
+}
+int bvc_splat_gradient(bvc_boundary_cache b, bvc_source_cache s, bvc_eval_points p, const bvc_splat_config* cfg) {
+    API(need(cfg, "null config"); splat(b, s, p, *cfg, 0, SIZE_MAX, false, true))
+}
+int bvc_splat_solution_gradient(bvc_boundary_cache b, bvc_source_cache s, bvc_eval_points p, const bvc_splat_config* cfg) {
+    API(need(cfg, "null config"); splat(b, s, p, *cfg, 0, SIZE_MAX, true, true))
+}
+int bvc_splat_range(bvc_boundary_cache b, bvc_source_cache s, bvc_eval_points p, const bvc_splat_config* cfg,
+                    size_t begin, size_t end, int value, int gradient) {
+    API(need(cfg, "null config"); splat(b, s, p, *cfg, begin, end, value != 0, gradient != 0))
+}
+
+int bvc_corrected_boundary_splat(bvc_boundary_cache b, bvc_eval_points p, bvc_region r, const bvc_splat_config* cfg,
+                                 double clampBound, int clampMode, const bvc_boundary_evaluator* eval, uint64_t seed,
+                                 uint64_t stream) {
+    API(need(cfg, "null config"); corrected_boundary(b, p, r, *cfg, clampBound, clampMode, eval, seed, stream))
+}
+int bvc_corrected_source_splat(bvc_source_cache s, bvc_eval_points p, bvc_region r, const bvc_splat_config* cfg,
+                               double clampBound, const bvc_field* f, uint64_t seed, uint64_t stream) {
+    API(need(cfg, "null config"); corrected_source(s, p, r, *cfg, clampBound, f, seed, stream))
+}
+
+int bvc_update_solution(bvc_scene s, const bvc_problem* pb, bvc_region r, const bvc_cache_config* cfg,
+                        bvc_eval_points p, uint64_t seed, uint64_t round, int gradients, bvc_round_stats* stats) {
+    API({
+        require_device();
+        need(s && pb && r && cfg && p, "null argument");
+        validate_kernel(pb->kernel);
+        if (cfg->sourceBall && gradients)
+            throw Error(BVC_ERR_SOLVER, "ball-kernel source mode does not support gradient splats");
+        bvc_splat_config scfg = make_splat_config(s, *pb, *cfg);
+        need(cfg->clampMode >= BVC_CLAMP_OFF && cfg->clampMode <= BVC_CLAMP_CORRECT, "unknown clamp mode");
+        cudaEvent_t e0, e1, e2;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventCreate(&e2));
+        CK(cudaEventRecord(e0, g_stream));
+        bvc_boundary_cache_s bc;
+        bvc_source_cache_s sc;
+        GenStats st;
+        generate_cache(s, *pb, r, *cfg, seed, round, 0, std::max(1, cfg->nBoundary), &bc, st);
+        generate_source(*pb, r, *cfg, seed, round, &sc);
+        CK(cudaEventRecord(e1, g_stream));
+        bool hasSource = pb->f.kind != BVC_FIELD_NONE;
+        bvc_source_cache_s* sp = sc.m ? &sc : nullptr;
+        // the mode dispatch of updateSolution (cache.cpp:639-662)
+        if (cfg->clampMode == BVC_CLAMP_OFF) {
+            // ball mode: splatSolution with G^B plus the unclamped (infinite-bound,
+            // correction-free) ball source splat, i.e. one ball-kernel splat
+            splat(&bc, sp, p, scfg, 0, SIZE_MAX, true, gradients != 0);
+        } else {
+            double c = cfg->clamp > 0.0 ? cfg->clamp : 10.0 / s->host.diagonal;  // resolvedClamp cache.h:129-131
+            bvc_boundary_evaluator ev{};
+            ev.kind = BVC_EVALUATOR_WALKS;
+            ev.scene = s;
+            ev.problem = pb;
+            ev.cfg = cfg;
+            corrected_boundary(&bc, p, r, scfg, c, cfg->clampMode, &ev, seed, bvc_dev::mixKey(kBoundaryCorrSalt, round));
+            if (hasSource) {
+                if (cfg->sourceBall) {
+                    corrected_source(sp, p, r, scfg, c, &pb->f, seed, bvc_dev::mixKey(kSourceCorrSalt, round));
+                } else {
+                    splat(nullptr, sp, p, scfg, 0, SIZE_MAX, true, false);
+                }
+            }
+            if (gradients) splat(&bc, sp, p, scfg, 0, SIZE_MAX, false, true);
+        }
+        fallback_walks(s, *pb, *cfg, p, seed, round, gradients != 0);
+        CK(cudaEventRecord(e2, g_stream));
+        CK(cudaEventSynchronize(e2));
+        if (stats) {
+            stats->resampled = st.resampled;
+            stats->cacheWalks = st.walks;
+            stats->cacheTruncated = st.truncated;
+            stats->cacheSteps = st.steps;
+            stats->generateSeconds = device_seconds(e0, e1);
+            stats->splatSeconds = device_seconds(e1, e2);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaEventDestroy(e2);
+    })
+}
+
+}  // extern "C"

@@ -219,15 +219,14 @@ __device__ __forceinline__ bool ray_box3(const float4& lo, const float4& hi, flo
 }
 
 // the same slab test, returning the entry distance (kFInf on a miss)
-__device__ __forceinline__ float ray_box3_t(const float4& lo, const float4& hi, float ox, float oy, float oz,
+// oxi = ox * idx etc. (see ray_box_t in scene_dev.cuh): one FFMA per slab bound
+__device__ __forceinline__ float ray_box3_t(const float4& lo, const float4& hi, float oxi, float oyi, float ozi,
                                             float idx, float idy, float idz, float tMax) {
-    float t0 = 0.0f, t1 = tMax;
-    float tn = (lo.x - ox) * idx, tf = (hi.x - ox) * idx;
-    t0 = fmaxf(t0, fminf(tn, tf)); t1 = fminf(t1, fmaxf(tn, tf));
-    tn = (lo.y - oy) * idy; tf = (hi.y - oy) * idy;
-    t0 = fmaxf(t0, fminf(tn, tf)); t1 = fminf(t1, fmaxf(tn, tf));
-    tn = (lo.z - oz) * idz; tf = (hi.z - oz) * idz;
-    t0 = fmaxf(t0, fminf(tn, tf)); t1 = fminf(t1, fmaxf(tn, tf));
+    float tnx = fmaf(lo.x, idx, -oxi), tfx = fmaf(hi.x, idx, -oxi);
+    float tny = fmaf(lo.y, idy, -oyi), tfy = fmaf(hi.y, idy, -oyi);
+    float tnz = fmaf(lo.z, idz, -ozi), tfz = fmaf(hi.z, idz, -ozi);
+    float t0 = fmaxf(fmaxf(fminf(tnx, tfx), fminf(tny, tfy)), fmaxf(fminf(tnz, tfz), 0.0f));
+    float t1 = fminf(fminf(fmaxf(tnx, tfx), fmaxf(tny, tfy)), fminf(fmaxf(tnz, tfz), tMax));
     return t0 <= t1 ? t0 : kFInf;
 }
 

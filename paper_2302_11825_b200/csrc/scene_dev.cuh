@@ -238,18 +238,16 @@ __device__ __forceinline__ bool ray_box(const float4& b, float ox, float oy, flo
     return t0 <= t1;
 }
 
-// the same slab test, returning the entry distance (kFInf on a miss)
-__device__ __forceinline__ float ray_box_t(const float4& b, float ox, float oy, float idx, float idy, float tMax) {
-    float t0 = 0.0f, t1 = tMax;
-    float tn = (b.x - ox) * idx, tf = (b.z - ox) * idx;
-    if (tn > tf) { float s = tn; tn = tf; tf = s; }
-    t0 = fmaxf(t0, tn);
-    t1 = fminf(t1, tf);
-    tn = (b.y - oy) * idy;
-    tf = (b.w - oy) * idy;
-    if (tn > tf) { float s = tn; tn = tf; tf = s; }
-    t0 = fmaxf(t0, tn);
-    t1 = fminf(t1, tf);
+// the same slab test, returning the entry distance (kFInf on a miss). Takes the
+// origin premultiplied by the reciprocal direction (oxi = ox * idx), so each slab
+// bound is one FFMA; the rounding of oxi moves a slab by about ulp(ox) in position,
+// far inside the boxes' padding. An axis with idx = inf yields NaN bounds, which
+// fminf / fmaxf drop: that axis then does not constrain (conservative).
+__device__ __forceinline__ float ray_box_t(const float4& b, float oxi, float oyi, float idx, float idy, float tMax) {
+    float tnx = fmaf(b.x, idx, -oxi), tfx = fmaf(b.z, idx, -oxi);
+    float tny = fmaf(b.y, idy, -oyi), tfy = fmaf(b.w, idy, -oyi);
+    float t0 = fmaxf(fmaxf(fminf(tnx, tfx), fminf(tny, tfy)), 0.0f);
+    float t1 = fminf(fminf(fmaxf(tnx, tfx), fmaxf(tny, tfy)), tMax);
     return t0 <= t1 ? t0 : kFInf;
 }
 
@@ -273,6 +271,7 @@ __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, f
                                                 float tMax, unsigned qmask, float tMin, int skipSeg) {
     RayHit h{kFInf, 0.0f, 0.0f, 0.0f, -1};
     float idx = f_rcp(dx), idy = f_rcp(dy);  // slab tests on padded boxes: an approximate reciprocal suffices
+    const float oxi = ox * idx, oyi = oy * idy;
     float limit = tMax;
     // nearer child first (entry distance), the other pushed with its entry distance and
     // dropped at pop time once a hit closer than it is known; while-while structure
@@ -292,8 +291,8 @@ __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, f
         while (ref >= 0) {
             const Node2 nd = S.nodes[ref];
             count_fetch<COUNT>(S, 0);
-            float tl = (nd.mask & qmask) ? ray_box_t(nd.lbox, ox, oy, idx, idy, limit) : kFInf;
-            float tr = ((nd.mask >> 3) & qmask) ? ray_box_t(nd.rbox, ox, oy, idx, idy, limit) : kFInf;
+            float tl = (nd.mask & qmask) ? ray_box_t(nd.lbox, oxi, oyi, idx, idy, limit) : kFInf;
+            float tr = ((nd.mask >> 3) & qmask) ? ray_box_t(nd.rbox, oxi, oyi, idx, idy, limit) : kFInf;
             bool vl = tl != kFInf, vr = tr != kFInf;
             if (vl && vr) {
                 bool lf = tl <= tr;
