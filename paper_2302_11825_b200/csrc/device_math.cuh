@@ -79,6 +79,32 @@ inline float f_ex2(float x) { return std::exp2(x); }
 inline float f_rcp(float x) { return 1.0f / x; }
 inline float f_rsq(float x) { return 1.0f / std::sqrt(x); }
 #endif
+// packed FP32 pairs (sm_100a FFMA2 / FMUL2 / FADD2): one instruction, two lanes,
+// each lane rounded exactly like the scalar FFMA / FMUL / FADD
+struct F2 {
+    unsigned long long v;
+};
+__device__ __forceinline__ F2 pk(float lo, float hi) {
+    F2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ F2 bc(float x) { return pk(x, x); }
+__device__ __forceinline__ void upk(F2 a, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v)); }
+__device__ __forceinline__ F2 add2(F2 a, F2 b) { F2 r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
+__device__ __forceinline__ F2 sub2(F2 a, F2 b) { F2 r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
+__device__ __forceinline__ F2 mul2(F2 a, F2 b) { F2 r; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+    F2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+    return r;
+}
+template <class Fn>
+__device__ __forceinline__ F2 each(F2 a, Fn&& f) {
+    float lo, hi;
+    upk(a, lo, hi);
+    return pk(f(lo), f(hi));
+}
 BVC_HD float f_ln(float x) { return f_lg2(x) * kLn2; }
 BVC_HD float f_exp(float x) { return f_ex2(x * 1.44269504088896340736f); }
 

@@ -196,9 +196,9 @@ __device__ __forceinline__ void pair(const float4 a, const float4 b, float px, f
             if constexpr (!SRC) {
                 float ndA = fmaf(a.w, dx, fmaf(b.x, dy, __fmul_rn(b.y, dz)));
                 float pA = __fmul_rn(ndA, ir3);  // A p
-                // A p Q + B e / r = (e / r) (A (n.d) / r^2 (1 + s r) + B): two fewer ops per pair
+                // A p Q + B e / r = (e / r) (A (n.d) / r (s + 1 / r) + B): three fewer ops per pair
                 if constexpr (VAL)
-                    acc.v = fmaf(__fmul_rn(e, ir), fmaf(__fmul_rn(ndA, ir2), fmaf(s, r, 1.0f), b.w), acc.v);
+                    acc.v = fmaf(__fmul_rn(e, ir), fmaf(__fmul_rn(ndA, ir), __fadd_rn(s, ir), b.w), acc.v);
                 if constexpr (GRAD) {
                     float q = fmaf(3.0f * Q * pA, ir2, b.w * Q * ir3);
                     q = fmaf(sigma * e, pA, q);
@@ -225,30 +225,6 @@ __device__ __forceinline__ void pair(const float4 a, const float4 b, float px, f
 // in one issue slot (measured: FFMA2 sustains the full 128 FP32 FMA/clk/SM), which
 // leaves slots for the MUFU, LDS and loop instructions. Scalar sample operands
 // broadcast for free (ptxas folds them into a .F32 operand).
-struct F2 {
-    unsigned long long v;
-};
-__device__ __forceinline__ F2 pk(float lo, float hi) {
-    F2 r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
-    return r;
-}
-__device__ __forceinline__ F2 bc(float x) { return pk(x, x); }
-__device__ __forceinline__ void upk(F2 a, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v)); }
-__device__ __forceinline__ F2 add2(F2 a, F2 b) { F2 r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
-__device__ __forceinline__ F2 sub2(F2 a, F2 b) { F2 r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
-__device__ __forceinline__ F2 mul2(F2 a, F2 b) { F2 r; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
-__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
-    F2 r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
-    return r;
-}
-template <class Fn>
-__device__ __forceinline__ F2 each(F2 a, Fn&& f) {
-    float lo, hi;
-    upk(a, lo, hi);
-    return pk(f(lo), f(hi));
-}
 struct Acc2 {
     F2 v, gx, gy, gz;
 };
@@ -327,7 +303,7 @@ __device__ __forceinline__ void pair2(const float4 a, const float4 b, F2 px, F2 
             F2 e = each(mul2(r, bc(-1.44269504088896340736f * s)), [](float x) { return f_ex2(x); });
             if constexpr (!SRC) {
                 F2 ndA = fma2(bc(a.w), dx, fma2(bc(b.x), dy, mul2(bc(b.y), dz)));
-                acc.v = fma2(mul2(e, ir), fma2(mul2(ndA, ir2), fma2(bc(s), r, bc(1.0f)), bc(b.w)), acc.v);
+                acc.v = fma2(mul2(e, ir), fma2(mul2(ndA, ir), add2(bc(s), ir), bc(b.w)), acc.v);
             } else {
                 acc.v = fma2(mul2(bc(a.w), ir), e, acc.v);
             }

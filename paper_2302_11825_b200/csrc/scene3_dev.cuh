@@ -47,6 +47,16 @@ __device__ __forceinline__ float box3_dist2(const float4& lo, const float4& hi, 
     float dz = fmaxf(fmaxf(lo.z - z, 0.0f), z - hi.z);
     return dx * dx + dy * dy + dz * dz;
 }
+// the same with (x, y) packed: the x and y differences are two FADD2
+__device__ __forceinline__ float box3_dist2(const float4& lo, const float4& hi, F2 pxy, float z) {
+    float ax, ay, cx, cy;
+    upk(sub2(pk(lo.x, lo.y), pxy), ax, ay);
+    upk(sub2(pxy, pk(hi.x, hi.y)), cx, cy);
+    float dx = fmaxf(fmaxf(ax, 0.0f), cx);
+    float dy = fmaxf(fmaxf(ay, 0.0f), cy);
+    float dz = fmaxf(fmaxf(lo.z - z, 0.0f), z - hi.z);
+    return dx * dx + dy * dy + dz * dz;
+}
 
 // closest point on triangle abc to p (Ericson, Real-Time Collision Detection 5.1.5)
 __device__ __forceinline__ float tri_closest(const Prim3& t, float px, float py, float pz, float& qx, float& qy,
@@ -104,6 +114,7 @@ __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, flo
                                                Visit&& visit, Thr&& threshold) {
     unsigned long long stack[kStack];  // (distance bits << 32 | ref): one local load per pop
     int sp = 0, ref = 0;
+    const F2 pxy = pk(x, y);
     auto pop = [&]() -> bool {  // next entry still within the pruning radius; false when empty
         for (;;) {
             if (sp == 0) return false;
@@ -119,8 +130,8 @@ __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, flo
             const Node3 nd = S.nodes[ref];
             count_fetch3<COUNT>(S, 0);
             float thr = threshold();
-            float dl = (nd.mask & qmask) ? box3_dist2(nd.llo, nd.lhi, x, y, z) : kFInf;
-            float dr = ((nd.mask >> 3) & qmask) ? box3_dist2(nd.rlo, nd.rhi, x, y, z) : kFInf;
+            float dl = (nd.mask & qmask) ? box3_dist2(nd.llo, nd.lhi, pxy, z) : kFInf;
+            float dr = ((nd.mask >> 3) & qmask) ? box3_dist2(nd.rlo, nd.rhi, pxy, z) : kFInf;
             bool vl = dl <= thr, vr = dr <= thr;
             if (vl && vr) {
                 bool lfirst = dl <= dr;
@@ -220,11 +231,12 @@ __device__ __forceinline__ bool ray_box3(const float4& lo, const float4& hi, flo
 
 // the same slab test, returning the entry distance (kFInf on a miss)
 // oxi = ox * idx etc. (see ray_box_t in scene_dev.cuh): one FFMA per slab bound
-__device__ __forceinline__ float ray_box3_t(const float4& lo, const float4& hi, float oxi, float oyi, float ozi,
-                                            float idx, float idy, float idz, float tMax) {
-    float tnx = fmaf(lo.x, idx, -oxi), tfx = fmaf(hi.x, idx, -oxi);
-    float tny = fmaf(lo.y, idy, -oyi), tfy = fmaf(hi.y, idy, -oyi);
-    float tnz = fmaf(lo.z, idz, -ozi), tfz = fmaf(hi.z, idz, -ozi);
+__device__ __forceinline__ float ray_box3_t(const float4& lo, const float4& hi, F2 noixy, float nozi, F2 idxy, float idz,
+                                            float tMax) {
+    float tnx, tny, tfx, tfy;
+    upk(fma2(pk(lo.x, lo.y), idxy, noixy), tnx, tny);
+    upk(fma2(pk(hi.x, hi.y), idxy, noixy), tfx, tfy);
+    float tnz = fmaf(lo.z, idz, nozi), tfz = fmaf(hi.z, idz, nozi);
     float t0 = fmaxf(fmaxf(fminf(tnx, tfx), fminf(tny, tfy)), fmaxf(fminf(tnz, tfz), 0.0f));
     float t1 = fminf(fminf(fmaxf(tnx, tfx), fmaxf(tny, tfy)), fminf(fmaxf(tnz, tfz), tMax));
     return t0 <= t1 ? t0 : kFInf;

@@ -56,6 +56,15 @@ __device__ __forceinline__ float box_dist2(const float4& b, float x, float y) {
     float dy = fmaxf(fmaxf(b.y - y, 0.0f), y - b.w);
     return dx * dx + dy * dy;
 }
+// the same with p = (x, y) packed: the four differences are two FADD2
+__device__ __forceinline__ float box_dist2(const float4& b, F2 p) {
+    float ax, ay, cx, cy;
+    upk(sub2(pk(b.x, b.y), p), ax, ay);
+    upk(sub2(p, pk(b.z, b.w)), cx, cy);
+    float dx = fmaxf(fmaxf(ax, 0.0f), cx);
+    float dy = fmaxf(fmaxf(ay, 0.0f), cy);
+    return dx * dx + dy * dy;
+}
 
 // closest point on a segment (bvh.h:153-159); returns squared distance
 __device__ __forceinline__ float seg_closest(const float4& s, float x, float y, float& px, float& py, float& t) {
@@ -87,6 +96,7 @@ __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, floa
     unsigned long long stack[kStack];
     int sp = 0;
     int ref = 0;
+    const F2 p2 = pk(x, y);
     auto pop = [&]() -> bool {  // next entry still within the pruning radius; false when empty
         for (;;) {
             if (sp == 0) return false;
@@ -102,8 +112,8 @@ __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, floa
             const Node2 nd = S.nodes[ref];
             count_fetch<COUNT>(S, 0);
             float thr = threshold();
-            float dl = (nd.mask & qmask) ? box_dist2(nd.lbox, x, y) : kFInf;
-            float dr = ((nd.mask >> 3) & qmask) ? box_dist2(nd.rbox, x, y) : kFInf;
+            float dl = (nd.mask & qmask) ? box_dist2(nd.lbox, p2) : kFInf;
+            float dr = ((nd.mask >> 3) & qmask) ? box_dist2(nd.rbox, p2) : kFInf;
             bool vl = dl <= thr, vr = dr <= thr;
             if (vl && vr) {
                 int nearRef = dl <= dr ? nd.left : nd.right;
@@ -243,9 +253,10 @@ __device__ __forceinline__ bool ray_box(const float4& b, float ox, float oy, flo
 // bound is one FFMA; the rounding of oxi moves a slab by about ulp(ox) in position,
 // far inside the boxes' padding. An axis with idx = inf yields NaN bounds, which
 // fminf / fmaxf drop: that axis then does not constrain (conservative).
-__device__ __forceinline__ float ray_box_t(const float4& b, float oxi, float oyi, float idx, float idy, float tMax) {
-    float tnx = fmaf(b.x, idx, -oxi), tfx = fmaf(b.z, idx, -oxi);
-    float tny = fmaf(b.y, idy, -oyi), tfy = fmaf(b.w, idy, -oyi);
+__device__ __forceinline__ float ray_box_t(const float4& b, F2 noi, F2 id, float tMax) {  // noi = -(ox idx, oy idy)
+    float tnx, tny, tfx, tfy;
+    upk(fma2(pk(b.x, b.y), id, noi), tnx, tny);
+    upk(fma2(pk(b.z, b.w), id, noi), tfx, tfy);
     float t0 = fmaxf(fmaxf(fminf(tnx, tfx), fminf(tny, tfy)), 0.0f);
     float t1 = fminf(fminf(fmaxf(tnx, tfx), fmaxf(tny, tfy)), tMax);
     return t0 <= t1 ? t0 : kFInf;
@@ -271,7 +282,7 @@ __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, f
                                                 float tMax, unsigned qmask, float tMin, int skipSeg) {
     RayHit h{kFInf, 0.0f, 0.0f, 0.0f, -1};
     float idx = f_rcp(dx), idy = f_rcp(dy);  // slab tests on padded boxes: an approximate reciprocal suffices
-    const float oxi = ox * idx, oyi = oy * idy;
+    const F2 id2 = pk(idx, idy), noi2 = pk(-(ox * idx), -(oy * idy));
     float limit = tMax;
     // nearer child first (entry distance), the other pushed with its entry distance and
     // dropped at pop time once a hit closer than it is known; while-while structure
@@ -291,8 +302,8 @@ __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, f
         while (ref >= 0) {
             const Node2 nd = S.nodes[ref];
             count_fetch<COUNT>(S, 0);
-            float tl = (nd.mask & qmask) ? ray_box_t(nd.lbox, oxi, oyi, idx, idy, limit) : kFInf;
-            float tr = ((nd.mask >> 3) & qmask) ? ray_box_t(nd.rbox, oxi, oyi, idx, idy, limit) : kFInf;
+            float tl = (nd.mask & qmask) ? ray_box_t(nd.lbox, noi2, id2, limit) : kFInf;
+            float tr = ((nd.mask >> 3) & qmask) ? ray_box_t(nd.rbox, noi2, id2, limit) : kFInf;
             bool vl = tl != kFInf, vr = tr != kFInf;
             if (vl && vr) {
                 bool lf = tl <= tr;

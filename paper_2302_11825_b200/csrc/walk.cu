@@ -277,8 +277,11 @@ __device__ __forceinline__ U4 draw4(const WalkEnv& E, Task& t) {
     return philox4x32_10(c, E.k0, E.k1);
 }
 
-template <bool NEU, bool SCR, bool SRC, bool COUNT>
-__global__ void __launch_bounds__(kWalkThreads, NEU ? 4 : 6) walk_kernel(const WalkEnv E, const WalkJob J) {
+// resident blocks per SM (registers per thread = 64K / (256 x MINB)), measured on
+// C1-C3: Neumann scenes 4 (C2: 6.36 ms vs 6.72 at 6), screened 8 (C3: 148 vs 155 ms
+// at 6), plain Laplace 6 (C1: 1.29 vs 1.40 ms at 8)
+template <bool NEU, bool SCR, bool SRC, bool COUNT, int MINB = NEU ? 4 : (SCR ? 8 : 6)>
+__global__ void __launch_bounds__(kWalkThreads, MINB) walk_kernel(const WalkEnv E, const WalkJob J) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const long long nUtot = static_cast<long long>(J.nPtsU) * J.nU;

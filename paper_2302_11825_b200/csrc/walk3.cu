@@ -16,8 +16,6 @@
 // sampleBallGreens is 2D-only, kernels.cpp:98-99).
 #include <cuda_runtime.h>
 
-#include <cstdlib>
-
 #include "internal.h"
 #include "scene3_dev.cuh"
 
@@ -85,7 +83,8 @@ __device__ __forceinline__ Hit3 ray_neumann3(const WalkEnv3& E, float ox, float 
                                              float dz, float tMax, int skip) {
     Hit3 h{kFInf, -1};
     float idx = f_rcp(dx), idy = f_rcp(dy), idz = f_rcp(dz);  // slab tests on padded boxes
-    const float oxi = ox * idx, oyi = oy * idy, ozi = oz * idz;
+    const F2 idxy = pk(idx, idy), noixy = pk(-(ox * idx), -(oy * idy));
+    const float nozi = -(oz * idz);
     float limit = tMax;
     // nearer child first, the other pushed with its entry distance (dropped at pop once
     // a closer hit is known); while-while structure
@@ -105,8 +104,8 @@ __device__ __forceinline__ Hit3 ray_neumann3(const WalkEnv3& E, float ox, float 
         while (ref >= 0) {
             const Node3 nd = E.S.nodes[ref];
             count_fetch3<COUNT>(E.S, 0);
-            float tl = (nd.mask & kClsNeumann) ? ray_box3_t(nd.llo, nd.lhi, oxi, oyi, ozi, idx, idy, idz, limit) : kFInf;
-            float tr = ((nd.mask >> 3) & kClsNeumann) ? ray_box3_t(nd.rlo, nd.rhi, oxi, oyi, ozi, idx, idy, idz, limit)
+            float tl = (nd.mask & kClsNeumann) ? ray_box3_t(nd.llo, nd.lhi, noixy, nozi, idxy, idz, limit) : kFInf;
+            float tr = ((nd.mask >> 3) & kClsNeumann) ? ray_box3_t(nd.rlo, nd.rhi, noixy, nozi, idxy, idz, limit)
                                                       : kFInf;
             bool vl = tl != kFInf, vr = tr != kFInf;
             if (vl && vr) {
@@ -291,8 +290,10 @@ __device__ __forceinline__ U4 draw3(const WalkEnv3& E, Task3& t) {
     return philox4x32_10(c, E.k0, E.k1);
 }
 
-template <bool NEU, bool SCR, bool COUNT, int MINB = 6>
-__global__ void __launch_bounds__(kThreads3, MINB) walk3_kernel(const WalkEnv3 E, const WalkJob3 J) {
+// 8 resident blocks per SM at 32 registers (spilling) beat fewer blocks with more
+// registers (C5: 4.24 s at 8, 4.47 s at 6, 5.58 s at 4; C4: 548 / 552 / 716 ms)
+template <bool NEU, bool SCR, bool COUNT>
+__global__ void __launch_bounds__(kThreads3, 8) walk3_kernel(const WalkEnv3 E, const WalkJob3 J) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const long long nUtot = static_cast<long long>(J.nPtsU) * J.nU;
@@ -537,25 +538,16 @@ __global__ void farfield3_kernel(const SceneView3 S, const FarField F, float* d)
     d[i] = sqrtf(closest_point3(S, x, y, z, kClsAny).d2);
 }
 
-template <bool NEU, bool SCR, bool COUNT, int MINB>
-void launch_walk3_m(const WalkEnv3& env, const WalkJob3& job, long long total, cudaStream_t st) {
+template <bool NEU, bool SCR, bool COUNT>
+void launch_walk3_t(const WalkEnv3& env, const WalkJob3& job, long long total, cudaStream_t st) {
     int dev = 0, sms = 148, perSm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, walk3_kernel<NEU, SCR, COUNT, MINB>, kThreads3, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, walk3_kernel<NEU, SCR, COUNT>, kThreads3, 0);
     perSm = perSm > 0 ? perSm : 1;
     long long want = (total + kThreads3 - 1) / kThreads3;
     int grid = static_cast<int>(want < static_cast<long long>(sms) * perSm ? want : static_cast<long long>(sms) * perSm);
-    walk3_kernel<NEU, SCR, COUNT, MINB><<<grid, kThreads3, 0, st>>>(env, job);
-}
-template <bool NEU, bool SCR, bool COUNT>
-void launch_walk3_t(const WalkEnv3& env, const WalkJob3& job, long long total, cudaStream_t st) {
-    static const int minb = [] { const char* e = std::getenv("BVC_WALK3_MINB"); return e ? std::atoi(e) : 6; }();
-    if constexpr (!COUNT) {
-        if (minb == 7) return launch_walk3_m<NEU, SCR, COUNT, 7>(env, job, total, st);
-        if (minb == 8) return launch_walk3_m<NEU, SCR, COUNT, 8>(env, job, total, st);
-    }
-    launch_walk3_m<NEU, SCR, COUNT, 6>(env, job, total, st);
+    walk3_kernel<NEU, SCR, COUNT><<<grid, kThreads3, 0, st>>>(env, job);
 }
 
 void launch_farfield3(const SceneView3& S, const FarField& F, float* d, cudaStream_t st) {
