@@ -303,7 +303,7 @@ def phase_breakdown(B, c, scene, region, pts, args):
     # walk traffic: algorithmic bytes per step from a counting launch
     prof = B.walk_traffic_profile(scene, c.problem, region, cfg, c.seed, 77)
     steps = max(prof["steps"], 1.0)
-    node_b, prim_b = (80, 48) if c.dim == 3 else (48, 32)  # Node3 / Prim3 vs Node2 / Prim2
+    node_b, prim_b = (64, 48) if c.dim == 3 else (48, 32)  # Node3 / Prim3 vs Node2 / Prim2
     bytes_per_step = (prof["node_fetches"] * node_b + prof["prim_fetches"] * prim_b) / steps + 32.0
     walk_bytes = bytes_per_step * stats["cacheSteps"]
     achieved = walk_bytes / t_gen / 1e9

@@ -158,10 +158,7 @@ void bvc_scene_s::upload3() {
             hn[i].lhi = make_float4(b[3], b[4], b[5], 0.f);
             hn[i].rlo = make_float4(b[6], b[7], b[8], 0.f);
             hn[i].rhi = make_float4(b[9], b[10], b[11], 0.f);
-            hn[i].left = bvh.children[2 * i];
-            hn[i].right = bvh.children[2 * i + 1];
-            hn[i].mask = bvh.masks[i];
-            hn[i].pad = 0;
+            hn[i].set_links(bvh.children[2 * i], bvh.children[2 * i + 1], bvh.masks[i]);
         }
         nodes3.upload(hn.data(), nn);
         std::vector<bvc_dev::Prim3> hp(host.ns);

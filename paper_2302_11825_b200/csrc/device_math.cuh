@@ -9,6 +9,7 @@
 //    PdeProblem, pointwise.h:19-26; names follow tools/src/fields.cpp:30-72).
 #pragma once
 #include <cstdint>
+#include <cstring>
 
 #ifndef BVC_HD
 #define BVC_HD __host__ __device__ __forceinline__
@@ -63,6 +64,26 @@ BVC_HD uint64_t mix64(uint64_t z) {
 }
 BVC_HD uint64_t mixKey(uint64_t key, uint64_t counter) {
     return mix64(key ^ (counter + 0x9e3779b97f4a7c15ull));
+}
+
+// float <-> int bit casts usable on both sides (node links stored in float slots)
+BVC_HD int float_bits(float f) {
+#ifdef __CUDA_ARCH__
+    return __float_as_int(f);
+#else
+    int i;
+    std::memcpy(&i, &f, sizeof i);
+    return i;
+#endif
+}
+BVC_HD float bits_float(int i) {
+#ifdef __CUDA_ARCH__
+    return __int_as_float(i);
+#else
+    float f;
+    std::memcpy(&f, &i, sizeof f);
+    return f;
+#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -223,10 +223,7 @@ __global__ void emit3_kernel(const Tmp* t, const Build* b, int nInternal, float 
     o.lhi = make_float4(q.box[0][3] + pad, q.box[0][4] + pad, q.box[0][5] + pad, 0.f);
     o.rlo = make_float4(q.box[1][0] - pad, q.box[1][1] - pad, q.box[1][2] - pad, 0.f);
     o.rhi = make_float4(q.box[1][3] + pad, q.box[1][4] + pad, q.box[1][5] + pad, 0.f);
-    o.left = t[i].left;
-    o.right = t[i].right;
-    o.mask = q.mask[0] | (q.mask[1] << 3);
-    o.pad = 0;
+    o.set_links(t[i].left, t[i].right, q.mask[0] | (q.mask[1] << 3));
     out[i] = o;
 }
 __global__ void prims2_kernel(PrimIn in, const int* ids, int n, Prim2* out) {

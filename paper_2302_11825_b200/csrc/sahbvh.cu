@@ -277,10 +277,7 @@ __global__ void __launch_bounds__(kB) sah_level_kernel(SahIn in, int* ids, int* 
             o.lhi = make_float4(bx[0][3], bx[0][4], bx[0][5], 0.f);
             o.rlo = make_float4(bx[1][0], bx[1][1], bx[1][2], 0.f);
             o.rhi = make_float4(bx[1][3], bx[1][4], bx[1][5], 0.f);
-            o.left = ref[0];
-            o.right = ref[1];
-            o.mask = m;
-            o.pad = 0;
+            o.set_links(ref[0], ref[1], m);
             static_cast<Node3*>(nodesOut)[task.node] = o;
         }
     }

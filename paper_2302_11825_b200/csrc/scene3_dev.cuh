@@ -9,14 +9,24 @@
 
 namespace bvc_dev {
 
-struct alignas(16) Node3 {
-    float4 llo, lhi;  // left box (xyz, w unused)
-    float4 rlo, rhi;  // right box
-    int left, right;
-    unsigned mask;    // class masks as Node2 (left | right << 3)
-    int pad;
+// 64 bytes, 64-byte aligned: one node is half a 128-byte line (4 x LDG.128). The
+// child refs and the class masks live in the w slots of the boxes.
+struct alignas(64) Node3 {
+    float4 llo;  // left box lo (xyz), w = left child ref (int bits)
+    float4 lhi;  // left box hi, w = right child ref
+    float4 rlo;  // right box lo, w = class masks as Node2 (left | right << 3)
+    float4 rhi;  // right box hi, w unused
+    BVC_HD int left() const { return float_bits(llo.w); }
+    BVC_HD int right() const { return float_bits(lhi.w); }
+    BVC_HD unsigned mask() const { return static_cast<unsigned>(float_bits(rlo.w)); }
+    BVC_HD void set_links(int l, int r, unsigned m) {
+        llo.w = bits_float(l);
+        lhi.w = bits_float(r);
+        rlo.w = bits_float(static_cast<int>(m));
+        rhi.w = 0.0f;
+    }
 };
-static_assert(sizeof(Node3) == 80, "Node3 layout");
+static_assert(sizeof(Node3) == 64, "Node3 layout");
 
 struct alignas(16) Prim3 {
     float4 a;  // a.xyz, w = id (as int bits)
@@ -130,18 +140,18 @@ __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, flo
             const Node3 nd = S.nodes[ref];
             count_fetch3<COUNT>(S, 0);
             float thr = threshold();
-            float dl = (nd.mask & qmask) ? box3_dist2(nd.llo, nd.lhi, pxy, z) : kFInf;
-            float dr = ((nd.mask >> 3) & qmask) ? box3_dist2(nd.rlo, nd.rhi, pxy, z) : kFInf;
+            float dl = (nd.mask() & qmask) ? box3_dist2(nd.llo, nd.lhi, pxy, z) : kFInf;
+            float dr = ((nd.mask() >> 3) & qmask) ? box3_dist2(nd.rlo, nd.rhi, pxy, z) : kFInf;
             bool vl = dl <= thr, vr = dr <= thr;
             if (vl && vr) {
                 bool lfirst = dl <= dr;
                 stack[sp++] = (static_cast<unsigned long long>(__float_as_uint(fmaxf(dl, dr))) << 32) |
-                              static_cast<unsigned>(lfirst ? nd.right : nd.left);
-                ref = lfirst ? nd.left : nd.right;
+                              static_cast<unsigned>(lfirst ? nd.right() : nd.left());
+                ref = lfirst ? nd.left() : nd.right();
             } else if (vl) {
-                ref = nd.left;
+                ref = nd.left();
             } else if (vr) {
-                ref = nd.right;
+                ref = nd.right();
             } else if (!pop()) {
                 return;
             }
@@ -257,11 +267,11 @@ __device__ __forceinline__ bool inside3(const SceneView3& S, float x, float y, f
     for (;;) {
         if (ref >= 0) {
             const Node3 nd = S.nodes[ref];
-            bool vl = (nd.mask & 7u) && ray_box3(nd.llo, nd.lhi, x, y, z, idx, idy, idz, kFInf);
-            bool vr = ((nd.mask >> 3) & 7u) && ray_box3(nd.rlo, nd.rhi, x, y, z, idx, idy, idz, kFInf);
-            if (vl && vr) { stack[sp++] = nd.right; ref = nd.left; continue; }
-            if (vl) { ref = nd.left; continue; }
-            if (vr) { ref = nd.right; continue; }
+            bool vl = (nd.mask() & 7u) && ray_box3(nd.llo, nd.lhi, x, y, z, idx, idy, idz, kFInf);
+            bool vr = ((nd.mask() >> 3) & 7u) && ray_box3(nd.rlo, nd.rhi, x, y, z, idx, idy, idz, kFInf);
+            if (vl && vr) { stack[sp++] = nd.right(); ref = nd.left(); continue; }
+            if (vl) { ref = nd.left(); continue; }
+            if (vr) { ref = nd.right(); continue; }
         } else {
             int code = ~ref;
             int start = code >> 3, count = (code & 7) + 1;

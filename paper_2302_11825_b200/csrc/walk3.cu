@@ -104,19 +104,19 @@ __device__ __forceinline__ Hit3 ray_neumann3(const WalkEnv3& E, float ox, float 
         while (ref >= 0) {
             const Node3 nd = E.S.nodes[ref];
             count_fetch3<COUNT>(E.S, 0);
-            float tl = (nd.mask & kClsNeumann) ? ray_box3_t(nd.llo, nd.lhi, noixy, nozi, idxy, idz, limit) : kFInf;
-            float tr = ((nd.mask >> 3) & kClsNeumann) ? ray_box3_t(nd.rlo, nd.rhi, noixy, nozi, idxy, idz, limit)
+            float tl = (nd.mask() & kClsNeumann) ? ray_box3_t(nd.llo, nd.lhi, noixy, nozi, idxy, idz, limit) : kFInf;
+            float tr = ((nd.mask() >> 3) & kClsNeumann) ? ray_box3_t(nd.rlo, nd.rhi, noixy, nozi, idxy, idz, limit)
                                                       : kFInf;
             bool vl = tl != kFInf, vr = tr != kFInf;
             if (vl && vr) {
                 bool lf = tl <= tr;
                 stack[sp++] = (static_cast<unsigned long long>(__float_as_uint(lf ? tr : tl)) << 32) |
-                              static_cast<unsigned>(lf ? nd.right : nd.left);
-                ref = lf ? nd.left : nd.right;
+                              static_cast<unsigned>(lf ? nd.right() : nd.left());
+                ref = lf ? nd.left() : nd.right();
             } else if (vl) {
-                ref = nd.left;
+                ref = nd.left();
             } else if (vr) {
-                ref = nd.right;
+                ref = nd.right();
             } else if (!pop()) {
                 return h;
             }
