@@ -9,9 +9,9 @@
 
 namespace bvc_dev {
 
-// 64 bytes, 64-byte aligned: one node is half a 128-byte line (4 x LDG.128). The
+// 64 bytes: one node is half a 128-byte line (4 x LDG.128). The
 // child refs and the class masks live in the w slots of the boxes.
-struct alignas(64) Node3 {
+struct alignas(16) Node3 {  // 64 B; device arrays are 256-B aligned, and an over-aligned device local (a 128-B node) miscompiled
     float4 llo;  // left box lo (xyz), w = left child ref (int bits)
     float4 lhi;  // left box hi, w = right child ref
     float4 rlo;  // right box lo, w = class masks as Node2 (left | right << 3)
