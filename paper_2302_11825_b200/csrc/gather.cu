@@ -61,6 +61,150 @@ __device__ __forceinline__ void k0_q(float t, float& K0, float& Q) {
     }
 }
 
+// --- screened 2D, written once for one lane (float) and two packed lanes (F2) ----
+// Every product and sum is an explicit fma / mul (never a mul feeding an add, which
+// ptxas would contract for f32x2), so a point gets identical bits on the scalar path
+// (slow tiles, clamp modes, eval_kernels) and on the packed one.
+struct SOps {
+    using V = float;
+    static __device__ __forceinline__ V c(float x) { return x; }
+    static __device__ __forceinline__ V mul(V a, V b) { return __fmul_rn(a, b); }
+    static __device__ __forceinline__ V sub(V a, V b) { return __fsub_rn(a, b); }
+    static __device__ __forceinline__ V fma(V a, V b, V d) { return fmaf(a, b, d); }
+    template <class Fn>
+    static __device__ __forceinline__ V map(V a, Fn&& f) { return f(a); }
+};
+struct POps {
+    using V = F2;
+    static __device__ __forceinline__ V c(float x) { return bc(x); }
+    static __device__ __forceinline__ V mul(V a, V b) { return mul2(a, b); }
+    static __device__ __forceinline__ V sub(V a, V b) { return sub2(a, b); }
+    static __device__ __forceinline__ V fma(V a, V b, V d) { return fma2(a, b, d); }
+    template <class Fn>
+    static __device__ __forceinline__ V map(V a, Fn&& f) { return each(a, f); }
+};
+
+// K0(t) and Q = t K1(t) for t <= 2 (A&S 9.8.1-9.8.4 with I0/I1 9.8.1/9.8.3), Horner with fma
+template <class O>
+__device__ __forceinline__ void k0q_small(typename O::V t, typename O::V& K0, typename O::V& Q) {
+    using V = typename O::V;
+    const V h = O::mul(t, O::c(0.5f));
+    const V y = O::mul(h, h);
+    const V l = O::map(h, [](float x) { return f_lg2(x); });
+    const V lnh = O::mul(l, O::c(kLn2)), nlnh = O::mul(l, O::c(-kLn2));
+    const V w = O::mul(O::mul(t, t), O::c(1.0f / 14.0625f));
+    V i0 = O::fma(w, O::c(0.0045813f), O::c(0.0360768f));
+    i0 = O::fma(w, i0, O::c(0.2659732f));
+    i0 = O::fma(w, i0, O::c(1.2067492f));
+    i0 = O::fma(w, i0, O::c(3.0899424f));
+    i0 = O::fma(w, i0, O::c(3.5156229f));
+    i0 = O::fma(w, i0, O::c(1.0f));
+    V i1 = O::fma(w, O::c(0.00032411f), O::c(0.00301532f));
+    i1 = O::fma(w, i1, O::c(0.02658733f));
+    i1 = O::fma(w, i1, O::c(0.15084934f));
+    i1 = O::fma(w, i1, O::c(0.51498869f));
+    i1 = O::fma(w, i1, O::c(0.87890594f));
+    i1 = O::fma(w, i1, O::c(0.5f));
+    i1 = O::mul(t, i1);
+    V p0 = O::fma(y, O::c(0.0000074f), O::c(0.00010750f));
+    p0 = O::fma(y, p0, O::c(0.00262698f));
+    p0 = O::fma(y, p0, O::c(0.03488590f));
+    p0 = O::fma(y, p0, O::c(0.23069756f));
+    p0 = O::fma(y, p0, O::c(0.42278420f));
+    p0 = O::fma(y, p0, O::c(-0.57721566f));
+    V p1 = O::fma(y, O::c(-0.00004686f), O::c(-0.00110404f));
+    p1 = O::fma(y, p1, O::c(-0.01919402f));
+    p1 = O::fma(y, p1, O::c(-0.18156897f));
+    p1 = O::fma(y, p1, O::c(-0.67278579f));
+    p1 = O::fma(y, p1, O::c(0.15443144f));
+    p1 = O::fma(y, p1, O::c(1.0f));
+    K0 = O::fma(nlnh, i0, p0);
+    Q = O::fma(O::mul(t, lnh), i1, p1);
+}
+// the same for t > 2 (A&S 9.8.5-9.8.8)
+template <class O>
+__device__ __forceinline__ void k0q_large(typename O::V t, typename O::V& K0, typename O::V& Q) {
+    using V = typename O::V;
+    const V rt = O::map(t, [](float x) { return f_rsq(x); });
+    const V e = O::map(O::mul(t, O::c(-1.44269504088896340736f)), [](float x) { return f_ex2(x); });
+    const V y = O::mul(O::mul(rt, rt), O::c(2.0f));
+    V p0 = O::fma(y, O::c(0.00053208f), O::c(-0.00251540f));
+    p0 = O::fma(y, p0, O::c(0.00587872f));
+    p0 = O::fma(y, p0, O::c(-0.01062446f));
+    p0 = O::fma(y, p0, O::c(0.02189568f));
+    p0 = O::fma(y, p0, O::c(-0.07832358f));
+    p0 = O::fma(y, p0, O::c(1.25331414f));
+    V p1 = O::fma(y, O::c(-0.00068245f), O::c(0.00325614f));
+    p1 = O::fma(y, p1, O::c(-0.00780353f));
+    p1 = O::fma(y, p1, O::c(0.01504268f));
+    p1 = O::fma(y, p1, O::c(-0.03655620f));
+    p1 = O::fma(y, p1, O::c(0.23498619f));
+    p1 = O::fma(y, p1, O::c(1.25331414f));
+    const V er = O::mul(e, rt);
+    K0 = O::mul(p0, er);
+    Q = O::mul(O::mul(p1, er), t);
+}
+
+// One screened-2D pair (kernels.h:62-129 with G = -K0/2pi folded into the payload):
+// a = (zx, zy, nx, ny), b = (w u / 2pi, w d / 2pi) for a boundary sample, b.x =
+// (f / pdf) / 2pi for a source sample. K0/Q pick their branch per lane.
+template <class O, bool SRC, bool VAL, bool GRAD, int MODE>
+__device__ __forceinline__ void scr2_pair(const float4 a, const float4 b, typename O::V px, typename O::V py,
+                                          float sigma, float s, typename O::V& v, typename O::V& gx,
+                                          typename O::V& gy, typename O::V& r2out, float c2pi) {
+    using V = typename O::V;
+    const V dx = O::sub(O::c(a.x), px), dy = O::sub(O::c(a.y), py);
+    const V r2 = O::fma(dx, dx, O::mul(dy, dy));
+    r2out = r2;
+    const V ir = O::map(r2, [](float x) { return f_rsq(x); });
+    const V ir2 = O::mul(ir, ir);
+    const V t = O::mul(O::c(s), O::mul(r2, ir));
+    V K0, Q;
+    if constexpr (sizeof(V) == sizeof(float)) {
+        if (t <= 2.0f) k0q_small<O>(t, K0, Q);
+        else k0q_large<O>(t, K0, Q);
+    } else {
+        float t0, t1;
+        upk(t, t0, t1);
+        const bool s0 = t0 <= 2.0f, s1 = t1 <= 2.0f;
+        V Ks = O::c(0.f), Qs = O::c(0.f), Kl = O::c(0.f), Ql = O::c(0.f);
+        if (s0 || s1) k0q_small<O>(t, Ks, Qs);
+        if (!s0 || !s1) k0q_large<O>(t, Kl, Ql);
+        float ks0, ks1, qs0, qs1, kl0, kl1, ql0, ql1;
+        upk(Ks, ks0, ks1);
+        upk(Qs, qs0, qs1);
+        upk(Kl, kl0, kl1);
+        upk(Ql, ql0, ql1);
+        K0 = pk(s0 ? ks0 : kl0, s1 ? ks1 : kl1);
+        Q = pk(s0 ? qs0 : ql0, s1 ? qs1 : ql1);
+    }
+    if constexpr (!SRC) {
+        const V nd = O::fma(O::c(a.z), dx, O::mul(O::c(a.w), dy));
+        const V p = O::mul(nd, ir2);
+        if constexpr (VAL) {
+            V qp = O::mul(Q, p);
+            if constexpr ((MODE & 1) != 0) qp = fminf(fmaxf(qp, -c2pi), c2pi);  // kClampP (scalar only)
+            v = O::fma(O::c(b.x), qp, O::fma(O::c(b.y), K0, v));
+        }
+        if constexpr (GRAD) {
+            // d (A (2 Q p / r^2 + sigma K0 p) + B Q / r^2) - n (A Q / r^2)
+            const V aq = O::mul(O::c(b.x), Q);
+            const V inner = O::fma(O::c(b.x * sigma), O::mul(K0, p), O::mul(O::mul(O::c(b.y), Q), ir2));
+            const V q = O::fma(O::mul(aq, O::c(2.0f)), O::mul(p, ir2), inner);
+            const V c = O::mul(aq, ir2);
+            gx = O::fma(q, dx, O::fma(c, O::c(-a.z), gx));
+            gy = O::fma(q, dy, O::fma(c, O::c(-a.w), gy));
+        }
+    } else {
+        if constexpr (VAL) v = O::fma(O::c(-b.x), K0, v);
+        if constexpr (GRAD) {
+            const V nc = O::mul(O::mul(O::c(-b.x), Q), ir2);
+            gx = O::fma(nc, dx, gx);
+            gy = O::fma(nc, dy, gy);
+        }
+    }
+}
+
 // splat variants of correctedBoundarySplat / correctedSourceSplat (cache.cpp:499-597):
 //   kClampP: dG/dn clamped to [-c, c] in the boundary term (clampKernel kernels.h:52)
 //   kBall:   G -> G^B(x, R_x) (ballGreens kernels.cpp:31-43) in the d-hat and source terms
@@ -131,35 +275,9 @@ __device__ __forceinline__ void pair(const float4 a, const float4 b, float px, f
                 }
             }
         } else {
-            float ir = f_rsq(r2);
-            float ir2 = ir * ir;
-            float t = s * (r2 * ir);
-            float K0, Q;
-            k0_q(t, K0, Q);
-            if constexpr (!SRC) {
-                float nd = fmaf(a.z, dx, a.w * dy);
-                float p = nd * ir2;
-                if constexpr (VAL) {
-                    float qp = Q * p;
-                    if constexpr ((MODE & kClampP) != 0) qp = fminf(fmaxf(qp, -mc->c2pi), mc->c2pi);
-                    acc.v = fmaf(b.x, qp, fmaf(b.y, K0, acc.v));
-                }
-                if constexpr (GRAD) {
-                    float aq = b.x * Q;
-                    // d (A (2 Q p ir2 + sigma K0 p) + Bk Q ir2) - n (A Q ir2)
-                    float q = fmaf(aq + aq, p * ir2, fmaf(b.x * sigma, K0 * p, b.y * Q * ir2));
-                    float c = aq * ir2;
-                    acc.gx = fmaf(q, dx, fmaf(-c, a.z, acc.gx));
-                    acc.gy = fmaf(q, dy, fmaf(-c, a.w, acc.gy));
-                }
-            } else {
-                if constexpr (VAL) acc.v = fmaf(-b.x, K0, acc.v);
-                if constexpr (GRAD) {
-                    float c = b.x * Q * ir2;
-                    acc.gx = fmaf(-c, dx, acc.gx);
-                    acc.gy = fmaf(-c, dy, acc.gy);
-                }
-            }
+            float r2o;
+            scr2_pair<SOps, SRC, VAL, GRAD, MODE>(a, b, px, py, sigma, s, acc.v, acc.gx, acc.gy, r2o,
+                                                  (MODE & kClampP) ? mc->c2pi : 0.0f);
         }
     } else {
         // 3D boundary payload a = (zx, zy, zz, A nx), b = (A ny, A nz, -B, B); source a = (y, -C)
@@ -232,14 +350,24 @@ struct Acc2 {
 // which (KIND, VAL, GRAD, MODE) run packed: 2D and 3D Laplace, 3D screened values
 template <int KIND, bool VAL, bool GRAD, int MODE>
 struct Packed {
-    static constexpr bool value = MODE == 0 && (KIND == kLap2 || KIND == kLap3 || (KIND == kScr3 && !GRAD));
+    static constexpr bool value =
+        MODE == 0 && (KIND == kLap2 || KIND == kLap3 || KIND == kScr2 || (KIND == kScr3 && !GRAD));
 };
 
 // pair() on two query points at once; same operations, same rounding per lane
 template <int KIND, bool SRC, bool VAL, bool GRAD, bool TRACK>
-__device__ __forceinline__ void pair2(const float4 a, const float4 b, F2 px, F2 py, F2 pz, float s, Acc2& acc,
-                                      float* mn) {
-    if constexpr (KIND == kLap2) {
+__device__ __forceinline__ void pair2(const float4 a, const float4 b, F2 px, F2 py, F2 pz, float sigma, float s,
+                                      Acc2& acc, float* mn) {
+    if constexpr (KIND == kScr2) {
+        F2 r2;
+        scr2_pair<POps, SRC, VAL, GRAD, 0>(a, b, px, py, sigma, s, acc.v, acc.gx, acc.gy, r2, 0.0f);
+        if constexpr (TRACK) {
+            float lo, hi;
+            upk(r2, lo, hi);
+            mn[0] = fminf(mn[0], lo);
+            mn[1] = fminf(mn[1], hi);
+        }
+    } else if constexpr (KIND == kLap2) {
         F2 dx = sub2(bc(a.x), px), dy = sub2(bc(a.y), py);
         F2 r2 = fma2(dx, dx, mul2(dy, dy));
         if constexpr (TRACK) {
@@ -374,7 +502,7 @@ __device__ __forceinline__ void tile_loop(const float4* S, int cnt, const float*
             const float4 a = S[2 * j], b = S[2 * j + 1];
 #pragma unroll
             for (int h = 0; h < kQ / 2; ++h)
-                pair2<KIND, SRC, VAL, GRAD, TRACK>(a, b, px2[h], py2[h], pz2[h], P.s, a2[h], mn + 2 * h);
+                pair2<KIND, SRC, VAL, GRAD, TRACK>(a, b, px2[h], py2[h], pz2[h], P.sigma, P.s, a2[h], mn + 2 * h);
         }
 #pragma unroll
         for (int h = 0; h < kQ / 2; ++h) {
@@ -423,7 +551,9 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
         int pidx[kQ];
 #pragma unroll
         for (int q = 0; q < kQ; ++q) {
-            int i = tile * kPT + q * kThreads + tid;
+            // each thread owns kQ consecutive points of the Morton order: a packed pair
+            // holds neighbours (same screened-Bessel branch), a warp one compact patch
+            int i = tile * kPT + tid * kQ + q;
             pidx[q] = i;
             bool ok = i < P.K;
             px[q] = ok ? P.px[P.dim * i] : 1e30f;
