@@ -111,6 +111,41 @@ FarField bvc_scene_s::farfield() {
 }
 
 
+HintGrid bvc_scene_s::hintgrid() {
+    const char* e = std::getenv("BVC_HINTGRID");
+    if (e && std::string(e) == "0") return HintGrid{};
+    if (hgBuilt) return hg;
+    upload();
+    const int dim = host.dim;
+    const int nLong = dim == 2 ? 1024 : 128;  // 1M / 2M vertices, 4 / 8 MB
+    double ext = 0.0, lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int k = 0; k < dim; ++k) {
+        lo[k] = host.lo[k];
+        hi[k] = host.hi[k];
+        ext = std::max(ext, hi[k] - lo[k]);
+    }
+    const double h = std::max(ext, 1e-30) / (nLong - 1);
+    int n[3] = {1, 1, 1};
+    for (int k = 0; k < dim; ++k) n[k] = static_cast<int>(std::ceil((hi[k] - lo[k]) / h)) + 1;
+    hg = HintGrid{};
+    hg.lox = static_cast<float>(lo[0]);
+    hg.loy = static_cast<float>(lo[1]);
+    hg.loz = static_cast<float>(lo[2]);
+    hg.h = static_cast<float>(h);
+    hg.invH = static_cast<float>(1.0 / h);
+    hg.nx = n[0];
+    hg.ny = n[1];
+    hg.nz = n[2];
+    hgIds.resize(static_cast<size_t>(n[0]) * n[1] * n[2]);
+    if (dim == 2) launch_hintgrid2(view(), hg, hgIds.p, g_stream);
+    else launch_hintgrid3(view3(), hg, hgIds.p, g_stream);
+    CK(cudaGetLastError());
+    hg.id = hgIds.p;
+    hgBuilt = true;
+    return hg;
+}
+
+
 std::string bvc_scene_s::builder() const {
     const char* e = std::getenv("BVC_BVH");
     std::string v = e ? e : "";

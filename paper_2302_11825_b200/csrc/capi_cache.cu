@@ -43,6 +43,7 @@ WalkEnv make_env(bvc_scene_s* S, const bvc_problem& pb, const bvc_walk_config& w
         throw Error(BVC_ERR_SOLVER, "walk cannot terminate: scene has no Dirichlet boundary");
     key_of(seed, salt, round, E.k0, E.k1);
     E.ff = S->farfield();
+    E.hg = S->hintgrid();
     return E;
 }
 
@@ -162,6 +163,7 @@ WalkEnv3 make_env3(bvc_scene_s* S, const bvc_problem& pb, const bvc_walk_config&
     E.closed = E.insideTol > 0.f ? 1 : 0;
     key_of(seed, salt, round, E.k0, E.k1);
     E.ff = S->farfield();
+    E.hg = S->hintgrid();
     return E;
 }
 

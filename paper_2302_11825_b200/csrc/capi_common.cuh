@@ -196,6 +196,11 @@ struct bvc_scene_s {
     FarField ff{};
     bool ffBuilt = false;
     FarField farfield();
+    // warm-start grid (HintGrid, internal.h), built on first walk use
+    DevBuf<int> hgIds;
+    HintGrid hg{};
+    bool hgBuilt = false;
+    HintGrid hintgrid();
 
     // per primitive id: class (host_scene.h primClass; also the GPU build input) and,
     // in 3D, its leaf index (walk warm starts name leaf slots)

@@ -15,6 +15,18 @@ namespace bvc_impl {
 using bvc_dev::DevField;
 using bvc_dev::SceneView2;
 
+// Warm-start grid: at the vertices of a uniform grid over the scene box, the closest
+// Dirichlet primitive (2D: segment id; 3D: leaf-order triangle index). A walk step at
+// x also seeds its closest-point query with the primitive of x's nearest vertex v,
+// whose distance is at most d(x) + 2|x - v|: the pruning radius starts near-tight
+// even after a long jump, and the result is unchanged (one more candidate of the same
+// minimum). BVC_HINTGRID=0 disables it.
+struct HintGrid {
+    const int* id;  // NULL: disabled
+    float lox, loy, loz, h, invH;
+    int nx, ny, nz;
+};
+
 // PdeProblem with device field descriptors (pointwise.h:19-26)
 struct DevProblem {
     int screened;   // KernelKind::ScreenedPoisson
@@ -44,6 +56,7 @@ struct WalkEnv {
     int hasNeumann, hasSource, hasH, closed;
     uint32_t k0, k1;  // Philox key of the job (seed, salt, round)
     FarField ff;
+    HintGrid hg;
 };
 
 // A batch of estimator tasks. U tasks: nU plain walks from each U start point.
@@ -76,6 +89,8 @@ struct WalkJob {
 void launch_walk_job(const WalkEnv& env, const WalkJob& job, cudaStream_t st);
 // fills the far-field grid (distance to any boundary primitive at every vertex)
 void launch_farfield2(const SceneView2& S, const FarField& F, float* d, cudaStream_t st);
+void launch_hintgrid2(const SceneView2& S, const HintGrid& G, int* id, cudaStream_t st);
+void launch_hintgrid3(const bvc_dev::SceneView3& S, const HintGrid& G, int* id, cudaStream_t st);
 void launch_farfield3(const bvc_dev::SceneView3& S, const FarField& F, float* d, cudaStream_t st);
 
 // per-point mean / standard error (runWalks pointwise.cpp:167-186), fixed order
@@ -169,6 +184,7 @@ struct WalkEnv3 {
     int hasNeumann, hasH, closed;
     uint32_t k0, k1;
     FarField ff;
+    HintGrid hg;
 };
 
 struct WalkJob3 {

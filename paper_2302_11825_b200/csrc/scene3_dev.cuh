@@ -187,10 +187,14 @@ __device__ __forceinline__ Closest3 closest_on3(const SceneView3& S, int prim, f
 // seeds the pruning radius (the walker's previous closest triangle)
 template <bool COUNT = false>
 __device__ __forceinline__ Closest3 closest_point3(const SceneView3& S, float x, float y, float z, unsigned qmask,
-                                                   float maxD2 = kFInf, int hint = -1) {
+                                                   float maxD2 = kFInf, int hint = -1, int hint2 = -1) {
     Closest3 c{maxD2, 0.f, 0.f, 0.f, -1, -1};
     if (hint >= 0) {
         Closest3 h = closest_on3(S, hint, x, y, z);
+        if (h.d2 < c.d2) c = h;
+    }
+    if (hint2 >= 0 && hint2 != hint) {  // a second seed (the warm-start grid's)
+        Closest3 h = closest_on3(S, hint2, x, y, z);
         if (h.d2 < c.d2) c = h;
     }
     traverse_near3<COUNT>(

@@ -159,10 +159,14 @@ __device__ __forceinline__ Closest closest_on(const SceneView2& S, int seg, floa
 // previous closest segment), so far subtrees are never pushed.
 template <bool COUNT = false>
 __device__ __forceinline__ Closest closest_point(const SceneView2& S, float x, float y, unsigned qmask,
-                                                 float maxD2 = kFInf, int hint = -1) {
+                                                 float maxD2 = kFInf, int hint = -1, int hint2 = -1) {
     Closest c{maxD2, 0.0f, 0.0f, 0.0f, -1};
     if (hint >= 0) {
         Closest h = closest_on(S, hint, x, y);
+        if (h.d2 < c.d2) c = h;
+    }
+    if (hint2 >= 0 && hint2 != hint) {  // a second seed (the warm-start grid's)
+        Closest h = closest_on(S, hint2, x, y);
         if (h.d2 < c.d2) c = h;
     }
     traverse_near<COUNT>(
@@ -211,9 +215,14 @@ struct StarQuery {
     float s2;
 };
 template <bool COUNT = false>
-__device__ __forceinline__ StarQuery star_query(const SceneView2& S, float x, float y, float eps2, int hint = -1) {
+__device__ __forceinline__ StarQuery star_query(const SceneView2& S, float x, float y, float eps2, int hint = -1,
+                                                int hint2 = -1) {
     StarQuery q;
     q.D = hint >= 0 ? closest_on(S, hint, x, y) : Closest{kFInf, 0.0f, 0.0f, 0.0f, -1};
+    if (hint2 >= 0 && hint2 != hint) {
+        Closest h = closest_on(S, hint2, x, y);
+        if (h.d2 < q.D.d2) q.D = h;
+    }
     q.s2 = kFInf;
     traverse_near<COUNT>(
         S, x, y, kClsD | kClsSil,

@@ -159,6 +159,15 @@ __device__ __forceinline__ float farfield_bound(const FarField& F, float x, floa
     return __ldg(F.d + static_cast<size_t>(iy) * F.nx + ix) - sqrtf(fmaf(dx, dx, dy * dy)) - F.margin;
 }
 
+// the warm-start grid's primitive at the grid vertex nearest to (x, y), or -1 (HintGrid)
+__device__ __forceinline__ int hint_at(const HintGrid& G, float x, float y) {
+    if (!G.id) return -1;
+    const int ix = __float2int_rn((x - G.lox) * G.invH), iy = __float2int_rn((y - G.loy) * G.invH);
+    if (static_cast<unsigned>(ix) >= static_cast<unsigned>(G.nx) || static_cast<unsigned>(iy) >= static_cast<unsigned>(G.ny))
+        return -1;
+    return __ldg(G.id + static_cast<size_t>(iy) * G.nx + ix);
+}
+
 // per-lane walk state
 struct Walk {
     float x, y, acc, weight, inx, iny;
@@ -192,13 +201,13 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
         if constexpr (NEU) {
             // a Dirichlet segment farther than the closest visible silhouette may be
             // pruned (q.D.seg < 0, d2 = inf): R is then the silhouette distance
-            StarQuery q = star_query<COUNT>(E.S, w.x, w.y, E.eps * E.eps, w.lastD);
+            StarQuery q = star_query<COUNT>(E.S, w.x, w.y, E.eps * E.eps, w.lastD, hint_at(E.hg, w.x, w.y));
             cp = q.D;
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
             R = fminf(dD, sqrtf(q.s2));
         } else {
-            cp = closest_point<COUNT>(E.S, w.x, w.y, kClsD, kFInf, w.lastD);
+            cp = closest_point<COUNT>(E.S, w.x, w.y, kClsD, kFInf, w.lastD, hint_at(E.hg, w.x, w.y));
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
             R = dD;
@@ -604,6 +613,14 @@ __global__ void farfield2_kernel(const SceneView2 S, const FarField F, float* d)
     d[i] = sqrtf(closest_point(S, x, y, kClsAny).d2);
 }
 
+__global__ void hintgrid2_kernel(const SceneView2 S, const HintGrid G, int* id) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= G.nx * G.ny) return;
+    int ix = i % G.nx, iy = i / G.nx;
+    float x = fmaf(static_cast<float>(ix), G.h, G.lox), y = fmaf(static_cast<float>(iy), G.h, G.loy);
+    id[i] = closest_point(S, x, y, kClsD).seg;
+}
+
 __global__ void start_hints_kernel(const CacheSample* samples, int n, const int* source, const int* cls,
                                    const int* leafOf, const int* dIdx, int nD, int* hintU, int* hintD) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -642,6 +659,11 @@ void launch_walk_t(const WalkEnv& env, const WalkJob& job, long long total, cuda
 
 void launch_farfield2(const SceneView2& S, const FarField& F, float* d, cudaStream_t st) {
     farfield2_kernel<<<blocks(static_cast<long long>(F.nx) * F.ny, 128), 128, 0, st>>>(S, F, d);
+    count_launch();
+}
+
+void launch_hintgrid2(const SceneView2& S, const HintGrid& G, int* id, cudaStream_t st) {
+    hintgrid2_kernel<<<blocks(static_cast<long long>(G.nx) * G.ny, 128), 128, 0, st>>>(S, G, id);
     count_launch();
 }
 

@@ -51,8 +51,12 @@ struct Star3 {
 };
 
 template <bool COUNT>
-__device__ __forceinline__ Star3 star_query3(const WalkEnv3& E, float x, float y, float z, int hint) {
+__device__ __forceinline__ Star3 star_query3(const WalkEnv3& E, float x, float y, float z, int hint, int hint2) {
     Star3 q{hint >= 0 ? closest_on3(E.S, hint, x, y, z) : Closest3{kFInf, 0.f, 0.f, 0.f, -1, -1}, kFInf};
+    if (hint2 >= 0 && hint2 != hint) {
+        Closest3 h = closest_on3(E.S, hint2, x, y, z);
+        if (h.d2 < q.D.d2) q.D = h;
+    }
     float eps2 = E.eps * E.eps;
     traverse_near3<COUNT>(
         E.S, x, y, z, kClsD | kClsSil,
@@ -173,6 +177,17 @@ __device__ __forceinline__ float sphere_weight3(float s, float R, float rHit) {
     return (rHit * s * ch + sh) / shR;
 }
 
+// the warm-start grid's primitive at the grid vertex nearest to x, or -1 (HintGrid)
+__device__ __forceinline__ int hint_at3(const HintGrid& G, float x, float y, float z) {
+    if (!G.id) return -1;
+    const int ix = __float2int_rn((x - G.lox) * G.invH), iy = __float2int_rn((y - G.loy) * G.invH),
+              iz = __float2int_rn((z - G.loz) * G.invH);
+    if (static_cast<unsigned>(ix) >= static_cast<unsigned>(G.nx) || static_cast<unsigned>(iy) >= static_cast<unsigned>(G.ny) ||
+        static_cast<unsigned>(iz) >= static_cast<unsigned>(G.nz))
+        return -1;
+    return __ldg(G.id + (static_cast<size_t>(iz) * G.ny + iy) * G.nx + ix);
+}
+
 struct Walk3 {
     float x, y, z, weight;
     float inx, iny, inz;
@@ -209,13 +224,13 @@ __device__ __forceinline__ bool walk3_step(const WalkEnv3& E, Walk3& w, U4 rnd, 
         R = lb;
     } else {
         if constexpr (NEU) {
-            Star3 q = star_query3<COUNT>(E, w.x, w.y, w.z, w.lastD);
+            Star3 q = star_query3<COUNT>(E, w.x, w.y, w.z, w.lastD, hint_at3(E.hg, w.x, w.y, w.z));
             cp = q.D;
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
             R = fminf(dD, sqrtf(q.s2));
         } else {
-            cp = closest_point3<COUNT>(E.S, w.x, w.y, w.z, kClsD, kFInf, w.lastD);
+            cp = closest_point3<COUNT>(E.S, w.x, w.y, w.z, kClsD, kFInf, w.lastD, hint_at3(E.hg, w.x, w.y, w.z));
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
             R = dD;
@@ -548,6 +563,20 @@ void launch_walk3_t(const WalkEnv3& env, const WalkJob3& job, long long total, c
     long long want = (total + kThreads3 - 1) / kThreads3;
     int grid = static_cast<int>(want < static_cast<long long>(sms) * perSm ? want : static_cast<long long>(sms) * perSm);
     walk3_kernel<NEU, SCR, COUNT><<<grid, kThreads3, 0, st>>>(env, job);
+}
+
+__global__ void hintgrid3_kernel(const SceneView3 S, const HintGrid G, int* id) {
+    long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<long long>(G.nx) * G.ny * G.nz) return;
+    int ix = static_cast<int>(i % G.nx), iy = static_cast<int>((i / G.nx) % G.ny), iz = static_cast<int>(i / (static_cast<long long>(G.nx) * G.ny));
+    float x = fmaf(static_cast<float>(ix), G.h, G.lox), y = fmaf(static_cast<float>(iy), G.h, G.loy),
+          z = fmaf(static_cast<float>(iz), G.h, G.loz);
+    id[i] = closest_point3(S, x, y, z, kClsD).prim;
+}
+
+void launch_hintgrid3(const SceneView3& S, const HintGrid& G, int* id, cudaStream_t st) {
+    hintgrid3_kernel<<<blocks(static_cast<long long>(G.nx) * G.ny * G.nz, 128), 128, 0, st>>>(S, G, id);
+    count_launch();
 }
 
 void launch_farfield3(const SceneView3& S, const FarField& F, float* d, cudaStream_t st) {
