@@ -117,7 +117,8 @@ HintGrid bvc_scene_s::hintgrid() {
     if (hgBuilt) return hg;
     upload();
     const int dim = host.dim;
-    const int nLong = dim == 2 ? 1024 : 128;  // 1M / 2M vertices, 4 / 8 MB
+    const char* en = std::getenv("BVC_HINTGRID_N");  // vertices along the longest side
+    const int nLong = en && std::atoi(en) >= 16 ? std::atoi(en) : (dim == 2 ? 1024 : 128);  // 4 / 8 MB
     double ext = 0.0, lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (int k = 0; k < dim; ++k) {
         lo[k] = host.lo[k];
