@@ -336,6 +336,17 @@ int bvc_update_solution(bvc_scene scene, const bvc_problem* problem, bvc_region 
                         const bvc_cache_config* cfg, bvc_eval_points pts, uint64_t seed,
                         uint64_t round, int gradients, bvc_round_stats* stats);
 
+/* runSolveInMemory's round on host-resident points (runner.cpp:116-169: points built from
+   x, markEvaluationPoints, updateSolution, then solution() / gradient() read back). x is
+   n points of the scene's dimension; u receives n values, grad (optional, needs
+   gradients) n x dim. Equals bvc_points_create + bvc_mark_evaluation_points +
+   bvc_update_solution + bvc_points_solution bit for bit; the upload and classification
+   of the points overlap the cache walks (second stream). */
+int bvc_update_solution_host(bvc_scene scene, const bvc_problem* problem, bvc_region region,
+                             const bvc_cache_config* cfg, const double* x, size_t n, uint64_t seed,
+                             uint64_t round, int gradients, double* u, double* grad,
+                             bvc_round_stats* stats);
+
 /* the fallback-band walks of updateSolution (cache.cpp:665-681) alone, for the
    sharded multi-GPU round (generate shard, all-gather, splat_range, then this) */
 int bvc_fallback_walks(bvc_scene scene, const bvc_problem* problem, const bvc_cache_config* cfg,

@@ -34,7 +34,7 @@ SYMBOLS = (
     "bvc_walk_traffic_profile bvc_eval_kernels bvc_eval_bessel bvc_corrected_boundary_splat "
     "bvc_corrected_source_splat bvc_trace_streamlines bvc_grid_save_csv bvc_grid_load_csv bvc_grid_rmse "
     "bvc_grid_save_pgm bvc_streamlines_write_csv bvc_pipe_probe bvc_boundary_cache_assign_voronoi "
-    "bvc_fallback_walks"
+    "bvc_fallback_walks bvc_update_solution_host"
 ).split()
 
 
@@ -579,6 +579,27 @@ def update_solution(scene: Scene, pb, region: SolveRegion, cfg, pts: EvaluationP
     _check(lib().bvc_update_solution(scene.h, C.byref(pb), region.h, C.byref(cfg), pts.h, C.c_uint64(seed),
                                      C.c_uint64(round_), int(gradients), C.byref(st)))
     return _stats_dict(st)
+
+
+def update_solution_host(scene: Scene, pb, region: SolveRegion, cfg, x, seed, round_, gradients=False, out=None,
+                         stats=None):
+    """runSolveInMemory's round on host points (runner.cpp:116-169): upload, classify, one
+    updateSolution round, read u (and grad u). Returns u or (u, grad). `out` = host arrays
+    to fill (e.g. pinned); the upload and classification overlap the cache walks."""
+    x = _f64(x, scene.dim)
+    n = len(x)
+    if out is not None:
+        u, g = out
+    else:
+        u = np.zeros(n)
+        g = np.zeros((n, scene.dim)) if gradients else None
+    st = abi.RoundStats()
+    _check(lib().bvc_update_solution_host(scene.h, C.byref(pb), region.h, C.byref(cfg), _ptr(x), C.c_size_t(n),
+                                          C.c_uint64(seed), C.c_uint64(round_), int(gradients), _ptr(u),
+                                          _ptr(g) if g is not None else None, C.byref(st)))
+    if stats is not None:
+        stats.update(_stats_dict(st))
+    return (u, g) if gradients else u
 
 
 def fallback_walks(scene: Scene, pb, cfg, pts: EvaluationPoints, seed, round_, gradients=False):

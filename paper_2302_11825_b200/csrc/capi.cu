@@ -13,6 +13,7 @@ namespace bvc_capi {
 
 thread_local std::string g_error;
 cudaStream_t g_stream = nullptr;
+std::function<void()> g_afterWalkLaunch;
 bool g_profile = false;
 unsigned long long g_profileTotals[2] = {0, 0};
 

@@ -109,6 +109,7 @@ void run_cache_walks(bvc_scene_s* S, bvc_region_s* R, const WalkEnv& E, const bv
     } else {
         launch_walk_job(E, J, g_stream);
     }
+    after_walk_launch();
     launch_finish_samples(samples, n, J.outU, nU, dIdx, nD, J.outD, nDw, failed, g_stream);
     unsigned long long h[3];
     CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, g_stream));
@@ -227,6 +228,7 @@ void run_cache_walks3(bvc_scene_s* S, bvc_region_s* R, const WalkEnv3& E, const 
     } else {
         launch_walk_job3(E, J, g_stream);
     }
+    after_walk_launch();
     launch_finish_samples(samples, n, J.outU, nU, dIdx, nD, J.outD, nDw, failed, g_stream);
     unsigned long long h[3];
     CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, g_stream));

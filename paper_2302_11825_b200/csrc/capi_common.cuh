@@ -9,6 +9,7 @@
 //   capi_walks.cu    pointwise estimators (pointwise.cpp:225-288) and fallback walks
 //   capi_stream.cu   runStreamlines (runner.cpp:285-373)
 #pragma once
+#include <functional>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -33,6 +34,25 @@ using bvc_dev::Prim2;
 
 extern thread_local std::string g_error;
 extern cudaStream_t g_stream;
+// One-shot host callback run right after a cache-walk job is enqueued: the host-buffer
+// round (bvc_update_solution_host) uploads and classifies its points on a second
+// stream while the walks run.
+extern std::function<void()> g_afterWalkLaunch;
+inline void after_walk_launch() {
+    if (g_afterWalkLaunch) {
+        std::function<void()> f = std::move(g_afterWalkLaunch);
+        g_afterWalkLaunch = nullptr;
+        f();
+    }
+}
+// the library's work stream for the lifetime of a scope
+struct StreamScope {
+    cudaStream_t saved;
+    explicit StreamScope(cudaStream_t s) : saved(g_stream) { g_stream = s; }
+    ~StreamScope() { g_stream = saved; }
+    StreamScope(const StreamScope&) = delete;
+    StreamScope& operator=(const StreamScope&) = delete;
+};
 // diagnostic traversal counting (bvc_walk_traffic_profile); off in production
 extern bool g_profile;
 extern unsigned long long g_profileTotals[2];

@@ -225,6 +225,128 @@ bvc_splat_config make_splat_config(bvc_scene_s* S, const bvc_problem& pb, const 
     return s;
 }
 
+// One progressive round (updateSolution cache.cpp:622-684). `points` is called once
+// the cache-walk job is enqueued and returns the evaluation points: a caller may
+// still be preparing them (on another stream) while the walks run.
+void update_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const bvc_cache_config& cfg,
+                  const std::function<bvc_eval_points_s*()>& points, uint64_t seed, uint64_t round, int gradients,
+                  bvc_round_stats* stats) {
+    require_device();
+    need(s && r, "null argument");
+    validate_kernel(pb.kernel);
+    if (cfg.sourceBall && gradients) throw Error(BVC_ERR_SOLVER, "ball-kernel source mode does not support gradient splats");
+    bvc_splat_config scfg = make_splat_config(s, pb, cfg);
+    need(cfg.clampMode >= BVC_CLAMP_OFF && cfg.clampMode <= BVC_CLAMP_CORRECT, "unknown clamp mode");
+    cudaEvent_t e0, e1, e2;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventCreate(&e2));
+    CK(cudaEventRecord(e0, g_stream));
+    bvc_boundary_cache_s bc;
+    bvc_source_cache_s sc;
+    GenStats st;
+    generate_cache(s, pb, r, cfg, seed, round, 0, std::max(1, cfg.nBoundary), &bc, st);
+    generate_source(pb, r, cfg, seed, round, &sc);
+    CK(cudaEventRecord(e1, g_stream));
+    bvc_eval_points_s* p = points();
+    need(p != nullptr, "null evaluation points");
+    bool hasSource = pb.f.kind != BVC_FIELD_NONE;
+    bvc_source_cache_s* sp = sc.m ? &sc : nullptr;
+    // the mode dispatch of updateSolution (cache.cpp:639-662)
+    if (cfg.clampMode == BVC_CLAMP_OFF) {
+        // ball mode: splatSolution with G^B plus the unclamped (infinite-bound,
+        // correction-free) ball source splat, i.e. one ball-kernel splat
+        splat(&bc, sp, p, scfg, 0, SIZE_MAX, true, gradients != 0);
+    } else {
+        double c = cfg.clamp > 0.0 ? cfg.clamp : 10.0 / s->host.diagonal;  // resolvedClamp cache.h:129-131
+        bvc_boundary_evaluator ev{};
+        ev.kind = BVC_EVALUATOR_WALKS;
+        ev.scene = s;
+        ev.problem = &pb;
+        ev.cfg = &cfg;
+        corrected_boundary(&bc, p, r, scfg, c, cfg.clampMode, &ev, seed, bvc_dev::mixKey(kBoundaryCorrSalt, round));
+        if (hasSource) {
+            if (cfg.sourceBall) {
+                corrected_source(sp, p, r, scfg, c, &pb.f, seed, bvc_dev::mixKey(kSourceCorrSalt, round));
+            } else {
+                splat(nullptr, sp, p, scfg, 0, SIZE_MAX, true, false);
+            }
+        }
+        if (gradients) splat(&bc, sp, p, scfg, 0, SIZE_MAX, false, true);
+    }
+    fallback_walks(s, pb, cfg, p, seed, round, gradients != 0);
+    CK(cudaEventRecord(e2, g_stream));
+    CK(cudaEventSynchronize(e2));
+    if (stats) {
+        stats->resampled = st.resampled;
+        stats->cacheWalks = st.walks;
+        stats->cacheTruncated = st.truncated;
+        stats->cacheSteps = st.steps;
+        stats->generateSeconds = device_seconds(e0, e1);
+        stats->splatSeconds = device_seconds(e1, e2);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+}
+
+// runSolveInMemory's round on host-resident points (runner.cpp:116-169: build the
+// points, markEvaluationPoints, updateSolution, read solution() / gradient()). The
+// points' upload, Morton order and classification run on a second stream while the
+// cache walks run; the result equals the handle-based sequence bit for bit.
+void update_round_host(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const bvc_cache_config& cfg,
+                       const double* x, size_t n, uint64_t seed, uint64_t round, int gradients, double* u, double* grad,
+                       bvc_round_stats* stats) {
+    require_device();
+    need(s && r && (x || n == 0) && (u || n == 0), "null argument");
+    need(!grad || gradients, "gradient output requested without gradients");
+    s->upload();
+    r->upload();
+    static cudaStream_t side = [] {
+        cudaStream_t t = nullptr;
+        CK(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+        return t;
+    }();
+    cudaEvent_t ready, done;
+    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    CK(cudaEventRecord(ready, g_stream));  // scene / region uploads precede the side stream's reads
+    std::unique_ptr<bvc_eval_points_s> P;
+    auto prep = [&] {
+        StreamScope scope(side);
+        CK(cudaStreamWaitEvent(side, ready, 0));
+        P = make_points(x, n, s->host.dim);
+        mark_points(s, r, cfg, P.get());
+        ensure_order(P.get());
+        CK(cudaEventRecord(done, side));
+    };
+    g_afterWalkLaunch = prep;
+    try {
+        update_round(s, pb, r, cfg,
+                     [&]() -> bvc_eval_points_s* {
+                         if (!P) after_walk_launch();  // no walk job was launched
+                         g_afterWalkLaunch = nullptr;
+                         CK(cudaStreamWaitEvent(g_stream, done, 0));
+                         return P.get();
+                     },
+                     seed, round, gradients, stats);
+    } catch (...) {
+        g_afterWalkLaunch = nullptr;
+        cudaEventDestroy(ready);
+        cudaEventDestroy(done);
+        throw;
+    }
+    cudaEventDestroy(ready);
+    cudaEventDestroy(done);
+    if (n == 0) return;
+    const int d = P->dim;
+    double* o = ws().get<double>(kWsEvalOut, (1 + d) * n);
+    launch_solution(P.get(), o, o + n);
+    CK(cudaMemcpyAsync(u, o, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+    if (grad) CK(cudaMemcpyAsync(grad, o + n, d * n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+}
+
 }  // namespace bvc_capi
 
 extern "C" {
@@ -262,62 +384,17 @@ int bvc_corrected_source_splat(bvc_source_cache s, bvc_eval_points p, bvc_region
 int bvc_update_solution(bvc_scene s, const bvc_problem* pb, bvc_region r, const bvc_cache_config* cfg,
                         bvc_eval_points p, uint64_t seed, uint64_t round, int gradients, bvc_round_stats* stats) {
     API({
-        require_device();
         need(s && pb && r && cfg && p, "null argument");
-        validate_kernel(pb->kernel);
-        if (cfg->sourceBall && gradients)
-            throw Error(BVC_ERR_SOLVER, "ball-kernel source mode does not support gradient splats");
-        bvc_splat_config scfg = make_splat_config(s, *pb, *cfg);
-        need(cfg->clampMode >= BVC_CLAMP_OFF && cfg->clampMode <= BVC_CLAMP_CORRECT, "unknown clamp mode");
-        cudaEvent_t e0, e1, e2;
-        CK(cudaEventCreate(&e0));
-        CK(cudaEventCreate(&e1));
-        CK(cudaEventCreate(&e2));
-        CK(cudaEventRecord(e0, g_stream));
-        bvc_boundary_cache_s bc;
-        bvc_source_cache_s sc;
-        GenStats st;
-        generate_cache(s, *pb, r, *cfg, seed, round, 0, std::max(1, cfg->nBoundary), &bc, st);
-        generate_source(*pb, r, *cfg, seed, round, &sc);
-        CK(cudaEventRecord(e1, g_stream));
-        bool hasSource = pb->f.kind != BVC_FIELD_NONE;
-        bvc_source_cache_s* sp = sc.m ? &sc : nullptr;
-        // the mode dispatch of updateSolution (cache.cpp:639-662)
-        if (cfg->clampMode == BVC_CLAMP_OFF) {
-            // ball mode: splatSolution with G^B plus the unclamped (infinite-bound,
-            // correction-free) ball source splat, i.e. one ball-kernel splat
-            splat(&bc, sp, p, scfg, 0, SIZE_MAX, true, gradients != 0);
-        } else {
-            double c = cfg->clamp > 0.0 ? cfg->clamp : 10.0 / s->host.diagonal;  // resolvedClamp cache.h:129-131
-            bvc_boundary_evaluator ev{};
-            ev.kind = BVC_EVALUATOR_WALKS;
-            ev.scene = s;
-            ev.problem = pb;
-            ev.cfg = cfg;
-            corrected_boundary(&bc, p, r, scfg, c, cfg->clampMode, &ev, seed, bvc_dev::mixKey(kBoundaryCorrSalt, round));
-            if (hasSource) {
-                if (cfg->sourceBall) {
-                    corrected_source(sp, p, r, scfg, c, &pb->f, seed, bvc_dev::mixKey(kSourceCorrSalt, round));
-                } else {
-                    splat(nullptr, sp, p, scfg, 0, SIZE_MAX, true, false);
-                }
-            }
-            if (gradients) splat(&bc, sp, p, scfg, 0, SIZE_MAX, false, true);
-        }
-        fallback_walks(s, *pb, *cfg, p, seed, round, gradients != 0);
-        CK(cudaEventRecord(e2, g_stream));
-        CK(cudaEventSynchronize(e2));
-        if (stats) {
-            stats->resampled = st.resampled;
-            stats->cacheWalks = st.walks;
-            stats->cacheTruncated = st.truncated;
-            stats->cacheSteps = st.steps;
-            stats->generateSeconds = device_seconds(e0, e1);
-            stats->splatSeconds = device_seconds(e1, e2);
-        }
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        cudaEventDestroy(e2);
+        update_round(s, *pb, r, *cfg, [p]() { return p; }, seed, round, gradients, stats);
+    })
+}
+
+int bvc_update_solution_host(bvc_scene s, const bvc_problem* pb, bvc_region r, const bvc_cache_config* cfg,
+                             const double* x, size_t n, uint64_t seed, uint64_t round, int gradients, double* u,
+                             double* grad, bvc_round_stats* stats) {
+    API({
+        need(s && pb && r && cfg, "null argument");
+        update_round_host(s, *pb, r, *cfg, x, n, seed, round, gradients, u, grad, stats);
     })
 }
 

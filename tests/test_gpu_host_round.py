@@ -1,0 +1,56 @@
+"""bvc_update_solution_host (runSolveInMemory's round on host points, runner.cpp:116-169)
+against the handle sequence it replaces (points_create, markEvaluationPoints,
+updateSolution, solution()/gradient()): same u and grad u bit for bit, although the
+points are uploaded and classified on a second stream while the cache walks run."""
+import numpy as np
+import pytest
+
+import paper_2302_11825_b200 as B
+from paper_2302_11825_b200 import abi, configs
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(cid, scale, n_points):
+    c = configs.CONFIGS[cid](scale=scale)
+    if c.extra.get("dim") == 3:
+        sc = B.Scene.mesh3(c.vertices, c.segments, c.labels)
+        region = B.SolveRegion(sc, offset=c.region_offset, epsilon=c.epsilon)
+        x = c.points[sc.inside(c.points).astype(bool)][:n_points]
+        return c, sc, region, x, 3
+    sc = B.Scene(c.vertices, c.segments, c.labels)
+    if c.region_mode == abi.REGION_SUBDOMAIN:
+        sub = B.Scene(c.sub_vertices, c.sub_segments, np.zeros(len(c.sub_segments), np.int32))
+        region = B.SolveRegion(sc, abi.REGION_SUBDOMAIN, c.region_offset, sub, epsilon=c.epsilon)
+        x = c.points[region.boundary.inside(c.points).astype(bool)][:n_points]
+    else:
+        region = B.SolveRegion(sc, offset=c.region_offset, epsilon=c.epsilon)
+        x = c.points[sc.inside(c.points).astype(bool)][:n_points]
+    return c, sc, region, x, 2
+
+
+@pytest.mark.parametrize("cid,scale", [(2, 1 / 32), (3, 1 / 128), (4, 1 / 256)])
+def test_host_round_equals_handle_sequence(cid, scale):
+    c, sc, region, x, dim = _setup(cid, scale, 20000)
+    grads = bool(c.gradients)
+    p = B.EvaluationPoints(x, dim)
+    B.mark_evaluation_points(sc, region, c.cache, p)
+    B.update_solution(sc, c.problem, region, c.cache, p, c.seed, 7, gradients=grads)
+    ref = p.read_solution(gradient=grads)
+    st = {}
+    got = B.update_solution_host(sc, c.problem, region, c.cache, x, c.seed, 7, gradients=grads, stats=st)
+    if grads:
+        np.testing.assert_array_equal(got[0], ref[0])
+        np.testing.assert_array_equal(got[1], ref[1])
+    else:
+        np.testing.assert_array_equal(got, ref)
+    assert st["cacheWalks"] > 0 and np.all(np.isfinite(got[0] if grads else got))
+
+
+def test_host_round_empty_and_errors():
+    c, sc, region, x, dim = _setup(2, 1 / 64, 10)
+    u = B.update_solution_host(sc, c.problem, region, c.cache, x[:0], c.seed, 1)
+    assert u.shape == (0,)
+    with pytest.raises(B.InvalidArgument):
+        B.update_solution_host(sc, c.problem, region, c.cache, x, c.seed, 1, gradients=False,
+                               out=(np.zeros(len(x)), np.zeros((len(x), 2))))
