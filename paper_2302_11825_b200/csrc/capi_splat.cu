@@ -302,11 +302,13 @@ void update_round_host(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, c
     need(!grad || gradients, "gradient output requested without gradients");
     s->upload();
     r->upload();
-    static cudaStream_t side = [] {
-        cudaStream_t t = nullptr;
-        CK(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
-        return t;
-    }();
+    // one side stream per device (bvc_set_device may switch devices between calls)
+    static cudaStream_t sides[64] = {};
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    need(dev >= 0 && dev < 64, "device index out of range");
+    if (!sides[dev]) CK(cudaStreamCreateWithFlags(&sides[dev], cudaStreamNonBlocking));
+    cudaStream_t side = sides[dev];
     cudaEvent_t ready, done;
     CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
