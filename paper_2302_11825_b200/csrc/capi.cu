@@ -138,11 +138,17 @@ HintGrid bvc_scene_s::hintgrid() {
     hg.nx = n[0];
     hg.ny = n[1];
     hg.nz = n[2];
-    hgIds.resize(static_cast<size_t>(n[0]) * n[1] * n[2]);
-    if (dim == 2) launch_hintgrid2(view(), hg, hgIds.p, g_stream);
-    else launch_hintgrid3(view3(), hg, hgIds.p, g_stream);
+    const size_t nv = static_cast<size_t>(n[0]) * n[1] * n[2];
+    hgIds.resize(nv);
+    hgEntry.resize(nv);
+    // ray lengths are max(R, rMin) with rMin <= eps; a generous 1e-2 diag covers any rMin
+    const float rmin = static_cast<float>(1e-2 * host.diagonal);
+    if (dim == 2) launch_hintgrid2(view(), hg, hgIds.p, hgEntry.p, rmin, g_stream);
+    else launch_hintgrid3(view3(), hg, hgIds.p, hgEntry.p, rmin, g_stream);
     CK(cudaGetLastError());
     hg.id = hgIds.p;
+    const char* ee = std::getenv("BVC_ENTRY");
+    hg.entry = (ee && std::string(ee) == "0") ? nullptr : hgEntry.p;
     hgBuilt = true;
     return hg;
 }

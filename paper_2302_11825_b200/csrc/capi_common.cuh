@@ -218,6 +218,7 @@ struct bvc_scene_s {
     FarField farfield();
     // warm-start grid (HintGrid, internal.h), built on first walk use
     DevBuf<int> hgIds;
+    DevBuf<int2> hgEntry;
     HintGrid hg{};
     bool hgBuilt = false;
     HintGrid hintgrid();

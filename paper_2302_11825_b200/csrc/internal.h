@@ -21,8 +21,19 @@ using bvc_dev::SceneView2;
 // whose distance is at most d(x) + 2|x - v|: the pruning radius starts near-tight
 // even after a long jump, and the result is unchanged (one more candidate of the same
 // minimum). BVC_HINTGRID=0 disables it.
+//
+// Per grid cell (the cell [v, v + h) of vertex v) the grid also keeps entry refs: with c
+// the cell centre and rho its half-diagonal, every Dirichlet or silhouette primitive a
+// star / closest-point query at x in the cell can use lies within dD(x) <= dD(c) + rho
+// of x, so within r = dD(c) + 2 rho of c; .x is the deepest BVH node whose subtree holds
+// every primitive box of those classes within r of c. A Neumann ray of such a step is no
+// longer than dD(x) either, so .y is the same for the Neumann classes (kNoEntry: the cell's
+// rays cannot reach any). Queries start there instead of the root: the top levels, which
+// every query of the cell would descend identically, are skipped, and the result is the
+// same (every candidate is in the subtree).
 struct HintGrid {
-    const int* id;  // NULL: disabled
+    const int* id;       // NULL: disabled
+    const int2* entry;   // per cell: (star / closest entry, Neumann ray entry)
     float lox, loy, loz, h, invH;
     int nx, ny, nz;
 };
@@ -89,8 +100,9 @@ struct WalkJob {
 void launch_walk_job(const WalkEnv& env, const WalkJob& job, cudaStream_t st);
 // fills the far-field grid (distance to any boundary primitive at every vertex)
 void launch_farfield2(const SceneView2& S, const FarField& F, float* d, cudaStream_t st);
-void launch_hintgrid2(const SceneView2& S, const HintGrid& G, int* id, cudaStream_t st);
-void launch_hintgrid3(const bvc_dev::SceneView3& S, const HintGrid& G, int* id, cudaStream_t st);
+void launch_hintgrid2(const SceneView2& S, const HintGrid& G, int* id, int2* entry, float rmin, cudaStream_t st);
+void launch_hintgrid3(const bvc_dev::SceneView3& S, const HintGrid& G, int* id, int2* entry, float rmin,
+                      cudaStream_t st);
 void launch_farfield3(const bvc_dev::SceneView3& S, const FarField& F, float* d, cudaStream_t st);
 
 // per-point mean / standard error (runWalks pointwise.cpp:167-186), fixed order

@@ -121,9 +121,10 @@ __device__ __forceinline__ float tri_closest(const Prim3& t, float px, float py,
 // code paths once per leaf instead of once per node visit
 template <bool COUNT = false, class Visit, class Thr>
 __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, float y, float z, unsigned qmask,
-                                               Visit&& visit, Thr&& threshold) {
+                                               Visit&& visit, Thr&& threshold, int start = 0) {
+    if (start == kNoEntry) return;
     unsigned long long stack[kStack];  // (distance bits << 32 | ref): one local load per pop
-    int sp = 0, ref = 0;
+    int sp = 0, ref = start;
     const F2 pxy = pk(x, y);
     auto pop = [&]() -> bool {  // next entry still within the pruning radius; false when empty
         for (;;) {
@@ -187,7 +188,8 @@ __device__ __forceinline__ Closest3 closest_on3(const SceneView3& S, int prim, f
 // seeds the pruning radius (the walker's previous closest triangle)
 template <bool COUNT = false>
 __device__ __forceinline__ Closest3 closest_point3(const SceneView3& S, float x, float y, float z, unsigned qmask,
-                                                   float maxD2 = kFInf, int hint = -1, int hint2 = -1) {
+                                                   float maxD2 = kFInf, int hint = -1, int hint2 = -1,
+                                                   int start = 0) {
     Closest3 c{maxD2, 0.f, 0.f, 0.f, -1, -1};
     if (hint >= 0) {
         Closest3 h = closest_on3(S, hint, x, y, z);
@@ -204,7 +206,7 @@ __device__ __forceinline__ Closest3 closest_point3(const SceneView3& S, float x,
             float d2 = tri_closest(p, x, y, z, qx, qy, qz);
             if (d2 < c.d2) c = Closest3{d2, qx, qy, qz, __float_as_int(p.a.w), i};
         },
-        [&]() { return c.d2; });
+        [&]() { return c.d2; }, start);
     return c;
 }
 
@@ -254,6 +256,21 @@ __device__ __forceinline__ float ray_box3_t(const float4& lo, const float4& hi, 
     float t0 = fmaxf(fmaxf(fminf(tnx, tfx), fminf(tny, tfy)), fmaxf(fminf(tnz, tfz), 0.0f));
     float t1 = fminf(fminf(fmaxf(tnx, tfx), fmaxf(tny, tfy)), fminf(fmaxf(tnz, tfz), tMax));
     return t0 <= t1 ? t0 : kFInf;
+}
+
+// entry_node (scene_dev.cuh) on the 3D tree
+__device__ __forceinline__ int entry_node3(const SceneView3& S, float x, float y, float z, float r2, unsigned qmask) {
+    int ref = 0;
+    while (ref >= 0) {
+        const Node3 nd = S.nodes[ref];
+        const bool vl = (nd.mask() & qmask) && box3_dist2(nd.llo, nd.lhi, x, y, z) <= r2;
+        const bool vr = ((nd.mask() >> 3) & qmask) && box3_dist2(nd.rlo, nd.rhi, x, y, z) <= r2;
+        if (vl && vr) return ref;
+        if (vl) ref = nd.left();
+        else if (vr) ref = nd.right();
+        else return kNoEntry;
+    }
+    return ref;
 }
 
 // inside: boundary-inclusive within tol, then ray-crossing parity along a fixed

@@ -89,13 +89,18 @@ constexpr unsigned kClsNeumann = kClsN | kClsSil, kClsAny = kClsD | kClsN | kCls
 // Generic best-first traversal. visit(prim) handles one primitive of a visited
 // leaf; threshold() returns the current squared pruning radius. "While-while"
 // structure (Aila & Laine, HPG 2009): inner nodes in one loop, leaves in the next.
+// Entry refs (HintGrid): a traversal may start at a subtree known to hold every
+// primitive that can matter for the query (start = 0: the root); kNoEntry = none.
+constexpr int kNoEntry = -2147483647 - 1;
+
 template <bool COUNT = false, class Visit, class Thr>
 __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, float y, unsigned qmask, Visit&& visit,
-                                              Thr&& threshold) {
+                                              Thr&& threshold, int start = 0) {
+    if (start == kNoEntry) return;
     // (distance bits << 32 | ref) per entry: one local load per pop
     unsigned long long stack[kStack];
     int sp = 0;
-    int ref = 0;
+    int ref = start;
     const F2 p2 = pk(x, y);
     auto pop = [&]() -> bool {  // next entry still within the pruning radius; false when empty
         for (;;) {
@@ -159,7 +164,7 @@ __device__ __forceinline__ Closest closest_on(const SceneView2& S, int seg, floa
 // previous closest segment), so far subtrees are never pushed.
 template <bool COUNT = false>
 __device__ __forceinline__ Closest closest_point(const SceneView2& S, float x, float y, unsigned qmask,
-                                                 float maxD2 = kFInf, int hint = -1, int hint2 = -1) {
+                                                 float maxD2 = kFInf, int hint = -1, int hint2 = -1, int start = 0) {
     Closest c{maxD2, 0.0f, 0.0f, 0.0f, -1};
     if (hint >= 0) {
         Closest h = closest_on(S, hint, x, y);
@@ -176,7 +181,7 @@ __device__ __forceinline__ Closest closest_point(const SceneView2& S, float x, f
             float d2 = seg_closest(p.seg, x, y, px, py, t);
             if (d2 < c.d2) { c.d2 = d2; c.px = px; c.py = py; c.t = t; c.seg = p.id; }
         },
-        [&]() { return c.d2; });
+        [&]() { return c.d2; }, start);
     return c;
 }
 
@@ -216,7 +221,7 @@ struct StarQuery {
 };
 template <bool COUNT = false>
 __device__ __forceinline__ StarQuery star_query(const SceneView2& S, float x, float y, float eps2, int hint = -1,
-                                                int hint2 = -1) {
+                                                int hint2 = -1, int start = 0) {
     StarQuery q;
     q.D = hint >= 0 ? closest_on(S, hint, x, y) : Closest{kFInf, 0.0f, 0.0f, 0.0f, -1};
     if (hint2 >= 0 && hint2 != hint) {
@@ -237,7 +242,7 @@ __device__ __forceinline__ StarQuery star_query(const SceneView2& S, float x, fl
                 if (p.sil1 >= 0 && silhouette_ok(S, p.sil1, x, y, d2) && d2 < q.s2) q.s2 = d2;
             }
         },
-        [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); });
+        [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); }, start);
     return q;
 }
 
@@ -288,15 +293,16 @@ struct RayHit {
 // hit it again, and skipping it keeps FP32 re-hits out).
 template <bool COUNT = false>
 __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, float oy, float dx, float dy,
-                                                float tMax, unsigned qmask, float tMin, int skipSeg) {
+                                                float tMax, unsigned qmask, float tMin, int skipSeg, int start = 0) {
     RayHit h{kFInf, 0.0f, 0.0f, 0.0f, -1};
+    if (start == kNoEntry) return h;
     float idx = f_rcp(dx), idy = f_rcp(dy);  // slab tests on padded boxes: an approximate reciprocal suffices
     const F2 id2 = pk(idx, idy), noi2 = pk(-(ox * idx), -(oy * idy));
     float limit = tMax;
     // nearer child first (entry distance), the other pushed with its entry distance and
     // dropped at pop time once a hit closer than it is known; while-while structure
     unsigned long long stack[kStack];
-    int sp = 0, ref = 0;
+    int sp = 0, ref = start;
     auto pop = [&]() -> bool {
         for (;;) {
             if (sp == 0) return false;
@@ -355,6 +361,23 @@ __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, f
         }
         if (!pop()) return h;
     }
+}
+
+// the deepest node whose subtree holds every primitive of the classes in qmask whose
+// box lies within sqrt(r2) of (x, y): descend while exactly one child qualifies
+// (a leaf ref when it narrows to one leaf; kNoEntry when nothing qualifies)
+__device__ __forceinline__ int entry_node(const SceneView2& S, float x, float y, float r2, unsigned qmask) {
+    int ref = 0;
+    while (ref >= 0) {
+        const Node2 nd = S.nodes[ref];
+        const bool vl = (nd.mask & qmask) && box_dist2(nd.lbox, x, y) <= r2;
+        const bool vr = ((nd.mask >> 3) & qmask) && box_dist2(nd.rbox, x, y) <= r2;
+        if (vl && vr) return ref;
+        if (vl) ref = nd.left;
+        else if (vr) ref = nd.right;
+        else return kNoEntry;
+    }
+    return ref;
 }
 
 // Scene::inside (scene.cpp:240-254): boundary-inclusive within tol, then crossing

@@ -168,6 +168,15 @@ __device__ __forceinline__ int hint_at(const HintGrid& G, float x, float y) {
     return __ldg(G.id + static_cast<size_t>(iy) * G.nx + ix);
 }
 
+// the cell entry refs of (x, y) (HintGrid), or the root for both outside the grid
+__device__ __forceinline__ int2 entry_at(const HintGrid& G, float x, float y) {
+    if (!G.entry) return make_int2(0, 0);
+    const int ix = __float2int_rd((x - G.lox) * G.invH), iy = __float2int_rd((y - G.loy) * G.invH);
+    if (static_cast<unsigned>(ix) >= static_cast<unsigned>(G.nx) || static_cast<unsigned>(iy) >= static_cast<unsigned>(G.ny))
+        return make_int2(0, 0);
+    return __ldg(G.entry + static_cast<size_t>(iy) * G.nx + ix);
+}
+
 // per-lane walk state
 struct Walk {
     float x, y, acc, weight, inx, iny;
@@ -194,6 +203,7 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
     // holds no boundary point, so no Neumann crossing and no Neumann-data term either
     const float lb = E.ff.d ? farfield_bound(E.ff, w.x, w.y) : -1.0f;
     const bool far = lb >= E.ff.tau;
+    const int2 entry = far ? make_int2(0, 0) : entry_at(E.hg, w.x, w.y);
     if (far) {
         R = lb;
     } else {
@@ -201,13 +211,13 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
         if constexpr (NEU) {
             // a Dirichlet segment farther than the closest visible silhouette may be
             // pruned (q.D.seg < 0, d2 = inf): R is then the silhouette distance
-            StarQuery q = star_query<COUNT>(E.S, w.x, w.y, E.eps * E.eps, w.lastD, hint_at(E.hg, w.x, w.y));
+            StarQuery q = star_query<COUNT>(E.S, w.x, w.y, E.eps * E.eps, w.lastD, hint_at(E.hg, w.x, w.y), entry.x);
             cp = q.D;
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
             R = fminf(dD, sqrtf(q.s2));
         } else {
-            cp = closest_point<COUNT>(E.S, w.x, w.y, kClsD, kFInf, w.lastD, hint_at(E.hg, w.x, w.y));
+            cp = closest_point<COUNT>(E.S, w.x, w.y, kClsD, kFInf, w.lastD, hint_at(E.hg, w.x, w.y), entry.x);
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
             R = dD;
@@ -231,7 +241,8 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
     float travel = R;
     bool hit = false;
     if (NEU && !far) {
-        RayHit h = intersect_ray<COUNT>(E.S, w.x, w.y, dx, dy, R, kClsNeumann, E.tguard, w.onN ? w.prevSeg : -1);
+        RayHit h = intersect_ray<COUNT>(E.S, w.x, w.y, dx, dy, R, kClsNeumann, E.tguard, w.onN ? w.prevSeg : -1,
+                                        entry.y);
         if (h.seg >= 0) {
             hit = true;
             travel = h.t;
@@ -613,13 +624,20 @@ __global__ void farfield2_kernel(const SceneView2 S, const FarField F, float* d)
     d[i] = sqrtf(closest_point(S, x, y, kClsAny).d2);
 }
 
-__global__ void hintgrid2_kernel(const SceneView2 S, const HintGrid G, int* id) {
+__global__ void hintgrid2_kernel(const SceneView2 S, const HintGrid G, int* id, int2* entry, float rmin) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= G.nx * G.ny) return;
     int ix = i % G.nx, iy = i / G.nx;
     float x = fmaf(static_cast<float>(ix), G.h, G.lox), y = fmaf(static_cast<float>(iy), G.h, G.loy);
     id[i] = closest_point(S, x, y, kClsD).seg;
+    // cell [v, v + h)^2: centre c, half-diagonal rho; r = dD(c) + 2 rho plus FP32 slack
+    const float cx = x + 0.5f * G.h, cy = y + 0.5f * G.h, rho = 0.70710678f * G.h;
+    const float r = sqrtf(closest_point(S, cx, cy, kClsD).d2) + 2.0f * rho + 1e-5f * S.diagonal;
+    const int star = entry_node(S, cx, cy, r * r, kClsD | kClsSil);
+    const float rr = r + rmin;
+    entry[i] = make_int2(star == kNoEntry ? 0 : star, entry_node(S, cx, cy, rr * rr, kClsNeumann));
 }
+
 
 __global__ void start_hints_kernel(const CacheSample* samples, int n, const int* source, const int* cls,
                                    const int* leafOf, const int* dIdx, int nD, int* hintU, int* hintD) {
@@ -662,8 +680,8 @@ void launch_farfield2(const SceneView2& S, const FarField& F, float* d, cudaStre
     count_launch();
 }
 
-void launch_hintgrid2(const SceneView2& S, const HintGrid& G, int* id, cudaStream_t st) {
-    hintgrid2_kernel<<<blocks(static_cast<long long>(G.nx) * G.ny, 128), 128, 0, st>>>(S, G, id);
+void launch_hintgrid2(const SceneView2& S, const HintGrid& G, int* id, int2* entry, float rmin, cudaStream_t st) {
+    hintgrid2_kernel<<<blocks(static_cast<long long>(G.nx) * G.ny, 128), 128, 0, st>>>(S, G, id, entry, rmin);
     count_launch();
 }
 

@@ -51,7 +51,8 @@ struct Star3 {
 };
 
 template <bool COUNT>
-__device__ __forceinline__ Star3 star_query3(const WalkEnv3& E, float x, float y, float z, int hint, int hint2) {
+__device__ __forceinline__ Star3 star_query3(const WalkEnv3& E, float x, float y, float z, int hint, int hint2,
+                                             int start) {
     Star3 q{hint >= 0 ? closest_on3(E.S, hint, x, y, z) : Closest3{kFInf, 0.f, 0.f, 0.f, -1, -1}, kFInf};
     if (hint2 >= 0 && hint2 != hint) {
         Closest3 h = closest_on3(E.S, hint2, x, y, z);
@@ -73,7 +74,7 @@ __device__ __forceinline__ Star3 star_query3(const WalkEnv3& E, float x, float y
                 if (sl.z >= 0 && sil_edge_ok(E, sl.z, x, y, z, d2) && d2 < q.s2) q.s2 = d2;
             }
         },
-        [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); });
+        [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); }, start);
     return q;
 }
 
@@ -84,8 +85,9 @@ struct Hit3 {
 
 template <bool COUNT>
 __device__ __forceinline__ Hit3 ray_neumann3(const WalkEnv3& E, float ox, float oy, float oz, float dx, float dy,
-                                             float dz, float tMax, int skip) {
+                                             float dz, float tMax, int skip, int start) {
     Hit3 h{kFInf, -1};
+    if (start == kNoEntry) return h;
     float idx = f_rcp(dx), idy = f_rcp(dy), idz = f_rcp(dz);  // slab tests on padded boxes
     const F2 idxy = pk(idx, idy), noixy = pk(-(ox * idx), -(oy * idy));
     const float nozi = -(oz * idz);
@@ -93,7 +95,7 @@ __device__ __forceinline__ Hit3 ray_neumann3(const WalkEnv3& E, float ox, float 
     // nearer child first, the other pushed with its entry distance (dropped at pop once
     // a closer hit is known); while-while structure
     unsigned long long stack[kStack];
-    int sp = 0, ref = 0;
+    int sp = 0, ref = start;
     auto pop = [&]() -> bool {
         for (;;) {
             if (sp == 0) return false;
@@ -188,6 +190,17 @@ __device__ __forceinline__ int hint_at3(const HintGrid& G, float x, float y, flo
     return __ldg(G.id + (static_cast<size_t>(iz) * G.ny + iy) * G.nx + ix);
 }
 
+// the cell entry refs of x (HintGrid), or the root for both outside the grid
+__device__ __forceinline__ int2 entry_at3(const HintGrid& G, float x, float y, float z) {
+    if (!G.entry) return make_int2(0, 0);
+    const int ix = __float2int_rd((x - G.lox) * G.invH), iy = __float2int_rd((y - G.loy) * G.invH),
+              iz = __float2int_rd((z - G.loz) * G.invH);
+    if (static_cast<unsigned>(ix) >= static_cast<unsigned>(G.nx) || static_cast<unsigned>(iy) >= static_cast<unsigned>(G.ny) ||
+        static_cast<unsigned>(iz) >= static_cast<unsigned>(G.nz))
+        return make_int2(0, 0);
+    return __ldg(G.entry + (static_cast<size_t>(iz) * G.ny + iy) * G.nx + ix);
+}
+
 struct Walk3 {
     float x, y, z, weight;
     float inx, iny, inz;
@@ -220,17 +233,19 @@ __device__ __forceinline__ bool walk3_step(const WalkEnv3& E, Walk3& w, U4 rnd, 
     // far field: a ball from the distance grid, no BVH queries (FarField)
     const float lb = E.ff.d ? farfield_bound3(E.ff, w.x, w.y, w.z) : -1.0f;
     const bool far = lb >= E.ff.tau;
+    const int2 entry = far ? make_int2(0, 0) : entry_at3(E.hg, w.x, w.y, w.z);
     if (far) {
         R = lb;
     } else {
         if constexpr (NEU) {
-            Star3 q = star_query3<COUNT>(E, w.x, w.y, w.z, w.lastD, hint_at3(E.hg, w.x, w.y, w.z));
+            Star3 q = star_query3<COUNT>(E, w.x, w.y, w.z, w.lastD, hint_at3(E.hg, w.x, w.y, w.z), entry.x);
             cp = q.D;
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
             R = fminf(dD, sqrtf(q.s2));
         } else {
-            cp = closest_point3<COUNT>(E.S, w.x, w.y, w.z, kClsD, kFInf, w.lastD, hint_at3(E.hg, w.x, w.y, w.z));
+            cp = closest_point3<COUNT>(E.S, w.x, w.y, w.z, kClsD, kFInf, w.lastD, hint_at3(E.hg, w.x, w.y, w.z),
+                                       entry.x);
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
             R = dD;
@@ -244,7 +259,7 @@ __device__ __forceinline__ bool walk3_step(const WalkEnv3& E, Walk3& w, U4 rnd, 
     float travel = R;
     bool hit = false;
     if (NEU && !far) {
-        Hit3 h = ray_neumann3<COUNT>(E, w.x, w.y, w.z, dx, dy, dz, R, w.onN ? w.prevTri : -1);
+        Hit3 h = ray_neumann3<COUNT>(E, w.x, w.y, w.z, dx, dy, dz, R, w.onN ? w.prevTri : -1, entry.y);
         if (h.tri >= 0) {
             hit = true;
             travel = h.t;
@@ -565,17 +580,23 @@ void launch_walk3_t(const WalkEnv3& env, const WalkJob3& job, long long total, c
     walk3_kernel<NEU, SCR, COUNT><<<grid, kThreads3, 0, st>>>(env, job);
 }
 
-__global__ void hintgrid3_kernel(const SceneView3 S, const HintGrid G, int* id) {
+__global__ void hintgrid3_kernel(const SceneView3 S, const HintGrid G, int* id, int2* entry, float rmin) {
     long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= static_cast<long long>(G.nx) * G.ny * G.nz) return;
     int ix = static_cast<int>(i % G.nx), iy = static_cast<int>((i / G.nx) % G.ny), iz = static_cast<int>(i / (static_cast<long long>(G.nx) * G.ny));
     float x = fmaf(static_cast<float>(ix), G.h, G.lox), y = fmaf(static_cast<float>(iy), G.h, G.loy),
           z = fmaf(static_cast<float>(iz), G.h, G.loz);
     id[i] = closest_point3(S, x, y, z, kClsD).prim;
+    // cell [v, v + h)^3: centre c, half-diagonal rho; r = dD(c) + 2 rho plus FP32 slack
+    const float cx = x + 0.5f * G.h, cy = y + 0.5f * G.h, cz = z + 0.5f * G.h, rho = 0.8660254f * G.h;
+    const float r = sqrtf(closest_point3(S, cx, cy, cz, kClsD).d2) + 2.0f * rho + 1e-5f * S.diagonal;
+    const int star = entry_node3(S, cx, cy, cz, r * r, kClsD | kClsSil);
+    const float rr = r + rmin;
+    entry[i] = make_int2(star == kNoEntry ? 0 : star, entry_node3(S, cx, cy, cz, rr * rr, kClsNeumann));
 }
 
-void launch_hintgrid3(const SceneView3& S, const HintGrid& G, int* id, cudaStream_t st) {
-    hintgrid3_kernel<<<blocks(static_cast<long long>(G.nx) * G.ny * G.nz, 128), 128, 0, st>>>(S, G, id);
+void launch_hintgrid3(const SceneView3& S, const HintGrid& G, int* id, int2* entry, float rmin, cudaStream_t st) {
+    hintgrid3_kernel<<<blocks(static_cast<long long>(G.nx) * G.ny * G.nz, 128), 128, 0, st>>>(S, G, id, entry, rmin);
     count_launch();
 }
 

@@ -57,3 +57,16 @@ def test_error_codes_map_to_reference_exceptions():
     assert issubclass(B.ParseError, B.BvcError) and issubclass(B.SolverError, B.BvcError)
     msg = B.lib().bvc_last_error()
     assert isinstance(msg, bytes)
+
+
+def test_library_has_no_unresolved_internal_symbols():
+    """A declaration/definition mismatch between translation units links into a .so
+    that only fails when it is loaded; catch it at build time."""
+    import shutil
+    import subprocess
+
+    if shutil.which("nm") is None:
+        pytest.skip("nm not available")
+    out = subprocess.run(["nm", "-D", "--undefined-only", B.library_path()], capture_output=True, text=True).stdout
+    bad = [line for line in out.splitlines() if "bvc_impl" in line or "bvc_capi" in line or "bvc_host" in line]
+    assert not bad, bad
