@@ -16,7 +16,9 @@ import numpy as np
 
 from . import abi
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libbvc_b200.so")
+# BVC_LIB: another build of the library (A/B runs of compile-time variants)
+_LIB_PATH = os.environ.get("BVC_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build",
+                                                      "libbvc_b200.so")
 _lib = None
 
 # exported symbols declared in include/bvc_b200.h (kept in sync by tests/test_abi.py)

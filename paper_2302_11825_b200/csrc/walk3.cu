@@ -320,10 +320,10 @@ __device__ __forceinline__ U4 draw3(const WalkEnv3& E, Task3& t) {
     return philox4x32_10(c, E.k0, E.k1);
 }
 
-// 8 resident blocks per SM at 32 registers (spilling) beat fewer blocks with more
-// registers (C5: 4.24 s at 8, 4.47 s at 6, 5.58 s at 4; C4: 548 / 552 / 716 ms)
-template <bool NEU, bool SCR, bool COUNT>
-__global__ void __launch_bounds__(kThreads3, 8) walk3_kernel(const WalkEnv3 E, const WalkJob3 J) {
+// resident blocks per SM: Neumann scenes 8 (32 registers, spilling; C5: 3.54 s at 8, 3.60 s
+// at 6), Dirichlet-only 6 (40 registers; C4 walks 435 ms at 6, 469 at 5, 521 at 4, 477 at 8)
+template <bool NEU, bool SCR, bool COUNT, int MINB = NEU ? 8 : 6>
+__global__ void __launch_bounds__(kThreads3, MINB) walk3_kernel(const WalkEnv3 E, const WalkJob3 J) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const long long nUtot = static_cast<long long>(J.nPtsU) * J.nU;
