@@ -237,7 +237,9 @@ void bvc_scene_s::upload3() {
     std::vector<float4> ea(ne), eb(ne), e1(ne), e2(ne);
     for (size_t k = 0; k < host.sil3Always.size(); ++k) {
         ea[k] = f4(&host.sil3A[3 * k], 0.f);
-        eb[k] = f4(&host.sil3B[3 * k], 0.f);
+        const double ex = host.sil3B[3 * k] - host.sil3A[3 * k], ey = host.sil3B[3 * k + 1] - host.sil3A[3 * k + 1],
+                     ez = host.sil3B[3 * k + 2] - host.sil3A[3 * k + 2], l2 = ex * ex + ey * ey + ez * ez;
+        eb[k] = f4(&host.sil3B[3 * k], l2 > 0.0 ? static_cast<float>(1.0 / l2) : 0.f);  // w: 1 / |b - a|^2
         e1[k] = f4(&host.sil3N1[3 * k], host.sil3Always[k] ? 1.f : 0.f);
         e2[k] = f4(&host.sil3N2[3 * k], 0.f);
     }

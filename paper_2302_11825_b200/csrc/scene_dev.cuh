@@ -237,9 +237,11 @@ __device__ __forceinline__ StarQuery star_query(const SceneView2& S, float x, fl
                 float d2 = seg_closest(p.seg, x, y, px, py, t);
                 if (d2 < q.D.d2) { q.D.d2 = d2; q.D.px = px; q.D.py = py; q.D.t = t; q.D.seg = p.id; }
             } else {
+                // a silhouette no closer than the closest Dirichlet point cannot shorten
+                // R = min(dD, dS) (pointwise.cpp:136-138) nor the pruning radius
                 float d2;
-                if (p.sil0 >= 0 && silhouette_ok(S, p.sil0, x, y, d2) && d2 < q.s2) q.s2 = d2;
-                if (p.sil1 >= 0 && silhouette_ok(S, p.sil1, x, y, d2) && d2 < q.s2) q.s2 = d2;
+                if (p.sil0 >= 0 && silhouette_ok(S, p.sil0, x, y, d2) && d2 < fminf(q.s2, q.D.d2)) q.s2 = d2;
+                if (p.sil1 >= 0 && silhouette_ok(S, p.sil1, x, y, d2) && d2 < fminf(q.s2, q.D.d2)) q.s2 = d2;
             }
         },
         [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); }, start);

@@ -30,19 +30,27 @@ constexpr int kChunk3 = 64;
 
 __device__ __forceinline__ float g3(const WalkEnv3& E, const Closest3& c) { return field_eval(E.P.g, c.px, c.py, c.pz); }
 
-// silhouette edge k visible from x (the 3D analogue of scene.cpp:166-172)
-__device__ __forceinline__ bool sil_edge_ok(const WalkEnv3& E, int k, float x, float y, float z, float& d2) {
-    float4 a = E.silA[k], b = E.silB[k], n1 = E.silN1[k], n2 = E.silN2[k];
-    float ux = b.x - a.x, uy = b.y - a.y, uz = b.z - a.z;
-    float l2 = ux * ux + uy * uy + uz * uz;
-    float tt = l2 > 0.f ? ((x - a.x) * ux + (y - a.y) * uy + (z - a.z) * uz) / l2 : 0.f;
+// Silhouette edge k visible from x (the 3D analogue of scene.cpp:166-172), closer than
+// `bound` (squared): d2 = squared distance to the edge. Visibility is tested first (it
+// needs only the edge's first endpoint and the two face normals), so an edge hidden
+// from x never loads its second endpoint or computes the distance; silB.w = 1 / |b - a|^2.
+__device__ __forceinline__ bool sil_edge_ok(const WalkEnv3& E, int k, float x, float y, float z, float bound,
+                                            float& d2) {
+    const float4 a = E.silA[k], n1 = E.silN1[k];
+    const float ax = a.x - x, ay = a.y - y, az = a.z - z;
+    if (n1.w == 0.f) {  // closed edge (n1.w != 0: open boundary edge, a silhouette from everywhere)
+        const float4 n2 = E.silN2[k];
+        const float s1 = n1.x * ax + n1.y * ay + n1.z * az, s2 = n2.x * ax + n2.y * ay + n2.z * az;
+        if (s1 * s2 > 0.0f) return false;
+    }
+    const float4 b = E.silB[k];
+    const float ux = b.x - a.x, uy = b.y - a.y, uz = b.z - a.z;
+    // the parameter only places the closest point (the distance is stationary in it)
+    float tt = -(ax * ux + ay * uy + az * uz) * b.w;
     tt = fminf(fmaxf(tt, 0.f), 1.f);
-    float qx = a.x + tt * ux - x, qy = a.y + tt * uy - y, qz = a.z + tt * uz - z;
+    const float qx = fmaf(tt, ux, ax), qy = fmaf(tt, uy, ay), qz = fmaf(tt, uz, az);
     d2 = qx * qx + qy * qy + qz * qz;
-    if (n1.w != 0.f) return true;  // open boundary edge: silhouette from everywhere
-    float ax = a.x - x, ay = a.y - y, az = a.z - z;
-    float s1 = n1.x * ax + n1.y * ay + n1.z * az, s2 = n2.x * ax + n2.y * ay + n2.z * az;
-    return s1 * s2 <= 0.0f;
+    return d2 < bound;
 }
 
 struct Star3 {
@@ -67,11 +75,13 @@ __device__ __forceinline__ Star3 star_query3(const WalkEnv3& E, float x, float y
                 float d2 = tri_closest(p, x, y, z, qx, qy, qz);
                 if (d2 < q.D.d2) q.D = Closest3{d2, qx, qy, qz, __float_as_int(p.a.w), i};
             } else {
+                // a silhouette no closer than the closest Dirichlet point cannot shorten
+                // R = min(dD, dS) (pointwise.cpp:136-138) nor the pruning radius
                 int4 sl = E.triSil[__float_as_int(p.a.w)];
                 float d2;
-                if (sl.x >= 0 && sil_edge_ok(E, sl.x, x, y, z, d2) && d2 < q.s2) q.s2 = d2;
-                if (sl.y >= 0 && sil_edge_ok(E, sl.y, x, y, z, d2) && d2 < q.s2) q.s2 = d2;
-                if (sl.z >= 0 && sil_edge_ok(E, sl.z, x, y, z, d2) && d2 < q.s2) q.s2 = d2;
+                if (sl.x >= 0 && sil_edge_ok(E, sl.x, x, y, z, fminf(q.s2, q.D.d2), d2)) q.s2 = d2;
+                if (sl.y >= 0 && sil_edge_ok(E, sl.y, x, y, z, fminf(q.s2, q.D.d2), d2)) q.s2 = d2;
+                if (sl.z >= 0 && sil_edge_ok(E, sl.z, x, y, z, fminf(q.s2, q.D.d2), d2)) q.s2 = d2;
             }
         },
         [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); }, start);
