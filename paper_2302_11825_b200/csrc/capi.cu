@@ -7,6 +7,8 @@
 // BVC_ERR_NO_DEVICE when no CUDA device is present.
 #include <atomic>
 
+#include <cub/device/device_scan.cuh>
+
 #include "capi_common.cuh"
 
 namespace bvc_capi {
@@ -253,7 +255,34 @@ void bvc_scene_s::upload3() {
     if (build_on_gpu()) gpu_build(3, triA.p, triB.p, triC.p, nullptr);
     leafOf.resize(std::max(host.ns, 1));  // triangle id -> leaf index (walk warm starts)
     launch_leaf_index(3, prims3.p, host.ns, leafOf.p, g_stream);
+    if (!host.sil3Always.empty()) build_sil_records();
     uploaded = true;
+}
+
+
+// Silhouette-edge records in leaf order: a star query that reaches a triangle with
+// silhouette edges reads them next to the triangle's neighbours in the same leaf,
+// without the dependent triSil -> edge-array loads (Prim3.c.w = first << 2 | count).
+void bvc_scene_s::build_sil_records() {
+    const int n = host.ns;
+    DevBuf<int> counts, offsets;
+    counts.resize(n);
+    offsets.resize(n);
+    launch_sil_count3(prims3.p, n, triSil.p, counts.p, g_stream);
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts.p, offsets.p, n, g_stream));
+    DevBuf<char> scratch;
+    scratch.resize(std::max<size_t>(tmp, 1));
+    CK(cub::DeviceScan::ExclusiveSum(scratch.p, tmp, counts.p, offsets.p, n, g_stream));
+    int last[2] = {0, 0};
+    CK(cudaMemcpyAsync(&last[0], offsets.p + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaMemcpyAsync(&last[1], counts.p + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+    silRec.resize(4 * static_cast<size_t>(std::max(last[0] + last[1], 1)));
+    launch_sil_fill3(prims3.p, n, triSil.p, counts.p, offsets.p, sil3A.p, sil3N1.p, sil3N2.p, sil3B.p, silRec.p,
+                     g_stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(g_stream));
 }
 
 

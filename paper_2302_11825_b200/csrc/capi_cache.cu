@@ -131,6 +131,7 @@ WalkEnv3 make_env3(bvc_scene_s* S, const bvc_problem& pb, const bvc_walk_config&
         throw Error(BVC_ERR_SOLVER, "walk cannot terminate: scene has no Dirichlet boundary");
     WalkEnv3 E{};
     E.S = S->view3();
+    E.silRec = S->silRec.p;
     E.triSil = S->triSil.p;
     E.silA = S->sil3A.p;
     E.silB = S->sil3B.p;

@@ -205,6 +205,7 @@ struct bvc_scene_s {
     DevBuf<bvc_dev::Prim3> prims3;
     DevBuf<float4> triNormal, triA, triB, triC, sil3A, sil3B, sil3N1, sil3N2;
     DevBuf<int4> triSil;
+    DevBuf<float4> silRec;  // silhouette-edge records in leaf order (WalkEnv3::silRec)
     // far-field distance grid (FarField, internal.h), built on first walk use. Opt-in
     // (BVC_FARFIELD=1): smaller balls in the far field keep the estimator unbiased but
     // change where walks enter the eps-shell, i.e. the O(eps) shell bias, so results
@@ -238,6 +239,7 @@ struct bvc_scene_s {
     void gpu_build(int dim, const float4* a, const float4* b, const float4* c, const int2* sil);
 
     void upload3();
+    void build_sil_records();
     bvc_dev::SceneView3 view3();
 
     void upload();

@@ -30,22 +30,22 @@ constexpr int kChunk3 = 64;
 
 __device__ __forceinline__ float g3(const WalkEnv3& E, const Closest3& c) { return field_eval(E.P.g, c.px, c.py, c.pz); }
 
-// Silhouette edge k visible from x (the 3D analogue of scene.cpp:166-172), closer than
-// `bound` (squared): d2 = squared distance to the edge. Visibility is tested first (it
-// needs only the edge's first endpoint and the two face normals), so an edge hidden
-// from x never loads its second endpoint or computes the distance; silB.w = 1 / |b - a|^2.
-__device__ __forceinline__ bool sil_edge_ok(const WalkEnv3& E, int k, float x, float y, float z, float bound,
-                                            float& d2) {
-    const float4 a = E.silA[k], n1 = E.silN1[k];
+// Silhouette edge visible from x (the 3D analogue of scene.cpp:166-172) and closer than
+// `bound` (squared); rec = its leaf-order record (a, n1, n2, b) in WalkEnv3::silRec, d2 =
+// squared distance. Visibility is tested first (the first endpoint and the two face
+// normals), so an edge hidden from x never loads its second endpoint or computes the
+// distance; n1.w != 0 marks an open boundary edge (a silhouette from
+// everywhere), b.w = 1 / |b - a|^2.
+__device__ __forceinline__ bool sil_rec_ok(const float4* rec, float x, float y, float z, float bound, float& d2) {
+    const float4 a = rec[0], n1 = rec[1];
     const float ax = a.x - x, ay = a.y - y, az = a.z - z;
-    if (n1.w == 0.f) {  // closed edge (n1.w != 0: open boundary edge, a silhouette from everywhere)
-        const float4 n2 = E.silN2[k];
+    if (n1.w == 0.f) {
+        const float4 n2 = rec[2];
         const float s1 = n1.x * ax + n1.y * ay + n1.z * az, s2 = n2.x * ax + n2.y * ay + n2.z * az;
         if (s1 * s2 > 0.0f) return false;
     }
-    const float4 b = E.silB[k];
+    const float4 b = rec[3];
     const float ux = b.x - a.x, uy = b.y - a.y, uz = b.z - a.z;
-    // the parameter only places the closest point (the distance is stationary in it)
     float tt = -(ax * ux + ay * uy + az * uz) * b.w;
     tt = fminf(fmaxf(tt, 0.f), 1.f);
     const float qx = fmaf(tt, ux, ax), qy = fmaf(tt, uy, ay), qz = fmaf(tt, uz, az);
@@ -77,11 +77,10 @@ __device__ __forceinline__ Star3 star_query3(const WalkEnv3& E, float x, float y
             } else {
                 // a silhouette no closer than the closest Dirichlet point cannot shorten
                 // R = min(dD, dS) (pointwise.cpp:136-138) nor the pruning radius
-                int4 sl = E.triSil[__float_as_int(p.a.w)];
+                const int code = __float_as_int(p.c.w);
                 float d2;
-                if (sl.x >= 0 && sil_edge_ok(E, sl.x, x, y, z, fminf(q.s2, q.D.d2), d2)) q.s2 = d2;
-                if (sl.y >= 0 && sil_edge_ok(E, sl.y, x, y, z, fminf(q.s2, q.D.d2), d2)) q.s2 = d2;
-                if (sl.z >= 0 && sil_edge_ok(E, sl.z, x, y, z, fminf(q.s2, q.D.d2), d2)) q.s2 = d2;
+                for (int k = code >> 2, e = (code >> 2) + (code & 3); k < e; ++k)
+                    if (sil_rec_ok(E.silRec + 4 * static_cast<size_t>(k), x, y, z, fminf(q.s2, q.D.d2), d2)) q.s2 = d2;
             }
         },
         [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); }, start);
@@ -607,6 +606,46 @@ __global__ void hintgrid3_kernel(const SceneView3 S, const HintGrid G, int* id, 
 
 void launch_hintgrid3(const SceneView3& S, const HintGrid& G, int* id, int2* entry, float rmin, cudaStream_t st) {
     hintgrid3_kernel<<<blocks(static_cast<long long>(G.nx) * G.ny * G.nz, 128), 128, 0, st>>>(S, G, id, entry, rmin);
+    count_launch();
+}
+
+__global__ void sil_count3_kernel(const Prim3* prims, int n, const int4* triSil, int* counts) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int4 sl = triSil[__float_as_int(prims[j].a.w)];
+    counts[j] = (sl.x >= 0) + (sl.y >= 0) + (sl.z >= 0);
+}
+
+__global__ void sil_fill3_kernel(Prim3* prims, int n, const int4* triSil, const int* counts, const int* offsets,
+                                 const float4* silA, const float4* silN1, const float4* silN2, const float4* silB,
+                                 float4* rec) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int4 sl = triSil[__float_as_int(prims[j].a.w)];
+    const int e[3] = {sl.x, sl.y, sl.z};
+    int k = offsets[j];
+    for (int r = 0; r < 3; ++r) {
+        if (e[r] < 0) continue;
+        float4* o = rec + 4 * static_cast<size_t>(k++);
+        o[0] = silA[e[r]];
+        o[1] = silN1[e[r]];
+        o[2] = silN2[e[r]];
+        o[3] = silB[e[r]];
+    }
+    prims[j].c.w = __int_as_float((offsets[j] << 2) | counts[j]);
+}
+
+void launch_sil_count3(const Prim3* prims, int n, const int4* triSil, int* counts, cudaStream_t st) {
+    if (n <= 0) return;
+    sil_count3_kernel<<<blocks(n, 256), 256, 0, st>>>(prims, n, triSil, counts);
+    count_launch();
+}
+
+void launch_sil_fill3(Prim3* prims, int n, const int4* triSil, const int* counts, const int* offsets,
+                      const float4* silA, const float4* silN1, const float4* silN2, const float4* silB, float4* rec,
+                      cudaStream_t st) {
+    if (n <= 0) return;
+    sil_fill3_kernel<<<blocks(n, 256), 256, 0, st>>>(prims, n, triSil, counts, offsets, silA, silN1, silN2, silB, rec);
     count_launch();
 }
 
