@@ -1,0 +1,46 @@
+"""Walk-query accelerations that must not change the walks: the warm-start grid
+(HintGrid: one more seed of the closest-point bound) and the cell entry nodes (queries
+start at a subtree holding every usable primitive). Each only prunes
+work, so caches with and without it agree bitwise except where a distance tie (the
+shared vertex of two primitives, the closest point of every query in a reflex
+vertex's wedge) is broken the other way: the two distances differ by rounding, the
+walker then moves by an ulp, and a later termination test can flip. Those walks
+change; the samples holding them are few."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(tmp_path, name, env_extra):
+    out = str(tmp_path / f"{name}.npz")
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    for k in ("BVC_HINTGRID", "BVC_ENTRY"):
+        env.pop(k, None)
+    env.update(env_extra)
+    subprocess.run([sys.executable, os.path.join(ROOT, "tests", "walk_accel_case.py"), out], env=env, check=True,
+                   timeout=600)
+    return np.load(out)
+
+
+@pytest.fixture(scope="module")
+def default_run(tmp_path_factory):
+    return _run(tmp_path_factory.mktemp("accel"), "default", {})
+
+
+@pytest.mark.parametrize("switch", ["BVC_HINTGRID", "BVC_ENTRY"])
+def test_acceleration_leaves_walks_unchanged(tmp_path, default_run, switch):
+    a, b = _run(tmp_path, switch, {switch: "0"}), default_run
+    for k in a.files:
+        if k.endswith("_steps"):
+            assert abs(int(a[k][0]) - int(b[k][0])) <= 1e-4 * int(a[k][0]), (switch, k)
+            continue
+        assert np.all(np.isfinite(b[k])), k
+        # ties move g(closest point) by ulps (same walk); rarely a walk changes path
+        close = np.mean(np.abs(a[k] - b[k]) <= 1e-5 * np.abs(a[k]).max())
+        assert close >= 0.97, (switch, k, close)

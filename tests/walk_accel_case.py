@@ -1,6 +1,7 @@
-"""Child process of tests/test_gpu_hintgrid.py: small versions of the BASELINE
-configs; dumps the walk outputs (cache u-hat / d-hat) of one round. Run once with
-BVC_HINTGRID=0 and once with the warm-start grid (the default)."""
+"""Child process of tests/test_gpu_walk_accel.py: small versions of the BASELINE
+configs; dumps the walk outputs (cache u-hat / d-hat) of one round. Run with one
+walk-query acceleration switched off (BVC_HINTGRID / BVC_ENTRY = 0) and
+with the defaults."""
 import sys
 
 import numpy as np
