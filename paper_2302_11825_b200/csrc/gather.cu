@@ -522,8 +522,8 @@ __device__ __forceinline__ void tile_loop(const float4* S, int cnt, const float*
     }
 }
 
-template <int KIND, bool VAL, bool GRAD, int MODE = 0>
-__global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
+template <int KIND, bool VAL, bool GRAD, int MODE>
+__device__ __forceinline__ void gather_body(const Params& P) {
     __shared__ __align__(128) float4 sm[2][2 * kTS];
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ int sUnit;
@@ -650,6 +650,17 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
         unit = sUnit;
         __syncthreads();
     }
+}
+
+template <int KIND, bool VAL, bool GRAD, int MODE = 0>
+__global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
+    gather_body<KIND, VAL, GRAD, MODE>(P);
+}
+// the Laplace kinds at 8 resident CTAs (64 registers): C2 gather -2%, C4 -5%; the
+// screened kinds spill 272-448 B at 64 registers and keep the compiler's choice (C3 +2%)
+template <int KIND, bool VAL, bool GRAD>
+__global__ void __launch_bounds__(kThreads, 8) gather_kernel8(const Params P) {
+    gather_body<KIND, VAL, GRAD, 0>(P);
 }
 
 // bounding box of each 256-sample tile (one warp per tile)
@@ -813,17 +824,29 @@ __global__ void gather_points_kernel(const double* x, const int* order, int K, i
 
 template <int KIND>
 void launch_kind(const Params& P, bool val, bool grad, int grid, cudaStream_t st) {
-    if (val && grad) gather_kernel<KIND, true, true><<<grid, kThreads, 0, st>>>(P);
-    else if (val) gather_kernel<KIND, true, false><<<grid, kThreads, 0, st>>>(P);
-    else gather_kernel<KIND, false, true><<<grid, kThreads, 0, st>>>(P);
+    if constexpr (KIND == kLap2 || KIND == kLap3) {
+        if (val && grad) gather_kernel8<KIND, true, true><<<grid, kThreads, 0, st>>>(P);
+        else if (val) gather_kernel8<KIND, true, false><<<grid, kThreads, 0, st>>>(P);
+        else gather_kernel8<KIND, false, true><<<grid, kThreads, 0, st>>>(P);
+    } else {
+        if (val && grad) gather_kernel<KIND, true, true><<<grid, kThreads, 0, st>>>(P);
+        else if (val) gather_kernel<KIND, true, false><<<grid, kThreads, 0, st>>>(P);
+        else gather_kernel<KIND, false, true><<<grid, kThreads, 0, st>>>(P);
+    }
 }
 
 template <int KIND>
 int occupancy(bool val, bool grad) {
     int occ = 0;
-    if (val && grad) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel<KIND, true, true>, kThreads, 0);
-    else if (val) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel<KIND, true, false>, kThreads, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel<KIND, false, true>, kThreads, 0);
+    if constexpr (KIND == kLap2 || KIND == kLap3) {
+        if (val && grad) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel8<KIND, true, true>, kThreads, 0);
+        else if (val) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel8<KIND, true, false>, kThreads, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel8<KIND, false, true>, kThreads, 0);
+    } else {
+        if (val && grad) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel<KIND, true, true>, kThreads, 0);
+        else if (val) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel<KIND, true, false>, kThreads, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel<KIND, false, true>, kThreads, 0);
+    }
     return occ > 0 ? occ : 1;
 }
 
