@@ -47,10 +47,32 @@ void ensure_pool() {
     device = d;
 }
 
+Workspace* g_wsActive = nullptr;
 Workspace& ws() {
     static Workspace w;
-    return w;
+    return g_wsActive ? *g_wsActive : w;
 }
+
+namespace {
+struct Side {
+    cudaStream_t stream = nullptr;
+    Workspace* work = nullptr;
+};
+Side& side_for_device() {
+    static Side sides[64];
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    need(dev >= 0 && dev < 64, "device index out of range");
+    Side& sd = sides[dev];
+    if (!sd.stream) {
+        CK(cudaStreamCreateWithFlags(&sd.stream, cudaStreamNonBlocking));
+        sd.work = new Workspace();  // lives for the process, like the main workspace
+    }
+    return sd;
+}
+}  // namespace
+
+SideScope::SideScope() : stream(side_for_device().stream), saved(g_wsActive) { g_wsActive = side_for_device().work; }
 
 int fail(const std::exception& e) {
     g_error = e.what();

@@ -113,7 +113,20 @@ struct Workspace {
         return reinterpret_cast<T*>(slots[slot]->p);
     }
 };
+// ws() hands out the active workspace: the main one, or (inside a SideScope) the side
+// stream's own, so work on the two streams never shares scratch buffers
+extern Workspace* g_wsActive;
 Workspace& ws();
+// a second stream with its own workspace (one per device), for work that overlaps the
+// main stream's cache walks
+struct SideScope {
+    StreamScope stream;
+    Workspace* saved;
+    SideScope();
+    ~SideScope() { g_wsActive = saved; }
+    SideScope(const SideScope&) = delete;
+    SideScope& operator=(const SideScope&) = delete;
+};
 enum Slot {
     kWsSamplesTmp, kWsStartU, kWsIsD, kWsGradR, kWsOutside, kWsDIdx, kWsCount, kWsXD, kWsND, kWsRD, kWsGidD, kWsOutU,
     kWsOutD, kWsCounter, kWsSteps, kWsTrunc, kWsFailed, kWsPack, kWsPart, kWsSkipB, kWsSkipS, kWsPts, kWsCtr,

@@ -225,9 +225,14 @@ bvc_splat_config make_splat_config(bvc_scene_s* S, const bvc_problem& pb, const 
     return s;
 }
 
-// One progressive round (updateSolution cache.cpp:622-684). `points` is called once
-// the cache-walk job is enqueued and returns the evaluation points: a caller may
-// still be preparing them (on another stream) while the walks run.
+// One progressive round (updateSolution cache.cpp:622-684). The fallback-band walks
+// (cache.cpp:665-681) do not depend on the cache: they run on a second stream with its
+// own workspace, started right after the cache-walk job is enqueued, so they overlap
+// the cache walks instead of following the splats (their duration is the longest band
+// walk's serial latency, ~0.3 ms on C2, however few band points there are). `points` runs
+// first on that stream and returns the evaluation points (the host-buffer round uploads
+// and classifies them there). The results equal the sequential order's: the band walks
+// and the splats write different fields, with the same per-point RNG streams.
 void update_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const bvc_cache_config& cfg,
                   const std::function<bvc_eval_points_s*()>& points, uint64_t seed, uint64_t round, int gradients,
                   bvc_round_stats* stats) {
@@ -237,19 +242,46 @@ void update_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const 
     if (cfg.sourceBall && gradients) throw Error(BVC_ERR_SOLVER, "ball-kernel source mode does not support gradient splats");
     bvc_splat_config scfg = make_splat_config(s, pb, cfg);
     need(cfg.clampMode >= BVC_CLAMP_OFF && cfg.clampMode <= BVC_CLAMP_CORRECT, "unknown clamp mode");
-    cudaEvent_t e0, e1, e2;
+    s->upload();
+    r->upload();
+    cudaEvent_t e0, e1, e2, ready, sideDone;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventCreate(&e2));
+    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&sideDone, cudaEventDisableTiming));
+    struct Events {
+        cudaEvent_t e[5];
+        ~Events() { for (cudaEvent_t x : e) cudaEventDestroy(x); }
+    } guard{{e0, e1, e2, ready, sideDone}};
     CK(cudaEventRecord(e0, g_stream));
+    CK(cudaEventRecord(ready, g_stream));  // uploads and earlier rounds precede the side stream's work
+    bvc_eval_points_s* p = nullptr;
+    bool sideRan = false;
+    auto side = [&] {
+        SideScope scope;
+        CK(cudaStreamWaitEvent(g_stream, ready, 0));
+        p = points();
+        need(p != nullptr, "null evaluation points");
+        fallback_walks(s, pb, cfg, p, seed, round, gradients != 0);
+        CK(cudaEventRecord(sideDone, g_stream));
+        sideRan = true;
+    };
+    g_afterWalkLaunch = side;
     bvc_boundary_cache_s bc;
     bvc_source_cache_s sc;
     GenStats st;
-    generate_cache(s, pb, r, cfg, seed, round, 0, std::max(1, cfg.nBoundary), &bc, st);
+    try {
+        generate_cache(s, pb, r, cfg, seed, round, 0, std::max(1, cfg.nBoundary), &bc, st);
+        if (!sideRan) after_walk_launch();  // no cache-walk job was launched
+    } catch (...) {
+        g_afterWalkLaunch = nullptr;
+        throw;
+    }
+    g_afterWalkLaunch = nullptr;
     generate_source(pb, r, cfg, seed, round, &sc);
     CK(cudaEventRecord(e1, g_stream));
-    bvc_eval_points_s* p = points();
-    need(p != nullptr, "null evaluation points");
+    CK(cudaStreamWaitEvent(g_stream, sideDone, 0));
     bool hasSource = pb.f.kind != BVC_FIELD_NONE;
     bvc_source_cache_s* sp = sc.m ? &sc : nullptr;
     // the mode dispatch of updateSolution (cache.cpp:639-662)
@@ -274,7 +306,6 @@ void update_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const 
         }
         if (gradients) splat(&bc, sp, p, scfg, 0, SIZE_MAX, false, true);
     }
-    fallback_walks(s, pb, cfg, p, seed, round, gradients != 0);
     CK(cudaEventRecord(e2, g_stream));
     CK(cudaEventSynchronize(e2));
     if (stats) {
@@ -285,15 +316,13 @@ void update_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const 
         stats->generateSeconds = device_seconds(e0, e1);
         stats->splatSeconds = device_seconds(e1, e2);
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaEventDestroy(e2);
 }
 
 // runSolveInMemory's round on host-resident points (runner.cpp:116-169: build the
 // points, markEvaluationPoints, updateSolution, read solution() / gradient()). The
-// points' upload, Morton order and classification run on a second stream while the
-// cache walks run; the result equals the handle-based sequence bit for bit.
+// points' upload, Morton order and classification run on the second stream, with the
+// band walks, while the cache walks run; the result equals the handle-based sequence
+// bit for bit.
 void update_round_host(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const bvc_cache_config& cfg,
                        const double* x, size_t n, uint64_t seed, uint64_t round, int gradients, double* u, double* grad,
                        bvc_round_stats* stats) {
@@ -302,44 +331,15 @@ void update_round_host(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, c
     need(!grad || gradients, "gradient output requested without gradients");
     s->upload();
     r->upload();
-    // one side stream per device (bvc_set_device may switch devices between calls)
-    static cudaStream_t sides[64] = {};
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    need(dev >= 0 && dev < 64, "device index out of range");
-    if (!sides[dev]) CK(cudaStreamCreateWithFlags(&sides[dev], cudaStreamNonBlocking));
-    cudaStream_t side = sides[dev];
-    cudaEvent_t ready, done;
-    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-    CK(cudaEventRecord(ready, g_stream));  // scene / region uploads precede the side stream's reads
     std::unique_ptr<bvc_eval_points_s> P;
-    auto prep = [&] {
-        StreamScope scope(side);
-        CK(cudaStreamWaitEvent(side, ready, 0));
-        P = make_points(x, n, s->host.dim);
-        mark_points(s, r, cfg, P.get());
-        ensure_order(P.get());
-        CK(cudaEventRecord(done, side));
-    };
-    g_afterWalkLaunch = prep;
-    try {
-        update_round(s, pb, r, cfg,
-                     [&]() -> bvc_eval_points_s* {
-                         if (!P) after_walk_launch();  // no walk job was launched
-                         g_afterWalkLaunch = nullptr;
-                         CK(cudaStreamWaitEvent(g_stream, done, 0));
-                         return P.get();
-                     },
-                     seed, round, gradients, stats);
-    } catch (...) {
-        g_afterWalkLaunch = nullptr;
-        cudaEventDestroy(ready);
-        cudaEventDestroy(done);
-        throw;
-    }
-    cudaEventDestroy(ready);
-    cudaEventDestroy(done);
+    update_round(s, pb, r, cfg,
+                 [&]() -> bvc_eval_points_s* {  // on the side stream
+                     P = make_points(x, n, s->host.dim);
+                     mark_points(s, r, cfg, P.get());
+                     ensure_order(P.get());
+                     return P.get();
+                 },
+                 seed, round, gradients, stats);
     if (n == 0) return;
     const int d = P->dim;
     double* o = ws().get<double>(kWsEvalOut, (1 + d) * n);

@@ -54,3 +54,23 @@ def test_host_round_empty_and_errors():
     with pytest.raises(B.InvalidArgument):
         B.update_solution_host(sc, c.problem, region, c.cache, x, c.seed, 1, gradients=False,
                                out=(np.zeros(len(x)), np.zeros((len(x), 2))))
+
+
+def test_overlapped_round_equals_sequential_pieces():
+    """updateSolution runs the fallback-band walks on a second stream while the cache
+    walks run; the reference's order (cache, splats, then band walks, cache.cpp:622-684)
+    rebuilt from the separate entry points gives the same sums bit for bit."""
+    c, sc, region, x, dim = _setup(2, 1 / 32, 20000)
+    p = B.EvaluationPoints(x, dim)
+    B.mark_evaluation_points(sc, region, c.cache, p)
+    B.update_solution(sc, c.problem, region, c.cache, p, c.seed, 3, gradients=True)
+    q = B.EvaluationPoints(x, dim)
+    B.mark_evaluation_points(sc, region, c.cache, q)
+    cache = B.generate_boundary_cache(sc, c.problem, region, c.cache, c.seed, 3)
+    spec = B.make_splat_config(sc, c.problem, c.cache)
+    B.splat_solution_gradient(cache, None, q, spec)
+    B.fallback_walks(sc, c.problem, c.cache, q, c.seed, 3, True)
+    a, b = p.download(), q.download()
+    assert a["fallback"].sum() > 0
+    for k in ("boundarySum", "boundaryGradSum", "nBoundary", "walkSum", "walkCount", "gradientWalkSum"):
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
