@@ -175,12 +175,12 @@ def run_gpu(args):
         from paper_2302_11825_b200 import distributed
 
         stats = {}
+        # the rank's band walks (fallback points) run during its shard's walks
         cache = distributed.generate_and_allgather(B, dist, torch, scene, c.problem, region, cfg, c.seed, rnd,
-                                                   rank, world, stats)
+                                                   rank, world, stats, points=p, gradients=bool(c.gradients))
         scache = B.generate_source_cache(c.problem, region, cfg, c.seed, rnd) if M else None
         spec = B.make_splat_config(scene, c.problem, cfg)
         B.splat_range(cache, scache, p, spec, 0, 1 << 62, True, bool(c.gradients))
-        B.fallback_walks(scene, c.problem, cfg, p, c.seed, rnd, bool(c.gradients))  # this rank's band points
         return stats
 
     def round_single(p, rnd):

@@ -262,6 +262,14 @@ int bvc_generate_boundary_cache_shard(bvc_scene scene, const bvc_problem* proble
                                       bvc_region region, const bvc_cache_config* cfg,
                                       uint64_t seed, uint64_t round, int begin, int end,
                                       bvc_round_stats* stats, bvc_boundary_cache* out);
+/* the shard above plus the fallback-band walks of `pts` (cache.cpp:665-681, as
+   bvc_fallback_walks) on a second stream while the shard's walks run: a rank's
+   cache work and band walks in one call (the sharded multi-GPU round) */
+int bvc_generate_boundary_cache_shard_fallback(bvc_scene scene, const bvc_problem* problem,
+                                               bvc_region region, const bvc_cache_config* cfg,
+                                               uint64_t seed, uint64_t round, int begin, int end,
+                                               bvc_eval_points pts, int gradients,
+                                               bvc_round_stats* stats, bvc_boundary_cache* out);
 /* generateSourceCache (cache.h:163-164; cache.cpp:392-406) */
 int bvc_generate_source_cache(const bvc_problem* problem, bvc_region region,
                               const bvc_cache_config* cfg, uint64_t seed, uint64_t round,

@@ -36,7 +36,7 @@ SYMBOLS = (
     "bvc_walk_traffic_profile bvc_eval_kernels bvc_eval_bessel bvc_corrected_boundary_splat "
     "bvc_corrected_source_splat bvc_trace_streamlines bvc_grid_save_csv bvc_grid_load_csv bvc_grid_rmse "
     "bvc_grid_save_pgm bvc_streamlines_write_csv bvc_pipe_probe bvc_boundary_cache_assign_voronoi "
-    "bvc_fallback_walks bvc_update_solution_host"
+    "bvc_fallback_walks bvc_update_solution_host bvc_generate_boundary_cache_shard_fallback"
 ).split()
 
 
@@ -485,6 +485,22 @@ def generate_boundary_cache(scene: Scene, pb, region: SolveRegion, cfg, seed, ro
         _check(lib().bvc_generate_boundary_cache_shard(scene.h, C.byref(pb), region.h, C.byref(cfg), C.c_uint64(seed),
                                                        C.c_uint64(round_), int(begin), int(end), C.byref(st),
                                                        C.byref(h)))
+    if stats is not None:
+        stats.update(_stats_dict(st))
+    return BoundaryCache(h)
+
+
+def generate_boundary_cache_with_fallback(scene: Scene, pb, region: SolveRegion, cfg, seed, round_, begin, end,
+                                         pts: "EvaluationPoints", gradients=False,
+                                         stats: dict | None = None) -> BoundaryCache:
+    """A shard [begin, end) of the round's cache plus the fallback-band walks of `pts`
+    (updateSolution cache.cpp:665-681), the latter overlapping the shard's walks."""
+    st = abi.RoundStats()
+    h = C.c_void_p()
+    _check(lib().bvc_generate_boundary_cache_shard_fallback(scene.h, C.byref(pb), region.h, C.byref(cfg),
+                                                            C.c_uint64(seed), C.c_uint64(round_), int(begin),
+                                                            int(end), pts.h, int(gradients), C.byref(st),
+                                                            C.byref(h)))
     if stats is not None:
         stats.update(_stats_dict(st))
     return BoundaryCache(h)

@@ -528,6 +528,53 @@ int bvc_generate_boundary_cache_shard(bvc_scene s, const bvc_problem* pb, bvc_re
         *out = c.release();
     })
 }
+int bvc_generate_boundary_cache_shard_fallback(bvc_scene s, const bvc_problem* pb, bvc_region r,
+                                               const bvc_cache_config* cfg, uint64_t seed, uint64_t round, int begin,
+                                               int end, bvc_eval_points pts, int gradients, bvc_round_stats* stats,
+                                               bvc_boundary_cache* out) {
+    API({
+        need(s && pb && r && cfg && pts && out, "null argument");
+        s->upload();
+        r->upload();
+        auto c = std::make_unique<bvc_boundary_cache_s>();
+        GenStats st;
+        cudaEvent_t ready, done;
+        CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        struct Events {
+            cudaEvent_t a, b;
+            ~Events() { cudaEventDestroy(a); cudaEventDestroy(b); }
+        } guard{ready, done};
+        CK(cudaEventRecord(ready, g_stream));
+        bool ran = false;
+        // the rank's band walks on the side stream while the shard's walks run (update_round)
+        auto side = [&] {
+            SideScope scope;
+            CK(cudaStreamWaitEvent(g_stream, ready, 0));
+            fallback_walks(s, *pb, *cfg, pts, seed, round, gradients != 0);
+            CK(cudaEventRecord(done, g_stream));
+            ran = true;
+        };
+        g_afterWalkLaunch = side;
+        try {
+            generate_cache(s, *pb, r, *cfg, seed, round, begin, end, c.get(), st);
+            if (!ran) after_walk_launch();
+        } catch (...) {
+            g_afterWalkLaunch = nullptr;
+            throw;
+        }
+        g_afterWalkLaunch = nullptr;
+        CK(cudaStreamWaitEvent(g_stream, done, 0));
+        CK(cudaStreamSynchronize(g_stream));
+        if (stats) {
+            stats->resampled += st.resampled;
+            stats->cacheWalks += st.walks;
+            stats->cacheTruncated += st.truncated;
+            stats->cacheSteps += st.steps;
+        }
+        *out = c.release();
+    })
+}
 int bvc_generate_boundary_cache(bvc_scene s, const bvc_problem* pb, bvc_region r, const bvc_cache_config* cfg,
                                 uint64_t seed, uint64_t round, bvc_round_stats* stats, bvc_boundary_cache* out) {
     return bvc_generate_boundary_cache_shard(s, pb, r, cfg, seed, round, 0, std::max(1, cfg ? cfg->nBoundary : 1), stats,

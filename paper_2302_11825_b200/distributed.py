@@ -40,6 +40,10 @@ class _DeviceBytes:
 def allgather_bytes(dist, torch, local, sizes_bytes):
     """All-gather variable-size int32 shards (padded to the largest) and concatenate."""
     words = max(sizes_bytes) // 4
+    if all(s == sizes_bytes[0] for s in sizes_bytes) and local.numel() == words:  # equal shards: one buffer
+        out = torch.empty(words * len(sizes_bytes), dtype=torch.int32, device=local.device)
+        dist.all_gather_into_tensor(out, local.contiguous())
+        return out
     buf = torch.zeros(words, dtype=torch.int32, device=local.device)
     buf[: local.numel()] = local
     parts = [torch.empty_like(buf) for _ in sizes_bytes]
@@ -47,10 +51,17 @@ def allgather_bytes(dist, torch, local, sizes_bytes):
     return torch.cat([p[: s // 4] for p, s in zip(parts, sizes_bytes)])
 
 
-def generate_and_allgather(B, dist, torch, scene, problem, region, cfg, seed, rnd, rank, world, stats=None):
+def generate_and_allgather(B, dist, torch, scene, problem, region, cfg, seed, rnd, rank, world, stats=None,
+                           points=None, gradients=False):
+    """The rank's shard of the cache, all-gathered; with `points`, the rank's fallback-band
+    walks run during the shard's walks (bvc_generate_boundary_cache_shard_fallback)."""
     N = max(1, cfg.nBoundary)
     s0, s1 = shard_range(N, rank, world)
-    shard = B.generate_boundary_cache(scene, problem, region, cfg, seed, rnd, begin=s0, end=s1, stats=stats)
+    if points is not None:
+        shard = B.generate_boundary_cache_with_fallback(scene, problem, region, cfg, seed, rnd, s0, s1, points,
+                                                        gradients, stats=stats)
+    else:
+        shard = B.generate_boundary_cache(scene, problem, region, cfg, seed, rnd, begin=s0, end=s1, stats=stats)
     ptr, nbytes = shard.packed()
     local = torch.as_tensor(_DeviceBytes(ptr, nbytes), device="cuda") if nbytes else \
         torch.empty(0, dtype=torch.int32, device="cuda")

@@ -1,7 +1,8 @@
 """Projected strong scaling of the sharded round on one GPU: time rank 0's share of a
 W-GPU round (its 1/W of the cache walks, a full-size cache assembled from copies of its
 shard in place of the NCCL all-gather, its 1/W of the points, its fallback band) for
-W = 1, 2, 4, 8. The all-gather itself (48 B x N over NVLink) is not included.
+W = 1, 2, 4, 8 (the band walks overlap the shard's walks, as in bench.py's sharded round).
+The all-gather itself (48 B x N over NVLink) is not included.
     python scripts/sim_rank.py [config]"""
 import sys
 import time
@@ -38,7 +39,8 @@ for W in (1, 2, 4, 8):
     def step(rnd):
         tick("t0")
         s0, s1 = distributed.shard_range(N, 0, W)
-        shard = B.generate_boundary_cache(scene, c.problem, region, cfg, c.seed, rnd, begin=s0, end=s1)
+        shard = B.generate_boundary_cache_with_fallback(scene, c.problem, region, cfg, c.seed, rnd, s0, s1, pts,
+                                                        bool(c.gradients))
         tick("walks")
         ptr, nbytes = shard.packed()
         local = torch.as_tensor(distributed._DeviceBytes(ptr, nbytes), device="cuda")
@@ -51,8 +53,6 @@ for W in (1, 2, 4, 8):
         tick("exchange")
         B.splat_range(cache, None, pts, spec, 0, 1 << 62, True, bool(c.gradients))
         tick("gather")
-        B.fallback_walks(scene, c.problem, cfg, pts, c.seed, rnd, bool(c.gradients))
-        tick("fallback")
 
     for r in range(3):
         step(100 + r)
@@ -63,7 +63,7 @@ for W in (1, 2, 4, 8):
         step(r)
         ts.append(time.perf_counter() - t)
     res[W] = float(np.median(ts))
-    names = ["t0", "walks", "exchange", "gather", "fallback"]
+    names = ["t0", "walks", "exchange", "gather"]
     print("   phases (ms):", {b: round((marks[b] - marks[a]) * 1e3, 3) for a, b in zip(names, names[1:])})
     print(f"W={W}: rank-0 round {res[W] * 1e3:.3f} ms, projected strong-scaling efficiency "
           f"{res[1] / (W * res[W]):.3f}", flush=True)

@@ -74,3 +74,24 @@ def test_overlapped_round_equals_sequential_pieces():
     assert a["fallback"].sum() > 0
     for k in ("boundarySum", "boundaryGradSum", "nBoundary", "walkSum", "walkCount", "gradientWalkSum"):
         np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
+
+def test_shard_with_fallback_equals_separate_calls():
+    """bvc_generate_boundary_cache_shard_fallback (a rank's shard plus its band walks on a
+    second stream) against the shard and bvc_fallback_walks called one after the other."""
+    c, sc, region, x, dim = _setup(2, 1 / 32, 20000)
+    N = c.cache.nBoundary
+    p = B.EvaluationPoints(x, dim)
+    B.mark_evaluation_points(sc, region, c.cache, p)
+    a = B.generate_boundary_cache_with_fallback(sc, c.problem, region, c.cache, c.seed, 5, N // 4, N // 2, p, True)
+    q = B.EvaluationPoints(x, dim)
+    B.mark_evaluation_points(sc, region, c.cache, q)
+    b = B.generate_boundary_cache(sc, c.problem, region, c.cache, c.seed, 5, begin=N // 4, end=N // 2)
+    B.fallback_walks(sc, c.problem, c.cache, q, c.seed, 5, True)
+    ca, cb = a.download(), b.download()
+    np.testing.assert_array_equal(ca["uHat"], cb["uHat"])
+    np.testing.assert_array_equal(ca["dHat"], cb["dHat"])
+    sa, sb = p.download(), q.download()
+    assert sa["fallback"].sum() > 0
+    for k in ("walkSum", "walkCount", "gradientWalkSum", "gradientWalkCount"):
+        np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
