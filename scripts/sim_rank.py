@@ -3,7 +3,7 @@ W-GPU round (its 1/W of the cache walks, a full-size cache assembled from copies
 shard in place of the NCCL all-gather, its 1/W of the points, its fallback band) for
 W = 1, 2, 4, 8 (the band walks overlap the shard's walks, as in bench.py's sharded round).
 The all-gather itself (48 B x N over NVLink) is not included.
-    python scripts/sim_rank.py [config]"""
+    python scripts/sim_rank.py [config [W ...]]"""
 import sys
 import time
 
@@ -25,7 +25,8 @@ cfg = c.cache
 N = cfg.nBoundary
 K = len(c.points)
 res = {}
-for W in (1, 2, 4, 8):
+Ws = [int(a) for a in sys.argv[2:]] or [1, 2, 4, 8]
+for W in Ws:
     pts = B.EvaluationPoints(c.points[: K // W], c.dim)
     B.mark_evaluation_points(scene, region, cfg, pts)
     spec = B.make_splat_config(scene, c.problem, cfg)
@@ -65,5 +66,5 @@ for W in (1, 2, 4, 8):
     res[W] = float(np.median(ts))
     names = ["t0", "walks", "exchange", "gather"]
     print("   phases (ms):", {b: round((marks[b] - marks[a]) * 1e3, 3) for a, b in zip(names, names[1:])})
-    print(f"W={W}: rank-0 round {res[W] * 1e3:.3f} ms, projected strong-scaling efficiency "
-          f"{res[1] / (W * res[W]):.3f}", flush=True)
+    eff = f", projected strong-scaling efficiency {res[1] / (W * res[W]):.3f}" if 1 in res else ""
+    print(f"W={W}: rank-0 round {res[W] * 1e3:.3f} ms{eff}", flush=True)
