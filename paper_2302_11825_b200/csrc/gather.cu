@@ -652,8 +652,11 @@ __device__ __forceinline__ void gather_body(const Params& P) {
     }
 }
 
+// (kThreads, 1): an explicit minimum of one CTA lets ptxas use more registers than the
+// bare bound does; screened 3D values run 2.3% faster with it (C5 4.52 -> 4.42 s), screened
+// 2D the same
 template <int KIND, bool VAL, bool GRAD, int MODE = 0>
-__global__ void __launch_bounds__(kThreads) gather_kernel(const Params P) {
+__global__ void __launch_bounds__(kThreads, 1) gather_kernel(const Params P) {
     gather_body<KIND, VAL, GRAD, MODE>(P);
 }
 // the Laplace kinds at 8 resident CTAs (64 registers): C2 gather -2%, C4 -5%; the
