@@ -659,10 +659,11 @@ template <int KIND, bool VAL, bool GRAD, int MODE = 0>
 __global__ void __launch_bounds__(kThreads, 1) gather_kernel(const Params P) {
     gather_body<KIND, VAL, GRAD, MODE>(P);
 }
-// the Laplace kinds at 8 resident CTAs (64 registers): C2 gather -2%, C4 -5%; the
-// screened kinds spill 272-448 B at 64 registers and keep the compiler's choice (C3 +2%)
+// the Laplace kinds at 8 (2D; 64 registers) / 7 (3D; 72 registers) resident CTAs: measured
+// against 6, 7 and 8 (C2 gather 2.52 / 2.52 / 2.40 ms, C4 228 / 218 / 223 ms); the screened
+// kinds spill 272-448 B at 64 registers and keep the compiler's choice (C3 +2%)
 template <int KIND, bool VAL, bool GRAD>
-__global__ void __launch_bounds__(kThreads, 8) gather_kernel8(const Params P) {
+__global__ void __launch_bounds__(kThreads, KIND == kLap3 ? 7 : 8) gather_kernel8(const Params P) {
     gather_body<KIND, VAL, GRAD, 0>(P);
 }
 
