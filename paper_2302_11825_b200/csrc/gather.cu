@@ -16,6 +16,8 @@
 // and a slow path redoes a tile for a point that hit one.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "gather.h"
 #include "tma.cuh"
 
@@ -914,7 +916,12 @@ GatherPlan plan_gather(int kind, int K, int N, int M, bool val, bool grad) {
     // block scheduler does not always place every slot at once.
     int total = N + M;
     int maxTiles = (total + kTS - 1) / kTS;
-    int ct = maxTiles > 16 ? (maxTiles + 15) / 16 : 1;
+    static const int nChunks = [] {  // BVC_GATHER_CHUNKS: sweep knob (default 16)
+        const char* e = std::getenv("BVC_GATHER_CHUNKS");
+        int v = e ? std::atoi(e) : 16;
+        return v >= 1 && v <= 1024 ? v : 16;
+    }();
+    int ct = maxTiles > nChunks ? (maxTiles + nChunks - 1) / nChunks : 1;
     g.chunk = ct * kTS;
     g.chunksB = (N + g.chunk - 1) / g.chunk;
     g.chunksS = (M + g.chunk - 1) / g.chunk;
