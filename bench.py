@@ -1,19 +1,22 @@
-"""BVC hot-path benchmark (BASELINE.json metric) on BASELINE config 2 by default.
+"""BVC hot-path benchmark (BASELINE.json metric); BASELINE config 5 by default.
 
-A step is one progressive BVC round, updateSolution (cache.cpp:622-684), on
-C2 — the 2D mixed Dirichlet/Neumann square: 16384 boundary samples x (512 u-walks
-+ 512 du/dn walks on the estimated pieces), WoSt walks with eps = 1e-3, then the
-u and grad-u gather at the 512 x 512 grid's non-fallback nodes plus pointwise
-walks at the fallback-band nodes. Inputs are seeded synthetic data of that shape
-(no dataset exists for this path).
+A step is one progressive BVC round, updateSolution (cache.cpp:622-684). The default
+workload is C5 (BASELINE.json configs[4], the largest single-GPU config): the 3D
+screened (sigma = 1) mixed problem on the outer shell of 8 overlapping displaced
+level-6 icospheres — 1,048,576 boundary samples x (128 u-walks + 128 du/dn walks),
+then the u gather at exactly 16,777,216 uniform interior query points. `--config
+1..4` runs the other configs. Inputs are seeded synthetic data of those shapes (no
+dataset exists for this path).
 
 value  = interactions/s = (non-fallback points x cache samples) per round / round time,
          whole job (all ranks). Walk steps/s (closest-Dirichlet queries) are reported
          next to it.
-e2e    = the same metric through the public API with host buffers: each step
+e2e    = the same metric through the public API with host buffers: each call
          uploads the query points (H2D), runs the round and reads u back (D2H).
---impl reference: the reference's own CPU implementation (oracle/_ref, compiled from
-         /root/reference) on a bounded sample of the same round, extrapolated.
+--impl reference: the reference's own CPU implementation on a bounded sample of the
+         same workload (oracle/_ref, compiled from /root/reference's sources; for the
+         3D configs, which the reference cannot run, the threaded port of its splat
+         loop over its own kernel templates).
 
 Multi-GPU (torchrun): cache samples and query points are sharded by rank; the
 packed cache shards are all-gathered with NCCL; each rank gathers its points.
@@ -113,17 +116,22 @@ def build_problem(cfg_id, B, configs, abi):
             # soup of 8 closed meshes: the walks and the cache live on its outer shell;
             # inside the union = inside any component
             tris, labels = configs.soup_shell(c)
-            keep = np.zeros(len(c.points), bool)
-            for comp in configs.soup_components(c):
-                keep |= comp.inside(c.points)
+            comps = configs.soup_components(c)
+
+            def inside(x):
+                keep = np.zeros(len(x), bool)
+                for comp in comps:
+                    keep |= comp.inside(x)
+                return keep
+
             c.extra["shell_triangles"] = int(len(tris))
             c.segments, c.labels = tris, labels
             scene = B.Scene.mesh3(c.vertices, c.segments, c.labels)
         else:
             scene = B.Scene.mesh3(c.vertices, c.segments, c.labels)
-            keep = scene.inside(c.points)
+            inside = scene.inside
         region = B.SolveRegion(scene, offset=c.region_offset, epsilon=c.epsilon)
-        c.points = c.points[keep][: c.extra["n_points"]]
+        c.points = configs.interior_points(c, inside)  # exactly n_points interior points
         c.dim = 3
         return c, scene, region
     c.dim = 2
@@ -137,6 +145,26 @@ def build_problem(cfg_id, B, configs, abi):
         keep = scene.inside(c.points)
     c.points = c.points[keep]
     return c, scene, region
+
+
+def workload_config(c, cfg_id):
+    """The `config` dict both arms print — identical by construction: it describes the
+    workload only (sizes, walk budgets, the query set), no measured counts."""
+    cfg = c.cache
+    M = cfg.nSource if c.problem.f.kind else 0
+    d = {"workload": c.name, "config_index": cfg_id, "boundary_samples": int(cfg.nBoundary), "source_samples": int(M),
+         "walks_u": int(cfg.nWalksNeumann), "walks_dudn": int(cfg.nWalksDirichlet), "epsilon": c.epsilon,
+         "region_offset": cfg.offset, "gradients": bool(c.gradients),
+         "l2": "flushed between timed steps (256 MB write)"}
+    if c.extra.get("n_points"):
+        d["query_points"] = int(c.extra["n_points"])  # exactly this many interior points (configs.interior_points)
+        d["query_set"] = "uniform interior points (bbox rejection, seeded)"
+    else:
+        d["query_set"] = c.extra.get("query_set", "grid")
+    return d
+
+
+METRIC = "BVC eval interactions/s and walk steps/s per GPU; % of FP32/SFU roofline"
 
 
 def run_gpu(args):
@@ -159,14 +187,14 @@ def run_gpu(args):
     cfg = c.cache
     N, M = cfg.nBoundary, (cfg.nSource if c.problem.f.kind else 0)
     K_all = len(c.points)
-    # points of this rank: a contiguous slice (the spatial sort keeps shards compact)
+    # points of this rank: a contiguous slice (the library sorts each rank's points spatially)
     lo_p, hi_p = rank * K_all // world, (rank + 1) * K_all // world
     my_points = c.points[lo_p:hi_p]
-    pts = B.EvaluationPoints(my_points, c.dim)
+    pts = B.EvaluationPoints(my_points, c.dim, index_base=lo_p)
     B.mark_evaluation_points(scene, region, cfg, pts)
     st0 = pts.download()
     k_active = int((~st0["fallback"]).sum())
-    k_fallback = len(my_points) - k_active
+    del st0
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
 
     def round_multi(p, rnd):
@@ -188,7 +216,8 @@ def run_gpu(args):
 
     # BVC_BENCH_SHARDED=1 runs the sharded path (NCCL all-gather) even at N=1, to
     # exercise the multi-GPU plumbing on a single device
-    step = round_multi if (world > 1 or os.environ.get("BVC_BENCH_SHARDED") == "1") else round_single
+    sharded = world > 1 or os.environ.get("BVC_BENCH_SHARDED") == "1"
+    step = round_multi if sharded else round_single
 
     def barrier():
         if dist is not None:
@@ -201,18 +230,17 @@ def run_gpu(args):
     barrier()
     torch.cuda.synchronize()
     launches0 = B.launch_count()
-    times, steps_total, walks_total = [], 0, 0
+    times, per_step = [], []
     clk.mark("start")
     for k in range(args.steps):
-        flush.fill_(float(k))
+        flush.fill_(float(k))  # L2 flush on the library's stream (the legacy default stream)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         st = step(pts, k)
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) / 1e3)
-        steps_total += st.get("cacheSteps", 0)
-        walks_total += st.get("cacheWalks", 0)
+        per_step.append(st)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -220,6 +248,8 @@ def run_gpu(args):
     clk.__exit__(None, None, None)
     launches = B.launch_count() - launches0
     t_step = float(np.mean(times))
+    steps_total = sum(s.get("cacheSteps", 0) for s in per_step)
+    walks_total = sum(s.get("cacheWalks", 0) for s in per_step)
     if dist is not None:
         t = torch.tensor([t_step], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -231,23 +261,31 @@ def run_gpu(args):
         k_active_all = k_active
     pairs = k_active_all * (N + M)
     value = pairs / t_step
-    out = {"metric": "BVC eval interactions/s and walk steps/s per GPU; % of FP32/SFU roofline",
-           "value": value, "unit": "interactions/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak" if False else "strong",
-           "vs_baseline": None, "dtype": "fp32 (fp64 accumulation)", "data": "synthetic (seeded, configs.py)",
+    out = {"metric": METRIC, "value": value, "unit": "interactions/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f32 (f64 accumulation)", "data": "synthetic (seeded, configs.py)",
            "gpu_launches": int(launches / max(args.steps, 1))}
+    out["step_ms"] = {"min": min(times) * 1e3, "median": float(np.median(times)) * 1e3, "max": max(times) * 1e3,
+                      "mean": float(np.mean(times)) * 1e3, "rank": "this rank's steps (rank 0)"}
+    out["resampled_per_step"] = [int(s.get("resampled", 0)) for s in per_step]
     out["walk_steps_per_s"] = steps_total / (t_step * args.steps)
     out["walks_per_s"] = walks_total / (t_step * args.steps)
-    out["config"] = {"workload": c.name, "config_index": args.config, "boundary_samples": N, "source_samples": M,
-                     "walks_u": cfg.nWalksNeumann, "walks_dudn": cfg.nWalksDirichlet, "epsilon": c.epsilon,
-                     "region_offset": cfg.offset, "query_points": int(K_all), "nonfallback_points": int(k_active_all),
-                     "fallback_points": int(K_all - k_active_all), "gradients": bool(c.gradients),
-                     "parallelism": f"dp{world} (samples and points sharded)",
-                     "l2": "flushed between timed steps (256 MB write)"}
+    out["config"] = workload_config(c, args.config)
+    out["counts"] = {"query_points": int(K_all), "nonfallback_points": int(k_active_all),
+                     "fallback_points": int(K_all - k_active_all), "pairs_per_step": pairs,
+                     "parallelism": f"dp{world} (samples and points sharded)" if sharded else "1 GPU"}
+    if "shell_triangles" in c.extra:
+        out["counts"]["shell_triangles"] = c.extra["shell_triangles"]
     out["clocks"] = clk.summary()
     if rank == 0:
-        out.update(phase_breakdown(B, c, scene, region, pts, args))
-        out["e2e"] = e2e_measure(B, c, scene, region, my_points, args, world)
+        # phase times measured live inside the timed steps: the round's own CUDA events on
+        # the library stream (RoundStats generateSeconds / splatSeconds)
+        live = None
+        if not sharded:
+            live = {"cache_generation": float(np.mean([s["generateSeconds"] for s in per_step])),
+                    "gather": float(np.mean([s["splatSeconds"] for s in per_step]))}
+        out.update(phase_breakdown(B, c, scene, region, pts, args, per_step[-1], live, k_active))
+        out["e2e"] = e2e_measure(B, c, scene, region, my_points, args, world, t_step)
         if world == 1 and not args.no_cpu:
             out["cpu_baseline"] = cpu_baseline(c, args.cpu_sample_s)
         print(json.dumps(out), flush=True)
@@ -255,12 +293,13 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
-def ncu_traffic(kernel="walk"):
-    """DRAM bytes (read + write) per launch from the latest committed ncu --set full
-    summary (profiles/<round>_<kernel>_ncu.txt), or None."""
+def ncu_traffic(kernel, cfg_id):
+    """DRAM bytes (read + write) per launch of `kernel` ("walk" / "gather") on config
+    cfg_id, from the latest committed ncu --set full summary
+    (profiles/<round>_<kernel>_c<cfg>_ncu.txt), or None."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_{kernel}_ncu.txt")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_{kernel}_c{cfg_id}_ncu.txt")))
     if not files:
         return None
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -270,57 +309,80 @@ def ncu_traffic(kernel="walk"):
             if line.startswith(key):
                 parts = line.split("=")[1].split()
                 total += float(parts[0]) * scale.get(parts[1] if len(parts) > 1 else "byte", 1.0)
-    return {"bytes": total, "source": os.path.relpath(files[-1], ROOT)}
+    scale_note = None
+    for line in open(files[-1]):
+        if line.startswith("# scale "):  # profiled at a reduced size: bytes per launch scaled to the bench's
+            scale_note = line[2:].strip()
+            total *= float(line.split()[2])
+    return {"bytes": total, "source": os.path.relpath(files[-1], ROOT), "scaled": scale_note}
 
 
-def phase_breakdown(B, c, scene, region, pts, args):
-    """Per-kernel timings with CUDA events (outside the timed steps) and the roofline."""
+# per-pair FP32-pipe instructions F and SFU ops S
+PER_PAIR = {"lap2_u": (9, 2), "lap2_ugrad": (18, 2), "scr2_ugrad": (50, 3), "lap3_u": (14, 1), "scr3_u": (20, 2)}
+
+
+def phase_breakdown(B, c, scene, region, pts, args, stats, live, k_active):
+    """Rooflines of the round's two kernels. Phase times come from the timed steps
+    themselves (`live`: the round's device events); without them (sharded rounds) one
+    extra round-equivalent is timed here with CUDA events."""
     import torch
 
     cfg = c.cache
     N, M = cfg.nBoundary, (cfg.nSource if c.problem.f.kind else 0)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    ev[0].record()
-    stats = {}
-    cache = B.generate_boundary_cache(scene, c.problem, region, cfg, c.seed, 77, stats=stats)
-    ev[1].record()
-    scache = B.generate_source_cache(c.problem, region, cfg, c.seed, 77) if M else None
-    spec = B.make_splat_config(scene, c.problem, cfg)
-    B.splat_range(cache, scache, pts, spec, 0, 1 << 62, True, bool(c.gradients))  # warm the sort/order
-    torch.cuda.synchronize()
-    reps = 5
-    ev[2].record()
-    for _ in range(reps):
-        B.splat_range(cache, scache, pts, spec, 0, 1 << 62, True, bool(c.gradients))
-    ev[3].record()
-    torch.cuda.synchronize()
-    t_gen = ev[0].elapsed_time(ev[1]) / 1e3
-    t_gather = ev[2].elapsed_time(ev[3]) / 1e3 / reps
-    st = pts.download()
-    k_active = int((~st["fallback"]).sum())
     pairs = k_active * (N + M)
+    extra = {}
+    if live is None or args.config == 1:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        st = {}
+        cache = B.generate_boundary_cache(scene, c.problem, region, cfg, c.seed, 77, stats=st)
+        ev[1].record()
+        scache = B.generate_source_cache(c.problem, region, cfg, c.seed, 77) if M else None
+        spec = B.make_splat_config(scene, c.problem, cfg)
+        ev[2].record()
+        B.splat_range(cache, scache, pts, spec, 0, 1 << 62, True, bool(c.gradients))
+        ev[3].record()
+        torch.cuda.synchronize()
+        if live is None:
+            live = {"cache_generation": ev[0].elapsed_time(ev[1]) / 1e3, "gather": ev[2].elapsed_time(ev[3]) / 1e3}
+            stats = st
+        if args.config == 1:  # BASELINE C1 also asks for fp64: the FP64 gather on the same cache
+            spec64 = B.make_splat_config(scene, c.problem, cfg)
+            spec64.fp64 = 1
+            B.splat_range(cache, scache, pts, spec64, 0, 1 << 62, True, bool(c.gradients))
+            torch.cuda.synchronize()
+            reps = 5
+            ev[2].record()
+            for _ in range(reps):
+                B.splat_range(cache, scache, pts, spec64, 0, 1 << 62, True, bool(c.gradients))
+            ev[3].record()
+            torch.cuda.synchronize()
+            t64 = ev[2].elapsed_time(ev[3]) / 1e3 / reps
+            extra["gather_fp64"] = {"ms": t64 * 1e3, "pairs_per_s": pairs / t64,
+                                    "note": "every pair in FP64 (rcp/rsqrt: FP32 seed + 2 Newton steps, libdevice "
+                                            "log); parity with the reference's double loop <= 1e-12 (tests)"}
+    t_gen, t_gather = live["cache_generation"], live["gather"]
     peaks = load_peaks()
-    # walk traffic: algorithmic bytes per step from a counting launch
+    # walk traffic: SURVEY §8(d) algorithmic bytes per step (packed fp32 node 32 B, 2D segment
+    # 16 + 4 B, 3D triangle 36 + 4 B, walk state 32 B) x the fetch counts of a counting launch
     prof = B.walk_traffic_profile(scene, c.problem, region, cfg, c.seed, 77)
     steps = max(prof["steps"], 1.0)
-    node_b, prim_b = (64, 48) if c.dim == 3 else (48, 32)  # Node3 / Prim3 vs Node2 / Prim2
+    node_b, prim_b = 32, (40 if c.dim == 3 else 20)
     bytes_per_step = (prof["node_fetches"] * node_b + prof["prim_fetches"] * prim_b) / steps + 32.0
     walk_bytes = bytes_per_step * stats["cacheSteps"]
-    achieved = walk_bytes / t_gen / 1e9
-    # gather bound: 148 SMs * f_SM / max(F/128, S/16) pairs/s (SURVEY §8d, V2 = 18 F, 2 S)
+    walk_achieved = walk_bytes / t_gen / 1e9
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    # gather bound: SMs * f_SM / max(F/128, S/16) pairs/s (SURVEY §8d)
     props = torch.cuda.get_device_properties(0)
     sms = props.multi_processor_count
     f_sm = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    per_pair = {"lap2_u": (9, 2), "lap2_ugrad": (18, 2), "scr2_ugrad": (50, 3), "lap3_u": (14, 1), "scr3_u": (20, 2)}
     if c.dim == 3:
         key = "scr3_u" if c.problem.kernel.kind else "lap3_u"
     else:
         key = ("scr2_ugrad" if c.problem.kernel.kind else "lap2_ugrad") if c.gradients else "lap2_u"
-    F, S = per_pair[key]
+    F, S = PER_PAIR[key]
     bound = sms * f_sm / max(F / 128.0, S / 16.0)
     gather_rate = pairs / t_gather
-    dominant = "walk" if t_gen >= t_gather else "gather"
-    # measured pipe rates and L2 bandwidth (bvc_pipe_probe) next to the canonical bound
     if args.no_probe:  # profiling runs: reuse the committed measurement
         pipes = json.load(open(os.path.join(ROOT, "profiles", "r1_pipe_peaks.json")))["rates"]
         pipes = {k: v["per_s"] for k, v in pipes.items()}
@@ -328,21 +390,31 @@ def phase_breakdown(B, c, scene, region, pts, args):
         pipes = B.pipe_probe()
     mufu = min(pipes["mufu_lg2"], pipes["mufu_rcp"]) if c.dim == 2 else pipes["mufu_rsq"]
     bound_meas = min(pipes["ffma"] / F, mufu / S)
-    extra = {}
-    if args.config == 1:  # BASELINE C1 also asks for fp64: the FP64 gather on the same cache
-        spec64 = B.make_splat_config(scene, c.problem, cfg)
-        spec64.fp64 = 1
-        B.splat_range(cache, scache, pts, spec64, 0, 1 << 62, True, bool(c.gradients))
-        torch.cuda.synchronize()
-        ev[2].record()
-        for _ in range(reps):
-            B.splat_range(cache, scache, pts, spec64, 0, 1 << 62, True, bool(c.gradients))
-        ev[3].record()
-        torch.cuda.synchronize()
-        t64 = ev[2].elapsed_time(ev[3]) / 1e3 / reps
-        extra["gather_fp64"] = {"ms": t64 * 1e3, "pairs_per_s": pairs / t64, "dfma_per_s": pipes["dfma"],
-                                "note": "every pair in FP64 (rcp/rsqrt: FP32 seed + 2 Newton steps, libdevice log); "
-                                        "parity with the reference's double loop <= 1e-12 (tests)"}
+    gtraffic = ncu_traffic("gather", args.config) or {}
+    wtraffic = ncu_traffic("walk", args.config) or {}
+    walk_roof = {"bound": "hbm", "kernel": "bvc walk_kernel (cache generation)", "achieved": walk_achieved,
+                 "peak": hbm, "unit": "GB/s", "frac": walk_achieved / hbm, "traffic": wtraffic.get("bytes"),
+                 "traffic_source": wtraffic.get("source"), "algorithmic_bytes_per_launch": walk_bytes,
+                 "algorithmic_bytes_per_step": bytes_per_step,
+                 "node_fetches_per_step": prof["node_fetches"] / steps,
+                 "prim_fetches_per_step": prof["prim_fetches"] / steps, "peak_source": peaks["source"],
+                 "l2_read_peak_gbs": pipes["l2_read_bytes"] / 1e9,
+                 "frac_of_l2_read_peak": walk_achieved / (pipes["l2_read_bytes"] / 1e9),
+                 "note": ("SURVEY §8(d) bytes: node 32 B, primitive 20 B (2D) / 40 B (3D), 32 B walk state per step; "
+                          "the scene is L1/L2-resident, the kernel is latency/divergence-bound (see profiles/)")}
+    gather_roof = {"bound": "fp32+sfu", "kernel": f"bvc gather_kernel ({key})", "achieved": gather_rate,
+                   "peak": bound, "unit": "pairs/s", "frac": gather_rate / bound,
+                   "peak_formula": f"{sms} SMs x {f_sm / 1e6:.0f} MHz / max({F}/128, {S}/16)",
+                   "peak_measured_pipes": bound_meas, "frac_measured_pipes": gather_rate / bound_meas,
+                   "pairs_per_launch": pairs, "traffic": gtraffic.get("bytes"),
+                   "traffic_source": gtraffic.get("source"),
+                   "algorithmic_bytes_per_launch": (k_active * (12 if c.dim == 3 else 8) + (N + M) * 32),
+                   "note": "compute-bound N-body gather: no tensor-core or HBM roofline applies (SURVEY §8d)"}
+    dominant = "walk" if t_gen >= t_gather else "gather"
+    roof = dict(walk_roof if dominant == "walk" else gather_roof)
+    roof["dominant"] = dominant
+    roof["timing"] = ("live: mean of the round's device events over the timed steps" if args.config != 1 or live
+                      else "one extra round")
     return {
         **extra,
         "pipe_peaks": {k: v for k, v in pipes.items()},
@@ -350,36 +422,18 @@ def phase_breakdown(B, c, scene, region, pts, args):
                        "truncated_fraction": stats["cacheTruncated"] / max(stats["cacheWalks"], 1),
                        "walks": stats["cacheWalks"]},
         "phases_s": {"cache_generation": t_gen, "gather": t_gather},
-        "roofline": {"bound": "hbm", "kernel": "bvc walk_kernel (cache generation)", "achieved": achieved,
-                     "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s",
-                     "frac": achieved / float(peaks.get("hbm_gbs", 6650.0)),
-                     "traffic": (ncu_traffic("walk") or {}).get("bytes"),
-                     "traffic_source": (ncu_traffic("walk") or {}).get("source"),
-                     "algorithmic_bytes_per_launch": walk_bytes,
-                     "note": ("algorithmic bytes = BVH node (48 B) + primitive (32 B) fetches + 32 B walk state per "
-                              "step (SURVEY §8d); the scene is L1/L2-resident (ncu: DRAM traffic per launch is the "
-                              "`traffic` field), so the fraction of the HBM copy peak can exceed 1 — the kernel is "
-                              "issue/latency-bound, see profiles/"),
-                     "algorithmic_bytes_per_step": bytes_per_step,
-                     "node_fetches_per_step": prof["node_fetches"] / steps,
-                     "prim_fetches_per_step": prof["prim_fetches"] / steps, "peak_source": peaks["source"],
-                     "l2_read_peak_gbs": pipes["l2_read_bytes"] / 1e9,
-                     "frac_of_l2_read_peak": achieved / (pipes["l2_read_bytes"] / 1e9),
-                     "dominant": dominant},
-        "gather_roofline": {"bound": "fp32+sfu", "kernel": f"bvc gather_kernel ({key})", "achieved": gather_rate,
-                            "peak": bound, "unit": "pairs/s", "frac": gather_rate / bound,
-                            "peak_formula": f"{sms} SMs x {f_sm / 1e6:.0f} MHz / max({F}/128, {S}/16)",
-                            "peak_measured_pipes": bound_meas, "frac_measured_pipes": gather_rate / bound_meas,
-                            "pairs_per_launch": pairs},
+        "roofline": roof,
+        "walk_roofline": walk_roof,
+        "gather_roofline": gather_roof,
     }
 
 
-def e2e_measure(B, c, scene, region, points, args, world):
+def e2e_measure(B, c, scene, region, points, args, world, t_step):
     """Public API with host buffers: H2D points, one round, D2H of u (and grad u)."""
     import torch
 
     times = []
-    reps = max(2, min(args.steps, 5))
+    reps = max(2, min(args.steps, 5)) if t_step < 1.0 else 2
     # pinned host buffers for the step's input points and its u / grad u results
     src = torch.from_numpy(np.ascontiguousarray(points, dtype=np.float64)).pin_memory().numpy()
     u_out = torch.empty(len(points), dtype=torch.float64).pin_memory().numpy()
@@ -402,20 +456,28 @@ def e2e_measure(B, c, scene, region, points, args, world):
     B.mark_evaluation_points(scene, region, c.cache, pts)
     k_active = int((~pts.download()["fallback"]).sum())
     t = float(np.mean(times))
-    d2h = len(points) * 8 * (1 + (2 if c.gradients else 0))
+    d2h = len(points) * 8 * (1 + (c.dim if c.gradients else 0))
     return {"value": k_active * world * (N + M) / t, "unit": "interactions/s", "ms_per_step": t * 1e3,
+            "ms_min": min(times) * 1e3, "ms_max": max(times) * 1e3, "calls": len(times),
             "h2d_bytes_per_step": int(points.size * 8), "d2h_bytes_per_step": int(d2h),
             "note": "wall clock per bvc_update_solution_host call from pinned host buffers: point upload (H2D) and "
-                    "classification (overlapping the cache walks on a second stream), one round, u/grad-u readout (D2H)"}
+                    "classification (overlapping the cache walks on a second stream), one round, u/grad-u readout "
+                    "(D2H); no L2 flush between calls"}
+
+
+_ACTIVE = {}  # the reference's non-fallback query points per config object (computed once)
 
 
 def reference_round_estimate(c, sample_s=20.0, threads=0):
     """Time the reference's own updateSolution pieces (oracle/_ref) on a bounded sample of
-    the round and extrapolate: generateBoundaryCache on n_sub samples (cost ~ #walks) and
-    splatSolution+splatGradient on k_sub points against the full cache (cost ~ K (N+M))."""
+    the round: generateBoundaryCache on n_sub samples (cost ~ #walks) and
+    splatSolution(+splatGradient) on k_sub points against a full-size cache (cost ~ K (N+M)).
+    The rate is the full round's pairs over the round time extrapolated from the sample;
+    `seconds` is the sample's measured wall time."""
     from oracle import oracle as O
     from paper_2302_11825_b200 import abi
 
+    t_all = time.perf_counter()
     O.ref_lib()
     rs = O.RefScene(c.vertices, c.segments, c.labels)
     if c.region_mode == abi.REGION_SUBDOMAIN:
@@ -447,8 +509,18 @@ def reference_round_estimate(c, sample_s=20.0, threads=0):
     scache = None
     if M:
         scache = O.ref_generate_source_cache(c.problem, rr, cfg, c.seed, 0)
-    fb, _ = O.ref_mark_points(rs, rr, cfg, c.points)
-    act = c.points[~fb]
+    # the query set: the config's points inside the scene (the reference's own inside test),
+    # then markEvaluationPoints' fallback split
+    act = _ACTIVE.get(id(c))
+    if act is None:
+        pts = c.points
+        if c.region_mode == abi.REGION_SUBDOMAIN:
+            sub = O.RefScene(c.sub_vertices, c.sub_segments, np.zeros(len(c.sub_segments), np.int32))
+            pts = pts[sub.inside(pts)]
+        else:
+            pts = pts[rs.inside(pts)]
+        fb, _ = O.ref_mark_points(rs, rr, cfg, pts)
+        act = _ACTIVE[id(c)] = pts[~fb]
     k_sub = 64
     while True:
         xs = act[rng.choice(len(act), size=min(k_sub, len(act)), replace=False)]
@@ -463,40 +535,52 @@ def reference_round_estimate(c, sample_s=20.0, threads=0):
     t_round = gen_full + splat_full
     pairs = len(act) * (N + M)
     return {"value": pairs / t_round, "unit": "interactions/s", "cores": int(cores), "kind": "reference",
-            "cpu": cpu_model(), "host_threads": os.cpu_count(),
-            "sample": (f"generateBoundaryCache on {n_sub}/{N} samples ({t_gen:.1f} s) + splatSolution"
-                       f"{'+splatGradient' if c.gradients else ''} on {len(xs)}/{len(act)} points vs the full "
-                       f"{N}+{M}-sample cache ({t_spl:.1f} s); extrapolated linearly (cost ~ walks, ~ K(N+M))"),
+            "cpu": cpu_model(), "host_threads": os.cpu_count(), "seconds": time.perf_counter() - t_all,
+            "sample": (f"the reference's generateBoundaryCache on {n_sub}/{N} samples ({t_gen:.2f} s) + splatSolution"
+                       f"{'+splatGradient' if c.gradients else ''} on {len(xs)}/{len(act)} points vs a full "
+                       f"{N}+{M}-sample cache ({t_spl:.2f} s); rate = full-round pairs / round time extrapolated "
+                       "linearly from the sample (cost ~ walks, ~ K(N+M))"),
             "round_seconds_extrapolated": t_round}
 
 
-def port_gather_estimate_3d(c, sample_s):
-    """3D has no reference path (pointwise.cpp:23 throws for dim != 2). The CPU number is
-    the restated 3D splat loop (oracle/bvc_oracle.c, the reference's 3D kernel templates
-    kernels.h:78-129) on a point subset against a full-size synthetic cache; walks have
-    no CPU counterpart and are not included."""
+def port_gather_3d(c, sample_s, threads=0):
+    """3D has no reference path (pointwise.cpp:23: the solver is 2D-only), so there are no
+    CPU walks to time. The CPU number is splatSolution's loop (cache.cpp:426-461) over
+    Vector3 calling the reference's own kernel templates (kernels.h:78-129), threaded with
+    its parallelFor (oracle/ref_driver.cpp ref_splat3), on k points against a full-size
+    N-sample cache (the per-pair cost does not depend on the values). Gather only."""
     from oracle import oracle as O
     from paper_2302_11825_b200 import abi
 
+    t_all = time.perf_counter()
     N = c.cache.nBoundary
-    rng = np.random.default_rng(0)
-    z = c.vertices[rng.integers(0, len(c.vertices), N)]
-    n = z / np.linalg.norm(z, axis=1)[:, None]
-    cache = dict(z=z, n=n, pdf=np.full(N, 0.1), uHat=rng.uniform(-1, 1, N), dHat=rng.uniform(-1, 1, N),
-                 weight=np.zeros(N))
-    spec = abi.KernelSpec(c.problem.kernel.kind, c.problem.kernel.sigma, 3, 4.0)
-    k = 4
+    cache = _ACTIVE.get(("cache3", id(c)))
+    if cache is None:
+        rng = np.random.default_rng(0)
+        z = c.vertices[rng.integers(0, len(c.vertices), N)]
+        n = rng.normal(size=(N, 3))
+        n /= np.linalg.norm(n, axis=1)[:, None]
+        cache = _ACTIVE[("cache3", id(c))] = dict(z=z, n=n, pdf=np.full(N, 0.1), uHat=rng.uniform(-1, 1, N),
+                                                   dHat=rng.uniform(-1, 1, N))
+    diag = float(np.linalg.norm(c.vertices.max(0) - c.vertices.min(0)))
+    spec = abi.KernelSpec(c.problem.kernel.kind, c.problem.kernel.sigma, 3, diag)
+    cores = O.ref_lib().ref_thread_count(threads)
+    # size the sample once per (config, budget); later steps time that size directly
+    k, fixed = _ACTIVE.get(("k3", id(c), sample_s), 4 * cores), ("k3", id(c), sample_s) in _ACTIVE
     while True:
         xs = c.points[:k]
-        t0 = time.perf_counter()
-        O.oracle_splat(spec, 4e-12, cache, None, xs, value=True)
-        t = time.perf_counter() - t0
-        if t > 0.5 * sample_s or k >= len(c.points):
+        st = O.ref_splat3(spec, 1e-12 * diag, cache, xs, threads=threads)
+        t = st["seconds"]
+        if fixed or t > 0.5 * sample_s or k >= len(c.points):
             break
         k = min(len(c.points), int(k * max(2.0, 0.5 * sample_s / max(t, 1e-3) * 0.8)))
-    return {"value": k * N / t, "unit": "interactions/s", "cores": 1, "kind": "port", "cpu": cpu_model(),
-            "sample": f"restated 3D splat (1 thread) on {k} points x {N} samples ({t:.1f} s); gather only — "
-                      "the reference has no 3D walk or splat path"}
+    _ACTIVE[("k3", id(c), sample_s)] = k
+    return {"value": k * N / t, "unit": "interactions/s", "cores": int(cores), "kind": "port", "cpu": cpu_model(),
+            "host_threads": os.cpu_count(), "seconds": time.perf_counter() - t_all,
+            "sample": (f"splatSolution's loop (cache.cpp:426-461) over Vector3 with the reference's kernel templates "
+                       f"(kernels.h:78-129) and parallelFor, {cores} threads, on {k} points x {N} samples "
+                       f"({t:.2f} s); gather only: the reference has no 3D walk path (pointwise.cpp:23), so the "
+                       "CPU round's walk time is not counted (the GPU value includes its walks)")}
 
 
 def cpu_model():
@@ -511,40 +595,54 @@ def cpu_model():
     return "unknown"
 
 
+def cpu_estimate(c, sample_s, threads=0):
+    if c.extra.get("dim") == 3:
+        return port_gather_3d(c, sample_s, threads)
+    return reference_round_estimate(c, sample_s, threads)
+
+
 def cpu_baseline(c, sample_s):
     try:
-        if getattr(c, "dim", 2) == 3:
-            return port_gather_estimate_3d(c, sample_s)
-        return reference_round_estimate(c, sample_s)
+        return cpu_estimate(c, sample_s)
     except Exception as e:  # oracle/_ref missing on this host
-        return {"value": None, "unit": "interactions/s", "cores": os.cpu_count(), "kind": "reference",
-                "sample": f"unavailable: {e}"}
+        return {"value": None, "unit": "interactions/s", "cores": os.cpu_count(),
+                "kind": "port" if c.extra.get("dim") == 3 else "reference", "sample": f"unavailable: {e}"}
 
 
 def run_reference(args):
+    """The reference arm: the reference's own CPU implementation of the path (oracle/_ref,
+    compiled from /root/reference's sources; for the 3D configs the threaded port of its
+    splat loop over its kernel templates), all host threads, rank 0 only. Each step is a
+    bounded sample of the same workload, timed; `ms_per_step` is that measured sample's
+    wall time, `value` the rate it implies for the full round."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2302_11825_b200 import abi, configs  # noqa: F401 (structs only; no GPU use)
+    from paper_2302_11825_b200 import configs
 
     c = configs.CONFIGS[args.config]()
-    vals = []
+    budget = min(args.cpu_sample_s, 150.0 / max(args.steps + args.warmup, 1))
+    vals, secs = [], []
     t0 = time.perf_counter()
     for k in range(args.warmup + args.steps):
-        est = reference_round_estimate(c, args.cpu_sample_s / max(args.steps + args.warmup, 1) * 2, threads=0)
+        est = cpu_estimate(c, budget)
         if k >= args.warmup:
             vals.append(est)
+            secs.append(est["seconds"])
     value = float(np.mean([v["value"] for v in vals]))
-    out = {"metric": "BVC eval interactions/s and walk steps/s per GPU; % of FP32/SFU roofline", "value": value,
-           "unit": "interactions/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": float(np.mean([v["round_seconds_extrapolated"] for v in vals])) * 1e3,
+    kind = vals[-1]["kind"]
+    out = {"metric": METRIC, "value": value, "unit": "interactions/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(secs)) * 1e3,
+           "ms_per_step_note": "measured wall time of one bounded-sample step (not an extrapolated round)",
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded, configs.py)", "impl": "reference",
-           "config": {"workload": c.name, "config_index": args.config},
+           "config": workload_config(c, args.config),
            "cpu_baseline": {"value": value, "unit": "interactions/s", "cores": vals[-1]["cores"],
-                            "cpu": vals[-1]["cpu"], "kind": "reference", "sample": vals[-1]["sample"]},
+                            "cpu": vals[-1]["cpu"], "kind": kind, "sample": vals[-1]["sample"]},
            "e2e": {"value": value, "unit": "interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "wall_s": time.perf_counter() - t0}
+    if "round_seconds_extrapolated" in vals[-1]:
+        out["round_seconds_extrapolated"] = float(np.mean([v["round_seconds_extrapolated"] for v in vals]))
     print(json.dumps(out), flush=True)
 
 
@@ -554,7 +652,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-probe", action="store_true", help="skip the pipe microbenchmarks (profiling runs)")

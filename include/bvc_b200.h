@@ -248,6 +248,11 @@ int bvc_points_upload(bvc_eval_points pts, const bvc_point_state* host); /* non-
    u: count doubles, grad: dim*count doubles (either may be NULL) */
 int bvc_points_solution(bvc_eval_points pts, double* u, double* grad);
 int bvc_points_reset(bvc_eval_points pts);  /* zero all running sums */
+/* the global index of this point set's first point when it is one shard of a larger
+   set (default 0). Per-point random streams (fallback-band walks, clamp corrections)
+   are keyed by base + index, so sharded point sets draw exactly what the whole set
+   would draw on one device (the reference keys them by point: cache.cpp:665-681) */
+int bvc_points_set_index_base(bvc_eval_points pts, long long base);
 /* markEvaluationPoints (cache.h:154; cache.cpp:263-276) */
 int bvc_mark_evaluation_points(bvc_scene scene, bvc_region region, const bvc_cache_config* cfg,
                                bvc_eval_points pts);

@@ -173,6 +173,8 @@ def ref_lib():
                                           C.POINTER(abi.CacheConfig), _dp, C.c_size_t, C.c_uint64,
                                           C.c_uint64, C.c_int, _dp, C.c_void_p, _u8p, _i64p, _dp]
         L.ref_thread_count.argtypes = [C.c_int]
+        L.ref_splat3.argtypes = [C.POINTER(abi.KernelSpec), C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp,
+                                 C.c_size_t, _dp, C.c_int, _dp, _i64p, _i64p, C.POINTER(C.c_double)]
         _ref = L
     return _ref
 
@@ -492,6 +494,20 @@ def ref_splat(spec, tol, bcache, scache, x, fallback=None, value=True, gradient=
                                    st["skipped"], C.byref(sec)))
     st["seconds"] = sec.value
     return st
+
+
+def ref_splat3(spec, tol, bcache, x, threads=0):
+    """cache.cpp:426-461's loop with Vector3 over the reference's own kernel templates
+    (kernels.h:78-129), threaded by its parallelFor: the CPU counterpart of the 3D gather."""
+    x = _f64(x).reshape(-1, 3)
+    K = len(x)
+    N = len(bcache["pdf"])
+    bsum, nb, sk = np.zeros(K), np.zeros(K, np.int64), np.zeros(K, np.int64)
+    sec = C.c_double()
+    _check_ref(ref_lib().ref_splat3(C.byref(spec), tol, N, _f64(bcache["z"]).ravel(), _f64(bcache["n"]).ravel(),
+                                    _f64(bcache["pdf"]), _f64(bcache["uHat"]), _f64(bcache["dHat"]), K, x.ravel(),
+                                    threads, bsum, nb, sk, C.byref(sec)))
+    return {"boundarySum": bsum, "nBoundary": nb, "skipped": sk, "seconds": sec.value}
 
 
 def _clamped_args(bcache, scache, x, ball_radius):

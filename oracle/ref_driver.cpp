@@ -398,6 +398,45 @@ int ref_splat(const bvc_kernel_spec* spec, double tol, int voronoi, int N, const
     });
 }
 
+// The 3D splatSolution loop. The reference's solver is 2D-only (pointwise.cpp:23), but its
+// kernel templates (kernels.h:78-129) compile for Vector3; this is cache.cpp:426-461 with
+// Vector3 points and samples, calling those templates unchanged, parallelised with the
+// reference's own parallelFor (parallel.h:25-50). Plain 1/pdf weights (no Voronoi), no
+// ball mode. This is the CPU counterpart of the C4/C5 gather (a "port" of the loop, not
+// reference code); sums accumulate like EvaluationPoint's.
+int ref_splat3(const bvc_kernel_spec* spec, double tol, int N, const double* bz, const double* bn,
+               const double* bpdf, const double* bu, const double* bd, size_t K, const double* px,
+               int threads, double* bsum, long long* nb, long long* skipped, double* seconds) {
+    GUARD({
+        struct S3 { Vector3 z, n; double pdf, u, d; };
+        std::vector<S3> cache(N);
+        for (int i = 0; i < N; ++i)
+            cache[i] = {Vector3(bz[3 * i], bz[3 * i + 1], bz[3 * i + 2]),
+                        Vector3(bn[3 * i], bn[3 * i + 1], bn[3 * i + 2]), bpdf[i], bu[i], bd[i]};
+        KernelSpec k = toSpec(*spec);
+        auto t0 = std::chrono::steady_clock::now();
+        parallelFor(K, resolveThreadCount(threads), [&](size_t pi) {
+            Vector3 x(px[3 * pi], px[3 * pi + 1], px[3 * pi + 2]);
+            double sum = 0.0;
+            long n = 0, skip = 0;
+            for (const auto& s : cache) {
+                double r = (x - s.z).norm();
+                if (r < tol) {
+                    ++skip;
+                    continue;
+                }
+                double val = poissonKernelFree(k, x, s.z, s.n) * s.u - greensFree(k, x, s.z) * s.d;
+                sum += val / s.pdf;
+                ++n;
+            }
+            bsum[pi] += sum;
+            nb[pi] += n;
+            skipped[pi] += skip;
+        });
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
 // correctedBoundarySplat (ClampOnly) / correctedSourceSplat without the sampled
 // terms (empty evaluator / f), or splatSolution, per the mode bits of or_clamped_splat
 int ref_clamped_splat(const bvc_kernel_spec* spec, double tol, int voronoi, int N, const double* bz,

@@ -36,7 +36,8 @@ SYMBOLS = (
     "bvc_walk_traffic_profile bvc_eval_kernels bvc_eval_bessel bvc_corrected_boundary_splat "
     "bvc_corrected_source_splat bvc_trace_streamlines bvc_grid_save_csv bvc_grid_load_csv bvc_grid_rmse "
     "bvc_grid_save_pgm bvc_streamlines_write_csv bvc_pipe_probe bvc_boundary_cache_assign_voronoi "
-    "bvc_fallback_walks bvc_update_solution_host bvc_generate_boundary_cache_shard_fallback"
+    "bvc_fallback_walks bvc_update_solution_host bvc_generate_boundary_cache_shard_fallback "
+    "bvc_points_set_index_base"
 ).split()
 
 
@@ -300,11 +301,13 @@ class SolveRegion:
 class EvaluationPoints:
     """Device-resident std::vector<EvaluationPoint> (cache.h:73-110)."""
 
-    def __init__(self, x, dim=2):
+    def __init__(self, x, dim=2, index_base=0):
         x = _f64(x, dim)
         self.n, self.dim = len(x), dim
         self.h = C.c_void_p()
         _check(lib().bvc_points_create(_ptr(x), C.c_size_t(self.n), dim, C.byref(self.h)))
+        if index_base:  # this set is a shard of a larger one: per-point streams use global indices
+            _check(lib().bvc_points_set_index_base(self.h, C.c_longlong(index_base)))
 
     def __del__(self):
         if getattr(self, "h", None):

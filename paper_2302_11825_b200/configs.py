@@ -196,7 +196,7 @@ def config4(scale: float = 1.0, n_points: int = 2097152) -> Config:
     g = abi.make_field(abi.FIELD_QUADRATIC3, [0, 0, 0, 0, -0.5, -0.5, 1.0, 1.0, 0.0, 0.0])
     N = max(1, int(262144 * scale))
     lo, hi = V.min(0), V.max(0)
-    pts = rng.uniform(lo, hi, (int(n_points * 2.8), 3))  # filtered to the interior by Scene.inside
+    pts = rng.uniform(lo, hi, (int(n_points * 2.8), 3))  # a first batch; interior_points() tops it up
     exact = lambda x: x[:, 0] * x[:, 1] + x[:, 2] ** 2 - 0.5 * (x[:, 0] ** 2 + x[:, 1] ** 2)  # noqa: E731
     return Config("C4 3D Laplace displaced icosphere", V, F, np.zeros(len(F), np.int32),
                   _problem(abi.KernelSpec(abi.KERNEL_POISSON, 0.0, 3, 1.0), g=g),
@@ -224,11 +224,34 @@ def config5(scale: float = 1.0, n_points: int = 16777216) -> Config:
     g = abi.make_field(abi.FIELD_TRIG3, [1.0, 1.0, 1.0, 2.0, 1.0, 0.0])
     N = max(1, int(1048576 * scale))
     lo, hi = V.min(0), V.max(0)
-    pts = rng.uniform(lo, hi, (int(n_points * 1.5), 3))
+    pts = rng.uniform(lo, hi, (int(n_points * 1.5), 3))  # a first batch; interior_points() tops it up
     return Config("C5 3D screened soup (sigma=1, mixed)", V, F, labels,
                   _problem(abi.KernelSpec(abi.KERNEL_SCREENED, 1.0, 3, 1.0), g=g),
                   _cache(1e-3, N, 128, 128, nWalks=128), pts, 1e-3, seed=MASTER_SEED + 5,
                   extra=dict(dim=3, n_points=n_points, components=comps))
+
+
+def interior_points(c: Config, inside) -> np.ndarray:
+    """Exactly c.extra["n_points"] uniform interior points of a 3D config.
+
+    The config's first bbox batch (c.points) is filtered by `inside` (a boolean
+    mask function, the device inside test); while fewer than n_points survive,
+    further bbox batches are drawn from a second seeded stream (seed + 1) sized by
+    the acceptance rate seen so far. The union of C5's spheres fills only about a
+    third of its box, so a fixed oversampling factor cannot guarantee the count."""
+    n = int(c.extra["n_points"])
+    lo, hi = c.vertices.min(0), c.vertices.max(0)
+    kept = [c.points[inside(c.points)]]
+    drawn, total = len(c.points), len(kept[0])
+    rng = np.random.default_rng(c.seed + 1)
+    while total < n:
+        rate = max(total / max(drawn, 1), 0.05)
+        batch = int(1.1 * (n - total) / rate) + 1024
+        b = rng.uniform(lo, hi, (batch, 3))
+        k = b[inside(b)]
+        kept.append(k)
+        drawn, total = drawn + batch, total + len(k)
+    return np.ascontiguousarray(np.concatenate(kept)[:n])
 
 
 def soup_components(c: Config):

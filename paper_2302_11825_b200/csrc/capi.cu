@@ -133,6 +133,9 @@ FarField bvc_scene_s::farfield() {
     if (dim == 2) launch_farfield2(view(), ff, ffGrid.p, g_stream);
     else launch_farfield3(view3(), ff, ffGrid.p, g_stream);
     CK(cudaGetLastError());
+    // built once per scene, possibly on another stream than its readers (the round's
+    // side stream runs band walks that use it): complete it before publishing it
+    CK(cudaStreamSynchronize(g_stream));
     ffBuilt = true;
     return ff;
 }
@@ -172,6 +175,9 @@ HintGrid bvc_scene_s::hintgrid() {
     if (dim == 2) launch_hintgrid2(view(), hg, hgIds.p, hgEntry.p, rmin, g_stream);
     else launch_hintgrid3(view3(), hg, hgIds.p, hgEntry.p, rmin, g_stream);
     CK(cudaGetLastError());
+    // built once per scene, possibly on another stream than its readers (the round's
+    // side stream runs band walks that use it): complete it before publishing it
+    CK(cudaStreamSynchronize(g_stream));
     hg.id = hgIds.p;
     const char* ee = std::getenv("BVC_ENTRY");
     hg.entry = (ee && std::string(ee) == "0") ? nullptr : hgEntry.p;

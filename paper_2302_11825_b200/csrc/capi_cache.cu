@@ -33,7 +33,11 @@ WalkEnv make_env(bvc_scene_s* S, const bvc_problem& pb, const bvc_walk_config& w
     E.nudge = static_cast<float>(9.5367431640625e-7 * diag);  // 2^-20 diag, << eps
     E.cx = static_cast<float>(0.5 * (S->host.lo[0] + S->host.hi[0]));
     E.cy = static_cast<float>(0.5 * (S->host.lo[1] + S->host.hi[1]));
-    E.escape = static_cast<float>(diag);
+    // FP32 safety net: in a closed scene a walker more than one diagonal from the box
+    // centre has leaked through the boundary (impossible in exact arithmetic) and ends
+    // like a truncated walk. Open scenes (subdomain chains, pointwise solves) keep
+    // walking until maxSteps, as the reference does (pointwise.cpp:162-164).
+    E.escape = S->host.closed() ? static_cast<float>(diag) : 3.0e38f;
     E.maxSteps = std::max(1, wc.maxSteps);
     E.hasNeumann = S->host.hasNeumann() ? 1 : 0;
     E.hasSource = pb.f.kind != BVC_FIELD_NONE ? 1 : 0;
@@ -158,7 +162,7 @@ WalkEnv3 make_env3(bvc_scene_s* S, const bvc_problem& pb, const bvc_walk_config&
     E.cx = static_cast<float>(0.5 * (S->host.lo[0] + S->host.hi[0]));
     E.cy = static_cast<float>(0.5 * (S->host.lo[1] + S->host.hi[1]));
     E.cz = static_cast<float>(0.5 * (S->host.lo[2] + S->host.hi[2]));
-    E.escape = static_cast<float>(diag);
+    E.escape = S->host.closed() ? static_cast<float>(diag) : 3.0e38f;  // meshes are closed soups
     E.maxSteps = std::max(1, wc.maxSteps);
     E.hasNeumann = S->host.hasNeumann() ? 1 : 0;
     E.hasH = pb.h.kind != BVC_FIELD_NONE ? 1 : 0;

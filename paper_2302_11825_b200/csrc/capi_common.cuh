@@ -287,6 +287,10 @@ struct bvc_source_cache_s {
 struct bvc_eval_points_s {
     size_t n = 0;
     int dim = 2;
+    // global index of point 0 when the caller's point set is one shard of a larger one
+    // (bvc_points_set_index_base): per-point RNG streams (band walks, clamp
+    // corrections) are keyed by base + index, so a sharded run draws what one GPU would
+    long long base = 0;
     DevBuf<double> x;
     DevBuf<uint8_t> fallback, unreliable;
     DevBuf<double> bsum, ssum, bgsum, sgsum, walkSum, gwalkSum;

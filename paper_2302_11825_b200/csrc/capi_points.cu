@@ -284,6 +284,14 @@ int bvc_points_create(const double* x, size_t n, int dim, bvc_eval_points* out) 
     })
 }
 int bvc_points_destroy(bvc_eval_points p) { API(delete p) }
+int bvc_points_set_index_base(bvc_eval_points p, long long base) {
+    API({
+        need(p, "null points");
+        need(base >= 0, "negative index base");
+        p->base = base;
+    })
+}
+
 int bvc_points_reset(bvc_eval_points p) {
     API({
         require_device();

@@ -133,6 +133,7 @@ void corrected_boundary(bvc_boundary_cache_s* b, bvc_eval_points_s* P, bvc_regio
     E.nRound = static_cast<double>(N);
     E.insideTol = static_cast<float>(1e-7 * R->boundary.host.diagonal);
     key_of(seed, stream, 0, E.k0, E.k1);
+    E.base = P->base;
     int* noHit = ws().get<int>(kWsCorrFlag, 1);
     CK(cudaMemsetAsync(noHit, 0, sizeof(int), g_stream));
     auto check_hits = [&]() {
@@ -208,7 +209,8 @@ void corrected_source(bvc_source_cache_s* s, bvc_eval_points_s* P, bvc_region_s*
     uint32_t k0, k1;
     key_of(seed, stream, 0, k0, k1);
     launch_ball_corr(R->boundary.view(), static_cast<float>(1e-7 * R->boundary.host.diagonal), P->x.p, P->order.p,
-                     P->ballR.p, K, to_dev(*f), clamp, static_cast<double>(s ? s->m : 0), k0, k1, P->ssum.p, g_stream);
+                     P->ballR.p, K, to_dev(*f), clamp, static_cast<double>(s ? s->m : 0), k0, k1, P->base, P->ssum.p,
+                     g_stream);
     CK(cudaGetLastError());
 }
 

@@ -131,21 +131,22 @@ __global__ void first_ball_radius_kernel(const double* dist, int n, float rmin, 
     if (i < n) r[i] = static_cast<float>(fmax(dist[i], static_cast<double>(rmin)));
 }
 
-__global__ void gather_fallback_kernel(const int* idx, int n, const double* x, float2* out, long long* gid) {
+__global__ void gather_fallback_kernel(const int* idx, int n, const double* x, float2* out, long long* gid,
+                                       long long base) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     int p = idx[j];
     out[j] = make_float2(static_cast<float>(x[2 * p]), static_cast<float>(x[2 * p + 1]));
-    gid[j] = p;
+    gid[j] = base + p;  // global point index: the same walk streams on any shard
 }
 
 __global__ void gather_fallback3_kernel(const int* idx, int n, const double* x, float4* out, long long* gid,
-                                        double* xd) {
+                                        double* xd, long long base) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     int p = idx[j];
     out[j] = make_float4(static_cast<float>(x[3 * p]), static_cast<float>(x[3 * p + 1]), static_cast<float>(x[3 * p + 2]), 0.f);
-    gid[j] = p;
+    gid[j] = base + p;  // global point index: the same walk streams on any shard
     xd[3 * j] = x[3 * p];
     xd[3 * j + 1] = x[3 * p + 1];
     xd[3 * j + 2] = x[3 * p + 2];
@@ -184,7 +185,7 @@ void fallback_walks3(bvc_scene_s* S, const bvc_problem& pb, const bvc_cache_conf
     float4* px = ws().get<float4>(kWsStartU, nf);
     long long* gid = ws().get<long long>(kWsGidU, nf);
     double* xd = ws().get<double>(kWsEvalIn, 3 * static_cast<size_t>(nf));
-    gather_fallback3_kernel<<<(nf + 127) / 128, 128, 0, g_stream>>>(idx, nf, P->x.p, px, gid, xd);
+    gather_fallback3_kernel<<<(nf + 127) / 128, 128, 0, g_stream>>>(idx, nf, P->x.p, px, gid, xd, P->base);
     count_launch();
     WalkEnv3 E = make_env3(S, pb, cfg.walk, seed, kFallbackSalt, round);
     auto* ctr = ws().get<unsigned long long>(kWsCounter, 3);
@@ -246,7 +247,7 @@ void fallback_walks(bvc_scene_s* S, const bvc_problem& pb, const bvc_cache_confi
     int nw = std::max(1, cfg.walk.nWalks);
     float2* px = ws().get<float2>(kWsStartU, nf);
     long long* gid = ws().get<long long>(kWsGidU, nf);
-    gather_fallback_kernel<<<(nf + 127) / 128, 128, 0, g_stream>>>(idx, nf, P->x.p, px, gid);
+    gather_fallback_kernel<<<(nf + 127) / 128, 128, 0, g_stream>>>(idx, nf, P->x.p, px, gid, P->base);
     count_launch();
     if (S->host.closed()) {  // requireInterior
         WalkEnv E0 = make_env(S, pb, cfg.walk, seed, kFallbackSalt, round);

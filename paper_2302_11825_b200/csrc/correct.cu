@@ -108,7 +108,7 @@ __global__ void corr_rays_kernel(const CorrRayEnv E, const double* x, const int*
     double px = x[2 * p], py = x[2 * p + 1];
     int nsat = 0;
     double corr = 0.0;
-    int hits = saturated_hits(E, px, py, p, [&](const SatHit& h) {
+    int hits = saturated_hits(E, px, py, E.base + p, [&](const SatHit& h) {
         ++nsat;
         if (E.useField) corr += h.w * static_cast<double>(field_eval(E.field, static_cast<float>(h.zx), static_cast<float>(h.zy)));
     });
@@ -125,7 +125,7 @@ __global__ void corr_emit_kernel(const CorrRayEnv E, const double* x, const int*
     int p = order[i];
     double px = x[2 * p], py = x[2 * p + 1];
     int o = offsets[i], k = 0;
-    saturated_hits(E, px, py, p, [&](const SatHit& h) {
+    saturated_hits(E, px, py, E.base + p, [&](const SatHit& h) {
         // makeDefaultEvaluator cache.cpp:608-616: KnownNeumann crossings start eps/2 inside
         double zx = h.zx, zy = h.zy;
         if (E.kinds[h.seg] == 0) {
@@ -134,7 +134,7 @@ __global__ void corr_emit_kernel(const CorrRayEnv E, const double* x, const int*
             zy -= 0.5 * E.eps * n.y;
         }
         starts[o + k] = make_float2(static_cast<float>(zx), static_cast<float>(zy));
-        gid[o + k] = static_cast<long long>(p) * 4096 + k;
+        gid[o + k] = (E.base + p) * 4096 + k;
         w[o + k] = h.w;
         ++k;
     });
@@ -171,12 +171,13 @@ __device__ double invert_ball_cdf_d(double u) {
 
 __global__ void ball_corr_kernel(const SceneView2 region, float insideTol, const double* x, const int* order,
                                  const double* ballR, int K, const DevField f, double clamp, double mRound, uint32_t k0,
-                                 uint32_t k1, double* ssum) {
+                                 uint32_t k1, long long base, double* ssum) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= K) return;
     int p = order[i];
     double px = x[2 * p], py = x[2 * p + 1], R = ballR[p];
-    U4 r = philox4x32_10(U4{static_cast<uint32_t>(p), 0u, 0u, 0u}, k0, k1);
+    const long long gp = base + p;  // global point index: the same stream on any shard
+    U4 r = philox4x32_10(U4{static_cast<uint32_t>(gp), static_cast<uint32_t>(gp >> 32), 0u, 0u}, k0, k1);
     // sampleBallGreens kernels.cpp:96-107
     double t = invert_ball_cdf_d(u01d(r.x, r.y));
     double rr = fmax(t * R, 1e-14 * R);
@@ -234,10 +235,10 @@ void launch_corr_apply(const int* offsets, const int* counts, const int* order, 
 }
 void launch_ball_corr(const SceneView2& region, float insideTol, const double* x, const int* order,
                       const double* ballR, int K, const DevField& f, double clamp, double mRound, uint32_t k0,
-                      uint32_t k1, double* ssum, cudaStream_t st) {
+                      uint32_t k1, long long base, double* ssum, cudaStream_t st) {
     if (K <= 0) return;
     ball_corr_kernel<<<blocks(K), 128, 0, st>>>(region, insideTol, x, order, ballR, K, f, clamp, mRound, k0, k1,
-                                                 ssum);
+                                                 base, ssum);
     count_launch();
 }
 void launch_ball_radius(const double* x, int n, int dim, const double* hull, int nh, double* R, cudaStream_t st) {

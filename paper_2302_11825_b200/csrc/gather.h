@@ -48,6 +48,7 @@ struct CorrRayEnv {
     float eps;                   // walk epsilon (Neumann crossings start eps/2 inside)
     float insideTol;
     uint32_t k0, k1;             // ray-direction key (seed, stream)
+    long long base;              // global index of the points' first point (sharded point sets)
     int useField;                // 1: u(z) = field(z); 0: counts for the walk evaluator
     bvc_dev::DevField field;
 };
@@ -59,7 +60,7 @@ void launch_corr_apply(const int* offsets, const int* counts, const int* order, 
                        const double* mean, double nRound, double* bsum, cudaStream_t st);
 void launch_ball_corr(const bvc_dev::SceneView2& region, float insideTol, const double* x, const int* order,
                       const double* ballR, int K, const bvc_dev::DevField& f, double clamp, double mRound, uint32_t k0,
-                      uint32_t k1, double* ssum, cudaStream_t st);
+                      uint32_t k1, long long base, double* ssum, cudaStream_t st);
 void launch_ball_radius(const double* x, int n, int dim, const double* hull, int nh, double* R, cudaStream_t st);
 void launch_gather_f32(const double* v, const int* order, int K, float* out, cudaStream_t st);
 // FP64 variant (gather64.cu): Poisson kernels, exact per-pair coincidence test

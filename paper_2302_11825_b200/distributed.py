@@ -70,6 +70,8 @@ def generate_and_allgather(B, dist, torch, scene, problem, region, cfg, seed, rn
     h = C.c_void_p()
     B.api._check(B.lib().bvc_boundary_cache_from_packed(C.c_void_p(full.data_ptr()), N, shard.dim, 0,
                                                         C.c_double(0.0), C.byref(h)))
+    # the library copies from `full` on its own stream; finish before torch may recycle it
+    B.synchronize()
     cache = B.BoundaryCache(h)
     if cfg.voronoi:  # the weights need the whole round's samples
         cache.assign_voronoi(region)
