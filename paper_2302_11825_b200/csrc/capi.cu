@@ -364,16 +364,19 @@ void bvc_scene_s::upload() {
     }
     std::vector<float2> hnrm(host.ns);
     std::vector<float4> hab(host.ns);
+    std::vector<double4> hab64(host.ns);
     std::vector<float> harc(host.ns), hlen(host.ns);
     for (int i = 0; i < host.ns; ++i) {
         hnrm[i] = make_float2(host.normal[2 * i], host.normal[2 * i + 1]);
         const double *a = host.vert(host.idx[2 * i]), *b = host.vert(host.idx[2 * i + 1]);
         hab[i] = make_float4(a[0], a[1], b[0], b[1]);
+        hab64[i] = make_double4(a[0], a[1], b[0], b[1]);
         harc[i] = static_cast<float>(host.arc[i]);
         hlen[i] = static_cast<float>(host.measure[i]);
     }
     segNormal.upload(hnrm.data(), hnrm.size());
     segAB.upload(hab.data(), hab.size());
+    segAB64.upload(hab64.data(), hab64.size());
     segArc.upload(harc.data(), harc.size());
     segLen.upload(hlen.data(), hlen.size());
     size_t nsil = host.silAlways.size();

@@ -207,6 +207,7 @@ struct bvc_scene_s {
     DevBuf<Prim2> prims;
     DevBuf<float2> segNormal, silP;
     DevBuf<float4> segAB, silN;
+    DevBuf<double4> segAB64;  // FP64 endpoints by segment id: exact classification decisions
     DevBuf<int> silAlways;
     // boundary sampler over all segments (BoundarySampler sampling.cpp:8-18)
     DevBuf<double> cdf;

@@ -196,22 +196,46 @@ __global__ void solution_kernel(int n, int d, const uint8_t* fb, const double* b
     }
 }
 
-__global__ void mark_kernel(const bvc_dev::SceneView2 scene, const bvc_dev::SceneView2 region, const double* x, int n,
-                            float offset, int whole, uint8_t* fb, uint8_t* gu) {
+// "some segment of the classes in qmask lies at distance < l from x", decided exactly as
+// the reference decides it (closestPointOnSegment bvh.h:153-159, then norm() < l, in
+// FP64 without contractions, like the host build): the FP32 BVH only proposes the
+// candidates — every primitive whose box lies within l + margin, the margin covering
+// the FP32 rounding of boxes and of x — and each candidate's distance is FP64.
+__device__ bool within_exact(const bvc_dev::SceneView2& S, const double4* ab, double x, double y, unsigned qmask,
+                             double l, float margin) {
+    const float r = static_cast<float>(l) + margin;
+    const float r2 = r * r;
+    bool hit = false;
+    bvc_dev::traverse_near(
+        S, static_cast<float>(x), static_cast<float>(y), qmask,
+        [&](const bvc_dev::Prim2& p) {
+            if (hit) return;
+            const double4 s = ab[p.id];
+            const double ux = __dsub_rn(s.z, s.x), uy = __dsub_rn(s.w, s.y);
+            const double len2 = __dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy));
+            double t = 0.0;
+            if (len2 > 0.0) {
+                t = __ddiv_rn(__dadd_rn(__dmul_rn(__dsub_rn(x, s.x), ux), __dmul_rn(__dsub_rn(y, s.y), uy)), len2);
+                t = fmin(fmax(t, 0.0), 1.0);
+            }
+            const double dx = __dsub_rn(__dadd_rn(s.x, __dmul_rn(t, ux)), x);
+            const double dy = __dsub_rn(__dadd_rn(s.y, __dmul_rn(t, uy)), y);
+            if (__dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy))) < l) hit = true;
+        },
+        [&]() { return hit ? -1.0f : r2; });
+    return hit;
+}
+
+__global__ void mark_kernel(const bvc_dev::SceneView2 scene, const double4* sceneAB, const bvc_dev::SceneView2 region,
+                            const double4* regionAB, const double* x, int n, double offset, int whole, float margin,
+                            uint8_t* fb, uint8_t* gu) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    float px = static_cast<float>(x[2 * i]), py = static_cast<float>(x[2 * i + 1]);
-    // fallbackBand cache.cpp:131-135: whole-domain points within l of the Dirichlet boundary
-    // both tests only ask "closer than l": queries bounded by l prune everything farther
-    const float l2 = offset * offset;
-    uint8_t f = 0;
-    if (whole) {
-        bvc_dev::Closest c = bvc_dev::closest_point(scene, px, py, bvc_dev::kClsD, l2);
-        f = c.seg >= 0 ? 1 : 0;
-    }
-    bvc_dev::Closest r = bvc_dev::closest_point(region, px, py, bvc_dev::kClsAny, l2);
-    fb[i] = f;
-    gu[i] = r.seg >= 0 ? 1 : 0;
+    const double px = x[2 * i], py = x[2 * i + 1];
+    // fallbackBand cache.cpp:131-135: whole-domain points within l of the Dirichlet
+    // boundary; gradientUnreliable cache.cpp:270-271: within l of the region boundary
+    fb[i] = whole && within_exact(scene, sceneAB, px, py, bvc_dev::kClsD, offset, margin) ? 1 : 0;
+    gu[i] = within_exact(region, regionAB, px, py, bvc_dev::kClsAny, offset, margin) ? 1 : 0;
 }
 
 // markEvaluationPoints (cache.cpp:263-276)
@@ -237,9 +261,13 @@ void mark_points(bvc_scene_s* s, bvc_region_s* r, const bvc_cache_config& cfg, b
                      r->host.wholeDomain ? 1 : 0, single ? static_cast<float>(1e-7 * r->boundary.host.diagonal) : -1.f,
                      p->fallback.p, p->unreliable.p, g_stream);
     } else if (n) {
-        mark_kernel<<<(n + 127) / 128, 128, 0, g_stream>>>(s->view(), r->boundary.view(), p->x.p, n,
-                                                           static_cast<float>(r->host.offset), r->host.wholeDomain ? 1 : 0,
-                                                           p->fallback.p, p->unreliable.p);
+        // FP32 boxes and query positions are within ~1e-7 diag of the exact ones
+        const float margin = static_cast<float>(1e-5 * std::max(s->host.diagonal, r->boundary.host.diagonal));
+        const bvc_dev::SceneView2 sv = s->view(), rv = r->boundary.view();  // uploads both (lazily)
+        mark_kernel<<<(n + 127) / 128, 128, 0, g_stream>>>(sv, s->segAB64.p, rv,
+                                                           r->boundary.segAB64.p, p->x.p, n, r->host.offset,
+                                                           r->host.wholeDomain ? 1 : 0, margin, p->fallback.p,
+                                                           p->unreliable.p);
         count_launch();
     }
     p->orderValid = false;

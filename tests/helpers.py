@@ -71,3 +71,10 @@ def rel_err(got, ref):
     got, ref = np.asarray(got, float), np.asarray(ref, float)
     scale = max(np.max(np.abs(ref)), float(np.sqrt(np.mean(ref ** 2))), 1e-300)
     return float(np.max(np.abs(got - ref)) / scale)
+
+
+def rel_err_pointwise(got, ref):
+    """SURVEY §8d's per-point form: max_k |got_k - ref_k| / max(|ref_k|, RMS(ref))."""
+    got, ref = np.asarray(got, float), np.asarray(ref, float)
+    rms = max(float(np.sqrt(np.mean(ref ** 2))), 1e-300)
+    return float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), rms)))

@@ -147,6 +147,77 @@ def test_source_cache_fields():
     assert B.generate_source_cache(pbl, rl, cfg, 23, 0).m == 0
 
 
+def _region_from_loop(loop_geom):
+    """a SolveRegion whose boundary is exactly `loop_geom` (a Subdomain loop inside a
+    larger all-Dirichlet square), so the source sampler samples that loop's interior"""
+    v, s, l = loop_geom
+    lo, hi = v.min(0) - 0.5, v.max(0) + 0.5
+    outer = O.rectangle_geometry(lo, hi, [0, 0, 0, 0])
+    sc = B.Scene(*outer)
+    sub = B.Scene(v, s, np.zeros(len(s), np.int32))
+    return sc, B.SolveRegion(sc, abi.REGION_SUBDOMAIN, 0.0, sub, epsilon=1e-3)
+
+
+def test_region_sampler_pdf_containment_moments():
+    """RegionSampler (sampling.cpp:62-108) through generateSourceCache (cache.cpp:392-406):
+    the reference's test_geometry.cpp:287-316 — unit square, 100000 unstratified samples,
+    pdf = 1 and mean (0.5, 0.5) within 0.003 (plus E[x^2] = 1/3); a 256-gon disk, 2000
+    stratified samples, pdf = 1/polygon area (FP32 storage) within 1e-3 of 1/pi, all inside."""
+    pb = H.make_problem(H.kspec(), f=abi.make_field(abi.FIELD_CONSTANT, [1.0]))
+    sc, region = _region_from_loop(O.rectangle_geometry([0, 0], [1, 1], [0, 0, 0, 0]))
+    assert abs(region.area - 1.0) < 1e-14
+    cfg = B.cache_config(nSource=100000, stratified=0)
+    d = B.generate_source_cache(pb, region, cfg, 29, 0).download()
+    assert len(d["pdf"]) == 100000
+    np.testing.assert_allclose(d["pdf"], 1.0, rtol=1e-7)
+    m = d["y"].mean(0)
+    assert np.all(np.abs(m - 0.5) < 0.003), m
+    m2 = (d["y"] ** 2).mean(0)
+    assert np.all(np.abs(m2 - 1.0 / 3.0) < 0.003), m2
+    assert np.all((d["y"] > 0) & (d["y"] < 1))
+    disk = O.circle_geometry(segments=256)
+    area = 0.5 * 256 * np.sin(2 * np.pi / 256)
+    sc, region = _region_from_loop(disk)
+    assert abs(region.area - area) < 1e-14 * area
+    d = B.generate_source_cache(pb, region, B.cache_config(nSource=2000, stratified=1), 29, 1).download()
+    np.testing.assert_allclose(d["pdf"], 1.0 / area, rtol=1e-7)
+    assert np.all(np.abs(d["pdf"] - 1.0 / np.pi) < 1e-3)
+    assert np.all(region.boundary.inside(d["y"]))
+    assert np.all(O.RefScene(*disk).inside(d["y"]))
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("stratified", [0, 1])
+def test_region_sampler_distribution_matches_reference(stratified):
+    """The GPU source samples and the reference's RegionSampler on C3's Subdomain loop
+    (a 5-star) draw from the same law: two-sample KS tests on x, y and the radius, and
+    the means / second moments within 4 standard errors."""
+    from scipy import stats
+
+    c = configs.config3(scale=1 / 16)
+    sc = B.Scene(c.vertices, c.segments, c.labels)
+    sub = B.Scene(c.sub_vertices, c.sub_segments, np.zeros(len(c.sub_segments), np.int32))
+    region = B.SolveRegion(sc, abi.REGION_SUBDOMAIN, c.region_offset, sub, epsilon=c.epsilon)
+    rs = O.RefScene(c.vertices, c.segments, c.labels)
+    rsub = O.RefScene(c.sub_vertices, c.sub_segments, np.zeros(len(c.sub_segments), np.int32))
+    rr = O.RefRegion(rs, abi.REGION_SUBDOMAIN, c.region_offset, rsub, eps=c.epsilon)
+    cfg = c.cache
+    cfg.nSource, cfg.stratified = 65536, stratified
+    g = B.generate_source_cache(c.problem, region, cfg, 5, 0).download()
+    r = O.ref_generate_source_cache(c.problem, rr, cfg, 5, 0)
+    assert len(g["y"]) == len(r["y"]) == 65536
+    assert np.all(rsub.inside(g["y"]))
+    np.testing.assert_allclose(g["pdf"], r["pdf"], rtol=1e-7)
+    for name, a, b in (("x", g["y"][:, 0], r["y"][:, 0]), ("y", g["y"][:, 1], r["y"][:, 1]),
+                       ("radius", np.hypot(*g["y"].T), np.hypot(*r["y"].T))):
+        assert stats.ks_2samp(a, b).pvalue > 1e-3, name
+    for k in range(2):
+        for mom in (1, 2):
+            a, b = g["y"][:, k] ** mom, r["y"][:, k] ** mom
+            se = np.sqrt(a.var() / len(a) + b.var() / len(b))
+            assert abs(a.mean() - b.mean()) < 4 * se, (k, mom)
+
+
 def test_update_solution_rounds_accumulate_and_commute():
     """test_cache.cpp:571-621."""
     geom, pb, sc, region = _setup(H.disk_poisson)
@@ -171,21 +242,63 @@ def test_update_solution_rounds_accumulate_and_commute():
     assert f["boundarySum"][0] == r["boundarySum"][0] and f["sourceSum"][0] == r["sourceSum"][0]
 
 
+def _near_band_points(v, s, l, n, rng):
+    """points placed at distance l (1 + delta) from random segments' interiors, delta in
+    {0, +-1e-15, +-1e-12, +-1e-9}: the band's edge, where an FP32 decision would flip"""
+    ids = rng.integers(0, len(s), n)
+    a, b = v[s[ids, 0]], v[s[ids, 1]]
+    t = rng.uniform(0.05, 0.95, n)
+    p = a + t[:, None] * (b - a)
+    d = b - a
+    nrm = np.stack([-d[:, 1], d[:, 0]], 1) / np.linalg.norm(d, axis=1)[:, None]  # left normal: inside of a CCW loop
+    delta = rng.choice([0.0, 1e-15, -1e-15, 1e-12, -1e-12, 1e-9, -1e-9], n)
+    return p + nrm * (l * (1.0 + delta))[:, None]
+
+
 @pytest.mark.ref
-def test_mark_points_match_reference():
-    geom, pb, sc, region = _setup(H.disk_poisson)
-    rs = O.RefScene(*geom)
-    rr = O.RefRegion(rs, abi.REGION_WHOLE_DOMAIN, 0.05, eps=1e-3)
-    cfg = B.cache_config(offset=0.05)
-    rng = np.random.default_rng(2)
-    r = np.sqrt(rng.uniform(0, 0.99, 4000))
-    a = rng.uniform(0, 2 * np.pi, 4000)
-    x = np.stack([r * np.cos(a), r * np.sin(a)], 1)
+@pytest.mark.parametrize("cid", [0, 1, 2, 3])
+def test_mark_points_match_reference(cid):
+    """markEvaluationPoints (cache.cpp:263-276) bit-exact: the fallback and gradientUnreliable
+    flags equal the reference's on every point — disk points, the full C1/C2/C3 query grids,
+    and points placed at the band's edge (distance l (1 +- 1e-15 ... 1e-9))."""
+    rng = np.random.default_rng(2 + cid)
+    if cid == 0:
+        geom, pb, sc, region = _setup(H.disk_poisson)
+        rs = O.RefScene(*geom)
+        rr = O.RefRegion(rs, abi.REGION_WHOLE_DOMAIN, 0.05, eps=1e-3)
+        cfg = B.cache_config(offset=0.05)
+        r = np.sqrt(rng.uniform(0, 0.99, 4000))
+        a = rng.uniform(0, 2 * np.pi, 4000)
+        x = np.stack([r * np.cos(a), r * np.sin(a)], 1)
+        v, s, lab = geom
+        l = 0.05
+    else:
+        c = configs.CONFIGS[cid]()
+        sc = B.Scene(c.vertices, c.segments, c.labels)
+        rs = O.RefScene(c.vertices, c.segments, c.labels)
+        cfg = c.cache
+        if c.region_mode == abi.REGION_SUBDOMAIN:
+            sub = B.Scene(c.sub_vertices, c.sub_segments, np.zeros(len(c.sub_segments), np.int32))
+            region = B.SolveRegion(sc, abi.REGION_SUBDOMAIN, c.region_offset, sub, epsilon=c.epsilon)
+            rsub = O.RefScene(c.sub_vertices, c.sub_segments, np.zeros(len(c.sub_segments), np.int32))
+            rr = O.RefRegion(rs, abi.REGION_SUBDOMAIN, c.region_offset, rsub, eps=c.epsilon)
+            x = c.points[rsub.inside(c.points)]
+            v, s, lab = c.sub_vertices, c.sub_segments, None
+        else:
+            region = B.SolveRegion(sc, offset=c.region_offset, epsilon=c.epsilon)
+            rr = O.RefRegion(rs, abi.REGION_WHOLE_DOMAIN, c.region_offset, eps=c.epsilon)
+            x = c.points
+            v, s, lab = c.vertices, c.segments, c.labels
+        l = region.offset
+    if lab is not None:
+        s = s[lab == abi.DIRICHLET]
+    x = np.concatenate([x, _near_band_points(v, s, l, 20000, rng)])
     pts = B.EvaluationPoints(x)
     B.mark_evaluation_points(sc, region, cfg, pts)
     st = pts.download()
     fb, gu = O.ref_mark_points(rs, rr, cfg, x)
-    assert np.mean(st["fallback"] == fb) > 0.999 and np.mean(st["gradientUnreliable"] == gu) > 0.999
+    assert np.array_equal(st["fallback"], fb), int(np.sum(st["fallback"] != fb))
+    assert np.array_equal(st["gradientUnreliable"], gu), int(np.sum(st["gradientUnreliable"] != gu))
 
 
 def test_end_to_end_config2_small_vs_exact_and_reference():
