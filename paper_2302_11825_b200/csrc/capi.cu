@@ -6,6 +6,7 @@
 // host_scene.cpp. There is no CPU fallback: every compute entry point fails with
 // BVC_ERR_NO_DEVICE when no CUDA device is present.
 #include <atomic>
+#include <mutex>
 
 #include <cub/device/device_scan.cuh>
 
@@ -14,65 +15,89 @@
 namespace bvc_capi {
 
 thread_local std::string g_error;
-cudaStream_t g_stream = nullptr;
-std::function<void()> g_afterWalkLaunch;
-bool g_profile = false;
-unsigned long long g_profileTotals[2] = {0, 0};
+// Runtime state is per host thread and per device: a thread's current stream, its
+// scratch workspaces and its side stream. Two threads driving two GPUs (or two
+// threads sharing one) never share a stream or a scratch buffer.
+__thread cudaStream_t g_stream = nullptr;
+thread_local std::function<void()> g_afterWalkLaunch;
+__thread bool g_profile = false;
+__thread unsigned long long g_profileTotals[2] = {0, 0};
 
 namespace {
 std::atomic<long long> g_launches{0};
+constexpr int kMaxDevices = 64;
+struct DeviceState {
+    cudaStream_t stream = nullptr;  // the thread's stream on this device (bvc_set_stream)
+    Workspace* work = nullptr;      // main-stream scratch (lives for the process)
+    cudaStream_t side = nullptr;    // second stream for work overlapping the cache walks
+    Workspace* sideWork = nullptr;  // its own scratch
+};
+thread_local DeviceState t_dev[kMaxDevices];
+thread_local int t_device = -1;  // device g_stream belongs to
+int current_device() {
+    int d = 0;
+    CK(cudaGetDevice(&d));
+    need(d >= 0 && d < kMaxDevices, "device index out of range");
+    return d;
+}
 }  // namespace
 
 void require_device() {
-    static int state = -1;  // -1 unknown, 0 none, 1 ok
-    if (state < 0) {
+    static std::atomic<int> state{-1};  // -1 unknown, 0 none, 1 ok
+    if (state.load() < 0) {
         int n = 0;
         cudaError_t e = cudaGetDeviceCount(&n);
-        state = (e == cudaSuccess && n > 0) ? 1 : 0;
+        state.store((e == cudaSuccess && n > 0) ? 1 : 0);
         if (e != cudaSuccess) cudaGetLastError();
     }
-    if (!state) throw Error(bvc_host::kNoDevice, "no CUDA device: the BVC path has no CPU fallback");
+    if (!state.load()) throw Error(bvc_host::kNoDevice, "no CUDA device: the BVC path has no CPU fallback");
 }
 
 void ensure_pool() {
-    static int device = -1;
-    int d = 0;
-    cudaGetDevice(&d);
-    if (d == device) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
-        uint64_t keep = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    device = d;
+    static std::once_flag once[kMaxDevices];
+    int d = current_device();
+    std::call_once(once[d], [d] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
 }
 
-Workspace* g_wsActive = nullptr;
+void bind_device(int device) {
+    if (t_device >= 0 && t_device < kMaxDevices) t_dev[t_device].stream = g_stream;
+    CK(cudaSetDevice(device));
+    t_device = current_device();
+    g_stream = t_dev[t_device].stream;
+}
+
+void bind_stream(cudaStream_t s) {
+    g_stream = s;
+    t_device = current_device();
+    t_dev[t_device].stream = s;
+}
+
+__thread Workspace* g_wsActive = nullptr;
 Workspace& ws() {
-    static Workspace w;
-    return g_wsActive ? *g_wsActive : w;
+    if (g_wsActive) return *g_wsActive;
+    DeviceState& d = t_dev[current_device()];
+    if (!d.work) d.work = new Workspace();  // lives for the process
+    return *d.work;
 }
 
 namespace {
-struct Side {
-    cudaStream_t stream = nullptr;
-    Workspace* work = nullptr;
-};
-Side& side_for_device() {
-    static Side sides[64];
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    need(dev >= 0 && dev < 64, "device index out of range");
-    Side& sd = sides[dev];
-    if (!sd.stream) {
-        CK(cudaStreamCreateWithFlags(&sd.stream, cudaStreamNonBlocking));
-        sd.work = new Workspace();  // lives for the process, like the main workspace
+DeviceState& side_for_device() {
+    DeviceState& d = t_dev[current_device()];
+    if (!d.side) {
+        CK(cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking));
+        d.sideWork = new Workspace();  // lives for the process, like the main workspace
     }
-    return sd;
+    return d;
 }
 }  // namespace
 
-SideScope::SideScope() : stream(side_for_device().stream), saved(g_wsActive) { g_wsActive = side_for_device().work; }
+SideScope::SideScope() : stream(side_for_device().side), saved(g_wsActive) { g_wsActive = side_for_device().sideWork; }
 
 int fail(const std::exception& e) {
     g_error = e.what();
@@ -438,8 +463,8 @@ const char* bvc_last_error(void) { return g_error.c_str(); }
 int bvc_abi_version(void) { return BVC_ABI_VERSION; }
 long long bvc_kernel_launch_count(void) { return bvc_capi::g_launches.load(); }
 
-int bvc_set_device(int device) { API(require_device(); CK(cudaSetDevice(device))) }
-int bvc_set_stream(void* s) { API(g_stream = static_cast<cudaStream_t>(s)) }
+int bvc_set_device(int device) { API(require_device(); bind_device(device)) }
+int bvc_set_stream(void* s) { API(require_device(); bind_stream(static_cast<cudaStream_t>(s))) }
 int bvc_synchronize(void) { API(require_device(); CK(cudaStreamSynchronize(g_stream))) }
 
 int bvc_scene_create(const double* v, int nv, const int* segs, const int* labels, int ns, bvc_scene* out) {

@@ -33,11 +33,11 @@ using bvc_dev::Node2;
 using bvc_dev::Prim2;
 
 extern thread_local std::string g_error;
-extern cudaStream_t g_stream;
+extern __thread cudaStream_t g_stream;  // __thread: POD, no TLS-init wrapper
 // One-shot host callback run right after a cache-walk job is enqueued: the host-buffer
 // round (bvc_update_solution_host) uploads and classifies its points on a second
 // stream while the walks run.
-extern std::function<void()> g_afterWalkLaunch;
+extern thread_local std::function<void()> g_afterWalkLaunch;
 inline void after_walk_launch() {
     if (g_afterWalkLaunch) {
         std::function<void()> f = std::move(g_afterWalkLaunch);
@@ -54,8 +54,8 @@ struct StreamScope {
     StreamScope& operator=(const StreamScope&) = delete;
 };
 // diagnostic traversal counting (bvc_walk_traffic_profile); off in production
-extern bool g_profile;
-extern unsigned long long g_profileTotals[2];
+extern __thread bool g_profile;
+extern __thread unsigned long long g_profileTotals[2];
 
 inline void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw Error(bvc_host::kCuda, std::string(what) + ": " + cudaGetErrorString(e));
@@ -71,6 +71,9 @@ inline float int_as_float_host(int v) {
 void require_device();
 
 void ensure_pool();
+// bvc_set_device / bvc_set_stream: the calling thread's device and its stream there
+void bind_device(int device);
+void bind_stream(cudaStream_t s);
 
 template <class T>
 struct DevBuf {
@@ -115,7 +118,7 @@ struct Workspace {
 };
 // ws() hands out the active workspace: the main one, or (inside a SideScope) the side
 // stream's own, so work on the two streams never shares scratch buffers
-extern Workspace* g_wsActive;
+extern __thread Workspace* g_wsActive;
 Workspace& ws();
 // a second stream with its own workspace (one per device), for work that overlaps the
 // main stream's cache walks
