@@ -906,6 +906,10 @@ GatherPlan plan_gather(int kind, int K, int N, int M, bool val, bool grad) {
               : kind == kScr2 ? occupancy<kScr2>(val, grad)
               : kind == kLap3 ? occupancy<kLap3>(val, grad)
                               : occupancy<kScr3>(val, grad);
+    if (const char* e = std::getenv("BVC_GATHER_OCC")) {  // co-residency experiments: CTAs per SM cap
+        int v = std::atoi(e);
+        if (v >= 1 && v < occ) occ = v;
+    }
     g.tiles = (K + kPT - 1) / kPT;
     long long slots = static_cast<long long>(sms) * occ;
     // The chunk size depends only on the cache (N + M), never on K: each point's

@@ -12,6 +12,8 @@
 // so results are independent of scheduling, launch geometry and GPU count.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace bvc_impl {
@@ -670,6 +672,10 @@ void launch_walk_t(const WalkEnv& env, const WalkJob& job, long long total, cuda
     int perSm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, walk_kernel<NEU, SCR, SRC, COUNT>, kWalkThreads, 0);
     perSm = perSm > 0 ? perSm : 1;
+    if (const char* e = std::getenv("BVC_WALK_OCC")) {  // co-residency experiments: blocks per SM cap
+        int v = std::atoi(e);
+        if (v >= 1 && v < perSm) perSm = v;
+    }
     long long want = (total + kWalkThreads - 1) / kWalkThreads;
     int grid = static_cast<int>(want < static_cast<long long>(sms) * perSm ? want : static_cast<long long>(sms) * perSm);
     walk_kernel<NEU, SCR, SRC, COUNT><<<grid, kWalkThreads, 0, st>>>(env, job);

@@ -16,6 +16,8 @@
 // sampleBallGreens is 2D-only, kernels.cpp:98-99).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "internal.h"
 #include "scene3_dev.cuh"
 
@@ -584,6 +586,10 @@ void launch_walk3_t(const WalkEnv3& env, const WalkJob3& job, long long total, c
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, walk3_kernel<NEU, SCR, COUNT>, kThreads3, 0);
     perSm = perSm > 0 ? perSm : 1;
+    if (const char* e = std::getenv("BVC_WALK_OCC")) {  // co-residency experiments: blocks per SM cap
+        int v = std::atoi(e);
+        if (v >= 1 && v < perSm) perSm = v;
+    }
     long long want = (total + kThreads3 - 1) / kThreads3;
     int grid = static_cast<int>(want < static_cast<long long>(sms) * perSm ? want : static_cast<long long>(sms) * perSm);
     walk3_kernel<NEU, SCR, COUNT><<<grid, kThreads3, 0, st>>>(env, job);
