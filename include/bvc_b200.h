@@ -348,6 +348,16 @@ int bvc_corrected_source_splat(bvc_source_cache scache, bvc_eval_points pts, bvc
 int bvc_update_solution(bvc_scene scene, const bvc_problem* problem, bvc_region region,
                         const bvc_cache_config* cfg, bvc_eval_points pts, uint64_t seed,
                         uint64_t round, int gradients, bvc_round_stats* stats);
+/* the same with updateSolution's correctionEval argument (cache.h:195-198, used at
+   cache.cpp:646-648): the BoundaryEvaluator the ClampCorrect correction multiplies each
+   saturated crossing by. NULL or kind NONE = the empty default, i.e. the reference's
+   makeDefaultEvaluator (cfg->correctionWalks walks in `scene`, cache.cpp:600-620);
+   FIELD = exact data; WALKS = walks in the evaluator's own scene/problem/cfg. */
+int bvc_update_solution_with_evaluator(bvc_scene scene, const bvc_problem* problem,
+                                       bvc_region region, const bvc_cache_config* cfg,
+                                       bvc_eval_points pts, uint64_t seed, uint64_t round,
+                                       int gradients, const bvc_boundary_evaluator* correctionEval,
+                                       bvc_round_stats* stats);
 
 /* runSolveInMemory's round on host-resident points (runner.cpp:116-169: points built from
    x, markEvaluationPoints, updateSolution, then solution() / gradient() read back). x is

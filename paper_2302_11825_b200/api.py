@@ -36,7 +36,7 @@ SYMBOLS = (
     "bvc_walk_traffic_profile bvc_eval_kernels bvc_eval_bessel bvc_corrected_boundary_splat "
     "bvc_corrected_source_splat bvc_trace_streamlines bvc_grid_save_csv bvc_grid_load_csv bvc_grid_rmse "
     "bvc_grid_save_pgm bvc_streamlines_write_csv bvc_pipe_probe bvc_boundary_cache_assign_voronoi "
-    "bvc_fallback_walks bvc_update_solution_host bvc_generate_boundary_cache_shard_fallback "
+    "bvc_fallback_walks bvc_update_solution_host bvc_update_solution_with_evaluator bvc_generate_boundary_cache_shard_fallback "
     "bvc_points_set_index_base"
 ).split()
 
@@ -594,11 +594,18 @@ def mark_evaluation_points(scene: Scene, region: SolveRegion, cfg, pts: Evaluati
 
 
 def update_solution(scene: Scene, pb, region: SolveRegion, cfg, pts: EvaluationPoints, seed, round_,
-                    gradients=False) -> dict:
-    """updateSolution (cache.h:195-198): one progressive round; returns RoundStats."""
+                    gradients=False, correction_eval=None) -> dict:
+    """updateSolution (cache.h:195-198): one progressive round; returns RoundStats.
+    correction_eval: a BoundaryEvaluator (field_evaluator / walk_evaluator) for the
+    ClampCorrect correction; None = the reference's default (makeDefaultEvaluator)."""
     st = abi.RoundStats()
-    _check(lib().bvc_update_solution(scene.h, C.byref(pb), region.h, C.byref(cfg), pts.h, C.c_uint64(seed),
-                                     C.c_uint64(round_), int(gradients), C.byref(st)))
+    if correction_eval is None:
+        _check(lib().bvc_update_solution(scene.h, C.byref(pb), region.h, C.byref(cfg), pts.h, C.c_uint64(seed),
+                                         C.c_uint64(round_), int(gradients), C.byref(st)))
+    else:
+        _check(lib().bvc_update_solution_with_evaluator(scene.h, C.byref(pb), region.h, C.byref(cfg), pts.h,
+                                                        C.c_uint64(seed), C.c_uint64(round_), int(gradients),
+                                                        C.byref(correction_eval), C.byref(st)))
     return _stats_dict(st)
 
 

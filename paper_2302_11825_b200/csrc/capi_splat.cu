@@ -237,7 +237,7 @@ bvc_splat_config make_splat_config(bvc_scene_s* S, const bvc_problem& pb, const 
 // and the splats write different fields, with the same per-point RNG streams.
 void update_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const bvc_cache_config& cfg,
                   const std::function<bvc_eval_points_s*()>& points, uint64_t seed, uint64_t round, int gradients,
-                  bvc_round_stats* stats) {
+                  bvc_round_stats* stats, const bvc_boundary_evaluator* correctionEval) {
     require_device();
     need(s && r, "null argument");
     validate_kernel(pb.kernel);
@@ -293,11 +293,17 @@ void update_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const 
         splat(&bc, sp, p, scfg, 0, SIZE_MAX, true, gradients != 0);
     } else {
         double c = cfg.clamp > 0.0 ? cfg.clamp : 10.0 / s->host.diagonal;  // resolvedClamp cache.h:129-131
+        // correctionEval (cache.cpp:646-648): the caller's evaluator, or, when it is
+        // empty (NULL / NONE), makeDefaultEvaluator's walks (cache.cpp:600-620)
         bvc_boundary_evaluator ev{};
-        ev.kind = BVC_EVALUATOR_WALKS;
-        ev.scene = s;
-        ev.problem = &pb;
-        ev.cfg = &cfg;
+        if (correctionEval && correctionEval->kind != BVC_EVALUATOR_NONE) {
+            ev = *correctionEval;
+        } else {
+            ev.kind = BVC_EVALUATOR_WALKS;
+            ev.scene = s;
+            ev.problem = &pb;
+            ev.cfg = &cfg;
+        }
         corrected_boundary(&bc, p, r, scfg, c, cfg.clampMode, &ev, seed, bvc_dev::mixKey(kBoundaryCorrSalt, round));
         if (hasSource) {
             if (cfg.sourceBall) {
@@ -341,7 +347,7 @@ void update_round_host(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, c
                      ensure_order(P.get());
                      return P.get();
                  },
-                 seed, round, gradients, stats);
+                 seed, round, gradients, stats, nullptr);
     if (n == 0) return;
     const int d = P->dim;
     double* o = ws().get<double>(kWsEvalOut, (1 + d) * n);
@@ -389,7 +395,19 @@ int bvc_update_solution(bvc_scene s, const bvc_problem* pb, bvc_region r, const 
                         bvc_eval_points p, uint64_t seed, uint64_t round, int gradients, bvc_round_stats* stats) {
     API({
         need(s && pb && r && cfg && p, "null argument");
-        update_round(s, *pb, r, *cfg, [p]() { return p; }, seed, round, gradients, stats);
+        update_round(s, *pb, r, *cfg, [p]() { return p; }, seed, round, gradients, stats, nullptr);
+    })
+}
+
+int bvc_update_solution_with_evaluator(bvc_scene s, const bvc_problem* pb, bvc_region r,
+                                       const bvc_cache_config* cfg, bvc_eval_points p, uint64_t seed,
+                                       uint64_t round, int gradients, const bvc_boundary_evaluator* correctionEval,
+                                       bvc_round_stats* stats) {
+    API({
+        need(s && pb && r && cfg && p, "null argument");
+        if (correctionEval && correctionEval->kind == BVC_EVALUATOR_WALKS)
+            need(correctionEval->scene && correctionEval->problem && correctionEval->cfg, "walk evaluator needs scene, problem and cfg");
+        update_round(s, *pb, r, *cfg, [p]() { return p; }, seed, round, gradients, stats, correctionEval);
     })
 }
 

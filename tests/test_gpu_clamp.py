@@ -292,3 +292,36 @@ def test_update_solution_clamp_modes(mode):
         assert abs(m - 0.9) <= 4 * se, (m, se)
     else:
         assert abs(m - 0.9) > 4 * se, (m, se)
+
+
+def test_update_solution_correction_evaluator():
+    """updateSolution's correctionEval argument (cache.h:195-198, cache.cpp:646-648): an
+    explicit walk evaluator equals the empty default bit for bit (makeDefaultEvaluator,
+    cache.cpp:600-620); an exact-data evaluator (u = x on disk-linear) replaces the
+    correction walks and stays unbiased."""
+    geom, pb = H.disk_linear()
+    sc = B.Scene(*geom)
+    region = B.SolveRegion(sc, epsilon=1e-3 * sc.diagonal)
+    x = np.array([[0.9, 0.1], [0.5, -0.3]])
+    cfg = B.cache_config(clampMode=abi.CLAMP_CORRECT, clamp=0.5, nBoundary=256, nWalksNeumann=16,
+                         nWalksDirichlet=64, correctionWalks=4)
+
+    def run(ev, seed):
+        p = B.EvaluationPoints(x)
+        B.mark_evaluation_points(sc, region, cfg, p)
+        B.update_solution(sc, pb, region, cfg, p, 3000 + seed, 0, correction_eval=ev)
+        return p.download()
+
+    a, b = run(None, 0), run(B.walk_evaluator(sc, pb, cfg), 0)
+    for k in a:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+    none = abi.BoundaryEvaluator()  # kind NONE = the empty std::function = the default
+    c = run(none, 0)
+    for k in a:
+        np.testing.assert_array_equal(a[k], c[k], err_msg=k)
+    exact = B.field_evaluator(abi.make_field(abi.FIELD_LINEAR, [1, 0, 0, 0]))
+    d = run(exact, 0)
+    assert not np.array_equal(a["boundarySum"], d["boundarySum"])  # the correction used the field
+    vals = [run(exact, seed) for seed in range(48)]
+    m, se = mean_se([st["boundarySum"][0] / st["nBoundary"][0] for st in vals])
+    assert abs(m - 0.9) <= 4 * se, (m, se)
