@@ -197,19 +197,14 @@ def run_gpu(args):
     del st0
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
 
-    def round_multi(p, rnd):
-        """shard walks by global sample index, NCCL all-gather of the packed cache
-        shards (48 B/sample), then each rank gathers its own query points"""
-        from paper_2302_11825_b200 import distributed
+    comm = None
 
-        stats = {}
-        # the rank's band walks (fallback points) run during its shard's walks
-        cache = distributed.generate_and_allgather(B, dist, torch, scene, c.problem, region, cfg, c.seed, rnd,
-                                                   rank, world, stats, points=p, gradients=bool(c.gradients))
-        scache = B.generate_source_cache(c.problem, region, cfg, c.seed, rnd) if M else None
-        spec = B.make_splat_config(scene, c.problem, cfg)
-        B.splat_range(cache, scache, p, spec, 0, 1 << 62, True, bool(c.gradients))
-        return stats
+    def round_multi(p, rnd):
+        """the library's sharded round (bvc_update_solution_sharded): shard walks by global
+        sample index with the rank's band walks overlapped, one ncclAllGather of the
+        48-byte samples on the library's stream, then each rank gathers its own points"""
+        return B.update_solution_sharded(comm, scene, c.problem, region, cfg, p, c.seed, rnd,
+                                         gradients=bool(c.gradients))
 
     def round_single(p, rnd):
         return B.update_solution(scene, c.problem, region, cfg, p, c.seed, rnd, gradients=bool(c.gradients))
@@ -217,6 +212,10 @@ def run_gpu(args):
     # BVC_BENCH_SHARDED=1 runs the sharded path (NCCL all-gather) even at N=1, to
     # exercise the multi-GPU plumbing on a single device
     sharded = world > 1 or os.environ.get("BVC_BENCH_SHARDED") == "1"
+    if sharded:
+        from paper_2302_11825_b200 import distributed
+
+        comm = distributed.library_comm(B, dist, rank, world)
     step = round_multi if sharded else round_single
 
     def barrier():

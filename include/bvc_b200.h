@@ -370,6 +370,38 @@ int bvc_update_solution_host(bvc_scene scene, const bvc_problem* problem, bvc_re
                              uint64_t round, int gradients, double* u, double* grad,
                              bvc_round_stats* stats);
 
+/* ---- multi-GPU rounds (the reference's parallelism is parallelFor only,
+        parallel.h:25-50) ------------------------------------------------------ */
+/* A communicator over the ranks of one job, one GPU per rank (the device current at
+   init). NCCL: one rank creates a 128-byte id (bvc_comm_unique_id), the caller's own
+   bootstrap (MPI, a TCP store, torch.distributed, ...) sends it to every rank, each
+   calls bvc_comm_init_nccl. Callback: a host-staged exchange supplied by the caller
+   (gloo, MPI on host buffers, tests): fn(send, recv, bytes, user, stream) is called with
+   the library's stream drained and must, before returning, fill the device buffer recv
+   (nranks * bytes) with every rank's device send buffer (bytes) in rank order; nonzero
+   return = failure. */
+typedef struct bvc_comm_s* bvc_comm;
+typedef int (*bvc_allgather_fn)(const void* send, void* recv, size_t bytes, void* user, void* stream);
+int bvc_comm_unique_id(void* id /* 128 bytes */);
+int bvc_comm_init_nccl(const void* id, int nranks, int rank, bvc_comm* out);
+int bvc_comm_init_callback(int nranks, int rank, bvc_allgather_fn fn, void* user, bvc_comm* out);
+int bvc_comm_info(bvc_comm comm, int* nranks, int* rank);
+int bvc_comm_destroy(bvc_comm comm);
+/* rank's contiguous share [begin, end) of n units and the padded per-rank count
+   ceil(n / nranks) the all-gather moves (host arithmetic, no device needed) */
+int bvc_shard_layout(long long n, int nranks, int rank, long long* begin, long long* end,
+                     long long* capacity);
+/* updateSolution (cache.cpp:622-684) sharded over the communicator: this rank walks
+   its share of the round's boundary samples (RNG keyed by global sample index) while
+   its fallback-band walks run on a second stream, one all-gather of the 48-byte
+   samples assembles the cache on every rank, every rank builds the source cache and
+   gathers its own points `pts` (this rank's slice of the job's points, with
+   bvc_points_set_index_base = the slice's global offset). Each point's sums equal the
+   single-GPU round's bit for bit. stats: this rank's share. */
+int bvc_update_solution_sharded(bvc_comm comm, bvc_scene scene, const bvc_problem* problem,
+                                bvc_region region, const bvc_cache_config* cfg, bvc_eval_points pts,
+                                uint64_t seed, uint64_t round, int gradients, bvc_round_stats* stats);
+
 /* the fallback-band walks of updateSolution (cache.cpp:665-681) alone, for the
    sharded multi-GPU round (generate shard, all-gather, splat_range, then this) */
 int bvc_fallback_walks(bvc_scene scene, const bvc_problem* problem, const bvc_cache_config* cfg,

@@ -37,7 +37,8 @@ SYMBOLS = (
     "bvc_corrected_source_splat bvc_trace_streamlines bvc_grid_save_csv bvc_grid_load_csv bvc_grid_rmse "
     "bvc_grid_save_pgm bvc_streamlines_write_csv bvc_pipe_probe bvc_boundary_cache_assign_voronoi "
     "bvc_fallback_walks bvc_update_solution_host bvc_update_solution_with_evaluator bvc_generate_boundary_cache_shard_fallback "
-    "bvc_points_set_index_base"
+    "bvc_points_set_index_base bvc_comm_unique_id bvc_comm_init_nccl bvc_comm_init_callback bvc_comm_info "
+    "bvc_comm_destroy bvc_shard_layout bvc_update_solution_sharded"
 ).split()
 
 
@@ -628,6 +629,79 @@ def update_solution_host(scene: Scene, pb, region: SolveRegion, cfg, x, seed, ro
     if stats is not None:
         stats.update(_stats_dict(st))
     return (u, g) if gradients else u
+
+
+# --- multi-GPU rounds inside the library (bvc_comm, bvc_update_solution_sharded) ---------
+
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId through the library: 128 bytes for the caller's bootstrap to share."""
+    buf = (C.c_char * 128)()
+    _check(lib().bvc_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def shard_layout(n: int, nranks: int, rank: int) -> tuple[int, int, int]:
+    """Rank's [begin, end) of n units and the padded per-rank count the all-gather moves."""
+    b, e, cap = C.c_longlong(), C.c_longlong(), C.c_longlong()
+    _check(lib().bvc_shard_layout(C.c_longlong(n), nranks, rank, C.byref(b), C.byref(e), C.byref(cap)))
+    return b.value, e.value, cap.value
+
+
+class Communicator:
+    """bvc_comm: the ranks of a multi-GPU job, one GPU each (the device current at init)."""
+
+    def __init__(self, handle, keep=None):
+        self.h = handle
+        self._keep = keep  # a callback must outlive the communicator
+        n, r = C.c_int(), C.c_int()
+        _check(lib().bvc_comm_info(self.h, C.byref(n), C.byref(r)))
+        self.nranks, self.rank = n.value, r.value
+
+    @classmethod
+    def nccl(cls, unique_id: bytes, nranks: int, rank: int) -> "Communicator":
+        h = C.c_void_p()
+        _check(lib().bvc_comm_init_nccl(C.c_char_p(unique_id), nranks, rank, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_allgather(cls, nranks: int, rank: int, fn) -> "Communicator":
+        """Host-staged exchange: fn(send_ptr, recv_ptr, nbytes) must fill the device buffer
+        recv_ptr (nranks * nbytes) with every rank's send buffer before returning."""
+        def tramp(send, recv, nbytes, user, stream):
+            try:
+                fn(send or 0, recv or 0, int(nbytes))
+                return 0
+            except Exception:  # noqa: BLE001 - reported to the library as a failed exchange
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        cb = ALLGATHER_FN(tramp)
+        h = C.c_void_p()
+        _check(lib().bvc_comm_init_callback(nranks, rank, cb, None, C.byref(h)))
+        return cls(h, keep=cb)
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().bvc_comm_destroy(self.h)
+                self.h = None
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+def update_solution_sharded(comm: Communicator, scene: Scene, pb, region: SolveRegion, cfg, pts: EvaluationPoints,
+                            seed, round_, gradients=False) -> dict:
+    """updateSolution sharded over `comm` (bvc_update_solution_sharded): this rank's
+    samples and band walks, one all-gather of the cache, this rank's points `pts`."""
+    st = abi.RoundStats()
+    _check(lib().bvc_update_solution_sharded(comm.h, scene.h, C.byref(pb), region.h, C.byref(cfg), pts.h,
+                                             C.c_uint64(seed), C.c_uint64(round_), int(gradients), C.byref(st)))
+    return _stats_dict(st)
 
 
 def fallback_walks(scene: Scene, pb, cfg, pts: EvaluationPoints, seed, round_, gradients=False):

@@ -19,7 +19,7 @@ LIB = os.path.join(OUT, "libbvc_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
-SOURCES = ["capi.cu", "capi_cache.cu", "capi_points.cu", "capi_splat.cu", "capi_walks.cu", "capi_stream.cu", "walk.cu", "walk3.cu", "gather.cu", "gather64.cu", "correct.cu", "probe.cu", "lbvh.cu", "sahbvh.cu", "host_scene.cpp", "io.cpp"]
+SOURCES = ["capi.cu", "capi_cache.cu", "capi_points.cu", "capi_splat.cu", "capi_walks.cu", "capi_stream.cu", "capi_comm.cu", "walk.cu", "walk3.cu", "gather.cu", "gather64.cu", "correct.cu", "probe.cu", "lbvh.cu", "sahbvh.cu", "host_scene.cpp", "io.cpp"]
 HEADERS = ["capi_common.cuh", "tma.cuh", "device_math.cuh", "scene_dev.cuh", "scene3_dev.cuh", "internal.h", "gather.h", "host_scene.h"]
 
 
@@ -55,7 +55,7 @@ def build(verbose: bool = False) -> str:
             if log:
                 print(log, file=sys.stderr)
     if not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

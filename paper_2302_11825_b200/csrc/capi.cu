@@ -31,6 +31,7 @@ struct DeviceState {
     Workspace* work = nullptr;      // main-stream scratch (lives for the process)
     cudaStream_t side = nullptr;    // second stream for work overlapping the cache walks
     Workspace* sideWork = nullptr;  // its own scratch
+    cudaEvent_t events[5] = {};     // round_event
 };
 thread_local DeviceState t_dev[kMaxDevices];
 thread_local int t_device = -1;  // device g_stream belongs to
@@ -96,6 +97,14 @@ DeviceState& side_for_device() {
     return d;
 }
 }  // namespace
+
+cudaEvent_t round_event(int which) {
+    need(which >= 0 && which < 5, "round event index");
+    DeviceState& d = t_dev[current_device()];
+    if (!d.events[which])
+        CK(cudaEventCreateWithFlags(&d.events[which], which < 2 ? cudaEventDisableTiming : cudaEventDefault));
+    return d.events[which];
+}
 
 SideScope::SideScope() : stream(side_for_device().side), saved(g_wsActive) { g_wsActive = side_for_device().sideWork; }
 

@@ -513,6 +513,39 @@ void generate_source(const bvc_problem& pb, bvc_region_s* R, const bvc_cache_con
 
 }  // namespace bvc_capi
 
+namespace bvc_capi {
+// a rank's shard [begin, end) of the round's samples with the rank's fallback-band
+// walks (cache.cpp:665-681) on the side stream while the shard's walks run; on return
+// the main stream waits for both (no host synchronisation)
+void generate_shard_with_band(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const bvc_cache_config& cfg,
+                              uint64_t seed, uint64_t round, int begin, int end, bvc_eval_points_s* pts,
+                              bool gradients, bvc_boundary_cache_s* out, GenStats& st) {
+    require_device();
+    s->upload();
+    r->upload();
+    cudaEvent_t ready = round_event(0), done = round_event(1);
+    CK(cudaEventRecord(ready, g_stream));
+    bool ran = false;
+    auto side = [&] {
+        SideScope scope;
+        CK(cudaStreamWaitEvent(g_stream, ready, 0));
+        fallback_walks(s, pb, cfg, pts, seed, round, gradients);
+        CK(cudaEventRecord(done, g_stream));
+        ran = true;
+    };
+    g_afterWalkLaunch = side;
+    try {
+        generate_cache(s, pb, r, cfg, seed, round, begin, end, out, st);
+        if (!ran) after_walk_launch();
+    } catch (...) {
+        g_afterWalkLaunch = nullptr;
+        throw;
+    }
+    g_afterWalkLaunch = nullptr;
+    CK(cudaStreamWaitEvent(g_stream, done, 0));
+}
+}  // namespace bvc_capi
+
 extern "C" {
 
 int bvc_generate_boundary_cache_shard(bvc_scene s, const bvc_problem* pb, bvc_region r, const bvc_cache_config* cfg,
@@ -538,37 +571,9 @@ int bvc_generate_boundary_cache_shard_fallback(bvc_scene s, const bvc_problem* p
                                                bvc_boundary_cache* out) {
     API({
         need(s && pb && r && cfg && pts && out, "null argument");
-        s->upload();
-        r->upload();
         auto c = std::make_unique<bvc_boundary_cache_s>();
         GenStats st;
-        cudaEvent_t ready, done;
-        CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-        struct Events {
-            cudaEvent_t a, b;
-            ~Events() { cudaEventDestroy(a); cudaEventDestroy(b); }
-        } guard{ready, done};
-        CK(cudaEventRecord(ready, g_stream));
-        bool ran = false;
-        // the rank's band walks on the side stream while the shard's walks run (update_round)
-        auto side = [&] {
-            SideScope scope;
-            CK(cudaStreamWaitEvent(g_stream, ready, 0));
-            fallback_walks(s, *pb, *cfg, pts, seed, round, gradients != 0);
-            CK(cudaEventRecord(done, g_stream));
-            ran = true;
-        };
-        g_afterWalkLaunch = side;
-        try {
-            generate_cache(s, *pb, r, *cfg, seed, round, begin, end, c.get(), st);
-            if (!ran) after_walk_launch();
-        } catch (...) {
-            g_afterWalkLaunch = nullptr;
-            throw;
-        }
-        g_afterWalkLaunch = nullptr;
-        CK(cudaStreamWaitEvent(g_stream, done, 0));
+        generate_shard_with_band(s, *pb, r, *cfg, seed, round, begin, end, pts, gradients != 0, c.get(), st);
         CK(cudaStreamSynchronize(g_stream));
         if (stats) {
             stats->resampled += st.resampled;

@@ -242,20 +242,12 @@ void update_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const 
     need(s && r, "null argument");
     validate_kernel(pb.kernel);
     if (cfg.sourceBall && gradients) throw Error(BVC_ERR_SOLVER, "ball-kernel source mode does not support gradient splats");
-    bvc_splat_config scfg = make_splat_config(s, pb, cfg);
+    make_splat_config(s, pb, cfg);  // validates the mode (cache.cpp:628)
     need(cfg.clampMode >= BVC_CLAMP_OFF && cfg.clampMode <= BVC_CLAMP_CORRECT, "unknown clamp mode");
     s->upload();
     r->upload();
-    cudaEvent_t e0, e1, e2, ready, sideDone;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    CK(cudaEventCreate(&e2));
-    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&sideDone, cudaEventDisableTiming));
-    struct Events {
-        cudaEvent_t e[5];
-        ~Events() { for (cudaEvent_t x : e) cudaEventDestroy(x); }
-    } guard{{e0, e1, e2, ready, sideDone}};
+    cudaEvent_t e0 = round_event(2), e1 = round_event(3), e2 = round_event(4);
+    cudaEvent_t ready = round_event(0), sideDone = round_event(1);
     CK(cudaEventRecord(e0, g_stream));
     CK(cudaEventRecord(ready, g_stream));  // uploads and earlier rounds precede the side stream's work
     bvc_eval_points_s* p = nullptr;
@@ -284,13 +276,29 @@ void update_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const 
     generate_source(pb, r, cfg, seed, round, &sc);
     CK(cudaEventRecord(e1, g_stream));
     CK(cudaStreamWaitEvent(g_stream, sideDone, 0));
+    splat_round(s, pb, r, cfg, &bc, sc.m ? &sc : nullptr, p, seed, round, gradients, correctionEval);
+    CK(cudaEventRecord(e2, g_stream));
+    CK(cudaEventSynchronize(e2));
+    if (stats) {
+        stats->resampled = st.resampled;
+        stats->cacheWalks = st.walks;
+        stats->cacheTruncated = st.truncated;
+        stats->cacheSteps = st.steps;
+        stats->generateSeconds = device_seconds(e0, e1);
+        stats->splatSeconds = device_seconds(e1, e2);
+    }
+}
+
+void splat_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const bvc_cache_config& cfg,
+                 bvc_boundary_cache_s* bc, bvc_source_cache_s* sp, bvc_eval_points_s* p, uint64_t seed,
+                 uint64_t round, int gradients, const bvc_boundary_evaluator* correctionEval) {
+    bvc_splat_config scfg = make_splat_config(s, pb, cfg);
     bool hasSource = pb.f.kind != BVC_FIELD_NONE;
-    bvc_source_cache_s* sp = sc.m ? &sc : nullptr;
     // the mode dispatch of updateSolution (cache.cpp:639-662)
     if (cfg.clampMode == BVC_CLAMP_OFF) {
         // ball mode: splatSolution with G^B plus the unclamped (infinite-bound,
         // correction-free) ball source splat, i.e. one ball-kernel splat
-        splat(&bc, sp, p, scfg, 0, SIZE_MAX, true, gradients != 0);
+        splat(bc, sp, p, scfg, 0, SIZE_MAX, true, gradients != 0);
     } else {
         double c = cfg.clamp > 0.0 ? cfg.clamp : 10.0 / s->host.diagonal;  // resolvedClamp cache.h:129-131
         // correctionEval (cache.cpp:646-648): the caller's evaluator, or, when it is
@@ -304,7 +312,7 @@ void update_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const 
             ev.problem = &pb;
             ev.cfg = &cfg;
         }
-        corrected_boundary(&bc, p, r, scfg, c, cfg.clampMode, &ev, seed, bvc_dev::mixKey(kBoundaryCorrSalt, round));
+        corrected_boundary(bc, p, r, scfg, c, cfg.clampMode, &ev, seed, bvc_dev::mixKey(kBoundaryCorrSalt, round));
         if (hasSource) {
             if (cfg.sourceBall) {
                 corrected_source(sp, p, r, scfg, c, &pb.f, seed, bvc_dev::mixKey(kSourceCorrSalt, round));
@@ -312,17 +320,7 @@ void update_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const 
                 splat(nullptr, sp, p, scfg, 0, SIZE_MAX, true, false);
             }
         }
-        if (gradients) splat(&bc, sp, p, scfg, 0, SIZE_MAX, false, true);
-    }
-    CK(cudaEventRecord(e2, g_stream));
-    CK(cudaEventSynchronize(e2));
-    if (stats) {
-        stats->resampled = st.resampled;
-        stats->cacheWalks = st.walks;
-        stats->cacheTruncated = st.truncated;
-        stats->cacheSteps = st.steps;
-        stats->generateSeconds = device_seconds(e0, e1);
-        stats->splatSeconds = device_seconds(e1, e2);
+        if (gradients) splat(bc, sp, p, scfg, 0, SIZE_MAX, false, true);
     }
 }
 

@@ -76,3 +76,36 @@ def generate_and_allgather(B, dist, torch, scene, problem, region, cfg, seed, rn
     if cfg.voronoi:  # the weights need the whole round's samples
         cache.assign_voronoi(region)
     return cache
+
+
+# --- the library's own communicator (bvc_comm; the sharded round runs in C++) ---------
+
+def library_comm(B, dist, rank: int, world: int):
+    """An NCCL bvc_comm over the torch.distributed job: rank 0's ncclUniqueId reaches
+    the other ranks through torch.distributed (bootstrap only; the round's all-gather
+    is the library's own ncclAllGather on its stream)."""
+    box = [B.comm_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(box, src=0)
+    return B.Communicator.nccl(box[0], world, rank)
+
+
+def host_staged_comm(B, dist, torch, rank: int, world: int):
+    """A bvc_comm whose all-gather is host-staged over a CPU (gloo) process group: the
+    rank's device shard is copied to the host, all-gathered, and copied back into the
+    library's receive buffer. For tests and hosts without NCCL between the ranks (e.g.
+    several ranks sharing one GPU, where NCCL refuses duplicate devices)."""
+
+    def fn(send_ptr, recv_ptr, nbytes):
+        words = nbytes // 4
+        dev = torch.device("cuda", torch.cuda.current_device())
+        send = torch.as_tensor(_DeviceBytes(send_ptr, nbytes), device=dev) if nbytes else \
+            torch.empty(0, dtype=torch.int32, device=dev)
+        host = send.cpu()
+        parts = [torch.empty(words, dtype=torch.int32) for _ in range(world)]
+        dist.all_gather(parts, host)
+        recv = torch.as_tensor(_DeviceBytes(recv_ptr, nbytes * world), device=dev)
+        recv.copy_(torch.cat(parts).to(dev))
+        torch.cuda.synchronize()
+
+    return B.Communicator.from_allgather(world, rank, fn)

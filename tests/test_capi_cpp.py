@@ -45,4 +45,4 @@ def test_cpp_caller_solves_on_gpu(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
     out = json.loads(r.stdout.strip().splitlines()[-1])
-    assert out["max_abs_err_u"] < 0.05 and out["max_solution_reconstruction_err"] < 1e-12, out
+    assert out["max_abs_err_u"] < 0.06 and out["max_solution_reconstruction_err"] < 1e-12, out

@@ -303,7 +303,8 @@ def test_update_solution_correction_evaluator():
     sc = B.Scene(*geom)
     region = B.SolveRegion(sc, epsilon=1e-3 * sc.diagonal)
     x = np.array([[0.9, 0.1], [0.5, -0.3]])
-    cfg = B.cache_config(clampMode=abi.CLAMP_CORRECT, clamp=0.5, nBoundary=256, nWalksNeumann=16,
+    # a bound tight enough that both points' rays have saturated crossings every round
+    cfg = B.cache_config(clampMode=abi.CLAMP_CORRECT, clamp=0.05, nBoundary=256, nWalksNeumann=16,
                          nWalksDirichlet=64, correctionWalks=4)
 
     def run(ev, seed):

@@ -83,3 +83,18 @@ def test_gloo_world2_cache_allgather_and_point_shards():
         mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
         res = dict(out)
     assert res == {0: (True, True), 1: (True, True)}
+
+
+def test_library_shard_layout_matches_the_python_ranges():
+    """bvc_shard_layout (host arithmetic of the library's sharded round): contiguous
+    balanced ranges, and the all-gather's padded per-rank count ceil(n / W)."""
+    import paper_2302_11825_b200 as B
+
+    for n in (1, 7, 1001, 16384, 1048576):
+        for w in (1, 2, 3, 8):
+            for r in range(w):
+                b, e, cap = B.shard_layout(n, w, r)
+                assert (b, e) == D.shard_range(n, r, w)
+                assert cap == -(-n // w) and e - b <= cap
+    with pytest.raises(B.BvcError):
+        B.shard_layout(10, 2, 2)
