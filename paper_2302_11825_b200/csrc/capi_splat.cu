@@ -43,9 +43,12 @@ void splat_launch(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_point
         CK(cudaGetLastError());
         return;
     }
+    // screened 3D values gather in scaled coordinates (gather.h kScr3V): one FP32 op less per pair
+    if (kind == kScr3 && val && !grad && mode == 0) kind = kScr3V;
+    const float k = kind == kScr3V ? scr3v_scale(cfg.kernel.sigma) : 1.0f;
     float4* pack = ws().get<float4>(kWsPack, 2 * static_cast<size_t>(std::max(N + M, 1)));
-    if (N) pack_boundary(b->samples.p, N, kind, cfg.voronoi, pack, g_stream);
-    if (M) pack_source(s->samples.p, M, kind, pack + 2 * static_cast<size_t>(N), g_stream);
+    if (N) pack_boundary(b->samples.p, N, kind, cfg.voronoi, pack, g_stream, k);
+    if (M) pack_source(s->samples.p, M, kind, pack + 2 * static_cast<size_t>(N), g_stream, k);
     GatherPlan plan = plan_gather(kind, K, N, M, val, grad);
     double* part = ws().get<double>(kWsPart, std::max<size_t>(static_cast<size_t>(plan.chunksB + plan.chunksS) * plan.comps * K, 1));
     int* skipB = ws().get<int>(kWsSkipB, K);

@@ -28,8 +28,13 @@ using namespace bvc_dev;
 namespace {
 
 constexpr int kThreads = 128;
-constexpr int kQ = 4;
-constexpr int kPT = kThreads * kQ;  // points per CTA tile
+constexpr int kQ = 4;  // query points per thread (register blocking), most kinds
+// screened-3D values (C5) hold BVC_Q_SCR3 points per thread (measured, see DESIGN)
+#ifndef BVC_Q_SCR3
+#define BVC_Q_SCR3 4
+#endif
+template <int KIND, bool VAL, bool GRAD, int MODE>
+constexpr int q_of() { return (KIND == 4 && VAL && !GRAD && MODE == 0) ? BVC_Q_SCR3 : kQ; }
 constexpr int kTS = 256;            // samples per shared-memory tile
 
 // --- per-pair kernels ---------------------------------------------------------
@@ -308,6 +313,19 @@ __device__ __forceinline__ void pair(const float4 a, const float4 b, float px, f
                     acc.gz = fmaf(c, dz, acc.gz);
                 }
             }
+        } else if constexpr (KIND == kScr3V) {
+            static_assert(!GRAD && MODE == 0, "kScr3V is the value-only kind");
+            // values in coordinates scaled by k = s log2(e) (see pack_boundary_one): with
+            // r' = k r, e^{-s r} = 2^{-r'} and s + 1/r = k (ln2 + 1/r'), the k factors fold into
+            // the payload (A k^2 n, k B; source k C), so the pair needs no scale multiply
+            const float ir1 = ir;
+            const float e = f_ex2(-__fmul_rn(r2, ir1));
+            if constexpr (!SRC) {
+                float ndA = fmaf(a.w, dx, fmaf(b.x, dy, __fmul_rn(b.y, dz)));
+                acc.v = fmaf(__fmul_rn(e, ir1), fmaf(__fmul_rn(ndA, ir1), __fadd_rn(kLn2, ir1), b.w), acc.v);
+            } else {
+                acc.v = fmaf(__fmul_rn(a.w, ir1), e, acc.v);
+            }
         } else {  // screened 3D: e = exp(-s r), Q = e (s r + 1)
             float r = __fmul_rn(r2, ir);
             float t = __fmul_rn(s, r);
@@ -353,7 +371,7 @@ struct Acc2 {
 template <int KIND, bool VAL, bool GRAD, int MODE>
 struct Packed {
     static constexpr bool value =
-        MODE == 0 && (KIND == kLap2 || KIND == kLap3 || KIND == kScr2 || (KIND == kScr3 && !GRAD));
+        MODE == 0 && (KIND == kLap2 || KIND == kLap3 || KIND == kScr2 || KIND == kScr3V || (KIND == kScr3 && !GRAD));
 };
 
 // pair() on two query points at once; same operations, same rounding per lane
@@ -428,6 +446,14 @@ __device__ __forceinline__ void pair2(const float4 a, const float4 b, F2 px, F2 
                     acc.gz = fma2(c, dz, acc.gz);
                 }
             }
+        } else if constexpr (KIND == kScr3V) {  // scaled coordinates (scalar pair above)
+            F2 e = each(mul2(r2, ir), [](float x) { return f_ex2(-x); });
+            if constexpr (!SRC) {
+                F2 ndA = fma2(bc(a.w), dx, fma2(bc(b.x), dy, mul2(bc(b.y), dz)));
+                acc.v = fma2(mul2(e, ir), fma2(mul2(ndA, ir), add2(bc(kLn2), ir), bc(b.w)), acc.v);
+            } else {
+                acc.v = fma2(mul2(bc(a.w), ir), e, acc.v);
+            }
         } else {  // kScr3, values only
             F2 r = mul2(r2, ir);
             F2 e = each(mul2(r, bc(-1.44269504088896340736f * s)), [](float x) { return f_ex2(x); });
@@ -450,6 +476,7 @@ struct Params {
     int chunksB, chunksS;    // chunks over boundary / source samples
     int tiles;               // point tiles
     float sigma, s, tol, tol2;
+    float coordScale;        // kScr3V: k = s log2(e) (points, pack and tol are scaled); else 1
     double* part;            // [(chunksB + chunksS)][comps][K]
     int comps;               // 1 (value) + dim (gradient) as enabled
     int* skipB;              // [K]
@@ -479,14 +506,14 @@ __device__ void tile_slow(const float4* sm, int cnt, float px, float py, float p
     acc = Acc{0.f, 0.f, 0.f, 0.f};
     for (int j = 0; j < cnt; ++j) {
         float4 a = sm[2 * j], b = sm[2 * j + 1];
-        float dx = a.x - px, dy = a.y - py, dz = (KIND == kLap3 || KIND == kScr3) ? a.z - pz : 0.0f;
+        float dx = a.x - px, dy = a.y - py, dz = (KIND == kLap3 || KIND == kScr3 || KIND == kScr3V) ? a.z - pz : 0.0f;
         if (dx * dx + dy * dy + dz * dz < P.tol2) { ++skips; continue; }  // cache.cpp:436-440
         float mn = 0.f;
         pair<KIND, SRC, VAL, GRAD, false, MODE>(a, b, px, py, pz, P.sigma, P.s, acc, mn, mc);
     }
 }
 
-template <int KIND, bool SRC, bool VAL, bool GRAD, bool TRACK, int MODE>
+template <int KIND, bool SRC, bool VAL, bool GRAD, bool TRACK, int MODE, int kQ>
 __device__ __forceinline__ void tile_loop(const float4* S, int cnt, const float* px, const float* py, const float* pz,
                                           const Params& P, Acc* acc, float* mn, const ModeCtx* mc) {
     if constexpr (Packed<KIND, VAL, GRAD, MODE>::value) {
@@ -526,12 +553,14 @@ __device__ __forceinline__ void tile_loop(const float4* S, int cnt, const float*
 
 template <int KIND, bool VAL, bool GRAD, int MODE>
 __device__ __forceinline__ void gather_body(const Params& P) {
+    constexpr int kQ = q_of<KIND, VAL, GRAD, MODE>();
+    constexpr int kPT = kThreads * kQ;  // points per CTA tile
     __shared__ __align__(128) float4 sm[2][2 * kTS];
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ int sUnit;
     const int tid = threadIdx.x;
     const int units = P.tiles * (P.chunksB + P.chunksS);
-    constexpr bool D3 = (KIND == kLap3 || KIND == kScr3);
+    constexpr bool D3 = (KIND == kLap3 || KIND == kScr3 || KIND == kScr3V);
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -561,6 +590,11 @@ __device__ __forceinline__ void gather_body(const Params& P) {
             px[q] = ok ? P.px[P.dim * i] : 1e30f;
             py[q] = ok ? P.px[P.dim * i + 1] : 1e30f;
             pz[q] = (ok && D3) ? P.px[P.dim * i + 2] : 0.0f;
+            if constexpr (KIND == kScr3V) {  // gather coordinates (pack_boundary_one)
+                px[q] = ok ? __fmul_rn(px[q], P.coordScale) : 1e30f;
+                py[q] = ok ? __fmul_rn(py[q], P.coordScale) : 1e30f;
+                pz[q] = __fmul_rn(pz[q], P.coordScale);
+            }
         }
         double dv[kQ], dg0[kQ], dg1[kQ], dg2[kQ];
         int skips[kQ];
@@ -603,11 +637,11 @@ __device__ __forceinline__ void gather_body(const Params& P) {
             for (int q = 0; q < kQ; ++q) { acc[q] = Acc{0.f, 0.f, 0.f, 0.f}; mn[q] = 3.0e38f; }
             const float4* S = sm[st];
             if (!src) {
-                if (track) tile_loop<KIND, false, VAL, GRAD, true, MODE>(S, cnt, px, py, pz, P, acc, mn, mc);
-                else tile_loop<KIND, false, VAL, GRAD, false, MODE>(S, cnt, px, py, pz, P, acc, mn, mc);
+                if (track) tile_loop<KIND, false, VAL, GRAD, true, MODE, kQ>(S, cnt, px, py, pz, P, acc, mn, mc);
+                else tile_loop<KIND, false, VAL, GRAD, false, MODE, kQ>(S, cnt, px, py, pz, P, acc, mn, mc);
             } else {
-                if (track) tile_loop<KIND, true, VAL, GRAD, true, MODE>(S, cnt, px, py, pz, P, acc, mn, mc);
-                else tile_loop<KIND, true, VAL, GRAD, false, MODE>(S, cnt, px, py, pz, P, acc, mn, mc);
+                if (track) tile_loop<KIND, true, VAL, GRAD, true, MODE, kQ>(S, cnt, px, py, pz, P, acc, mn, mc);
+                else tile_loop<KIND, true, VAL, GRAD, false, MODE, kQ>(S, cnt, px, py, pz, P, acc, mn, mc);
             }
 #pragma unroll
             for (int q = 0; q < kQ; ++q) {
@@ -679,7 +713,7 @@ __global__ void tile_box_kernel(const float4* pack, int N, int M, int kind, floa
     float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
     for (int j = s0 + lane; j < s1; j += 32) {
         float4 a = pack[2 * j];
-        float c[3] = {a.x, a.y, (kind == kLap3 || kind == kScr3) ? a.z : 0.f};
+        float c[3] = {a.x, a.y, (kind == kLap3 || kind == kScr3 || kind == kScr3V) ? a.z : 0.f};
         for (int k = 0; k < 3; ++k) { lo[k] = fminf(lo[k], c[k]); hi[k] = fmaxf(hi[k], c[k]); }
     }
     for (int o = 16; o > 0; o >>= 1)
@@ -695,7 +729,7 @@ __global__ void tile_box_kernel(const float4* pack, int N, int M, int kind, floa
 
 // fold per-sample constants (the "pack-cache epilogue")
 __device__ __forceinline__ void pack_boundary_one(const CacheSample& s, int n, int kind, int voronoi, float4* out,
-                                                  int i) {
+                                                  int i, float k = 1.f) {
     double w = voronoi ? static_cast<double>(s.weight) * n : 1.0 / static_cast<double>(s.pdf);
     double u = s.uHat, d = s.dHat;
     const double inv2pi = 0.15915494309189533577, inv4pi = 0.07957747154594766788, ln2 = 0.69314718055994530942;
@@ -708,6 +742,13 @@ __device__ __forceinline__ void pack_boundary_one(const CacheSample& s, int n, i
     } else if (kind == kScr2) {
         a = make_float4(s.z[0], s.z[1], s.n[0], s.n[1]);
         b = make_float4(static_cast<float>(w * u * inv2pi), static_cast<float>(w * d * inv2pi), 0.f, 0.f);
+    } else if (kind == kScr3V) {  // scaled coordinates z' = k z; A k^2 in the normal, k B
+        const double kk = k;
+        double A = w * u * inv4pi * kk * kk, Bv = w * d * inv4pi * kk;
+        a = make_float4(static_cast<float>(kk * s.z[0]), static_cast<float>(kk * s.z[1]), static_cast<float>(kk * s.z[2]),
+                        static_cast<float>(A * s.n[0]));
+        b = make_float4(static_cast<float>(A * s.n[1]), static_cast<float>(A * s.n[2]), static_cast<float>(-Bv),
+                        static_cast<float>(Bv));
     } else {  // 3D: A folded into the normal, b = (A ny, A nz, -B, B)
         double A = w * u * inv4pi, Bv = w * d * inv4pi;
         a = make_float4(s.z[0], s.z[1], s.z[2], static_cast<float>(A * s.n[0]));
@@ -717,13 +758,13 @@ __device__ __forceinline__ void pack_boundary_one(const CacheSample& s, int n, i
     out[2 * i] = a;
     out[2 * i + 1] = b;
 }
-__global__ void pack_boundary_kernel(const CacheSample* cs, int n, int kind, int voronoi, float4* out) {
+__global__ void pack_boundary_kernel(const CacheSample* cs, int n, int kind, int voronoi, float4* out, float k) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    pack_boundary_one(cs[i], n, kind, voronoi, out, i);
+    pack_boundary_one(cs[i], n, kind, voronoi, out, i, k);
 }
 
-__device__ __forceinline__ void pack_source_one(const SourceSampleDev& s, int kind, float4* out, int i) {
+__device__ __forceinline__ void pack_source_one(const SourceSampleDev& s, int kind, float4* out, int i, float k = 1.f) {
     double c = static_cast<double>(s.f) / static_cast<double>(s.pdf);
     const double inv2pi = 0.15915494309189533577, inv4pi = 0.07957747154594766788, ln2 = 0.69314718055994530942;
     float4 a, b = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -733,16 +774,20 @@ __device__ __forceinline__ void pack_source_one(const SourceSampleDev& s, int ki
     } else if (kind == kScr2) {
         a = make_float4(s.y[0], s.y[1], 0.f, 0.f);
         b = make_float4(static_cast<float>(c * inv2pi), 0.f, 0.f, 0.f);
+    } else if (kind == kScr3V) {
+        const double kk = k;
+        a = make_float4(static_cast<float>(kk * s.y[0]), static_cast<float>(kk * s.y[1]), static_cast<float>(kk * s.y[2]),
+                        static_cast<float>(-c * inv4pi * kk));
     } else {
         a = make_float4(s.y[0], s.y[1], s.y[2], static_cast<float>(-c * inv4pi));
     }
     out[2 * i] = a;
     out[2 * i + 1] = b;
 }
-__global__ void pack_source_kernel(const SourceSampleDev* ss, int m, int kind, float4* out) {
+__global__ void pack_source_kernel(const SourceSampleDev* ss, int m, int kind, float4* out, float k) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
-    pack_source_one(ss[i], kind, out, i);
+    pack_source_one(ss[i], kind, out, i, k);
 }
 
 // G, dG/dx, dG/dn_y, d2G/dx dn_y through the hot loop's own pair() code with
@@ -844,7 +889,9 @@ void launch_kind(const Params& P, bool val, bool grad, int grid, cudaStream_t st
 template <int KIND>
 int occupancy(bool val, bool grad) {
     int occ = 0;
-    if constexpr (KIND == kLap2 || KIND == kLap3) {
+    if constexpr (KIND == kScr3V) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel<kScr3V, true, false>, kThreads, 0);
+    } else if constexpr (KIND == kLap2 || KIND == kLap3) {
         if (val && grad) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel8<KIND, true, true>, kThreads, 0);
         else if (val) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel8<KIND, true, false>, kThreads, 0);
         else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel8<KIND, false, true>, kThreads, 0);
@@ -860,15 +907,15 @@ inline int blocks(long long n, int t) { return static_cast<int>((n + t - 1) / t)
 
 }  // namespace
 
-void pack_boundary(const CacheSample* cs, int n, int kind, int voronoi, float4* out, cudaStream_t st) {
+void pack_boundary(const CacheSample* cs, int n, int kind, int voronoi, float4* out, cudaStream_t st, float k) {
     if (n <= 0) return;
-    pack_boundary_kernel<<<blocks(n, 256), 256, 0, st>>>(cs, n, kind, voronoi, out);
+    pack_boundary_kernel<<<blocks(n, 256), 256, 0, st>>>(cs, n, kind, voronoi, out, k);
     count_launch();
 }
 
-void pack_source(const SourceSampleDev* ss, int m, int kind, float4* out, cudaStream_t st) {
+void pack_source(const SourceSampleDev* ss, int m, int kind, float4* out, cudaStream_t st, float k) {
     if (m <= 0) return;
-    pack_source_kernel<<<blocks(m, 256), 256, 0, st>>>(ss, m, kind, out);
+    pack_source_kernel<<<blocks(m, 256), 256, 0, st>>>(ss, m, kind, out, k);
     count_launch();
 }
 
@@ -905,12 +952,14 @@ GatherPlan plan_gather(int kind, int K, int N, int M, bool val, bool grad) {
     int occ = kind == kLap2 ? occupancy<kLap2>(val, grad)
               : kind == kScr2 ? occupancy<kScr2>(val, grad)
               : kind == kLap3 ? occupancy<kLap3>(val, grad)
+              : kind == kScr3V ? occupancy<kScr3V>(true, false)
                               : occupancy<kScr3>(val, grad);
     if (const char* e = std::getenv("BVC_GATHER_OCC")) {  // co-residency experiments: CTAs per SM cap
         int v = std::atoi(e);
         if (v >= 1 && v < occ) occ = v;
     }
-    g.tiles = (K + kPT - 1) / kPT;
+    const int q = kind == kScr3V && val && !grad ? q_of<4, true, false, 0>() : kQ;
+    g.tiles = (K + kThreads * q - 1) / (kThreads * q);
     long long slots = static_cast<long long>(sms) * occ;
     // The chunk size depends only on the cache (N + M), never on K: each point's
     // sum runs over the same chunks in the same order however the points are
@@ -954,8 +1003,9 @@ void launch_gather(int kind, const GatherPlan& g, const float4* pack, int N, int
     P.tiles = g.tiles;
     P.sigma = sigma;
     P.s = sqrtf(sigma);
-    P.tol = tol;
-    P.tol2 = tol * tol;
+    P.coordScale = kind == kScr3V ? scr3v_scale(sigma) : 1.0f;  // the pack is scaled alike
+    P.tol = tol * P.coordScale;
+    P.tol2 = P.tol * P.tol;
     P.tilesB = (N + kTS - 1) / kTS;
     P.tileBox = tileBox;
     P.unitCounter = unitCounter;
@@ -990,6 +1040,7 @@ void launch_gather(int kind, const GatherPlan& g, const float4* pack, int N, int
         case kLap2: launch_kind<kLap2>(P, val, grad, g.grid, st); break;
         case kScr2: launch_kind<kScr2>(P, val, grad, g.grid, st); break;
         case kLap3: launch_kind<kLap3>(P, val, grad, g.grid, st); break;
+        case kScr3V: gather_kernel<kScr3V, true, false><<<g.grid, kThreads, 0, st>>>(P); break;
         default: launch_kind<kScr3>(P, val, grad, g.grid, st); break;
     }
     count_launch();

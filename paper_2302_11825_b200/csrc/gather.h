@@ -1,10 +1,17 @@
 // gather.h — interface of the splat (gather) kernels in gather.cu.
 #pragma once
+#include <cmath>
+
 #include "internal.h"
 
 namespace bvc_impl {
 
-enum GatherKind { kLap2 = 0, kScr2 = 1, kLap3 = 2, kScr3 = 3 };
+enum GatherKind { kLap2 = 0, kScr2 = 1, kLap3 = 2, kScr3 = 3,
+                  // screened 3D, values only (C5), evaluated in coordinates scaled by
+                  // k = sqrt(sigma) log2(e): gather-internal (pack, tile boxes, points, tolerance)
+                  kScr3V = 4 };
+// the scale of kScr3V's coordinates
+inline float scr3v_scale(double sigma) { return static_cast<float>(std::sqrt(sigma) * 1.4426950408889634074); }
 
 // device pointers of the EvaluationPoint running sums (cache.h:79-89)
 struct PointsDev {
@@ -24,8 +31,9 @@ struct GatherPlan {
 };
 
 GatherPlan plan_gather(int kind, int K, int N, int M, bool val, bool grad);
-void pack_boundary(const CacheSample* cs, int n, int kind, int voronoi, float4* out, cudaStream_t st);
-void pack_source(const SourceSampleDev* ss, int m, int kind, float4* out, cudaStream_t st);
+// k: kScr3V's coordinate scale (1 for the other kinds)
+void pack_boundary(const CacheSample* cs, int n, int kind, int voronoi, float4* out, cudaStream_t st, float k = 1.f);
+void pack_source(const SourceSampleDev* ss, int m, int kind, float4* out, cudaStream_t st, float k = 1.f);
 void eval_kernels(int kind, const double* x, const double* y, const double* n, int count, int dim, float sigma,
                   double* out, cudaStream_t st);
 void eval_bessel(int which, const double* t, int count, double* out, cudaStream_t st);
