@@ -47,14 +47,15 @@ void splat_launch(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_point
     if (kind == kScr3 && val && !grad && mode == 0) kind = kScr3V;
     const float k = kind == kScr3V ? scr3v_scale(cfg.kernel.sigma) : 1.0f;
     float4* pack = ws().get<float4>(kWsPack, 2 * static_cast<size_t>(std::max(N + M, 1)));
-    if (N) pack_boundary(b->samples.p, N, kind, cfg.voronoi, pack, g_stream, k);
-    if (M) pack_source(s->samples.p, M, kind, pack + 2 * static_cast<size_t>(N), g_stream, k);
     GatherPlan plan = plan_gather(kind, K, N, M, val, grad);
     double* part = ws().get<double>(kWsPart, std::max<size_t>(static_cast<size_t>(plan.chunksB + plan.chunksS) * plan.comps * K, 1));
     int* skipB = ws().get<int>(kWsSkipB, K);
     int* skipS = ws().get<int>(kWsSkipS, K);
-    CK(cudaMemsetAsync(skipB, 0, K * sizeof(int), g_stream));
-    CK(cudaMemsetAsync(skipS, 0, K * sizeof(int), g_stream));
+    float4* tileBox = ws().get<float4>(kWsTileBox, 2 * static_cast<size_t>((N + 255) / 256 + (M + 255) / 256 + 1));
+    unsigned* unitCtr = ws().get<unsigned>(kWsUnitCtr, 1);
+    // one launch: pack + tile boxes + zeroed skips and unit queue
+    launch_prologue(b ? b->samples.p : nullptr, N, s ? s->samples.p : nullptr, M, kind, cfg.voronoi, k, pack, tileBox,
+                    unitCtr, skipB, skipS, K, g_stream);
     float* ballRs = nullptr;
     if (mode & kModeBall) {
         ballRs = ws().get<float>(kWsBallRs, K);
@@ -63,8 +64,7 @@ void splat_launch(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_point
     if (N + M > 0)
         launch_gather(kind, plan, pack, N, M, P->xs.p + static_cast<size_t>(dim) * begin, K, dim,
                       static_cast<float>(cfg.kernel.sigma), static_cast<float>(cfg.coincidenceTol), val, grad, part,
-                      skipB, skipS, ws().get<float4>(kWsTileBox, 2 * static_cast<size_t>((N + 255) / 256 + (M + 255) / 256 + 1)),
-                      ws().get<unsigned>(kWsUnitCtr, 1), g_stream, mode, static_cast<float>(clamp), ballRs);
+                      skipB, skipS, tileBox, unitCtr, g_stream, mode, static_cast<float>(clamp), ballRs);
     else
         CK(cudaMemsetAsync(part, 0, sizeof(double), g_stream));
     if (N + M > 0)

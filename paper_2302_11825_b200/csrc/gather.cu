@@ -704,29 +704,6 @@ __global__ void __launch_bounds__(kThreads, KIND == kLap3 ? 7 : 8) gather_kernel
 }
 
 // bounding box of each 256-sample tile (one warp per tile)
-__global__ void tile_box_kernel(const float4* pack, int N, int M, int kind, float4* box) {
-    int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    int tilesB = (N + kTS - 1) / kTS, tilesS = (M + kTS - 1) / kTS;
-    if (warp >= tilesB + tilesS) return;
-    int s0 = warp < tilesB ? warp * kTS : N + (warp - tilesB) * kTS;
-    int s1 = warp < tilesB ? min(s0 + kTS, N) : min(s0 + kTS, N + M);
-    float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
-    for (int j = s0 + lane; j < s1; j += 32) {
-        float4 a = pack[2 * j];
-        float c[3] = {a.x, a.y, (kind == kLap3 || kind == kScr3 || kind == kScr3V) ? a.z : 0.f};
-        for (int k = 0; k < 3; ++k) { lo[k] = fminf(lo[k], c[k]); hi[k] = fmaxf(hi[k], c[k]); }
-    }
-    for (int o = 16; o > 0; o >>= 1)
-        for (int k = 0; k < 3; ++k) {
-            lo[k] = fminf(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
-            hi[k] = fmaxf(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
-        }
-    if (lane == 0) {
-        box[2 * warp] = make_float4(lo[0], lo[1], lo[2], 0.f);
-        box[2 * warp + 1] = make_float4(hi[0], hi[1], hi[2], 0.f);
-    }
-}
-
 // fold per-sample constants (the "pack-cache epilogue")
 __device__ __forceinline__ void pack_boundary_one(const CacheSample& s, int n, int kind, int voronoi, float4* out,
                                                   int i, float k = 1.f) {
@@ -758,11 +735,6 @@ __device__ __forceinline__ void pack_boundary_one(const CacheSample& s, int n, i
     out[2 * i] = a;
     out[2 * i + 1] = b;
 }
-__global__ void pack_boundary_kernel(const CacheSample* cs, int n, int kind, int voronoi, float4* out, float k) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    pack_boundary_one(cs[i], n, kind, voronoi, out, i, k);
-}
 
 __device__ __forceinline__ void pack_source_one(const SourceSampleDev& s, int kind, float4* out, int i, float k = 1.f) {
     double c = static_cast<double>(s.f) / static_cast<double>(s.pdf);
@@ -784,11 +756,58 @@ __device__ __forceinline__ void pack_source_one(const SourceSampleDev& s, int ki
     out[2 * i] = a;
     out[2 * i + 1] = b;
 }
-__global__ void pack_source_kernel(const SourceSampleDev* ss, int m, int kind, float4* out, float k) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= m) return;
-    pack_source_one(ss[i], kind, out, i, k);
+// The gather's prologue in one launch: pack the boundary and source samples (one CTA
+// per 256-sample shared-memory tile), each tile's coordinate box (the near-coincidence
+// test, gather_body), and zeroed skip counters and work-unit queue for the gather that
+// follows on the same stream (instead of 2 pack launches, a box launch and 3 memsets)
+__global__ void __launch_bounds__(kTS) prologue_kernel(const CacheSample* cs, int N, const SourceSampleDev* ss, int M,
+                                                        int kind, int voronoi, float k, float4* pack, float4* box,
+                                                        unsigned* unitCounter, int* skipB, int* skipS, int K) {
+    const int tilesB = (N + kTS - 1) / kTS;
+    const int t = blockIdx.x;
+    const bool src = t >= tilesB;
+    const int s0 = src ? N + (t - tilesB) * kTS : t * kTS;
+    const int s1 = src ? min(s0 + kTS, N + M) : min(s0 + kTS, N);
+    const int i = s0 + threadIdx.x;
+    const bool d3 = kind == kLap3 || kind == kScr3 || kind == kScr3V;
+    float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
+    if (i < s1) {
+        if (!src) pack_boundary_one(cs[i], N, kind, voronoi, pack, i, k);
+        else pack_source_one(ss[i - N], kind, pack + 2 * static_cast<size_t>(N), i - N, k);
+        const float4 a = pack[2 * static_cast<size_t>(i)];
+        const float c[3] = {a.x, a.y, d3 ? a.z : 0.f};
+        for (int q = 0; q < 3; ++q) lo[q] = hi[q] = c[q];
+    }
+    __shared__ float red[6][kTS / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int q = 0; q < 3; ++q)
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[q] = fminf(lo[q], __shfl_xor_sync(0xffffffffu, lo[q], o));
+            hi[q] = fmaxf(hi[q], __shfl_xor_sync(0xffffffffu, hi[q], o));
+        }
+    if (lane == 0)
+        for (int q = 0; q < 3; ++q) {
+            red[q][warp] = lo[q];
+            red[3 + q][warp] = hi[q];
+        }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kTS / 32; ++w)
+            for (int q = 0; q < 3; ++q) {
+                red[q][0] = fminf(red[q][0], red[q][w]);
+                red[3 + q][0] = fmaxf(red[3 + q][0], red[3 + q][w]);
+            }
+        box[2 * t] = make_float4(red[0][0], red[1][0], red[2][0], 0.f);
+        box[2 * t + 1] = make_float4(red[3][0], red[4][0], red[5][0], 0.f);
+    }
+    const int g = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    if (g == 0) *unitCounter = 0u;
+    for (int j = g; j < K; j += stride) {
+        skipB[j] = 0;
+        skipS[j] = 0;
+    }
 }
+
 
 // G, dG/dx, dG/dn_y, d2G/dx dn_y through the hot loop's own pair() code with
 // unit payloads (u = 1, d = 0, w = 1 for the double layer; f/pdf = 1 for G)
@@ -907,17 +926,16 @@ inline int blocks(long long n, int t) { return static_cast<int>((n + t - 1) / t)
 
 }  // namespace
 
-void pack_boundary(const CacheSample* cs, int n, int kind, int voronoi, float4* out, cudaStream_t st, float k) {
-    if (n <= 0) return;
-    pack_boundary_kernel<<<blocks(n, 256), 256, 0, st>>>(cs, n, kind, voronoi, out, k);
+
+void launch_prologue(const CacheSample* cs, int N, const SourceSampleDev* ss, int M, int kind, int voronoi, float k,
+                     float4* pack, float4* tileBox, unsigned* unitCounter, int* skipB, int* skipS, int K,
+                     cudaStream_t st) {
+    const int tiles = (N + kTS - 1) / kTS + (M + kTS - 1) / kTS;
+    if (tiles <= 0) return;
+    prologue_kernel<<<tiles, kTS, 0, st>>>(cs, N, ss, M, kind, voronoi, k, pack, tileBox, unitCounter, skipB, skipS, K);
     count_launch();
 }
 
-void pack_source(const SourceSampleDev* ss, int m, int kind, float4* out, cudaStream_t st, float k) {
-    if (m <= 0) return;
-    pack_source_kernel<<<blocks(m, 256), 256, 0, st>>>(ss, m, kind, out, k);
-    count_launch();
-}
 
 void eval_kernels(int kind, const double* x, const double* y, const double* n, int count, int dim, float sigma,
                   double* out, cudaStream_t st) {
@@ -1009,12 +1027,6 @@ void launch_gather(int kind, const GatherPlan& g, const float4* pack, int N, int
     P.tilesB = (N + kTS - 1) / kTS;
     P.tileBox = tileBox;
     P.unitCounter = unitCounter;
-    {
-        int tiles = P.tilesB + (M + kTS - 1) / kTS;
-        tile_box_kernel<<<blocks(static_cast<long long>(tiles) * 32, 256), 256, 0, st>>>(pack, N, M, kind, tileBox);
-        count_launch();
-        cudaMemsetAsync(unitCounter, 0, sizeof(unsigned), st);
-    }
     P.part = part;
     P.comps = g.comps;
     P.skipB = skipB;

@@ -31,9 +31,11 @@ struct GatherPlan {
 };
 
 GatherPlan plan_gather(int kind, int K, int N, int M, bool val, bool grad);
-// k: kScr3V's coordinate scale (1 for the other kinds)
-void pack_boundary(const CacheSample* cs, int n, int kind, int voronoi, float4* out, cudaStream_t st, float k = 1.f);
-void pack_source(const SourceSampleDev* ss, int m, int kind, float4* out, cudaStream_t st, float k = 1.f);
+// the FP32 gather's prologue (gather.cu): pack (k: kScr3V's coordinate scale, 1 for the
+// other kinds), per-tile boxes, zeroed skips and unit queue
+void launch_prologue(const CacheSample* cs, int N, const SourceSampleDev* ss, int M, int kind, int voronoi, float k,
+                     float4* pack, float4* tileBox, unsigned* unitCounter, int* skipB, int* skipS, int K,
+                     cudaStream_t st);
 void eval_kernels(int kind, const double* x, const double* y, const double* n, int count, int dim, float sigma,
                   double* out, cudaStream_t st);
 void eval_bessel(int which, const double* t, int count, double* out, cudaStream_t st);
