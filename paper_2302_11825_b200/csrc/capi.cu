@@ -326,7 +326,8 @@ void bvc_scene_s::upload3() {
 
 // Silhouette-edge records in leaf order: a star query that reaches a triangle with
 // silhouette edges reads them next to the triangle's neighbours in the same leaf,
-// without the dependent triSil -> edge-array loads (Prim3.c.w = first << 2 | count).
+// without the dependent triSil -> edge-array loads, behind a per-triangle visibility
+// pre-test (header; Prim3.c.w = float4 offset << 2 | count).
 void bvc_scene_s::build_sil_records() {
     const int n = host.ns;
     DevBuf<int> counts, offsets;
@@ -342,9 +343,9 @@ void bvc_scene_s::build_sil_records() {
     CK(cudaMemcpyAsync(&last[0], offsets.p + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, g_stream));
     CK(cudaMemcpyAsync(&last[1], counts.p + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, g_stream));
     CK(cudaStreamSynchronize(g_stream));
-    silRec.resize(4 * static_cast<size_t>(std::max(last[0] + last[1], 1)));
-    launch_sil_fill3(prims3.p, n, triSil.p, counts.p, offsets.p, sil3A.p, sil3N1.p, sil3N2.p, sil3B.p, silRec.p,
-                     g_stream);
+    silRec.resize(static_cast<size_t>(std::max(last[0] + last[1], 1)));  // float4 units
+    launch_sil_fill3(prims3.p, n, triSil.p, counts.p, offsets.p, sil3A.p, sil3N1.p, sil3N2.p, sil3B.p, triNormal.p,
+                     silRec.p, g_stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(g_stream));
 }

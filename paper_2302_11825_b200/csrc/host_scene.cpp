@@ -212,7 +212,11 @@ HostScene buildMesh3(const double* vertices, int nv, const int* tris, const int*
         s.sil3N1.insert(s.sil3N1.end(), na, na + 3);
         s.sil3N2.insert(s.sil3N2.end(), nb, nb + 3);
         s.sil3Always.push_back(always ? 1 : 0);
-        for (int t : neu) attach(t, id);
+        // one of its faces carries the edge: the leaf of every face containing the edge
+        // has a box no farther from x than the edge, so a star query that can use the
+        // edge visits that face's leaf; the other face stays a plain Neumann primitive
+        // (class 1), which star queries skip
+        attach(neu[0], id);
     }
     s.component.resize(nt);
     std::map<int, int> comp;

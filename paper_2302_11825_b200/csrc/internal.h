@@ -102,8 +102,8 @@ void launch_walk_job(const WalkEnv& env, const WalkJob& job, cudaStream_t st);
 void launch_farfield2(const SceneView2& S, const FarField& F, float* d, cudaStream_t st);
 void launch_sil_count3(const bvc_dev::Prim3* prims, int n, const int4* triSil, int* counts, cudaStream_t st);
 void launch_sil_fill3(bvc_dev::Prim3* prims, int n, const int4* triSil, const int* counts, const int* offsets,
-                      const float4* silA, const float4* silN1, const float4* silN2, const float4* silB, float4* rec,
-                      cudaStream_t st);
+                      const float4* silA, const float4* silN1, const float4* silN2, const float4* silB,
+                      const float4* triN, float4* rec, cudaStream_t st);
 void launch_hintgrid2(const SceneView2& S, const HintGrid& G, int* id, int2* entry, float rmin, cudaStream_t st);
 void launch_hintgrid3(const bvc_dev::SceneView3& S, const HintGrid& G, int* id, int2* entry, float rmin,
                       cudaStream_t st);
@@ -188,7 +188,9 @@ void launch_leaf_prims(int dim, const float4* a, const float4* b, const float4* 
 // ---------------------------------------------------------------------------
 struct WalkEnv3 {
     bvc_dev::SceneView3 S;
-    const float4* silRec;  // silhouette-edge records in leaf order (a, n1, n2, b; Prim3.c.w = first << 2 | count)
+    // silhouette-edge blocks in leaf order: per triangle a header (n_t, delta'^2) then its
+    // edge records (a, n1, n2, b); Prim3.c.w = float4 offset << 2 | edge count (walk3.cu)
+    const float4* silRec;
     const int4* triSil;   // by triangle id: up to 3 silhouette-edge slots
     const float4* silA;   // silhouette edge endpoints
     const float4* silB;

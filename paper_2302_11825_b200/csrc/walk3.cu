@@ -77,12 +77,27 @@ __device__ __forceinline__ Star3 star_query3(const WalkEnv3& E, float x, float y
                 float d2 = tri_closest(p, x, y, z, qx, qy, qz);
                 if (d2 < q.D.d2) q.D = Closest3{d2, qx, qy, qz, __float_as_int(p.a.w), i};
             } else {
-                // a silhouette no closer than the closest Dirichlet point cannot shorten
-                // R = min(dD, dS) (pointwise.cpp:136-138) nor the pruning radius
                 const int code = __float_as_int(p.c.w);
-                float d2;
-                for (int k = code >> 2, e = (code >> 2) + (code & 3); k < e; ++k)
-                    if (sil_rec_ok(E.silRec + 4 * static_cast<size_t>(k), x, y, z, fminf(q.s2, q.D.d2), d2)) q.s2 = d2;
+                const int cnt = code & 3;
+                if (cnt) {
+                    // triangle-level pre-test (sil_fill3_kernel): x strictly on one side of
+                    // both faces of every edge of this triangle => no silhouette here
+                    const float4* blk = E.silRec + (code >> 2);
+                    const float4 h = blk[0];
+                    const float ax = p.a.x - x, ay = p.a.y - y, az = p.a.z - z;
+                    const float st = fmaf(h.x, ax, fmaf(h.y, ay, h.z * az));
+                    const float bx = p.b.x - x, by = p.b.y - y, bz = p.b.z - z;
+                    const float cx = p.c.x - x, cy = p.c.y - y, cz = p.c.z - z;
+                    const float R2 = fmaxf(fmaf(ax, ax, fmaf(ay, ay, az * az)),
+                                           fmaxf(fmaf(bx, bx, fmaf(by, by, bz * bz)), fmaf(cx, cx, fmaf(cy, cy, cz * cz))));
+                    if (st * st <= h.w * R2) {
+                        // a silhouette no closer than the closest Dirichlet point cannot shorten
+                        // R = min(dD, dS) (pointwise.cpp:136-138) nor the pruning radius
+                        float d2;
+                        for (int k = 0; k < cnt; ++k)
+                            if (sil_rec_ok(blk + 1 + 4 * k, x, y, z, fminf(q.s2, q.D.d2), d2)) q.s2 = d2;
+                    }
+                }
             }
         },
         [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); }, start);
@@ -615,30 +630,53 @@ void launch_hintgrid3(const SceneView3& S, const HintGrid& G, int* id, int2* ent
     count_launch();
 }
 
+// per triangle: the float4 count of its record block (a header plus 4 per edge), or 0
 __global__ void sil_count3_kernel(const Prim3* prims, int n, const int4* triSil, int* counts) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     const int4 sl = triSil[__float_as_int(prims[j].a.w)];
-    counts[j] = (sl.x >= 0) + (sl.y >= 0) + (sl.z >= 0);
+    const int k = (sl.x >= 0) + (sl.y >= 0) + (sl.z >= 0);
+    counts[j] = k ? 1 + 4 * k : 0;
 }
-
+// A triangle's block: header (n_t, delta'^2), then its edges' records (a, n1, n2, b).
+// The header is the triangle-level visibility pre-test of star_query3: every edge of
+// the triangle has the triangle's plane through it, so s_t = n_t.(a - x) is the same for
+// all of them, and the other face's s_o = n_o.(a_e - x) differs from s_t by at most
+// |n_o - n_t| |a_e - x| <= delta R (R = the farthest vertex from x). |s_t| > delta' R
+// therefore proves every edge of the triangle invisible from x (s_t s_o > 0) without
+// reading its records. delta' = delta (1 + 1e-5) + 4e-6 covers the FP32 rounding of
+// both tests (|s| errors ~4e-7 R), so the pre-test never rejects an edge that
+// sil_rec_ok would accept; an open (always-silhouette) edge makes delta' infinite.
 __global__ void sil_fill3_kernel(Prim3* prims, int n, const int4* triSil, const int* counts, const int* offsets,
                                  const float4* silA, const float4* silN1, const float4* silN2, const float4* silB,
-                                 float4* rec) {
+                                 const float4* triN, float4* rec) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
-    const int4 sl = triSil[__float_as_int(prims[j].a.w)];
+    const int id = __float_as_int(prims[j].a.w);
+    const int4 sl = triSil[id];
     const int e[3] = {sl.x, sl.y, sl.z};
-    int k = offsets[j];
+    const int off = offsets[j];
+    int k = 0;
+    float delta = 0.f;
+    bool always = false;
     for (int r = 0; r < 3; ++r) {
         if (e[r] < 0) continue;
-        float4* o = rec + 4 * static_cast<size_t>(k++);
+        float4* o = rec + off + 1 + 4 * static_cast<size_t>(k++);
+        const float4 n1 = silN1[e[r]], n2 = silN2[e[r]];
         o[0] = silA[e[r]];
-        o[1] = silN1[e[r]];
-        o[2] = silN2[e[r]];
+        o[1] = n1;
+        o[2] = n2;
         o[3] = silB[e[r]];
+        always |= n1.w != 0.f;
+        const float dx = n1.x - n2.x, dy = n1.y - n2.y, dz = n1.z - n2.z;
+        delta = fmaxf(delta, sqrtf(dx * dx + dy * dy + dz * dz));
     }
-    prims[j].c.w = __int_as_float((offsets[j] << 2) | counts[j]);
+    if (k) {
+        const float4 nt = triN[id];
+        const float dp = fmaf(delta, 1.00001f, 4e-6f);
+        rec[off] = make_float4(nt.x, nt.y, nt.z, always ? kFInf : dp * dp);
+    }
+    prims[j].c.w = __int_as_float((off << 2) | k);
 }
 
 void launch_sil_count3(const Prim3* prims, int n, const int4* triSil, int* counts, cudaStream_t st) {
@@ -648,10 +686,11 @@ void launch_sil_count3(const Prim3* prims, int n, const int4* triSil, int* count
 }
 
 void launch_sil_fill3(Prim3* prims, int n, const int4* triSil, const int* counts, const int* offsets,
-                      const float4* silA, const float4* silN1, const float4* silN2, const float4* silB, float4* rec,
-                      cudaStream_t st) {
+                      const float4* silA, const float4* silN1, const float4* silN2, const float4* silB,
+                      const float4* triN, float4* rec, cudaStream_t st) {
     if (n <= 0) return;
-    sil_fill3_kernel<<<blocks(n, 256), 256, 0, st>>>(prims, n, triSil, counts, offsets, silA, silN1, silN2, silB, rec);
+    sil_fill3_kernel<<<blocks(n, 256), 256, 0, st>>>(prims, n, triSil, counts, offsets, silA, silN1, silN2, silB, triN,
+                                                      rec);
     count_launch();
 }
 
