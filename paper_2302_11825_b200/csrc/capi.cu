@@ -32,6 +32,7 @@ struct DeviceState {
     cudaStream_t side = nullptr;    // second stream for work overlapping the cache walks
     Workspace* sideWork = nullptr;  // its own scratch
     cudaEvent_t events[5] = {};     // round_event
+    unsigned long long* pinned = nullptr;  // GenStats::snapshot
 };
 thread_local DeviceState t_dev[kMaxDevices];
 thread_local int t_device = -1;  // device g_stream belongs to
@@ -97,6 +98,31 @@ DeviceState& side_for_device() {
     return d;
 }
 }  // namespace
+
+unsigned long long* GenStats::device_counters() {
+    if (!dev) {
+        dev = ws().get<unsigned long long>(kWsRoundCtr, 4);
+        CK(cudaMemsetAsync(dev, 0, 4 * sizeof(unsigned long long), g_stream));
+    }
+    return dev;
+}
+
+void GenStats::snapshot() {
+    if (!dev) return;
+    DeviceState& d = t_dev[current_device()];
+    if (!d.pinned) CK(cudaMallocHost(reinterpret_cast<void**>(&d.pinned), 4 * sizeof(unsigned long long)));
+    CK(cudaMemcpyAsync(d.pinned, dev, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, g_stream));
+    pinned = d.pinned;
+    dev = nullptr;
+}
+
+void GenStats::resolve() {
+    if (!pinned) return;
+    steps += static_cast<long long>(pinned[0]);
+    truncated += static_cast<long long>(pinned[1]);
+    walks += static_cast<long long>(pinned[2]);
+    pinned = nullptr;
+}
 
 cudaEvent_t round_event(int which) {
     need(which >= 0 && which < 5, "round event index");

@@ -63,18 +63,17 @@ void run_cache_walks(bvc_scene_s* S, bvc_region_s* R, const WalkEnv& E, const bv
     int* dIdx = ws().get<int>(kWsDIdx, n);
     int* cnt = ws().get<int>(kWsCount, 1);
     launch_compact(isD, n, dIdx, cnt, g_stream);
-    int nD = 0;
-    CK(cudaMemcpyAsync(&nD, cnt, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
-    CK(cudaStreamSynchronize(g_stream));
-    float2* xD = ws().get<float2>(kWsXD, std::max(nD, 1));
-    float2* nrmD = ws().get<float2>(kWsND, std::max(nD, 1));
-    float* rD = ws().get<float>(kWsRD, std::max(nD, 1));
-    long long* gidD = ws().get<long long>(kWsGidD, std::max(nD, 1));
-    launch_gather_dpoints(samples, dIdx, nD, gradR, gidBase, gid, xD, nrmD, rD, gidD, g_stream);
+    // the D points stay on the device: buffers sized for all n samples, kernels read the
+    // count (no host round trip between the compaction and the walks)
+    float2* xD = ws().get<float2>(kWsXD, n);
+    float2* nrmD = ws().get<float2>(kWsND, n);
+    float* rD = ws().get<float>(kWsRD, n);
+    long long* gidD = ws().get<long long>(kWsGidD, n);
+    launch_gather_dpoints(samples, dIdx, n, gradR, gidBase, gid, xD, nrmD, rD, gidD, g_stream, cnt);
     int nU = std::max(1, cfg.nWalksNeumann), nDw = std::max(1, cfg.nWalksDirichlet);
     int* hintU = ws().get<int>(kWsHintU, std::max(n, 1));
-    int* hintD = ws().get<int>(kWsHintD, std::max(nD, 1));
-    launch_start_hints(samples, n, R->source.p, S->cls.p, nullptr, dIdx, nD, hintU, hintD, g_stream);
+    int* hintD = ws().get<int>(kWsHintD, std::max(n, 1));
+    launch_start_hints(samples, n, R->source.p, S->cls.p, nullptr, dIdx, n, hintU, hintD, g_stream, cnt);
     WalkJob J{};
     J.hintU = hintU;
     J.hintD = hintD;
@@ -85,42 +84,38 @@ void run_cache_walks(bvc_scene_s* S, bvc_region_s* R, const WalkEnv& E, const bv
     J.gidBaseU = gidBase;
     J.outU = ws().get<float>(kWsOutU, static_cast<size_t>(n) * nU);
     J.nD = nDw;
-    J.nPtsD = nD;
+    J.nPtsD = n;         // capacity
+    J.nPtsDdev = cnt;    // count
     J.xD = xD;
     J.normalD = nrmD;
     J.radiusD = rD;
     J.gidD = gidD;
-    J.outD = ws().get<float>(kWsOutD, std::max<size_t>(static_cast<size_t>(nD) * nDw, 1));
-    auto* ctr = ws().get<unsigned long long>(kWsCounter, 3);
-    CK(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), g_stream));
+    J.outD = ws().get<float>(kWsOutD, std::max<size_t>(static_cast<size_t>(n) * nDw, 1));
+    auto* ctr = ws().get<unsigned long long>(kWsCounter, 1);
+    CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), g_stream));
     J.counter = ctr;
-    J.steps = ctr + 1;
-    J.truncTotal = ctr + 2;
+    unsigned long long* rc = st.device_counters();  // the generation's steps, truncations, walks
+    J.steps = rc;
+    J.truncTotal = rc + 1;
     if (g_profile) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         size_t slots = static_cast<size_t>(sms) * 32 * 256 * 2;
-        auto* cnt = ws().get<unsigned long long>(kWsEvalOut, slots);
-        CK(cudaMemsetAsync(cnt, 0, slots * sizeof(unsigned long long), g_stream));
+        auto* cc = ws().get<unsigned long long>(kWsEvalOut, slots);
+        CK(cudaMemsetAsync(cc, 0, slots * sizeof(unsigned long long), g_stream));
         WalkEnv Ec = E;
-        Ec.S.counts = cnt;
+        Ec.S.counts = cc;
         launch_walk_job(Ec, J, g_stream);
         std::vector<unsigned long long> h(slots);
-        CK(cudaMemcpyAsync(h.data(), cnt, slots * sizeof(unsigned long long), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaMemcpyAsync(h.data(), cc, slots * sizeof(unsigned long long), cudaMemcpyDeviceToHost, g_stream));
         CK(cudaStreamSynchronize(g_stream));
         for (size_t i = 0; i < slots; ++i) g_profileTotals[i & 1] += h[i];
     } else {
         launch_walk_job(E, J, g_stream);
     }
     after_walk_launch();
-    launch_finish_samples(samples, n, J.outU, nU, dIdx, nD, J.outD, nDw, failed, g_stream);
-    unsigned long long h[3];
-    CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, g_stream));
-    CK(cudaStreamSynchronize(g_stream));
-    st.walks += static_cast<long long>(n) * nU + static_cast<long long>(nD) * nDw;
-    st.steps += static_cast<long long>(h[1]);
-    st.truncated += static_cast<long long>(h[2]);
+    launch_finish_samples(samples, n, J.outU, nU, dIdx, n, J.outD, nDw, failed, g_stream, cnt, rc + 2);
 }
 
 __global__ void redraw_copy_kernel(const CacheSample* src, const int* idx, int n, CacheSample* dst);
@@ -183,18 +178,17 @@ void run_cache_walks3(bvc_scene_s* S, bvc_region_s* R, const WalkEnv3& E, const 
     int* dIdx = ws().get<int>(kWsDIdx, n);
     int* cnt = ws().get<int>(kWsCount, 1);
     launch_compact(isD, n, dIdx, cnt, g_stream);
-    int nD = 0;
-    CK(cudaMemcpyAsync(&nD, cnt, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
-    CK(cudaStreamSynchronize(g_stream));
-    float4* xD = ws().get<float4>(kWsXD, std::max(nD, 1));
-    float4* nrmD = ws().get<float4>(kWsND, std::max(nD, 1));
-    float* rD = ws().get<float>(kWsRD, std::max(nD, 1));
-    long long* gidD = ws().get<long long>(kWsGidD, std::max(nD, 1));
-    launch_gather_dpoints3(samples, dIdx, nD, gradR, gidBase, gid, xD, nrmD, rD, gidD, g_stream);
+    // the D points stay on the device: buffers sized for all n samples, kernels read the
+    // count (no host round trip between the compaction and the walks)
+    float4* xD = ws().get<float4>(kWsXD, n);
+    float4* nrmD = ws().get<float4>(kWsND, n);
+    float* rD = ws().get<float>(kWsRD, n);
+    long long* gidD = ws().get<long long>(kWsGidD, n);
+    launch_gather_dpoints3(samples, dIdx, n, gradR, gidBase, gid, xD, nrmD, rD, gidD, g_stream, cnt);
     int nU = std::max(1, cfg.nWalksNeumann), nDw = std::max(1, cfg.nWalksDirichlet);
     int* hintU = ws().get<int>(kWsHintU, std::max(n, 1));
-    int* hintD = ws().get<int>(kWsHintD, std::max(nD, 1));
-    launch_start_hints(samples, n, R->source.p, S->cls.p, S->leafOf.p, dIdx, nD, hintU, hintD, g_stream);
+    int* hintD = ws().get<int>(kWsHintD, std::max(n, 1));
+    launch_start_hints(samples, n, R->source.p, S->cls.p, S->leafOf.p, dIdx, n, hintU, hintD, g_stream, cnt);
     WalkJob3 J{};
     J.hintU = hintU;
     J.hintD = hintD;
@@ -205,17 +199,19 @@ void run_cache_walks3(bvc_scene_s* S, bvc_region_s* R, const WalkEnv3& E, const 
     J.gidBaseU = gidBase;
     J.outU = ws().get<float>(kWsOutU, static_cast<size_t>(n) * nU);
     J.nD = nDw;
-    J.nPtsD = nD;
+    J.nPtsD = n;         // capacity
+    J.nPtsDdev = cnt;    // count
     J.xD = xD;
     J.normalD = nrmD;
     J.radiusD = rD;
     J.gidD = gidD;
-    J.outD = ws().get<float>(kWsOutD, std::max<size_t>(static_cast<size_t>(nD) * nDw, 1));
-    auto* ctr = ws().get<unsigned long long>(kWsCounter, 3);
-    CK(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), g_stream));
+    J.outD = ws().get<float>(kWsOutD, std::max<size_t>(static_cast<size_t>(n) * nDw, 1));
+    auto* ctr = ws().get<unsigned long long>(kWsCounter, 1);
+    CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), g_stream));
     J.counter = ctr;
-    J.steps = ctr + 1;
-    J.truncTotal = ctr + 2;
+    unsigned long long* rc = st.device_counters();  // the generation's steps, truncations, walks
+    J.steps = rc;
+    J.truncTotal = rc + 1;
     if (g_profile) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
@@ -234,13 +230,7 @@ void run_cache_walks3(bvc_scene_s* S, bvc_region_s* R, const WalkEnv3& E, const 
         launch_walk_job3(E, J, g_stream);
     }
     after_walk_launch();
-    launch_finish_samples(samples, n, J.outU, nU, dIdx, nD, J.outD, nDw, failed, g_stream);
-    unsigned long long h[3];
-    CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, g_stream));
-    CK(cudaStreamSynchronize(g_stream));
-    st.walks += static_cast<long long>(n) * nU + static_cast<long long>(nD) * nDw;
-    st.steps += static_cast<long long>(h[1]);
-    st.truncated += static_cast<long long>(h[2]);
+    launch_finish_samples(samples, n, J.outU, nU, dIdx, n, J.outD, nDw, failed, g_stream, cnt, rc + 2);
 }
 
 void generate_cache3(bvc_scene_s* S, const bvc_problem& pb, bvc_region_s* R, const bvc_cache_config& cfg, uint64_t seed,
@@ -262,11 +252,20 @@ void generate_cache3(bvc_scene_s* S, const bvc_problem& pb, bvc_region_s* R, con
     WalkEnv3 E = make_env3(S, pb, cfg.walk, seed, kBoundaryWalkSalt, round);
     uint8_t* failed = ws().get<uint8_t>(kWsFailed, n);
     run_cache_walks3(S, R, E, cfg, out->samples.p, n, begin, nullptr, failed, st);
-    std::vector<uint8_t> hf(n);
-    CK(cudaMemcpyAsync(hf.data(), failed, n, cudaMemcpyDeviceToHost, g_stream));
+    // deterministic redraw of failed samples (cache.cpp:365-379): the failures are
+    // compacted on the device and the host reads one 4-byte count (the list only when
+    // it is not empty)
+    int* badIdx = ws().get<int>(kWsBadIdx, n);
+    int* badCnt = ws().get<int>(kWsBadCnt, 1);
+    launch_compact_u8(failed, n, badIdx, badCnt, g_stream);
+    int nbad = 0;
+    CK(cudaMemcpyAsync(&nbad, badCnt, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
     CK(cudaStreamSynchronize(g_stream));
-    std::vector<int> bad;
-    for (int i = 0; i < n; ++i) if (hf[i]) bad.push_back(i);
+    std::vector<int> bad(nbad);
+    if (nbad) {
+        CK(cudaMemcpyAsync(bad.data(), badIdx, nbad * sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+    }
     WalkEnv3 Er = make_env3(S, pb, cfg.walk, seed, kBoundaryRedrawSalt, round);
     for (int guard = 1; !bad.empty(); ++guard) {
         if (guard > 64) throw Error(BVC_ERR_SOLVER, "boundary cache: sample kept failing after 64 redraws");
@@ -294,6 +293,7 @@ void generate_cache3(bvc_scene_s* S, const bvc_problem& pb, bvc_region_s* R, con
         for (int j = 0; j < nb; ++j) if (hf2[j]) still.push_back(bad[j]);
         bad.swap(still);
     }
+    st.snapshot();
 }
 
 __global__ void redraw_copy_kernel(const CacheSample* src, const int* idx, int n, CacheSample* dst) {
@@ -361,13 +361,20 @@ void generate_cache(bvc_scene_s* S, const bvc_problem& pb, bvc_region_s* R, cons
     WalkEnv E = make_env(S, pb, cfg.walk, seed, kBoundaryWalkSalt, round);
     uint8_t* failed = ws().get<uint8_t>(kWsFailed, n);
     run_cache_walks(S, R, E, cfg, out->samples.p, n, begin, nullptr, failed, st);
-    // deterministic redraw of failed samples (cache.cpp:365-379): a fresh uniform
-    // position per (sample, attempt), walks keyed by the redraw salt
-    std::vector<uint8_t> hf(n);
-    CK(cudaMemcpyAsync(hf.data(), failed, n, cudaMemcpyDeviceToHost, g_stream));
+    // deterministic redraw of failed samples (cache.cpp:365-379): the failures are
+    // compacted on the device and the host reads one 4-byte count (the list only when
+    // it is not empty)
+    int* badIdx = ws().get<int>(kWsBadIdx, n);
+    int* badCnt = ws().get<int>(kWsBadCnt, 1);
+    launch_compact_u8(failed, n, badIdx, badCnt, g_stream);
+    int nbad = 0;
+    CK(cudaMemcpyAsync(&nbad, badCnt, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
     CK(cudaStreamSynchronize(g_stream));
-    std::vector<int> bad;
-    for (int i = 0; i < n; ++i) if (hf[i]) bad.push_back(i);
+    std::vector<int> bad(nbad);
+    if (nbad) {
+        CK(cudaMemcpyAsync(bad.data(), badIdx, nbad * sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+    }
     WalkEnv Er = make_env(S, pb, cfg.walk, seed, kBoundaryRedrawSalt, round);
     for (int guard = 1; !bad.empty(); ++guard) {
         if (guard > 64) throw Error(BVC_ERR_SOLVER, "boundary cache: sample kept failing after 64 redraws");
@@ -399,6 +406,7 @@ void generate_cache(bvc_scene_s* S, const bvc_problem& pb, bvc_region_s* R, cons
     // assignVoronoiWeights needs every sample of the round: a shard leaves it to the
     // caller (distributed.py assigns after the all-gather)
     if (cfg.voronoi && begin == 0 && end == N) assign_voronoi(R, out);
+    st.snapshot();
 }
 
 // RegionSampler::sample (sampling.cpp:62-108): jittered strata over the bounding
@@ -556,6 +564,8 @@ int bvc_generate_boundary_cache_shard(bvc_scene s, const bvc_problem* pb, bvc_re
         auto c = std::make_unique<bvc_boundary_cache_s>();
         GenStats st;
         generate_cache(s, *pb, r, *cfg, seed, round, begin, end, c.get(), st);
+        CK(cudaStreamSynchronize(g_stream));
+        st.resolve();
         if (stats) {
             stats->resampled += st.resampled;
             stats->cacheWalks += st.walks;
@@ -575,6 +585,7 @@ int bvc_generate_boundary_cache_shard_fallback(bvc_scene s, const bvc_problem* p
         GenStats st;
         generate_shard_with_band(s, *pb, r, *cfg, seed, round, begin, end, pts, gradients != 0, c.get(), st);
         CK(cudaStreamSynchronize(g_stream));
+        st.resolve();
         if (stats) {
             stats->resampled += st.resampled;
             stats->cacheWalks += st.walks;
@@ -739,6 +750,8 @@ int bvc_walk_traffic_profile(bvc_scene s, const bvc_problem* pb, bvc_region r, c
             throw;
         }
         g_profile = false;
+        CK(cudaStreamSynchronize(g_stream));
+        st.resolve();
         out[0] = static_cast<double>(st.steps);
         out[1] = static_cast<double>(g_profileTotals[0]);
         out[2] = static_cast<double>(g_profileTotals[1]);

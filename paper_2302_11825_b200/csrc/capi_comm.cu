@@ -140,6 +140,7 @@ void update_round_sharded(bvc_comm_s* C, bvc_scene_s* s, const bvc_problem& pb, 
     splat_round(s, pb, r, cfg, &full, sc.m ? &sc : nullptr, p, seed, round, gradients, nullptr);
     CK(cudaEventRecord(e2, g_stream));
     CK(cudaEventSynchronize(e2));
+    st.resolve();
     if (stats) {
         stats->resampled = st.resampled;
         stats->cacheWalks = st.walks;

@@ -136,7 +136,7 @@ enum Slot {
     kWsSortKeysIn, kWsSortKeysOut, kWsSortValsIn, kWsSortTemp, kWsMean, kWsSe, kWsTruncPt, kWsHost1, kWsRegion,
     kWsMean2, kWsSe2, kWsGidU, kWsSrcTmp, kWsSrcFlag, kWsEvalIn, kWsEvalOut, kWsTileBox, kWsUnitCtr,
     kWsCorrCounts, kWsCorrOffsets, kWsCorrStarts, kWsCorrGid, kWsCorrW, kWsCorrOut, kWsCorrMean, kWsCorrScan,
-    kWsCorrFlag, kWsBallRs, kWsHull, kWsXs64, kWsBounds, kWsFlag2, kWsHintU, kWsHintD, kWsCommSend, kWsCommRecv
+    kWsCorrFlag, kWsBallRs, kWsHull, kWsXs64, kWsBounds, kWsFlag2, kWsHintU, kWsHintD, kWsCommSend, kWsCommRecv, kWsRoundCtr, kWsBadIdx, kWsBadCnt
 };
 
 int fail(const std::exception& e);
@@ -193,6 +193,15 @@ int leaf_size(int dim, int ns);
 
 struct GenStats {
     long long walks = 0, truncated = 0, steps = 0, resampled = 0;
+    // The walk jobs of one generation count on the device ([steps, truncated, walks]):
+    // snapshot() enqueues one copy into pinned memory at the end of the generation and
+    // resolve() adds it once the caller has synchronised its stream anyway (no host round
+    // trip per walk job).
+    unsigned long long* dev = nullptr;
+    const volatile unsigned long long* pinned = nullptr;
+    unsigned long long* device_counters();
+    void snapshot();
+    void resolve();
 };
 
 }  // namespace bvc_capi

@@ -282,6 +282,7 @@ void update_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const 
     splat_round(s, pb, r, cfg, &bc, sc.m ? &sc : nullptr, p, seed, round, gradients, correctionEval);
     CK(cudaEventRecord(e2, g_stream));
     CK(cudaEventSynchronize(e2));
+    st.resolve();
     if (stats) {
         stats->resampled = st.resampled;
         stats->cacheWalks = st.walks;

@@ -82,6 +82,7 @@ struct WalkJob {
     int* truncU;            // per point, may be NULL
     int nD;
     int nPtsD;
+    const int* nPtsDdev;    // device count of the D points (then nPtsD is only the capacity), or NULL
     const float2* xD;       // gradient ball center
     const float2* normalD;  // NULL => vector output (wostGradient)
     const float* radiusD;   // first-ball radius
@@ -145,13 +146,19 @@ void launch_prepare_samples(const WalkEnv& env, CacheSample* samples, int n, con
                             cudaStream_t st);
 
 // gathers the D points of a cache job from their samples
+// nD: the count, or with nDdev (device count) the capacity
 void launch_gather_dpoints(const CacheSample* samples, const int* dIdx, int nD, const float* gradR,
                            long long gidBase, const long long* gid, float2* xD, float2* nD_, float* rD,
-                           long long* gidD, cudaStream_t st);
+                           long long* gidD, cudaStream_t st, const int* nDdev = nullptr);
 
-// writes uHat / dHat means into the cache samples and flags non-finite results
+// writes uHat / dHat means into the cache samples and flags non-finite results; with
+// nDdev the D-point count is read on the device (nDpts = capacity) and, with walksCtr,
+// the job's walk count n nU + nD nDw is added there
 void launch_finish_samples(CacheSample* samples, int n, const float* outU, int nU, const int* dIdx, int nDpts,
-                           const float* outD, int nD, uint8_t* failed, cudaStream_t st);
+                           const float* outD, int nD, uint8_t* failed, cudaStream_t st, const int* nDdev = nullptr,
+                           unsigned long long* walksCtr = nullptr);
+// compaction of nonzero byte flags (failed samples) into indices with a device count
+void launch_compact_u8(const uint8_t* flags, int n, int* outIdx, int* outCount, cudaStream_t st);
 
 // single-CTA stream compaction of nonzero flags; writes the count to *outCount
 void launch_compact(const int* flags, int n, int* outIdx, int* outCount, cudaStream_t st);
@@ -178,7 +185,7 @@ int build_sah_gpu(int dim, const float4* a, const float4* b, const float4* c, co
 // first-step warm starts for cache walks: the scene primitive a sample's region
 // segment came from, if Dirichlet (its distance seeds the first closest-point query)
 void launch_start_hints(const CacheSample* samples, int n, const int* source, const int* cls, const int* leafOf,
-                        const int* dIdx, int nD, int* hintU, int* hintD, cudaStream_t st);
+                        const int* dIdx, int nD, int* hintU, int* hintD, cudaStream_t st, const int* nDdev = nullptr);
 void launch_leaf_index(int dim, const void* prims, int n, int* leafOf, cudaStream_t st);
 void launch_leaf_prims(int dim, const float4* a, const float4* b, const float4* c, const int* cls, const int2* sil,
                        const int* ids, int n, void* primsOut, cudaStream_t st);
@@ -214,6 +221,7 @@ struct WalkJob3 {
     float* outU;
     int* truncU;
     int nD, nPtsD;
+    const int* nPtsDdev;  // device count of the D points (then nPtsD is only the capacity), or NULL
     const float4* xD;
     const float4* normalD;  // NULL => vector output (3 components)
     const float* radiusD;
@@ -235,14 +243,12 @@ void launch_sample_mesh(const double* cdf, int m, double total, const float4* tr
 void launch_prepare3(const WalkEnv3& env, CacheSample* samples, int n, const int* kinds, float4* startU, int* isD,
                      float* gradR, uint8_t* outside, cudaStream_t st);
 void launch_gather_dpoints3(const CacheSample* samples, const int* dIdx, int nD, const float* gradR, long long gidBase,
-                            const long long* gid, float4* xD, float4* nD_, float* rD, long long* gidD, cudaStream_t st);
+                            const long long* gid, float4* xD, float4* nD_, float* rD, long long* gidD, cudaStream_t st,
+                            const int* nDdev = nullptr);
 void launch_closest3(const bvc_dev::SceneView3& S, const double* x, int n, unsigned mask, double* point, double* dist,
                      int* tri, cudaStream_t st);
 void launch_inside3(const bvc_dev::SceneView3& S, const double* x, int n, float tol, uint8_t* out, cudaStream_t st);
 void launch_mark3(const bvc_dev::SceneView3& scene, const bvc_dev::SceneView3& region, const double* x, int n,
                   float offset, int whole, float insideTol, uint8_t* fb, uint8_t* gu, cudaStream_t st);
-// per-sample means of a 3D cache job (uHat from U walks, dHat from D samples)
-void launch_finish_samples(CacheSample* samples, int n, const float* outU, int nU, const int* dIdx, int nDpts,
-                           const float* outD, int nD, uint8_t* failed, cudaStream_t st);
 
 }  // namespace bvc_impl

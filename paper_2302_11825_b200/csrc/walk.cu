@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(kWalkThreads, MINB) walk_kernel(const WalkEnv 
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const long long nUtot = static_cast<long long>(J.nPtsU) * J.nU;
-    const long long total = nUtot + static_cast<long long>(J.nPtsD) * J.nD;
+    const long long total = nUtot + static_cast<long long>(J.nPtsDdev ? *J.nPtsDdev : J.nPtsD) * J.nD;
     long long qNext = 0, qEnd = 0;
     bool exhausted = false;
     bool active = false;
@@ -526,9 +526,9 @@ __global__ void prepare_kernel(const WalkEnv E, CacheSample* samples, int n, con
 
 __global__ void gather_dpoints_kernel(const CacheSample* samples, const int* dIdx, int nD, const float* gradR,
                                       long long gidBase, const long long* gid, float2* xD, float2* nD_, float* rD,
-                                      long long* gidD) {
+                                      long long* gidD, const int* nDdev) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= nD) return;
+    if (j >= (nDdev ? *nDdev : nD)) return;
     int i = dIdx[j];
     CacheSample s = samples[i];
     xD[j] = make_float2(s.z[0], s.z[1]);
@@ -537,10 +537,14 @@ __global__ void gather_dpoints_kernel(const CacheSample* samples, const int* dId
     gidD[j] = gid ? gid[i] : gidBase + i;
 }
 
-__global__ void finish_kernel(CacheSample* samples, int n, const float* outU, int nU, const int* dIdx, int nDpts,
-                              const float* outD, int nD, uint8_t* failed) {
+__global__ void finish_kernel(CacheSample* samples, int n, const float* outU, int nU, const int* dIdx, int nDcap,
+                              const float* outD, int nD, uint8_t* failed, const int* nDdev,
+                              unsigned long long* walksCtr) {
     int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
+    const int nDpts = nDdev ? *nDdev : nDcap;
+    if (walksCtr && warp == 0 && lane == 0)
+        atomicAdd(walksCtr, static_cast<unsigned long long>(n) * nU + static_cast<unsigned long long>(nDpts) * nD);
     if (warp >= n + nDpts) return;
     const float* v;
     int per, i;
@@ -554,6 +558,26 @@ __global__ void finish_kernel(CacheSample* samples, int n, const float* outU, in
         if (warp < n) samples[i].uHat = m; else samples[i].dHat = m;
         if (!isfinite(s)) failed[i] = 1;
     }
+}
+__global__ void compact_u8_kernel(const uint8_t* flags, int n, int* outIdx, int* outCount) {
+    __shared__ int sums[1024];
+    int tid = threadIdx.x, nt = blockDim.x;
+    int chunk = (n + nt - 1) / nt;
+    int b = tid * chunk, e = min(n, b + chunk);
+    int c = 0;
+    for (int i = b; i < e; ++i) c += flags[i] != 0;
+    sums[tid] = c;
+    __syncthreads();
+    for (int off = 1; off < nt; off <<= 1) {
+        int v = tid >= off ? sums[tid - off] : 0;
+        __syncthreads();
+        sums[tid] += v;
+        __syncthreads();
+    }
+    int pos = sums[tid] - c;
+    for (int i = b; i < e; ++i)
+        if (flags[i]) outIdx[pos++] = i;
+    if (tid == nt - 1) *outCount = sums[tid];
 }
 
 // single-CTA compaction: each thread scans a contiguous chunk
@@ -642,8 +666,10 @@ __global__ void hintgrid2_kernel(const SceneView2 S, const HintGrid G, int* id, 
 
 
 __global__ void start_hints_kernel(const CacheSample* samples, int n, const int* source, const int* cls,
-                                   const int* leafOf, const int* dIdx, int nD, int* hintU, int* hintD) {
+                                   const int* leafOf, const int* dIdx, int nD, int* hintU, int* hintD,
+                                   const int* nDdev) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (nDdev) nD = *nDdev;
     auto hint = [&](int k) {
         int seg = samples[k].segment;
         int src = source ? (seg >= 0 ? source[seg] : -1) : seg;
@@ -692,10 +718,10 @@ void launch_hintgrid2(const SceneView2& S, const HintGrid& G, int* id, int2* ent
 }
 
 void launch_start_hints(const CacheSample* samples, int n, const int* source, const int* cls, const int* leafOf,
-                        const int* dIdx, int nD, int* hintU, int* hintD, cudaStream_t st) {
+                        const int* dIdx, int nD, int* hintU, int* hintD, cudaStream_t st, const int* nDdev) {
     int m = n > nD ? n : nD;
     if (m <= 0) return;
-    start_hints_kernel<<<blocks(m, 256), 256, 0, st>>>(samples, n, source, cls, leafOf, dIdx, nD, hintU, hintD);
+    start_hints_kernel<<<blocks(m, 256), 256, 0, st>>>(samples, n, source, cls, leafOf, dIdx, nD, hintU, hintD, nDdev);
     count_launch();
 }
 void launch_leaf_index(int dim, const void* prims, int n, int* leafOf, cudaStream_t st) {
@@ -750,17 +776,25 @@ void launch_prepare_samples(const WalkEnv& env, CacheSample* samples, int n, con
 
 void launch_gather_dpoints(const CacheSample* samples, const int* dIdx, int nD, const float* gradR, long long gidBase,
                            const long long* gid, float2* xD, float2* nD_, float* rD, long long* gidD,
-                           cudaStream_t st) {
+                           cudaStream_t st, const int* nDdev) {
     if (nD <= 0) return;
-    gather_dpoints_kernel<<<blocks(nD, 256), 256, 0, st>>>(samples, dIdx, nD, gradR, gidBase, gid, xD, nD_, rD, gidD);
+    gather_dpoints_kernel<<<blocks(nD, 256), 256, 0, st>>>(samples, dIdx, nD, gradR, gidBase, gid, xD, nD_, rD, gidD,
+                                                            nDdev);
     count_launch();
 }
 
 void launch_finish_samples(CacheSample* samples, int n, const float* outU, int nU, const int* dIdx, int nDpts,
-                           const float* outD, int nD, uint8_t* failed, cudaStream_t st) {
+                           const float* outD, int nD, uint8_t* failed, cudaStream_t st, const int* nDdev,
+                           unsigned long long* walksCtr) {
     long long warps = static_cast<long long>(n) + nDpts;
     if (warps <= 0) return;
-    finish_kernel<<<blocks(warps * 32, 256), 256, 0, st>>>(samples, n, outU, nU, dIdx, nDpts, outD, nD, failed);
+    finish_kernel<<<blocks(warps * 32, 256), 256, 0, st>>>(samples, n, outU, nU, dIdx, nDpts, outD, nD, failed, nDdev,
+                                                           walksCtr);
+    count_launch();
+}
+
+void launch_compact_u8(const uint8_t* flags, int n, int* outIdx, int* outCount, cudaStream_t st) {
+    compact_u8_kernel<<<1, 1024, 0, st>>>(flags, n, outIdx, outCount);
     count_launch();
 }
 

@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(kThreads3, MINB) walk3_kernel(const WalkEnv3 E
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const long long nUtot = static_cast<long long>(J.nPtsU) * J.nU;
-    const long long total = nUtot + static_cast<long long>(J.nPtsD) * J.nD;
+    const long long total = nUtot + static_cast<long long>(J.nPtsDdev ? *J.nPtsDdev : J.nPtsD) * J.nD;
     long long qNext = 0, qEnd = 0;
     bool exhausted = false, active = false;
     Task3 t;
@@ -532,9 +532,9 @@ __global__ void prepare3_kernel(const WalkEnv3 E, CacheSample* samples, int n, c
 
 __global__ void gather_dpoints3_kernel(const CacheSample* samples, const int* dIdx, int nD, const float* gradR,
                                        long long gidBase, const long long* gid, float4* xD, float4* nD_, float* rD,
-                                       long long* gidD) {
+                                       long long* gidD, const int* nDdev) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= nD) return;
+    if (j >= (nDdev ? *nDdev : nD)) return;
     int i = dIdx[j];
     CacheSample s = samples[i];
     xD[j] = make_float4(s.z[0], s.z[1], s.z[2], 0.f);
@@ -735,9 +735,11 @@ void launch_prepare3(const WalkEnv3& env, CacheSample* samples, int n, const int
 }
 
 void launch_gather_dpoints3(const CacheSample* samples, const int* dIdx, int nD, const float* gradR, long long gidBase,
-                            const long long* gid, float4* xD, float4* nD_, float* rD, long long* gidD, cudaStream_t st) {
+                            const long long* gid, float4* xD, float4* nD_, float* rD, long long* gidD, cudaStream_t st,
+                            const int* nDdev) {
     if (nD <= 0) return;
-    gather_dpoints3_kernel<<<blocks(nD, 256), 256, 0, st>>>(samples, dIdx, nD, gradR, gidBase, gid, xD, nD_, rD, gidD);
+    gather_dpoints3_kernel<<<blocks(nD, 256), 256, 0, st>>>(samples, dIdx, nD, gradR, gidBase, gid, xD, nD_, rD, gidD,
+                                                             nDdev);
     count_launch();
 }
 
