@@ -165,6 +165,8 @@ FarField bvc_scene_s::farfield() {
     if (!(e && std::string(e) == "1") || host.hasNeumann()) return FarField{};
     if (ffBuilt) return ff;
     upload();
+    std::lock_guard<std::recursive_mutex> lk(lazyMu);
+    if (ffBuilt) return ff;
     int dim = host.dim;
     const int nLong = dim == 2 ? 1024 : 128;  // 1M / 2M vertices
     double ext = 0.0, lo[3], hi[3];
@@ -206,6 +208,8 @@ HintGrid bvc_scene_s::hintgrid() {
     if (e && std::string(e) == "0") return HintGrid{};
     if (hgBuilt) return hg;
     upload();
+    std::lock_guard<std::recursive_mutex> lk(lazyMu);
+    if (hgBuilt) return hg;
     const int dim = host.dim;
     const char* en = std::getenv("BVC_HINTGRID_N");  // vertices along the longest side
     const int nLong = en && std::atoi(en) >= 16 ? std::atoi(en) : (dim == 2 ? 1024 : 128);  // 4 / 8 MB
@@ -346,7 +350,6 @@ void bvc_scene_s::upload3() {
     leafOf.resize(std::max(host.ns, 1));  // triangle id -> leaf index (walk warm starts)
     launch_leaf_index(3, prims3.p, host.ns, leafOf.p, g_stream);
     if (!host.sil3Always.empty()) build_sil_records();
-    uploaded = true;
 }
 
 
@@ -393,10 +396,15 @@ bvc_dev::SceneView3 bvc_scene_s::view3() {
 void bvc_scene_s::upload() {
     if (uploaded) return;
     require_device();
-    if (host.dim == 3) {
-        upload3();
-        return;
-    }
+    std::lock_guard<std::recursive_mutex> lk(lazyMu);
+    if (uploaded) return;
+    if (host.dim == 3) upload3();
+    else upload2();
+    CK(cudaStreamSynchronize(g_stream));  // published to every thread and stream
+    uploaded = true;
+}
+
+void bvc_scene_s::upload2() {
     if (!build_on_gpu()) {
         bvh = bvc_host::buildBvh(host, leaf_size(2, host.ns));
         size_t nn = bvh.children.size() / 2;
@@ -472,7 +480,6 @@ void bvc_scene_s::upload() {
     total = run;
     cdf.upload(hc.data(), hc.size());
     cdfIds.upload(hid.data(), hid.size());
-    uploaded = true;
 }
 
 

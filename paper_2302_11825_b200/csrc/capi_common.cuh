@@ -16,7 +16,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -214,7 +216,11 @@ using namespace bvc_capi;
 struct bvc_scene_s {
     bvc_host::HostScene host;
     bvc_host::HostBvh bvh;
-    bool uploaded = false;
+    // lazy device state (upload, hint grid, far field) is built once, under lazyMu, and
+    // published only after its stream has finished: any host thread and stream may then
+    // read it (the flags are atomics, set after the data)
+    std::recursive_mutex lazyMu;
+    std::atomic<bool> uploaded{false};
     DevBuf<Node2> nodes;
     DevBuf<Prim2> prims;
     DevBuf<float2> segNormal, silP;
@@ -241,13 +247,13 @@ struct bvc_scene_s {
     // (C2 +17%) and is not applied to Neumann scenes.
     DevBuf<float> ffGrid;
     FarField ff{};
-    bool ffBuilt = false;
+    std::atomic<bool> ffBuilt{false};
     FarField farfield();
     // warm-start grid (HintGrid, internal.h), built on first walk use
     DevBuf<int> hgIds;
     DevBuf<int2> hgEntry;
     HintGrid hg{};
-    bool hgBuilt = false;
+    std::atomic<bool> hgBuilt{false};
     HintGrid hintgrid();
 
     // per primitive id: class (host_scene.h primClass; also the GPU build input) and,
@@ -264,6 +270,7 @@ struct bvc_scene_s {
     bool build_on_gpu() const { return builder() != "host"; }
     void gpu_build(int dim, const float4* a, const float4* b, const float4* c, const int2* sil);
 
+    void upload2();
     void upload3();
     void build_sil_records();
     bvc_dev::SceneView3 view3();
@@ -276,12 +283,17 @@ struct bvc_region_s {
     bvc_host::HostRegion host;
     bvc_scene_s boundary;
     DevBuf<int> kinds, source;
+    std::mutex mu;
+    std::atomic<bool> up{false};
     void upload() {
         boundary.upload();
-        if (!kinds.n) {
-            kinds.upload(host.kinds.data(), host.kinds.size());
-            source.upload(host.source.data(), host.source.size());
-        }
+        if (up) return;
+        std::lock_guard<std::mutex> lk(mu);
+        if (up) return;
+        kinds.upload(host.kinds.data(), host.kinds.size());
+        source.upload(host.source.data(), host.source.size());
+        CK(cudaStreamSynchronize(g_stream));  // published to every thread and stream
+        up = true;
     }
 };
 

@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 import paper_2302_11825_b200 as B
+from tests import helpers as H
 from paper_2302_11825_b200 import abi, configs
 
 pytestmark = pytest.mark.gpu
@@ -95,3 +96,48 @@ def test_shard_with_fallback_equals_separate_calls():
     assert sa["fallback"].sum() > 0
     for k in ("walkSum", "walkCount", "gradientWalkSum", "gradientWalkCount"):
         np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
+
+
+def test_two_host_threads_run_rounds_concurrently():
+    """Runtime state is per host thread and per device (capi.cu): two threads on their own
+    streams run rounds at the same time and get exactly the sequential results."""
+    import threading
+
+    import torch
+
+    geom, pb = H.square_mixed()
+    sc = B.Scene(*geom)
+    region = B.SolveRegion(sc, offset=0.02, epsilon=1e-3 * sc.diagonal)
+    cfg = B.cache_config(nBoundary=2048, nWalksNeumann=32, nWalksDirichlet=64, offset=0.02)
+    rng = np.random.default_rng(3)
+    xs = [rng.uniform(0.01, 0.99, (4000, 2)) for _ in range(2)]
+
+    def run(x, seed, out, key, stream=None, scene=None, reg=None):
+        scene, reg = scene or sc, reg or region
+        if stream is not None:
+            B.set_stream(stream.cuda_stream)
+        p = B.EvaluationPoints(x)
+        B.mark_evaluation_points(scene, reg, cfg, p)
+        for r in range(2):
+            B.update_solution(scene, pb, reg, cfg, p, seed, r, gradients=True)
+        out[key] = p.download()
+        if stream is not None:
+            B.synchronize()
+            B.set_stream(None)
+
+    seq = {}
+    for k in range(2):
+        run(xs[k], 100 + k, seq, k)
+    # a fresh scene and region: both threads race for its lazy device state (upload, hint grid)
+    sc2 = B.Scene(*geom)
+    region2 = B.SolveRegion(sc2, offset=0.02, epsilon=1e-3 * sc2.diagonal)
+    par = {}
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    th = [threading.Thread(target=run, args=(xs[k], 100 + k, par, k, streams[k], sc2, region2)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for k in range(2):
+        for name, v in seq[k].items():
+            assert np.array_equal(np.asarray(par[k][name]), np.asarray(v), equal_nan=True), (k, name)
