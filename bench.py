@@ -432,7 +432,7 @@ def e2e_measure(B, c, scene, region, points, args, world, t_step):
     import torch
 
     times = []
-    reps = max(2, min(args.steps, 5)) if t_step < 1.0 else 2
+    reps = max(2, min(args.steps, 5)) if t_step < 1.0 else 3
     # pinned host buffers for the step's input points and its u / grad u results
     src = torch.from_numpy(np.ascontiguousarray(points, dtype=np.float64)).pin_memory().numpy()
     u_out = torch.empty(len(points), dtype=torch.float64).pin_memory().numpy()
@@ -457,7 +457,8 @@ def e2e_measure(B, c, scene, region, points, args, world, t_step):
     t = float(np.mean(times))
     d2h = len(points) * 8 * (1 + (c.dim if c.gradients else 0))
     return {"value": k_active * world * (N + M) / t, "unit": "interactions/s", "ms_per_step": t * 1e3,
-            "ms_min": min(times) * 1e3, "ms_max": max(times) * 1e3, "calls": len(times),
+            "ms_min": min(times) * 1e3, "ms_median": float(np.median(times)) * 1e3, "ms_max": max(times) * 1e3,
+            "calls": len(times),
             "h2d_bytes_per_step": int(points.size * 8), "d2h_bytes_per_step": int(d2h),
             "note": "wall clock per bvc_update_solution_host call from pinned host buffers: point upload (H2D) and "
                     "classification (overlapping the cache walks on a second stream), one round, u/grad-u readout "
