@@ -87,12 +87,24 @@ def test_bvh_queries_vs_reference(golden, k):
         t, seg, _, _ = sc.intersect_ray(q, d, np.inf, filt, 0.0)
         rt, rseg = g[f"s{k}_ray{filt}_t"], g[f"s{k}_ray{filt}_seg"]
         hit = rseg >= 0
-        assert np.mean((seg >= 0) == hit) > 0.995
+        # hit/miss and the hit segment agree exactly, except for rays that pass within
+        # 1e-5 diag of a vertex (the FP32 watertight endpoint tests and the reference's
+        # FP64 parametric test may then pick the other neighbour, or graze past)
+        v, sg = g[f"s{k}_v"], g[f"s{k}_s"]
+        used = np.unique(sg[(g[f"s{k}_lab"] == 1) if filt == abi.FILTER_NEUMANN else slice(None)].ravel())
+        bad = np.nonzero(((seg >= 0) != hit) | (hit & (seg >= 0) & (seg != rseg)))[0]
+        for i in bad:
+            w = v[used] - q[i]
+            dd = d[i] / np.linalg.norm(d[i])
+            tt = np.maximum(w @ dd, 0.0)
+            gap = np.min(np.linalg.norm(w - tt[:, None] * dd[None, :], axis=1))
+            assert gap <= 1e-5 * sc.diagonal, (filt, i, gap)
+        assert len(bad) <= max(2, 0.005 * len(q))
         both = hit & (seg >= 0)
         np.testing.assert_allclose(t[both], rt[both], atol=tol, rtol=1e-5)
     ins = sc.inside(q)
     _, dany, _, _ = sc.closest_point(q, abi.FILTER_ANY)
-    clear = dany > 1e-5
+    clear = dany > 1e-6 * sc.diagonal  # FP32 parity decisions differ only at the boundary itself
     assert np.array_equal(ins[clear], g[f"s{k}_inside"][clear])
 
 

@@ -1,8 +1,8 @@
 """Walk estimators on the GPU (pointwise.cpp:125-288): statistical parity with the
 reference at the same points and with the closed forms. The RNG differs (Philox vs
 xoshiro256++), so parity is |z| = |m_gpu - m_ref| / sqrt(se_gpu^2 + se_ref^2) below
-a threshold (BASELINE.json: |z| < 3 per sample mean; a single fixed-seed test uses 4
-to keep the suite's false-failure rate negligible)."""
+a threshold: BASELINE.json's |z| < 3 per sample mean. The seeds are fixed, so each
+check is deterministic (Philox streams keyed by seed and walk index).""" 
 import numpy as np
 import pytest
 
@@ -12,7 +12,7 @@ from paper_2302_11825_b200 import abi
 from tests import helpers as H
 
 pytestmark = pytest.mark.gpu
-Z = 4.0
+Z = 3.0
 
 
 def _scene(geom):
