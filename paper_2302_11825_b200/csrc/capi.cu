@@ -259,6 +259,53 @@ std::string bvc_scene_s::builder() const {
 }
 
 
+namespace {
+// Node order for the traversals' caches. The device builders number nodes in the order
+// their CTAs finish (atomic counters), so a node's two children land anywhere in the
+// array. This relayout numbers them depth first with each node's children in one
+// adjacent pair, the pair starting at an even index: for 64-byte 3D nodes a sibling pair
+// is one 128-byte line, so the sibling a traversal pops later was fetched with the child
+// it descended into, and root-to-leaf paths run forward through memory. Leaf references
+// (primitive ranges) are unchanged; the root stays at 0 (index 1 is padding).
+template <class Node, class GetL, class GetR, class Set>
+void relayout_pairs(DevBuf<Node>& buf, size_t nn, GetL left, GetR right, Set setLinks) {
+    if (nn < 3) return;
+    std::vector<Node> h(nn);
+    buf.download(h.data(), nn);
+    CK(cudaStreamSynchronize(g_stream));
+    std::vector<int> newId(nn, -1), order;  // order[new] = old
+    order.reserve(2 * nn + 2);
+    newId[0] = 0;
+    order.push_back(0);
+    order.push_back(-1);  // padding: pairs start at even indices
+    std::vector<int> stack{0};
+    while (!stack.empty()) {
+        int o = stack.back();
+        stack.pop_back();
+        int l = left(h[o]), r = right(h[o]);
+        int base = static_cast<int>(order.size());
+        order.push_back(l >= 0 ? l : -1);
+        order.push_back(r >= 0 ? r : -1);
+        if (l >= 0) newId[l] = base;
+        if (r >= 0) newId[r] = base + 1;
+        if (r >= 0) stack.push_back(r);  // left subtree first (it is popped first)
+        if (l >= 0) stack.push_back(l);
+    }
+    std::vector<Node> out(order.size());
+    for (size_t k = 0; k < order.size(); ++k) {
+        if (order[k] < 0) {
+            std::memset(&out[k], 0, sizeof(Node));
+            continue;
+        }
+        Node nd = h[order[k]];
+        int l = left(nd), r = right(nd);
+        setLinks(nd, l >= 0 ? newId[l] : l, r >= 0 ? newId[r] : r);
+        out[k] = nd;
+    }
+    buf.upload(out.data(), out.size());
+}
+}  // namespace
+
 void bvc_scene_s::gpu_build(int dim, const float4* a, const float4* b, const float4* c, const int2* sil) {
     int n = host.ns, leaf = leaf_size(dim, n);
     double pad = 9.5367431640625e-7 * std::max(host.diagonal, 1e-30);
@@ -282,6 +329,16 @@ void bvc_scene_s::gpu_build(int dim, const float4* a, const float4* b, const flo
     if (h < 0 || h >= 47)  // deeper than the device traversal stack
         throw Error(BVC_ERR_SOLVER, "GPU BVH build: tree deeper than the traversal stack; use BVC_BVH=host");
     bvhHeight = h;
+    const char* rl = std::getenv("BVC_RELAYOUT");  // measurement knob: 0 keeps the builder's order
+    if (!(rl && std::string(rl) == "0")) {
+        if (dim == 3)
+            relayout_pairs(nodes3, nn, [](const bvc_dev::Node3& x) { return x.left(); },
+                           [](const bvc_dev::Node3& x) { return x.right(); },
+                           [](bvc_dev::Node3& x, int l, int r) { x.set_links(l, r, x.mask()); });
+        else
+            relayout_pairs(nodes, nn, [](const Node2& x) { return x.left; }, [](const Node2& x) { return x.right; },
+                           [](Node2& x, int l, int r) { x.left = l; x.right = r; });
+    }
 }
 
 
