@@ -987,11 +987,15 @@ GatherPlan plan_gather(int kind, int K, int N, int M, bool val, bool grad) {
     // block scheduler does not always place every slot at once.
     int total = N + M;
     int maxTiles = (total + kTS - 1) / kTS;
-    static const int nChunks = [] {  // BVC_GATHER_CHUNKS: sweep knob (default 16)
+    static const int knob = [] {  // BVC_GATHER_CHUNKS: sweep knob (0 = the default below)
         const char* e = std::getenv("BVC_GATHER_CHUNKS");
-        int v = e ? std::atoi(e) : 16;
-        return v >= 1 && v <= 1024 ? v : 16;
+        int v = e ? std::atoi(e) : 0;
+        return v >= 1 && v <= 1024 ? v : 0;
     }();
+    // Caches of 2^19+ samples (C5) take 4 chunks: their units are plentiful at any useful
+    // K, and every chunk costs an FP64 partial per point (C5: 16 chunks wrote 2.1 GB of
+    // partials per round, 4 write 0.53 GB). Still a function of the cache size only.
+    const int nChunks = knob ? knob : (total >= (1 << 19) ? 4 : 16);
     int ct = maxTiles > nChunks ? (maxTiles + nChunks - 1) / nChunks : 1;
     g.chunk = ct * kTS;
     g.chunksB = (N + g.chunk - 1) / g.chunk;
