@@ -276,15 +276,17 @@ def run_gpu(args):
     if "shell_triangles" in c.extra:
         out["counts"]["shell_triangles"] = c.extra["shell_triangles"]
     out["clocks"] = clk.summary()
+    # e2e on every rank (the sharded host-buffer round is collective); rank 0 reports the
+    # slowest rank's call time over the whole job's interactions
+    e2e = e2e_measure(B, c, scene, region, my_points, args, world, t_step, comm=comm if sharded else None,
+                      index_base=lo_p, k_active_all=k_active_all, dist=dist)
     if rank == 0:
         # phase times measured live inside the timed steps: the round's own CUDA events on
         # the library stream (RoundStats generateSeconds / splatSeconds)
-        live = None
-        if not sharded:
-            live = {"cache_generation": float(np.mean([s["generateSeconds"] for s in per_step])),
-                    "gather": float(np.mean([s["splatSeconds"] for s in per_step]))}
+        live = {"cache_generation": float(np.mean([s["generateSeconds"] for s in per_step])),
+                "gather": float(np.mean([s["splatSeconds"] for s in per_step]))}
         out.update(phase_breakdown(B, c, scene, region, pts, args, per_step[-1], live, k_active))
-        out["e2e"] = e2e_measure(B, c, scene, region, my_points, args, world, t_step)
+        out["e2e"] = e2e
         if world == 1 and not args.no_cpu:
             out["cpu_baseline"] = cpu_baseline(c, args.cpu_sample_s)
         print(json.dumps(out), flush=True)
@@ -427,8 +429,11 @@ def phase_breakdown(B, c, scene, region, pts, args, stats, live, k_active):
     }
 
 
-def e2e_measure(B, c, scene, region, points, args, world, t_step):
-    """Public API with host buffers: H2D points, one round, D2H of u (and grad u)."""
+def e2e_measure(B, c, scene, region, points, args, world, t_step, comm=None, index_base=0, k_active_all=None,
+                dist=None):
+    """Public API with host buffers: H2D points, one round, D2H of u (and grad u). With a
+    communicator (N > 1, or BVC_BENCH_SHARDED) the sharded host-buffer round: this rank's
+    points, its share of the walks, the all-gather, its gather."""
     import torch
 
     times = []
@@ -443,26 +448,36 @@ def e2e_measure(B, c, scene, region, points, args, world, t_step):
         # one call (runSolveInMemory's round): H2D of the points from pinned memory,
         # classification, the round, D2H of u and grad u into pinned memory; the
         # upload and classification overlap the cache walks (second stream)
-        res = B.update_solution_host(scene, c.problem, region, c.cache, src, c.seed, 500 + k,
-                                     gradients=bool(c.gradients), out=(u_out, g_out))
+        if comm is not None:
+            res = B.update_solution_sharded_host(comm, scene, c.problem, region, c.cache, src, index_base, c.seed,
+                                                 500 + k, gradients=bool(c.gradients), out=(u_out, g_out))
+        else:
+            res = B.update_solution_host(scene, c.problem, region, c.cache, src, c.seed, 500 + k,
+                                         gradients=bool(c.gradients), out=(u_out, g_out))
         torch.cuda.synchronize()
         if k:
             times.append(time.perf_counter() - t0)
         u = res[0] if c.gradients else res
         assert np.all(np.isfinite(u))
     N, M = c.cache.nBoundary, (c.cache.nSource if c.problem.f.kind else 0)
-    pts = B.EvaluationPoints(src, c.dim)
-    B.mark_evaluation_points(scene, region, c.cache, pts)
-    k_active = int((~pts.download()["fallback"]).sum())
+    if k_active_all is None:
+        pts = B.EvaluationPoints(src, c.dim)
+        B.mark_evaluation_points(scene, region, c.cache, pts)
+        k_active_all = int((~pts.download()["fallback"]).sum())
     t = float(np.mean(times))
+    if dist is not None:  # the job's call time is the slowest rank's
+        tt = torch.tensor([t], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
     d2h = len(points) * 8 * (1 + (c.dim if c.gradients else 0))
-    return {"value": k_active * world * (N + M) / t, "unit": "interactions/s", "ms_per_step": t * 1e3,
+    return {"value": k_active_all * (N + M) / t, "unit": "interactions/s", "ms_per_step": t * 1e3,
             "ms_min": min(times) * 1e3, "ms_median": float(np.median(times)) * 1e3, "ms_max": max(times) * 1e3,
             "calls": len(times),
             "h2d_bytes_per_step": int(points.size * 8), "d2h_bytes_per_step": int(d2h),
-            "note": "wall clock per bvc_update_solution_host call from pinned host buffers: point upload (H2D) and "
-                    "classification (overlapping the cache walks on a second stream), one round, u/grad-u readout "
-                    "(D2H); no L2 flush between calls"}
+            "note": "wall clock per bvc_update_solution_host call (bvc_update_solution_sharded_host per rank for "
+                    "N > 1, max over ranks) from pinned host buffers: point upload (H2D) and classification "
+                    "(overlapping the cache walks on a second stream), one round, u/grad-u readout (D2H), per rank's "
+                    "points; no L2 flush between calls"}
 
 
 _ACTIVE = {}  # the reference's non-fallback query points per config object (computed once)

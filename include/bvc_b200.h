@@ -401,6 +401,14 @@ int bvc_shard_layout(long long n, int nranks, int rank, long long* begin, long l
 int bvc_update_solution_sharded(bvc_comm comm, bvc_scene scene, const bvc_problem* problem,
                                 bvc_region region, const bvc_cache_config* cfg, bvc_eval_points pts,
                                 uint64_t seed, uint64_t round, int gradients, bvc_round_stats* stats);
+/* the same on host buffers (bvc_update_solution_host's sharded form): x = this rank's n
+   points (global indices indexBase ...), u (n) and grad (n x dim, optional) receive
+   their solution() / gradient(); the upload and classification run under the shard's
+   walks */
+int bvc_update_solution_sharded_host(bvc_comm comm, bvc_scene scene, const bvc_problem* problem,
+                                     bvc_region region, const bvc_cache_config* cfg, const double* x,
+                                     size_t n, long long indexBase, uint64_t seed, uint64_t round,
+                                     int gradients, double* u, double* grad, bvc_round_stats* stats);
 
 /* the fallback-band walks of updateSolution (cache.cpp:665-681) alone, for the
    sharded multi-GPU round (generate shard, all-gather, splat_range, then this) */

@@ -38,7 +38,7 @@ SYMBOLS = (
     "bvc_grid_save_pgm bvc_streamlines_write_csv bvc_pipe_probe bvc_boundary_cache_assign_voronoi "
     "bvc_fallback_walks bvc_update_solution_host bvc_update_solution_with_evaluator bvc_generate_boundary_cache_shard_fallback "
     "bvc_points_set_index_base bvc_comm_unique_id bvc_comm_init_nccl bvc_comm_init_callback bvc_comm_info "
-    "bvc_comm_destroy bvc_shard_layout bvc_update_solution_sharded"
+    "bvc_comm_destroy bvc_shard_layout bvc_update_solution_sharded bvc_update_solution_sharded_host"
 ).split()
 
 
@@ -702,6 +702,27 @@ def update_solution_sharded(comm: Communicator, scene: Scene, pb, region: SolveR
     _check(lib().bvc_update_solution_sharded(comm.h, scene.h, C.byref(pb), region.h, C.byref(cfg), pts.h,
                                              C.c_uint64(seed), C.c_uint64(round_), int(gradients), C.byref(st)))
     return _stats_dict(st)
+
+
+def update_solution_sharded_host(comm: Communicator, scene: Scene, pb, region: SolveRegion, cfg, x, index_base, seed,
+                                 round_, gradients=False, out=None, stats=None):
+    """The sharded round on host buffers (bvc_update_solution_sharded_host): x = this
+    rank's points (global indices index_base ...); returns u or (u, grad)."""
+    x = _f64(x, scene.dim)
+    n = len(x)
+    if out is not None:
+        u, g = out
+    else:
+        u = np.zeros(n)
+        g = np.zeros((n, scene.dim)) if gradients else None
+    st = abi.RoundStats()
+    _check(lib().bvc_update_solution_sharded_host(comm.h, scene.h, C.byref(pb), region.h, C.byref(cfg), _ptr(x),
+                                                  C.c_size_t(n), C.c_longlong(index_base), C.c_uint64(seed),
+                                                  C.c_uint64(round_), int(gradients), _ptr(u),
+                                                  _ptr(g) if g is not None else None, C.byref(st)))
+    if stats is not None:
+        stats.update(_stats_dict(st))
+    return (u, g) if gradients else u
 
 
 def fallback_walks(scene: Scene, pb, cfg, pts: EvaluationPoints, seed, round_, gradients=False):

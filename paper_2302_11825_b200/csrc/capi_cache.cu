@@ -524,20 +524,26 @@ void generate_source(const bvc_problem& pb, bvc_region_s* R, const bvc_cache_con
 namespace bvc_capi {
 // a rank's shard [begin, end) of the round's samples with the rank's fallback-band
 // walks (cache.cpp:665-681) on the side stream while the shard's walks run; on return
-// the main stream waits for both (no host synchronisation)
-void generate_shard_with_band(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const bvc_cache_config& cfg,
-                              uint64_t seed, uint64_t round, int begin, int end, bvc_eval_points_s* pts,
-                              bool gradients, bvc_boundary_cache_s* out, GenStats& st) {
+// the main stream waits for both (no host synchronisation). `points` runs on the side
+// stream (it may build the points there, as the host-buffer rounds do) and its result
+// is returned.
+bvc_eval_points_s* generate_shard_with_band(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r,
+                                           const bvc_cache_config& cfg, uint64_t seed, uint64_t round, int begin,
+                                           int end, const std::function<bvc_eval_points_s*()>& points,
+                                           bool gradients, bvc_boundary_cache_s* out, GenStats& st) {
     require_device();
     s->upload();
     r->upload();
     cudaEvent_t ready = round_event(0), done = round_event(1);
     CK(cudaEventRecord(ready, g_stream));
     bool ran = false;
+    bvc_eval_points_s* p = nullptr;
     auto side = [&] {
         SideScope scope;
         CK(cudaStreamWaitEvent(g_stream, ready, 0));
-        fallback_walks(s, pb, cfg, pts, seed, round, gradients);
+        p = points();
+        need(p != nullptr, "null evaluation points");
+        fallback_walks(s, pb, cfg, p, seed, round, gradients);
         CK(cudaEventRecord(done, g_stream));
         ran = true;
     };
@@ -551,6 +557,7 @@ void generate_shard_with_band(bvc_scene_s* s, const bvc_problem& pb, bvc_region_
     }
     g_afterWalkLaunch = nullptr;
     CK(cudaStreamWaitEvent(g_stream, done, 0));
+    return p;
 }
 }  // namespace bvc_capi
 
@@ -583,7 +590,8 @@ int bvc_generate_boundary_cache_shard_fallback(bvc_scene s, const bvc_problem* p
         need(s && pb && r && cfg && pts && out, "null argument");
         auto c = std::make_unique<bvc_boundary_cache_s>();
         GenStats st;
-        generate_shard_with_band(s, *pb, r, *cfg, seed, round, begin, end, pts, gradients != 0, c.get(), st);
+        generate_shard_with_band(s, *pb, r, *cfg, seed, round, begin, end, [pts]() { return pts; }, gradients != 0,
+                                 c.get(), st);
         CK(cudaStreamSynchronize(g_stream));
         st.resolve();
         if (stats) {

@@ -92,11 +92,12 @@ void shard_layout(long long n, int nranks, int rank, long long& begin, long long
 }
 
 // one updateSolution round sharded over the communicator's ranks (see the file comment)
-void update_round_sharded(bvc_comm_s* C, bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r,
-                          const bvc_cache_config& cfg, bvc_eval_points_s* p, uint64_t seed, uint64_t round,
-                          int gradients, bvc_round_stats* stats) {
+bvc_eval_points_s* update_round_sharded(bvc_comm_s* C, bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r,
+                                        const bvc_cache_config& cfg,
+                                        const std::function<bvc_eval_points_s*()>& points, uint64_t seed,
+                                        uint64_t round, int gradients, bvc_round_stats* stats) {
     require_device();
-    need(s && r && p, "null argument");
+    need(s && r, "null argument");
     validate_kernel(pb.kernel);
     if (cfg.sourceBall && gradients) throw Error(BVC_ERR_SOLVER, "ball-kernel source mode does not support gradient splats");
     make_splat_config(s, pb, cfg);
@@ -108,8 +109,8 @@ void update_round_sharded(bvc_comm_s* C, bvc_scene_s* s, const bvc_problem& pb, 
     // 1. the rank's shard, its band walks on the side stream
     bvc_boundary_cache_s shard;
     GenStats st;
-    generate_shard_with_band(s, pb, r, cfg, seed, round, static_cast<int>(b), static_cast<int>(e), p, gradients != 0,
-                             &shard, st);
+    bvc_eval_points_s* p = generate_shard_with_band(s, pb, r, cfg, seed, round, static_cast<int>(b),
+                                                    static_cast<int>(e), points, gradients != 0, &shard, st);
     // 2. one equal-count all-gather of the padded shards, then the shards' samples in
     //    global order (one device copy per rank)
     const size_t bytes = static_cast<size_t>(cap) * sizeof(CacheSample);
@@ -149,6 +150,7 @@ void update_round_sharded(bvc_comm_s* C, bvc_scene_s* s, const bvc_problem& pb, 
         stats->generateSeconds = device_seconds(e0, e1);
         stats->splatSeconds = device_seconds(e1, e2);
     }
+    return p;
 }
 
 }  // namespace bvc_capi
@@ -223,7 +225,35 @@ int bvc_update_solution_sharded(bvc_comm comm, bvc_scene s, const bvc_problem* p
                                 int gradients, bvc_round_stats* stats) {
     API({
         need(comm && s && pb && r && cfg && pts, "null argument");
-        update_round_sharded(comm, s, *pb, r, *cfg, pts, seed, round, gradients, stats);
+        update_round_sharded(comm, s, *pb, r, *cfg, [pts]() { return pts; }, seed, round, gradients, stats);
+    })
+}
+
+int bvc_update_solution_sharded_host(bvc_comm comm, bvc_scene s, const bvc_problem* pb, bvc_region r,
+                                     const bvc_cache_config* cfg, const double* x, size_t n, long long indexBase,
+                                     uint64_t seed, uint64_t round, int gradients, double* u, double* grad,
+                                     bvc_round_stats* stats) {
+    API({
+        need(comm && s && pb && r && cfg && (x || n == 0) && (u || n == 0), "null argument");
+        need(!grad || gradients, "gradient output requested without gradients");
+        need(indexBase >= 0, "negative point index base");
+        std::unique_ptr<bvc_eval_points_s> P;
+        update_round_sharded(comm, s, *pb, r, *cfg,
+                             [&]() -> bvc_eval_points_s* {  // on the side stream, under the shard's walks
+                                 P = make_points(x, n, s->host.dim);
+                                 P->base = indexBase;
+                                 mark_points(s, r, *cfg, P.get());
+                                 ensure_order(P.get());
+                                 return P.get();
+                             },
+                             seed, round, gradients, stats);
+        if (n == 0) return BVC_OK;
+        const int d = P->dim;
+        double* o = ws().get<double>(kWsEvalOut, (1 + d) * n);
+        launch_solution(P.get(), o, o + n);
+        CK(cudaMemcpyAsync(u, o, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        if (grad) CK(cudaMemcpyAsync(grad, o + n, d * n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
     })
 }
 

@@ -358,9 +358,10 @@ void splat(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_points_s* P,
            size_t begin, size_t end, bool val, bool grad, int mode = 0, double clamp = 0.0);
 void fallback_walks(bvc_scene_s* S, const bvc_problem& pb, const bvc_cache_config& cfg, bvc_eval_points_s* P,
                     uint64_t seed, uint64_t round, bool gradients);             // capi_walks.cu
-void generate_shard_with_band(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const bvc_cache_config& cfg,
-                              uint64_t seed, uint64_t round, int begin, int end, bvc_eval_points_s* pts,
-                              bool gradients, bvc_boundary_cache_s* out, GenStats& st);  // capi_cache.cu
+bvc_eval_points_s* generate_shard_with_band(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r,
+                                           const bvc_cache_config& cfg, uint64_t seed, uint64_t round, int begin,
+                                           int end, const std::function<bvc_eval_points_s*()>& points,
+                                           bool gradients, bvc_boundary_cache_s* out, GenStats& st);  // capi_cache.cu
 // updateSolution's splat dispatch (cache.cpp:639-663) over a round's caches
 void splat_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const bvc_cache_config& cfg,
                  bvc_boundary_cache_s* bc, bvc_source_cache_s* sc, bvc_eval_points_s* p, uint64_t seed,

@@ -53,7 +53,11 @@ def _worker(rank, world, port, n_boundary, q):
     walks = 0
     for rnd in range(2):
         walks += B.update_solution_sharded(comm, sc, pb, region, cfg, pts, SEED, rnd, gradients=True)["cacheWalks"]
-    q.put((rank, {k: np.asarray(v) for k, v in pts.download().items()}, walks))
+    state = {k: np.asarray(v) for k, v in pts.download().items()}
+    # the host-buffer form of one round (bvc_update_solution_sharded_host)
+    u, g = B.update_solution_sharded_host(comm, sc, pb, region, cfg, x[b:e], b, SEED, 7, gradients=True)
+    state["host_u"], state["host_g"] = u, g
+    q.put((rank, state, walks))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -68,7 +72,9 @@ def _single(n_boundary):
     walks = 0
     for rnd in range(2):
         walks += B.update_solution(sc, pb, region, cfg, pts, SEED, rnd, gradients=True)["cacheWalks"]
-    return pts.download(), walks, (sc, region, pb, cfg, x)
+    state = dict(pts.download())
+    state["host_u"], state["host_g"] = B.update_solution_host(sc, pb, region, cfg, x, SEED, 7, gradients=True)
+    return state, walks, (sc, region, pb, cfg, x)
 
 
 @pytest.mark.parametrize("n_boundary", [1024, 1001])  # even and padded (uneven) shards
@@ -103,6 +109,8 @@ def test_one_rank_nccl_sharded_round_equals_single_gpu_round():
     B.mark_evaluation_points(sc, region, cfg, pts)
     for rnd in range(2):
         B.update_solution_sharded(comm, sc, pb, region, cfg, pts, SEED, rnd, gradients=True)
-    got = pts.download()
+    got = dict(pts.download())
+    got["host_u"], got["host_g"] = B.update_solution_sharded_host(comm, sc, pb, region, cfg, x, 0, SEED, 7,
+                                                                  gradients=True)
     for k, v in ref.items():
         assert np.array_equal(np.asarray(got[k]), np.asarray(v), equal_nan=True), k
