@@ -167,6 +167,22 @@ def workload_config(c, cfg_id):
 METRIC = "BVC eval interactions/s and walk steps/s per GPU; % of FP32/SFU roofline"
 
 
+class _StdoutToStderr:
+    """Native libraries (NCCL prints its version line at communicator init) write to fd 1;
+    the bench's stdout must hold exactly one JSON line, so fd 1 points at stderr meanwhile."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *a):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 def run_gpu(args):
     import torch
 
@@ -178,7 +194,8 @@ def run_gpu(args):
     if world > 1 or os.environ.get("BVC_BENCH_SHARDED") == "1":
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        with _StdoutToStderr():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2302_11825_b200 as B
     from paper_2302_11825_b200 import abi, configs
 
@@ -215,7 +232,8 @@ def run_gpu(args):
     if sharded:
         from paper_2302_11825_b200 import distributed
 
-        comm = distributed.library_comm(B, dist, rank, world)
+        with _StdoutToStderr():
+            comm = distributed.library_comm(B, dist, rank, world)
     step = round_multi if sharded else round_single
 
     def barrier():
