@@ -28,6 +28,10 @@ using namespace bvc_dev;
 namespace {
 
 constexpr int kThreads = 128;
+#ifndef BVC_UNROLL_PACKED
+#define BVC_UNROLL_PACKED 2
+#endif
+constexpr int kUnrollPacked = BVC_UNROLL_PACKED;  // samples per packed tile-loop iteration
 constexpr int kQ = 4;  // query points per thread (register blocking), most kinds
 // screened-3D values (C5) hold BVC_Q_SCR3 points per thread (measured, see DESIGN)
 #ifndef BVC_Q_SCR3
@@ -44,29 +48,6 @@ struct Acc {
     float v, gx, gy, gz;
 };
 
-// Bessel pieces for screened 2D: K0(t) and Q = t K1(t)
-__device__ __forceinline__ void k0_q(float t, float& K0, float& Q) {
-    if (t <= 2.0f) {
-        float h = 0.5f * t, y = h * h;
-        float lnh = f_lg2(h) * kLn2;
-        float w = t * t * (1.0f / 14.0625f);
-        float i0 = 1.0f + w * (3.5156229f + w * (3.0899424f + w * (1.2067492f + w * (0.2659732f + w * (0.0360768f + w * 0.0045813f)))));
-        float i1 = t * (0.5f + w * (0.87890594f + w * (0.51498869f + w * (0.15084934f + w * (0.02658733f + w * (0.00301532f + w * 0.00032411f))))));
-        float p0 = -0.57721566f + y * (0.42278420f + y * (0.23069756f + y * (0.03488590f + y * (0.00262698f + y * (0.00010750f + y * 0.0000074f)))));
-        float p1 = 1.0f + y * (0.15443144f + y * (-0.67278579f + y * (-0.18156897f + y * (-0.01919402f + y * (-0.00110404f - y * 0.00004686f)))));
-        K0 = fmaf(-lnh, i0, p0);
-        Q = fmaf(t * lnh, i1, p1);
-    } else {
-        float rt = f_rsq(t);
-        float e = f_ex2(-1.44269504088896340736f * t);
-        float y = 2.0f * rt * rt;
-        float p0 = 1.25331414f + y * (-0.07832358f + y * (0.02189568f + y * (-0.01062446f + y * (0.00587872f + y * (-0.00251540f + y * 0.00053208f)))));
-        float p1 = 1.25331414f + y * (0.23498619f + y * (-0.03655620f + y * (0.01504268f + y * (-0.00780353f + y * (0.00325614f - y * 0.00068245f)))));
-        float er = e * rt;
-        K0 = p0 * er;
-        Q = p1 * er * t;
-    }
-}
 
 // --- screened 2D, written once for one lane (float) and two packed lanes (F2) ----
 // Every product and sum is an explicit fma / mul (never a mul feeding an add, which
@@ -526,7 +507,7 @@ __device__ __forceinline__ void tile_loop(const float4* S, int cnt, const float*
             pz2[h] = pk(pz[2 * h], pz[2 * h + 1]);
             a2[h].v = a2[h].gx = a2[h].gy = a2[h].gz = pk(0.f, 0.f);
         }
-#pragma unroll 2
+#pragma unroll kUnrollPacked
         for (int j = 0; j < cnt; ++j) {
             const float4 a = S[2 * j], b = S[2 * j + 1];
 #pragma unroll
