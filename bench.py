@@ -307,6 +307,8 @@ def run_gpu(args):
         out["e2e"] = e2e
         if world == 1 and not args.no_cpu:
             out["cpu_baseline"] = cpu_baseline(c, args.cpu_sample_s)
+        if world == 1 and args.extra_configs:
+            out["other_configs"] = other_configs(args)
         print(json.dumps(out), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -679,6 +681,37 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+_T_START = time.perf_counter()
+
+
+def other_configs(args):
+    """The other BASELINE configs (not the headline): a short bench.py run of each in a
+    fresh process (3 timed rounds, 2 warm-up), so one driver run leaves evidence for all
+    five. Skipped once the run has used 7 minutes; each run is capped at 80 s."""
+    res = {}
+    for cid in (1, 2, 3, 4):
+        if cid == args.config:
+            continue
+        if time.perf_counter() - _T_START > 420.0:
+            res[f"C{cid}"] = {"skipped": "time budget of the default run"}
+            continue
+        cmd = [sys.executable, os.path.abspath(__file__), "--config", str(cid), "--steps", "3", "--warmup", "2",
+               "--no-cpu", "--no-probe", "--no-extra"]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=80, cwd=ROOT,
+                               env={k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE")})
+            line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+            d = json.loads(line)
+            res[f"C{cid}"] = {"workload": d["config"]["workload"], "ms_per_step": d["ms_per_step"],
+                              "step_ms": d["step_ms"], "value": d["value"], "unit": d["unit"],
+                              "e2e_ms_per_call": d["e2e"]["ms_per_step"], "phases_s": d.get("phases_s"),
+                              "gather_frac_of_bound": d.get("gather_roofline", {}).get("frac"),
+                              "walk_steps_per_s": d.get("walk_steps_per_s"), "clocks": d.get("clocks")}
+        except Exception as e:  # noqa: BLE001 - reported, the headline line stands
+            res[f"C{cid}"] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -689,6 +722,8 @@ def main():
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-probe", action="store_true", help="skip the pipe microbenchmarks (profiling runs)")
+    ap.add_argument("--no-extra", dest="extra_configs", action="store_false",
+                    help="skip the short runs of the other configs (other_configs key)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

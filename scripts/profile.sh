@@ -4,7 +4,7 @@
 export PYTHONPATH=$PWD
 CFG=${1:-2}
 TAG=${2:+_$2}
-CMD="python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu --no-probe"
+CMD="python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu --no-probe --no-extra"
 $CMD > gpurun_out/plain$TAG.log 2>&1 || { echo "plain run failed"; tail -5 gpurun_out/plain$TAG.log; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches$TAG.csv $CMD > gpurun_out/ncu_list$TAG.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:gather_kernel -s 2 -c 1 -o gpurun_out/prof_gather$TAG -f $CMD > gpurun_out/ncu_gather$TAG.log 2>&1
