@@ -707,6 +707,8 @@ def other_configs(args):
                               "e2e_ms_per_call": d["e2e"]["ms_per_step"], "phases_s": d.get("phases_s"),
                               "gather_frac_of_bound": d.get("gather_roofline", {}).get("frac"),
                               "walk_steps_per_s": d.get("walk_steps_per_s"), "clocks": d.get("clocks")}
+            if "gather_fp64" in d:  # C1's fp64 variant (BASELINE configs[0])
+                res[f"C{cid}"]["gather_fp64"] = d["gather_fp64"]
         except Exception as e:  # noqa: BLE001 - reported, the headline line stands
             res[f"C{cid}"] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
     return res
