@@ -98,3 +98,26 @@ def test_library_shard_layout_matches_the_python_ranges():
                 assert cap == -(-n // w) and e - b <= cap
     with pytest.raises(B.BvcError):
         B.shard_layout(10, 2, 2)
+
+
+def test_library_communicators_host_side():
+    """bvc_comm handles without a device: a host-staged communicator is created, reports
+    its ranks and is destroyed; invalid ranks are refused; the sharded round itself
+    needs the GPU and says so (no CPU fallback)."""
+    import paper_2302_11825_b200 as B
+
+    calls = []
+    comm = B.Communicator.from_allgather(4, 3, lambda s, r, n: calls.append(n))
+    assert (comm.nranks, comm.rank) == (4, 3)
+    del comm
+    with pytest.raises(B.BvcError):
+        B.Communicator.from_allgather(2, 2, lambda s, r, n: None)
+    if torch.cuda.is_available():
+        pytest.skip("no-device behaviour only")
+    one = B.Communicator.from_allgather(1, 0, lambda s, r, n: None)
+    geom = ([[0, 0], [1, 0], [1, 1], [0, 1]], [[0, 1], [1, 2], [2, 3], [3, 0]], [0, 0, 0, 0])
+    sc = B.Scene(*geom)
+    region = B.SolveRegion(sc, offset=0.05, epsilon=1e-3)
+    pb = B.problem(B.poisson(2), g=B.field(B.abi.FIELD_LINEAR, 1.0, 0.0, 0.0, 0.0))
+    with pytest.raises(B.NoDeviceError):
+        B.update_solution_sharded_host(one, sc, pb, region, B.cache_config(), np.zeros((3, 2)) + 0.5, 0, 1, 0)
