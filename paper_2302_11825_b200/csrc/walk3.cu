@@ -346,6 +346,103 @@ __device__ __forceinline__ U4 draw3(const WalkEnv3& E, Task3& t) {
     return philox4x32_10(c, E.k0, E.k1);
 }
 
+// A task's start (a U walk from its point, or a D task's first-ball walk) and what
+// follows the end of one of its walks (the U value, the D phase change or its
+// gradient): shared by the persistent kernel and the wavefront step kernel, so both
+// compute every walk bit for bit alike.
+template <bool SCR>
+__device__ __forceinline__ void task3_begin(const WalkEnv3& E, const WalkJob3& J, long long nUtot, long long id,
+                                            Task3& t, Walk3& w) {
+    t.id = id;
+    t.draw = 0;
+    t.phase = 0;
+    t.trunc = 0;
+    if (id < nUtot) {
+        t.role = 0;
+        t.pt = id < 0x7fffffffLL ? static_cast<int>(static_cast<unsigned>(id) / static_cast<unsigned>(J.nU))
+                                 : static_cast<int>(id / J.nU);
+        int k = static_cast<int>(id - static_cast<long long>(t.pt) * J.nU);
+        long long g = J.gidU ? J.gidU[t.pt] : J.gidBaseU + t.pt;
+        t.rid = static_cast<unsigned long long>(g) * J.nU + k;
+        float4 s = J.startU[t.pt];
+        walk3_start(w, s.x, s.y, s.z);
+        if (J.hintU) w.lastD = J.hintU[t.pt];
+    } else {
+        long long d = id - nUtot;
+        t.role = 1;
+        t.pt = d < 0x7fffffffLL ? static_cast<int>(static_cast<unsigned>(d) / static_cast<unsigned>(J.nD))
+                                : static_cast<int>(d / J.nD);
+        int k = static_cast<int>(d - static_cast<long long>(t.pt) * J.nD);
+        long long g = J.gidD ? J.gidD[t.pt] : t.pt;
+        t.rid = static_cast<unsigned long long>(g) * J.nD + k;
+        float4 c = J.xD[t.pt];
+        t.R = J.radiusD[t.pt];
+        U4 r0 = draw3(E, t);
+        U4 r1 = draw3(E, t);
+        sphere_dir(u01(r0.x), u01(r0.y), t.dx, t.dy, t.dz);
+        t.vx = t.vy = t.vz = 0.f;
+        if (SCR && E.P.sigma > 0.f) {
+            // y ~ |G^B| in the Poisson ball, grad G^B (kernels.cpp:68-75, 3D) sigma / pdf
+            float tt = invert_ball_cdf3(u01(r0.z));
+            float r = fmaxf(tt * t.R, 1e-6f * t.R);
+            float ex, ey, ez;
+            sphere_dir(u01(r0.w), u01(r1.x), ex, ey, ez);
+            float gb = (1.0f / t.R - 1.0f / r) * kInv4Pi;            // G^B 3D
+            float pdf = gb / (-t.R * t.R / 6.0f);                     // / mass
+            float gf = (1.0f / (t.R * t.R * t.R) - 1.0f / (r * r * r)) * kInv4Pi * (E.P.sigma / pdf);
+            t.cx = r * ex * gf; t.cy = r * ey * gf; t.cz = r * ez * gf;
+            t.y2x = c.x + r * ex; t.y2y = c.y + r * ey; t.y2z = c.z + r * ez;
+        }
+        float rr = t.R * 0.99999952f;
+        walk3_start(w, fmaf(rr, t.dx, c.x), fmaf(rr, t.dy, c.y), fmaf(rr, t.dz, c.z));
+        if (J.hintD) w.lastD = J.hintD[t.pt];
+    }
+}
+
+// returns whether the task continues (a screened D task's nested walk)
+template <bool SCR>
+__device__ __forceinline__ bool task3_walk_done(const WalkEnv3& E, const WalkJob3& J, long long nUtot, Task3& t,
+                                                Walk3& w, float value) {
+    bool active = true;
+    if (t.role == 0) {
+        J.outU[t.id] = value;
+        if (t.trunc && J.truncU) atomicAdd(J.truncU + t.pt, 1);
+        if (t.trunc && J.truncTotal) atomicAdd(J.truncTotal, 1ull);
+        active = false;
+    } else if (t.phase == 0) {
+        float s = (3.0f / t.R) * value;
+        t.vx = fmaf(s, t.dx, t.vx);
+        t.vy = fmaf(s, t.dy, t.vy);
+        t.vz = fmaf(s, t.dz, t.vz);
+        if (SCR && E.P.sigma > 0.f) {
+            t.phase = 1;
+            walk3_start(w, t.y2x, t.y2y, t.y2z);
+            if (J.hintD) w.lastD = J.hintD[t.pt];
+        } else {
+            active = false;
+        }
+    } else {
+        t.vx = fmaf(t.cx, value, t.vx);
+        t.vy = fmaf(t.cy, value, t.vy);
+        t.vz = fmaf(t.cz, value, t.vz);
+        active = false;
+    }
+    if (!active && t.role == 1) {
+        long long slot = t.id - nUtot;
+        if (J.normalD) {
+            float4 n = J.normalD[t.pt];
+            J.outD[slot] = n.x * t.vx + n.y * t.vy + n.z * t.vz;
+        } else {
+            J.outD[3 * slot] = t.vx;
+            J.outD[3 * slot + 1] = t.vy;
+            J.outD[3 * slot + 2] = t.vz;
+        }
+        if (t.trunc && J.truncD) atomicAdd(J.truncD + t.pt, 1);
+        if (t.trunc && J.truncTotal) atomicAdd(J.truncTotal, 1ull);
+    }
+    return active;
+}
+
 // resident blocks per SM: Neumann scenes 8 (32 registers, spilling; C5: 3.54 s at 8, 3.60 s
 // at 6), Dirichlet-only 6 (40 registers; C4 walks 435 ms at 6, 469 at 5, 521 at 4, 477 at 8)
 template <bool NEU, bool SCR, bool COUNT, int MINB = NEU ? 8 : 6>
@@ -373,51 +470,7 @@ __global__ void __launch_bounds__(kThreads3, MINB) walk3_kernel(const WalkEnv3 E
             int take = static_cast<int>(min(static_cast<long long>(__popc(need)), qEnd - qNext));
             int rank = __popc(need & lt);
             if (((need >> lane) & 1u) && rank < take) {
-                long long id = qNext + rank;
-                t.id = id;
-                t.draw = 0;
-                t.phase = 0;
-                t.trunc = 0;
-                if (id < nUtot) {
-                    t.role = 0;
-                    t.pt = id < 0x7fffffffLL ? static_cast<int>(static_cast<unsigned>(id) / static_cast<unsigned>(J.nU))
-                                             : static_cast<int>(id / J.nU);
-                    int k = static_cast<int>(id - static_cast<long long>(t.pt) * J.nU);
-                    long long g = J.gidU ? J.gidU[t.pt] : J.gidBaseU + t.pt;
-                    t.rid = static_cast<unsigned long long>(g) * J.nU + k;
-                    float4 s = J.startU[t.pt];
-                    walk3_start(w, s.x, s.y, s.z);
-                    if (J.hintU) w.lastD = J.hintU[t.pt];
-                } else {
-                    long long d = id - nUtot;
-                    t.role = 1;
-                    t.pt = d < 0x7fffffffLL ? static_cast<int>(static_cast<unsigned>(d) / static_cast<unsigned>(J.nD))
-                                            : static_cast<int>(d / J.nD);
-                    int k = static_cast<int>(d - static_cast<long long>(t.pt) * J.nD);
-                    long long g = J.gidD ? J.gidD[t.pt] : t.pt;
-                    t.rid = static_cast<unsigned long long>(g) * J.nD + k;
-                    float4 c = J.xD[t.pt];
-                    t.R = J.radiusD[t.pt];
-                    U4 r0 = draw3(E, t);
-                    U4 r1 = draw3(E, t);
-                    sphere_dir(u01(r0.x), u01(r0.y), t.dx, t.dy, t.dz);
-                    t.vx = t.vy = t.vz = 0.f;
-                    if (SCR && E.P.sigma > 0.f) {
-                        // y ~ |G^B| in the Poisson ball, grad G^B (kernels.cpp:68-75, 3D) sigma / pdf
-                        float tt = invert_ball_cdf3(u01(r0.z));
-                        float r = fmaxf(tt * t.R, 1e-6f * t.R);
-                        float ex, ey, ez;
-                        sphere_dir(u01(r0.w), u01(r1.x), ex, ey, ez);
-                        float gb = (1.0f / t.R - 1.0f / r) * kInv4Pi;            // G^B 3D
-                        float pdf = gb / (-t.R * t.R / 6.0f);                     // / mass
-                        float gf = (1.0f / (t.R * t.R * t.R) - 1.0f / (r * r * r)) * kInv4Pi * (E.P.sigma / pdf);
-                        t.cx = r * ex * gf; t.cy = r * ey * gf; t.cz = r * ez * gf;
-                        t.y2x = c.x + r * ex; t.y2y = c.y + r * ey; t.y2z = c.z + r * ez;
-                    }
-                    float rr = t.R * 0.99999952f;
-                    walk3_start(w, fmaf(rr, t.dx, c.x), fmaf(rr, t.dy, c.y), fmaf(rr, t.dz, c.z));
-                    if (J.hintD) w.lastD = J.hintD[t.pt];
-                }
+                task3_begin<SCR>(E, J, nUtot, qNext + rank, t, w);
                 active = true;
             }
             qNext += take;
@@ -427,44 +480,8 @@ __global__ void __launch_bounds__(kThreads3, MINB) walk3_kernel(const WalkEnv3 E
         if (active) {
             U4 rnd = draw3(E, t);
             float value;
-            if (walk3_step<NEU, SCR, COUNT>(E, w, rnd, value, t.trunc, steps)) {
-                if (t.role == 0) {
-                    J.outU[t.id] = value;
-                    if (t.trunc && J.truncU) atomicAdd(J.truncU + t.pt, 1);
-                    if (t.trunc && J.truncTotal) atomicAdd(J.truncTotal, 1ull);
-                    active = false;
-                } else if (t.phase == 0) {
-                    float s = (3.0f / t.R) * value;
-                    t.vx = fmaf(s, t.dx, t.vx);
-                    t.vy = fmaf(s, t.dy, t.vy);
-                    t.vz = fmaf(s, t.dz, t.vz);
-                    if (SCR && E.P.sigma > 0.f) {
-                        t.phase = 1;
-                        walk3_start(w, t.y2x, t.y2y, t.y2z);
-                        if (J.hintD) w.lastD = J.hintD[t.pt];
-                    } else {
-                        active = false;
-                    }
-                } else {
-                    t.vx = fmaf(t.cx, value, t.vx);
-                    t.vy = fmaf(t.cy, value, t.vy);
-                    t.vz = fmaf(t.cz, value, t.vz);
-                    active = false;
-                }
-                if (!active && t.role == 1) {
-                    long long slot = t.id - nUtot;
-                    if (J.normalD) {
-                        float4 n = J.normalD[t.pt];
-                        J.outD[slot] = n.x * t.vx + n.y * t.vy + n.z * t.vz;
-                    } else {
-                        J.outD[3 * slot] = t.vx;
-                        J.outD[3 * slot + 1] = t.vy;
-                        J.outD[3 * slot + 2] = t.vz;
-                    }
-                    if (t.trunc && J.truncD) atomicAdd(J.truncD + t.pt, 1);
-                    if (t.trunc && J.truncTotal) atomicAdd(J.truncTotal, 1ull);
-                }
-            }
+            if (walk3_step<NEU, SCR, COUNT>(E, w, rnd, value, t.trunc, steps))
+                active = task3_walk_done<SCR>(E, J, nUtot, t, w, value);
         }
     }
     if (J.steps) {
