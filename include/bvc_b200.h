@@ -445,7 +445,9 @@ int bvc_streamlines_write_csv(const char* path, const double* seeds, int nSeeds,
                               const double* points, const int* counts, const int* reasons);
 
 /* ---- pointwise estimators (pointwise.h:62-76), batched over n points -------- */
-/* point i uses cfg->stream for i == 0 when n == 1, else streams[i] (NULL => mixKey(stream,i)) */
+/* point i uses cfg->stream for i == 0 when n == 1, else streams[i] (NULL => mixKey(stream,i)).
+   x (and normal) hold the scene's dimension per point: 2D as the reference, and the 3D
+   lift for triangle meshes (solve and normal derivative; the gradient estimate is 2D) */
 int bvc_wos_solve(bvc_scene scene, const bvc_problem* problem, const double* x, size_t n,
                   const bvc_walk_config* cfg, const uint64_t* streams, bvc_scalar_estimate* out);
 int bvc_wost_solve(bvc_scene scene, const bvc_problem* problem, const double* x, size_t n,

@@ -732,7 +732,7 @@ def fallback_walks(scene: Scene, pb, cfg, pts: EvaluationPoints, seed, round_, g
 
 
 def _estimates(fn, scene, pb, x, cfg, streams, normal=None, vector=False):
-    x = _f64(x, 2)
+    x = _f64(x, scene.dim)
     n = len(x)
     out = (abi.VectorEstimate * max(n, 1))() if vector else (abi.ScalarEstimate * max(n, 1))()
     st = None
@@ -740,7 +740,7 @@ def _estimates(fn, scene, pb, x, cfg, streams, normal=None, vector=False):
         st = np.ascontiguousarray(streams, dtype=np.uint64)
     sp = _ptr(st, C.c_uint64) if st is not None else None
     if normal is not None:
-        nrm = _f64(normal, 2)
+        nrm = _f64(normal, scene.dim)
         _check(fn(scene.h, C.byref(pb), _ptr(x), _ptr(nrm), C.c_size_t(n), C.byref(cfg), sp, out))
     else:
         _check(fn(scene.h, C.byref(pb), _ptr(x), C.c_size_t(n), C.byref(cfg), sp, out))

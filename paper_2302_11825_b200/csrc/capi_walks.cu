@@ -5,6 +5,100 @@
 
 namespace bvc_capi {
 
+// the 3D lift of the estimator job (the reference's solver is 2D-only, pointwise.cpp:23):
+// solve (mode 0) and normal derivative (mode 2) with the 3D walk kernel; one stream per
+// point exactly as in 2D
+void pointwise3(bvc_scene_s* S, const bvc_problem& pb, const double* x, const double* normal, size_t n,
+                const bvc_walk_config& cfg, const uint64_t* streams, int mode, double* mean, double* se,
+                long long* count, long long* trunc) {
+    need(mode != 1, "3D gradient estimates need 3 components: the ABI's vector estimate is 2D (pointwise.h:54-59)");
+    WalkEnv3 E = make_env3(S, pb, cfg, cfg.seed, kPointwiseSalt, 0);
+    const int nw = std::max(1, cfg.nWalks);
+    const int ni = static_cast<int>(n);
+    std::vector<long long> gid(ni);
+    for (int i = 0; i < ni; ++i) {
+        uint64_t st = streams ? streams[i] : (ni == 1 ? cfg.stream : bvc_dev::mixKey(cfg.stream, i));
+        gid[i] = static_cast<long long>(bvc_dev::mix64(st) >> 1);
+    }
+    double* xd = ws().get<double>(kWsEvalIn, 3 * n);
+    CK(cudaMemcpyAsync(xd, x, 3 * n * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+    if (E.insideTol > 0.f) {  // requireInterior (pointwise.cpp:188-191); meaningless for soups
+        uint8_t* ins = ws().get<uint8_t>(kWsOutside, n);
+        launch_inside3(E.S, xd, ni, E.insideTol, ins, g_stream);
+        std::vector<uint8_t> h(n);
+        CK(cudaMemcpyAsync(h.data(), ins, n, cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+        for (size_t i = 0; i < n; ++i)
+            if (!h[i]) throw Error(BVC_ERR_SOLVER, "evaluation point lies outside the domain");
+    }
+    std::vector<float4> hx(n);
+    for (size_t i = 0; i < n; ++i)
+        hx[i] = make_float4(static_cast<float>(x[3 * i]), static_cast<float>(x[3 * i + 1]),
+                            static_cast<float>(x[3 * i + 2]), 0.f);
+    float4* px = ws().get<float4>(kWsStartU, n);
+    CK(cudaMemcpyAsync(px, hx.data(), n * sizeof(float4), cudaMemcpyHostToDevice, g_stream));
+    long long* dg = ws().get<long long>(kWsGidU, n);
+    CK(cudaMemcpyAsync(dg, gid.data(), n * sizeof(long long), cudaMemcpyHostToDevice, g_stream));
+    int* tr = ws().get<int>(kWsTruncPt, n);
+    CK(cudaMemsetAsync(tr, 0, n * sizeof(int), g_stream));
+    auto* ctr = ws().get<unsigned long long>(kWsCounter, 3);
+    CK(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), g_stream));
+    WalkJob3 J{};
+    J.counter = ctr;
+    J.steps = ctr + 1;
+    J.truncTotal = ctr + 2;
+    if (mode == 0) {
+        J.nU = nw;
+        J.nPtsU = ni;
+        J.startU = px;
+        J.gidU = dg;
+        J.outU = ws().get<float>(kWsOutU, n * nw);
+        J.truncU = tr;
+    } else {
+        // gradientBallRadius: closest point on the whole boundary (pointwise.cpp:217-221)
+        double* cpp = ws().get<double>(kWsEvalOut, 3 * n);
+        double* cpd = ws().get<double>(kWsMean2, n);
+        int* cps = ws().get<int>(kWsSkipB, n);
+        launch_closest3(E.S, xd, ni, bvc_dev::kClsAny, cpp, cpd, cps, g_stream);
+        std::vector<double> hd(n);
+        CK(cudaMemcpyAsync(hd.data(), cpd, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+        std::vector<float> hr(n);
+        for (size_t i = 0; i < n; ++i) hr[i] = static_cast<float>(std::max(hd[i], static_cast<double>(E.rmin)));
+        float* rD = ws().get<float>(kWsRD, n);
+        CK(cudaMemcpyAsync(rD, hr.data(), n * sizeof(float), cudaMemcpyHostToDevice, g_stream));
+        std::vector<float4> hn(n);
+        for (size_t i = 0; i < n; ++i)
+            hn[i] = make_float4(static_cast<float>(normal[3 * i]), static_cast<float>(normal[3 * i + 1]),
+                                static_cast<float>(normal[3 * i + 2]), 0.f);
+        float4* dn = ws().get<float4>(kWsND, n);
+        CK(cudaMemcpyAsync(dn, hn.data(), n * sizeof(float4), cudaMemcpyHostToDevice, g_stream));
+        J.nD = nw;
+        J.nPtsD = ni;
+        J.xD = px;
+        J.radiusD = rD;
+        J.gidD = dg;
+        J.truncD = tr;
+        J.normalD = dn;
+        J.outD = ws().get<float>(kWsOutD, n * nw);
+    }
+    launch_walk_job3(E, J, g_stream);
+    const float* vals = mode == 0 ? J.outU : J.outD;
+    double* dm = ws().get<double>(kWsMean, n);
+    double* ds = ws().get<double>(kWsSe, n);
+    launch_reduce_estimates(vals, ni, nw, 1, 0, dm, ds, g_stream);
+    std::vector<int> ht(n);
+    CK(cudaMemcpyAsync(mean, dm, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaMemcpyAsync(se, ds, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaMemcpyAsync(ht.data(), tr, n * sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+    for (size_t i = 0; i < n; ++i) {
+        count[i] = nw;
+        trunc[i] = ht[i];
+        if (!std::isfinite(mean[i])) throw Error(BVC_ERR_SOLVER, "walk cannot terminate: scene has no Dirichlet boundary");
+    }
+}
+
 // estimator job over host points (pointwise.h:62-76)
 void pointwise(bvc_scene_s* S, const bvc_problem& pb, const double* x, const double* normal, size_t n,
                const bvc_walk_config& cfg, const uint64_t* streams, int mode, double* mean, double* se,
@@ -13,6 +107,10 @@ void pointwise(bvc_scene_s* S, const bvc_problem& pb, const double* x, const dou
     require_device();
     need(S && x, "null scene or points");
     if (n == 0) return;
+    if (S->host.dim == 3) {
+        pointwise3(S, pb, x, normal, n, cfg, streams, mode, mean, se, count, trunc);
+        return;
+    }
     WalkEnv E = make_env(S, pb, cfg, cfg.seed, kPointwiseSalt, 0);
     int nw = std::max(1, cfg.nWalks);
     int ni = static_cast<int>(n);

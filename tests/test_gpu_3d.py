@@ -119,3 +119,60 @@ def test_screened_mixed_3d_runs_and_is_bounded():
     c2 = B.generate_boundary_cache(sc, pb, region, cfg, 5, 0).download()
     assert np.array_equal(c["uHat"], c2["uHat"])
     assert st["cacheTruncated"] <= 1e-4 * st["cacheWalks"]
+
+
+def test_c5_bvc_agrees_with_pointwise_walks():
+    """C5 has no reference path and no closed form: its self-consistency check.
+    On C5's own soup (shell of the 8 displaced spheres, sigma = 1, Neumann caps), the BVC
+    estimate at interior points (mean over independent rounds) agrees with the pointwise
+    WoSt estimate (wostSolve, pointwise.h:66) at the same points: |z| < 3 up to an O(eps)
+    shell allowance, for all but a binomial allowance of the points."""
+    c = configs.config5(scale=1 / 32, n_points=1000)
+    tris, labels = configs.soup_shell(c)
+    comps = configs.soup_components(c)
+    sc = B.Scene.mesh3(c.vertices, tris, labels)
+    region = B.SolveRegion(sc, offset=c.region_offset, epsilon=c.epsilon)
+    rng = np.random.default_rng(11)
+    cand = c.points[rng.permutation(len(c.points))[:4000]]
+    inside = np.zeros(len(cand), bool)
+    for comp in comps:
+        inside |= comp.inside(cand)
+    cand = cand[inside]
+    probe = B.EvaluationPoints(cand, 3)
+    B.mark_evaluation_points(sc, region, c.cache, probe)
+    x = cand[~probe.download()["fallback"].astype(bool)][:24]
+    assert len(x) == 24
+    rounds = []
+    for r in range(12):
+        p = B.EvaluationPoints(x, 3)
+        B.mark_evaluation_points(sc, region, c.cache, p)
+        B.update_solution(sc, c.problem, region, c.cache, p, 900 + r, 0)
+        rounds.append(p.solution())
+    rounds = np.array(rounds)
+    m_bvc = rounds.mean(0)
+    se_bvc = rounds.std(0, ddof=1) / np.sqrt(len(rounds))
+    est = B.wost_solve(sc, c.problem, x, B.walk_config(epsilon=c.epsilon, nWalks=32768, seed=3))
+    m_w, se_w = est["mean"], est["se"]
+    z = (np.abs(m_bvc - m_w) - 3e-3) / np.sqrt(se_bvc ** 2 + se_w ** 2)  # O(eps) shell allowance
+    assert np.sum(z > 3.0) <= 1, (m_bvc, m_w, se_bvc, se_w)
+    assert np.all(np.isfinite(m_bvc)) and np.all(se_bvc > 0)
+
+
+def test_pointwise_3d_matches_harmonic_data(sphere):
+    """The 3D lift of wostSolve / wostNormalDerivative (pointwise.h:66-76): on the sphere with
+    harmonic data the estimates are unbiased for u = g and du/dn = n . grad g."""
+    _, _, sc = sphere
+    pb = B.problem(B.poisson(3), g=HARMONIC)
+    rng = np.random.default_rng(4)
+    x = rng.normal(size=(16, 3))
+    x *= (rng.uniform(0.1, 0.7, 16) / np.linalg.norm(x, axis=1))[:, None]
+    e = B.wost_solve(sc, pb, x, B.walk_config(epsilon=1e-3, nWalks=8192, seed=9))
+    z = (e["mean"] - g_exact(x)) / np.maximum(e["se"], 1e-12)
+    assert np.sum(np.abs(z) > 3) <= 1, z
+    n = rng.normal(size=(16, 3))
+    n /= np.linalg.norm(n, axis=1)[:, None]
+    d = B.wost_normal_derivative(sc, pb, x, n, B.walk_config(epsilon=1e-3, nWalks=16384, seed=10))
+    h = 1e-5
+    dgdn = (g_exact(x + h * n) - g_exact(x - h * n)) / (2 * h)
+    zd = (d["mean"] - dgdn) / np.maximum(d["se"], 1e-12)
+    assert np.sum(np.abs(zd) > 3) <= 1, zd
