@@ -537,6 +537,64 @@ void bvc_scene_s::upload2() {
     total = run;
     cdf.upload(hc.data(), hc.size());
     cdfIds.upload(hid.data(), hid.size());
+    build_runs();
+}
+
+// A ray that hits a Neumann segment hits the same point of the line through it, so
+// consecutive exactly collinear Neumann segments of a chain can answer the walks' rays
+// as one segment (the hit's normal is the run's, and a walker standing on the run
+// skips the whole line, which a ray leaving it cannot meet again). A subdivided
+// straight wall (C2: 2 x 512 segments) becomes 2 segments, tested in a loop instead of a
+// BVH traversal. Used only when the runs are few (<= 32) and merge >= 4 segments each
+// on average; curved Neumann boundaries keep the BVH.
+void bvc_scene_s::build_runs() {
+    runN = 0;
+    std::vector<float4> seg;
+    std::vector<int> ids;
+    int neumann = 0;
+    for (const auto& L : host.loops) {
+        const size_t m = L.size();
+        if (m == 0) continue;
+        auto dir = [&](int i, double& ex, double& ey) {
+            const double *a = host.vert(host.idx[2 * i]), *b = host.vert(host.idx[2 * i + 1]);
+            ex = b[0] - a[0];
+            ey = b[1] - a[1];
+        };
+        auto joins = [&](int i, int j) {  // j continues i's straight Neumann run
+            if (!host.label[i] || !host.label[j] || host.idx[2 * i + 1] != host.idx[2 * j]) return false;
+            double ax, ay, bx, by;
+            dir(i, ax, ay);
+            dir(j, bx, by);
+            return ax * by - ay * bx == 0.0 && ax * bx + ay * by > 0.0;
+        };
+        const bool closed = host.loopClosed[host.loop[L[0]]] != 0;
+        // start at a segment that does not continue its predecessor's run
+        size_t s0 = 0;
+        if (closed) {
+            size_t k = 0;
+            while (k < m && joins(L[(k + m - 1) % m], L[k])) ++k;
+            if (k == m) return;  // a closed loop cannot be one straight run
+            s0 = k;
+        }
+        for (size_t c = 0; c < m;) {
+            const int first = L[(s0 + c) % m];
+            size_t len = 1;
+            while (c + len < m && joins(L[(s0 + c + len - 1) % m], L[(s0 + c + len) % m])) ++len;
+            if (host.label[first]) {
+                const int last = L[(s0 + c + len - 1) % m];
+                const double *a = host.vert(host.idx[2 * first]), *b = host.vert(host.idx[2 * last + 1]);
+                seg.push_back(make_float4(a[0], a[1], b[0], b[1]));
+                ids.push_back(first);
+                neumann += static_cast<int>(len);
+            }
+            c += len;
+        }
+    }
+    const int n = static_cast<int>(seg.size());
+    if (n == 0 || n > 32 || 4 * n > neumann) return;
+    runSeg.upload(seg.data(), n);
+    runId.upload(ids.data(), n);
+    runN = n;
 }
 
 

@@ -12,6 +12,9 @@ WalkEnv make_env(bvc_scene_s* S, const bvc_problem& pb, const bvc_walk_config& w
     if (pb.kernel.dim != 2) throw Error(BVC_ERR_SOLVER, "walk estimators support dim == 2 only");
     WalkEnv E{};
     E.S = S->view();
+    E.runSeg = S->runSeg.p;
+    E.runId = S->runId.p;
+    E.runN = S->runN;
     E.P.screened = pb.kernel.kind == BVC_KERNEL_SCREENED;
     E.P.sigma = static_cast<float>(pb.kernel.sigma);
     E.P.sqrtSigma = static_cast<float>(std::sqrt(pb.kernel.sigma));

@@ -270,6 +270,11 @@ struct bvc_scene_s {
     bool build_on_gpu() const { return builder() != "host"; }
     void gpu_build(int dim, const float4* a, const float4* b, const float4* c, const int2* sil);
 
+    // straight Neumann runs for the walks' rays (2D; WalkEnv::runSeg)
+    DevBuf<float4> runSeg;
+    DevBuf<int> runId;
+    int runN = 0;
+    void build_runs();
     void upload2();
     void upload3();
     void build_sil_records();

@@ -60,6 +60,12 @@ struct FarField {
 // WalkContext (pointwise.cpp:11-35) in device form
 struct WalkEnv {
     SceneView2 S;
+    // Neumann rays against the scene's straight Neumann runs (bvc_scene_s::build_runs):
+    // consecutive exactly collinear Neumann segments merged into one; used when there are
+    // few (runN > 0), else rays traverse the BVH
+    const float4* runSeg;
+    const int* runId;  // a segment of the run (its normal is the run's)
+    int runN;
     DevProblem P;
     float eps, rmin, tguard, insideTol, scale, nudge;
     float cx, cy, escape;  // scene box centre and escape half-width

@@ -293,6 +293,30 @@ struct RayHit {
 // with t in (tMin, tMax] among the filtered segments, skipping `skipSeg` (the
 // segment the walk currently stands on: a ray leaving a straight segment cannot
 // hit it again, and skipping it keeps FP32 re-hits out).
+// one segment against the ray o + t d (unit d), keeping the nearest hit with
+// tMin < t <= limit in h (limit shrinks to it). Watertight crossing test: each endpoint
+// is classified by its side of the ray; a vertex shared by two segments gets the same
+// sign in both, so a ray can never slip between them (raySegment bvh.cpp:71-83 decides
+// via s in [0,1], which FP32 cancellation breaks near vertices).
+__device__ __forceinline__ void ray_segment_hit(const float4 seg, int id, float ox, float oy, float dx, float dy,
+                                                float tMin, float& limit, RayHit& h) {
+    float sa = ray_side(dx, dy, ox, oy, seg.x, seg.y);
+    float sb = ray_side(dx, dy, ox, oy, seg.z, seg.w);
+    if ((sa > 0.0f && sb > 0.0f) || (sa < 0.0f && sb < 0.0f)) return;
+    float den = sa - sb;  // = cross(d, e) with e = b - a, up to sign convention
+    if (den == 0.0f) return;  // parallel / collinear: miss
+    float s = sa / den;
+    float ex = seg.z - seg.x, ey = seg.w - seg.y;
+    float px = fmaf(s, ex, seg.x), py = fmaf(s, ey, seg.y);
+    float t = (px - ox) * dx + (py - oy) * dy;  // unit direction: distance along the ray
+    if (t <= 0.0f || t > limit) return;
+    if (t > tMin && t < h.t) {
+        h.t = t; h.s = s; h.seg = id;
+        h.px = px; h.py = py;
+        limit = t;
+    }
+}
+
 template <bool COUNT = false>
 __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, float oy, float dx, float dy,
                                                 float tMax, unsigned qmask, float tMin, int skipSeg, int start = 0) {
@@ -341,25 +365,7 @@ __device__ __forceinline__ RayHit intersect_ray(const SceneView2& S, float ox, f
             const Prim2 p = S.prims[i];
             count_fetch<COUNT>(S, 1);
             if (!((1u << p.label) & qmask) || p.id == skipSeg) continue;
-            // watertight crossing test: each endpoint is classified by its side
-            // of the ray; a vertex shared by two segments gets the same sign in
-            // both, so a ray can never slip between them (raySegment bvh.cpp:71-83
-            // decides via s in [0,1], which FP32 cancellation breaks near vertices)
-            float sa = ray_side(dx, dy, ox, oy, p.seg.x, p.seg.y);
-            float sb = ray_side(dx, dy, ox, oy, p.seg.z, p.seg.w);
-            if ((sa > 0.0f && sb > 0.0f) || (sa < 0.0f && sb < 0.0f)) continue;
-            float den = sa - sb;  // = cross(d, e) with e = b - a, up to sign convention
-            if (den == 0.0f) continue;  // parallel / collinear: miss
-            float s = sa / den;
-            float ex = p.seg.z - p.seg.x, ey = p.seg.w - p.seg.y;
-            float px = fmaf(s, ex, p.seg.x), py = fmaf(s, ey, p.seg.y);
-            float t = (px - ox) * dx + (py - oy) * dy;  // unit direction: distance along the ray
-            if (t <= 0.0f || t > limit) continue;
-            if (t > tMin && t < h.t) {
-                h.t = t; h.s = s; h.seg = p.id;
-                h.px = px; h.py = py;
-                limit = t;
-            }
+            ray_segment_hit(p.seg, p.id, ox, oy, dx, dy, tMin, limit, h);
         }
         if (!pop()) return h;
     }

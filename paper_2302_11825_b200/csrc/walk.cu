@@ -193,6 +193,21 @@ __device__ __forceinline__ void walk_start(Walk& w, float x, float y) {
 
 // One iteration of walkSampleImpl's loop (pointwise.cpp:130-161). Returns true
 // when the walk terminated; then *value holds its estimate. The scene traits
+// Neumann ray against the straight Neumann runs (WalkEnv::runSeg): the first hit within
+// (tguard, R], the same point as on the run's own segments; no run is reachable from a
+// cell without a ray entry node (HintGrid)
+__device__ __forceinline__ RayHit ray_runs(const WalkEnv& E, float ox, float oy, float dx, float dy, float tMax,
+                                           int skip, int entry) {
+    RayHit h{kFInf, 0.0f, 0.0f, 0.0f, -1};
+    if (entry == kNoEntry) return h;
+    float limit = tMax;
+    for (int i = 0; i < E.runN; ++i) {
+        const int id = __ldg(E.runId + i);
+        if (id != skip) ray_segment_hit(__ldg(E.runSeg + i), id, ox, oy, dx, dy, E.tguard, limit, h);
+    }
+    return h;
+}
+
 // (Neumann boundary, screening, source) and the traffic counters are
 // compile-time, so each configuration runs only its own code.
 template <bool NEU, bool SCR, bool SRC, bool COUNT>
@@ -243,8 +258,9 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
     float travel = R;
     bool hit = false;
     if (NEU && !far) {
-        RayHit h = intersect_ray<COUNT>(E.S, w.x, w.y, dx, dy, R, kClsNeumann, E.tguard, w.onN ? w.prevSeg : -1,
-                                        entry.y);
+        RayHit h = E.runN ? ray_runs(E, w.x, w.y, dx, dy, R, w.onN ? w.prevSeg : -1, entry.y)
+                          : intersect_ray<COUNT>(E.S, w.x, w.y, dx, dy, R, kClsNeumann, E.tguard,
+                                                 w.onN ? w.prevSeg : -1, entry.y);
         if (h.seg >= 0) {
             hit = true;
             travel = h.t;
