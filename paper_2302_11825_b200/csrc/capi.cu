@@ -545,13 +545,15 @@ void bvc_scene_s::upload2() {
 // as one segment (the hit's normal is the run's, and a walker standing on the run
 // skips the whole line, which a ray leaving it cannot meet again). A subdivided
 // straight wall (C2: 2 x 512 segments) becomes 2 segments, tested in a loop instead of a
-// BVH traversal. Used only when the runs are few (<= 32) and merge >= 4 segments each
-// on average; curved Neumann boundaries keep the BVH.
+// BVH traversal. The same holds for the closest Dirichlet point (the closest point of a
+// straight wall is the closest point of its subdivisions) and, with the silhouette
+// candidates tested directly, for the star radius. Used only when the runs are few
+// (<= 32) and merge >= 4 segments each on average; curved boundaries keep the BVH.
 void bvc_scene_s::build_runs() {
-    runN = 0;
-    std::vector<float4> seg;
-    std::vector<int> ids;
-    int neumann = 0;
+    runN = drunN = 0;
+    std::vector<float4> seg[2];
+    std::vector<int> ids[2];
+    int count[2] = {0, 0};
     for (const auto& L : host.loops) {
         const size_t m = L.size();
         if (m == 0) continue;
@@ -560,8 +562,8 @@ void bvc_scene_s::build_runs() {
             ex = b[0] - a[0];
             ey = b[1] - a[1];
         };
-        auto joins = [&](int i, int j) {  // j continues i's straight Neumann run
-            if (!host.label[i] || !host.label[j] || host.idx[2 * i + 1] != host.idx[2 * j]) return false;
+        auto joins = [&](int i, int j) {  // j continues i's straight run of the same label
+            if (host.label[i] != host.label[j] || host.idx[2 * i + 1] != host.idx[2 * j]) return false;
             double ax, ay, bx, by;
             dir(i, ax, ay);
             dir(j, bx, by);
@@ -580,21 +582,29 @@ void bvc_scene_s::build_runs() {
             const int first = L[(s0 + c) % m];
             size_t len = 1;
             while (c + len < m && joins(L[(s0 + c + len - 1) % m], L[(s0 + c + len) % m])) ++len;
-            if (host.label[first]) {
-                const int last = L[(s0 + c + len - 1) % m];
-                const double *a = host.vert(host.idx[2 * first]), *b = host.vert(host.idx[2 * last + 1]);
-                seg.push_back(make_float4(a[0], a[1], b[0], b[1]));
-                ids.push_back(first);
-                neumann += static_cast<int>(len);
-            }
+            const int last = L[(s0 + c + len - 1) % m];
+            const double *a = host.vert(host.idx[2 * first]), *b = host.vert(host.idx[2 * last + 1]);
+            const int lab = host.label[first] ? 1 : 0;
+            seg[lab].push_back(make_float4(a[0], a[1], b[0], b[1]));
+            ids[lab].push_back(first);
+            count[lab] += static_cast<int>(len);
             c += len;
         }
     }
-    const int n = static_cast<int>(seg.size());
-    if (n == 0 || n > 32 || 4 * n > neumann) return;
-    runSeg.upload(seg.data(), n);
-    runId.upload(ids.data(), n);
-    runN = n;
+    // Neumann runs answer the rays; Dirichlet runs (with the silhouette candidates, when
+    // few) answer the star and closest-point queries of the walks
+    const int nN = static_cast<int>(seg[1].size()), nD = static_cast<int>(seg[0].size());
+    if (nN > 0 && nN <= 32 && 4 * nN <= count[1]) {
+        runSeg.upload(seg[1].data(), nN);
+        runId.upload(ids[1].data(), nN);
+        runN = nN;
+    }
+    const int nSil = static_cast<int>(host.silAlways.size());
+    if (nD > 0 && nD <= 32 && 4 * nD <= count[0] && nSil <= 32 && (host.neumannMeasure == 0.0 || runN > 0)) {
+        drunSeg.upload(seg[0].data(), nD);
+        drunId.upload(ids[0].data(), nD);
+        drunN = nD;
+    }
 }
 
 

@@ -15,6 +15,10 @@ WalkEnv make_env(bvc_scene_s* S, const bvc_problem& pb, const bvc_walk_config& w
     E.runSeg = S->runSeg.p;
     E.runId = S->runId.p;
     E.runN = S->runN;
+    E.drunSeg = S->drunSeg.p;
+    E.drunId = S->drunId.p;
+    E.drunN = S->drunN;
+    E.nSil = static_cast<int>(S->host.silAlways.size());
     E.P.screened = pb.kernel.kind == BVC_KERNEL_SCREENED;
     E.P.sigma = static_cast<float>(pb.kernel.sigma);
     E.P.sqrtSigma = static_cast<float>(std::sqrt(pb.kernel.sigma));

@@ -271,9 +271,9 @@ struct bvc_scene_s {
     void gpu_build(int dim, const float4* a, const float4* b, const float4* c, const int2* sil);
 
     // straight Neumann runs for the walks' rays (2D; WalkEnv::runSeg)
-    DevBuf<float4> runSeg;
-    DevBuf<int> runId;
-    int runN = 0;
+    DevBuf<float4> runSeg, drunSeg;  // Neumann runs (rays), Dirichlet runs (star queries)
+    DevBuf<int> runId, drunId;
+    int runN = 0, drunN = 0;
     void build_runs();
     void upload2();
     void upload3();

@@ -66,6 +66,11 @@ struct WalkEnv {
     const float4* runSeg;
     const int* runId;  // a segment of the run (its normal is the run's)
     int runN;
+    // with Dirichlet runs (drunN > 0) the star / closest-point queries test the runs and
+    // the silhouette candidates (S.silP, nSil of them) directly, without the BVH
+    const float4* drunSeg;
+    const int* drunId;
+    int drunN, nSil;
     DevProblem P;
     float eps, rmin, tguard, insideTol, scale, nudge;
     float cx, cy, escape;  // scene box centre and escape half-width

@@ -193,6 +193,28 @@ __device__ __forceinline__ void walk_start(Walk& w, float x, float y) {
 
 // One iteration of walkSampleImpl's loop (pointwise.cpp:130-161). Returns true
 // when the walk terminated; then *value holds its estimate. The scene traits
+// star query against the straight Dirichlet runs and the silhouette candidates
+// (WalkEnv::drunSeg): the closest Dirichlet point of the runs (the closest point of a
+// straight wall is that of its subdivisions) and the closest visible silhouette nearer
+// than it (pointwise.cpp:136-138), as star_query returns them
+__device__ __forceinline__ StarQuery star_runs(const WalkEnv& E, float x, float y, bool sil) {
+    StarQuery q;
+    q.D = Closest{kFInf, 0.0f, 0.0f, 0.0f, -1};
+    q.s2 = kFInf;
+    for (int i = 0; i < E.drunN; ++i) {
+        float px, py, t;
+        const float d2 = seg_closest(__ldg(E.drunSeg + i), x, y, px, py, t);
+        if (d2 < q.D.d2) q.D = Closest{d2, px, py, t, __ldg(E.drunId + i)};
+    }
+    if (sil) {
+        for (int k = 0; k < E.nSil; ++k) {
+            float d2;
+            if (silhouette_ok(E.S, k, x, y, d2) && d2 < fminf(q.s2, q.D.d2)) q.s2 = d2;
+        }
+    }
+    return q;
+}
+
 // Neumann ray against the straight Neumann runs (WalkEnv::runSeg): the first hit within
 // (tguard, R], the same point as on the run's own segments; no run is reachable from a
 // cell without a ray entry node (HintGrid)
@@ -220,9 +242,16 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
     // holds no boundary point, so no Neumann crossing and no Neumann-data term either
     const float lb = E.ff.d ? farfield_bound(E.ff, w.x, w.y) : -1.0f;
     const bool far = lb >= E.ff.tau;
-    const int2 entry = far ? make_int2(0, 0) : entry_at(E.hg, w.x, w.y);
+    const int2 entry = (far || E.drunN) ? make_int2(0, 0) : entry_at(E.hg, w.x, w.y);
     if (far) {
         R = lb;
+    } else if (E.drunN) {  // straight-run scene: no BVH (bvc_scene_s::build_runs)
+        StarQuery q = star_runs(E, w.x, w.y, NEU);
+        cp = q.D;
+        float dD = sqrtf(cp.d2);
+        if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
+        R = NEU ? fminf(dD, sqrtf(q.s2)) : dD;
+        w.lastD = cp.seg;
     } else {
         // (scenes without Dirichlet segments are rejected on the host, pointwise.cpp:217-218)
         if constexpr (NEU) {
@@ -290,7 +319,7 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
     bool escaped = fabsf(w.x - E.cx) > E.escape || fabsf(w.y - E.cy) > E.escape;
     if (++w.step >= E.maxSteps || escaped) {  // truncation: g at the closest Dirichlet point (pointwise.cpp:162-164)
         trunc = 1;
-        Closest c = closest_point(E.S, w.x, w.y, kClsD);
+        Closest c = E.drunN ? star_runs(E, w.x, w.y, false).D : closest_point(E.S, w.x, w.y, kClsD);
         value = w.acc + w.weight * g_value(E, c);
         return true;
     }
