@@ -551,6 +551,8 @@ void bvc_scene_s::upload2() {
 // (<= 32) and merge >= 4 segments each on average; curved boundaries keep the BVH.
 void bvc_scene_s::build_runs() {
     runN = drunN = 0;
+    if (const char* e = std::getenv("BVC_RUNS"))  // 0: always query through the BVH (tests, A/B)
+        if (std::string(e) == "0") return;
     std::vector<float4> seg[2];
     std::vector<int> ids[2];
     int count[2] = {0, 0};

@@ -154,3 +154,40 @@ def test_farfield_option_stays_within_the_eps_shell_bias(monkeypatch):
         e = B.wos_solve(sc, pb, [x], _wc(200000, seed=9))
         m, se = e["mean"][0], e["se"][0]
         assert abs(m - exact) <= Z * se + 2e-3, (x, m, se, exact)
+
+
+def test_straight_runs_answer_the_queries_like_the_bvh():
+    """Straight-run scenes (bvc_scene_s::build_runs) answer star / closest-point queries and
+    Neumann rays from merged collinear segments instead of the BVH: the same geometry, so
+    the walks draw the same Philox streams and take the same decisions up to FP32
+    rounding at ties. Square-mixed caches built both ways agree sample by sample."""
+    import os
+
+    from paper_2302_11825_b200 import configs
+
+    c2 = configs.config2()  # [-1,1]^2, 4 x 512 segments: 2 Dirichlet and 2 Neumann straight runs
+    geom, pb = (c2.vertices, c2.segments, c2.labels), c2.problem
+    cfg = B.cache_config(B.walk_config(epsilon=1e-3), nBoundary=2048, nWalksNeumann=64, nWalksDirichlet=64,
+                         offset=c2.region_offset)
+
+    def cache(runs):
+        old = os.environ.get("BVC_RUNS")
+        os.environ["BVC_RUNS"] = runs
+        try:
+            sc = _scene(geom)
+            region = B.SolveRegion(sc, offset=c2.region_offset, epsilon=1e-3)
+            st = {}
+            c = B.generate_boundary_cache(sc, pb, region, cfg, 21, 0, stats=st).download()
+        finally:
+            if old is None:
+                os.environ.pop("BVC_RUNS")
+            else:
+                os.environ["BVC_RUNS"] = old
+        return c, st
+
+    a, sa = cache("1")
+    b, sb = cache("0")
+    for k in ("uHat", "dHat"):
+        d = np.abs(a[k] - b[k])
+        assert np.mean(d > 1e-5) < 0.02, (k, np.mean(d > 1e-5))  # identical walks but for rounding ties
+    assert abs(sa["cacheSteps"] - sb["cacheSteps"]) <= 1e-3 * sb["cacheSteps"]
