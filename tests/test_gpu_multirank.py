@@ -77,7 +77,7 @@ def _single(n_boundary):
     return state, walks, (sc, region, pb, cfg, x)
 
 
-@pytest.mark.parametrize("n_boundary", [1024, 1001])  # even and padded (uneven) shards
+@pytest.mark.parametrize("n_boundary", [1024, 1001, 1])  # even, padded, and an empty shard
 def test_two_rank_sharded_round_equals_single_gpu_round(n_boundary):
     import torch.multiprocessing as mp
 
