@@ -447,7 +447,7 @@ int bvc_streamlines_write_csv(const char* path, const double* seeds, int nSeeds,
 /* ---- pointwise estimators (pointwise.h:62-76), batched over n points -------- */
 /* point i uses cfg->stream for i == 0 when n == 1, else streams[i] (NULL => mixKey(stream,i)).
    x (and normal) hold the scene's dimension per point: 2D as the reference, and the 3D
-   lift for triangle meshes (solve and normal derivative; the gradient estimate is 2D) */
+   lift for triangle meshes (bvc_wost_gradient3 for the 3D gradient) */
 int bvc_wos_solve(bvc_scene scene, const bvc_problem* problem, const double* x, size_t n,
                   const bvc_walk_config* cfg, const uint64_t* streams, bvc_scalar_estimate* out);
 int bvc_wost_solve(bvc_scene scene, const bvc_problem* problem, const double* x, size_t n,
@@ -455,6 +455,11 @@ int bvc_wost_solve(bvc_scene scene, const bvc_problem* problem, const double* x,
 int bvc_wost_gradient(bvc_scene scene, const bvc_problem* problem, const double* x, size_t n,
                       const bvc_walk_config* cfg, const uint64_t* streams,
                       bvc_vector_estimate* out);
+/* the 3D lift of wostGradient on triangle meshes: mean/se are 3*n (x, y, z per point),
+   count / truncated n each (may be NULL) */
+int bvc_wost_gradient3(bvc_scene scene, const bvc_problem* problem, const double* x, size_t n,
+                       const bvc_walk_config* cfg, const uint64_t* streams, double* mean, double* se,
+                       long long* count, long long* truncated);
 int bvc_wost_normal_derivative(bvc_scene scene, const bvc_problem* problem, const double* x,
                                const double* normal, size_t n, const bvc_walk_config* cfg,
                                const uint64_t* streams, bvc_scalar_estimate* out);

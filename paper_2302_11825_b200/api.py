@@ -38,7 +38,7 @@ SYMBOLS = (
     "bvc_grid_save_pgm bvc_streamlines_write_csv bvc_pipe_probe bvc_boundary_cache_assign_voronoi "
     "bvc_fallback_walks bvc_update_solution_host bvc_update_solution_with_evaluator bvc_generate_boundary_cache_shard_fallback "
     "bvc_points_set_index_base bvc_comm_unique_id bvc_comm_init_nccl bvc_comm_init_callback bvc_comm_info "
-    "bvc_comm_destroy bvc_shard_layout bvc_update_solution_sharded bvc_update_solution_sharded_host"
+    "bvc_comm_destroy bvc_shard_layout bvc_update_solution_sharded bvc_update_solution_sharded_host bvc_wost_gradient3"
 ).split()
 
 
@@ -763,7 +763,17 @@ def wost_solve(scene, pb, x, cfg, streams=None):
 
 
 def wost_gradient(scene, pb, x, cfg, streams=None):
-    """wostGradient (pointwise.h:71-72), batched."""
+    """wostGradient (pointwise.h:71-72), batched; 3D meshes through bvc_wost_gradient3."""
+    if scene.dim == 3:
+        x = _f64(x, 3)
+        n = len(x)
+        mean, se = np.zeros((n, 3)), np.zeros((n, 3))
+        count, trunc = np.zeros(n, np.int64), np.zeros(n, np.int64)
+        st = np.ascontiguousarray(streams, dtype=np.uint64) if streams is not None else None
+        _check(lib().bvc_wost_gradient3(scene.h, C.byref(pb), _ptr(x), C.c_size_t(n), C.byref(cfg),
+                                        _ptr(st, C.c_uint64) if st is not None else None, _ptr(mean), _ptr(se),
+                                        _ptr(count, C.c_longlong), _ptr(trunc, C.c_longlong)))
+        return dict(mean=mean, se=se, count=count, truncated=trunc)
     return _estimates(lib().bvc_wost_gradient, scene, pb, x, cfg, streams, vector=True)
 
 

@@ -11,7 +11,7 @@ namespace bvc_capi {
 void pointwise3(bvc_scene_s* S, const bvc_problem& pb, const double* x, const double* normal, size_t n,
                 const bvc_walk_config& cfg, const uint64_t* streams, int mode, double* mean, double* se,
                 long long* count, long long* trunc) {
-    need(mode != 1, "3D gradient estimates need 3 components: the ABI's vector estimate is 2D (pointwise.h:54-59)");
+    // mode 1: the 3-component gradient (bvc_wost_gradient3)
     WalkEnv3 E = make_env3(S, pb, cfg, cfg.seed, kPointwiseSalt, 0);
     const int nw = std::max(1, cfg.nWalks);
     const int ni = static_cast<int>(n);
@@ -67,36 +67,45 @@ void pointwise3(bvc_scene_s* S, const bvc_problem& pb, const double* x, const do
         for (size_t i = 0; i < n; ++i) hr[i] = static_cast<float>(std::max(hd[i], static_cast<double>(E.rmin)));
         float* rD = ws().get<float>(kWsRD, n);
         CK(cudaMemcpyAsync(rD, hr.data(), n * sizeof(float), cudaMemcpyHostToDevice, g_stream));
-        std::vector<float4> hn(n);
-        for (size_t i = 0; i < n; ++i)
-            hn[i] = make_float4(static_cast<float>(normal[3 * i]), static_cast<float>(normal[3 * i + 1]),
-                                static_cast<float>(normal[3 * i + 2]), 0.f);
-        float4* dn = ws().get<float4>(kWsND, n);
-        CK(cudaMemcpyAsync(dn, hn.data(), n * sizeof(float4), cudaMemcpyHostToDevice, g_stream));
         J.nD = nw;
         J.nPtsD = ni;
         J.xD = px;
         J.radiusD = rD;
         J.gidD = dg;
         J.truncD = tr;
-        J.normalD = dn;
-        J.outD = ws().get<float>(kWsOutD, n * nw);
+        if (mode == 2) {
+            std::vector<float4> hn(n);
+            for (size_t i = 0; i < n; ++i)
+                hn[i] = make_float4(static_cast<float>(normal[3 * i]), static_cast<float>(normal[3 * i + 1]),
+                                    static_cast<float>(normal[3 * i + 2]), 0.f);
+            float4* dn = ws().get<float4>(kWsND, n);
+            CK(cudaMemcpyAsync(dn, hn.data(), n * sizeof(float4), cudaMemcpyHostToDevice, g_stream));
+            J.normalD = dn;
+        }
+        J.outD = ws().get<float>(kWsOutD, n * nw * (mode == 1 ? 3 : 1));
     }
     launch_walk_job3(E, J, g_stream);
+    const int comps = mode == 1 ? 3 : 1;
     const float* vals = mode == 0 ? J.outU : J.outD;
-    double* dm = ws().get<double>(kWsMean, n);
-    double* ds = ws().get<double>(kWsSe, n);
-    launch_reduce_estimates(vals, ni, nw, 1, 0, dm, ds, g_stream);
+    double* dm = ws().get<double>(kWsMean, n * comps);
+    double* ds = ws().get<double>(kWsSe, n * comps);
+    for (int c = 0; c < comps; ++c) launch_reduce_estimates(vals, ni, nw, comps, c, dm + c * n, ds + c * n, g_stream);
+    std::vector<double> hm(n * comps), hs(n * comps);
     std::vector<int> ht(n);
-    CK(cudaMemcpyAsync(mean, dm, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
-    CK(cudaMemcpyAsync(se, ds, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaMemcpyAsync(hm.data(), dm, n * comps * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaMemcpyAsync(hs.data(), ds, n * comps * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
     CK(cudaMemcpyAsync(ht.data(), tr, n * sizeof(int), cudaMemcpyDeviceToHost, g_stream));
     CK(cudaStreamSynchronize(g_stream));
     for (size_t i = 0; i < n; ++i) {
+        for (int c = 0; c < comps; ++c) {
+            mean[comps * i + c] = hm[c * n + i];
+            se[comps * i + c] = hs[c * n + i];
+        }
         count[i] = nw;
         trunc[i] = ht[i];
-        if (!std::isfinite(mean[i])) throw Error(BVC_ERR_SOLVER, "walk cannot terminate: scene has no Dirichlet boundary");
     }
+    for (size_t i = 0; i < n * comps; ++i)
+        if (!std::isfinite(mean[i])) throw Error(BVC_ERR_SOLVER, "walk cannot terminate: scene has no Dirichlet boundary");
 }
 
 // estimator job over host points (pointwise.h:62-76)
@@ -450,6 +459,7 @@ int bvc_wost_gradient(bvc_scene s, const bvc_problem* pb, const double* x, size_
                       const uint64_t* streams, bvc_vector_estimate* out) {
     API({
         need(s && pb && cfg && out, "null argument");
+        need(s->host.dim == 2, "bvc_wost_gradient is the 2D gradient (3D: bvc_wost_gradient3)");
         std::vector<double> m(2 * n), se(2 * n);
         std::vector<long long> c(n), t(n);
         pointwise(s, *pb, x, nullptr, n, *cfg, streams, 1, m.data(), se.data(), c.data(), t.data());
@@ -460,6 +470,19 @@ int bvc_wost_gradient(bvc_scene s, const bvc_problem* pb, const double* x, size_
             out[i].se[1] = se[2 * i + 1];
             out[i].count = c[i];
             out[i].truncated = t[i];
+        }
+    })
+}
+int bvc_wost_gradient3(bvc_scene s, const bvc_problem* pb, const double* x, size_t n, const bvc_walk_config* cfg,
+                       const uint64_t* streams, double* mean, double* se, long long* count, long long* truncated) {
+    API({
+        need(s && pb && cfg && mean && se, "null argument");
+        need(s->host.dim == 3, "bvc_wost_gradient3 is the 3D gradient (2D: bvc_wost_gradient)");
+        std::vector<long long> c(n), t(n);
+        pointwise(s, *pb, x, nullptr, n, *cfg, streams, 1, mean, se, c.data(), t.data());
+        for (size_t i = 0; i < n; ++i) {
+            if (count) count[i] = c[i];
+            if (truncated) truncated[i] = t[i];
         }
     })
 }

@@ -159,8 +159,9 @@ def test_c5_bvc_agrees_with_pointwise_walks():
 
 
 def test_pointwise_3d_matches_harmonic_data(sphere):
-    """The 3D lift of wostSolve / wostNormalDerivative (pointwise.h:66-76): on the sphere with
-    harmonic data the estimates are unbiased for u = g and du/dn = n . grad g."""
+    """The 3D lift of wostSolve / wostGradient / wostNormalDerivative (pointwise.h:66-76): on
+    the sphere with harmonic data the estimates are unbiased for u = g, grad u = grad g and
+    du/dn = n . grad g."""
     _, _, sc = sphere
     pb = B.problem(B.poisson(3), g=HARMONIC)
     rng = np.random.default_rng(4)
@@ -176,3 +177,7 @@ def test_pointwise_3d_matches_harmonic_data(sphere):
     dgdn = (g_exact(x + h * n) - g_exact(x - h * n)) / (2 * h)
     zd = (d["mean"] - dgdn) / np.maximum(d["se"], 1e-12)
     assert np.sum(np.abs(zd) > 3) <= 1, zd
+    gr = B.wost_gradient(sc, pb, x, B.walk_config(epsilon=1e-3, nWalks=16384, seed=11))
+    grad = np.stack([0.3 - x[:, 0] + x[:, 1], -0.2 - x[:, 1] + x[:, 0], 0.5 + 2 * x[:, 2]], 1)
+    zg = (gr["mean"] - grad) / np.maximum(gr["se"], 1e-12)
+    assert np.sum(np.abs(zg) > 3) <= 2, zg
