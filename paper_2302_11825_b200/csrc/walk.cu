@@ -191,8 +191,6 @@ __device__ __forceinline__ void walk_start(Walk& w, float x, float y) {
     w.onN = 0; w.prevSeg = -1; w.step = 0; w.lastD = -1;
 }
 
-// One iteration of walkSampleImpl's loop (pointwise.cpp:130-161). Returns true
-// when the walk terminated; then *value holds its estimate. The scene traits
 // star query against the straight Dirichlet runs and the silhouette candidates
 // (WalkEnv::drunSeg): the closest Dirichlet point of the runs (the closest point of a
 // straight wall is that of its subdivisions) and the closest visible silhouette nearer
@@ -230,6 +228,8 @@ __device__ __forceinline__ RayHit ray_runs(const WalkEnv& E, float ox, float oy,
     return h;
 }
 
+// One iteration of walkSampleImpl's loop (pointwise.cpp:130-161). Returns true
+// when the walk terminated; then *value holds its estimate. The scene traits
 // (Neumann boundary, screening, source) and the traffic counters are
 // compile-time, so each configuration runs only its own code.
 template <bool NEU, bool SCR, bool SRC, bool COUNT>
