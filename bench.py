@@ -307,6 +307,9 @@ def run_gpu(args):
         out["e2e"] = e2e
         if world == 1 and not args.no_cpu:
             out["cpu_baseline"] = cpu_baseline(c, args.cpu_sample_s)
+            wps = out["cpu_baseline"].get("walks_per_s")
+            if wps and out.get("walk_stats"):
+                out["cpu_baseline"]["steps_per_s_derived"] = wps * out["walk_stats"]["steps_per_walk"]
         if world == 1 and args.extra_configs:
             out["other_configs"] = other_configs(args)
         print(json.dumps(out), flush=True)
@@ -536,6 +539,8 @@ def reference_round_estimate(c, sample_s=20.0, threads=0):
             break
         n_sub = min(N, int(n_sub * max(2.0, 0.4 * sample_s / max(t_gen, 1e-3) * 0.8)))
     gen_full = t_gen * N / n_sub
+    # the reference's walk throughput (RoundStats cacheWalks / generation time, cache.cpp:381-387)
+    sample_walks = int(small["stats"][1]) if "stats" in small else 0
     # gather: the reference splats on a point subset against a full-size cache
     rng = np.random.default_rng(0)
     reps = int(np.ceil(N / n_sub))
@@ -575,7 +580,10 @@ def reference_round_estimate(c, sample_s=20.0, threads=0):
                        f"{'+splatGradient' if c.gradients else ''} on {len(xs)}/{len(act)} points vs a full "
                        f"{N}+{M}-sample cache ({t_spl:.2f} s); rate = full-round pairs / round time extrapolated "
                        "linearly from the sample (cost ~ walks, ~ K(N+M))"),
-            "round_seconds_extrapolated": t_round}
+            "round_seconds_extrapolated": t_round,
+            "walks_per_s": sample_walks / t_gen if t_gen > 0 and sample_walks else None,
+            "walks_note": "the reference's walks/s in its generateBoundaryCache sample (RoundStats.cacheWalks / time); "
+                          "CPU steps/s = walks/s x the GPU's mean steps per walk (derived, the reference counts no steps)"}
 
 
 def port_gather_3d(c, sample_s, threads=0):
