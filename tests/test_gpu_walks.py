@@ -191,3 +191,49 @@ def test_straight_runs_answer_the_queries_like_the_bvh():
         d = np.abs(a[k] - b[k])
         assert np.mean(d > 1e-5) < 0.02, (k, np.mean(d > 1e-5))  # identical walks but for rounding ties
     assert abs(sa["cacheSteps"] - sb["cacheSteps"]) <= 1e-3 * sb["cacheSteps"]
+
+
+def test_straight_runs_with_reflex_neumann_corner():
+    """Straight-run queries when the scene has silhouette candidates: an L-shaped domain whose
+    reflex corner joins two Neumann walls (a silhouette vertex, scene.cpp:85-114), every wall
+    subdivided; run-mode and BVH caches agree sample by sample but for rounding ties."""
+    import os
+
+    corners = [(0.0, 0.0), (2.0, 0.0), (2.0, 1.0), (1.0, 1.0), (1.0, 2.0), (0.0, 2.0)]
+    neumann_edges = {2, 3}  # (2,1)->(1,1) and (1,1)->(1,2): the reflex corner at (1,1)
+    per_unit = 64
+    verts, labels = [], []
+    for e, (a, b) in enumerate(zip(corners, corners[1:] + corners[:1])):
+        n = int(round(per_unit * max(abs(b[0] - a[0]), abs(b[1] - a[1]))))
+        for k in range(n):
+            t = k / n
+            verts.append((a[0] + t * (b[0] - a[0]), a[1] + t * (b[1] - a[1])))
+            labels.append(1 if e in neumann_edges else 0)
+    v = np.array(verts)
+    segs = np.stack([np.arange(len(v)), (np.arange(len(v)) + 1) % len(v)], 1).astype(np.int32)
+    lab = np.array(labels, np.int32)
+    pb = H.make_problem(H.kspec(), g=abi.make_field(abi.FIELD_LINEAR, [1, 0, 0, 0]))
+    cfg = B.cache_config(B.walk_config(epsilon=1e-3), nBoundary=2048, nWalksNeumann=64, nWalksDirichlet=64,
+                         offset=0.01)
+
+    def cache(runs):
+        old = os.environ.get("BVC_RUNS")
+        os.environ["BVC_RUNS"] = runs
+        try:
+            sc = B.Scene(v, segs, lab)
+            region = B.SolveRegion(sc, offset=0.01, epsilon=1e-3)
+            st = {}
+            c = B.generate_boundary_cache(sc, pb, region, cfg, 33, 0, stats=st).download()
+        finally:
+            if old is None:
+                os.environ.pop("BVC_RUNS")
+            else:
+                os.environ["BVC_RUNS"] = old
+        return c, st
+
+    a, sa = cache("1")
+    b, sb = cache("0")
+    for k in ("uHat", "dHat"):
+        d = np.abs(a[k] - b[k])
+        assert np.mean(d > 1e-5) < 0.03, (k, np.mean(d > 1e-5))
+    assert abs(sa["cacheSteps"] - sb["cacheSteps"]) <= 2e-3 * sb["cacheSteps"]
