@@ -257,6 +257,8 @@ def run_gpu(args):
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) / 1e3)
+        st = dict(st)
+        st["kernelSeconds"] = B.last_round_kernel_seconds()  # the round's main walk / gather launches
         per_step.append(st)
     torch.cuda.synchronize()
     barrier()
@@ -302,7 +304,9 @@ def run_gpu(args):
         # phase times measured live inside the timed steps: the round's own CUDA events on
         # the library stream (RoundStats generateSeconds / splatSeconds)
         live = {"cache_generation": float(np.mean([s["generateSeconds"] for s in per_step])),
-                "gather": float(np.mean([s["splatSeconds"] for s in per_step]))}
+                "gather": float(np.mean([s["splatSeconds"] for s in per_step])),
+                "walk_kernel": float(np.mean([s["kernelSeconds"]["walk"] for s in per_step])),
+                "gather_kernel": float(np.mean([s["kernelSeconds"]["gather"] for s in per_step]))}
         out.update(phase_breakdown(B, c, scene, region, pts, args, per_step[-1], live, k_active))
         out["e2e"] = e2e
         if world == 1 and not args.no_cpu:
@@ -386,6 +390,10 @@ def phase_breakdown(B, c, scene, region, pts, args, stats, live, k_active):
                                     "note": "every pair in FP64 (rcp/rsqrt: FP32 seed + 2 Newton steps, libdevice "
                                             "log); parity with the reference's double loop <= 1e-12 (tests)"}
     t_gen, t_gather = live["cache_generation"], live["gather"]
+    # the rooflines divide by the dominant launches' own durations (events around the main
+    # cache-walk launch and the main gather launch inside each timed round); the phase
+    # times (pack/prologue, finalize, sampling, reductions included) are reported beside them
+    k_walk, k_gather = live.get("walk_kernel") or t_gen, live.get("gather_kernel") or t_gather
     peaks = load_peaks()
     # walk traffic: SURVEY §8(d) algorithmic bytes per step (packed fp32 node 32 B, 2D segment
     # 16 + 4 B, 3D triangle 36 + 4 B, walk state 32 B) x the fetch counts of a counting launch
@@ -394,7 +402,7 @@ def phase_breakdown(B, c, scene, region, pts, args, stats, live, k_active):
     node_b, prim_b = 32, (40 if c.dim == 3 else 20)
     bytes_per_step = (prof["node_fetches"] * node_b + prof["prim_fetches"] * prim_b) / steps + 32.0
     walk_bytes = bytes_per_step * stats["cacheSteps"]
-    walk_achieved = walk_bytes / t_gen / 1e9
+    walk_achieved = walk_bytes / k_walk / 1e9
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     # gather bound: SMs * f_SM / max(F/128, S/16) pairs/s
     props = torch.cuda.get_device_properties(0)
@@ -406,7 +414,7 @@ def phase_breakdown(B, c, scene, region, pts, args, stats, live, k_active):
         key = ("scr2_ugrad" if c.problem.kernel.kind else "lap2_ugrad") if c.gradients else "lap2_u"
     F, S = PER_PAIR[key]
     bound = sms * f_sm / max(F / 128.0, S / 16.0)
-    gather_rate = pairs / t_gather
+    gather_rate = pairs / k_gather
     if args.no_probe:  # profiling runs: reuse the committed measurement
         pipes = json.load(open(os.path.join(ROOT, "profiles", "r1_pipe_peaks.json")))["rates"]
         pipes = {k: v["per_s"] for k, v in pipes.items()}
@@ -437,7 +445,7 @@ def phase_breakdown(B, c, scene, region, pts, args, stats, live, k_active):
     dominant = "walk" if t_gen >= t_gather else "gather"
     roof = dict(walk_roof if dominant == "walk" else gather_roof)
     roof["dominant"] = dominant
-    roof["timing"] = ("live: mean of the round's device events over the timed steps" if args.config != 1 or live
+    roof["timing"] = ("live: mean over the timed steps of the launch's own device events" if args.config != 1 or live
                       else "one extra round")
     return {
         **extra,
@@ -446,6 +454,8 @@ def phase_breakdown(B, c, scene, region, pts, args, stats, live, k_active):
                        "truncated_fraction": stats["cacheTruncated"] / max(stats["cacheWalks"], 1),
                        "walks": stats["cacheWalks"]},
         "phases_s": {"cache_generation": t_gen, "gather": t_gather},
+        "kernel_s": {"walk": k_walk, "gather": k_gather,
+                     "note": "the round's main cache-walk and gather launches (events on the library stream)"},
         "roofline": roof,
         "walk_roofline": walk_roof,
         "gather_roofline": gather_roof,
@@ -713,6 +723,7 @@ def other_configs(args):
             res[f"C{cid}"] = {"workload": d["config"]["workload"], "ms_per_step": d["ms_per_step"],
                               "step_ms": d["step_ms"], "value": d["value"], "unit": d["unit"],
                               "e2e_ms_per_call": d["e2e"]["ms_per_step"], "phases_s": d.get("phases_s"),
+                              "kernel_s": d.get("kernel_s"),
                               "gather_frac_of_bound": d.get("gather_roofline", {}).get("frac"),
                               "walk_steps_per_s": d.get("walk_steps_per_s"), "clocks": d.get("clocks")}
             if "gather_fp64" in d:  # C1's fp64 variant (BASELINE configs[0])

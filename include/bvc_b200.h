@@ -197,6 +197,10 @@ int bvc_set_stream(void* cuda_stream);       /* stream for all subsequent launch
 int bvc_synchronize(void);
 /* launches of this library's kernels since process start (bench gpu_launches) */
 long long bvc_kernel_launch_count(void);
+/* device time (CUDA events on the launching stream) of the main cache-walk launch and the
+   main gather launch of this thread's last updateSolution round (plain or sharded), in
+   seconds; 0 for a kernel that round did not launch (the rooflines' per-launch durations) */
+int bvc_last_round_kernel_seconds(double* walkSeconds, double* gatherSeconds);
 /* pipe / cache microbenchmarks behind the rooflines: which = 0 FFMA,
    1 MUFU.LG2, 2 MUFU.RCP, 3 DFMA, 4 MUFU.RSQ, 5 MUFU.EX2 (instructions/s, per GPU),
    6 L2-resident read bandwidth (bytes/s), 7 FFMA / 8 FMUL / 9 FADD with register

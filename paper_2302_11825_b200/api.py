@@ -38,7 +38,8 @@ SYMBOLS = (
     "bvc_grid_save_pgm bvc_streamlines_write_csv bvc_pipe_probe bvc_boundary_cache_assign_voronoi "
     "bvc_fallback_walks bvc_update_solution_host bvc_update_solution_with_evaluator bvc_generate_boundary_cache_shard_fallback "
     "bvc_points_set_index_base bvc_comm_unique_id bvc_comm_init_nccl bvc_comm_init_callback bvc_comm_info "
-    "bvc_comm_destroy bvc_shard_layout bvc_update_solution_sharded bvc_update_solution_sharded_host bvc_wost_gradient3"
+    "bvc_comm_destroy bvc_shard_layout bvc_update_solution_sharded bvc_update_solution_sharded_host bvc_wost_gradient3 "
+    "bvc_last_round_kernel_seconds"
 ).split()
 
 
@@ -122,6 +123,14 @@ def _ptr(a, t=C.c_double):
 
 def launch_count() -> int:
     return int(lib().bvc_kernel_launch_count())
+
+
+def last_round_kernel_seconds() -> dict:
+    """Device time of the main cache-walk launch and the main gather launch of this
+    thread's last updateSolution round (bvc_last_round_kernel_seconds; 0 = not launched)."""
+    w, g = C.c_double(0.0), C.c_double(0.0)
+    _check(lib().bvc_last_round_kernel_seconds(C.byref(w), C.byref(g)))
+    return {"walk": w.value, "gather": g.value}
 
 
 def set_stream(stream_ptr: int | None) -> None:

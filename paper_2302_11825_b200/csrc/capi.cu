@@ -31,7 +31,7 @@ struct DeviceState {
     Workspace* work = nullptr;      // main-stream scratch (lives for the process)
     cudaStream_t side = nullptr;    // second stream for work overlapping the cache walks
     Workspace* sideWork = nullptr;  // its own scratch
-    cudaEvent_t events[5] = {};     // round_event
+    cudaEvent_t events[9] = {};     // round_event
     unsigned long long* pinned = nullptr;  // GenStats::snapshot
 };
 thread_local DeviceState t_dev[kMaxDevices];
@@ -125,12 +125,41 @@ void GenStats::resolve() {
 }
 
 cudaEvent_t round_event(int which) {
-    need(which >= 0 && which < 5, "round event index");
+    need(which >= 0 && which < 9, "round event index");
     DeviceState& d = t_dev[current_device()];
     if (!d.events[which])
         CK(cudaEventCreateWithFlags(&d.events[which], which < 2 ? cudaEventDisableTiming : cudaEventDefault));
     return d.events[which];
 }
+
+namespace {
+// KernelTimer state: 0 idle, 1 armed, 2 begun, 3 ended, per kind (walk, gather)
+thread_local int t_ktState[2] = {0, 0};
+thread_local double t_ktLast[2] = {0.0, 0.0};
+}  // namespace
+
+void KernelTimer::arm() { t_ktState[0] = t_ktState[1] = 1; }
+void KernelTimer::begin(int which) {
+    if (t_ktState[which] != 1) return;
+    CK(cudaEventRecord(round_event(5 + 2 * which), g_stream));
+    t_ktState[which] = 2;
+}
+void KernelTimer::end(int which) {
+    if (t_ktState[which] != 2) return;
+    CK(cudaEventRecord(round_event(6 + 2 * which), g_stream));
+    t_ktState[which] = 3;
+}
+void KernelTimer::resolve() {
+    for (int k = 0; k < 2; ++k) {
+        t_ktLast[k] = 0.0;
+        if (t_ktState[k] == 3) {
+            CK(cudaEventSynchronize(round_event(6 + 2 * k)));
+            t_ktLast[k] = device_seconds(round_event(5 + 2 * k), round_event(6 + 2 * k));
+        }
+        t_ktState[k] = 0;
+    }
+}
+const double* KernelTimer::last() { return t_ktLast; }
 
 SideScope::SideScope() : stream(side_for_device().side), saved(g_wsActive) { g_wsActive = side_for_device().sideWork; }
 
@@ -632,6 +661,12 @@ extern "C" {
 const char* bvc_last_error(void) { return g_error.c_str(); }
 int bvc_abi_version(void) { return BVC_ABI_VERSION; }
 long long bvc_kernel_launch_count(void) { return bvc_capi::g_launches.load(); }
+int bvc_last_round_kernel_seconds(double* walkSeconds, double* gatherSeconds) {
+    const double* t = bvc_capi::KernelTimer::last();
+    if (walkSeconds) *walkSeconds = t[0];
+    if (gatherSeconds) *gatherSeconds = t[1];
+    return BVC_OK;
+}
 
 int bvc_set_device(int device) { API(require_device(); bind_device(device)) }
 int bvc_set_stream(void* s) { API(require_device(); bind_stream(static_cast<cudaStream_t>(s))) }

@@ -119,7 +119,9 @@ void run_cache_walks(bvc_scene_s* S, bvc_region_s* R, const WalkEnv& E, const bv
         CK(cudaStreamSynchronize(g_stream));
         for (size_t i = 0; i < slots; ++i) g_profileTotals[i & 1] += h[i];
     } else {
+        KernelTimer::begin(KernelTimer::kWalk);
         launch_walk_job(E, J, g_stream);
+        KernelTimer::end(KernelTimer::kWalk);
     }
     after_walk_launch();
     launch_finish_samples(samples, n, J.outU, nU, dIdx, n, J.outD, nDw, failed, g_stream, cnt, rc + 2);
@@ -234,7 +236,9 @@ void run_cache_walks3(bvc_scene_s* S, bvc_region_s* R, const WalkEnv3& E, const 
         CK(cudaStreamSynchronize(g_stream));
         for (size_t i = 0; i < slots; ++i) g_profileTotals[i & 1] += h[i];
     } else {
+        KernelTimer::begin(KernelTimer::kWalk);
         launch_walk_job3(E, J, g_stream);
+        KernelTimer::end(KernelTimer::kWalk);
     }
     after_walk_launch();
     launch_finish_samples(samples, n, J.outU, nU, dIdx, n, J.outD, nDw, failed, g_stream, cnt, rc + 2);

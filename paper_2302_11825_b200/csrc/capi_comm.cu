@@ -105,6 +105,7 @@ bvc_eval_points_s* update_round_sharded(bvc_comm_s* C, bvc_scene_s* s, const bvc
     long long b, e, cap;
     shard_layout(N, C->nranks, C->rank, b, e, cap);
     cudaEvent_t e0 = round_event(2), e1 = round_event(3), e2 = round_event(4);
+    KernelTimer::arm();
     CK(cudaEventRecord(e0, g_stream));
     // 1. the rank's shard, its band walks on the side stream
     bvc_boundary_cache_s shard;
@@ -141,6 +142,7 @@ bvc_eval_points_s* update_round_sharded(bvc_comm_s* C, bvc_scene_s* s, const bvc
     splat_round(s, pb, r, cfg, &full, sc.m ? &sc : nullptr, p, seed, round, gradients, nullptr);
     CK(cudaEventRecord(e2, g_stream));
     CK(cudaEventSynchronize(e2));
+    KernelTimer::resolve();
     st.resolve();
     if (stats) {
         stats->resampled = st.resampled;

@@ -372,7 +372,20 @@ void splat_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const b
                  bvc_boundary_cache_s* bc, bvc_source_cache_s* sc, bvc_eval_points_s* p, uint64_t seed,
                  uint64_t round, int gradients, const bvc_boundary_evaluator* correctionEval);  // capi_splat.cu
 // per-thread, per-device events reused by every round (no create/destroy per call):
-// 0-1 stream dependencies, 2-4 timing
+// 0-1 stream dependencies, 2-4 round phases, 5-8 the round's main kernels (KernelTimer)
 cudaEvent_t round_event(int which);                                             // capi.cu
+
+// Device time of a round's two hot launches (the main cache-walk job and the main gather),
+// bracketed by events on the launching stream: the rooflines' per-launch durations
+// (bvc_last_round_kernel_seconds). Armed by a round; only the first launch of each kind
+// inside it is timed, and the values are read once the round has synchronized.
+struct KernelTimer {
+    enum { kWalk = 0, kGather = 1 };
+    static void arm();                  // a round starts: forget the previous round's launches
+    static void begin(int which);       // before the launch (no-op unless armed and not yet timed)
+    static void end(int which);         // after it
+    static void resolve();              // after the round's sync: elapsed times -> last()
+    static const double* last();        // [walk, gather] seconds of the last resolved round (0 = none)
+};
 
 }  // namespace bvc_capi

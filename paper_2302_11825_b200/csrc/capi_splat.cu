@@ -36,8 +36,10 @@ void splat_launch(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_point
         double* px64 = ws().get<double>(kWsXs64, static_cast<size_t>(dim) * K);
         gather_points64(P->x.p, P->order.p + begin, K, dim, px64, g_stream);
         if (N + M > 0) {
+            KernelTimer::begin(KernelTimer::kGather);
             launch_gather64(kind, plan, pack64, N, M, px64, K, dim, cfg.coincidenceTol, val, grad, part, skipB, skipS,
                             ws().get<unsigned>(kWsUnitCtr, 1), g_stream);
+            KernelTimer::end(KernelTimer::kGather);
             launch_finalize(part, plan, K, P->order.p + begin, N, M, val, grad, dim, skipB, skipS, P->dev(), g_stream);
         }
         CK(cudaGetLastError());
@@ -61,11 +63,13 @@ void splat_launch(bvc_boundary_cache_s* b, bvc_source_cache_s* s, bvc_eval_point
         ballRs = ws().get<float>(kWsBallRs, K);
         launch_gather_f32(P->ballR.p, P->order.p + begin, K, ballRs, g_stream);
     }
-    if (N + M > 0)
+    if (N + M > 0) {
+        KernelTimer::begin(KernelTimer::kGather);
         launch_gather(kind, plan, pack, N, M, P->xs.p + static_cast<size_t>(dim) * begin, K, dim,
                       static_cast<float>(cfg.kernel.sigma), static_cast<float>(cfg.coincidenceTol), val, grad, part,
                       skipB, skipS, tileBox, unitCtr, g_stream, mode, static_cast<float>(clamp), ballRs);
-    else
+        KernelTimer::end(KernelTimer::kGather);
+    } else
         CK(cudaMemsetAsync(part, 0, sizeof(double), g_stream));
     if (N + M > 0)
         launch_finalize(part, plan, K, P->order.p + begin, N, M, val, grad, dim, skipB, skipS, P->dev(), g_stream);
@@ -251,6 +255,7 @@ void update_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const 
     r->upload();
     cudaEvent_t e0 = round_event(2), e1 = round_event(3), e2 = round_event(4);
     cudaEvent_t ready = round_event(0), sideDone = round_event(1);
+    KernelTimer::arm();
     CK(cudaEventRecord(e0, g_stream));
     CK(cudaEventRecord(ready, g_stream));  // uploads and earlier rounds precede the side stream's work
     bvc_eval_points_s* p = nullptr;
@@ -282,6 +287,7 @@ void update_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const 
     splat_round(s, pb, r, cfg, &bc, sc.m ? &sc : nullptr, p, seed, round, gradients, correctionEval);
     CK(cudaEventRecord(e2, g_stream));
     CK(cudaEventSynchronize(e2));
+    KernelTimer::resolve();
     st.resolve();
     if (stats) {
         stats->resampled = st.resampled;

@@ -1,7 +1,7 @@
 """Build a variant of libbvc_b200.so with extra nvcc defines for one source file, for A/B
 runs on the GPU box (select it with BVC_LIB=...):
     python scripts/variant_lib.py NAME SOURCE.cu -DMACRO=VALUE ...
-Output: _variants/NAME/libbvc_b200.so (git-ignored, travels with gpurun)."""
+Output: paper_2302_11825_b200/_build/variants/NAME/libbvc_b200.so (git-ignored; travels with gpurun)."""
 import os
 import subprocess
 import sys
@@ -12,7 +12,7 @@ from paper_2302_11825_b200 import build as Bd  # noqa: E402
 
 name, src, defs = sys.argv[1], sys.argv[2], sys.argv[3:]
 Bd.build()
-out = os.path.join(ROOT, "_variants", name)
+out = os.path.join(Bd.OUT, "variants", name)
 os.makedirs(out, exist_ok=True)
 obj = os.path.join(out, src + ".o")
 cmd = [Bd.NVCC, *Bd.ARCH, *Bd.FLAGS, *defs, "-c", os.path.join(Bd.CSRC, src), "-o", obj]

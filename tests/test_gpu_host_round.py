@@ -141,3 +141,20 @@ def test_two_host_threads_run_rounds_concurrently():
     for k in range(2):
         for name, v in seq[k].items():
             assert np.array_equal(np.asarray(par[k][name]), np.asarray(v), equal_nan=True), (k, name)
+
+
+@pytest.mark.parametrize("cid,scale", [(1, 1 / 16), (4, 1 / 256)])
+def test_last_round_kernel_seconds_bracket_the_hot_launches(cid, scale):
+    """bvc_last_round_kernel_seconds: the round's main walk and gather launches, each
+    inside its phase (generateSeconds / splatSeconds), reset by a round without them"""
+    c, sc, region, x, dim = _setup(cid, scale, 4000)
+    p = B.EvaluationPoints(x, dim)
+    B.mark_evaluation_points(sc, region, c.cache, p)
+    st = B.update_solution(sc, c.problem, region, c.cache, p, c.seed, 3, gradients=bool(c.gradients))
+    k = B.last_round_kernel_seconds()
+    assert 0.0 < k["walk"] <= st["generateSeconds"] * 1.001
+    assert 0.0 < k["gather"] <= st["splatSeconds"] * 1.001
+    empty = B.EvaluationPoints(x[:0], dim)
+    B.update_solution(sc, c.problem, region, c.cache, empty, c.seed, 4)
+    k2 = B.last_round_kernel_seconds()
+    assert k2["walk"] > 0.0 and k2["gather"] == 0.0  # no points: no gather launch
