@@ -241,7 +241,13 @@ HintGrid bvc_scene_s::hintgrid() {
     if (hgBuilt) return hg;
     const int dim = host.dim;
     const char* en = std::getenv("BVC_HINTGRID_N");  // vertices along the longest side
-    const int nLong = en && std::atoi(en) >= 16 ? std::atoi(en) : (dim == 2 ? 1024 : 128);  // 4 / 8 MB
+    // 3D: cells about the triangle size (1.35 sqrt(triangles) along the longest side, 64-384):
+    // a cell's candidate ball is dD(c) + 2 rho, so near the surface smaller cells give deeper
+    // entry frontiers. Walk time by vertices along the side (C4 / C5, frontier of 4):
+    // 128: 0.377 / 2.633 s, 256: 0.349 / 2.523, 384: 0.335 / 2.461, 512: 0.324 / 2.420 (one-time
+    // build 0.05 / 0.13 / 0.25 / 0.47 s; 28 B per cell: 1.6 GB at 384^3, 3.8 GB at 512^3)
+    const int n3 = static_cast<int>(std::lround(1.35 * std::sqrt(static_cast<double>(host.ns))));
+    const int nLong = en && std::atoi(en) >= 16 ? std::atoi(en) : (dim == 2 ? 1024 : std::min(384, std::max(64, n3)));
     double ext = 0.0, lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (int k = 0; k < dim; ++k) {
         lo[k] = host.lo[k];
@@ -266,7 +272,11 @@ HintGrid bvc_scene_s::hintgrid() {
     // ray lengths are max(R, rMin) with rMin <= eps; a generous 1e-2 diag covers any rMin
     const float rmin = static_cast<float>(1e-2 * host.diagonal);
     if (dim == 2) launch_hintgrid2(view(), hg, hgIds.p, hgEntry.p, rmin, g_stream);
-    else launch_hintgrid3(view3(), hg, hgIds.p, hgEntry.p, rmin, g_stream);
+    else {
+        const char* ef = std::getenv("BVC_FRONT");  // 0: one entry node per cell
+        if (!(ef && std::string(ef) == "0")) hgFront.resize(nv * front_words3());
+        launch_hintgrid3(view3(), hg, hgIds.p, hgEntry.p, hgFront.n ? hgFront.p : nullptr, rmin, g_stream);
+    }
     CK(cudaGetLastError());
     // built once per scene, possibly on another stream than its readers (the round's
     // side stream runs band walks that use it): complete it before publishing it
@@ -274,6 +284,7 @@ HintGrid bvc_scene_s::hintgrid() {
     hg.id = hgIds.p;
     const char* ee = std::getenv("BVC_ENTRY");
     hg.entry = (ee && std::string(ee) == "0") ? nullptr : hgEntry.p;
+    hg.front = (hg.entry && hgFront.n) ? hgFront.p : nullptr;
     hgBuilt = true;
     return hg;
 }

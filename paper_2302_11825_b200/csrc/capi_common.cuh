@@ -252,6 +252,7 @@ struct bvc_scene_s {
     // warm-start grid (HintGrid, internal.h), built on first walk use
     DevBuf<int> hgIds;
     DevBuf<int2> hgEntry;
+    DevBuf<int4> hgFront;  // 3D entry frontiers (HintGrid::front)
     HintGrid hg{};
     std::atomic<bool> hgBuilt{false};
     HintGrid hintgrid();

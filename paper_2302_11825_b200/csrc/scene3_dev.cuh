@@ -119,12 +119,39 @@ __device__ __forceinline__ float tri_closest(const Prim3& t, float px, float py,
 // "while-while" structure (Aila & Laine, HPG 2009): each lane descends inner nodes
 // in one loop and handles leaves in the next, so the warp switches between the two
 // code paths once per leaf instead of once per node visit
+// Entry frontiers (HintGrid::front): kFront starts per grid cell whose subtrees together
+// hold every primitive a query from the cell can need (kNoEntry = unused slot)
+#ifndef BVC_FRONT_N
+#define BVC_FRONT_N 4
+#endif
+constexpr int kFront = BVC_FRONT_N;
+constexpr int kFrontWords = (kFront + 3) / 4;  // int4 words per cell
+static_assert(kFront >= 2 && kFront <= 16, "frontier size");
+
+// `front`: the query cell's frontier (kFront starts; front[0].x replaces `start`), or
+// nullptr. The further starts are stacked at distance 0 and visited after the first.
 template <bool COUNT = false, class Visit, class Thr>
 __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, float y, float z, unsigned qmask,
-                                               Visit&& visit, Thr&& threshold, int start = 0) {
-    if (start == kNoEntry) return;
+                                               Visit&& visit, Thr&& threshold, int start = 0,
+                                               const int4* front = nullptr) {
     unsigned long long stack[kStack];  // (distance bits << 32 | ref): one local load per pop
-    int sp = 0, ref = start;
+    int sp = 0;
+    if (front) {
+#pragma unroll
+        for (int k = kFrontWords - 1; k >= 0; --k) {
+            const int4 f = __ldg(front + k);
+            if (f.w != kNoEntry) stack[sp++] = static_cast<unsigned>(f.w);
+            if (f.z != kNoEntry) stack[sp++] = static_cast<unsigned>(f.z);
+            if (f.y != kNoEntry) stack[sp++] = static_cast<unsigned>(f.y);
+            if (k > 0) {
+                if (f.x != kNoEntry) stack[sp++] = static_cast<unsigned>(f.x);
+            } else {
+                start = f.x;
+            }
+        }
+    }
+    if (start == kNoEntry) return;
+    int ref = start;
     const F2 pxy = pk(x, y);
     auto pop = [&]() -> bool {  // next entry still within the pruning radius; false when empty
         for (;;) {
@@ -189,7 +216,7 @@ __device__ __forceinline__ Closest3 closest_on3(const SceneView3& S, int prim, f
 template <bool COUNT = false>
 __device__ __forceinline__ Closest3 closest_point3(const SceneView3& S, float x, float y, float z, unsigned qmask,
                                                    float maxD2 = kFInf, int hint = -1, int hint2 = -1,
-                                                   int start = 0) {
+                                                   int start = 0, const int4* front = nullptr) {
     Closest3 c{maxD2, 0.f, 0.f, 0.f, -1, -1};
     if (hint >= 0) {
         Closest3 h = closest_on3(S, hint, x, y, z);
@@ -206,7 +233,7 @@ __device__ __forceinline__ Closest3 closest_point3(const SceneView3& S, float x,
             float d2 = tri_closest(p, x, y, z, qx, qy, qz);
             if (d2 < c.d2) c = Closest3{d2, qx, qy, qz, __float_as_int(p.a.w), i};
         },
-        [&]() { return c.d2; }, start);
+        [&]() { return c.d2; }, start, front);
     return c;
 }
 
@@ -271,6 +298,44 @@ __device__ __forceinline__ int entry_node3(const SceneView3& S, float x, float y
         else return kNoEntry;
     }
     return ref;
+}
+
+// Up to kFront nodes whose subtrees together hold every primitive of qmask within
+// sqrt(r2) of p: entry_node3's node, then, while there is room, a frontier node whose two
+// children both qualify is replaced by them (single qualifying children are descended
+// into, nodes with none dropped). A cell straddling a high split of the tree gets deep
+// starts on both sides instead of their common ancestor. f[0] == kNoEntry: none.
+__device__ __forceinline__ void entry_frontier3(const SceneView3& S, float x, float y, float z, float r2,
+                                                unsigned qmask, int (&f)[4 * kFrontWords]) {
+    for (int k = 0; k < 4 * kFrontWords; ++k) f[k] = kNoEntry;
+    f[0] = entry_node3(S, x, y, z, r2, qmask);
+    int nf = f[0] == kNoEntry ? 0 : 1;
+    for (int guard = 0; guard < 1024; ++guard) {
+        bool changed = false;
+        for (int i = 0; i < nf; ++i) {
+            const int ref = f[i];
+            if (ref < 0) continue;  // a leaf
+            const Node3 nd = S.nodes[ref];
+            const bool vl = (nd.mask() & qmask) && box3_dist2(nd.llo, nd.lhi, x, y, z) <= r2;
+            const bool vr = ((nd.mask() >> 3) & qmask) && box3_dist2(nd.rlo, nd.rhi, x, y, z) <= r2;
+            if (vl && vr) {
+                if (nf < kFront) {
+                    f[i] = nd.left();
+                    f[nf++] = nd.right();
+                    changed = true;
+                }
+            } else if (vl || vr) {
+                f[i] = vl ? nd.left() : nd.right();
+                changed = true;
+            } else {
+                f[i] = f[--nf];
+                f[nf] = kNoEntry;
+                changed = true;
+                --i;
+            }
+        }
+        if (!changed) break;
+    }
 }
 
 // inside: boundary-inclusive within tol, then ray-crossing parity along a fixed

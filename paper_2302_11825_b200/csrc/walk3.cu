@@ -62,7 +62,7 @@ struct Star3 {
 
 template <bool COUNT>
 __device__ __forceinline__ Star3 star_query3(const WalkEnv3& E, float x, float y, float z, int hint, int hint2,
-                                             int start) {
+                                             int start, const int4* front = nullptr) {
     Star3 q{hint >= 0 ? closest_on3(E.S, hint, x, y, z) : Closest3{kFInf, 0.f, 0.f, 0.f, -1, -1}, kFInf};
     if (hint2 >= 0 && hint2 != hint) {
         Closest3 h = closest_on3(E.S, hint2, x, y, z);
@@ -100,7 +100,7 @@ __device__ __forceinline__ Star3 star_query3(const WalkEnv3& E, float x, float y
                 }
             }
         },
-        [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); }, start);
+        [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); }, start, front);
     return q;
 }
 
@@ -216,15 +216,19 @@ __device__ __forceinline__ int hint_at3(const HintGrid& G, float x, float y, flo
     return __ldg(G.id + (static_cast<size_t>(iz) * G.ny + iy) * G.nx + ix);
 }
 
-// the cell entry refs of x (HintGrid), or the root for both outside the grid
-__device__ __forceinline__ int2 entry_at3(const HintGrid& G, float x, float y, float z) {
+// the cell entry refs of x (HintGrid), or the root for both outside the grid; with the
+// entry frontiers, `front` receives the cell's kFront star / closest-point starts
+__device__ __forceinline__ int2 entry_at3(const HintGrid& G, float x, float y, float z, const int4*& front) {
+    front = nullptr;
     if (!G.entry) return make_int2(0, 0);
     const int ix = __float2int_rd((x - G.lox) * G.invH), iy = __float2int_rd((y - G.loy) * G.invH),
               iz = __float2int_rd((z - G.loz) * G.invH);
     if (static_cast<unsigned>(ix) >= static_cast<unsigned>(G.nx) || static_cast<unsigned>(iy) >= static_cast<unsigned>(G.ny) ||
         static_cast<unsigned>(iz) >= static_cast<unsigned>(G.nz))
         return make_int2(0, 0);
-    return __ldg(G.entry + (static_cast<size_t>(iz) * G.ny + iy) * G.nx + ix);
+    const size_t cell = (static_cast<size_t>(iz) * G.ny + iy) * G.nx + ix;
+    if (G.front) front = G.front + cell * kFrontWords;
+    return __ldg(G.entry + cell);
 }
 
 struct Walk3 {
@@ -259,19 +263,20 @@ __device__ __forceinline__ bool walk3_step(const WalkEnv3& E, Walk3& w, U4 rnd, 
     // far field: a ball from the distance grid, no BVH queries (FarField)
     const float lb = E.ff.d ? farfield_bound3(E.ff, w.x, w.y, w.z) : -1.0f;
     const bool far = lb >= E.ff.tau;
-    const int2 entry = far ? make_int2(0, 0) : entry_at3(E.hg, w.x, w.y, w.z);
+    const int4* front = nullptr;
+    const int2 entry = far ? make_int2(0, 0) : entry_at3(E.hg, w.x, w.y, w.z, front);
     if (far) {
         R = lb;
     } else {
         if constexpr (NEU) {
-            Star3 q = star_query3<COUNT>(E, w.x, w.y, w.z, w.lastD, hint_at3(E.hg, w.x, w.y, w.z), entry.x);
+            Star3 q = star_query3<COUNT>(E, w.x, w.y, w.z, w.lastD, hint_at3(E.hg, w.x, w.y, w.z), entry.x, front);
             cp = q.D;
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
             R = fminf(dD, sqrtf(q.s2));
         } else {
             cp = closest_point3<COUNT>(E.S, w.x, w.y, w.z, kClsD, kFInf, w.lastD, hint_at3(E.hg, w.x, w.y, w.z),
-                                       entry.x);
+                                       entry.x, front);
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
             R = dD;
@@ -627,7 +632,7 @@ void launch_walk3_t(const WalkEnv3& env, const WalkJob3& job, long long total, c
     walk3_kernel<NEU, SCR, COUNT><<<grid, kThreads3, 0, st>>>(env, job);
 }
 
-__global__ void hintgrid3_kernel(const SceneView3 S, const HintGrid G, int* id, int2* entry, float rmin) {
+__global__ void hintgrid3_kernel(const SceneView3 S, const HintGrid G, int* id, int2* entry, int4* front, float rmin) {
     long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= static_cast<long long>(G.nx) * G.ny * G.nz) return;
     int ix = static_cast<int>(i % G.nx), iy = static_cast<int>((i / G.nx) % G.ny), iz = static_cast<int>(i / (static_cast<long long>(G.nx) * G.ny));
@@ -640,10 +645,21 @@ __global__ void hintgrid3_kernel(const SceneView3 S, const HintGrid G, int* id, 
     const int star = entry_node3(S, cx, cy, cz, r * r, kClsD | kClsSil);
     const float rr = r + rmin;
     entry[i] = make_int2(star == kNoEntry ? 0 : star, entry_node3(S, cx, cy, cz, rr * rr, kClsNeumann));
+    if (front) {
+        int f[4 * kFrontWords];
+        entry_frontier3(S, cx, cy, cz, r * r, kClsD | kClsSil, f);
+        if (f[0] == kNoEntry) f[0] = 0;  // as the single entry: the root
+        for (int k = 0; k < kFrontWords; ++k)
+            front[i * kFrontWords + k] = make_int4(f[4 * k], f[4 * k + 1], f[4 * k + 2], f[4 * k + 3]);
+    }
 }
 
-void launch_hintgrid3(const SceneView3& S, const HintGrid& G, int* id, int2* entry, float rmin, cudaStream_t st) {
-    hintgrid3_kernel<<<blocks(static_cast<long long>(G.nx) * G.ny * G.nz, 128), 128, 0, st>>>(S, G, id, entry, rmin);
+int front_words3() { return kFrontWords; }
+
+void launch_hintgrid3(const SceneView3& S, const HintGrid& G, int* id, int2* entry, int4* front, float rmin,
+                      cudaStream_t st) {
+    hintgrid3_kernel<<<blocks(static_cast<long long>(G.nx) * G.ny * G.nz, 128), 128, 0, st>>>(S, G, id, entry, front,
+                                                                                            rmin);
     count_launch();
 }
 

@@ -41,5 +41,5 @@ for r in range(reps + 1):
         chk = float(np.sum(d["uHat"]) + np.sum(d["dHat"]))
     del cc
 tag = " ".join(f"{k}={v}" for k, v in sorted(os.environ.items()) if k.startswith("BVC_"))
-print(f"C{cid} [{tag}] walks s: min {min(ts[1:]):.4f} all {[round(x, 4) for x in ts[1:]]} steps {st.get('cacheSteps')} "
+print(f"C{cid} [{tag}] walks s: first {ts[0]:.3f} min {min(ts[1:]):.4f} all {[round(x, 4) for x in ts[1:]]} steps {st.get('cacheSteps')} "
       f"checksum {chk:.9e}", flush=True)
