@@ -110,7 +110,7 @@ unsigned long long* GenStats::device_counters() {
 void GenStats::snapshot() {
     if (!dev) return;
     DeviceState& d = t_dev[current_device()];
-    if (!d.pinned) CK(cudaMallocHost(reinterpret_cast<void**>(&d.pinned), 4 * sizeof(unsigned long long)));
+    if (!d.pinned) CK(cudaMallocHost(reinterpret_cast<void**>(&d.pinned), 8 * sizeof(unsigned long long)));
     CK(cudaMemcpyAsync(d.pinned, dev, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, g_stream));
     pinned = d.pinned;
     dev = nullptr;
@@ -122,6 +122,18 @@ void GenStats::resolve() {
     truncated += static_cast<long long>(pinned[1]);
     walks += static_cast<long long>(pinned[2]);
     pinned = nullptr;
+}
+
+// One int read back from the device through this thread's pinned scratch. A copy into
+// pageable memory blocks inside the driver until the stream reaches it, and other host
+// threads' launches queue up behind that call; a pinned copy plus a stream wait does not.
+int read_device_int(const int* dev) {
+    DeviceState& d = t_dev[current_device()];
+    if (!d.pinned) CK(cudaMallocHost(reinterpret_cast<void**>(&d.pinned), 8 * sizeof(unsigned long long)));
+    volatile int* slot = reinterpret_cast<volatile int*>(d.pinned + 4);
+    CK(cudaMemcpyAsync(const_cast<int*>(slot), dev, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+    return *slot;
 }
 
 cudaEvent_t round_event(int which) {

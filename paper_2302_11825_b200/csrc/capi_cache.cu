@@ -269,9 +269,7 @@ void generate_cache3(bvc_scene_s* S, const bvc_problem& pb, bvc_region_s* R, con
     int* badIdx = ws().get<int>(kWsBadIdx, n);
     int* badCnt = ws().get<int>(kWsBadCnt, 1);
     launch_compact_u8(failed, n, badIdx, badCnt, g_stream);
-    int nbad = 0;
-    CK(cudaMemcpyAsync(&nbad, badCnt, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
-    CK(cudaStreamSynchronize(g_stream));
+    const int nbad = read_device_int(badCnt);
     std::vector<int> bad(nbad);
     if (nbad) {
         CK(cudaMemcpyAsync(bad.data(), badIdx, nbad * sizeof(int), cudaMemcpyDeviceToHost, g_stream));
@@ -378,9 +376,7 @@ void generate_cache(bvc_scene_s* S, const bvc_problem& pb, bvc_region_s* R, cons
     int* badIdx = ws().get<int>(kWsBadIdx, n);
     int* badCnt = ws().get<int>(kWsBadCnt, 1);
     launch_compact_u8(failed, n, badIdx, badCnt, g_stream);
-    int nbad = 0;
-    CK(cudaMemcpyAsync(&nbad, badCnt, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
-    CK(cudaStreamSynchronize(g_stream));
+    const int nbad = read_device_int(badCnt);
     std::vector<int> bad(nbad);
     if (nbad) {
         CK(cudaMemcpyAsync(bad.data(), badIdx, nbad * sizeof(int), cudaMemcpyDeviceToHost, g_stream));
@@ -505,9 +501,7 @@ void generate_source(const bvc_problem& pb, bvc_region_s* R, const bvc_cache_con
                                                                       cfg.stratified, k0, k1, tol, SV, y, ok, prio);
         count_launch();
         launch_compact(ok, nc, idx, cnt, g_stream);
-        int na = 0;
-        CK(cudaMemcpyAsync(&na, cnt, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
-        CK(cudaStreamSynchronize(g_stream));
+        const int na = read_device_int(cnt);
         proposals += nc;
         if (proposals >= 1000000 && accepted + na < proposals / 10000)
             throw Error(BVC_ERR_PARSE, "degenerate region: rejection acceptance rate below 1e-4");

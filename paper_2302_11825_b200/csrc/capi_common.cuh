@@ -374,6 +374,7 @@ void splat_round(bvc_scene_s* s, const bvc_problem& pb, bvc_region_s* r, const b
                  uint64_t round, int gradients, const bvc_boundary_evaluator* correctionEval);  // capi_splat.cu
 // per-thread, per-device events reused by every round (no create/destroy per call):
 // 0-1 stream dependencies, 2-4 round phases, 5-8 the round's main kernels (KernelTimer)
+int read_device_int(const int* dev);  // via pinned memory (capi.cu)
 cudaEvent_t round_event(int which);                                             // capi.cu
 
 // Device time of a round's two hot launches (the main cache-walk job and the main gather),

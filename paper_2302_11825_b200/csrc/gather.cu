@@ -913,6 +913,8 @@ void launch_prologue(const CacheSample* cs, int N, const SourceSampleDev* ss, in
                      cudaStream_t st) {
     const int tiles = (N + kTS - 1) / kTS + (M + kTS - 1) / kTS;
     if (tiles <= 0) return;
+    if (const char* e = std::getenv("BVC_GATHER_CARVEOUT"))  // co-residency experiments (percent)
+        cudaFuncSetAttribute(prologue_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e));
     prologue_kernel<<<tiles, kTS, 0, st>>>(cs, N, ss, M, kind, voronoi, k, pack, tileBox, unitCounter, skipB, skipS, K);
     count_launch();
 }
@@ -1037,7 +1039,12 @@ void launch_gather(int kind, const GatherPlan& g, const float4* pack, int N, int
         case kLap2: launch_kind<kLap2>(P, val, grad, g.grid, st); break;
         case kScr2: launch_kind<kScr2>(P, val, grad, g.grid, st); break;
         case kLap3: launch_kind<kLap3>(P, val, grad, g.grid, st); break;
-        case kScr3V: gather_kernel<kScr3V, true, false><<<g.grid, kThreads, 0, st>>>(P); break;
+        case kScr3V:
+            if (const char* e = std::getenv("BVC_GATHER_CARVEOUT"))  // co-residency experiments (percent)
+                cudaFuncSetAttribute(gather_kernel<kScr3V, true, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     std::atoi(e));
+            gather_kernel<kScr3V, true, false><<<g.grid, kThreads, 0, st>>>(P);
+            break;
         default: launch_kind<kScr3>(P, val, grad, g.grid, st); break;
     }
     count_launch();

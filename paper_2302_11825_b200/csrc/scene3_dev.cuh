@@ -121,6 +121,10 @@ __device__ __forceinline__ float tri_closest(const Prim3& t, float px, float py,
 // code paths once per leaf instead of once per node visit
 // Entry frontiers (HintGrid::front): kFront starts per grid cell whose subtrees together
 // hold every primitive a query from the cell can need (kNoEntry = unused slot)
+// loads of the warm-start grid (one cell per step out of gigabytes: streaming, evict-first)
+#ifndef BVC_GRID_LD
+#define BVC_GRID_LD __ldcs
+#endif
 #ifndef BVC_FRONT_N
 #define BVC_FRONT_N 4
 #endif
@@ -139,7 +143,7 @@ __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, flo
     if (front) {
 #pragma unroll
         for (int k = kFrontWords - 1; k >= 0; --k) {
-            const int4 f = __ldg(front + k);
+            const int4 f = BVC_GRID_LD(front + k);
             if (f.w != kNoEntry) stack[sp++] = static_cast<unsigned>(f.w);
             if (f.z != kNoEntry) stack[sp++] = static_cast<unsigned>(f.z);
             if (f.y != kNoEntry) stack[sp++] = static_cast<unsigned>(f.y);

@@ -213,7 +213,7 @@ __device__ __forceinline__ int hint_at3(const HintGrid& G, float x, float y, flo
     if (static_cast<unsigned>(ix) >= static_cast<unsigned>(G.nx) || static_cast<unsigned>(iy) >= static_cast<unsigned>(G.ny) ||
         static_cast<unsigned>(iz) >= static_cast<unsigned>(G.nz))
         return -1;
-    return __ldg(G.id + (static_cast<size_t>(iz) * G.ny + iy) * G.nx + ix);
+    return BVC_GRID_LD(G.id + (static_cast<size_t>(iz) * G.ny + iy) * G.nx + ix);
 }
 
 // the cell entry refs of x (HintGrid), or the root for both outside the grid; with the
@@ -228,7 +228,7 @@ __device__ __forceinline__ int2 entry_at3(const HintGrid& G, float x, float y, f
         return make_int2(0, 0);
     const size_t cell = (static_cast<size_t>(iz) * G.ny + iy) * G.nx + ix;
     if (G.front) front = G.front + cell * kFrontWords;
-    return __ldg(G.entry + cell);
+    return BVC_GRID_LD(G.entry + cell);
 }
 
 struct Walk3 {
@@ -629,6 +629,8 @@ void launch_walk3_t(const WalkEnv3& env, const WalkJob3& job, long long total, c
     }
     long long want = (total + kThreads3 - 1) / kThreads3;
     int grid = static_cast<int>(want < static_cast<long long>(sms) * perSm ? want : static_cast<long long>(sms) * perSm);
+    if (const char* e = std::getenv("BVC_WALK_CARVEOUT"))  // co-residency experiments: shared-memory carve-out, percent
+        cudaFuncSetAttribute(walk3_kernel<NEU, SCR, COUNT>, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e));
     walk3_kernel<NEU, SCR, COUNT><<<grid, kThreads3, 0, st>>>(env, job);
 }
 
