@@ -259,7 +259,11 @@ HintGrid bvc_scene_s::hintgrid() {
     // 128: 0.377 / 2.633 s, 256: 0.349 / 2.523, 384: 0.335 / 2.461, 512: 0.324 / 2.420 (one-time
     // build 0.05 / 0.13 / 0.25 / 0.47 s; 28 B per cell: 1.6 GB at 384^3, 3.8 GB at 512^3)
     const int n3 = static_cast<int>(std::lround(1.35 * std::sqrt(static_cast<double>(host.ns))));
-    const int nLong = en && std::atoi(en) >= 16 ? std::atoi(en) : (dim == 2 ? 1024 : std::min(384, std::max(64, n3)));
+    // 2D: a quarter of the segment count along the longest side, 1024-4096 (28 B per cell: 29-470 MB).
+    // Walk time with frontiers by vertices along the side, C3 (16384 segments): 1024: 93.7 ms, 2048: 89.4,
+    // 4096: 86.9 (one entry node per cell: 112.6 at any size); C1 (1024 segments): 1.1 ms at 1024-4096
+    const int n2 = std::min(4096, std::max(1024, host.ns / 4));
+    const int nLong = en && std::atoi(en) >= 16 ? std::atoi(en) : (dim == 2 ? n2 : std::min(384, std::max(64, n3)));
     double ext = 0.0, lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (int k = 0; k < dim; ++k) {
         lo[k] = host.lo[k];
@@ -283,10 +287,13 @@ HintGrid bvc_scene_s::hintgrid() {
     hgEntry.resize(nv);
     // ray lengths are max(R, rMin) with rMin <= eps; a generous 1e-2 diag covers any rMin
     const float rmin = static_cast<float>(1e-2 * host.diagonal);
-    if (dim == 2) launch_hintgrid2(view(), hg, hgIds.p, hgEntry.p, rmin, g_stream);
-    else {
-        const char* ef = std::getenv("BVC_FRONT");  // 0: one entry node per cell
-        if (!(ef && std::string(ef) == "0")) hgFront.resize(nv * front_words3());
+    const char* ef = std::getenv("BVC_FRONT");  // 0: one entry node per cell
+    const bool fronts = !(ef && std::string(ef) == "0");
+    if (dim == 2) {
+        if (fronts) hgFront.resize(nv);
+        launch_hintgrid2(view(), hg, hgIds.p, hgEntry.p, hgFront.n ? hgFront.p : nullptr, rmin, g_stream);
+    } else {
+        if (fronts) hgFront.resize(nv * front_words3());
         launch_hintgrid3(view3(), hg, hgIds.p, hgEntry.p, hgFront.n ? hgFront.p : nullptr, rmin, g_stream);
     }
     CK(cudaGetLastError());

@@ -34,7 +34,7 @@ using bvc_dev::SceneView2;
 struct HintGrid {
     const int* id;       // NULL: disabled
     const int2* entry;   // per cell: (star / closest entry, Neumann ray entry)
-    const int4* front;   // 3D, per cell: up to 4 star / closest starts (entry_frontier3), or NULL
+    const int4* front;   // per cell: up to 4 star / closest starts (entry_frontier2 / 3), or NULL
     float lox, loy, loz, h, invH;
     int nx, ny, nz;
 };
@@ -117,7 +117,8 @@ void launch_sil_count3(const bvc_dev::Prim3* prims, int n, const int4* triSil, i
 void launch_sil_fill3(bvc_dev::Prim3* prims, int n, const int4* triSil, const int* counts, const int* offsets,
                       const float4* silA, const float4* silN1, const float4* silN2, const float4* silB,
                       const float4* triN, float4* rec, cudaStream_t st);
-void launch_hintgrid2(const SceneView2& S, const HintGrid& G, int* id, int2* entry, float rmin, cudaStream_t st);
+void launch_hintgrid2(const SceneView2& S, const HintGrid& G, int* id, int2* entry, int4* front, float rmin,
+                      cudaStream_t st);
 void launch_hintgrid3(const bvc_dev::SceneView3& S, const HintGrid& G, int* id, int2* entry, int4* front, float rmin,
                       cudaStream_t st);
 int front_words3();  // int4 words per cell of HintGrid::front (walk3.cu)

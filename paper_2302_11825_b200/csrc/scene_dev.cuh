@@ -95,11 +95,18 @@ constexpr int kNoEntry = -2147483647 - 1;
 
 template <bool COUNT = false, class Visit, class Thr>
 __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, float y, unsigned qmask, Visit&& visit,
-                                              Thr&& threshold, int start = 0) {
-    if (start == kNoEntry) return;
+                                              Thr&& threshold, int start = 0, const int4* front = nullptr) {
     // (distance bits << 32 | ref) per entry: one local load per pop
     unsigned long long stack[kStack];
     int sp = 0;
+    if (front) {  // the cell's entry frontier (entry_frontier2): starts 2-4 stacked at distance 0
+        const int4 f = __ldcs(front);
+        if (f.w != kNoEntry) stack[sp++] = static_cast<unsigned>(f.w);
+        if (f.z != kNoEntry) stack[sp++] = static_cast<unsigned>(f.z);
+        if (f.y != kNoEntry) stack[sp++] = static_cast<unsigned>(f.y);
+        start = f.x;
+    }
+    if (start == kNoEntry) return;
     int ref = start;
     const F2 p2 = pk(x, y);
     auto pop = [&]() -> bool {  // next entry still within the pruning radius; false when empty
@@ -164,7 +171,8 @@ __device__ __forceinline__ Closest closest_on(const SceneView2& S, int seg, floa
 // previous closest segment), so far subtrees are never pushed.
 template <bool COUNT = false>
 __device__ __forceinline__ Closest closest_point(const SceneView2& S, float x, float y, unsigned qmask,
-                                                 float maxD2 = kFInf, int hint = -1, int hint2 = -1, int start = 0) {
+                                                 float maxD2 = kFInf, int hint = -1, int hint2 = -1, int start = 0,
+                                                 const int4* front = nullptr) {
     Closest c{maxD2, 0.0f, 0.0f, 0.0f, -1};
     if (hint >= 0) {
         Closest h = closest_on(S, hint, x, y);
@@ -181,7 +189,7 @@ __device__ __forceinline__ Closest closest_point(const SceneView2& S, float x, f
             float d2 = seg_closest(p.seg, x, y, px, py, t);
             if (d2 < c.d2) { c.d2 = d2; c.px = px; c.py = py; c.t = t; c.seg = p.id; }
         },
-        [&]() { return c.d2; }, start);
+        [&]() { return c.d2; }, start, front);
     return c;
 }
 
@@ -221,7 +229,7 @@ struct StarQuery {
 };
 template <bool COUNT = false>
 __device__ __forceinline__ StarQuery star_query(const SceneView2& S, float x, float y, float eps2, int hint = -1,
-                                                int hint2 = -1, int start = 0) {
+                                                int hint2 = -1, int start = 0, const int4* front = nullptr) {
     StarQuery q;
     q.D = hint >= 0 ? closest_on(S, hint, x, y) : Closest{kFInf, 0.0f, 0.0f, 0.0f, -1};
     if (hint2 >= 0 && hint2 != hint) {
@@ -244,7 +252,7 @@ __device__ __forceinline__ StarQuery star_query(const SceneView2& S, float x, fl
                 if (p.sil1 >= 0 && silhouette_ok(S, p.sil1, x, y, d2) && d2 < fminf(q.s2, q.D.d2)) q.s2 = d2;
             }
         },
-        [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); }, start);
+        [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); }, start, front);
     return q;
 }
 
@@ -386,6 +394,43 @@ __device__ __forceinline__ int entry_node(const SceneView2& S, float x, float y,
         else return kNoEntry;
     }
     return ref;
+}
+
+// Up to 4 nodes whose subtrees together hold every primitive of qmask within sqrt(r2) of
+// (x, y): entry_node's node, then, while there is room, a frontier node whose two children
+// both qualify is replaced by them (single qualifying children are descended into, nodes
+// with none dropped). f[0] == kNoEntry: none. (The 2D form of entry_frontier3.)
+__device__ __forceinline__ void entry_frontier2(const SceneView2& S, float x, float y, float r2, unsigned qmask,
+                                                int (&f)[4]) {
+    for (int k = 0; k < 4; ++k) f[k] = kNoEntry;
+    f[0] = entry_node(S, x, y, r2, qmask);
+    int nf = f[0] == kNoEntry ? 0 : 1;
+    for (int guard = 0; guard < 1024; ++guard) {
+        bool changed = false;
+        for (int i = 0; i < nf; ++i) {
+            const int ref = f[i];
+            if (ref < 0) continue;  // a leaf
+            const Node2 nd = S.nodes[ref];
+            const bool vl = (nd.mask & qmask) && box_dist2(nd.lbox, x, y) <= r2;
+            const bool vr = ((nd.mask >> 3) & qmask) && box_dist2(nd.rbox, x, y) <= r2;
+            if (vl && vr) {
+                if (nf < 4) {
+                    f[i] = nd.left;
+                    f[nf++] = nd.right;
+                    changed = true;
+                }
+            } else if (vl || vr) {
+                f[i] = vl ? nd.left : nd.right;
+                changed = true;
+            } else {
+                f[i] = f[--nf];
+                f[nf] = kNoEntry;
+                changed = true;
+                --i;
+            }
+        }
+        if (!changed) break;
+    }
 }
 
 // Scene::inside (scene.cpp:240-254): boundary-inclusive within tol, then crossing

@@ -170,13 +170,17 @@ __device__ __forceinline__ int hint_at(const HintGrid& G, float x, float y) {
     return __ldg(G.id + static_cast<size_t>(iy) * G.nx + ix);
 }
 
-// the cell entry refs of (x, y) (HintGrid), or the root for both outside the grid
-__device__ __forceinline__ int2 entry_at(const HintGrid& G, float x, float y) {
+// the cell entry refs of (x, y) (HintGrid), or the root for both outside the grid; with the
+// entry frontiers, `front` receives the cell's 4 star / closest-point starts
+__device__ __forceinline__ int2 entry_at(const HintGrid& G, float x, float y, const int4*& front) {
+    front = nullptr;
     if (!G.entry) return make_int2(0, 0);
     const int ix = __float2int_rd((x - G.lox) * G.invH), iy = __float2int_rd((y - G.loy) * G.invH);
     if (static_cast<unsigned>(ix) >= static_cast<unsigned>(G.nx) || static_cast<unsigned>(iy) >= static_cast<unsigned>(G.ny))
         return make_int2(0, 0);
-    return __ldg(G.entry + static_cast<size_t>(iy) * G.nx + ix);
+    const size_t cell = static_cast<size_t>(iy) * G.nx + ix;
+    if (G.front) front = G.front + cell;
+    return __ldg(G.entry + cell);
 }
 
 // per-lane walk state
@@ -242,7 +246,8 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
     // holds no boundary point, so no Neumann crossing and no Neumann-data term either
     const float lb = E.ff.d ? farfield_bound(E.ff, w.x, w.y) : -1.0f;
     const bool far = lb >= E.ff.tau;
-    const int2 entry = (far || E.drunN) ? make_int2(0, 0) : entry_at(E.hg, w.x, w.y);
+    const int4* front = nullptr;
+    const int2 entry = (far || E.drunN) ? make_int2(0, 0) : entry_at(E.hg, w.x, w.y, front);
     if (far) {
         R = lb;
     } else if (E.drunN) {  // straight-run scene: no BVH (bvc_scene_s::build_runs)
@@ -257,13 +262,13 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
         if constexpr (NEU) {
             // a Dirichlet segment farther than the closest visible silhouette may be
             // pruned (q.D.seg < 0, d2 = inf): R is then the silhouette distance
-            StarQuery q = star_query<COUNT>(E.S, w.x, w.y, E.eps * E.eps, w.lastD, hint_at(E.hg, w.x, w.y), entry.x);
+            StarQuery q = star_query<COUNT>(E.S, w.x, w.y, E.eps * E.eps, w.lastD, hint_at(E.hg, w.x, w.y), entry.x, front);
             cp = q.D;
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
             R = fminf(dD, sqrtf(q.s2));
         } else {
-            cp = closest_point<COUNT>(E.S, w.x, w.y, kClsD, kFInf, w.lastD, hint_at(E.hg, w.x, w.y), entry.x);
+            cp = closest_point<COUNT>(E.S, w.x, w.y, kClsD, kFInf, w.lastD, hint_at(E.hg, w.x, w.y), entry.x, front);
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
             R = dD;
@@ -695,7 +700,7 @@ __global__ void farfield2_kernel(const SceneView2 S, const FarField F, float* d)
     d[i] = sqrtf(closest_point(S, x, y, kClsAny).d2);
 }
 
-__global__ void hintgrid2_kernel(const SceneView2 S, const HintGrid G, int* id, int2* entry, float rmin) {
+__global__ void hintgrid2_kernel(const SceneView2 S, const HintGrid G, int* id, int2* entry, int4* front, float rmin) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= G.nx * G.ny) return;
     int ix = i % G.nx, iy = i / G.nx;
@@ -707,6 +712,13 @@ __global__ void hintgrid2_kernel(const SceneView2 S, const HintGrid G, int* id, 
     const int star = entry_node(S, cx, cy, r * r, kClsD | kClsSil);
     const float rr = r + rmin;
     entry[i] = make_int2(star == kNoEntry ? 0 : star, entry_node(S, cx, cy, rr * rr, kClsNeumann));
+    if (front) {
+        int f[4];
+        entry_frontier2(S, cx, cy, r * r, kClsD | kClsSil, f);
+        // nothing within the radius cannot happen for a star query (the closest Dirichlet
+        // primitive is); keep the root in that case like entry.x does
+        front[i] = f[0] == kNoEntry ? make_int4(0, kNoEntry, kNoEntry, kNoEntry) : make_int4(f[0], f[1], f[2], f[3]);
+    }
 }
 
 
@@ -757,8 +769,9 @@ void launch_farfield2(const SceneView2& S, const FarField& F, float* d, cudaStre
     count_launch();
 }
 
-void launch_hintgrid2(const SceneView2& S, const HintGrid& G, int* id, int2* entry, float rmin, cudaStream_t st) {
-    hintgrid2_kernel<<<blocks(static_cast<long long>(G.nx) * G.ny, 128), 128, 0, st>>>(S, G, id, entry, rmin);
+void launch_hintgrid2(const SceneView2& S, const HintGrid& G, int* id, int2* entry, int4* front, float rmin,
+                      cudaStream_t st) {
+    hintgrid2_kernel<<<blocks(static_cast<long long>(G.nx) * G.ny, 128), 128, 0, st>>>(S, G, id, entry, front, rmin);
     count_launch();
 }
 
