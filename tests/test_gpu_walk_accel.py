@@ -1,6 +1,7 @@
 """Walk-query accelerations that must not change the walks: the warm-start grid
-(HintGrid: one more seed of the closest-point bound) and the cell entry nodes (queries
-start at a subtree holding every usable primitive). Each only prunes
+(HintGrid: one more seed of the closest-point bound), the cell entry nodes (queries
+start at a subtree holding every usable primitive) and the entry frontiers (up to four
+deeper starts per cell instead of their common ancestor, 2D and 3D). Each only prunes
 work, so caches with and without it agree bitwise except where a distance tie (the
 shared vertex of two primitives, the closest point of every query in a reflex
 vertex's wedge) is broken the other way: the two distances differ by rounding, the
@@ -20,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _run(tmp_path, name, env_extra):
     out = str(tmp_path / f"{name}.npz")
     env = dict(os.environ, PYTHONPATH=ROOT)
-    for k in ("BVC_HINTGRID", "BVC_ENTRY"):
+    for k in ("BVC_HINTGRID", "BVC_ENTRY", "BVC_FRONT"):
         env.pop(k, None)
     env.update(env_extra)
     subprocess.run([sys.executable, os.path.join(ROOT, "tests", "walk_accel_case.py"), out], env=env, check=True,
@@ -33,7 +34,7 @@ def default_run(tmp_path_factory):
     return _run(tmp_path_factory.mktemp("accel"), "default", {})
 
 
-@pytest.mark.parametrize("switch", ["BVC_HINTGRID", "BVC_ENTRY"])
+@pytest.mark.parametrize("switch", ["BVC_HINTGRID", "BVC_ENTRY", "BVC_FRONT"])
 def test_acceleration_leaves_walks_unchanged(tmp_path, default_run, switch):
     a, b = _run(tmp_path, switch, {switch: "0"}), default_run
     for k in a.files:
