@@ -38,7 +38,7 @@ def _compile(src: str) -> tuple[str, str]:
         return obj, ""
     cmd = [NVCC, *ARCH, *FLAGS, "-c", path, "-o", obj]
     if src.endswith(".cpp"):
-        cmd = [NVCC, "-std=c++17", "-O3", "-Xcompiler", "-fPIC", "-c", path, "-o", obj]
+        cmd = [NVCC, *ARCH, "-std=c++17", "-O3", "-Xcompiler", "-fPIC", "-c", path, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")

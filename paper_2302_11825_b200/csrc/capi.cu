@@ -257,9 +257,9 @@ HintGrid bvc_scene_s::hintgrid() {
     // a cell's candidate ball is dD(c) + 2 rho, so near the surface smaller cells give deeper
     // entry frontiers. Walk time by vertices along the side (C4 / C5, frontier of 4):
     // 128: 0.377 / 2.633 s, 256: 0.349 / 2.523, 384: 0.335 / 2.461, 512: 0.324 / 2.420 (one-time
-    // build 0.05 / 0.13 / 0.25 / 0.47 s; 28 B per cell: 1.6 GB at 384^3, 3.8 GB at 512^3)
+    // build 0.05 / 0.13 / 0.25 / 0.47 s; 32 B per cell: 1.8 GB at 384^3, 4.3 GB at 512^3)
     const int n3 = static_cast<int>(std::lround(1.35 * std::sqrt(static_cast<double>(host.ns))));
-    // 2D: a quarter of the segment count along the longest side, 1024-4096 (28 B per cell: 29-470 MB).
+    // 2D: a quarter of the segment count along the longest side, 1024-4096 (32 B per cell: 34-540 MB).
     // Walk time with frontiers by vertices along the side, C3 (16384 segments): 1024: 93.7 ms, 2048: 89.4,
     // 4096: 86.9 (one entry node per cell: 112.6 at any size); C1 (1024 segments): 1.1 ms at 1024-4096
     const int n2 = std::min(4096, std::max(1024, host.ns / 4));
@@ -283,27 +283,20 @@ HintGrid bvc_scene_s::hintgrid() {
     hg.ny = n[1];
     hg.nz = n[2];
     const size_t nv = static_cast<size_t>(n[0]) * n[1] * n[2];
-    hgIds.resize(nv);
-    hgEntry.resize(nv);
+    hgCells.resize(nv);
     // ray lengths are max(R, rMin) with rMin <= eps; a generous 1e-2 diag covers any rMin
     const float rmin = static_cast<float>(1e-2 * host.diagonal);
+    const char* ee = std::getenv("BVC_ENTRY");  // 0: queries start at the root
     const char* ef = std::getenv("BVC_FRONT");  // 0: one entry node per cell
-    const bool fronts = !(ef && std::string(ef) == "0");
-    if (dim == 2) {
-        if (fronts) hgFront.resize(nv);
-        launch_hintgrid2(view(), hg, hgIds.p, hgEntry.p, hgFront.n ? hgFront.p : nullptr, rmin, g_stream);
-    } else {
-        if (fronts) hgFront.resize(nv * front_words3());
-        launch_hintgrid3(view3(), hg, hgIds.p, hgEntry.p, hgFront.n ? hgFront.p : nullptr, rmin, g_stream);
-    }
+    const bool entries = !(ee && std::string(ee) == "0");
+    const bool fronts = entries && !(ef && std::string(ef) == "0");
+    if (dim == 2) launch_hintgrid2(view(), hg, hgCells.p, entries, fronts, rmin, g_stream);
+    else launch_hintgrid3(view3(), hg, hgCells.p, entries, fronts, rmin, g_stream);
     CK(cudaGetLastError());
     // built once per scene, possibly on another stream than its readers (the round's
     // side stream runs band walks that use it): complete it before publishing it
     CK(cudaStreamSynchronize(g_stream));
-    hg.id = hgIds.p;
-    const char* ee = std::getenv("BVC_ENTRY");
-    hg.entry = (ee && std::string(ee) == "0") ? nullptr : hgEntry.p;
-    hg.front = (hg.entry && hgFront.n) ? hgFront.p : nullptr;
+    hg.cell = hgCells.p;
     hgBuilt = true;
     return hg;
 }

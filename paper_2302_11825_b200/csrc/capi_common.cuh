@@ -250,9 +250,7 @@ struct bvc_scene_s {
     std::atomic<bool> ffBuilt{false};
     FarField farfield();
     // warm-start grid (HintGrid, internal.h), built on first walk use
-    DevBuf<int> hgIds;
-    DevBuf<int2> hgEntry;
-    DevBuf<int4> hgFront;  // 3D entry frontiers (HintGrid::front)
+    DevBuf<HintCell> hgCells;
     HintGrid hg{};
     std::atomic<bool> hgBuilt{false};
     HintGrid hintgrid();

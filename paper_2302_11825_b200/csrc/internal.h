@@ -31,12 +31,26 @@ using bvc_dev::SceneView2;
 // rays cannot reach any). Queries start there instead of the root: the top levels, which
 // every query of the cell would descend identically, are skipped, and the result is the
 // same (every candidate is in the subtree).
+// One 32-byte record per cell (one memory sector per walk step): the cell's star /
+// closest-point starts (`front`: entry_frontier2 / 3, up to 4 nodes whose subtrees hold every
+// usable primitive; front.x alone when frontiers are off; kNoEntry = unused slot), its Neumann
+// ray entry, and the Dirichlet primitive closest to the cell centre (the warm start).
+struct alignas(32) HintCell {
+    int4 front;
+    int ray;  // Neumann ray entry node, or kNoEntry
+    int id;   // leaf-order (3D) / segment (2D) index of the warm-start primitive, or -1
+    int pad0, pad1;
+};
+static_assert(sizeof(HintCell) == 32, "HintCell layout");
 struct HintGrid {
-    const int* id;       // NULL: disabled
-    const int2* entry;   // per cell: (star / closest entry, Neumann ray entry)
-    const int4* front;   // per cell: up to 4 star / closest starts (entry_frontier2 / 3), or NULL
+    const HintCell* cell;  // NULL: disabled
     float lox, loy, loz, h, invH;
     int nx, ny, nz;
+};
+// what a step takes from its cell (roots and no warm start outside the grid)
+struct CellHints {
+    int4 front;
+    int ray, id;
 };
 
 // PdeProblem with device field descriptors (pointwise.h:19-26)
@@ -117,11 +131,11 @@ void launch_sil_count3(const bvc_dev::Prim3* prims, int n, const int4* triSil, i
 void launch_sil_fill3(bvc_dev::Prim3* prims, int n, const int4* triSil, const int* counts, const int* offsets,
                       const float4* silA, const float4* silN1, const float4* silN2, const float4* silB,
                       const float4* triN, float4* rec, cudaStream_t st);
-void launch_hintgrid2(const SceneView2& S, const HintGrid& G, int* id, int2* entry, int4* front, float rmin,
+// entries / fronts false: the records hold the root / the single entry node instead
+void launch_hintgrid2(const SceneView2& S, const HintGrid& G, HintCell* cells, bool entries, bool fronts, float rmin,
                       cudaStream_t st);
-void launch_hintgrid3(const bvc_dev::SceneView3& S, const HintGrid& G, int* id, int2* entry, int4* front, float rmin,
-                      cudaStream_t st);
-int front_words3();  // int4 words per cell of HintGrid::front (walk3.cu)
+void launch_hintgrid3(const bvc_dev::SceneView3& S, const HintGrid& G, HintCell* cells, bool entries, bool fronts,
+                      float rmin, cudaStream_t st);
 void launch_farfield3(const bvc_dev::SceneView3& S, const FarField& F, float* d, cudaStream_t st);
 
 // per-point mean / standard error (runWalks pointwise.cpp:167-186), fixed order

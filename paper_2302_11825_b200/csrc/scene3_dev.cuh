@@ -119,41 +119,19 @@ __device__ __forceinline__ float tri_closest(const Prim3& t, float px, float py,
 // "while-while" structure (Aila & Laine, HPG 2009): each lane descends inner nodes
 // in one loop and handles leaves in the next, so the warp switches between the two
 // code paths once per leaf instead of once per node visit
-// Entry frontiers (HintGrid::front): kFront starts per grid cell whose subtrees together
-// hold every primitive a query from the cell can need (kNoEntry = unused slot)
-// loads of the warm-start grid (one cell per step out of gigabytes: streaming, evict-first)
-#ifndef BVC_GRID_LD
-#define BVC_GRID_LD __ldcs
-#endif
-#ifndef BVC_FRONT_N
-#define BVC_FRONT_N 4
-#endif
-constexpr int kFront = BVC_FRONT_N;
-constexpr int kFrontWords = (kFront + 3) / 4;  // int4 words per cell
-static_assert(kFront >= 2 && kFront <= 16, "frontier size");
-
-// `front`: the query cell's frontier (kFront starts; front[0].x replaces `start`), or
-// nullptr. The further starts are stacked at distance 0 and visited after the first.
+// Entry frontiers (HintCell::front): up to 4 starts per grid cell whose subtrees together
+// hold every primitive a query from the cell can need (kNoEntry = unused slot).
+// `starts`: the query cell's frontier; starts.x is the first node visited, the others are
+// stacked at distance 0 and visited after it. kRootStart: the whole tree.
 template <bool COUNT = false, class Visit, class Thr>
 __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, float y, float z, unsigned qmask,
-                                               Visit&& visit, Thr&& threshold, int start = 0,
-                                               const int4* front = nullptr) {
+                                               Visit&& visit, Thr&& threshold, const int4 starts = kRootStart) {
     unsigned long long stack[kStack];  // (distance bits << 32 | ref): one local load per pop
     int sp = 0;
-    if (front) {
-#pragma unroll
-        for (int k = kFrontWords - 1; k >= 0; --k) {
-            const int4 f = BVC_GRID_LD(front + k);
-            if (f.w != kNoEntry) stack[sp++] = static_cast<unsigned>(f.w);
-            if (f.z != kNoEntry) stack[sp++] = static_cast<unsigned>(f.z);
-            if (f.y != kNoEntry) stack[sp++] = static_cast<unsigned>(f.y);
-            if (k > 0) {
-                if (f.x != kNoEntry) stack[sp++] = static_cast<unsigned>(f.x);
-            } else {
-                start = f.x;
-            }
-        }
-    }
+    if (starts.w != kNoEntry) stack[sp++] = static_cast<unsigned>(starts.w);
+    if (starts.z != kNoEntry) stack[sp++] = static_cast<unsigned>(starts.z);
+    if (starts.y != kNoEntry) stack[sp++] = static_cast<unsigned>(starts.y);
+    const int start = starts.x;
     if (start == kNoEntry) return;
     int ref = start;
     const F2 pxy = pk(x, y);
@@ -189,8 +167,8 @@ __device__ __forceinline__ void traverse_near3(const SceneView3& S, float x, flo
             }
         }
         int code = ~ref;
-        int start = code >> 3, count = (code & 7) + 1;
-        for (int i = start; i < start + count; ++i) {
+        int first = code >> 3, count = (code & 7) + 1;
+        for (int i = first; i < first + count; ++i) {
             const Prim3 p = S.prims[i];
             count_fetch3<COUNT>(S, 1);
             if ((1u << __float_as_int(p.b.w)) & qmask) visit(p, i);
@@ -220,7 +198,7 @@ __device__ __forceinline__ Closest3 closest_on3(const SceneView3& S, int prim, f
 template <bool COUNT = false>
 __device__ __forceinline__ Closest3 closest_point3(const SceneView3& S, float x, float y, float z, unsigned qmask,
                                                    float maxD2 = kFInf, int hint = -1, int hint2 = -1,
-                                                   int start = 0, const int4* front = nullptr) {
+                                                   const int4 starts = kRootStart) {
     Closest3 c{maxD2, 0.f, 0.f, 0.f, -1, -1};
     if (hint >= 0) {
         Closest3 h = closest_on3(S, hint, x, y, z);
@@ -237,7 +215,7 @@ __device__ __forceinline__ Closest3 closest_point3(const SceneView3& S, float x,
             float d2 = tri_closest(p, x, y, z, qx, qy, qz);
             if (d2 < c.d2) c = Closest3{d2, qx, qy, qz, __float_as_int(p.a.w), i};
         },
-        [&]() { return c.d2; }, start, front);
+        [&]() { return c.d2; }, starts);
     return c;
 }
 
@@ -304,14 +282,14 @@ __device__ __forceinline__ int entry_node3(const SceneView3& S, float x, float y
     return ref;
 }
 
-// Up to kFront nodes whose subtrees together hold every primitive of qmask within
+// Up to 4 nodes whose subtrees together hold every primitive of qmask within
 // sqrt(r2) of p: entry_node3's node, then, while there is room, a frontier node whose two
 // children both qualify is replaced by them (single qualifying children are descended
 // into, nodes with none dropped). A cell straddling a high split of the tree gets deep
 // starts on both sides instead of their common ancestor. f[0] == kNoEntry: none.
 __device__ __forceinline__ void entry_frontier3(const SceneView3& S, float x, float y, float z, float r2,
-                                                unsigned qmask, int (&f)[4 * kFrontWords]) {
-    for (int k = 0; k < 4 * kFrontWords; ++k) f[k] = kNoEntry;
+                                                unsigned qmask, int (&f)[4]) {
+    for (int k = 0; k < 4; ++k) f[k] = kNoEntry;
     f[0] = entry_node3(S, x, y, z, r2, qmask);
     int nf = f[0] == kNoEntry ? 0 : 1;
     for (int guard = 0; guard < 1024; ++guard) {
@@ -323,7 +301,7 @@ __device__ __forceinline__ void entry_frontier3(const SceneView3& S, float x, fl
             const bool vl = (nd.mask() & qmask) && box3_dist2(nd.llo, nd.lhi, x, y, z) <= r2;
             const bool vr = ((nd.mask() >> 3) & qmask) && box3_dist2(nd.rlo, nd.rhi, x, y, z) <= r2;
             if (vl && vr) {
-                if (nf < kFront) {
+                if (nf < 4) {
                     f[i] = nd.left();
                     f[nf++] = nd.right();
                     changed = true;

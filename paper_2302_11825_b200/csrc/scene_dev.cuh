@@ -92,20 +92,20 @@ constexpr unsigned kClsNeumann = kClsN | kClsSil, kClsAny = kClsD | kClsN | kCls
 // Entry refs (HintGrid): a traversal may start at a subtree known to hold every
 // primitive that can matter for the query (start = 0: the root); kNoEntry = none.
 constexpr int kNoEntry = -2147483647 - 1;
+// starts of a traversal (HintCell::front): .x first, the others stacked; kRootStart: the whole tree
+#define kRootStart make_int4(0, kNoEntry, kNoEntry, kNoEntry)
 
 template <bool COUNT = false, class Visit, class Thr>
 __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, float y, unsigned qmask, Visit&& visit,
-                                              Thr&& threshold, int start = 0, const int4* front = nullptr) {
+                                              Thr&& threshold, const int4 starts = kRootStart) {
     // (distance bits << 32 | ref) per entry: one local load per pop
     unsigned long long stack[kStack];
     int sp = 0;
-    if (front) {  // the cell's entry frontier (entry_frontier2): starts 2-4 stacked at distance 0
-        const int4 f = __ldcs(front);
-        if (f.w != kNoEntry) stack[sp++] = static_cast<unsigned>(f.w);
-        if (f.z != kNoEntry) stack[sp++] = static_cast<unsigned>(f.z);
-        if (f.y != kNoEntry) stack[sp++] = static_cast<unsigned>(f.y);
-        start = f.x;
-    }
+    // the cell's entry frontier (entry_frontier2): starts 2-4 stacked at distance 0
+    if (starts.w != kNoEntry) stack[sp++] = static_cast<unsigned>(starts.w);
+    if (starts.z != kNoEntry) stack[sp++] = static_cast<unsigned>(starts.z);
+    if (starts.y != kNoEntry) stack[sp++] = static_cast<unsigned>(starts.y);
+    const int start = starts.x;
     if (start == kNoEntry) return;
     int ref = start;
     const F2 p2 = pk(x, y);
@@ -142,8 +142,8 @@ __device__ __forceinline__ void traverse_near(const SceneView2& S, float x, floa
             }
         }
         int code = ~ref;
-        int start = code >> 3, count = (code & 7) + 1;
-        for (int i = start; i < start + count; ++i) {
+        int first = code >> 3, count = (code & 7) + 1;
+        for (int i = first; i < first + count; ++i) {
             const Prim2 p = S.prims[i];
             count_fetch<COUNT>(S, 1);
             if ((1u << p.label) & qmask) visit(p);
@@ -171,8 +171,8 @@ __device__ __forceinline__ Closest closest_on(const SceneView2& S, int seg, floa
 // previous closest segment), so far subtrees are never pushed.
 template <bool COUNT = false>
 __device__ __forceinline__ Closest closest_point(const SceneView2& S, float x, float y, unsigned qmask,
-                                                 float maxD2 = kFInf, int hint = -1, int hint2 = -1, int start = 0,
-                                                 const int4* front = nullptr) {
+                                                 float maxD2 = kFInf, int hint = -1, int hint2 = -1,
+                                                 const int4 starts = kRootStart) {
     Closest c{maxD2, 0.0f, 0.0f, 0.0f, -1};
     if (hint >= 0) {
         Closest h = closest_on(S, hint, x, y);
@@ -189,7 +189,7 @@ __device__ __forceinline__ Closest closest_point(const SceneView2& S, float x, f
             float d2 = seg_closest(p.seg, x, y, px, py, t);
             if (d2 < c.d2) { c.d2 = d2; c.px = px; c.py = py; c.t = t; c.seg = p.id; }
         },
-        [&]() { return c.d2; }, start, front);
+        [&]() { return c.d2; }, starts);
     return c;
 }
 
@@ -229,7 +229,7 @@ struct StarQuery {
 };
 template <bool COUNT = false>
 __device__ __forceinline__ StarQuery star_query(const SceneView2& S, float x, float y, float eps2, int hint = -1,
-                                                int hint2 = -1, int start = 0, const int4* front = nullptr) {
+                                                int hint2 = -1, const int4 starts = kRootStart) {
     StarQuery q;
     q.D = hint >= 0 ? closest_on(S, hint, x, y) : Closest{kFInf, 0.0f, 0.0f, 0.0f, -1};
     if (hint2 >= 0 && hint2 != hint) {
@@ -252,7 +252,7 @@ __device__ __forceinline__ StarQuery star_query(const SceneView2& S, float x, fl
                 if (p.sil1 >= 0 && silhouette_ok(S, p.sil1, x, y, d2) && d2 < fminf(q.s2, q.D.d2)) q.s2 = d2;
             }
         },
-        [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); }, start, front);
+        [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); }, starts);
     return q;
 }
 

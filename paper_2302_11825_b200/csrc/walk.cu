@@ -161,26 +161,20 @@ __device__ __forceinline__ float farfield_bound(const FarField& F, float x, floa
     return __ldg(F.d + static_cast<size_t>(iy) * F.nx + ix) - sqrtf(fmaf(dx, dx, dy * dy)) - F.margin;
 }
 
-// the warm-start grid's primitive at the grid vertex nearest to (x, y), or -1 (HintGrid)
-__device__ __forceinline__ int hint_at(const HintGrid& G, float x, float y) {
-    if (!G.id) return -1;
-    const int ix = __float2int_rn((x - G.lox) * G.invH), iy = __float2int_rn((y - G.loy) * G.invH);
-    if (static_cast<unsigned>(ix) >= static_cast<unsigned>(G.nx) || static_cast<unsigned>(iy) >= static_cast<unsigned>(G.ny))
-        return -1;
-    return __ldg(G.id + static_cast<size_t>(iy) * G.nx + ix);
-}
-
-// the cell entry refs of (x, y) (HintGrid), or the root for both outside the grid; with the
-// entry frontiers, `front` receives the cell's 4 star / closest-point starts
-__device__ __forceinline__ int2 entry_at(const HintGrid& G, float x, float y, const int4*& front) {
-    front = nullptr;
-    if (!G.entry) return make_int2(0, 0);
+// what a step at (x, y) takes from its grid cell (HintCell): one 32-byte record, read as a
+// streaming load. Outside the grid, or without one: the root for both queries and no warm start.
+__device__ __forceinline__ CellHints cell_hints(const HintGrid& G, float x, float y) {
+    CellHints c{kRootStart, 0, -1};
+    if (!G.cell) return c;
     const int ix = __float2int_rd((x - G.lox) * G.invH), iy = __float2int_rd((y - G.loy) * G.invH);
     if (static_cast<unsigned>(ix) >= static_cast<unsigned>(G.nx) || static_cast<unsigned>(iy) >= static_cast<unsigned>(G.ny))
-        return make_int2(0, 0);
-    const size_t cell = static_cast<size_t>(iy) * G.nx + ix;
-    if (G.front) front = G.front + cell;
-    return __ldg(G.entry + cell);
+        return c;
+    const int4* rec = reinterpret_cast<const int4*>(G.cell + static_cast<size_t>(iy) * G.nx + ix);
+    c.front = __ldcs(rec);
+    const int4 t = __ldcs(rec + 1);
+    c.ray = t.x;
+    c.id = t.y;
+    return c;
 }
 
 // per-lane walk state
@@ -246,8 +240,7 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
     // holds no boundary point, so no Neumann crossing and no Neumann-data term either
     const float lb = E.ff.d ? farfield_bound(E.ff, w.x, w.y) : -1.0f;
     const bool far = lb >= E.ff.tau;
-    const int4* front = nullptr;
-    const int2 entry = (far || E.drunN) ? make_int2(0, 0) : entry_at(E.hg, w.x, w.y, front);
+    const CellHints cell = (far || E.drunN) ? CellHints{kRootStart, 0, -1} : cell_hints(E.hg, w.x, w.y);
     if (far) {
         R = lb;
     } else if (E.drunN) {  // straight-run scene: no BVH (bvc_scene_s::build_runs)
@@ -262,13 +255,13 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
         if constexpr (NEU) {
             // a Dirichlet segment farther than the closest visible silhouette may be
             // pruned (q.D.seg < 0, d2 = inf): R is then the silhouette distance
-            StarQuery q = star_query<COUNT>(E.S, w.x, w.y, E.eps * E.eps, w.lastD, hint_at(E.hg, w.x, w.y), entry.x, front);
+            StarQuery q = star_query<COUNT>(E.S, w.x, w.y, E.eps * E.eps, w.lastD, cell.id, cell.front);
             cp = q.D;
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
             R = fminf(dD, sqrtf(q.s2));
         } else {
-            cp = closest_point<COUNT>(E.S, w.x, w.y, kClsD, kFInf, w.lastD, hint_at(E.hg, w.x, w.y), entry.x, front);
+            cp = closest_point<COUNT>(E.S, w.x, w.y, kClsD, kFInf, w.lastD, cell.id, cell.front);
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.acc + w.weight * g_value(E, cp); return true; }
             R = dD;
@@ -292,9 +285,9 @@ __device__ __forceinline__ bool walk_step(const WalkEnv& E, Walk& w, U4 rnd, flo
     float travel = R;
     bool hit = false;
     if (NEU && !far) {
-        RayHit h = E.runN ? ray_runs(E, w.x, w.y, dx, dy, R, w.onN ? w.prevSeg : -1, entry.y)
+        RayHit h = E.runN ? ray_runs(E, w.x, w.y, dx, dy, R, w.onN ? w.prevSeg : -1, cell.ray)
                           : intersect_ray<COUNT>(E.S, w.x, w.y, dx, dy, R, kClsNeumann, E.tguard,
-                                                 w.onN ? w.prevSeg : -1, entry.y);
+                                                 w.onN ? w.prevSeg : -1, cell.ray);
         if (h.seg >= 0) {
             hit = true;
             travel = h.t;
@@ -700,25 +693,31 @@ __global__ void farfield2_kernel(const SceneView2 S, const FarField F, float* d)
     d[i] = sqrtf(closest_point(S, x, y, kClsAny).d2);
 }
 
-__global__ void hintgrid2_kernel(const SceneView2 S, const HintGrid G, int* id, int2* entry, int4* front, float rmin) {
+__global__ void hintgrid2_kernel(const SceneView2 S, const HintGrid G, HintCell* cells, int entries, int fronts,
+                                 float rmin) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= G.nx * G.ny) return;
     int ix = i % G.nx, iy = i / G.nx;
-    float x = fmaf(static_cast<float>(ix), G.h, G.lox), y = fmaf(static_cast<float>(iy), G.h, G.loy);
-    id[i] = closest_point(S, x, y, kClsD).seg;
     // cell [v, v + h)^2: centre c, half-diagonal rho; r = dD(c) + 2 rho plus FP32 slack
-    const float cx = x + 0.5f * G.h, cy = y + 0.5f * G.h, rho = 0.70710678f * G.h;
-    const float r = sqrtf(closest_point(S, cx, cy, kClsD).d2) + 2.0f * rho + 1e-5f * S.diagonal;
-    const int star = entry_node(S, cx, cy, r * r, kClsD | kClsSil);
-    const float rr = r + rmin;
-    entry[i] = make_int2(star == kNoEntry ? 0 : star, entry_node(S, cx, cy, rr * rr, kClsNeumann));
-    if (front) {
-        int f[4];
-        entry_frontier2(S, cx, cy, r * r, kClsD | kClsSil, f);
-        // nothing within the radius cannot happen for a star query (the closest Dirichlet
-        // primitive is); keep the root in that case like entry.x does
-        front[i] = f[0] == kNoEntry ? make_int4(0, kNoEntry, kNoEntry, kNoEntry) : make_int4(f[0], f[1], f[2], f[3]);
+    const float cx = fmaf(static_cast<float>(ix) + 0.5f, G.h, G.lox), cy = fmaf(static_cast<float>(iy) + 0.5f, G.h, G.loy),
+                rho = 0.70710678f * G.h;
+    const Closest c = closest_point(S, cx, cy, kClsD);
+    HintCell out;
+    out.id = c.seg;  // at x in the cell its distance is at most d(x) + 2 |x - c|
+    out.pad0 = out.pad1 = 0;
+    out.front = kRootStart;
+    out.ray = 0;
+    if (entries) {
+        const float r = sqrtf(c.d2) + 2.0f * rho + 1e-5f * S.diagonal;
+        const float rr = r + rmin;
+        out.ray = entry_node(S, cx, cy, rr * rr, kClsNeumann);
+        int f[4] = {kNoEntry, kNoEntry, kNoEntry, kNoEntry};
+        if (fronts) entry_frontier2(S, cx, cy, r * r, kClsD | kClsSil, f);
+        else f[0] = entry_node(S, cx, cy, r * r, kClsD | kClsSil);
+        if (f[0] == kNoEntry) f[0] = 0;  // cannot happen for a star query (the closest Dirichlet primitive qualifies)
+        out.front = make_int4(f[0], f[1], f[2], f[3]);
     }
+    cells[i] = out;
 }
 
 
@@ -769,9 +768,10 @@ void launch_farfield2(const SceneView2& S, const FarField& F, float* d, cudaStre
     count_launch();
 }
 
-void launch_hintgrid2(const SceneView2& S, const HintGrid& G, int* id, int2* entry, int4* front, float rmin,
+void launch_hintgrid2(const SceneView2& S, const HintGrid& G, HintCell* cells, bool entries, bool fronts, float rmin,
                       cudaStream_t st) {
-    hintgrid2_kernel<<<blocks(static_cast<long long>(G.nx) * G.ny, 128), 128, 0, st>>>(S, G, id, entry, front, rmin);
+    hintgrid2_kernel<<<blocks(static_cast<long long>(G.nx) * G.ny, 128), 128, 0, st>>>(S, G, cells, entries ? 1 : 0,
+                                                                                   fronts ? 1 : 0, rmin);
     count_launch();
 }
 

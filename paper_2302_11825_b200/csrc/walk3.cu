@@ -62,7 +62,7 @@ struct Star3 {
 
 template <bool COUNT>
 __device__ __forceinline__ Star3 star_query3(const WalkEnv3& E, float x, float y, float z, int hint, int hint2,
-                                             int start, const int4* front = nullptr) {
+                                             const int4 starts) {
     Star3 q{hint >= 0 ? closest_on3(E.S, hint, x, y, z) : Closest3{kFInf, 0.f, 0.f, 0.f, -1, -1}, kFInf};
     if (hint2 >= 0 && hint2 != hint) {
         Closest3 h = closest_on3(E.S, hint2, x, y, z);
@@ -100,7 +100,7 @@ __device__ __forceinline__ Star3 star_query3(const WalkEnv3& E, float x, float y
                 }
             }
         },
-        [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); }, start, front);
+        [&]() { return fmaxf(fminf(q.D.d2, q.s2), eps2); }, starts);
     return q;
 }
 
@@ -205,30 +205,23 @@ __device__ __forceinline__ float sphere_weight3(float s, float R, float rHit) {
     return (rHit * s * ch + sh) / shR;
 }
 
-// the warm-start grid's primitive at the grid vertex nearest to x, or -1 (HintGrid)
-__device__ __forceinline__ int hint_at3(const HintGrid& G, float x, float y, float z) {
-    if (!G.id) return -1;
-    const int ix = __float2int_rn((x - G.lox) * G.invH), iy = __float2int_rn((y - G.loy) * G.invH),
-              iz = __float2int_rn((z - G.loz) * G.invH);
-    if (static_cast<unsigned>(ix) >= static_cast<unsigned>(G.nx) || static_cast<unsigned>(iy) >= static_cast<unsigned>(G.ny) ||
-        static_cast<unsigned>(iz) >= static_cast<unsigned>(G.nz))
-        return -1;
-    return BVC_GRID_LD(G.id + (static_cast<size_t>(iz) * G.ny + iy) * G.nx + ix);
-}
-
-// the cell entry refs of x (HintGrid), or the root for both outside the grid; with the
-// entry frontiers, `front` receives the cell's kFront star / closest-point starts
-__device__ __forceinline__ int2 entry_at3(const HintGrid& G, float x, float y, float z, const int4*& front) {
-    front = nullptr;
-    if (!G.entry) return make_int2(0, 0);
+// what a step at x takes from its grid cell (HintCell): one 32-byte record, read as a
+// streaming load (one cell per step out of gigabytes: evict-first). Outside the grid, or
+// without one: the root for both queries and no warm start.
+__device__ __forceinline__ CellHints cell_hints3(const HintGrid& G, float x, float y, float z) {
+    CellHints c{kRootStart, 0, -1};
+    if (!G.cell) return c;
     const int ix = __float2int_rd((x - G.lox) * G.invH), iy = __float2int_rd((y - G.loy) * G.invH),
               iz = __float2int_rd((z - G.loz) * G.invH);
     if (static_cast<unsigned>(ix) >= static_cast<unsigned>(G.nx) || static_cast<unsigned>(iy) >= static_cast<unsigned>(G.ny) ||
         static_cast<unsigned>(iz) >= static_cast<unsigned>(G.nz))
-        return make_int2(0, 0);
-    const size_t cell = (static_cast<size_t>(iz) * G.ny + iy) * G.nx + ix;
-    if (G.front) front = G.front + cell * kFrontWords;
-    return BVC_GRID_LD(G.entry + cell);
+        return c;
+    const int4* rec = reinterpret_cast<const int4*>(G.cell + (static_cast<size_t>(iz) * G.ny + iy) * G.nx + ix);
+    c.front = __ldcs(rec);
+    const int4 t = __ldcs(rec + 1);
+    c.ray = t.x;
+    c.id = t.y;
+    return c;
 }
 
 struct Walk3 {
@@ -263,20 +256,18 @@ __device__ __forceinline__ bool walk3_step(const WalkEnv3& E, Walk3& w, U4 rnd, 
     // far field: a ball from the distance grid, no BVH queries (FarField)
     const float lb = E.ff.d ? farfield_bound3(E.ff, w.x, w.y, w.z) : -1.0f;
     const bool far = lb >= E.ff.tau;
-    const int4* front = nullptr;
-    const int2 entry = far ? make_int2(0, 0) : entry_at3(E.hg, w.x, w.y, w.z, front);
+    const CellHints cell = far ? CellHints{kRootStart, 0, -1} : cell_hints3(E.hg, w.x, w.y, w.z);
     if (far) {
         R = lb;
     } else {
         if constexpr (NEU) {
-            Star3 q = star_query3<COUNT>(E, w.x, w.y, w.z, w.lastD, hint_at3(E.hg, w.x, w.y, w.z), entry.x, front);
+            Star3 q = star_query3<COUNT>(E, w.x, w.y, w.z, w.lastD, cell.id, cell.front);
             cp = q.D;
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
             R = fminf(dD, sqrtf(q.s2));
         } else {
-            cp = closest_point3<COUNT>(E.S, w.x, w.y, w.z, kClsD, kFInf, w.lastD, hint_at3(E.hg, w.x, w.y, w.z),
-                                       entry.x, front);
+            cp = closest_point3<COUNT>(E.S, w.x, w.y, w.z, kClsD, kFInf, w.lastD, cell.id, cell.front);
             float dD = sqrtf(cp.d2);
             if (dD <= E.eps) { value = w.weight * g3(E, cp); return true; }
             R = dD;
@@ -290,7 +281,7 @@ __device__ __forceinline__ bool walk3_step(const WalkEnv3& E, Walk3& w, U4 rnd, 
     float travel = R;
     bool hit = false;
     if (NEU && !far) {
-        Hit3 h = ray_neumann3<COUNT>(E, w.x, w.y, w.z, dx, dy, dz, R, w.onN ? w.prevTri : -1, entry.y);
+        Hit3 h = ray_neumann3<COUNT>(E, w.x, w.y, w.z, dx, dy, dz, R, w.onN ? w.prevTri : -1, cell.ray);
         if (h.tri >= 0) {
             hit = true;
             travel = h.t;
@@ -634,34 +625,37 @@ void launch_walk3_t(const WalkEnv3& env, const WalkJob3& job, long long total, c
     walk3_kernel<NEU, SCR, COUNT><<<grid, kThreads3, 0, st>>>(env, job);
 }
 
-__global__ void hintgrid3_kernel(const SceneView3 S, const HintGrid G, int* id, int2* entry, int4* front, float rmin) {
+__global__ void hintgrid3_kernel(const SceneView3 S, const HintGrid G, HintCell* cells, int entries, int fronts,
+                                 float rmin) {
     long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= static_cast<long long>(G.nx) * G.ny * G.nz) return;
     int ix = static_cast<int>(i % G.nx), iy = static_cast<int>((i / G.nx) % G.ny), iz = static_cast<int>(i / (static_cast<long long>(G.nx) * G.ny));
-    float x = fmaf(static_cast<float>(ix), G.h, G.lox), y = fmaf(static_cast<float>(iy), G.h, G.loy),
-          z = fmaf(static_cast<float>(iz), G.h, G.loz);
-    id[i] = closest_point3(S, x, y, z, kClsD).prim;
     // cell [v, v + h)^3: centre c, half-diagonal rho; r = dD(c) + 2 rho plus FP32 slack
-    const float cx = x + 0.5f * G.h, cy = y + 0.5f * G.h, cz = z + 0.5f * G.h, rho = 0.8660254f * G.h;
-    const float r = sqrtf(closest_point3(S, cx, cy, cz, kClsD).d2) + 2.0f * rho + 1e-5f * S.diagonal;
-    const int star = entry_node3(S, cx, cy, cz, r * r, kClsD | kClsSil);
-    const float rr = r + rmin;
-    entry[i] = make_int2(star == kNoEntry ? 0 : star, entry_node3(S, cx, cy, cz, rr * rr, kClsNeumann));
-    if (front) {
-        int f[4 * kFrontWords];
-        entry_frontier3(S, cx, cy, cz, r * r, kClsD | kClsSil, f);
-        if (f[0] == kNoEntry) f[0] = 0;  // as the single entry: the root
-        for (int k = 0; k < kFrontWords; ++k)
-            front[i * kFrontWords + k] = make_int4(f[4 * k], f[4 * k + 1], f[4 * k + 2], f[4 * k + 3]);
+    const float cx = fmaf(static_cast<float>(ix) + 0.5f, G.h, G.lox), cy = fmaf(static_cast<float>(iy) + 0.5f, G.h, G.loy),
+                cz = fmaf(static_cast<float>(iz) + 0.5f, G.h, G.loz), rho = 0.8660254f * G.h;
+    const Closest3 c = closest_point3(S, cx, cy, cz, kClsD);
+    HintCell out;
+    out.id = c.prim;  // at x in the cell its distance is at most d(x) + 2 |x - c|
+    out.pad0 = out.pad1 = 0;
+    out.front = kRootStart;
+    out.ray = 0;
+    if (entries) {
+        const float r = sqrtf(c.d2) + 2.0f * rho + 1e-5f * S.diagonal;
+        const float rr = r + rmin;
+        out.ray = entry_node3(S, cx, cy, cz, rr * rr, kClsNeumann);
+        int f[4] = {kNoEntry, kNoEntry, kNoEntry, kNoEntry};
+        if (fronts) entry_frontier3(S, cx, cy, cz, r * r, kClsD | kClsSil, f);
+        else f[0] = entry_node3(S, cx, cy, cz, r * r, kClsD | kClsSil);
+        if (f[0] == kNoEntry) f[0] = 0;  // cannot happen for a star query (the closest Dirichlet primitive qualifies)
+        out.front = make_int4(f[0], f[1], f[2], f[3]);
     }
+    cells[i] = out;
 }
 
-int front_words3() { return kFrontWords; }
-
-void launch_hintgrid3(const SceneView3& S, const HintGrid& G, int* id, int2* entry, int4* front, float rmin,
+void launch_hintgrid3(const SceneView3& S, const HintGrid& G, HintCell* cells, bool entries, bool fronts, float rmin,
                       cudaStream_t st) {
-    hintgrid3_kernel<<<blocks(static_cast<long long>(G.nx) * G.ny * G.nz, 128), 128, 0, st>>>(S, G, id, entry, front,
-                                                                                            rmin);
+    hintgrid3_kernel<<<blocks(static_cast<long long>(G.nx) * G.ny * G.nz, 128), 128, 0, st>>>(S, G, cells, entries ? 1 : 0,
+                                                                                            fronts ? 1 : 0, rmin);
     count_launch();
 }
 
