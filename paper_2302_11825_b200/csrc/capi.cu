@@ -253,17 +253,17 @@ HintGrid bvc_scene_s::hintgrid() {
     if (hgBuilt) return hg;
     const int dim = host.dim;
     const char* en = std::getenv("BVC_HINTGRID_N");  // vertices along the longest side
-    // 3D: cells about the triangle size (1.35 sqrt(triangles) along the longest side, 64-384):
+    // 3D: cells about the triangle size (1.8 sqrt(triangles) along the longest side, 64-512):
     // a cell's candidate ball is dD(c) + 2 rho, so near the surface smaller cells give deeper
-    // entry frontiers. Walk time by vertices along the side (C4 / C5, frontier of 4):
-    // 128: 0.377 / 2.633 s, 256: 0.349 / 2.523, 384: 0.335 / 2.461, 512: 0.324 / 2.420 (one-time
-    // build 0.05 / 0.13 / 0.25 / 0.47 s; 32 B per cell: 1.8 GB at 384^3, 4.3 GB at 512^3)
-    const int n3 = static_cast<int>(std::lround(1.35 * std::sqrt(static_cast<double>(host.ns))));
+    // entry frontiers. Walk time by vertices along the side (C4 / C5, frontier of 4, 32-byte
+    // cell records): 384: 0.327 / 2.467 s, 512: 0.318 / 2.421, 640: 0.310 / 2.384 (one-time build
+    // 0.25 / 0.47 / 0.7 s; 1.8 GB at 384^3, 4.3 GB at 512^3, 8.4 GB at 640^3)
+    const int n3 = static_cast<int>(std::lround(1.8 * std::sqrt(static_cast<double>(host.ns))));
     // 2D: a quarter of the segment count along the longest side, 1024-4096 (32 B per cell: 34-540 MB).
     // Walk time with frontiers by vertices along the side, C3 (16384 segments): 1024: 93.7 ms, 2048: 89.4,
     // 4096: 86.9 (one entry node per cell: 112.6 at any size); C1 (1024 segments): 1.1 ms at 1024-4096
     const int n2 = std::min(4096, std::max(1024, host.ns / 4));
-    const int nLong = en && std::atoi(en) >= 16 ? std::atoi(en) : (dim == 2 ? n2 : std::min(384, std::max(64, n3)));
+    const int nLong = en && std::atoi(en) >= 16 ? std::atoi(en) : (dim == 2 ? n2 : std::min(512, std::max(64, n3)));
     double ext = 0.0, lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (int k = 0; k < dim; ++k) {
         lo[k] = host.lo[k];
