@@ -181,3 +181,84 @@ def test_pointwise_3d_matches_harmonic_data(sphere):
     grad = np.stack([0.3 - x[:, 0] + x[:, 1], -0.2 - x[:, 1] + x[:, 0], 0.5 + 2 * x[:, 2]], 1)
     zg = (gr["mean"] - grad) / np.maximum(gr["se"], 1e-12)
     assert np.sum(np.abs(zg) > 3) <= 2, zg
+
+
+def _cube_mesh(n=8):
+    """Unit cube [0,1]^3, n x n x 2 triangles per face, outward orientation; labels: the faces
+    x = 0 and x = 1 Dirichlet (0), the other four Neumann (1)."""
+    V, F, L = [], [], []
+    t = np.linspace(0.0, 1.0, n + 1)
+
+    def face(origin, du, dv, label):
+        base = len(V)
+        for j in range(n + 1):
+            for i in range(n + 1):
+                V.append(origin + t[i] * du + t[j] * dv)
+        for j in range(n):
+            for i in range(n):
+                a = base + j * (n + 1) + i
+                b, c, d = a + 1, a + n + 1, a + n + 2
+                F.extend([[a, b, d], [a, d, c]])  # normal du x dv
+                L.extend([label, label])
+
+    e = np.eye(3)
+    face(np.zeros(3), e[2], e[1], 0)          # x = 0, normal -x
+    face(e[0].copy(), e[1], e[2], 0)          # x = 1, normal +x
+    face(np.zeros(3), e[0], e[2], 1)          # y = 0, normal -y
+    face(e[1].copy(), e[2], e[0], 1)          # y = 1, normal +y
+    face(np.zeros(3), e[1], e[0], 1)          # z = 0, normal -z
+    face(e[2].copy(), e[0], e[1], 1)          # z = 1, normal +z
+    V, F = np.array(V), np.array(F, np.int32)
+    # weld the duplicated edge / corner vertices so that the faces share edges
+    key = np.round(V * (1 << 20)).astype(np.int64)
+    _, first, inv = np.unique(key, axis=0, return_index=True, return_inverse=True)
+    return V[first], inv.reshape(-1)[F].astype(np.int32), np.array(L, np.int32)
+
+
+def test_screened_mixed_cube_closed_form():
+    """C5's physics with a closed form: screened (sigma = 1) on the unit cube, Dirichlet
+    g = e^x on x = 0 and x = 1 (linear data 1 + (e - 1) x agrees there), reflecting h = 0 on
+    the other four faces: u = e^x (u'' = u, no y/z dependence). Pointwise walk-on-stars
+    values and gradients, and BVC rounds, against it at |z| < 3."""
+    V, F, lab = _cube_mesh(8)
+    sc = B.Scene.mesh3(V, F, lab)
+    pb = B.problem(B.screened(1.0, 3), g=abi.make_field(abi.FIELD_LINEAR, [np.e - 1.0, 0.0, 1.0, 0.0]))
+    rng = np.random.default_rng(12)
+    x = rng.uniform(0.15, 0.85, size=(24, 3))
+    e = B.wost_solve(sc, pb, x, B.walk_config(epsilon=1e-3, nWalks=16384, seed=21))
+    z = (e["mean"] - np.exp(x[:, 0])) / np.maximum(e["se"], 1e-12)
+    assert np.all(e["se"] < 0.02) and np.sum(np.abs(z) > 3) <= 1, z
+    gr = B.wost_gradient(sc, pb, x, B.walk_config(epsilon=1e-3, nWalks=32768, seed=22))
+    exact = np.stack([np.exp(x[:, 0]), np.zeros(len(x)), np.zeros(len(x))], 1)
+    zg = (gr["mean"] - exact) / np.maximum(gr["se"], 1e-12)
+    assert np.sum(np.abs(zg) > 3) <= 2, zg
+    # the cache's estimators at the region's samples, by kind (0: known Neumann, u by walks;
+    # 1: offset Dirichlet patch, u and du/dn by walks), against u = e^x and du/dn = n_x e^x.
+    # (The du/dn estimates are heavy-tailed where the offset patch bends down to the Neumann
+    # rim and the first ball is tiny, so their mean is checked against its own standard error.)
+    region = B.SolveRegion(sc, offset=0.1, epsilon=1e-3)
+    cfg = B.cache_config(B.walk_config(epsilon=1e-3, nWalks=512), nBoundary=16384, nWalksNeumann=512,
+                         nWalksDirichlet=512, offset=0.1)
+    c = B.generate_boundary_cache(sc, pb, region, cfg, 7, 0).download()
+    kinds = region.kinds[c["segment"]]
+    ux = np.exp(c["z"][:, 0])
+    dx = c["n"][:, 0] * ux
+    assert set(np.unique(kinds)) == {0, 1}
+    for k in (0, 1):
+        m = kinds == k
+        eu = c["uHat"][m] - ux[m]
+        assert abs(eu.mean()) <= 4 * eu.std(ddof=1) / np.sqrt(m.sum()) + 2e-3, (k, eu.mean())  # O(eps) shell
+        ed = c["dHat"][m] - dx[m]
+        assert abs(ed.mean()) <= 5 * ed.std(ddof=1) / np.sqrt(m.sum()) + 1e-6, (k, ed.mean())
+    assert np.all(c["dHat"][kinds == 0] == 0.0)  # h = 0 is data there
+    assert abs(np.mean(1.0 / c["pdf"]) - 6.24) < 0.05  # the region surface's area
+    # the representation itself: the gather over this sample set with the exact u and du/dn
+    # reproduces e^x (quadrature error of 16384 samples), and with the walks' u as well
+    xi = rng.uniform(0.2, 0.8, size=(512, 3))
+    spec = B.make_splat_config(sc, pb, cfg)
+    for uh in (ux, c["uHat"]):
+        cache = B.BoundaryCache.from_arrays(c["z"], c["n"], c["pdf"], uh, dx, segment=c["segment"])
+        p = B.EvaluationPoints(xi, 3)
+        B.splat_solution(cache, None, p, spec)
+        err = p.solution() - np.exp(xi[:, 0])
+        assert np.sqrt(np.mean(err ** 2)) < 6e-3 and abs(err.mean()) < 3e-3, (err.mean(), np.sqrt(np.mean(err ** 2)))
