@@ -1,4 +1,6 @@
-"""Which of the library's kernels can share an SM with a resident 1-CTA-per-SM kernel of a
+"""(Build the spinning kernel first: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -shared -Xcompiler -fPIC
+-o paper_2302_11825_b200/_build/libspin.so scripts/cuda/spin.cu)
+Which of the library's kernels can share an SM with a resident 1-CTA-per-SM kernel of a
 given shared-memory carve-out? A spinning kernel (scripts/cuda/spin.cu) holds one CTA on
 every SM for ~T s on one stream; the gather / the walks run on another and report how long
 they took. Usage: python scripts/spin_probe.py"""

@@ -1,4 +1,6 @@
-"""Does a kernel with shared memory start while the library's walks (1-3 blocks per SM) are
+"""(Build the spinning kernel first: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -shared -Xcompiler -fPIC
+-o paper_2302_11825_b200/_build/libspin.so scripts/cuda/spin.cu)
+Does a kernel with shared memory start while the library's walks (1-3 blocks per SM) are
 resident? Thread W runs a cache generation; the main thread launches a 0.2 s spinning
 kernel with 16 KB of shared memory per CTA on another stream and times it."""
 import ctypes as C
