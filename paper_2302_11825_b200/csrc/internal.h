@@ -15,22 +15,22 @@ namespace bvc_impl {
 using bvc_dev::DevField;
 using bvc_dev::SceneView2;
 
-// Warm-start grid: at the vertices of a uniform grid over the scene box, the closest
-// Dirichlet primitive (2D: segment id; 3D: leaf-order triangle index). A walk step at
-// x also seeds its closest-point query with the primitive of x's nearest vertex v,
-// whose distance is at most d(x) + 2|x - v|: the pruning radius starts near-tight
-// even after a long jump, and the result is unchanged (one more candidate of the same
-// minimum). BVC_HINTGRID=0 disables it.
+// Warm-start grid: for every cell of a uniform grid over the scene box, the Dirichlet
+// primitive closest to the cell centre c (2D: segment id; 3D: leaf-order triangle index). A
+// walk step at x also seeds its closest-point query with its cell's primitive, whose
+// distance is at most d(x) + 2|x - c|: the pruning radius starts near-tight even after a
+// long jump, and the result is unchanged (one more candidate of the same minimum).
+// BVC_HINTGRID=0 disables it.
 //
-// Per grid cell (the cell [v, v + h) of vertex v) the grid also keeps entry refs: with c
-// the cell centre and rho its half-diagonal, every Dirichlet or silhouette primitive a
-// star / closest-point query at x in the cell can use lies within dD(x) <= dD(c) + rho
-// of x, so within r = dD(c) + 2 rho of c; .x is the deepest BVH node whose subtree holds
-// every primitive box of those classes within r of c. A Neumann ray of such a step is no
-// longer than dD(x) either, so .y is the same for the Neumann classes (kNoEntry: the cell's
-// rays cannot reach any). Queries start there instead of the root: the top levels, which
-// every query of the cell would descend identically, are skipped, and the result is the
-// same (every candidate is in the subtree).
+// The cell also keeps entry refs: with rho its half-diagonal, every Dirichlet or silhouette
+// primitive a star / closest-point query at x in the cell can use lies within
+// dD(x) <= dD(c) + rho of x, so within r = dD(c) + 2 rho of c; the single entry is the deepest
+// BVH node whose subtree holds every primitive box of those classes within r of c, and the
+// entry frontier (BVC_FRONT=0 disables it) up to four deeper nodes that together do. A Neumann
+// ray of such a step is no longer than dD(x) either, so the ray entry is the same for the
+// Neumann classes (kNoEntry: the cell's rays cannot reach any). Queries start there instead
+// of the root (BVC_ENTRY=0): the top levels, which every query of the cell would descend
+// identically, are skipped, and the result is the same (every candidate is in the subtrees).
 // One 32-byte record per cell (one memory sector per walk step): the cell's star /
 // closest-point starts (`front`: entry_frontier2 / 3, up to 4 nodes whose subtrees hold every
 // usable primitive; front.x alone when frontiers are off; kNoEntry = unused slot), its Neumann
