@@ -143,6 +143,49 @@ def test_two_host_threads_run_rounds_concurrently():
             assert np.array_equal(np.asarray(par[k][name]), np.asarray(v), equal_nan=True), (k, name)
 
 
+def test_a_waiting_round_does_not_block_another_threads_launches(monkeypatch):
+    """A cache generation waits on the host for its failed-sample count. That read goes
+    through pinned memory (read_device_int, capi.cu): a copy into pageable memory blocks inside
+    the driver, and launches from other host threads queue up behind it. While thread A's
+    walks (held to one block per SM, so that they last) are running, a small library call from
+    thread B on its own stream returns in a fraction of their time."""
+    import threading
+    import time
+
+    import torch
+
+    monkeypatch.setenv("BVC_WALK_OCC", "1")
+    c, sc, region, x, dim = _setup(4, 1 / 4, 1000)
+    B.generate_boundary_cache(sc, c.problem, region, c.cache, c.seed, 0)  # lazy scene state, warm-up
+    t_ref = np.linspace(0.5, 4.0, 256)
+    B.eval_bessel(0, t_ref)
+    res = {}
+
+    def walks():
+        B.set_stream(sa.cuda_stream)
+        t0 = time.perf_counter()
+        B.generate_boundary_cache(sc, c.problem, region, c.cache, c.seed, 1)
+        B.synchronize()
+        res["walks"] = time.perf_counter() - t0
+        B.set_stream(None)
+
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    th = threading.Thread(target=walks)
+    torch.cuda.synchronize()
+    th.start()
+    time.sleep(0.05)
+    B.set_stream(sb.cuda_stream)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        B.eval_bessel(0, t_ref)
+    B.synchronize()
+    small = time.perf_counter() - t0
+    B.set_stream(None)
+    th.join()
+    assert res["walks"] > 0.15, res  # long enough for the comparison to mean something
+    assert small < 0.3 * res["walks"], (small, res)
+
+
 @pytest.mark.parametrize("cid,scale", [(1, 1 / 16), (4, 1 / 256)])
 def test_last_round_kernel_seconds_bracket_the_hot_launches(cid, scale):
     """bvc_last_round_kernel_seconds: the round's main walk and gather launches, each
