@@ -135,6 +135,10 @@ WalkEnv3 make_env3(bvc_scene_s* S, const bvc_problem& pb, const bvc_walk_config&
     if (pb.kernel.dim != 3) throw Error(BVC_ERR_INVALID_ARGUMENT, "3D scene needs a dim-3 kernel");
     if (pb.f.kind != BVC_FIELD_NONE)
         throw Error(BVC_ERR_SOLVER, "source terms are not supported by the 3D walks (kernels.cpp:98-99 is 2D-only)");
+    // the walks' Neumann-data term (neumannTerm pointwise.cpp:52-107, clipped to the ball) has no 3D
+    // form here: nonzero data would be dropped silently, so only h = 0 is accepted on Neumann faces
+    if (S->host.hasNeumann() && pb.h.kind != BVC_FIELD_NONE && !(pb.h.kind == BVC_FIELD_CONSTANT && pb.h.p[0] == 0.0))
+        throw Error(BVC_ERR_SOLVER, "Neumann data h is not supported by the 3D walks: reflecting faces (h = 0) only");
     if (!(S->host.dirichletMeasure > 0.0))
         throw Error(BVC_ERR_SOLVER, "walk cannot terminate: scene has no Dirichlet boundary");
     WalkEnv3 E{};

@@ -262,3 +262,20 @@ def test_screened_mixed_cube_closed_form():
         B.splat_solution(cache, None, p, spec)
         err = p.solution() - np.exp(xi[:, 0])
         assert np.sqrt(np.mean(err ** 2)) < 6e-3 and abs(err.mean()) < 3e-3, (err.mean(), np.sqrt(np.mean(err ** 2)))
+
+
+def test_3d_walks_reject_neumann_data_and_sources():
+    """What the 3D walks do not implement fails loudly instead of being dropped: nonzero
+    Neumann data h (the ball-clipped neumannTerm of pointwise.cpp:52-107 is 2D) and source
+    terms f (sampleBallGreens, kernels.cpp:98-99, is 2D-only); h = 0 as data is accepted."""
+    V, F, lab = _cube_mesh(4)
+    sc = B.Scene.mesh3(V, F, lab)
+    g = abi.make_field(abi.FIELD_LINEAR, [1.0, 0.0, 0.0, 0.0])
+    x = np.array([[0.5, 0.5, 0.5]])
+    wc = B.walk_config(epsilon=1e-3, nWalks=64, seed=1)
+    with pytest.raises(B.SolverError, match="Neumann data"):
+        B.wost_solve(sc, B.problem(B.poisson(3), g=g, h=abi.make_field(abi.FIELD_CONSTANT, [1.0])), x, wc)
+    with pytest.raises(B.SolverError, match="source terms"):
+        B.wost_solve(sc, B.problem(B.poisson(3), g=g, f=abi.make_field(abi.FIELD_CONSTANT, [1.0])), x, wc)
+    e = B.wost_solve(sc, B.problem(B.poisson(3), g=g, h=abi.make_field(abi.FIELD_CONSTANT, [0.0])), x, wc)
+    assert np.isfinite(e["mean"][0]) and abs(e["mean"][0] - 0.5) < 0.2  # u = x with reflecting side faces
