@@ -345,7 +345,17 @@ __device__ __forceinline__ U4 draw4(const WalkEnv& E, Task& t) {
 // resident blocks per SM (registers per thread = 64K / (256 x MINB)), measured on
 // C1-C3: Neumann scenes 4 (C2: 6.36 ms vs 6.72 at 6), screened 8 (C3: 148 vs 155 ms
 // at 6), plain Laplace 6 (C1: 1.29 vs 1.40 ms at 8)
-template <bool NEU, bool SCR, bool SRC, bool COUNT, int MINB = NEU ? 4 : (SCR ? 8 : 6)>
+#ifndef BVC_W2_MINB_NEU
+#define BVC_W2_MINB_NEU 4
+#endif
+#ifndef BVC_W2_MINB_SCR
+#define BVC_W2_MINB_SCR 8
+#endif
+#ifndef BVC_W2_MINB_DIR
+#define BVC_W2_MINB_DIR 6
+#endif
+template <bool NEU, bool SCR, bool SRC, bool COUNT,
+          int MINB = NEU ? BVC_W2_MINB_NEU : (SCR ? BVC_W2_MINB_SCR : BVC_W2_MINB_DIR)>
 __global__ void __launch_bounds__(kWalkThreads, MINB) walk_kernel(const WalkEnv E, const WalkJob J) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
